@@ -1,0 +1,257 @@
+/*
+ * codecsight.h — C ABI of the CodecSight hot path on B200 (sm_100a).
+ *
+ * Paper: "CodecSight: Leveraging Video Codec Signals for Efficient Streaming VLM Inference"
+ * (arXiv 2604.06036).  Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * The library implements three calls, each a plain-pointer, asynchronous, stream-ordered operation:
+ *
+ *   codecsight_score_patches  per-macroblock codec metadata -> patch scores -> keep mask
+ *                             (Eq. 1-4, GOP accumulation, group-complete expansion)
+ *   codecsight_compact        keep mask + frames -> packed ViT input, position ids, source index,
+ *                             per-frame offsets ("executes the ViT only on the selected patches")
+ *   codecsight_kv_refresh     sliding-window reuse/anchor/new token index + K/V gather with RoPE key
+ *                             correction (Eq. 5) and value reuse, refreshed-row scatter
+ *
+ * Conventions (all calls):
+ *  - Ownership: the caller owns every buffer.  The library allocates nothing, frees nothing and keeps no
+ *    pointer after a call returns (SPEC single-owner stream state).
+ *  - Pointers named "device" must be CUDA device (or managed) memory valid on the current device; host
+ *    structs (cs_grid, cs_kv_desc, cs_window) are read during the call only.
+ *  - Execution: every call validates its arguments on the host, then enqueues kernels on `stream` and returns
+ *    without synchronising.  Calls are reentrant; concurrent calls on different streams with disjoint output
+ *    buffers are allowed.
+ *  - Synchronous errors: a negative return code means NOTHING was enqueued (except CS_ERR_CUDA, returned when a
+ *    launch itself failed).  Device-detected conditions are OR-ed as CS_STATUS_* bits into the caller-owned
+ *    device int32 `status` (never cleared by the library); read it after the stream is synchronised.
+ *  - Counters: `counters` is a caller-owned device array of CS_NCOUNTERS u64, accumulated with atomic adds.
+ *  - There is no CPU fallback: without a CUDA device the calls return CS_ERR_CUDA.
+ */
+#ifndef CODECSIGHT_H_
+#define CODECSIGHT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- synchronous return codes -------------------------------------------------------------------------- */
+enum {
+  CS_OK = 0,
+  CS_ERR_INVALID_ARGUMENT = -1, /* NULL required pointer, negative count, NaN/negative tau or alpha             */
+  CS_ERR_SHAPE = -2,            /* SPEC "dimension mismatch": mb grid != ceil(src/mb), group does
+                                   not divide the patch grid, ring shorter than w+s, ...                          */
+  CS_ERR_UNSUPPORTED = -3,      /* dtype not in {bf16,fp32}, odd head_dim, s > w, sizes above the
+                                   documented limits                                                              */
+  CS_ERR_CUDA = -4              /* a CUDA launch failed (cudaGetLastError), or no device                          */
+};
+
+/* ---- asynchronous status bits (OR-ed into *status on the device) ---------------------------------------- */
+enum {
+  CS_STATUS_CAPACITY = 1,       /* an output capacity was exceeded; writes beyond it were dropped (offsets and
+                                   counts still report the full, unclamped sizes)                                */
+  CS_STATUS_NO_IFRAME = 2,      /* a P-frame arrived on a stream whose GOP state was never initialised by an
+                                   I-frame; the accumulated state is taken as empty (reading Q11)                */
+  CS_STATUS_ORIGIN = 4,         /* an ANCHOR/REUSE token's p_old lies outside the old cache's capacity (the
+                                   previous window was truncated; SPEC "origin mismatch"); row skipped    */
+  CS_STATUS_BAD_FRAME_TYPE = 8, /* frame type not in {I, P} (B-frames are out of scope, S:8); treated as I       */
+  CS_STATUS_BAD_MB_TYPE = 16    /* macroblock type not in {INTER, SKIP, INTRA}; treated as INTRA (dynamic)        */
+};
+
+enum { CS_FRAME_I = 0, CS_FRAME_P = 1 };
+enum { CS_MB_INTER = 0, CS_MB_SKIP = 1, CS_MB_INTRA = 2 };
+enum { CS_DISP_NEW = 0, CS_DISP_ANCHOR = 1, CS_DISP_REUSE = 2 };
+enum { CS_BF16 = 0, CS_FP32 = 1 };
+
+/* ---- counters (u64 each) -------------------------------------------------------------------------------- */
+enum {
+  CS_CNT_FRAMES = 0,        /* frames scored (I + P)                                                          */
+  CS_CNT_PFRAMES = 1,       /* P-frames scored                                                                */
+  CS_CNT_PATCHES = 2,       /* patches scored (= frames x grid_h x grid_w)                                    */
+  CS_CNT_KEPT = 3,          /* patches kept (group-complete mask)                                             */
+  CS_CNT_NEAR_TAU = 4,      /* P-frame patches with finite M and |M - tau| <= 1e-5 (north star)               */
+  CS_CNT_TOK_REUSE = 5,     /* kv_refresh: REUSE tokens                                                       */
+  CS_CNT_TOK_ANCHOR = 6,    /* kv_refresh: ANCHOR tokens                                                      */
+  CS_CNT_TOK_NEW = 7,       /* kv_refresh: NEW tokens including prompt rows                                   */
+  CS_CNT_BYTES_SCORE = 8,   /* algorithmic bytes of score_patches             */
+  CS_CNT_BYTES_COMPACT = 9, /* algorithmic bytes of compact                                                    */
+  CS_CNT_BYTES_KV = 10,     /* algorithmic bytes of the K/V row moves of kv_refresh                            */
+  CS_CNT_PACKED_ROWS = 11,  /* compact: packed rows written                                                   */
+  CS_CNT_STREAM_STEPS = 12, /* kv_refresh: stream-window steps processed                                       */
+  CS_NCOUNTERS = 16
+};
+
+/* One coded macroblock of a P-frame (D2 in SURVEY §2.2).  8 bytes, no padding.
+ *   mvx_qpel, mvy_qpel : motion vector in QUARTER-pel units of the source (displayed) frame (reading Q2)
+ *   sad                : sum of absolute differences of the block vs its prediction (Eq. 2)
+ *   mb_type            : CS_MB_INTER | CS_MB_SKIP | CS_MB_INTRA                                           */
+typedef struct {
+  int16_t mvx_qpel;
+  int16_t mvy_qpel;
+  uint16_t sad;
+  uint8_t mb_type;
+  uint8_t reserved;
+} cs_mb;
+
+/* Frame / macroblock / patch geometry and the pruning policy parameters.
+ * Limits: 1 <= src_w, src_h <= 16384; 1 <= mb_size <= 64; mb_cols == ceil(src_w/mb_size) and
+ * mb_rows == ceil(src_h/mb_size) (coded grid, reading Q3); 1 <= grid_w, grid_h; grid_w*grid_h <= 4096;
+ * group >= 1 divides grid_w and grid_h; mb_rows*grid_w <= 8192; 1 <= patch <= 32 (compact only);
+ * tau >= 0 (may be +inf), alpha >= 0 finite.                                                                 */
+typedef struct {
+  int32_t src_w, src_h;     /* displayed source size in px (448x448, 1920x1080, 3840x2160)                   */
+  int32_t mb_size;          /* 16                                                                           */
+  int32_t mb_cols, mb_rows; /* coded MB grid = ceil(src/mb_size): 28x28, 120x68, 240x135                     */
+  int32_t patch;            /* ViT patch edge in model px (14)                                              */
+  int32_t grid_w, grid_h;   /* patch grid of the model input (32x32 for 448x448)                             */
+  int32_t group;            /* spatial merge group edge (2: 2x2 patches -> one LLM token)             */
+  float tau;                /* threshold in source px, default 0.25; dynamic iff M >= tau (Eq. 4)   */
+  float alpha;              /* residual weight of Eq. 3, default 0                                  */
+} cs_grid;
+
+/* grid_words = ceil(grid_w*grid_h / 32): u32 words of one patch bitmap; patch i = h*grid_w + w is bit (i%32)
+ * of word (i/32).                                                                                            */
+
+/* ------------------------------------------------------------------------------------------------------------
+ * codecsight_score_patches — Eq. 1-4 + GOP accumulation + group-complete expansion.
+ *
+ * Per stream sigma and new frame j (time order), for a P-frame:
+ *   v_m   = |mv_m| / 4 px (Eq. 1); INTRA (or unknown type) MBs have v_m = +inf.
+ *   V(i)  = max of v_m over MBs whose rectangle overlaps patch i with positive area; R(i) = area-weighted
+ *           mean per-pixel |residual| / 255 (resampling).
+ *   M(i)  = V(i) + alpha*R(i) (Eq. 3, one fp32 fma), dynamic(i) = M(i) >= tau (Eq. 4).
+ *   state = state OR dynamic (GOP accumulation); out = state.
+ * For an I-frame: state = empty, out = all patches, score = +inf, metadata not read (reading Q7, Q10).
+ * keep = group-complete expansion of out: a group is kept iff any of its patches is in out.
+ *
+ *   g            host   geometry and policy
+ *   n_streams    >= 0   streams in this call (0 = no-op)
+ *   n_frames     1..256 new frames per stream (the stride s; w for the first window)
+ *   mb           device [n_streams][n_frames][mb_rows][mb_cols] cs_mb; I-frame slots are not read.
+ *                       16-B alignment of `mb` enables the bulk-copy (TMA) path.
+ *   frame_type   device [n_streams][frame_stride] u8 CS_FRAME_*, frame j of stream sigma at sigma*frame_stride+j
+ *   keep_mask    device [n_streams][frame_stride][grid_words] u32 out (same slot addressing as frame_type,
+ *                       so a caller can point both at the slots of a per-stream ring)
+ *   frame_stride >= n_frames
+ *   gop_state    device [n_streams][grid_words+1] u32 in/out: accumulated patch bits, then a flag word whose
+ *                       bit 0 = "initialised by an I-frame".  Zero-initialise for a new stream.
+ *   score        device [n_streams][n_frames][grid_h*grid_w] fp32 out: M(i) (+inf for I-frames); NULL = skip
+ *   kept_count   device [n_streams][n_frames] i32 out: kept patches (a multiple of group^2)
+ *   counters     device [CS_NCOUNTERS] u64 (FRAMES, PFRAMES, PATCHES, KEPT, NEAR_TAU, BYTES_SCORE)
+ *   status       device i32 (NO_IFRAME, BAD_FRAME_TYPE, BAD_MB_TYPE)
+ * --------------------------------------------------------------------------------------------------------- */
+int codecsight_score_patches(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                             const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
+                             uint32_t* gop_state, float* score, int32_t* kept_count,
+                             unsigned long long* counters, int32_t* status, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------------------------------
+ * codecsight_compact — stream compaction of kept patches into the packed ViT input.
+ *
+ * The batch is n_streams x n_frames frames, flattened stream-major: slot = sigma*n_frames + j.
+ * A group (group x group patches) is emitted iff any of its patches has its keep bit set; every emitted group
+ * contributes all group^2 patches (group-complete, idempotent on masks produced by score_patches).
+ * Order (reading Q14, "group-major"): slot, then group row-major, then patch (dy, dx) row-major in the group.
+ * For the n-th emitted patch (h, w) of slot `slot` whose stream-local frame index is t:
+ *   packed[n][c][y][x] = frame[slot][c][patch*h + y][patch*w + x]   (bit copy, c < 3, y, x < patch)
+ *   pos_ids[n]         = (t, h, w)                                   (reading Q15)
+ *   src_index[n]       = slot*grid_h*grid_w + h*grid_w + w
+ * frame_offsets[slot] = exclusive scan of emitted patches per slot; frame_offsets[n_slots] = total
+ * (cu_seqlens for a varlen ViT).  Rows n >= capacity are not written (CS_STATUS_CAPACITY); offsets are not clamped.
+ *
+ *   keep_mask         device [n_streams][mask_frame_stride][grid_words] u32, frame j of stream sigma at
+ *                            sigma*mask_frame_stride + j (mask_frame_stride >= n_frames)
+ *   frame_index       device [n_slots] i32 stream-local absolute frame index (pos id t)
+ *   frames            device [n_slots] array of device pointers, each a [3][grid_h*patch][grid_w*patch] bf16
+ *                            frame (the preprocessed model input); 16-B alignment enables wide loads
+ *   capacity          rows available in packed / pos_ids / src_index
+ *   packed            device [capacity][3*patch*patch] bf16 out
+ *   pos_ids           device [capacity][3] i32 out
+ *   src_index         device [capacity] i32 out
+ *   frame_offsets     device [n_slots+1] i32 out
+ *   counters          BYTES_COMPACT, PACKED_ROWS;  status: CAPACITY
+ * n_slots * grid_h * grid_w must be < 2^31.
+ * --------------------------------------------------------------------------------------------------------- */
+int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
+                       int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
+                       int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                       int32_t* frame_offsets, unsigned long long* counters, int32_t* status,
+                       cudaStream_t stream);
+
+/* KV cache description.  One cache buffer (one stream, one window) is laid out as
+ *   [layers][2 (K, V)][capacity][kv_heads][head_dim]  of dtype,
+ * so one (token, layer, K-or-V) row is kv_heads*head_dim contiguous elements.                                */
+typedef struct {
+  int32_t layers, kv_heads, head_dim; /* 28, 4, 128 (Qwen2-VL-7B shape) | toy 2, 2, 16; head_dim even <= 512 */
+  int32_t dtype;                      /* CS_BF16 | CS_FP32                                                    */
+  int64_t capacity;                   /* token rows per cache buffer                                          */
+  int64_t refresh_capacity;           /* token rows per refreshed (recompute) buffer                          */
+  double rope_base;                   /* 1e4 (S:355 default) | 1e6 (Qwen2)                                    */
+  int32_t n_prompt;                   /* prompt rows after the visual tokens; always NEW        */
+  int32_t reserved;
+} cs_kv_desc;
+
+/* Sliding window: window k covers frames [k*stride, k*stride + window).                   */
+typedef struct {
+  int32_t window, stride; /* w, s with 1 <= s <= w                                                 */
+  int32_t step;           /* k >= 0 (window index)                                                         */
+  int32_t ring_frames;    /* slots in the per-stream mask/type ring; frame f lives in slot f % ring_frames;
+                             must be >= w + s for k >= 1 (>= w for k = 0)                                   */
+} cs_window;
+
+/* ------------------------------------------------------------------------------------------------------------
+ * codecsight_kv_refresh — selective KVC refresh for window k of every stream.
+ *
+ * Tokens of window k (reading Q16): visual tokens in (frame, group row-major) order over frames [ks, ks+w),
+ * one per emitted group (as in codecsight_compact), followed by n_prompt prompt rows.  n_f = tokens of frame f.
+ *   p_new(f, g) = sum_{f' in [ks, f)} n_f' + rank_f(g);  p_old(f, g) = sum_{f' in [(k-1)s, f)} n_f' + rank_f(g)
+ *   disposition: f >= (k-1)s + w          -> NEW      (frames that arrived with this stride)
+ *                else type(f) == I or f == ks -> ANCHOR (I-frame anchors; first overlap frame, Q17)
+ *                else                      -> REUSE
+ *   prompt rows: p_new = n_visual + j, NEW.  k == 0: every token NEW.
+ * REUSE (Eq. 5), for every layer l:  K_new[l][p_new] = R(p_new - p_old) K_old[l][p_old]  (rotate_half
+ *   pairing (i, i + D/2), inv_freq_i = base^(-2i/D), fp64 angle -> fp32 cos/sin, fp32 fma, RNE store; Q19-Q21)
+ *   and V_new[l][p_new] = V_old[l][p_old] (bit copy).
+ * Non-REUSE tokens (ANCHOR, NEW, prompt), in p_new order, take row r = 0, 1, ... of `refreshed` (bit copy of K and
+ * V for all layers) if `refreshed` is not NULL; otherwise those rows of new_cache are left untouched for the
+ * prefill (Q18).
+ *
+ *   keep_mask_ring    device [n_streams][ring_frames][grid_words] u32 (masks from score_patches)
+ *   frame_type_ring   device [n_streams][ring_frames] u8
+ *   old_cache         device array [n_streams] of device pointers to window k-1 caches (not read when k == 0)
+ *   new_cache         device array [n_streams] of device pointers to window k caches; must not alias old_cache
+ *   refreshed         device array [n_streams] of device pointers to [layers][2][refresh_capacity][H][D]
+ *                            recompute buffers, or NULL
+ *   token_cap         per-stream capacity of the index outputs
+ *   disposition       device [n_streams][token_cap] u8 out, indexed by p_new
+ *   p_old             device [n_streams][token_cap] i32 out, -1 for NEW
+ *   n_tokens          device [n_streams][4] i32 out: n_visual, n_reuse, n_anchor, n_new (incl. prompt)
+ *   workspace         device scratch of >= codecsight_kv_refresh_workspace_size() bytes, 16-B aligned; its
+ *                            content is undefined after the call (the per-stream plan segments)
+ *   counters          TOK_REUSE, TOK_ANCHOR, TOK_NEW, BYTES_KV, STREAM_STEPS;  status: CAPACITY, ORIGIN
+ * Rows with p_new >= min(capacity, token_cap) and refreshed rows r >= refresh_capacity are dropped
+ * (CS_STATUS_CAPACITY); n_tokens reports the unclamped counts.
+ * --------------------------------------------------------------------------------------------------------- */
+int codecsight_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                          const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                          const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
+                          int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens,
+                          void* workspace, size_t workspace_bytes, unsigned long long* counters,
+                          int32_t* status, cudaStream_t stream);
+
+/* Bytes of device workspace codecsight_kv_refresh needs for this window and stream count (0 on bad args). */
+size_t codecsight_kv_refresh_workspace_size(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams);
+
+/* Static string for a return code. */
+const char* codecsight_strerror(int code);
+
+/* Library ABI version (major*100 + minor). */
+int codecsight_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CODECSIGHT_H_ */

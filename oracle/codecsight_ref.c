@@ -1,0 +1,432 @@
+/*
+ * oracle/codecsight_ref.c — ORACLE for the CodecSight hot path.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, single-threaded C, compiled with `gcc -O2 -ffp-contract=off` (no FMA contraction, no SIMD
+ * intrinsics).  Every function follows the paper's definitions in the paper's order, written as loops
+ * so a reader can check it against PAPER.md by eye.  Readings of silent or ambiguous passages are the
+ * Q-numbered readings of DESIGN.md (taken from SURVEY.md §8(c)).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline, --impl reference) may load this
+ * library.  It shares no code with the CUDA path (paper_2604_06036_b200/csrc), and the CUDA path never
+ * calls it.
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_*.py (worked examples of the paper
+ * and SPEC, hand-derived examples, closed forms, invariants and an independent pure-Python transcription,
+ * oracle/pyref.py).  No function is "parity unpinned".
+ */
+#include "codecsight_ref.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* small helpers: bit access on u32 words, bf16 <-> fp32                                               */
+/* ---------------------------------------------------------------------------------------------------- */
+static int64_t ref_words(const ref_grid* g) { return ((int64_t)g->grid_w * g->grid_h + 31) / 32; }
+static int ref_bit(const uint32_t* w, int64_t i) { return (int)((w[i / 32] >> (i % 32)) & 1u); }
+static void ref_set(uint32_t* w, int64_t i) { w[i / 32] |= (1u << (i % 32)); }
+
+static float ref_bf16_to_f32(uint16_t h) {
+  uint32_t u = ((uint32_t)h) << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+/* fp32 -> bf16, round to nearest, ties to even (reading Q20: "RNE store"). */
+static uint16_t ref_f32_to_bf16(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu) != 0) return (uint16_t)((u >> 16) | 0x0040u); /* NaN */
+  uint32_t lsb = (u >> 16) & 1u;
+  u = u + 0x7fffu + lsb;
+  return (uint16_t)(u >> 16);
+}
+
+static int ref_grid_ok(const ref_grid* g) {
+  if (!g) return -1;
+  if (g->src_w < 1 || g->src_h < 1 || g->src_w > 16384 || g->src_h > 16384) return -2;
+  if (g->mb_size < 1 || g->mb_size > 64) return -2;
+  if (g->mb_cols != (g->src_w + g->mb_size - 1) / g->mb_size) return -2;
+  if (g->mb_rows != (g->src_h + g->mb_size - 1) / g->mb_size) return -2;
+  if (g->grid_w < 1 || g->grid_h < 1 || (int64_t)g->grid_w * g->grid_h > 4096) return -2;
+  if (g->group < 1 || g->grid_w % g->group != 0 || g->grid_h % g->group != 0) return -2;
+  if ((int64_t)g->mb_rows * g->grid_w > 8192) return -3;
+  if (g->patch < 1 || g->patch > 32) return -2;
+  if (isnan(g->tau) || g->tau < 0.0f) return -1;
+  if (isnan(g->alpha) || isinf(g->alpha) || g->alpha < 0.0f) return -1;
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* Eq. 1: V_t^m = ||v_t^m||.  The MV is in quarter-pel units, so the magnitude in source     */
+/* pixels is sqrt(dx^2 + dy^2) / 4 (reading Q2).  INTRA macroblocks have no motion vector; they are      */
+/* treated as maximally dynamic, v = +inf (reading Q9).  Unknown types are treated as INTRA.            */
+/* ---------------------------------------------------------------------------------------------------- */
+float codecsight_ref_mb_magnitude(int16_t dx_qpel, int16_t dy_qpel, uint8_t mb_type) {
+  if (mb_type != REF_MB_INTER && mb_type != REF_MB_SKIP) return INFINITY;
+  uint32_t sq = (uint32_t)((int32_t)dx_qpel * (int32_t)dx_qpel) + (uint32_t)((int32_t)dy_qpel * (int32_t)dy_qpel);
+  return sqrtf((float)sq) * 0.25f;
+}
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* Resampling onto the patch grid followed by Eq. 3.                      */
+/* Coordinates are scaled by (grid_w, grid_h) so every rectangle edge is an integer (reading Q3):        */
+/*   patch (r, c):  X [c*src_w, (c+1)*src_w)            Y [r*src_h, (r+1)*src_h)                          */
+/*   MB (j, i):     X [mb*i*grid_w, mb*(i+1)*grid_w)    Y [mb*j*grid_h, mb*(j+1)*grid_h)                  */
+/* V(i) = max of v_m over MBs with positive-area overlap ("max over blocks overlapping").           */
+/* R(i) = sum_m a(i,m) * sad_m / (mb^2 * 255 * src_w * src_h): the area-weighted mean of the per-pixel    */
+/*        |residual| (uniform inside an MB: sad/mb^2) over the patch (area src_w*src_h in scaled units), */
+/*        normalised to [0,1] by /255.  Numerator and denominator are exact in double.     */
+/* M(i) = V(i) + alpha R(i) as one fp32 fma; +inf stays +inf.                                             */
+/* ---------------------------------------------------------------------------------------------------- */
+void codecsight_ref_patch_fields(const ref_grid* g, const ref_mb* mb, float* V, float* R, float* M,
+                                 int32_t* status) {
+  const int64_t gw = g->grid_w, gh = g->grid_h, mbs = g->mb_size;
+  const double denom = (double)mbs * (double)mbs * 255.0 * (double)g->src_w * (double)g->src_h;
+  for (int64_t r = 0; r < gh; ++r) {
+    for (int64_t c = 0; c < gw; ++c) {
+      const int64_t px0 = c * g->src_w, px1 = (c + 1) * g->src_w;
+      const int64_t py0 = r * g->src_h, py1 = (r + 1) * g->src_h;
+      float v = -INFINITY;
+      int64_t area_sad = 0;
+      for (int64_t j = 0; j < g->mb_rows; ++j) {
+        const int64_t my0 = mbs * j * gh, my1 = mbs * (j + 1) * gh;
+        const int64_t oy = (py1 < my1 ? py1 : my1) - (py0 > my0 ? py0 : my0);
+        if (oy <= 0) continue;
+        for (int64_t i = 0; i < g->mb_cols; ++i) {
+          const int64_t mx0 = mbs * i * gw, mx1 = mbs * (i + 1) * gw;
+          const int64_t ox = (px1 < mx1 ? px1 : mx1) - (px0 > mx0 ? px0 : mx0);
+          if (ox <= 0) continue;
+          const ref_mb* b = &mb[j * g->mb_cols + i];
+          if (b->mb_type > REF_MB_INTRA && status) *status |= REF_ST_BAD_MB_TYPE;
+          const float vm = codecsight_ref_mb_magnitude(b->mvx_qpel, b->mvy_qpel, b->mb_type);
+          if (vm > v) v = vm;
+          area_sad += ox * oy * (int64_t)b->sad;
+        }
+      }
+      const float rr = (float)((double)area_sad / denom);
+      const float mm = isinf(v) ? INFINITY : fmaf(g->alpha, rr, v);
+      if (V) V[r * gw + c] = v;
+      if (R) R[r * gw + c] = rr;
+      if (M) M[r * gw + c] = mm;
+    }
+  }
+}
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* score_patches: Eq. 4 threshold, GOP accumulation, group-complete expansion */
+/* ---------------------------------------------------------------------------------------------------- */
+int codecsight_ref_score_patches(const ref_grid* g, int32_t n_streams, int32_t n_frames, const ref_mb* mb,
+                                 const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
+                                 uint32_t* gop_state, float* score, int32_t* kept_count,
+                                 unsigned long long* counters, int32_t* status) {
+  int rc = ref_grid_ok(g);
+  if (rc) return rc;
+  if (n_streams < 0 || n_frames < 1 || n_frames > 256 || frame_stride < n_frames) return -1;
+  if (n_streams == 0) return 0;
+  if (!mb || !frame_type || !keep_mask || !gop_state || !kept_count || !counters || !status) return -1;
+
+  const int64_t np = (int64_t)g->grid_w * g->grid_h, nw = ref_words(g), G = g->group;
+  const int64_t n_mb = (int64_t)g->mb_rows * g->mb_cols;
+  float* M = (float*)malloc(sizeof(float) * np);
+  uint32_t* out = (uint32_t*)malloc(sizeof(uint32_t) * nw);
+  uint32_t* keep = (uint32_t*)malloc(sizeof(uint32_t) * nw);
+  if (!M || !out || !keep) { free(M); free(out); free(keep); return -1; }
+
+  for (int64_t s = 0; s < n_streams; ++s) {
+    uint32_t* st = gop_state + s * (nw + 1); /* accumulated bits, then the flag word */
+    for (int64_t j = 0; j < n_frames; ++j) {
+      const int64_t slot = s * frame_stride + j;
+      const uint8_t type = frame_type[slot];
+      int is_i = (type == REF_FRAME_I);
+      if (type != REF_FRAME_I && type != REF_FRAME_P) { *status |= REF_ST_BAD_FRAME_TYPE; is_i = 1; }
+      counters[REF_C_FRAMES] += 1;
+      if (is_i) {
+        /* "I-frames are always fully encoded" and reset the mask: output every patch,
+           accumulation state := empty (reading Q7), score = +inf, metadata not read (Q10). */
+        for (int64_t w = 0; w < nw; ++w) st[w] = 0;
+        st[nw] |= 1u;
+        for (int64_t w = 0; w < nw; ++w) out[w] = 0;
+        for (int64_t i = 0; i < np; ++i) ref_set(out, i);
+        if (score)
+          for (int64_t i = 0; i < np; ++i) score[(s * n_frames + j) * np + i] = INFINITY;
+      } else {
+        counters[REF_C_PFRAMES] += 1;
+        if (!(st[nw] & 1u)) { /* reading Q11 */
+          *status |= REF_ST_NO_IFRAME;
+          for (int64_t w = 0; w < nw; ++w) st[w] = 0;
+          st[nw] |= 1u;
+        }
+        codecsight_ref_patch_fields(g, mb + (s * n_frames + j) * n_mb, NULL, NULL, M, status);
+        for (int64_t i = 0; i < np; ++i) {
+          /* Eq. 4: dynamic(i) = M_t(i) >= tau (inclusive, reading Q1) */
+          if (M[i] >= g->tau) ref_set(st, i);
+          /* union with the preceding P-frames of the GOP is the |= above */
+          if (isfinite(M[i]) && fabsf(M[i] - g->tau) <= 1e-5f) counters[REF_C_NEAR_TAU] += 1;
+        }
+        for (int64_t w = 0; w < nw; ++w) out[w] = st[w];
+        if (score)
+          for (int64_t i = 0; i < np; ++i) score[(s * n_frames + j) * np + i] = M[i];
+      }
+      /* group-complete expansion: keep every patch of a group with any active patch */
+      for (int64_t w = 0; w < nw; ++w) keep[w] = 0;
+      for (int64_t gr = 0; gr < g->grid_h / G; ++gr)
+        for (int64_t gc = 0; gc < g->grid_w / G; ++gc) {
+          int any = 0;
+          for (int64_t dy = 0; dy < G; ++dy)
+            for (int64_t dx = 0; dx < G; ++dx) any |= ref_bit(out, (gr * G + dy) * g->grid_w + gc * G + dx);
+          if (any)
+            for (int64_t dy = 0; dy < G; ++dy)
+              for (int64_t dx = 0; dx < G; ++dx) ref_set(keep, (gr * G + dy) * g->grid_w + gc * G + dx);
+        }
+      int64_t kept = 0;
+      for (int64_t i = 0; i < np; ++i) kept += ref_bit(keep, i);
+      for (int64_t w = 0; w < nw; ++w) keep_mask[slot * nw + w] = keep[w];
+      kept_count[s * n_frames + j] = (int32_t)kept;
+      counters[REF_C_PATCHES] += (unsigned long long)np;
+      counters[REF_C_KEPT] += (unsigned long long)kept;
+      counters[REF_C_BYTES_SCORE] +=
+          (unsigned long long)((is_i ? 0 : 8 * n_mb) + 4 * nw + 4 + (score ? 4 * np : 0));
+    }
+    counters[REF_C_BYTES_SCORE] += (unsigned long long)(2 * 4 * (nw + 1));
+  }
+  free(M);
+  free(out);
+  free(keep);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* compact: "executes the ViT only on the selected patches" — the packed, group-major ViT input. */
+/* ---------------------------------------------------------------------------------------------------- */
+int codecsight_ref_compact(const ref_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
+                           int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
+                           int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                           int32_t* frame_offsets, unsigned long long* counters, int32_t* status) {
+  int rc = ref_grid_ok(g);
+  if (rc) return rc;
+  if (n_streams < 0 || n_frames < 1 || mask_frame_stride < n_frames || capacity < 0) return -1;
+  const int64_t np = (int64_t)g->grid_w * g->grid_h, nw = ref_words(g), G = g->group, p = g->patch;
+  const int64_t n_slots = (int64_t)n_streams * n_frames;
+  if (n_slots * np >= 2147483648LL) return -3;
+  if (!frame_offsets || !counters || !status) return -1;
+  if (n_slots > 0 && (!keep_mask || !frame_index || !frames)) return -1;
+  if (capacity > 0 && (!packed || !pos_ids || !src_index)) return -1;
+
+  const int64_t fh = g->grid_h * p, fw = g->grid_w * p; /* model-input frame [3][fh][fw] bf16 */
+  const int64_t row = 3 * p * p;                         /* elements of one packed patch row */
+  uint16_t* out = (uint16_t*)packed;
+  int64_t off = 0, written = 0;
+  for (int64_t s = 0; s < n_streams; ++s)
+    for (int64_t j = 0; j < n_frames; ++j) {
+      const int64_t slot = s * n_frames + j;
+      const uint32_t* m = keep_mask + (s * mask_frame_stride + j) * nw;
+      const uint16_t* fr = (const uint16_t*)frames[slot];
+      frame_offsets[slot] = (int32_t)off;
+      for (int64_t gr = 0; gr < g->grid_h / G; ++gr)
+        for (int64_t gc = 0; gc < g->grid_w / G; ++gc) {
+          int any = 0;
+          for (int64_t dy = 0; dy < G; ++dy)
+            for (int64_t dx = 0; dx < G; ++dx) any |= ref_bit(m, (gr * G + dy) * g->grid_w + gc * G + dx);
+          if (!any) continue;
+          for (int64_t dy = 0; dy < G; ++dy)
+            for (int64_t dx = 0; dx < G; ++dx) {
+              const int64_t h = gr * G + dy, w = gc * G + dx, n = off++;
+              if (n >= capacity) { *status |= REF_ST_CAPACITY; continue; }
+              for (int64_t c = 0; c < 3; ++c)
+                for (int64_t y = 0; y < p; ++y)
+                  for (int64_t x = 0; x < p; ++x)
+                    out[n * row + c * p * p + y * p + x] = fr[c * fh * fw + (h * p + y) * fw + (w * p + x)];
+              pos_ids[3 * n + 0] = frame_index[slot];
+              pos_ids[3 * n + 1] = (int32_t)h;
+              pos_ids[3 * n + 2] = (int32_t)w;
+              src_index[n] = (int32_t)(slot * np + h * g->grid_w + w);
+              ++written;
+            }
+        }
+    }
+  frame_offsets[n_slots] = (int32_t)off;
+  counters[REF_C_PACKED_ROWS] += (unsigned long long)written;
+  counters[REF_C_BYTES_COMPACT] +=
+      (unsigned long long)(n_slots * (4 * nw + 4) + written * (2 * row * 2 + 16));
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* Eq. 5: K^_t(j) = R(p_new - p_old) K_{t-1}(j), rotate_half pairing (reading Q19-Q21).      */
+/* ---------------------------------------------------------------------------------------------------- */
+static void ref_rot_pair(float x1, float x2, int64_t i, int64_t D, double base, int64_t dp, float* o1, float* o2) {
+  const double inv = pow(base, -2.0 * (double)i / (double)D);
+  const double ang = (double)dp * inv;
+  const float c = (float)cos(ang), s = (float)sin(ang);
+  *o1 = fmaf(x1, c, -(x2 * s));
+  *o2 = fmaf(x2, c, x1 * s);
+}
+
+void codecsight_ref_rope_rotate_f32(const float* k, int32_t n_heads, int32_t head_dim, double base, int64_t dp,
+                                    float* out) {
+  const int64_t half = head_dim / 2;
+  for (int64_t h = 0; h < n_heads; ++h)
+    for (int64_t i = 0; i < half; ++i)
+      ref_rot_pair(k[h * head_dim + i], k[h * head_dim + i + half], i, head_dim, base, dp,
+                   &out[h * head_dim + i], &out[h * head_dim + i + half]);
+}
+
+static int64_t ref_tokens_of(const ref_grid* g, const uint32_t* m) {
+  /* one token per emitted group (same rule as compaction, "(2x2) group ... projected into a token") */
+  const int64_t G = g->group;
+  int64_t n = 0;
+  for (int64_t gr = 0; gr < g->grid_h / G; ++gr)
+    for (int64_t gc = 0; gc < g->grid_w / G; ++gc) {
+      int any = 0;
+      for (int64_t dy = 0; dy < G; ++dy)
+        for (int64_t dx = 0; dx < G; ++dx) any |= ref_bit(m, (gr * G + dy) * g->grid_w + gc * G + dx);
+      n += any;
+    }
+  return n;
+}
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* kv_refresh: critical-token refresh + position-consistent reuse.               */
+/* ---------------------------------------------------------------------------------------------------- */
+int codecsight_ref_kv_refresh(const ref_grid* g, const ref_kv* kv, const ref_window* win, int32_t n_streams,
+                              const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                              const void* const* old_cache, void* const* new_cache,
+                              const void* const* refreshed, int64_t token_cap, uint8_t* disposition,
+                              int32_t* p_old, int32_t* n_tokens, unsigned long long* counters, int32_t* status) {
+  int rc = ref_grid_ok(g);
+  if (rc) return rc;
+  if (!kv || !win) return -1;
+  if (n_streams < 0 || token_cap < 0) return -1;
+  if (kv->dtype != REF_BF16 && kv->dtype != REF_FP32) return -3;
+  if (kv->layers < 1 || kv->kv_heads < 1 || kv->head_dim < 2 || kv->head_dim > 512) return -3;
+  if (kv->head_dim % 2 != 0) return -3;
+  if (kv->capacity < 0 || kv->refresh_capacity < 0 || kv->n_prompt < 0) return -1;
+  if (!(kv->rope_base > 0.0)) return -1;
+  const int64_t w = win->window, s = win->stride, k = win->step;
+  if (w < 1 || s < 1 || k < 0) return -1;
+  if (s > w) return -3;
+  if (win->ring_frames < (k >= 1 ? w + s : w)) return -2;
+  if (n_streams == 0) return 0;
+  if (!keep_mask_ring || !frame_type_ring || !new_cache || !disposition || !p_old || !n_tokens || !counters ||
+      !status)
+    return -1;
+  if (k >= 1 && !old_cache) return -1;
+
+  const int64_t nw = ref_words(g), G = g->group, ring = win->ring_frames;
+  const int64_t L = kv->layers, H = kv->kv_heads, D = kv->head_dim, cap = kv->capacity;
+  const int64_t rowel = H * D, esz = (kv->dtype == REF_BF16) ? 2 : 4;
+  const int64_t ks = k * s, new_first = (k - 1) * s + w; /* frames >= new_first arrived with this stride */
+
+  for (int64_t sg = 0; sg < n_streams; ++sg) {
+    const uint32_t* mring = keep_mask_ring + sg * ring * nw;
+    const uint8_t* tring = frame_type_ring + sg * ring;
+    /* sum of n_f over the dropped frames [(k-1)s, ks): p_old(f) = drop + sum_{[ks, f)} n_f' */
+    int64_t drop = 0;
+    if (k >= 1)
+      for (int64_t f = (k - 1) * s; f < ks; ++f) drop += ref_tokens_of(g, mring + (f % ring) * nw);
+
+    int64_t pn = 0, before = 0, n_reuse = 0, n_anchor = 0, n_new = 0, rrow = 0, moved = 0;
+    const uint8_t* oc = k >= 1 ? (const uint8_t*)old_cache[sg] : NULL;
+    uint8_t* nc = (uint8_t*)new_cache[sg];
+    const uint8_t* rf = refreshed ? (const uint8_t*)refreshed[sg] : NULL;
+
+    /* visual tokens in (frame, group row-major) order, then the prompt rows */
+    for (int64_t f = ks; f < ks + w + 1; ++f) {
+      const int is_prompt = (f == ks + w);
+      const uint32_t* m = is_prompt ? NULL : mring + (f % ring) * nw;
+      const uint8_t type = is_prompt ? 0 : tring[f % ring];
+      const int64_t nslots = is_prompt ? kv->n_prompt : (g->grid_h / G) * (g->grid_w / G);
+      int64_t rank = 0;
+      for (int64_t q = 0; q < nslots; ++q) {
+        if (!is_prompt) {
+          const int64_t gr = q / (g->grid_w / G), gc = q % (g->grid_w / G);
+          int any = 0;
+          for (int64_t dy = 0; dy < G; ++dy)
+            for (int64_t dx = 0; dx < G; ++dx) any |= ref_bit(m, (gr * G + dy) * g->grid_w + gc * G + dx);
+          if (!any) continue;
+        }
+        const int64_t p_new = pn++;
+        int disp;
+        int64_t po;
+        if (is_prompt || k == 0 || f >= new_first) {
+          disp = REF_DISP_NEW;
+          po = -1;
+        } else {
+          /* I-frame tokens are anchors; the first overlap frame anchors the boundary (Q17) */
+          disp = (type == REF_FRAME_I || f == ks) ? REF_DISP_ANCHOR : REF_DISP_REUSE;
+          po = drop + before + rank; /* before = sum of n_f' over [ks, f) */
+        }
+        ++rank;
+        if (disp == REF_DISP_REUSE) ++n_reuse;
+        else if (disp == REF_DISP_ANCHOR) ++n_anchor;
+        else ++n_new;
+        if (p_new < token_cap) {
+          disposition[sg * token_cap + p_new] = (uint8_t)disp;
+          p_old[sg * token_cap + p_new] = (int32_t)po;
+        } else {
+          *status |= REF_ST_CAPACITY;
+        }
+        /* K/V rows of this token, all layers */
+        if (disp == REF_DISP_REUSE) {
+          if (p_new >= cap) { *status |= REF_ST_CAPACITY; continue; }
+          if (po >= cap) { *status |= REF_ST_ORIGIN; continue; }
+          const int64_t dp = p_new - po;
+          for (int64_t l = 0; l < L; ++l) {
+            /* value reuse: V^_t(j) = V_{t-1}(j) */
+            memcpy(nc + ((l * 2 + 1) * cap + p_new) * rowel * esz, oc + ((l * 2 + 1) * cap + po) * rowel * esz,
+                   (size_t)(rowel * esz));
+            /* key correction (Eq. 5) */
+            for (int64_t h = 0; h < H; ++h)
+              for (int64_t i = 0; i < D / 2; ++i) {
+                const int64_t e1 = h * D + i, e2 = h * D + i + D / 2;
+                const int64_t src = ((l * 2 + 0) * cap + po) * rowel, dst = ((l * 2 + 0) * cap + p_new) * rowel;
+                float x1, x2, o1, o2;
+                if (esz == 2) {
+                  x1 = ref_bf16_to_f32(((const uint16_t*)oc)[src + e1]);
+                  x2 = ref_bf16_to_f32(((const uint16_t*)oc)[src + e2]);
+                } else {
+                  x1 = ((const float*)oc)[src + e1];
+                  x2 = ((const float*)oc)[src + e2];
+                }
+                ref_rot_pair(x1, x2, i, D, kv->rope_base, dp, &o1, &o2);
+                if (esz == 2) {
+                  ((uint16_t*)nc)[dst + e1] = ref_f32_to_bf16(o1);
+                  ((uint16_t*)nc)[dst + e2] = ref_f32_to_bf16(o2);
+                } else {
+                  ((float*)nc)[dst + e1] = o1;
+                  ((float*)nc)[dst + e2] = o2;
+                }
+              }
+          }
+          ++moved;
+        } else {
+          const int64_t r = rrow++; /* r-th non-REUSE token in p_new order (reading Q18) */
+          if (!rf) continue;
+          if (p_new >= cap || r >= kv->refresh_capacity) { *status |= REF_ST_CAPACITY; continue; }
+          for (int64_t l = 0; l < L; ++l)
+            for (int64_t h2 = 0; h2 < 2; ++h2)
+              memcpy(nc + ((l * 2 + h2) * cap + p_new) * rowel * esz,
+                     rf + ((l * 2 + h2) * kv->refresh_capacity + r) * rowel * esz, (size_t)(rowel * esz));
+          ++moved;
+        }
+      }
+      if (!is_prompt) before += rank; /* rank == n_f once the frame is done */
+    }
+    const int64_t n_visual = pn - kv->n_prompt;
+    n_tokens[sg * 4 + 0] = (int32_t)n_visual;
+    n_tokens[sg * 4 + 1] = (int32_t)n_reuse;
+    n_tokens[sg * 4 + 2] = (int32_t)n_anchor;
+    n_tokens[sg * 4 + 3] = (int32_t)n_new;
+    counters[REF_C_TOK_REUSE] += (unsigned long long)n_reuse;
+    counters[REF_C_TOK_ANCHOR] += (unsigned long long)n_anchor;
+    counters[REF_C_TOK_NEW] += (unsigned long long)n_new;
+    counters[REF_C_BYTES_KV] += (unsigned long long)(moved * L * 2 * rowel * esz * 2);
+    counters[REF_C_STREAM_STEPS] += 1;
+  }
+  return 0;
+}

@@ -1,0 +1,207 @@
+"""Seeded synthetic inputs shared by the tests, the bench and the smoke check.
+
+This module holds NO arithmetic of the method (no scoring, thresholding, accumulation, compaction or
+indexing).  It only draws inputs: H.264-style per-macroblock metadata (quarter-pel motion vectors, MB type,
+SAD residual energy), I/P frame types, model-input frames and KV-cache contents, with the shapes and value
+distributions of the paper's surveillance / traffic workloads (recipe in DESIGN.md "Input recipe").
+
+Configs C1..C5 are BASELINE.json ``configs[0..4]`` with the concrete readings of SURVEY.md §8(d) / Q28-Q31.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+MB_DTYPE = np.dtype([("mvx", "<i2"), ("mvy", "<i2"), ("sad", "<u2"), ("type", "u1"), ("rsv", "u1")])
+FRAME_I, FRAME_P = 0, 1
+MB_INTER, MB_SKIP, MB_INTRA = 0, 1, 2
+
+
+def make_grid(src_w: int, src_h: int, tau: float = 0.25, alpha: float = 0.0, mb_size: int = 16, patch: int = 14,
+              grid_w: int = 32, grid_h: int = 32, group: int = 2) -> dict:
+    """Geometry dict accepted by both the oracle binding and the CUDA binding."""
+    return dict(src_w=src_w, src_h=src_h, mb_size=mb_size, mb_cols=-(-src_w // mb_size),
+                mb_rows=-(-src_h // mb_size), patch=patch, grid_w=grid_w, grid_h=grid_h, group=group,
+                tau=float(tau), alpha=float(alpha))
+
+
+QWEN_KV = dict(layers=28, kv_heads=4, head_dim=128, dtype=0, rope_base=1e6)  # Qwen2-VL-7B shape, bf16
+TOY_KV = dict(layers=2, kv_heads=2, head_dim=16, dtype=1, rope_base=1e4)     # SPEC toy scale, fp32
+
+# BASELINE.json configs with SURVEY §8(d) readings.  "scenes" is either a list cycled over stream ids or
+# the string "mixed" (even ids static, odd ids high-motion: C4).
+CONFIGS = {
+    "C1": dict(name="C1-oracle", src=(448, 448), streams=1, window=8, stride=2, gop=4, frames=64,
+               scenes=["static", "translating_object", "multi_object", "noise", "scene_cut"], kv=TOY_KV,
+               n_prompt=32, config_id=1),
+    "C2": dict(name="C2-prune-compact-1080p", src=(1920, 1080), streams=32, window=16, stride=4, gop=16,
+               frames=512, scenes=["low", "medium"], kv=None, n_prompt=0, config_id=2),
+    "C3": dict(name="C3-kv-refresh-qwen2vl7b", src=(1920, 1080), streams=64, window=32, stride=4, gop=16,
+               frames=None, scenes=["low", "medium"], kv=QWEN_KV, n_prompt=32, config_id=3),
+    "C4": dict(name="C4-full-1080p-mixed", src=(1920, 1080), streams=256, window=16, stride=4, gop=16,
+               frames=None, scenes="mixed", kv=QWEN_KV, n_prompt=32, config_id=4),
+    "C5": dict(name="C5-full-4k-traffic", src=(3840, 2160), streams=1024, window=64, stride=8, gop=16,
+               frames=None, scenes=["traffic"], kv=QWEN_KV, n_prompt=32, config_id=5),
+}
+
+
+def scene_of(cfg: dict, stream_id: int) -> str:
+    if cfg["scenes"] == "mixed":
+        return "static" if stream_id % 2 == 0 else "high"
+    sc = cfg["scenes"]
+    return sc[stream_id % len(sc)]
+
+
+def stream_seed(cfg: dict, stream_id: int, salt: int = 0) -> int:
+    return 1000 * cfg["config_id"] + stream_id + 7919 * salt
+
+
+def frame_types(n_frames: int, gop: int, first: int = 0) -> np.ndarray:
+    """I-frame at every f % gop == 0, P otherwise (no B-frames, S:8)."""
+    f = np.arange(first, first + n_frames)
+    return np.where(f % gop == 0, FRAME_I, FRAME_P).astype(np.uint8)
+
+
+# Scene kinds (SURVEY §8(d) generator table; SPEC S:516 kinds for parity).
+SCENES = {
+    #                 objects      speed px/frame  noise MB prob  object size (fraction of width)
+    "static": dict(k=(0, 0), v=(0.0, 0.0), p_noise=0.0, size=(0.05, 0.1)),
+    "low": dict(k=(1, 2), v=(0.25, 1.0), p_noise=0.004, size=(0.12, 0.30)),
+    "medium": dict(k=(3, 5), v=(0.5, 3.0), p_noise=0.01, size=(0.12, 0.28)),
+    "high": dict(k=(6, 10), v=(1.0, 6.0), p_noise=0.05, size=(0.10, 0.25)),
+    "traffic": dict(k=(0, 0), v=(2.0, 8.0), p_noise=0.01, size=(0.03, 0.06), lanes=(3, 4), cars=(8, 20)),
+    "translating_object": dict(k=(1, 1), v=(1.0, 2.0), p_noise=0.0, size=(0.15, 0.3)),
+    "multi_object": dict(k=(3, 5), v=(0.25, 3.0), p_noise=0.0, size=(0.08, 0.2)),
+    "noise": dict(k=(0, 0), v=(0.0, 0.0), p_noise=0.3, size=(0.05, 0.1)),
+    "scene_cut": dict(k=(1, 2), v=(0.5, 2.0), p_noise=0.002, size=(0.1, 0.25), p_cut=0.15),
+}
+
+
+class StreamGen:
+    """Per-stream seeded generator of P-frame macroblock metadata (one record set per consumed frame, Q25).
+
+    Objects are axis-aligned boxes moving with a constant velocity (bouncing at the borders).  Macroblocks whose
+    centre lies in a moving object get MV = round(4 v) qpel with +-1 qpel jitter (p = 0.2), type INTER,
+    SAD ~ 256 U(8, 40); with p = 0.02 an object MB is INTRA (entering content).  Background MBs are SKIP with a
+    zero MV and SAD 0, except a fraction p_noise of INTER MBs with a +-1 qpel MV and SAD ~ 256 U(0, 3)
+    (sensor noise).  "scene_cut" P-frames (probability p_cut) turn >= 80% of MBs INTRA."""
+
+    def __init__(self, src_w: int, src_h: int, scene: str, seed: int, mb_size: int = 16):
+        self.src_w, self.src_h, self.mb = src_w, src_h, mb_size
+        self.cols, self.rows = -(-src_w // mb_size), -(-src_h // mb_size)
+        self.scene = SCENES[scene]
+        self.kind = scene
+        self.rng = np.random.default_rng(seed)
+        r = self.rng
+        sc = self.scene
+        objs = []
+        if scene == "traffic":
+            n_lanes = int(r.integers(sc["lanes"][0], sc["lanes"][1] + 1))
+            for ln in range(n_lanes):
+                y = (ln + 0.5) * src_h / n_lanes
+                direction = 1.0 if ln % 2 == 0 else -1.0
+                for _ in range(int(r.integers(sc["cars"][0], sc["cars"][1] + 1))):
+                    w = r.uniform(*sc["size"]) * src_w * 1.6
+                    h = w * 0.6
+                    objs.append([r.uniform(0, src_w), y + r.uniform(-0.1, 0.1) * src_h / n_lanes, w, h,
+                                 direction * r.uniform(*sc["v"]), 0.0])
+        else:
+            n = int(r.integers(sc["k"][0], sc["k"][1] + 1))
+            for _ in range(n):
+                w = r.uniform(*sc["size"]) * src_w
+                h = w * r.uniform(0.6, 1.6)
+                speed = r.uniform(*sc["v"])
+                ang = r.uniform(0, 2 * math.pi)
+                objs.append([r.uniform(0, src_w), r.uniform(0, src_h), w, h, speed * math.cos(ang),
+                             speed * math.sin(ang)])
+        self.objs = np.array(objs, dtype=np.float64).reshape(-1, 6)
+        self.cx = (np.arange(self.cols) * mb_size + mb_size / 2.0)[None, :]
+        self.cy = (np.arange(self.rows) * mb_size + mb_size / 2.0)[:, None]
+
+    def _advance(self):
+        o = self.objs
+        if len(o) == 0:
+            return
+        o[:, 0] += o[:, 4]
+        o[:, 1] += o[:, 5]
+        if self.kind == "traffic":
+            o[:, 0] = np.mod(o[:, 0], self.src_w)
+        else:
+            for ax, vel, lim in ((0, 4, self.src_w), (1, 5, self.src_h)):
+                lo = o[:, ax] < 0
+                hi = o[:, ax] > lim
+                o[lo | hi, vel] *= -1.0
+                o[:, ax] = np.clip(o[:, ax], 0, lim)
+
+    def next_frame(self) -> np.ndarray:
+        """MB records [rows][cols] for the next consumed frame (also advances the scene)."""
+        self._advance()
+        r = self.rng
+        sc = self.scene
+        rec = np.zeros((self.rows, self.cols), MB_DTYPE)
+        rec["type"] = MB_SKIP
+        if sc["p_noise"] > 0:
+            noise = r.random((self.rows, self.cols)) < sc["p_noise"]
+            if noise.any():
+                k = int(noise.sum())
+                mv = r.integers(-1, 2, size=(k, 2))
+                zero = (mv[:, 0] == 0) & (mv[:, 1] == 0)
+                mv[zero, 0] = 1
+                rec["mvx"][noise] = mv[:, 0]
+                rec["mvy"][noise] = mv[:, 1]
+                rec["sad"][noise] = (256 * r.uniform(0, 3, size=k)).astype(np.uint16)
+                rec["type"][noise] = MB_INTER
+        for o in self.objs:
+            x, y, w, h, vx, vy = o
+            if vx == 0.0 and vy == 0.0:
+                continue
+            inside = (np.abs(self.cx - x) <= w / 2) & (np.abs(self.cy - y) <= h / 2)
+            k = int(inside.sum())
+            if k == 0:
+                continue
+            jit = (r.random((k, 2)) < 0.2) * r.choice(np.array([-1, 1]), size=(k, 2))
+            rec["mvx"][inside] = np.clip(np.round(4 * vx) + jit[:, 0], -32768, 32767).astype(np.int16)
+            rec["mvy"][inside] = np.clip(np.round(4 * vy) + jit[:, 1], -32768, 32767).astype(np.int16)
+            rec["sad"][inside] = (256 * r.uniform(8, 40, size=k)).astype(np.uint16)
+            intra = r.random(k) < 0.02
+            t = np.full(k, MB_INTER, np.uint8)
+            t[intra] = MB_INTRA
+            rec["type"][inside] = t
+        if "p_cut" in sc and r.random() < sc["p_cut"]:
+            cut = r.random((self.rows, self.cols)) < 0.85
+            rec["type"][cut] = MB_INTRA
+            rec["sad"][cut] = (256 * r.uniform(20, 60, size=int(cut.sum()))).astype(np.uint16)
+        return rec
+
+
+def random_mb(rows: int, cols: int, rng: np.random.Generator, p_intra: float = 0.05, mv_max: int = 12,
+              p_bad_type: float = 0.0) -> np.ndarray:
+    """Unstructured random MB records (edge cases: ties at 1 qpel, INTRA, extreme vectors)."""
+    rec = np.zeros((rows, cols), MB_DTYPE)
+    rec["mvx"] = rng.integers(-mv_max, mv_max + 1, size=(rows, cols))
+    rec["mvy"] = rng.integers(-mv_max, mv_max + 1, size=(rows, cols))
+    rec["sad"] = rng.integers(0, 65536, size=(rows, cols))
+    t = rng.choice(np.array([MB_INTER, MB_SKIP], np.uint8), size=(rows, cols))
+    t[rng.random((rows, cols)) < p_intra] = MB_INTRA
+    if p_bad_type > 0:
+        t[rng.random((rows, cols)) < p_bad_type] = 7
+    rec["type"] = t
+    return rec
+
+
+def stream_metadata(src_w: int, src_h: int, scene: str, seed: int, n_frames: int, mb_size: int = 16) -> np.ndarray:
+    """[n_frames][rows][cols] MB records of one stream (I-frame slots are filled but never read)."""
+    gen = StreamGen(src_w, src_h, scene, seed, mb_size)
+    return np.stack([gen.next_frame() for _ in range(n_frames)])
+
+
+def random_bf16(shape, rng: np.random.Generator) -> np.ndarray:
+    """N(0, 1) values truncated to bf16, returned as raw uint16 bits."""
+    x = rng.standard_normal(size=shape, dtype=np.float32)
+    return (x.view(np.uint32) >> 16).astype(np.uint16)
+
+
+def random_frames(n: int, H: int, W: int, rng: np.random.Generator) -> list:
+    """n model-input frames [3][H][W] (bf16 bits)."""
+    return [random_bf16((3, H, W), rng) for _ in range(n)]
