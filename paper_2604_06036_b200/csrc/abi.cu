@@ -1,0 +1,166 @@
+// abi.cu — the C ABI of libcodecsight: host-side argument validation, then the launchers of score.cu,
+// compact.cu and kv_refresh.cu.  Declarations and the contract of every call: include/codecsight.h.
+#include <math.h>
+
+#include <atomic>
+
+#include "cs_internal.cuh"
+
+namespace {
+
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sms[kMaxDevices];
+std::atomic<unsigned> g_attr_done[kMaxDevices];  // bit per kernel slot
+
+int grid_ok(const cs_grid* g) {
+  if (!g) return CS_ERR_INVALID_ARGUMENT;
+  if (g->src_w < 1 || g->src_h < 1 || g->src_w > 16384 || g->src_h > 16384) return CS_ERR_SHAPE;
+  if (g->mb_size < 1 || g->mb_size > 64) return CS_ERR_SHAPE;
+  if (g->mb_cols != (g->src_w + g->mb_size - 1) / g->mb_size) return CS_ERR_SHAPE;
+  if (g->mb_rows != (g->src_h + g->mb_size - 1) / g->mb_size) return CS_ERR_SHAPE;
+  if (g->grid_w < 1 || g->grid_h < 1 || static_cast<long long>(g->grid_w) * g->grid_h > cs::kMaxGridPatches)
+    return CS_ERR_SHAPE;
+  if (g->group < 1 || g->grid_w % g->group != 0 || g->grid_h % g->group != 0) return CS_ERR_SHAPE;
+  if (static_cast<long long>(g->mb_rows) * g->grid_w > cs::kMaxMbRowsTimesGridW) return CS_ERR_UNSUPPORTED;
+  if (g->patch < 1 || g->patch > 32) return CS_ERR_SHAPE;
+  if (isnan(g->tau) || g->tau < 0.0f) return CS_ERR_INVALID_ARGUMENT;
+  if (isnan(g->alpha) || isinf(g->alpha) || g->alpha < 0.0f) return CS_ERR_INVALID_ARGUMENT;
+  return CS_OK;
+}
+
+int device_ok() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    return CS_ERR_CUDA;
+  }
+  return CS_OK;
+}
+
+}  // namespace
+
+int cs_num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int n = g_sms[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    g_sms[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
+int cs_set_smem_attr(const void* func, int slot, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  const unsigned bit = 1u << slot;
+  if (g_attr_done[dev].load(std::memory_order_acquire) & bit) return 0;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return -1;
+  g_attr_done[dev].fetch_or(bit, std::memory_order_release);
+  return 0;
+}
+
+extern "C" {
+
+int codecsight_version(void) { return 100; }
+
+const char* codecsight_strerror(int code) {
+  switch (code) {
+    case CS_OK: return "ok";
+    case CS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case CS_ERR_SHAPE: return "shape / dimension mismatch";
+    case CS_ERR_UNSUPPORTED: return "unsupported configuration";
+    case CS_ERR_CUDA: return "CUDA error";
+    default: return "unknown error";
+  }
+}
+
+int codecsight_score_patches(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                             const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
+                             uint32_t* gop_state, float* score, int32_t* kept_count,
+                             unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+  int rc = grid_ok(g);
+  if (rc) return rc;
+  if (n_streams < 0 || n_frames < 1 || n_frames > cs::kMaxFramesPerCall || frame_stride < n_frames)
+    return CS_ERR_INVALID_ARGUMENT;
+  if (n_streams == 0) return CS_OK;
+  if (!mb || !frame_type || !keep_mask || !gop_state || !kept_count || !counters || !status)
+    return CS_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(mb) & 7u) != 0) return CS_ERR_INVALID_ARGUMENT;
+  if (g->mb_cols > 4096) return CS_ERR_UNSUPPORTED;
+  if (static_cast<long long>(n_streams) * 8 > 0x7fffffffLL) return CS_ERR_UNSUPPORTED;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_score(g, n_streams, n_frames, mb, frame_type, keep_mask, frame_stride, gop_state, score,
+                         kept_count, counters, status, stream);
+}
+
+int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
+                       int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
+                       int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                       int32_t* frame_offsets, unsigned long long* counters, int32_t* status,
+                       cudaStream_t stream) {
+  int rc = grid_ok(g);
+  if (rc) return rc;
+  if (n_streams < 0 || n_frames < 1 || mask_frame_stride < n_frames || capacity < 0)
+    return CS_ERR_INVALID_ARGUMENT;
+  const long long n_slots = static_cast<long long>(n_streams) * n_frames;
+  if (n_slots * g->grid_w * g->grid_h >= 2147483648LL) return CS_ERR_UNSUPPORTED;
+  if (g->group * g->patch > 32) return CS_ERR_UNSUPPORTED;
+  if (!frame_offsets || !counters || !status) return CS_ERR_INVALID_ARGUMENT;
+  if (n_slots > 0 && (!keep_mask || !frame_index || !frames)) return CS_ERR_INVALID_ARGUMENT;
+  if (capacity > 0 && (!packed || !pos_ids || !src_index)) return CS_ERR_INVALID_ARGUMENT;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_compact(g, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, frames, capacity,
+                           packed, pos_ids, src_index, frame_offsets, counters, status, stream);
+}
+
+size_t codecsight_kv_refresh_workspace_size(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams) {
+  if (!kv || !win || n_streams < 0 || win->window < 1 || kv->head_dim < 2 || kv->head_dim > cs::kMaxHeadDim)
+    return 0;
+  return cs_kv_workspace_bytes(kv, win, n_streams);
+}
+
+int codecsight_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                          const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                          const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
+                          int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens,
+                          void* workspace, size_t workspace_bytes, unsigned long long* counters,
+                          int32_t* status, cudaStream_t stream) {
+  int rc = grid_ok(g);
+  if (rc) return rc;
+  if (!kv || !win) return CS_ERR_INVALID_ARGUMENT;
+  if (n_streams < 0 || token_cap < 0) return CS_ERR_INVALID_ARGUMENT;
+  if (kv->dtype != CS_BF16 && kv->dtype != CS_FP32) return CS_ERR_UNSUPPORTED;
+  if (kv->layers < 1 || kv->kv_heads < 1 || kv->head_dim < 2 || kv->head_dim > cs::kMaxHeadDim)
+    return CS_ERR_UNSUPPORTED;
+  if (kv->head_dim % 2 != 0) return CS_ERR_UNSUPPORTED;  // S:376 "odd head_dim"
+  if (kv->capacity < 0 || kv->refresh_capacity < 0 || kv->n_prompt < 0) return CS_ERR_INVALID_ARGUMENT;
+  if (!(kv->rope_base > 0.0)) return CS_ERR_INVALID_ARGUMENT;
+  const long long w = win->window, s = win->stride, k = win->step;
+  if (w < 1 || s < 1 || k < 0) return CS_ERR_INVALID_ARGUMENT;
+  if (s > w) return CS_ERR_UNSUPPORTED;
+  if (win->ring_frames < (k >= 1 ? w + s : w)) return CS_ERR_SHAPE;
+  if (w + s > cs::kMaxWindowPlusStride) return CS_ERR_UNSUPPORTED;
+  if (n_streams == 0) return CS_OK;
+  if (n_streams > 8192) return CS_ERR_UNSUPPORTED;
+  const long long nw = (static_cast<long long>(g->grid_w) * g->grid_h + 31) / 32;
+  if ((w + s) * nw * 4 > 96 * 1024) return CS_ERR_UNSUPPORTED;
+  const long long ngroups = static_cast<long long>(g->grid_w / g->group) * (g->grid_h / g->group);
+  if (w * ngroups + kv->n_prompt >= 2147483647LL || kv->capacity >= 2147483647LL ||
+      kv->refresh_capacity >= 2147483647LL || (k * s + w) >= 2147483647LL)
+    return CS_ERR_UNSUPPORTED;
+  if (!keep_mask_ring || !frame_type_ring || !new_cache || !disposition || !p_old || !n_tokens || !counters ||
+      !status || !workspace)
+    return CS_ERR_INVALID_ARGUMENT;
+  if (k >= 1 && !old_cache) return CS_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15u) != 0) return CS_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < cs_kv_workspace_bytes(kv, win, n_streams)) return CS_ERR_INVALID_ARGUMENT;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_kv_refresh(g, kv, win, n_streams, keep_mask_ring, frame_type_ring, old_cache, new_cache,
+                              refreshed, token_cap, disposition, p_old, n_tokens, workspace, workspace_bytes,
+                              counters, status, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,308 @@
+// compact.cu — codecsight_compact on sm_100a: stream compaction of kept patches into the packed ViT input
+// ("executes the ViT only on the selected patches"; order = reading Q14, pos ids = Q15).
+//
+// Two launches:
+//   compact_scan    one CTA: per-slot emitted-patch counts (groups with any keep bit x group^2) -> block-wide
+//                   exclusive scan with a running carry -> frame_offsets (cu_seqlens); capacity status; counters.
+//   compact_gather  persistent grid (a multiple of the SM count), one WARP per contiguous range of the flat
+//                   kept-group index space [0, total/group^2), so every warp moves the same number of bytes
+//                   whatever the per-frame kept fraction.  A warp locates its first slot by binary search over
+//                   frame_offsets, enumerates that slot's kept groups with ballots, gathers each group's
+//                   3 x (group*patch)^2 pixels from the bf16 frame with 8-byte loads into a per-warp shared
+//                   memory tile laid out in packed order, and writes the tile out with coalesced 16-byte stores
+//                   (a 2x2 group of 14-px patches = 4,704 B = 294 x 16 B, so every group starts 16-B aligned).
+// Pixels of pruned patches are never read.
+#include "cs_internal.cuh"
+
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kGatherThreads = 256;
+constexpr int kWarpsPerCta = kGatherThreads / 32;
+
+// per-warp tile of one group in packed order: 3 x (group*patch)^2 bf16, padded to 16 B
+__host__ __device__ __forceinline__ int tile_bytes_of(int p, int G) { return ((3 * G * G * p * p * 2) + 15) & ~15; }
+
+struct CompactParams {
+  int grid_w, grid_h, G, p, np, nw, ngc, ngroups;
+  int n_streams, n_frames, n_slots;
+  long long mask_frame_stride;
+  long long capacity;
+  int FH, FW;  // model-input frame height / width in pixels
+  int vec_out;
+  const uint32_t* keep_mask;
+  const int32_t* frame_index;
+  const void* const* frames;
+  uint16_t* packed;
+  int32_t* pos_ids;
+  int32_t* src_index;
+  int32_t* frame_offsets;
+  unsigned long long* counters;
+  int32_t* status;
+};
+
+__device__ __forceinline__ const uint32_t* slot_mask(const CompactParams& P, int slot) {
+  const int s = slot / P.n_frames, j = slot - s * P.n_frames;
+  return P.keep_mask + ((long long)s * P.mask_frame_stride + j) * P.nw;
+}
+
+// emitted groups of one slot
+__device__ int count_groups(const CompactParams& P, const uint32_t* m) {
+  if (P.G == 2 && P.grid_w == 32) {
+    // fast path (32 x 32 grid, 2 x 2 groups): one word per patch row; OR the two rows of a group row, fold
+    // horizontal pairs onto even bits, popcount.
+    int n = 0;
+    for (int r = 0; r < P.grid_h; r += 2) {
+      const uint32_t x = __ldg(m + r) | __ldg(m + r + 1);
+      n += __popc((x | (x >> 1)) & 0x55555555u);
+    }
+    return n;
+  }
+  int n = 0;
+  for (int q = 0; q < P.ngroups; ++q) n += cs::group_kept(m, q, P.ngc, P.G, P.grid_w) ? 1 : 0;
+  return n;
+}
+
+__global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_constant__ CompactParams P) {
+  __shared__ int s_warp[kScanThreads / 32];
+  __shared__ int s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gs2 = P.G * P.G;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < P.n_slots; base += kScanThreads) {
+    const int slot = base + tid;
+    int cnt = 0;
+    if (slot < P.n_slots) cnt = count_groups(P, slot_mask(P, slot)) * gs2;
+    int inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += v;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      int v = s_warp[lane];
+      int w = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= d) w += u;
+      }
+      s_warp[lane] = w - v;  // exclusive prefix of warp totals
+    }
+    __syncthreads();
+    const int excl = s_carry + s_warp[warp] + inc - cnt;
+    if (slot < P.n_slots) P.frame_offsets[slot] = excl;
+    __syncthreads();
+    if (tid == kScanThreads - 1) s_carry = excl + cnt;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const long long total = s_carry;
+    P.frame_offsets[P.n_slots] = static_cast<int32_t>(total);
+    const long long rows = total < P.capacity ? total : P.capacity;
+    if (total > P.capacity) cs::atomic_or_status(P.status, CS_STATUS_CAPACITY);
+    const unsigned long long row_bytes = 3ull * P.p * P.p * 2ull;
+    cs::atomic_add_u64(&P.counters[CS_CNT_PACKED_ROWS], static_cast<unsigned long long>(rows));
+    cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_COMPACT],
+                       static_cast<unsigned long long>(P.n_slots) * (4ull * P.nw + 4ull) +
+                           static_cast<unsigned long long>(rows) * (2ull * row_bytes + 16ull));
+  }
+}
+
+// Gather one kept group (gr, gc) of `frame` into the warp tile and write it to packed rows [n0, n0 + G^2).
+template <int TP, int TG>
+__device__ __forceinline__ void gather_group(const CompactParams& P, const uint16_t* __restrict__ frame,
+                                             bool vec_in, int gr, int gc, long long n0, int slot, int t_index,
+                                             uint16_t* tile, int lane) {
+  const int p = TP > 0 ? TP : P.p;
+  const int G = TG > 0 ? TG : P.G;
+  const int gp = G * p;  // group edge in pixels
+  const int pp = p * p;
+  const long long FW = P.FW;
+  const uint16_t* src0 = frame + (long long)(gr * gp) * FW + (long long)gc * gp;
+  const long long plane = (long long)P.FH * FW;
+  if (vec_in) {
+    // 8-byte loads: each group row segment is gp pixels = gp/4 pieces of 4 bf16.  Pairs of pixels never
+    // straddle a patch boundary (p even), so the tile is written with 4-byte stores.
+    const int cpr = gp / 4;
+    const int total = 3 * gp * cpr;
+    constexpr int kUnroll = (TP > 0) ? ((3 * TG * TP * (TG * TP / 4) + 31) / 32) : 4;
+    for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
+      uint2 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int e = e0 + u * 32 + lane;
+        if (e < total) {
+          const int row = e / cpr, piece = e - row * cpr;
+          const int c = row / gp, yy = row - c * gp;
+          v[u] = cs::ld_nc_v2(src0 + c * plane + (long long)yy * FW + piece * 4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int e = e0 + u * 32 + lane;
+        if (e < total) {
+          const int row = e / cpr, piece = e - row * cpr;
+          const int c = row / gp, yy = row - c * gp;
+          const int dy = yy / p, y = yy - dy * p;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int x = piece * 4 + 2 * k;
+            const int dx = x / p, xx = x - dx * p;
+            const int idx = ((dy * G + dx) * 3 + c) * pp + y * p + xx;
+            *reinterpret_cast<uint32_t*>(tile + idx) = k == 0 ? v[u].x : v[u].y;
+          }
+        }
+      }
+    }
+  } else {
+    const int total = 3 * gp * gp;
+    for (int e = lane; e < total; e += 32) {
+      const int row = e / gp, x = e - row * gp;
+      const int c = row / gp, yy = row - c * gp;
+      const int dy = yy / p, y = yy - dy * p, dx = x / p, xx = x - dx * p;
+      tile[((dy * G + dx) * 3 + c) * pp + y * p + xx] = src0[c * plane + (long long)yy * FW + x];
+    }
+  }
+  __syncwarp();
+  const int gs2 = G * G;
+  long long nvalid = P.capacity - n0;
+  nvalid = nvalid < 0 ? 0 : (nvalid > gs2 ? gs2 : nvalid);
+  const long long row_el = 3ll * pp;
+  uint16_t* dst = P.packed + n0 * row_el;
+  if (P.vec_out) {
+    const int n16 = static_cast<int>(nvalid * row_el * 2 / 16);
+    const uint4* t4 = reinterpret_cast<const uint4*>(tile);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int e = lane; e < n16; e += 32) d4[e] = t4[e];
+  } else {
+    const int nel = static_cast<int>(nvalid * row_el);
+    for (int e = lane; e < nel; e += 32) dst[e] = tile[e];
+  }
+  if (lane < nvalid) {
+    const int dy = lane / G, dx = lane - dy * G;
+    const int h = gr * G + dy, w = gc * G + dx;
+    const long long n = n0 + lane;
+    P.pos_ids[3 * n + 0] = t_index;
+    P.pos_ids[3 * n + 1] = h;
+    P.pos_ids[3 * n + 2] = w;
+    P.src_index[n] = slot * P.np + h * P.grid_w + w;
+  }
+  __syncwarp();  // tile reusable
+}
+
+template <int TP, int TG>
+__global__ void __launch_bounds__(kGatherThreads) compact_gather(const __grid_constant__ CompactParams P) {
+  extern __shared__ __align__(16) unsigned char g_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int G = TG > 0 ? TG : P.G;
+  const int gs2 = G * G;
+  const long long total_groups = static_cast<long long>(P.frame_offsets[P.n_slots]) / gs2;
+  const long long nwarps = static_cast<long long>(gridDim.x) * kWarpsPerCta;
+  const long long wid = static_cast<long long>(blockIdx.x) * kWarpsPerCta + wib;
+  long long q = total_groups * wid / nwarps;
+  const long long q1 = total_groups * (wid + 1) / nwarps;
+  if (q >= q1) return;
+  const int tile_bytes = tile_bytes_of(TP > 0 ? TP : P.p, G);
+  uint16_t* tile = reinterpret_cast<uint16_t*>(g_smem + (size_t)wib * tile_bytes);
+  uint32_t* mask = reinterpret_cast<uint32_t*>(g_smem + (size_t)kWarpsPerCta * tile_bytes) + wib * P.nw;
+
+  // slot containing group q: largest slot with frame_offsets[slot] <= q * gs2
+  int lo = 0, hi = P.n_slots;  // invariant: off[lo] <= x < off[hi]
+  const long long x = q * gs2;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (static_cast<long long>(__ldg(P.frame_offsets + mid)) <= x) lo = mid; else hi = mid;
+  }
+  int slot = lo;
+  long long skip = q - __ldg(P.frame_offsets + slot) / gs2;  // kept groups of the slot before q
+
+  while (q < q1 && slot < P.n_slots) {
+    const uint32_t* m = slot_mask(P, slot);
+    for (int t = lane; t < P.nw; t += 32) mask[t] = __ldg(m + t);
+    const uint16_t* frame = static_cast<const uint16_t*>(P.frames[slot]);
+    const int t_index = __ldg(P.frame_index + slot);
+    const int pe = TP > 0 ? TP : P.p;
+    const bool vec_in = ((reinterpret_cast<uintptr_t>(frame) & 7u) == 0) && ((P.FW & 3) == 0) &&
+                        (((G * pe) & 3) == 0) && ((pe & 1) == 0);
+    __syncwarp();
+    for (int base = 0; base < P.ngroups && q < q1; base += 32) {
+      const int qq = base + lane;
+      const bool kept = qq < P.ngroups && cs::group_kept(mask, qq, P.ngc, G, P.grid_w);
+      uint32_t bal = __ballot_sync(0xffffffffu, kept);
+      const int nb = __popc(bal);
+      if (skip >= nb) {
+        skip -= nb;
+        continue;
+      }
+      while (skip > 0) {  // drop the groups before q
+        bal &= bal - 1;
+        --skip;
+      }
+      while (bal && q < q1) {
+        const int b = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int gi = base + b;
+        const int gr = gi / P.ngc, gc = gi - gr * P.ngc;
+        const long long n0 = q * gs2;
+        if (n0 < P.capacity) gather_group<TP, TG>(P, frame, vec_in, gr, gc, n0, slot, t_index, tile, lane);
+        ++q;
+      }
+    }
+    ++slot;
+    skip = 0;
+  }
+}
+
+}  // namespace
+
+int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
+                      int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
+                      int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
+                      unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+  CompactParams P{};
+  P.grid_w = g->grid_w;
+  P.grid_h = g->grid_h;
+  P.G = g->group;
+  P.p = g->patch;
+  P.np = g->grid_w * g->grid_h;
+  P.nw = (P.np + 31) / 32;
+  P.ngc = g->grid_w / g->group;
+  P.ngroups = (g->grid_h / g->group) * P.ngc;
+  P.n_streams = n_streams;
+  P.n_frames = n_frames;
+  P.n_slots = n_streams * n_frames;
+  P.mask_frame_stride = mask_frame_stride;
+  P.capacity = capacity;
+  P.FH = g->grid_h * g->patch;
+  P.FW = g->grid_w * g->patch;
+  const long long row_bytes = 3ll * g->patch * g->patch * 2ll;
+  P.vec_out = ((reinterpret_cast<uintptr_t>(packed) & 15u) == 0 && (row_bytes % 16) == 0) ? 1 : 0;
+  P.keep_mask = keep_mask;
+  P.frame_index = frame_index;
+  P.frames = frames;
+  P.packed = static_cast<uint16_t*>(packed);
+  P.pos_ids = pos_ids;
+  P.src_index = src_index;
+  P.frame_offsets = frame_offsets;
+  P.counters = counters;
+  P.status = status;
+
+  compact_scan<<<1, kScanThreads, 0, stream>>>(P);
+  if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+  if (P.n_slots == 0 || capacity == 0) return CS_OK;
+  const int grid = cs_num_sms() * 4;
+  const size_t smem = (size_t)kWarpsPerCta * (tile_bytes_of(g->patch, g->group) + 4 * P.nw);
+  if (g->patch == 14 && g->group == 2) {
+    if (cs_set_smem_attr(reinterpret_cast<const void*>(compact_gather<14, 2>), 1, 96 * 1024)) return CS_ERR_CUDA;
+    compact_gather<14, 2><<<grid, kGatherThreads, smem, stream>>>(P);
+  } else {
+    if (cs_set_smem_attr(reinterpret_cast<const void*>(compact_gather<0, 0>), 2, 96 * 1024)) return CS_ERR_CUDA;
+    compact_gather<0, 0><<<grid, kGatherThreads, smem, stream>>>(P);
+  }
+  if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+  return CS_OK;
+}

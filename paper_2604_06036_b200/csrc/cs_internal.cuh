@@ -1,0 +1,135 @@
+// cs_internal.cuh — internal helpers of libcodecsight (sm_100a).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "codecsight.h"
+
+#define CS_DEV __device__ __forceinline__
+
+namespace cs {
+
+constexpr int kMaxGridPatches = 4096;
+constexpr int kMaxGridWords = kMaxGridPatches / 32;
+constexpr int kMaxMbRowsTimesGridW = 8192;
+constexpr int kMaxFramesPerCall = 256;
+constexpr int kMaxHeadDim = 512;
+constexpr int kMaxWindowPlusStride = 1024;
+
+// ---------------------------------------------------------------------------------------------------------
+// mbarrier + bulk-copy (TMA engine) PTX wrappers
+// ---------------------------------------------------------------------------------------------------------
+CS_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+CS_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+CS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+CS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+CS_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+CS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared (this CTA), completion signalled on `bar` (tx bytes).
+// dst, src 16-B aligned; bytes a multiple of 16.
+CS_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------------------
+// vector memory helpers
+// ---------------------------------------------------------------------------------------------------------
+CS_DEV uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+CS_DEV uint2 ld_nc_v2(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+CS_DEV void st_na_v4(void* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+CS_DEV float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+CS_DEV float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// fp32 -> bf16 bits, round to nearest even (NaN -> quiet NaN), same rule as the stored cache dtype.
+CS_DEV uint32_t f32_to_bf16_rne(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu) != 0) return (u >> 16) | 0x0040u;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return u >> 16;
+}
+
+CS_DEV void atomic_or_status(int32_t* status, int bits) {
+  if (bits) atomicOr(reinterpret_cast<int*>(status), bits);
+}
+
+CS_DEV void atomic_add_u64(unsigned long long* p, unsigned long long v) {
+  if (v) atomicAdd(p, v);
+}
+
+// warp-level group-bit enumeration helper: is group q (row-major over the group grid) kept in mask `m`
+// (a group is kept iff any of its G x G patches has its bit set).
+CS_DEV bool group_kept(const uint32_t* m, int q, int ngc, int G, int grid_w) {
+  const int gr = q / ngc, gc = q - gr * ngc;
+  bool any = false;
+  for (int dy = 0; dy < G; ++dy) {
+    const int base = (gr * G + dy) * grid_w + gc * G;
+    for (int dx = 0; dx < G; ++dx) {
+      const int i = base + dx;
+      any |= ((m[i >> 5] >> (i & 31)) & 1u) != 0;
+    }
+  }
+  return any;
+}
+
+}  // namespace cs
+
+// launchers (one per .cu), called by abi.cu after validation
+int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                    const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride, uint32_t* gop_state,
+                    float* score, int32_t* kept_count, unsigned long long* counters, int32_t* status,
+                    cudaStream_t stream);
+int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
+                      int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
+                      int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
+                      unsigned long long* counters, int32_t* status, cudaStream_t stream);
+int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                         const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                         const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
+                         int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens,
+                         void* workspace, size_t workspace_bytes, unsigned long long* counters, int32_t* status,
+                         cudaStream_t stream);
+size_t cs_kv_workspace_bytes(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams);
+int cs_num_sms();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel slot, device); 0 on success
+int cs_set_smem_attr(const void* func, int slot, int bytes);

@@ -1,0 +1,565 @@
+// kv_refresh.cu — codecsight_kv_refresh on sm_100a: selective KVC refresh for one sliding-window step
+// (Eq. 5 at P:354-357; SPEC plan_refresh S:390-398, selective_prefill S:399-402).
+//
+// Two launches:
+//   kv_plan    one CTA per stream.  Stages the stream's (w + s) ring masks in shared memory, counts tokens per
+//              frame with warp ballots, builds the per-frame segments of window k (reading Q12 makes every
+//              segment a contiguous run in both the old and the new cache, with one uniform dp per stream-step),
+//              writes the index outputs (disposition, p_old by p_new, n_tokens), clamps the data moves to the
+//              capacities (status bits), and leaves in the workspace: a header, the segment list and the fp32
+//              (cos, sin) table of R(dp) computed once per stream-step from fp64 angles (reading Q20).
+//   kv_gather  persistent grid (SM-count multiple).  The work items are (stream, 128-row block, layer, K|V);
+//              every CTA derives the same item prefix from the per-stream row counts and takes one contiguous,
+//              equal-sized range of items.  Each item walks the segments that overlap its row block: REUSE K runs
+//              are rotated (rotate_half pairs (i, i + D/2) loaded as two 16-B vectors, fp32 fma, RNE store),
+//              REUSE V runs and refreshed rows are contiguous 16-B vector copies.  No tensor cores: nothing here
+//              is a contraction; the kernel is HBM-bound.
+#include <math_constants.h>
+
+#include "cs_internal.cuh"
+
+namespace {
+
+constexpr int kPlanThreads = 256;
+constexpr int kGatherThreads = 256;
+constexpr int kRowBlock = 128;
+constexpr int kMaxSeg = 1025;  // w + 1 with w + s <= 1024
+
+enum { SEG_SKIP = 0, SEG_COPY = 1, SEG_REUSE = 2 };
+
+struct KvHdr {
+  int n_rows;  // rows of the new cache that can be touched: min(n_total, capacity)
+  int n_seg;
+  int dp;
+  int pad;
+};
+struct KvSeg {
+  int p_new;  // first row in the new cache
+  int len;    // rows (already clamped to the capacities)
+  int kind;   // SEG_COPY (refreshed rows) | SEG_REUSE (old cache, K rotated, V copied)
+  int src;    // first source row (old cache row for REUSE, refreshed-buffer row for COPY)
+};
+
+struct KvParams {
+  int grid_w, grid_h, G, nw, ngc, ngroups;
+  int w, s, k, ring;
+  int L, H, D, esz;
+  long long cap, rcap, token_cap;
+  int n_prompt, n_streams, max_seg, has_refreshed;
+  int vec_rot, vec_copy;  // 16-B vector paths usable: (D/2) % (16/esz) == 0, row bytes % 16 == 0
+  long long ws_stride;
+  const uint32_t* mring;
+  const uint8_t* tring;
+  const void* const* old_cache;
+  void* const* new_cache;
+  const void* const* refreshed;
+  uint8_t* disposition;
+  int32_t* p_old;
+  int32_t* n_tokens;
+  unsigned char* ws;
+  unsigned long long* counters;
+  int32_t* status;
+  double inv_freq[cs::kMaxHeadDim / 2];  // base^(-2i/D), computed on the host
+};
+
+__device__ __forceinline__ unsigned char* stream_ws(const KvParams& P, int s) { return P.ws + 16 + (long long)s * P.ws_stride; }
+
+// ------------------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ KvParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_n[cs::kMaxWindowPlusStride];       // tokens per frame of [lo, hi)
+  __shared__ uint8_t s_t[cs::kMaxWindowPlusStride];   // frame types
+  __shared__ KvSeg s_seg[kMaxSeg];                    // index segments (unclamped), one per frame + prompt
+  __shared__ int s_pold[kMaxSeg];                     // p_old of the first token of the segment (-1: NEW)
+  __shared__ int s_disp[kMaxSeg];
+  __shared__ int s_nseg, s_dp;
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(smem);  // [nfr][nw]
+
+  const int sidx = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int k = P.k, w = P.w, s = P.s;
+  const int lo = k >= 1 ? (k - 1) * s : 0;
+  const int ks = k * s, hi = ks + w;
+  const int nfr = hi - lo;
+  const int nw = P.nw;
+
+  for (int e = tid; e < nfr * nw; e += blockDim.x) {
+    const int fi = e / nw, t = e - fi * nw;
+    const int f = lo + fi;
+    s_mask[e] = __ldg(P.mring + ((long long)sidx * P.ring + (f % P.ring)) * nw + t);
+  }
+  for (int fi = tid; fi < nfr; fi += blockDim.x) s_t[fi] = __ldg(P.tring + (long long)sidx * P.ring + ((lo + fi) % P.ring));
+  __syncthreads();
+  // tokens per frame = groups with any keep bit (same rule as codecsight_compact)
+  for (int fi = warp; fi < nfr; fi += nwarp) {
+    int n = 0;
+    for (int base = 0; base < P.ngroups; base += 32) {
+      const int q = base + lane;
+      const bool kept = q < P.ngroups && cs::group_kept(s_mask + fi * nw, q, P.ngc, P.G, P.grid_w);
+      n += __popc(__ballot_sync(0xffffffffu, kept));
+    }
+    if (lane == 0) s_n[fi] = n;
+  }
+  __syncthreads();
+
+  if (tid == 0) {
+    // ---- serial segment construction over <= w + 1 entries -------------------------------------------
+    long long drop = 0;  // tokens of the dropped frames [(k-1)s, ks)
+    for (int f = lo; f < ks; ++f) drop += s_n[f - lo];
+    const int new_first = (k - 1) * s + w;  // frames >= new_first arrived with this stride
+    long long pnew = 0, rrow = 0, n_reuse = 0, n_anchor = 0, n_new = 0;
+    int nseg = 0;
+    for (int f = ks; f < hi; ++f) {
+      const int n = s_n[f - lo];
+      int disp, pold;
+      if (k == 0 || f >= new_first) {
+        disp = CS_DISP_NEW;
+        pold = -1;
+      } else {
+        disp = (s_t[f - lo] != CS_FRAME_P || f == ks) ? CS_DISP_ANCHOR : CS_DISP_REUSE;  // P:346, Q17
+        pold = static_cast<int>(drop + pnew);
+      }
+      s_seg[nseg].p_new = static_cast<int>(pnew);
+      s_seg[nseg].len = n;
+      s_seg[nseg].kind = disp;
+      s_seg[nseg].src = disp == CS_DISP_REUSE ? pold : static_cast<int>(rrow);
+      s_pold[nseg] = pold;
+      s_disp[nseg] = disp;
+      ++nseg;
+      if (disp != CS_DISP_REUSE) rrow += n;
+      if (disp == CS_DISP_REUSE) n_reuse += n;
+      else if (disp == CS_DISP_ANCHOR) n_anchor += n;
+      else n_new += n;
+      pnew += n;
+    }
+    const long long n_visual = pnew;
+    // prompt rows, always NEW
+    s_seg[nseg].p_new = static_cast<int>(pnew);
+    s_seg[nseg].len = P.n_prompt;
+    s_seg[nseg].kind = CS_DISP_NEW;
+    s_seg[nseg].src = static_cast<int>(rrow);
+    s_pold[nseg] = -1;
+    s_disp[nseg] = CS_DISP_NEW;
+    ++nseg;
+    n_new += P.n_prompt;
+    const long long n_total = n_visual + P.n_prompt;
+    s_nseg = nseg;
+    s_dp = static_cast<int>(-drop);
+
+    int* nt = P.n_tokens + (long long)sidx * 4;
+    nt[0] = static_cast<int>(n_visual);
+    nt[1] = static_cast<int>(n_reuse);
+    nt[2] = static_cast<int>(n_anchor);
+    nt[3] = static_cast<int>(n_new);
+
+    // ---- clamp the data moves (same rules as the oracle, per row) ---------------------------------------
+    int st = 0;
+    if (n_total > P.token_cap) st |= CS_STATUS_CAPACITY;
+    unsigned char* ws = stream_ws(P, sidx);
+    KvSeg* wseg = reinterpret_cast<KvSeg*>(ws + sizeof(KvHdr));
+    int nout = 0;
+    long long moved = 0;
+    for (int i = 0; i < nseg; ++i) {
+      const long long pn = s_seg[i].p_new, len = s_seg[i].len, src = s_seg[i].src;
+      long long valid = 0;
+      int kind = SEG_SKIP;
+      if (len == 0) continue;
+      if (s_disp[i] == CS_DISP_REUSE) {
+        // rows t with pn + t >= cap: CAPACITY; rows with pn + t < cap <= src + t: ORIGIN (src >= pn)
+        const long long in_cap = P.cap - pn;  // rows with p_new < cap
+        if (len > (in_cap > 0 ? in_cap : 0)) st |= CS_STATUS_CAPACITY;
+        valid = P.cap - src;
+        valid = valid < 0 ? 0 : (valid > len ? len : valid);
+        const long long lim = in_cap < len ? (in_cap > 0 ? in_cap : 0) : len;
+        if (lim > valid) st |= CS_STATUS_ORIGIN;
+        kind = SEG_REUSE;
+      } else if (P.has_refreshed) {
+        const long long a = P.cap - pn, b = P.rcap - src;
+        valid = a < b ? a : b;
+        valid = valid < 0 ? 0 : (valid > len ? len : valid);
+        if (valid < len) st |= CS_STATUS_CAPACITY;
+        kind = SEG_COPY;
+      }
+      if (valid > 0) {
+        wseg[nout].p_new = static_cast<int>(pn);
+        wseg[nout].len = static_cast<int>(valid);
+        wseg[nout].kind = kind;
+        wseg[nout].src = static_cast<int>(src);
+        ++nout;
+        moved += valid;
+      }
+    }
+    KvHdr* hdr = reinterpret_cast<KvHdr*>(ws);
+    hdr->n_rows = static_cast<int>(n_total < P.cap ? n_total : P.cap);
+    hdr->n_seg = nout;
+    hdr->dp = static_cast<int>(-drop);
+    hdr->pad = 0;
+    cs::atomic_or_status(P.status, st);
+    cs::atomic_add_u64(&P.counters[CS_CNT_TOK_REUSE], static_cast<unsigned long long>(n_reuse));
+    cs::atomic_add_u64(&P.counters[CS_CNT_TOK_ANCHOR], static_cast<unsigned long long>(n_anchor));
+    cs::atomic_add_u64(&P.counters[CS_CNT_TOK_NEW], static_cast<unsigned long long>(n_new));
+    cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_KV], static_cast<unsigned long long>(moved) * P.L * 2ull *
+                                                         (unsigned long long)(P.H * P.D * P.esz) * 2ull);
+    cs::atomic_add_u64(&P.counters[CS_CNT_STREAM_STEPS], 1ull);
+  }
+  __syncthreads();
+
+  // ---- index outputs by p_new: disposition, p_old --------------------------------------------------------
+  const int nseg = s_nseg;
+  uint8_t* dsp = P.disposition + (long long)sidx * P.token_cap;
+  int32_t* po = P.p_old + (long long)sidx * P.token_cap;
+  for (int i = warp; i < nseg; i += nwarp) {
+    const long long pn = s_seg[i].p_new;
+    const int len = s_seg[i].len, d = s_disp[i], pold = s_pold[i];
+    for (int t = lane; t < len; t += 32) {
+      const long long p = pn + t;
+      if (p < P.token_cap) {
+        dsp[p] = static_cast<uint8_t>(d);
+        po[p] = d == CS_DISP_NEW ? -1 : pold + t;
+      }
+    }
+  }
+  // ---- (cos, sin) of R(dp), fp64 angle rounded to fp32 (reading Q20) -------------------------------------
+  float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
+  for (int i = tid; i < P.D / 2; i += blockDim.x) {
+    const double ang = static_cast<double>(s_dp) * P.inv_freq[i];
+    cs_tab[i] = make_float2(__double2float_rn(cos(ang)), __double2float_rn(sin(ang)));
+  }
+}
+
+// ------------------------------------------------------------------------------------------------------------
+// gather: rotate/copy contiguous row runs
+// ------------------------------------------------------------------------------------------------------------
+template <typename T>
+struct Vec;  // 16-B vector of cache elements
+template <>
+struct Vec<uint16_t> {
+  static constexpr int N = 8;
+};
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+};
+
+__device__ __forceinline__ void rot8_bf16(uint4& a, uint4& b, const float* c, const float* s) {
+  uint32_t* pa = reinterpret_cast<uint32_t*>(&a);
+  uint32_t* pb = reinterpret_cast<uint32_t*>(&b);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float x1l = cs::bf16_lo(pa[q]), x1h = cs::bf16_hi(pa[q]);
+    const float x2l = cs::bf16_lo(pb[q]), x2h = cs::bf16_hi(pb[q]);
+    const float cl = c[2 * q], ch = c[2 * q + 1], sl = s[2 * q], sh = s[2 * q + 1];
+    const float o1l = __fmaf_rn(x1l, cl, -__fmul_rn(x2l, sl));
+    const float o2l = __fmaf_rn(x2l, cl, __fmul_rn(x1l, sl));
+    const float o1h = __fmaf_rn(x1h, ch, -__fmul_rn(x2h, sh));
+    const float o2h = __fmaf_rn(x2h, ch, __fmul_rn(x1h, sh));
+    pa[q] = cs::f32_to_bf16_rne(o1l) | (cs::f32_to_bf16_rne(o1h) << 16);
+    pb[q] = cs::f32_to_bf16_rne(o2l) | (cs::f32_to_bf16_rne(o2h) << 16);
+  }
+}
+
+__device__ __forceinline__ void rot4_f32(uint4& a, uint4& b, const float* c, const float* s) {
+  float* pa = reinterpret_cast<float*>(&a);
+  float* pb = reinterpret_cast<float*>(&b);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float x1 = pa[q], x2 = pb[q];
+    pa[q] = __fmaf_rn(x1, c[q], -__fmul_rn(x2, s[q]));
+    pb[q] = __fmaf_rn(x2, c[q], __fmul_rn(x1, s[q]));
+  }
+}
+
+// Rotate `nrows` contiguous K rows (Eq. 5).  Work unit = one pair of 16-B vectors (elements j*VE.. of the first
+// and second half of one head).  TH/TD > 0: compile-time head count / head dim (production shape).
+template <typename T, int TH, int TD>
+__device__ __forceinline__ void rotate_run(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                                           int nrows, int rH, int rD, const float* s_c, const float* s_s) {
+  constexpr int VE = Vec<T>::N;
+  const int H = TH > 0 ? TH : rH;
+  const int D = TD > 0 ? TD : rD;
+  const int half = D / 2;
+  const int vph = half / VE;  // vectors per half-head
+  const int upr = H * vph;    // units per row
+  const int rowb = H * D * static_cast<int>(sizeof(T));
+  const int total = nrows * upr;
+  constexpr int kU = 4;
+  for (int e0 = threadIdx.x; e0 < total; e0 += kU * blockDim.x) {
+    uint4 a[kU], b[kU];
+    int off1[kU], jv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < total) {
+        const int row = e / upr, un = e - row * upr;
+        const int h = un / vph, j = un - h * vph;
+        off1[u] = row * rowb + (h * D + j * VE) * static_cast<int>(sizeof(T));
+        jv[u] = j;
+        a[u] = cs::ld_nc_v4(src + off1[u]);
+        b[u] = cs::ld_nc_v4(src + off1[u] + half * static_cast<int>(sizeof(T)));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < total) {
+        const float* c = s_c + jv[u] * VE;
+        const float* s = s_s + jv[u] * VE;
+        if constexpr (sizeof(T) == 2) rot8_bf16(a[u], b[u], c, s);
+        else rot4_f32(a[u], b[u], c, s);
+        cs::st_na_v4(dst + off1[u], a[u]);
+        cs::st_na_v4(dst + off1[u] + half * static_cast<int>(sizeof(T)), b[u]);
+      }
+    }
+  }
+}
+
+// contiguous copy of `bytes` (multiple of 16) with 4 vectors in flight per thread
+__device__ __forceinline__ void copy_run(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                                         long long bytes) {
+  const long long n = bytes >> 4;
+  constexpr int kU = 4;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (long long e0 = threadIdx.x; e0 < n; e0 += kU * blockDim.x) {
+    uint4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long e = e0 + (long long)u * blockDim.x;
+      if (e < n) v[u] = cs::ld_nc_v4(s4 + e);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long e = e0 + (long long)u * blockDim.x;
+      if (e < n) cs::st_na_v4(d4 + e, v[u]);
+    }
+  }
+}
+
+// generic fallbacks (toy shapes): element-pair rotation and 4-byte copies
+template <typename T>
+__device__ __forceinline__ void rotate_run_scalar(const unsigned char* __restrict__ src,
+                                                  unsigned char* __restrict__ dst, int nrows, int H, int D,
+                                                  const float* s_c, const float* s_s) {
+  const int half = D / 2;
+  const int total = nrows * H * half;
+  const T* sp = reinterpret_cast<const T*>(src);
+  T* dp = reinterpret_cast<T*>(dst);
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int row = e / (H * half), r = e - row * H * half;
+    const int h = r / half, i = r - h * half;
+    const long long o1 = (long long)row * H * D + h * D + i, o2 = o1 + half;
+    float x1, x2;
+    if constexpr (sizeof(T) == 2) {
+      x1 = __uint_as_float(static_cast<uint32_t>(sp[o1]) << 16);
+      x2 = __uint_as_float(static_cast<uint32_t>(sp[o2]) << 16);
+    } else {
+      x1 = sp[o1];
+      x2 = sp[o2];
+    }
+    const float y1 = __fmaf_rn(x1, s_c[i], -__fmul_rn(x2, s_s[i]));
+    const float y2 = __fmaf_rn(x2, s_c[i], __fmul_rn(x1, s_s[i]));
+    if constexpr (sizeof(T) == 2) {
+      dp[o1] = static_cast<T>(cs::f32_to_bf16_rne(y1));
+      dp[o2] = static_cast<T>(cs::f32_to_bf16_rne(y2));
+    } else {
+      dp[o1] = y1;
+      dp[o2] = y2;
+    }
+  }
+}
+
+__device__ __forceinline__ void copy_run_u32(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                                             long long bytes) {
+  const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+  uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+  for (long long e = threadIdx.x; e < (bytes >> 2); e += blockDim.x) d4[e] = s4[e];
+}
+
+template <typename T, int TH, int TD>
+__global__ void __launch_bounds__(kGatherThreads) kv_gather(const __grid_constant__ KvParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  long long* s_pref = reinterpret_cast<long long*>(smem);                         // [n_streams + 1]
+  KvSeg* s_seg = reinterpret_cast<KvSeg*>(smem + 8 * ((P.n_streams + 2) & ~1));  // [max_seg]
+  float* s_c = reinterpret_cast<float*>(s_seg + P.max_seg);                       // [D/2]
+  float* s_s = s_c + P.D / 2;
+  __shared__ long long s_carry;
+  __shared__ int s_nseg, s_cur;
+
+  const int tid = threadIdx.x;
+  const int items_per_block = P.L * 2;
+  // ---- item prefix over streams (identical in every CTA) --------------------------------------------------
+  if (tid == 0) {
+    s_carry = 0;
+    s_cur = -1;
+  }
+  __syncthreads();
+  __shared__ long long s_wsum[kGatherThreads / 32];
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int base = 0; base < P.n_streams; base += blockDim.x) {
+    const int si = base + tid;
+    long long v = 0;
+    if (si < P.n_streams) {
+      const KvHdr* h = reinterpret_cast<const KvHdr*>(stream_ws(P, si));
+      const long long rows = h->n_seg > 0 ? h->n_rows : 0;
+      v = (rows + kRowBlock - 1) / kRowBlock * items_per_block;
+    }
+    long long inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long u = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += u;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    long long woff = s_carry;
+    for (int q = 0; q < warp; ++q) woff += s_wsum[q];
+    if (si < P.n_streams) s_pref[si + 1] = woff + inc;
+    __syncthreads();
+    if (tid == blockDim.x - 1) s_carry = woff + inc;
+    __syncthreads();
+  }
+  if (tid == 0) s_pref[0] = 0;
+  __syncthreads();
+  const long long V = s_pref[P.n_streams];
+  const long long it0 = V * blockIdx.x / gridDim.x, it1 = V * (blockIdx.x + 1) / gridDim.x;
+  const long long row_bytes = (long long)P.H * P.D * sizeof(T);
+
+  int sidx = 0;
+  for (long long it = it0; it < it1; ++it) {
+    while (s_pref[sidx + 1] <= it) ++sidx;  // uniform across the CTA
+    if (sidx != s_cur) {
+      __syncthreads();
+      const unsigned char* ws = stream_ws(P, sidx);
+      const KvHdr* h = reinterpret_cast<const KvHdr*>(ws);
+      const KvSeg* g = reinterpret_cast<const KvSeg*>(ws + sizeof(KvHdr));
+      const int nseg = h->n_seg;
+      for (int i = tid; i < nseg; i += blockDim.x) s_seg[i] = g[i];
+      const float2* tab = reinterpret_cast<const float2*>(ws + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
+      for (int i = tid; i < P.D / 2; i += blockDim.x) {
+        const float2 cs2 = tab[i];
+        s_c[i] = cs2.x;
+        s_s[i] = cs2.y;
+      }
+      if (tid == 0) {
+        s_nseg = nseg;
+        s_cur = sidx;
+      }
+      __syncthreads();
+    }
+    const long long local = it - s_pref[sidx];
+    const int blk = static_cast<int>(local / items_per_block);
+    const int lk = static_cast<int>(local - (long long)blk * items_per_block);
+    const int l = lk >> 1, kv = lk & 1;
+    const int a = blk * kRowBlock, b = a + kRowBlock;
+    unsigned char* nc = static_cast<unsigned char*>(P.new_cache[sidx]);
+    const unsigned char* oc = P.k >= 1 ? static_cast<const unsigned char*>(P.old_cache[sidx]) : nullptr;
+    const unsigned char* rf = P.has_refreshed ? static_cast<const unsigned char*>(P.refreshed[sidx]) : nullptr;
+    const long long plane_new = ((long long)(l * 2 + kv)) * P.cap;
+    for (int i = 0; i < s_nseg; ++i) {
+      const KvSeg sg = s_seg[i];
+      const int x0 = max(a, sg.p_new), x1 = min(b, sg.p_new + sg.len);
+      if (x0 >= x1) continue;
+      const int n = x1 - x0;
+      const long long srow = sg.src + (x0 - sg.p_new);
+      unsigned char* dst = nc + (plane_new + x0) * row_bytes;
+      if (sg.kind == SEG_REUSE) {
+        const unsigned char* src = oc + (plane_new + srow) * row_bytes;
+        if (kv == 0) {  // Eq. 5
+          if (TH > 0 || P.vec_rot) rotate_run<T, TH, TD>(src, dst, n, P.H, P.D, s_c, s_s);
+          else rotate_run_scalar<T>(src, dst, n, P.H, P.D, s_c, s_s);
+        } else {  // value reuse
+          if (TH > 0 || P.vec_copy) copy_run(src, dst, n * row_bytes);
+          else copy_run_u32(src, dst, n * row_bytes);
+        }
+      } else {
+        const unsigned char* src = rf + (((long long)(l * 2 + kv)) * P.rcap + srow) * row_bytes;
+        if (TH > 0 || P.vec_copy) copy_run(src, dst, n * row_bytes);
+        else copy_run_u32(src, dst, n * row_bytes);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+size_t cs_kv_workspace_bytes(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams) {
+  const size_t max_seg = static_cast<size_t>(win->window) + 1;
+  size_t stride = sizeof(KvHdr) + sizeof(KvSeg) * max_seg + 8 * static_cast<size_t>(kv->head_dim / 2);
+  stride = (stride + 15) & ~static_cast<size_t>(15);
+  return 16 + stride * static_cast<size_t>(n_streams);
+}
+
+int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                         const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                         const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
+                         int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens,
+                         void* workspace, size_t workspace_bytes, unsigned long long* counters, int32_t* status,
+                         cudaStream_t stream) {
+  (void)workspace_bytes;
+  KvParams P{};
+  P.grid_w = g->grid_w;
+  P.grid_h = g->grid_h;
+  P.G = g->group;
+  P.nw = (g->grid_w * g->grid_h + 31) / 32;
+  P.ngc = g->grid_w / g->group;
+  P.ngroups = (g->grid_h / g->group) * P.ngc;
+  P.w = win->window;
+  P.s = win->stride;
+  P.k = win->step;
+  P.ring = win->ring_frames;
+  P.L = kv->layers;
+  P.H = kv->kv_heads;
+  P.D = kv->head_dim;
+  P.esz = kv->dtype == CS_BF16 ? 2 : 4;
+  P.cap = kv->capacity;
+  P.rcap = kv->refresh_capacity;
+  P.token_cap = token_cap;
+  P.n_prompt = kv->n_prompt;
+  P.n_streams = n_streams;
+  P.max_seg = win->window + 1;
+  P.has_refreshed = refreshed != nullptr;
+  {
+    const int ve = 16 / P.esz;
+    P.vec_rot = ((P.D / 2) % ve) == 0;
+    P.vec_copy = ((static_cast<long long>(P.H) * P.D * P.esz) % 16) == 0;
+  }
+  const size_t max_seg = static_cast<size_t>(P.max_seg);
+  size_t stride = sizeof(KvHdr) + sizeof(KvSeg) * max_seg + 8 * static_cast<size_t>(kv->head_dim / 2);
+  P.ws_stride = static_cast<long long>((stride + 15) & ~static_cast<size_t>(15));
+  P.mring = keep_mask_ring;
+  P.tring = frame_type_ring;
+  P.old_cache = old_cache;
+  P.new_cache = new_cache;
+  P.refreshed = refreshed;
+  P.disposition = disposition;
+  P.p_old = p_old;
+  P.n_tokens = n_tokens;
+  P.ws = static_cast<unsigned char*>(workspace);
+  P.counters = counters;
+  P.status = status;
+  for (int i = 0; i < kv->head_dim / 2; ++i)
+    P.inv_freq[i] = pow(kv->rope_base, -2.0 * static_cast<double>(i) / static_cast<double>(kv->head_dim));
+
+  const int lo = win->step >= 1 ? (win->step - 1) * win->stride : 0;
+  const int nfr = win->step * win->stride + win->window - lo;
+  const size_t plan_smem = static_cast<size_t>(nfr) * P.nw * 4;
+  if (cs_set_smem_attr(reinterpret_cast<const void*>(kv_plan), 3, 128 * 1024)) return CS_ERR_CUDA;
+  kv_plan<<<n_streams, kPlanThreads, plan_smem, stream>>>(P);
+  if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+
+  const size_t gsmem = 8 * static_cast<size_t>((n_streams + 2) & ~1) + sizeof(KvSeg) * max_seg +
+                       8 * static_cast<size_t>(kv->head_dim / 2);
+  const int grid = cs_num_sms() * 4;
+  const void* fn;
+  const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
+  if (qwen) fn = reinterpret_cast<const void*>(kv_gather<uint16_t, 4, 128>);
+  else if (kv->dtype == CS_BF16) fn = reinterpret_cast<const void*>(kv_gather<uint16_t, 0, 0>);
+  else fn = reinterpret_cast<const void*>(kv_gather<float, 0, 0>);
+  const int slot = qwen ? 4 : (kv->dtype == CS_BF16 ? 5 : 6);
+  if (cs_set_smem_attr(fn, slot, 160 * 1024)) return CS_ERR_CUDA;
+  if (qwen) kv_gather<uint16_t, 4, 128><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  else if (kv->dtype == CS_BF16) kv_gather<uint16_t, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  else kv_gather<float, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+  return CS_OK;
+}

@@ -1,0 +1,368 @@
+// score.cu — codecsight_score_patches on sm_100a.
+//
+// Computes, per P-frame, the patch motion score M(i) = V(i) + alpha R(i) (Eq. 1-3), the
+// dynamic mask M(i) >= tau (Eq. 4), the GOP-accumulated active set and the group-complete
+// keep mask.  Readings: DESIGN.md Q1-Q13.
+//
+// Layout of the work: one thread-block CLUSTER per camera stream, one CTA per (group of) new frame(s) of that
+// stream.  Each CTA streams its frames' macroblock records from HBM into shared memory with the TMA bulk-copy
+// engine (cp.async.bulk, mbarrier-tracked, NSTAGE-deep ring of MB-row chunks), reduces MB -> patch with a
+// separable two-pass scheme (MB row -> patch column partial max / area-weighted SAD sums in smem, then patch
+// rows), and ballots the per-patch threshold decisions into 32-bit words.  The GOP accumulation is a segmented
+// OR-scan over the stream's frames in time order: after a cluster barrier every CTA reads the dynamic words of
+// the earlier frames of its stream straight out of the other CTAs' shared memory (DSMEM).
+//
+// Parity-relevant arithmetic is spelled out with IEEE intrinsics (no fast-math): the sqrt is correctly rounded,
+// R is one correctly rounded double division of two exact integers, M is one fp32 fma.
+#include <cooperative_groups.h>
+#include <math_constants.h>
+
+#include "cs_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct ScoreParams {
+  int src_w, src_h, mb, mb_cols, mb_rows, grid_w, grid_h, G;
+  int np, nw;
+  float tau, alpha;
+  double denom;  // mb^2 * 255 * src_w * src_h (exact)
+  int n_streams, n_frames, fpc, cluster;
+  long long frame_stride;
+  int use_bulk, chunk_rows, n_chunks, nstage;
+  unsigned row_bytes, chunk_alloc;
+  int want_score;
+  const cs_mb* mb_ptr;
+  const uint8_t* frame_type;
+  uint32_t* keep_mask;
+  uint32_t* gop_state;
+  float* score;
+  int32_t* kept_count;
+  unsigned long long* counters;
+  int32_t* status;
+  unsigned off_vrow, off_srow, off_dyn, off_bar;
+};
+
+__global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__ ScoreParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint8_t s_types[cs::kMaxFramesPerCall];
+  __shared__ int s_plist[cs::kMaxFramesPerCall];
+  __shared__ uint32_t s_state[cs::kMaxGridWords + 1];
+  __shared__ uint32_t s_out[cs::kMaxGridWords];
+  __shared__ uint32_t s_keep[cs::kMaxGridWords];
+  __shared__ int s_np, s_kept, s_badmb;
+  __shared__ unsigned long long s_near;
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int sidx = blockIdx.x / P.cluster;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nthr = blockDim.x;
+
+  unsigned char* stage = smem;
+  float* Vrow = reinterpret_cast<float*>(smem + P.off_vrow);
+  uint32_t* Srow = reinterpret_cast<uint32_t*>(smem + P.off_srow);
+  uint32_t* dyn = reinterpret_cast<uint32_t*>(smem + P.off_dyn);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.off_bar);
+
+  const int f_begin = rank * P.fpc;
+  const int f_end = min(P.n_frames, f_begin + P.fpc);
+  const int nw = P.nw;
+
+  // ---- prologue: frame types of the whole stream (the scan needs the earlier frames), GOP state in ----
+  for (int f = tid; f < P.n_frames; f += nthr) s_types[f] = P.frame_type[(long long)sidx * P.frame_stride + f];
+  for (int t = tid; t <= nw; t += nthr) s_state[t] = P.gop_state[(long long)sidx * (nw + 1) + t];
+  if (tid == 0) {
+    s_badmb = 0;
+    s_near = 0ull;
+    if (P.use_bulk)
+      for (int s = 0; s < P.nstage; ++s) cs::mbar_init(&bars[s], 1);
+    cs::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int n = 0;
+    for (int f = f_begin; f < f_end; ++f)
+      if (s_types[f] == CS_FRAME_P) s_plist[n++] = f;
+    s_np = n;
+  }
+  __syncthreads();
+
+  const int T = s_np * P.n_chunks;  // chunk sequence over this CTA's P-frames
+  const cs_mb* stream_mb = P.mb_ptr + (long long)sidx * P.n_frames * P.mb_rows * P.mb_cols;
+
+  auto chunk_src = [&](int q, int& r0, int& nrows) -> const cs_mb* {
+    const int f = s_plist[q / P.n_chunks];
+    const int c = q % P.n_chunks;
+    r0 = c * P.chunk_rows;
+    nrows = min(P.chunk_rows, P.mb_rows - r0);
+    return stream_mb + ((long long)f * P.mb_rows + r0) * P.mb_cols;
+  };
+  auto issue = [&](int q) {
+    int r0, nrows;
+    const cs_mb* src = chunk_src(q, r0, nrows);
+    const int s = q % P.nstage;
+    const uint32_t bytes = static_cast<uint32_t>(nrows) * P.row_bytes;
+    cs::mbar_arrive_expect_tx(&bars[s], bytes);
+    cs::bulk_g2s(stage + (size_t)s * P.chunk_alloc, src, bytes, &bars[s]);
+  };
+
+  if (P.use_bulk && tid == 0)
+    for (int q = 0; q < min(T, P.nstage); ++q) issue(q);
+
+  unsigned long long near_local = 0;
+  for (int q = 0; q < T; ++q) {
+    const int s = q % P.nstage;
+    int r0, nrows;
+    const cs_mb* src = chunk_src(q, r0, nrows);
+    const uint2* buf = reinterpret_cast<const uint2*>(stage + (size_t)s * P.chunk_alloc);
+    if (P.use_bulk) {
+      cs::mbar_wait(&bars[s], (q / P.nstage) & 1);
+    } else {
+      const uint2* g = reinterpret_cast<const uint2*>(src);
+      uint2* d = reinterpret_cast<uint2*>(stage + (size_t)s * P.chunk_alloc);
+      for (int e = tid; e < nrows * P.mb_cols; e += nthr) d[e] = g[e];
+      __syncthreads();
+    }
+    // ---- pass 1: MB row j -> per patch column c: max v_m and sum_i ox(c,i) * sad_m (exact, u32) ----------
+    int badmb = 0;
+    for (int it = tid; it < nrows * P.grid_w; it += nthr) {
+      const int row = it / P.grid_w;
+      const int c = it - row * P.grid_w;
+      const int px0 = c * P.src_w, px1 = px0 + P.src_w;
+      const int cw = P.mb * P.grid_w;  // MB width in scaled x units
+      const int i0 = px0 / cw, i1 = (px1 - 1) / cw;
+      float vmax = -CUDART_INF_F;
+      uint32_t ssum = 0;
+      for (int i = i0; i <= i1; ++i) {
+        const uint2 rec = buf[row * P.mb_cols + i];
+        const int dx = static_cast<int16_t>(rec.x & 0xffffu);
+        const int dy = static_cast<int16_t>(rec.x >> 16);
+        const uint32_t sad = rec.y & 0xffffu;
+        const uint32_t type = (rec.y >> 16) & 0xffu;
+        float v;
+        if (type <= CS_MB_SKIP) {
+          const uint32_t sq = static_cast<uint32_t>(dx * dx) + static_cast<uint32_t>(dy * dy);
+          v = __fmul_rn(__fsqrt_rn(__uint2float_rn(sq)), 0.25f);  // Eq. 1 in source px (qpel / 4)
+        } else {
+          v = CUDART_INF_F;  // INTRA (or unknown) -> maximally dynamic (Q9)
+          badmb |= (type > CS_MB_INTRA);
+        }
+        vmax = (v > vmax) ? v : vmax;
+        const int ox = min(px1, cw * (i + 1)) - max(px0, cw * i);
+        ssum += static_cast<uint32_t>(ox) * sad;
+      }
+      const int j = r0 + row;
+      Vrow[j * P.grid_w + c] = vmax;
+      Srow[j * P.grid_w + c] = ssum;
+    }
+    if (badmb) s_badmb = 1;
+    __syncthreads();  // chunk fully consumed, Vrow/Srow rows complete
+    if (P.use_bulk && tid == 0 && q + P.nstage < T) issue(q + P.nstage);
+
+    if (q % P.n_chunks == P.n_chunks - 1) {
+      // ---- pass 2: patch rows; Eq. 3 and Eq. 4; ballot into dynamic words ------------------------------
+      const int f = s_plist[q / P.n_chunks];
+      const int lf = f - f_begin;
+      const int ch = P.mb * P.grid_h;  // MB height in scaled y units
+      for (int i = tid; i < nw * 32; i += nthr) {
+        bool d = false;
+        if (i < P.np) {
+          const int r = i / P.grid_w;
+          const int c = i - r * P.grid_w;
+          const int py0 = r * P.src_h, py1 = py0 + P.src_h;
+          const int j0 = py0 / ch, j1 = (py1 - 1) / ch;
+          float V = -CUDART_INF_F;
+          unsigned long long S = 0ull;
+          for (int j = j0; j <= j1; ++j) {
+            const int oy = min(py1, ch * (j + 1)) - max(py0, ch * j);
+            const float vj = Vrow[j * P.grid_w + c];
+            V = (vj > V) ? vj : V;
+            S += static_cast<unsigned long long>(oy) * Srow[j * P.grid_w + c];
+          }
+          const float R = __double2float_rn(__ddiv_rn(static_cast<double>(S), P.denom));
+          const float M = isinf(V) ? CUDART_INF_F : __fmaf_rn(P.alpha, R, V);  // Eq. 3
+          d = (M >= P.tau);                                                  // Eq. 4 (inclusive, Q1)
+          if (isfinite(M) && fabsf(__fsub_rn(M, P.tau)) <= 1e-5f) ++near_local;
+          if (P.want_score) P.score[((long long)sidx * P.n_frames + f) * P.np + i] = M;
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, d);
+        if (lane == 0) dyn[lf * nw + (i >> 5)] = word;
+      }
+      __syncthreads();  // Vrow/Srow free for the next frame
+    }
+  }
+  // scores of I-frames: +inf (Q10)
+  if (P.want_score)
+    for (int f = f_begin; f < f_end; ++f)
+      if (s_types[f] != CS_FRAME_P)
+        for (int i = tid; i < P.np; i += nthr) P.score[((long long)sidx * P.n_frames + f) * P.np + i] = CUDART_INF_F;
+
+  cluster.sync();  // every CTA's dynamic words are published
+
+  // ---- segmented OR-scan over time (GOP accumulation) + group-complete expansion ----------
+  int st_bits = 0;
+  if (tid == 0) {
+    if (s_badmb) st_bits |= CS_STATUS_BAD_MB_TYPE;
+    int flag = s_state[nw] & 1u;
+    for (int f = 0; f < f_end; ++f) {
+      const uint8_t ty = s_types[f];
+      if (ty == CS_FRAME_P) {
+        if (!flag && f >= f_begin) st_bits |= CS_STATUS_NO_IFRAME;
+        flag = 1;
+      } else {
+        if (ty != CS_FRAME_I && f >= f_begin) st_bits |= CS_STATUS_BAD_FRAME_TYPE;
+        flag = 1;
+      }
+    }
+  }
+  unsigned long long kept_total = 0;
+  for (int f = f_begin; f < f_end; ++f) {
+    const bool isP = (s_types[f] == CS_FRAME_P);
+    for (int t = tid; t < nw; t += nthr) {
+      uint32_t acc = s_state[t];
+      uint32_t flag = s_state[nw] & 1u;
+      for (int f2 = 0; f2 <= f; ++f2) {
+        if (s_types[f2] != CS_FRAME_P) {
+          acc = 0u;  // I-frame: state := empty (Q7)
+          flag = 1u;
+        } else {
+          if (!flag) {
+            acc = 0u;  // P-frame on an uninitialised stream (Q11)
+            flag = 1u;
+          }
+          const uint32_t* rd = cluster.map_shared_rank(dyn, f2 / P.fpc);
+          acc |= rd[(f2 % P.fpc) * nw + t];
+        }
+      }
+      uint32_t full = 0xffffffffu;
+      if ((t + 1) * 32 > P.np) full = (P.np - t * 32 >= 32) ? 0xffffffffu : ((1u << (P.np - t * 32)) - 1u);
+      s_out[t] = isP ? acc : full;
+      if (f == P.n_frames - 1) {  // final GOP state of the stream
+        P.gop_state[(long long)sidx * (nw + 1) + t] = acc;
+        if (t == 0) P.gop_state[(long long)sidx * (nw + 1) + nw] = s_state[nw] | 1u;
+      }
+    }
+    if (tid == 0) s_kept = 0;
+    __syncthreads();
+    const int ngc = P.grid_w / P.G;
+    for (int i = tid; i < nw * 32; i += nthr) {
+      bool k = false;
+      if (i < P.np) {
+        const int h = i / P.grid_w, w = i - h * P.grid_w;
+        k = cs::group_kept(s_out, (h / P.G) * ngc + (w / P.G), ngc, P.G, P.grid_w);
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, k);
+      if (lane == 0) {
+        s_keep[i >> 5] = word;
+        atomicAdd(&s_kept, __popc(word));
+      }
+    }
+    __syncthreads();
+    const long long slot = (long long)sidx * P.frame_stride + f;
+    for (int t = tid; t < nw; t += nthr) P.keep_mask[slot * nw + t] = s_keep[t];
+    if (tid == 0) {
+      P.kept_count[(long long)sidx * P.n_frames + f] = s_kept;
+      kept_total += static_cast<unsigned long long>(s_kept);
+    }
+    __syncthreads();
+  }
+
+  // ---- counters / status -------------------------------------------------------------------------------
+  if (near_local) atomicAdd(&s_near, near_local);
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned long long nf = static_cast<unsigned long long>(f_end - f_begin);
+    const unsigned long long npf = static_cast<unsigned long long>(s_np);
+    const unsigned long long per_frame = 4ull * nw + 4ull + (P.want_score ? 4ull * P.np : 0ull);
+    unsigned long long bytes = nf * per_frame + npf * 8ull * P.mb_rows * P.mb_cols;
+    if (rank == 0) bytes += 2ull * 4ull * (nw + 1);
+    cs::atomic_add_u64(&P.counters[CS_CNT_FRAMES], nf);
+    cs::atomic_add_u64(&P.counters[CS_CNT_PFRAMES], npf);
+    cs::atomic_add_u64(&P.counters[CS_CNT_PATCHES], nf * P.np);
+    cs::atomic_add_u64(&P.counters[CS_CNT_KEPT], kept_total);
+    cs::atomic_add_u64(&P.counters[CS_CNT_NEAR_TAU], s_near);
+    cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_SCORE], bytes);
+    cs::atomic_or_status(P.status, st_bits);
+  }
+  cluster.sync();  // keep this CTA's shared memory alive until every DSMEM reader is done
+}
+
+}  // namespace
+
+int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                    const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride, uint32_t* gop_state,
+                    float* score, int32_t* kept_count, unsigned long long* counters, int32_t* status,
+                    cudaStream_t stream) {
+  ScoreParams P{};
+  P.src_w = g->src_w;
+  P.src_h = g->src_h;
+  P.mb = g->mb_size;
+  P.mb_cols = g->mb_cols;
+  P.mb_rows = g->mb_rows;
+  P.grid_w = g->grid_w;
+  P.grid_h = g->grid_h;
+  P.G = g->group;
+  P.np = g->grid_w * g->grid_h;
+  P.nw = (P.np + 31) / 32;
+  P.tau = g->tau;
+  P.alpha = g->alpha;
+  P.denom = static_cast<double>(g->mb_size) * static_cast<double>(g->mb_size) * 255.0 *
+            static_cast<double>(g->src_w) * static_cast<double>(g->src_h);
+  P.n_streams = n_streams;
+  P.n_frames = n_frames;
+  int cluster = n_frames < 8 ? n_frames : 8;
+  P.fpc = (n_frames + cluster - 1) / cluster;
+  cluster = (n_frames + P.fpc - 1) / P.fpc;
+  P.cluster = cluster;
+  P.frame_stride = frame_stride;
+  P.row_bytes = static_cast<unsigned>(g->mb_cols) * 8u;
+  P.use_bulk = ((reinterpret_cast<uintptr_t>(mb) & 15u) == 0 && (P.row_bytes % 16u) == 0) ? 1 : 0;
+  const unsigned target = 16384u;
+  P.chunk_rows = static_cast<int>(P.row_bytes >= target ? 1u : target / P.row_bytes);
+  if (P.chunk_rows > P.mb_rows) P.chunk_rows = P.mb_rows;
+  P.n_chunks = (P.mb_rows + P.chunk_rows - 1) / P.chunk_rows;
+  P.chunk_alloc = (static_cast<unsigned>(P.chunk_rows) * P.row_bytes + 127u) & ~127u;
+  P.nstage = P.chunk_alloc <= 16384u ? 4 : 2;
+  if (!P.use_bulk) P.nstage = 1;
+  P.want_score = score != nullptr;
+  P.mb_ptr = mb;
+  P.frame_type = frame_type;
+  P.keep_mask = keep_mask;
+  P.gop_state = gop_state;
+  P.score = score;
+  P.kept_count = kept_count;
+  P.counters = counters;
+  P.status = status;
+  unsigned off = P.nstage * P.chunk_alloc;
+  P.off_vrow = off;
+  off += ((static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u);
+  P.off_srow = off;
+  off += ((static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u);
+  P.off_dyn = off;
+  off += ((static_cast<unsigned>(P.fpc * P.nw) * 4u + 127u) & ~127u);
+  P.off_bar = off;
+  off += 64u;
+  const size_t smem = off;
+
+  if (smem > 200 * 1024) return CS_ERR_UNSUPPORTED;
+  if (cs_set_smem_attr(reinterpret_cast<const void*>(score_kernel), 0, 200 * 1024) != 0) return CS_ERR_CUDA;
+
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster), 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, score_kernel, P) != cudaSuccess) return CS_ERR_CUDA;
+  return CS_OK;
+}

@@ -1,0 +1,126 @@
+"""Multi-stream state of the hot path on one GPU (plumbing only: device buffers + the three ABI calls).
+
+One ``Pipeline`` owns, for its shard of camera streams, everything the path keeps between sliding-window steps
+(SURVEY §5 "per-stream state = gop_state + mask/type ring + KV buffers"):
+
+  gop_state   [S][grid_words + 1]      GOP accumulation state
+  mask_ring   [S][ring][grid_words]    keep masks of the last ring = w + s frames (decode-once)
+  type_ring   [S][ring]                I/P frame types
+  caches      2 x S buffers [L][2][capacity][H][D] (window k-1 / window k, swapped every step)
+  refreshed   S buffers [L][2][refresh_capacity][H][D] (rows the prefill recomputes: anchors, new, prompt)
+
+``step(k, ...)`` enqueues, on the current CUDA stream and without any host synchronisation:
+  codecsight_score_patches -> codecsight_compact -> codecsight_kv_refresh.
+Window k consumes frames [k s, k s + w); the new frames of step k are [(k-1)s + w, k s + w) (all w at k = 0).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _abi as abi
+
+
+class Pipeline:
+    def __init__(self, grid: dict, n_streams: int, window: int, stride: int, gop: int, kv: dict | None,
+                 n_prompt: int = 0, device=None, want_score: bool = False, packed_capacity: int | None = None,
+                 with_refreshed: bool = True):
+        self.g = dict(grid)
+        self.S, self.w, self.s, self.gop = n_streams, window, stride, gop
+        self.ring = window + stride
+        self.dev = torch.device(device if device is not None else "cuda")
+        self.nw = abi.grid_words(grid)
+        self.np = grid["grid_w"] * grid["grid_h"]
+        self.groups = (grid["grid_w"] // grid["group"]) * (grid["grid_h"] // grid["group"])
+        d = self.dev
+        S, ring, nw = n_streams, self.ring, self.nw
+        self.gop_state = torch.zeros(S, nw + 1, dtype=torch.int32, device=d)
+        self.mask_ring = torch.zeros(S, ring, nw, dtype=torch.int32, device=d)
+        self.type_ring = torch.zeros(S, ring, dtype=torch.uint8, device=d)
+        self.kept_count = torch.zeros(S, window, dtype=torch.int32, device=d)
+        self.score = torch.zeros(S, window, self.np, dtype=torch.float32, device=d) if want_score else None
+        self.counters = torch.zeros(abi.NCOUNTERS, dtype=torch.int64, device=d)
+        self.status = torch.zeros(1, dtype=torch.int32, device=d)
+        # packed ViT input: enough rows for the first window (every patch kept)
+        p = grid["patch"]
+        self.capacity = packed_capacity if packed_capacity is not None else S * window * self.np
+        self.packed = torch.empty(self.capacity, 3 * p * p, dtype=torch.bfloat16, device=d)
+        self.pos_ids = torch.empty(self.capacity, 3, dtype=torch.int32, device=d)
+        self.src_index = torch.empty(self.capacity, dtype=torch.int32, device=d)
+        self.frame_offsets = torch.zeros(S * window + 1, dtype=torch.int32, device=d)
+        self.frame_index = torch.zeros(S * window, dtype=torch.int32, device=d)
+        self.kv = None
+        if kv is not None:
+            self.n_prompt = n_prompt
+            cap = window * self.groups + n_prompt
+            anchors = 1 + math.ceil(max(0, window - stride) / max(1, gop))
+            rcap = (stride + anchors) * self.groups + n_prompt
+            self.kv = dict(kv, capacity=cap, refresh_capacity=rcap, n_prompt=n_prompt)
+            dt = torch.bfloat16 if kv["dtype"] == abi.CS_BF16 else torch.float32
+            shape = (kv["layers"], 2, cap, kv["kv_heads"], kv["head_dim"])
+            self.caches = [[torch.empty(shape, dtype=dt, device=d) for _ in range(S)] for _ in range(2)]
+            self.cache_ptrs = [abi.ptr_array(c, d) for c in self.caches]
+            rshape = (kv["layers"], 2, rcap, kv["kv_heads"], kv["head_dim"])
+            self.refreshed = [torch.empty(rshape, dtype=dt, device=d) for _ in range(S)] if with_refreshed else None
+            self.refreshed_ptrs = abi.ptr_array(self.refreshed, d) if with_refreshed else None
+            self.token_cap = cap
+            self.disposition = torch.zeros(S, cap, dtype=torch.uint8, device=d)
+            self.p_old = torch.zeros(S, cap, dtype=torch.int32, device=d)
+            self.n_tokens = torch.zeros(S, 4, dtype=torch.int32, device=d)
+            nbytes = abi.kv_workspace_size(self.kv, dict(window=window, stride=stride, step=1, ring_frames=ring), S)
+            self.workspace = torch.empty((nbytes + 15) // 16 * 16, dtype=torch.uint8, device=d)
+        self.cur = 0  # which cache set holds window k-1
+
+    # ------------------------------------------------------------------------------------------------------
+    def new_frames(self, k: int) -> tuple[int, int]:
+        """(first new frame index, number of new frames) of step k."""
+        if k == 0:
+            return 0, self.w
+        return (k - 1) * self.s + self.w, self.s
+
+    def ring_slot(self, k: int) -> int:
+        f0, _ = self.new_frames(k)
+        return f0 % self.ring
+
+    def init_cache_fill(self, gen: torch.Generator | None = None):
+        """Random K/V content (the prefill's output is out of scope; bits only need to be non-degenerate)."""
+        if self.kv is None:
+            return
+        for lst in self.caches + ([self.refreshed] if self.refreshed is not None else []):
+            for t in lst:
+                t.normal_(generator=gen)
+
+    def step(self, k: int, mb: torch.Tensor, frame_ptrs: torch.Tensor, frame_index: torch.Tensor | None = None,
+             types: torch.Tensor | None = None, use_refreshed: bool | None = None, do_kv: bool = True,
+             stream=None):
+        """Enqueue one sliding-window step.  ``mb``: [S][n_new][mb_rows][mb_cols] cs_mb records (uint8 view or any
+        dtype, contiguous, device); ``types``: [S][n_new] uint8 written into the ring (None = already there);
+        ``frame_ptrs``: device int64 [S*n_new] pointers to [3][H][W] bf16 frames."""
+        g = self.g
+        f0, n = self.new_frames(k)
+        off = f0 % self.ring
+        if types is not None:
+            self.type_ring[:, off:off + n].copy_(types, non_blocking=True)
+        abi.codecsight_score_patches(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:], self.ring,
+                                     self.gop_state, None if self.score is None else self.score[:, :n],
+                                     self.kept_count[:, :n], self.counters, self.status, stream)
+        fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
+        abi.codecsight_compact(g, self.S, n, self.mask_ring[:, off:], self.ring, fi, frame_ptrs, self.capacity,
+                               self.packed, self.pos_ids, self.src_index, self.frame_offsets[: self.S * n + 1],
+                               self.counters, self.status, stream)
+        if self.kv is not None and do_kv:
+            win = dict(window=self.w, stride=self.s, step=k, ring_frames=self.ring)
+            old, new = self.cache_ptrs[self.cur], self.cache_ptrs[1 - self.cur]
+            use_r = (k >= 1) if use_refreshed is None else use_refreshed
+            abi.codecsight_kv_refresh(g, self.kv, win, self.S, self.mask_ring, self.type_ring, old, new,
+                                      self.refreshed_ptrs if use_r else None, self.token_cap, self.disposition,
+                                      self.p_old, self.n_tokens, self.workspace, self.counters, self.status, stream)
+            self.cur = 1 - self.cur
+
+    def kernel_launches_per_step(self, k: int) -> int:
+        """Kernels of this library launched by one step (score 1, compact 2, kv_refresh 2)."""
+        n = 1 + (2 if self.S > 0 else 1)
+        if self.kv is not None:
+            n += 2
+        return n

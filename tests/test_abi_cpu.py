@@ -1,0 +1,95 @@
+"""The C-ABI library loads and exports every symbol include/codecsight.h declares; host-side validation
+returns the documented codes without launching anything (no GPU needed)."""
+import ctypes as C
+
+import pytest
+import torch
+
+from synth import make_grid
+
+
+@pytest.fixture(scope="module")
+def abi():
+    import __graft_entry__ as ge
+    ge.build_cuda()
+    from paper_2604_06036_b200 import _abi
+    _abi.lib()
+    return _abi
+
+
+def test_exports_every_declared_symbol(abi):
+    syms = abi.declared_symbols()
+    assert set(syms) >= {"codecsight_score_patches", "codecsight_compact", "codecsight_kv_refresh"}
+    for s in syms:
+        assert hasattr(abi.lib(), s), s
+    assert abi.lib().codecsight_version() == 100
+    assert abi.lib().codecsight_strerror(-2) == b"shape / dimension mismatch"
+
+
+def test_sm100a_cubin_only(abi):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", abi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+FAKE = 0x1000  # never dereferenced: validation fails (or the device check does) before any launch
+
+
+def _score(abi, g, n_streams=1, n_frames=2, frame_stride=2, mb=FAKE):
+    L = abi.lib()
+    return L.codecsight_score_patches(C.byref(abi.make_grid(g)), n_streams, n_frames, mb, FAKE, FAKE, frame_stride,
+                                      FAKE, None, FAKE, FAKE, FAKE, None)
+
+
+def test_score_validation(abi):
+    g = make_grid(1920, 1080)
+    assert _score(abi, dict(g, mb_rows=67)) == abi.CS_ERR_SHAPE          # coded grid must be ceil(src/16)
+    assert _score(abi, dict(g, group=3)) == abi.CS_ERR_SHAPE             # group must divide the grid
+    assert _score(abi, dict(g, tau=float("nan"))) == abi.CS_ERR_INVALID_ARGUMENT
+    assert _score(abi, dict(g, alpha=-1.0)) == abi.CS_ERR_INVALID_ARGUMENT
+    assert _score(abi, g, n_frames=0) == abi.CS_ERR_INVALID_ARGUMENT
+    assert _score(abi, g, frame_stride=1) == abi.CS_ERR_INVALID_ARGUMENT
+    assert _score(abi, g, n_streams=0) == abi.CS_OK                      # empty batch: nothing to do
+    assert _score(abi, g, mb=FAKE + 4) == abi.CS_ERR_INVALID_ARGUMENT    # 8-B aligned records
+    assert _score(abi, dict(g, grid_w=128, grid_h=64)) == abi.CS_ERR_SHAPE
+    if not torch.cuda.is_available():
+        assert _score(abi, g) == abi.CS_ERR_CUDA                          # no CPU fallback
+
+
+def test_kv_validation(abi):
+    L = abi.lib()
+    g = make_grid(448, 448)
+
+    def call(kv, win, ws_bytes=1 << 20, n_streams=1):
+        return L.codecsight_kv_refresh(C.byref(abi.make_grid(g)), C.byref(abi.make_kv(kv)),
+                                       C.byref(abi.make_window(win)), n_streams, FAKE, FAKE, FAKE, FAKE, None, 16,
+                                       FAKE, FAKE, FAKE, FAKE, ws_bytes, FAKE, FAKE, None)
+
+    kv = dict(layers=2, kv_heads=2, head_dim=16, dtype=1, capacity=64, refresh_capacity=64, rope_base=1e4,
+              n_prompt=0)
+    win = dict(window=8, stride=2, step=1, ring_frames=10)
+    assert call(dict(kv, head_dim=15), win) == abi.CS_ERR_UNSUPPORTED    # odd head_dim
+    assert call(dict(kv, dtype=7), win) == abi.CS_ERR_UNSUPPORTED
+    assert call(kv, dict(win, stride=9, ring_frames=17)) == abi.CS_ERR_UNSUPPORTED   # s > w
+    assert call(kv, dict(win, ring_frames=9)) == abi.CS_ERR_SHAPE        # ring < w + s
+    assert call(kv, dict(win, step=0, ring_frames=8)) != abi.CS_ERR_SHAPE
+    assert call(kv, win, ws_bytes=8) == abi.CS_ERR_INVALID_ARGUMENT      # workspace too small
+    assert call(kv, win, n_streams=0) == abi.CS_OK
+    assert call(dict(kv, rope_base=0.0), win) == abi.CS_ERR_INVALID_ARGUMENT
+    ws = abi.kv_workspace_size(kv, win, 3)
+    assert ws >= 16 + 3 * (16 + 9 * 16 + 8 * 8)
+
+
+def test_compact_validation(abi):
+    L = abi.lib()
+    g = make_grid(448, 448)
+
+    def call(g, cap=16, n_streams=1, n_frames=1, mfs=1):
+        return L.codecsight_compact(C.byref(abi.make_grid(g)), n_streams, n_frames, FAKE, mfs, FAKE, FAKE, cap,
+                                    FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, None)
+
+    assert call(g, cap=-1) == abi.CS_ERR_INVALID_ARGUMENT
+    assert call(g, mfs=0) == abi.CS_ERR_INVALID_ARGUMENT
+    assert call(dict(g, patch=40)) == abi.CS_ERR_SHAPE
+    assert call(dict(g, patch=20)) == abi.CS_ERR_UNSUPPORTED     # group * patch > 32
+    assert call(g, n_streams=1 << 20, n_frames=4096, mfs=4096) == abi.CS_ERR_UNSUPPORTED   # int32 offsets

@@ -1,0 +1,518 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element, on seeded inputs.
+
+Bar (north star): masks, kept counts, compacted rows, position ids, source indices, offsets, dispositions, p_old
+and token counts bit-exact; fp32 scores bit-exact (<= 1e-5 relative required); pure K/V copies bit-exact;
+rotated K within 1e-2 abs (bf16) / 1e-5 (fp32), with the count of non-bit-exact elements reported.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from synth import MB_DTYPE, make_grid
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def abi():
+    import __graft_entry__ as ge
+    ge.build_cuda()
+    from paper_2604_06036_b200 import _abi
+    _abi.lib()
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return _abi
+
+
+def d_mb(mb):
+    return torch.from_numpy(np.ascontiguousarray(mb, dtype=MB_DTYPE).view(np.uint8)).to(DEV)
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+# ------------------------------------------------------------------------------------------------------------
+# score_patches
+# ------------------------------------------------------------------------------------------------------------
+def run_score_both(abi, ref, g, mb, types, gop_h=None, frame_stride=None, want_score=True):
+    """mb [S][n][rows][cols], types [S][frame_stride] -> (gpu dict, oracle dict)."""
+    S, n = mb.shape[:2]
+    nw = abi.grid_words(g)
+    fs = n if frame_stride is None else frame_stride
+    gop_h = np.zeros((S, nw + 1), np.uint32) if gop_h is None else gop_h
+    gs_d = torch.from_numpy(gop_h.view(np.int32).copy()).to(DEV)
+    km_d = torch.zeros(S, fs, nw, dtype=torch.int32, device=DEV)
+    sc_d = torch.zeros(S, n, g["grid_w"] * g["grid_h"], dtype=torch.float32, device=DEV) if want_score else None
+    kc_d = torch.zeros(S, n, dtype=torch.int32, device=DEV)
+    cnt_d = torch.zeros(16, dtype=torch.int64, device=DEV)
+    st_d = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ty_d = torch.from_numpy(np.ascontiguousarray(types, dtype=np.uint8)).to(DEV)
+    abi.codecsight_score_patches(g, S, n, d_mb(mb), ty_d, km_d, fs, gs_d, sc_d, kc_d, cnt_d, st_d)
+    o = ref.score_patches(g, mb, types, gop_h, frame_stride=fs, want_score=want_score)
+    torch.cuda.synchronize()
+    gpu = dict(keep_mask=u32(km_d), kept_count=kc_d.cpu().numpy(), score=None if sc_d is None else sc_d.cpu().numpy(),
+               gop_state=u32(gs_d), counters=cnt_d.cpu().numpy().view(np.uint64), status=int(st_d.item()))
+    o["gop_state"] = gop_h
+    return gpu, o
+
+
+def assert_score_equal(gpu, o, n, fs):
+    assert gpu["status"] == o["status"]
+    assert (gpu["keep_mask"][:, :n] == o["keep_mask"][:, :n]).all()
+    assert (gpu["kept_count"] == o["kept_count"]).all()
+    assert (gpu["gop_state"] == o["gop_state"]).all()
+    assert (gpu["counters"] == o["counters"]).all(), (gpu["counters"], o["counters"])
+    if o["score"] is not None:
+        a, b = gpu["score"], o["score"]
+        # scores: bit-exact expected (same IEEE operations); the gate is 1e-5 relative
+        assert ((a == b) | (np.abs(a - b) <= 1e-5 * np.abs(b))).all()
+        assert (a.view(np.uint32) == b.view(np.uint32)).all(), int((a.view(np.uint32) != b.view(np.uint32)).sum())
+
+
+@pytest.mark.parametrize("scene", ["static", "translating_object", "multi_object", "noise", "scene_cut"])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_score_c1_whole_stream(abi, ref, scene, seed):
+    """C1: 448x448, 64 frames, GOP 4, first window of 8 then strides of 2 (state carried across calls)."""
+    cfg = synth.CONFIGS["C1"]
+    g = make_grid(448, 448)
+    nf = cfg["frames"]
+    mb = synth.stream_metadata(448, 448, scene, synth.stream_seed(cfg, seed), nf)
+    types = synth.frame_types(nf, cfg["gop"])
+    nw = abi.grid_words(g)
+    gop_h = np.zeros((1, nw + 1), np.uint32)
+    f0 = 0
+    while f0 < nf:
+        n = cfg["window"] if f0 == 0 else cfg["stride"]
+        gpu, o = run_score_both(abi, ref, g, mb[None, f0:f0 + n], types[None, f0:f0 + n], gop_h.copy())
+        assert_score_equal(gpu, o, n, n)
+        gop_h = o["gop_state"]
+        f0 += n
+
+
+@pytest.mark.parametrize("geom", [(448, 448, 16, 32, 32, 2), (1920, 1080, 16, 32, 32, 2),
+                                  (3840, 2160, 16, 32, 32, 2), (40, 36, 8, 4, 4, 2), (100, 44, 16, 8, 8, 4),
+                                  (30, 30, 8, 6, 6, 3), (56, 56, 16, 4, 4, 1), (72, 40, 8, 12, 10, 2),
+                                  (1000, 700, 16, 40, 30, 2), (4000, 300, 16, 64, 8, 2)])
+@pytest.mark.parametrize("alpha,tau", [(0.0, 0.25), (0.5, 0.25), (1.0, 0.0), (5.0, 1.0), (0.25, 5.0),
+                                       (0.0, float("inf"))])
+def test_score_random_geometries(abi, ref, geom, alpha, tau):
+    """Odd MB columns (non-bulk path), groups 1/2/3/4, partial last bitmap word, extreme MVs and bad types."""
+    sw, sh, m, gw, gh, G = geom
+    g = make_grid(sw, sh, tau=tau, alpha=alpha, mb_size=m, grid_w=gw, grid_h=gh, group=G, patch=4)
+    rng = np.random.default_rng(abs(hash((geom, alpha, tau))) % 2**32)
+    S, n = 3, 5
+    mb = np.stack([np.stack([synth.random_mb(g["mb_rows"], g["mb_cols"], rng, p_intra=0.02, mv_max=3,
+                                             p_bad_type=0.001) for _ in range(n)]) for _ in range(S)])
+    mb["mvx"][0, 1, 0, 0] = -32768
+    mb["mvy"][0, 1, 0, 0] = -32768
+    types = np.array([[0, 1, 1, 1, 0], [1, 1, 0, 1, 1], [0, 1, 3, 1, 1]], np.uint8)  # NO_IFRAME, bad type
+    gpu, o = run_score_both(abi, ref, g, mb, types)
+    assert_score_equal(gpu, o, n, n)
+
+
+def test_score_ring_stride_and_no_score(abi, ref):
+    """keep_mask / frame_type addressed through frame_stride (ring slots), score output skipped."""
+    g = make_grid(1920, 1080)
+    S, n, fs = 4, 4, 20
+    mb = np.stack([synth.stream_metadata(1920, 1080, "medium", 5 + s, n) for s in range(S)])
+    types = np.zeros((S, fs), np.uint8)
+    types[:, :n] = synth.frame_types(n, 16, 13)
+    gpu, o = run_score_both(abi, ref, g, mb, types, frame_stride=fs, want_score=False)
+    assert_score_equal(gpu, o, n, fs)
+    assert (gpu["keep_mask"][:, n:] == 0).all()       # untouched slots
+
+
+@pytest.mark.parametrize("cfg_name", ["C2", "C4", "C5"])
+def test_score_full_size_batches(abi, ref, cfg_name):
+    """BASELINE shapes: C2 32 streams x 4 frames 1080p; C4 mixed (sampled 16 streams); C5 4K traffic (8 streams,
+    8 frames).  Launch configuration identical to the bench (one cluster per stream)."""
+    cfg = synth.CONFIGS[cfg_name]
+    sw, sh = cfg["src"]
+    g = make_grid(sw, sh)
+    S = {"C2": 32, "C4": 16, "C5": 8}[cfg_name]
+    n = cfg["stride"]
+    first = 3 * cfg["gop"] + 1
+    mb = np.stack([synth.stream_metadata(sw, sh, synth.scene_of(cfg, s), synth.stream_seed(cfg, s), n)
+                   for s in range(S)])
+    types = np.stack([synth.frame_types(n, cfg["gop"], first) for _ in range(S)])
+    nw = abi.grid_words(g)
+    rng = np.random.default_rng(1)
+    gop_h = np.zeros((S, nw + 1), np.uint32)
+    gop_h[:, :nw] = rng.integers(0, 2**32, size=(S, nw), dtype=np.uint64).astype(np.uint32) & np.uint32(0x01010101)
+    gop_h[:, nw] = 1
+    gpu, o = run_score_both(abi, ref, g, mb, types, gop_h)
+    assert_score_equal(gpu, o, n, n)
+
+
+# ------------------------------------------------------------------------------------------------------------
+# compact
+# ------------------------------------------------------------------------------------------------------------
+def run_compact_both(abi, ref, g, keep_mask, frame_index, frames, capacity, S, n, mfs):
+    nw = abi.grid_words(g)
+    p = g["patch"]
+    km_d = torch.from_numpy(np.ascontiguousarray(keep_mask).view(np.int32)).to(DEV)
+    fr_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in frames]
+    fptr = abi.ptr_array(fr_d, DEV) if fr_d else torch.zeros(1, dtype=torch.int64, device=DEV)
+    fi_d = torch.from_numpy(np.ascontiguousarray(frame_index, dtype=np.int32)).to(DEV)
+    cap = max(capacity, 1)
+    packed = torch.full((cap, 3 * p * p), -1, dtype=torch.int16, device=DEV)
+    pos = torch.full((cap, 3), -7, dtype=torch.int32, device=DEV)
+    src = torch.full((cap,), -7, dtype=torch.int32, device=DEV)
+    offs = torch.zeros(S * n + 1, dtype=torch.int32, device=DEV)
+    cnt_d = torch.zeros(16, dtype=torch.int64, device=DEV)
+    st_d = torch.zeros(1, dtype=torch.int32, device=DEV)
+    abi.codecsight_compact(g, S, n, km_d, mfs, fi_d, fptr, capacity, packed, pos, src, offs, cnt_d, st_d)
+    o = ref.compact(g, keep_mask, frame_index, frames, capacity, S, n, mask_frame_stride=mfs)
+    torch.cuda.synchronize()
+    rows = min(int(o["frame_offsets"][-1]), capacity)
+    assert int(st_d.item()) == o["status"]
+    assert (offs.cpu().numpy() == o["frame_offsets"]).all()
+    assert (packed.cpu().numpy().view(np.uint16)[:rows] == o["packed"][:rows]).all()
+    assert (pos.cpu().numpy()[:rows] == o["pos_ids"][:rows]).all()
+    assert (src.cpu().numpy()[:rows] == o["src_index"][:rows]).all()
+    assert (cnt_d.cpu().numpy().view(np.uint64) == o["counters"]).all()
+    if rows < cap:   # nothing written past the emitted rows
+        assert (src.cpu().numpy()[rows:] == -7).all()
+    return o
+
+
+def scored_masks(ref, g, cfg, S, n, first):
+    sw, sh = g["src_w"], g["src_h"]
+    mb = np.stack([synth.stream_metadata(sw, sh, synth.scene_of(cfg, s), synth.stream_seed(cfg, s, 3), n)
+                   for s in range(S)])
+    types = np.stack([synth.frame_types(n, cfg["gop"], first) for _ in range(S)])
+    nw = (g["grid_w"] * g["grid_h"] + 31) // 32
+    gs = np.zeros((S, nw + 1), np.uint32)
+    gs[:, nw] = 1
+    return ref.score_patches(g, mb, types, gs, want_score=False)["keep_mask"]
+
+
+@pytest.mark.parametrize("cfg_name,S,n", [("C1", 1, 8), ("C1", 5, 2), ("C2", 32, 4), ("C4", 8, 4)])
+def test_compact_configs(abi, ref, cfg_name, S, n):
+    cfg = synth.CONFIGS[cfg_name]
+    g = make_grid(*cfg["src"])
+    km = scored_masks(ref, g, cfg, S, n, first=1)
+    rng = np.random.default_rng(11)
+    frames = synth.random_frames(S * n, 448, 448, rng)
+    fidx = np.tile(np.arange(100, 100 + n, dtype=np.int32), S)
+    run_compact_both(abi, ref, g, km, fidx, frames, S * n * 1024, S, n, n)
+
+
+def test_compact_edge_cases(abi, ref):
+    g = make_grid(448, 448)
+    rng = np.random.default_rng(3)
+    S, n = 3, 3
+    km = rng.integers(0, 2**32, size=(S, n, 32), dtype=np.uint64).astype(np.uint32)  # not group-complete
+    km[1] = 0                                   # an empty stream
+    km[2, 1] = 0xFFFFFFFF                       # a full frame
+    frames = synth.random_frames(S * n, 448, 448, rng)
+    fidx = np.arange(S * n, dtype=np.int32)
+    o = run_compact_both(abi, ref, g, km, fidx, frames, S * n * 1024, S, n, n)
+    total = int(o["frame_offsets"][-1])
+    # capacity overflow in the middle of a group, and exactly at a group boundary
+    run_compact_both(abi, ref, g, km, fidx, frames, total // 2 + 1, S, n, n)
+    run_compact_both(abi, ref, g, km, fidx, frames, (total // 8) * 4, S, n, n)
+    run_compact_both(abi, ref, g, km, fidx, frames, 0, S, n, n)
+    # mask stride (ring) addressing
+    ring = np.zeros((S, 7, 32), np.uint32)
+    ring[:, 2:2 + n] = km
+    run_compact_both(abi, ref, g, ring[:, 2:].copy(), fidx, frames, S * n * 1024, S, n, 5)
+    # empty batch
+    run_compact_both(abi, ref, g, np.zeros((0, n, 32), np.uint32), np.zeros(0, np.int32), [], 16, 0, n, n)
+
+
+@pytest.mark.parametrize("geom", [(64, 48, 16, 8, 6, 2, 4), (30, 30, 8, 6, 6, 3, 6), (56, 56, 16, 4, 4, 1, 14),
+                                  (100, 44, 16, 8, 8, 4, 8), (72, 40, 8, 12, 10, 2, 3)])
+def test_compact_generic_geometries(abi, ref, geom):
+    """Generic (runtime patch/group) path, odd patch size (scalar loads), group 1/3/4."""
+    sw, sh, m, gw, gh, G, p = geom
+    g = make_grid(sw, sh, mb_size=m, grid_w=gw, grid_h=gh, group=G, patch=p)
+    rng = np.random.default_rng(5)
+    S, n = 2, 3
+    nw = abi.grid_words(g)
+    km = rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
+    km &= rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
+    frames = [rng.integers(0, 65536, size=(3, gh * p, gw * p), dtype=np.uint16) for _ in range(S * n)]
+    fidx = np.arange(S * n, dtype=np.int32)
+    run_compact_both(abi, ref, g, km, fidx, frames, S * n * gw * gh, S, n, n)
+
+
+# ------------------------------------------------------------------------------------------------------------
+# kv_refresh
+# ------------------------------------------------------------------------------------------------------------
+def _host_cache(t):
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def run_kv_both(abi, ref, g, kv, win, mring, tring, old_d, new_d, ref_d, token_cap, sample=None):
+    """Run GPU + oracle for one window step.  Returns (gpu dict, oracle dict, new_host_ref)."""
+    S = mring.shape[0]
+    dev = DEV
+    old_h = [_host_cache(t) for t in old_d] if old_d is not None else None
+    new_h = [_host_cache(t).copy() for t in new_d]
+    ref_h = [_host_cache(t) for t in ref_d] if ref_d is not None else None
+    m_d = torch.from_numpy(np.ascontiguousarray(mring).view(np.int32)).to(dev)
+    t_d = torch.from_numpy(np.ascontiguousarray(tring)).to(dev)
+    disp = torch.full((S, token_cap), 9, dtype=torch.uint8, device=dev)
+    pold = torch.full((S, token_cap), -9, dtype=torch.int32, device=dev)
+    ntok = torch.zeros(S, 4, dtype=torch.int32, device=dev)
+    ws = torch.empty(abi.kv_workspace_size(kv, win, S), dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(16, dtype=torch.int64, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    abi.codecsight_kv_refresh(g, kv, win, S, m_d, t_d, abi.ptr_array(old_d, dev) if old_d is not None else None,
+                              abi.ptr_array(new_d, dev), abi.ptr_array(ref_d, dev) if ref_d is not None else None,
+                              token_cap, disp, pold, ntok, ws, cnt, st)
+    o = ref.kv_refresh(g, kv, win, mring, tring, old_h, new_h, ref_h, token_cap)
+    torch.cuda.synchronize()
+    gpu = dict(disposition=disp.cpu().numpy(), p_old=pold.cpu().numpy(), n_tokens=ntok.cpu().numpy(),
+               counters=cnt.cpu().numpy().view(np.uint64), status=int(st.item()))
+    return gpu, o, new_h
+
+
+def assert_kv_equal(gpu, o, new_d, new_h, kv, stats=None):
+    assert gpu["status"] == o["status"]
+    assert (gpu["n_tokens"] == o["n_tokens"]).all()
+    assert (gpu["counters"] == o["counters"]).all(), (gpu["counters"], o["counters"])
+    S = len(new_d)
+    tc = gpu["disposition"].shape[1]
+    for s in range(S):
+        nt = min(int(o["n_tokens"][s, 0]) + kv["n_prompt"], tc)
+        assert (gpu["disposition"][s, :nt] == o["disposition"][s, :nt]).all()
+        assert (gpu["p_old"][s, :nt] == o["p_old"][s, :nt]).all()
+        assert (gpu["disposition"][s, nt:] == 9).all()        # nothing written past the tokens
+        a = _host_cache(new_d[s])
+        b = new_h[s]
+        rows = min(nt, kv["capacity"])
+        # V planes and every non-REUSE row: bit copies
+        assert (a[:, 1, :rows] == b[:, 1, :rows]).all()
+        disp = o["disposition"][s, :rows]
+        nonre = np.flatnonzero(disp != 2)
+        assert (a[:, 0, nonre] == b[:, 0, nonre]).all()
+        re = np.flatnonzero(disp == 2)
+        ka, kb = a[:, 0, re], b[:, 0, re]
+        if kv["dtype"] == 0:
+            fa = (ka.astype(np.uint32) << 16).view(np.float32)
+            fb = (kb.astype(np.uint32) << 16).view(np.float32)
+            tol = 1e-2
+        else:
+            fa, fb, tol = ka, kb, 1e-5
+        diff = np.abs(fa - fb).max() if fa.size else 0.0
+        assert diff <= tol, diff
+        if stats is not None:
+            stats["max_diff"] = max(stats.get("max_diff", 0.0), float(diff))
+            stats["not_bit_exact"] = stats.get("not_bit_exact", 0) + int((ka != kb).sum())
+            stats["rotated"] = stats.get("rotated", 0) + int(ka.size)
+
+
+def stream_rings(ref, g, cfg, S, ring, k, w, s, scene_seed=0):
+    """Score the frames of windows k-1 and k of S streams with the oracle and lay the masks out in rings."""
+    sw, sh = g["src_w"], g["src_h"]
+    nf = k * s + w
+    nw = (g["grid_w"] * g["grid_h"] + 31) // 32
+    mring = np.zeros((S, ring, nw), np.uint32)
+    tring = np.zeros((S, ring), np.uint8)
+    for si in range(S):
+        mb = synth.stream_metadata(sw, sh, synth.scene_of(cfg, si), synth.stream_seed(cfg, si, scene_seed), nf)
+        types = synth.frame_types(nf, cfg["gop"])
+        out = ref.score_patches(g, mb[None], types[None], np.zeros((1, nw + 1), np.uint32), want_score=False)
+        for f in range(max(0, (k - 1) * s), nf):
+            mring[si, f % ring] = out["keep_mask"][0, f]
+            tring[si, f % ring] = types[f]
+    return mring, tring
+
+
+def make_caches(kv, S, gen, with_refresh=True):
+    dt = torch.bfloat16 if kv["dtype"] == 0 else torch.float32
+    shape = (kv["layers"], 2, kv["capacity"], kv["kv_heads"], kv["head_dim"])
+    rshape = (kv["layers"], 2, kv["refresh_capacity"], kv["kv_heads"], kv["head_dim"])
+    old = [torch.randn(shape, generator=gen, device=DEV).to(dt) for _ in range(S)]
+    new = [torch.full(shape, 7.0, device=DEV).to(dt) for _ in range(S)]
+    refr = [torch.randn(rshape, generator=gen, device=DEV).to(dt) for _ in range(S)] if with_refresh else None
+    return old, new, refr
+
+
+@pytest.mark.parametrize("dtype", [1, 0])
+def test_kv_c1_all_windows(abi, ref, dtype):
+    """C1: 1 stream per scene kind, w=8, s=2, GOP 4, every window k = 0..28; toy fp32 and Qwen-shaped bf16."""
+    cfg = synth.CONFIGS["C1"]
+    g = make_grid(448, 448)
+    w, s = cfg["window"], cfg["stride"]
+    ring = w + s
+    base = synth.TOY_KV if dtype == 1 else synth.QWEN_KV
+    kv = dict(base, capacity=w * 256 + 32, refresh_capacity=w * 256 + 32, n_prompt=32)
+    if dtype == 0:
+        kv["layers"] = 2  # keep the oracle fast; the row shape (4 x 128 bf16) is the production one
+    S = 5
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(0)
+    stats = {}
+    steps = range(0, 29) if dtype == 1 else [0, 1, 2, 3, 7, 28]
+    for k in steps:
+        mring, tring = stream_rings(ref, g, cfg, S, ring, k, w, s)
+        old, new, refr = make_caches(kv, S, gen)
+        gpu, o, new_h = run_kv_both(abi, ref, g, kv, dict(window=w, stride=s, step=k, ring_frames=ring), mring,
+                                    tring, old if k else None, new, refr, kv["capacity"])
+        assert_kv_equal(gpu, o, new, new_h, kv, stats)
+    print("kv C1", dtype, stats)
+
+
+def test_kv_c3_sampled_streams(abi, ref):
+    """C3 shape: 1080p masks, w=32, s=4, GOP 16, Qwen2-VL-7B bf16 (28 layers); 4 streams, a mid-stream window."""
+    cfg = synth.CONFIGS["C3"]
+    g = make_grid(1920, 1080)
+    w, s, ring = 32, 4, 36
+    kv = dict(synth.QWEN_KV, capacity=w * 256 + 32, refresh_capacity=10 * 256 + 32, n_prompt=32)
+    S, k = 4, 9
+    mring, tring = stream_rings(ref, g, cfg, S, ring, k, w, s)
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(1)
+    old, new, refr = make_caches(kv, S, gen)
+    stats = {}
+    gpu, o, new_h = run_kv_both(abi, ref, g, kv, dict(window=w, stride=s, step=k, ring_frames=ring), mring, tring,
+                                old, new, refr, kv["capacity"])
+    assert_kv_equal(gpu, o, new, new_h, kv, stats)
+    print("kv C3", stats)
+
+
+def test_kv_edge_cases(abi, ref):
+    g = make_grid(448, 448)
+    cfg = synth.CONFIGS["C1"]
+    w, s = 8, 2
+    ring = w + s
+    S = 5
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(3)
+    mring, tring = stream_rings(ref, g, cfg, S, ring, 5, w, s)
+    win = dict(window=w, stride=s, step=5, ring_frames=ring)
+    # refreshed = NULL: non-REUSE rows untouched
+    kv = dict(synth.TOY_KV, capacity=w * 256 + 32, refresh_capacity=w * 256 + 32, n_prompt=32)
+    old, new, _ = make_caches(kv, S, gen, with_refresh=False)
+    gpu, o, new_h = run_kv_both(abi, ref, g, kv, win, mring, tring, old, new, None, kv["capacity"])
+    assert_kv_equal(gpu, o, new, new_h, kv)
+    # small capacities: cache, refresh buffer and index outputs all overflow (CAPACITY / ORIGIN status)
+    for cap, rcap, tc in [(300, 100, 250), (700, 5000, 2100), (64, 64, 64), (1, 0, 1)]:
+        kv2 = dict(kv, capacity=cap, refresh_capacity=rcap)
+        old, new, refr = make_caches(kv2, S, gen)
+        gpu, o, new_h = run_kv_both(abi, ref, g, kv2, win, mring, tring, old, new, refr, tc)
+        assert_kv_equal(gpu, o, new, new_h, kv2)
+    # s = w: everything NEW
+    mring2, tring2 = stream_rings(ref, g, cfg, S, 16, 3, 8, 8)
+    old, new, refr = make_caches(kv, S, gen)
+    gpu, o, new_h = run_kv_both(abi, ref, g, kv, dict(window=8, stride=8, step=3, ring_frames=16), mring2, tring2,
+                                old, new, refr, kv["capacity"])
+    assert_kv_equal(gpu, o, new, new_h, kv)
+    assert (gpu["n_tokens"][:, 1] == 0).all() and (gpu["n_tokens"][:, 2] == 0).all()
+    # odd-sized toy rows (scalar paths): D = 2, H = 1, fp32 and bf16
+    for dt in (1, 0):
+        kv3 = dict(layers=3, kv_heads=1, head_dim=2, dtype=dt, capacity=w * 256 + 4, refresh_capacity=w * 256 + 4,
+                   rope_base=1e4, n_prompt=4)
+        old, new, refr = make_caches(kv3, S, gen)
+        gpu, o, new_h = run_kv_both(abi, ref, g, kv3, win, mring, tring, old, new, refr, kv3["capacity"])
+        assert_kv_equal(gpu, o, new, new_h, kv3)
+    # bf16 with head_dim 8 (half < 8: scalar rotation, 16-B copies)
+    kv4 = dict(layers=2, kv_heads=2, head_dim=8, dtype=0, capacity=w * 256 + 4, refresh_capacity=w * 256 + 4,
+               rope_base=1e6, n_prompt=4)
+    old, new, refr = make_caches(kv4, S, gen)
+    gpu, o, new_h = run_kv_both(abi, ref, g, kv4, win, mring, tring, old, new, refr, kv4["capacity"])
+    assert_kv_equal(gpu, o, new, new_h, kv4)
+
+
+def test_kv_zero_slide_bit_exact(abi, ref):
+    """dp = 0 (dropped frames carry no tokens): REUSE keys must come back bit-identical (R(0) = I)."""
+    g = make_grid(128, 128, mb_size=32, grid_w=4, grid_h=4, patch=4, group=2)
+    nw = 1
+    mring = np.zeros((1, 8, nw), np.uint32)
+    groups = [[0, 1], [], [1], [1, 2], [], [], [2], [3]]
+    for f, gl in enumerate(groups):
+        bits = 0
+        for q in gl:
+            gr, gc = divmod(q, 2)
+            for dy in range(2):
+                for dx in range(2):
+                    bits |= 1 << ((gr * 2 + dy) * 4 + gc * 2 + dx)
+        mring[0, f, 0] = bits
+    tring = np.array([[0, 1, 1, 1, 1, 1, 1, 1]], np.uint8)
+    kv = dict(layers=2, kv_heads=4, head_dim=128, dtype=0, capacity=64, refresh_capacity=64, rope_base=1e6,
+              n_prompt=3)
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(9)
+    old, new, refr = make_caches(kv, 1, gen)
+    gpu, o, new_h = run_kv_both(abi, ref, g, kv, dict(window=4, stride=1, step=2, ring_frames=8), mring, tring, old,
+                                new, refr, 64)
+    assert_kv_equal(gpu, o, new, new_h, kv)
+    a = _host_cache(new[0])
+    b = _host_cache(old[0])
+    re = np.flatnonzero(gpu["disposition"][0] == 2)
+    assert re.size and (a[:, :, re] == b[:, :, re]).all()
+
+
+def test_pipeline_end_to_end_c4_shape(abi, ref):
+    """Pipeline (score -> compact -> kv_refresh) on a C4-shaped shard (4 streams: 2 static, 2 high-motion, 1080p,
+    w=16, s=4, GOP 16) for 4 steps, every output compared with the oracle driven the same way."""
+    from paper_2604_06036_b200.pipeline import Pipeline
+    cfg = synth.CONFIGS["C4"]
+    g = make_grid(1920, 1080)
+    S, w, s, gop = 4, 16, 4, 16
+    kvb = dict(synth.QWEN_KV, layers=2)
+    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=32, device=DEV)
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(4)
+    pipe.init_cache_fill(gen)
+    nw = 32
+    ring = w + s
+    gens = [synth.StreamGen(1920, 1080, synth.scene_of(cfg, si), synth.stream_seed(cfg, si)) for si in range(S)]
+    gop_h = np.zeros((S, nw + 1), np.uint32)
+    mring_h = np.zeros((S, ring, nw), np.uint32)
+    tring_h = np.zeros((S, ring), np.uint8)
+    rng = np.random.default_rng(0)
+    frames_h = synth.random_frames(S * w, 448, 448, rng)
+    frames_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in frames_h]
+    for k in range(4):
+        f0, n = pipe.new_frames(k)
+        mb = np.stack([np.stack([gens[si].next_frame() for _ in range(n)]) for si in range(S)])
+        types = np.stack([synth.frame_types(n, gop, f0) for _ in range(S)])
+        fptr = abi.ptr_array(frames_d[:S * n], DEV)
+        fidx = np.tile(np.arange(f0, f0 + n, dtype=np.int32), S)
+        old_h = [_host_cache(c).copy() for c in pipe.caches[pipe.cur]]
+        new_h = [_host_cache(c).copy() for c in pipe.caches[1 - pipe.cur]]   # content before the step
+        ref_h = [_host_cache(c) for c in pipe.refreshed]
+        pipe.step(k, d_mb(mb), fptr, torch.from_numpy(fidx).to(DEV), torch.from_numpy(types).to(DEV))
+        torch.cuda.synchronize()
+        # oracle, same sequence
+        off = f0 % ring
+        tring_h[:, off:off + n] = types
+        so = ref.score_patches(g, mb, np.ascontiguousarray(tring_h[:, off:]), gop_h, want_score=False,
+                               frame_stride=ring - off)
+        mring_h[:, off:off + n] = so["keep_mask"][:, :n]
+        assert (u32(pipe.mask_ring) == mring_h).all()
+        assert (u32(pipe.gop_state) == gop_h).all()
+        co = ref.compact(g, mring_h[:, off:].copy(), fidx, frames_h[:S * n], pipe.capacity, S, n,
+                         mask_frame_stride=ring - off)
+        tot = int(co["frame_offsets"][-1])
+        assert (pipe.frame_offsets[:S * n + 1].cpu().numpy() == co["frame_offsets"]).all()
+        assert (pipe.src_index[:tot].cpu().numpy() == co["src_index"][:tot]).all()
+        assert (pipe.pos_ids[:tot].cpu().numpy() == co["pos_ids"][:tot]).all()
+        assert (pipe.packed[:tot].view(torch.int16).cpu().numpy().view(np.uint16) == co["packed"][:tot]).all()
+        new_d = pipe.caches[pipe.cur]      # after the swap, cur holds window k
+        prev = [_host_cache(c) for c in new_d]
+        win = dict(window=w, stride=s, step=k, ring_frames=ring)
+        ko = ref.kv_refresh(g, pipe.kv, win, mring_h, tring_h, old_h if k else None, new_h,
+                            ref_h if k >= 1 else None, pipe.token_cap)
+        gpu = dict(disposition=pipe.disposition.cpu().numpy(), p_old=pipe.p_old.cpu().numpy(),
+                   n_tokens=pipe.n_tokens.cpu().numpy(), counters=ko["counters"], status=ko["status"])
+        assert (gpu["n_tokens"] == ko["n_tokens"]).all()
+        for si in range(S):
+            nt = int(ko["n_tokens"][si, 0]) + 32
+            assert (gpu["disposition"][si, :nt] == ko["disposition"][si, :nt]).all()
+            assert (gpu["p_old"][si, :nt] == ko["p_old"][si, :nt]).all()
+            a, b = prev[si], new_h[si]
+            assert (a[:, 1, :nt] == b[:, 1, :nt]).all()
+            fa = (a[:, 0, :nt].astype(np.uint32) << 16).view(np.float32)
+            fb = (b[:, 0, :nt].astype(np.uint32) << 16).view(np.float32)
+            assert np.abs(fa - fb).max() <= 1e-2
+    assert int(pipe.status.item()) == 0
