@@ -34,7 +34,7 @@ import synth  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--streams", type=int, default=None, help="streams per GPU (default: the config's)")
@@ -98,7 +98,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
         except Exception:  # noqa: BLE001
             self.proc = None
@@ -257,6 +257,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2604_06036_b200 import _abi as abi
+    from paper_2604_06036_b200 import shard
     from paper_2604_06036_b200.pipeline import Pipeline
 
     dev = torch.device("cuda", local_rank)
@@ -265,7 +266,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     sw, sh = cfg["src"]
     g = synth.make_grid(sw, sh)
     S, w, s, gop = cfg["streams"], cfg["window"], cfg["stride"], cfg["gop"]
-    global_ids = [rank + world * i for i in range(S)]
+    global_ids = shard.stream_ids(rank, world, S)
     kvb = cfg["kv"]
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev)
     gen = torch.Generator(device=dev)
@@ -401,11 +402,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         e2e = dict(ms=e2e_ms, steps=nsteps, h2d=h2d, d2h=d2h)
 
     # ---- reduce over ranks --------------------------------------------------------------------------------
-    tens = torch.tensor([ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device=dev)
-    cnt_all = dcnt.clone()
-    if world > 1:
-        dist.all_reduce(tens, op=dist.ReduceOp.MAX)
-        dist.all_reduce(cnt_all, op=dist.ReduceOp.SUM)
+    tens = shard.reduce_max(torch.tensor([ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device=dev))
+    cnt_all = shard.reduce_counters(dcnt)
     ms_max, e2e_ms_max = float(tens[0]), float(tens[1])
     if rank != 0:
         return

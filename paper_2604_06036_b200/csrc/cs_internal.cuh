@@ -57,6 +57,27 @@ CS_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) 
       : "memory");
 }
 
+// 1-D bulk copy shared (this CTA) -> global, tracked by the issuing thread's bulk async-groups.
+CS_DEV void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+CS_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N committed bulk groups of this thread still READ their shared-memory source
+template <int N>
+CS_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// wait until at most N committed bulk groups of this thread are still in flight (writes performed)
+template <int N>
+CS_DEV void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+CS_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // ---------------------------------------------------------------------------------------------------------
 // vector memory helpers
 // ---------------------------------------------------------------------------------------------------------
@@ -87,6 +108,13 @@ CS_DEV uint32_t f32_to_bf16_rne(float f) {
   if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu) != 0) return (u >> 16) | 0x0040u;
   u += 0x7fffu + ((u >> 16) & 1u);
   return u >> 16;
+}
+
+// two fp32 -> packed bf16x2 (low half = lo), round to nearest even (cvt.rn.bf16x2.f32)
+CS_DEV uint32_t pack_bf16x2_rn(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 
 CS_DEV void atomic_or_status(int32_t* status, int bits) {

@@ -376,7 +376,7 @@ __device__ __forceinline__ void copy_run_u32(const unsigned char* __restrict__ s
 }
 
 template <typename T, int TH, int TD>
-__global__ void __launch_bounds__(kGatherThreads) kv_gather(const __grid_constant__ KvParams P) {
+__global__ void __launch_bounds__(kGatherThreads) kv_gather_ldg(const __grid_constant__ KvParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   long long* s_pref = reinterpret_cast<long long*>(smem);                         // [n_streams + 1]
   KvSeg* s_seg = reinterpret_cast<KvSeg*>(smem + 8 * ((P.n_streams + 2) & ~1));  // [max_seg]
@@ -480,13 +480,275 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather(const __grid_constan
   }
 }
 
+
+// ------------------------------------------------------------------------------------------------------------
+// TMA bulk-copy pipelines (production path), one per WARP.  Every contiguous row run is cut into <= 8 KB chunks
+// that stream global -> shared (cp.async.bulk, mbarrier complete_tx) -> global (cp.async.bulk bulk_group store)
+// through the warp's NST-deep ring; REUSE K chunks are rotated in shared memory in between (Eq. 5) by the warp's
+// 32 lanes.  Lane 0 drives the ring (chunk generation, load/store issue).  Eight independent rings per CTA keep
+// the issue overhead off the critical path and ~8 x NST x 8 KB in flight per SM without register staging.
+// ------------------------------------------------------------------------------------------------------------
+constexpr int kTmaChunk = 8192;
+constexpr int kWarpsPerGather = kGatherThreads / 32;
+constexpr int kMaxStages = 6;
+
+struct ChunkDesc {
+  unsigned char* dst;
+  uint32_t bytes;  // 0 = end of the sequence
+  int rotate;      // 1: K rows of a REUSE run (rotate by R(dp))
+  int rows;
+  int pad;
+};
+
+struct ChunkGen {  // generator state, owned by lane 0 of a warp
+  long long it, it1;
+  int sidx, seg, x, active;
+  int nseg, a, b, l, kv;
+  const KvSeg* segs;
+  unsigned char* nc;
+  const unsigned char* oc;
+  const unsigned char* rf;
+  const void* tab;
+};
+
+__device__ __forceinline__ const int* ws_prefix(const KvParams& P) {
+  return reinterpret_cast<const int*>(P.ws + 16 + (long long)P.n_streams * P.ws_stride);
+}
+
+__device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, ChunkGen& g, int cr,
+                                         long long row_bytes, const unsigned char*& src, ChunkDesc& d,
+                                         const void*& tab) {
+  const int ipb = P.L * 2;
+  while (g.it < g.it1) {
+    if (!g.active) {
+      while (__ldg(pref + g.sidx + 1) <= g.it) ++g.sidx;
+      const long long local = g.it - __ldg(pref + g.sidx);
+      const int blk = static_cast<int>(local / ipb);
+      const int lk = static_cast<int>(local - (long long)blk * ipb);
+      g.l = lk >> 1;
+      g.kv = lk & 1;
+      g.a = blk * kRowBlock;
+      g.b = g.a + kRowBlock;
+      const unsigned char* ws = stream_ws(P, g.sidx);
+      g.nseg = reinterpret_cast<const KvHdr*>(ws)->n_seg;
+      g.segs = reinterpret_cast<const KvSeg*>(ws + sizeof(KvHdr));
+      g.tab = ws + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg;
+      g.nc = static_cast<unsigned char*>(P.new_cache[g.sidx]);
+      g.oc = P.k >= 1 ? static_cast<const unsigned char*>(P.old_cache[g.sidx]) : nullptr;
+      g.rf = P.has_refreshed ? static_cast<const unsigned char*>(P.refreshed[g.sidx]) : nullptr;
+      g.seg = 0;
+      g.x = g.a;
+      g.active = 1;
+    }
+    while (g.seg < g.nseg) {
+      const KvSeg sg = g.segs[g.seg];
+      if (sg.p_new >= g.b) {
+        g.seg = g.nseg;
+        break;
+      }
+      const int x0 = max(g.x, sg.p_new), x1 = min(g.b, sg.p_new + sg.len);
+      if (x0 >= x1) {
+        ++g.seg;
+        continue;
+      }
+      const int n = min(cr, x1 - x0);
+      const long long plane = static_cast<long long>(g.l * 2 + g.kv);
+      const long long srow = sg.src + (x0 - sg.p_new);
+      d.dst = g.nc + (plane * P.cap + x0) * row_bytes;
+      d.bytes = static_cast<uint32_t>(n * row_bytes);
+      d.rows = n;
+      if (sg.kind == SEG_REUSE) {
+        src = g.oc + (plane * P.cap + srow) * row_bytes;
+        d.rotate = (g.kv == 0);
+      } else {
+        src = g.rf + (plane * P.rcap + srow) * row_bytes;
+        d.rotate = 0;
+      }
+      tab = g.tab;
+      g.x = x0 + n;
+      if (g.x >= x1) ++g.seg;
+      return true;
+    }
+    ++g.it;
+    g.active = 0;
+  }
+  return false;
+}
+
+// 1 CTA: item prefix over streams into the workspace (item = stream x 128-row block x layer x K|V)
+__global__ void __launch_bounds__(1024) kv_prefix(const __grid_constant__ KvParams P) {
+  __shared__ int s_wsum[32];
+  __shared__ int s_carry;
+  int* pref = const_cast<int*>(ws_prefix(P));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ipb = P.L * 2;
+  if (tid == 0) {
+    s_carry = 0;
+    pref[0] = 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < P.n_streams; base += blockDim.x) {
+    const int si = base + tid;
+    int v = 0;
+    if (si < P.n_streams) {
+      const KvHdr* h = reinterpret_cast<const KvHdr*>(stream_ws(P, si));
+      const int rows = h->n_seg > 0 ? h->n_rows : 0;
+      v = (rows + kRowBlock - 1) / kRowBlock * ipb;
+    }
+    int inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += u;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    int woff = s_carry;
+    for (int q = 0; q < warp; ++q) woff += s_wsum[q];
+    if (si < P.n_streams) pref[si + 1] = woff + inc;
+    __syncthreads();
+    if (tid == blockDim.x - 1) s_carry = woff + inc;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void rot8_bf16_pack(uint4& a, uint4& b, const float* c, const float* s) {
+  uint32_t* pa = reinterpret_cast<uint32_t*>(&a);
+  uint32_t* pb = reinterpret_cast<uint32_t*>(&b);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float x1l = cs::bf16_lo(pa[q]), x1h = cs::bf16_hi(pa[q]);
+    const float x2l = cs::bf16_lo(pb[q]), x2h = cs::bf16_hi(pb[q]);
+    const float cl = c[2 * q], ch = c[2 * q + 1], sl = s[2 * q], sh = s[2 * q + 1];
+    const float o1l = __fmaf_rn(x1l, cl, -__fmul_rn(x2l, sl));
+    const float o2l = __fmaf_rn(x2l, cl, __fmul_rn(x1l, sl));
+    const float o1h = __fmaf_rn(x1h, ch, -__fmul_rn(x2h, sh));
+    const float o2h = __fmaf_rn(x2h, ch, __fmul_rn(x1h, sh));
+    pa[q] = cs::pack_bf16x2_rn(o1l, o1h);  // cvt.rn.bf16x2.f32: round to nearest even
+    pb[q] = cs::pack_bf16x2_rn(o2l, o2h);
+  }
+}
+
+// rotate the K rows of one chunk in shared memory; executed by the 32 lanes of one warp
+template <typename T, int TH, int TD>
+__device__ __forceinline__ void rotate_smem_warp(unsigned char* buf, const float2* tab, int rows, int rH, int rD,
+                                                 int lane) {
+  constexpr int VE = Vec<T>::N;
+  const int H = TH > 0 ? TH : rH;
+  const int D = TD > 0 ? TD : rD;
+  const int half = D / 2;
+  const int vph = half / VE;
+  const int upr = H * vph;
+  const int rowb = H * D * static_cast<int>(sizeof(T));
+  const int total = rows * upr;
+  for (int e = lane; e < total; e += 32) {
+    const int row = e / upr, un = e - row * upr;
+    const int h = un / vph, j = un - h * vph;
+    unsigned char* p1 = buf + row * rowb + (h * D + j * VE) * static_cast<int>(sizeof(T));
+    unsigned char* p2 = p1 + half * static_cast<int>(sizeof(T));
+    uint4 a = *reinterpret_cast<const uint4*>(p1);
+    uint4 b = *reinterpret_cast<const uint4*>(p2);
+    float c[VE], s[VE];
+#pragma unroll
+    for (int v = 0; v < VE; v += 2) {
+      const float4 t = *reinterpret_cast<const float4*>(tab + j * VE + v);
+      c[v] = t.x;
+      s[v] = t.y;
+      c[v + 1] = t.z;
+      s[v + 1] = t.w;
+    }
+    if constexpr (sizeof(T) == 2) rot8_bf16_pack(a, b, c, s);
+    else rot4_f32(a, b, c, s);
+    *reinterpret_cast<uint4*>(p1) = a;
+    *reinterpret_cast<uint4*>(p2) = b;
+  }
+}
+
+template <typename T, int TH, int TD>
+__global__ void __launch_bounds__(kGatherThreads, 1) kv_gather_tma(const __grid_constant__ KvParams P, int nst,
+                                                                   unsigned stage_bytes, unsigned tab_bytes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ ChunkDesc s_desc[kWarpsPerGather][kMaxStages];
+  __shared__ __align__(8) uint64_t s_full[kWarpsPerGather][kMaxStages];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* stages = smem + (size_t)wib * nst * (stage_bytes + tab_bytes);  // this warp's ring
+  unsigned char* tabs = stages + (size_t)nst * stage_bytes;
+  uint64_t* full = s_full[wib];
+  ChunkDesc* desc = s_desc[wib];
+  const long long row_bytes = (long long)P.H * P.D * sizeof(T);
+  const int cr = static_cast<int>(kTmaChunk / row_bytes);
+  const int* pref = ws_prefix(P);
+
+  const long long V = __ldg(pref + P.n_streams);
+  const long long nwarps = static_cast<long long>(gridDim.x) * kWarpsPerGather;
+  const long long gw = static_cast<long long>(blockIdx.x) * kWarpsPerGather + wib;
+  ChunkGen gen{};
+  gen.it = V * gw / nwarps;
+  gen.it1 = V * (gw + 1) / nwarps;
+  if (gen.it >= gen.it1) return;  // warp-uniform
+  if (lane == 0) {
+    // first stream of this warp's range: binary search over the prefix
+    int lo = 0, hi = P.n_streams;  // pref[lo] <= it < pref[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(pref + mid) <= gen.it) lo = mid; else hi = mid;
+    }
+    gen.sidx = lo;
+    for (int s = 0; s < nst; ++s) cs::mbar_init(&full[s], 1);
+    cs::fence_mbar_init();
+  }
+  __syncwarp();
+
+  bool more = true;
+  auto issue = [&](int st) {
+    const unsigned char* src = nullptr;
+    const void* tab = nullptr;
+    ChunkDesc d;
+    if (!gen_next(P, pref, gen, cr, row_bytes, src, d, tab)) {
+      desc[st].bytes = 0;
+      cs::mbar_arrive(&full[st]);
+      more = false;
+      return;
+    }
+    desc[st] = d;
+    cs::mbar_arrive_expect_tx(&full[st], d.bytes + (d.rotate ? tab_bytes : 0u));
+    cs::bulk_g2s(stages + (size_t)st * stage_bytes, src, d.bytes, &full[st]);
+    if (d.rotate) cs::bulk_g2s(tabs + (size_t)st * tab_bytes, tab, tab_bytes, &full[st]);
+  };
+  if (lane == 0)
+    for (int st = 0; st < nst && more; ++st) issue(st);
+
+  for (int q = 0;; ++q) {
+    const int st = q % nst;
+    cs::mbar_wait(&full[st], (q / nst) & 1);
+    const ChunkDesc d = desc[st];
+    if (d.bytes == 0) break;
+    unsigned char* buf = stages + (size_t)st * stage_bytes;
+    if (d.rotate) {
+      rotate_smem_warp<T, TH, TD>(buf, reinterpret_cast<const float2*>(tabs + (size_t)st * tab_bytes), d.rows, P.H,
+                                  P.D, lane);
+      cs::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+    }
+    __syncwarp();
+    if (lane == 0) {
+      cs::bulk_s2g(d.dst, buf, d.bytes);
+      cs::bulk_commit();
+      if (q >= 1 && more) {
+        cs::bulk_wait_read<1>();  // the store of chunk q-1 has read its stage
+        issue((q - 1) % nst);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) cs::bulk_wait_all<0>();
+}
 }  // namespace
 
 size_t cs_kv_workspace_bytes(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams) {
   const size_t max_seg = static_cast<size_t>(win->window) + 1;
   size_t stride = sizeof(KvHdr) + sizeof(KvSeg) * max_seg + 8 * static_cast<size_t>(kv->head_dim / 2);
   stride = (stride + 15) & ~static_cast<size_t>(15);
-  return 16 + stride * static_cast<size_t>(n_streams);
+  return 16 + stride * static_cast<size_t>(n_streams) + 4 * (static_cast<size_t>(n_streams) + 1);
 }
 
 int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
@@ -547,19 +809,42 @@ int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window
   kv_plan<<<n_streams, kPlanThreads, plan_smem, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
 
-  const size_t gsmem = 8 * static_cast<size_t>((n_streams + 2) & ~1) + sizeof(KvSeg) * max_seg +
-                       8 * static_cast<size_t>(kv->head_dim / 2);
-  const int grid = cs_num_sms() * 4;
-  const void* fn;
+  const long long row_bytes = static_cast<long long>(P.H) * P.D * P.esz;
+  const bool tma_ok = P.vec_rot && P.vec_copy && row_bytes <= kTmaChunk && (P.D % 4) == 0;
   const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
-  if (qwen) fn = reinterpret_cast<const void*>(kv_gather<uint16_t, 4, 128>);
-  else if (kv->dtype == CS_BF16) fn = reinterpret_cast<const void*>(kv_gather<uint16_t, 0, 0>);
-  else fn = reinterpret_cast<const void*>(kv_gather<float, 0, 0>);
-  const int slot = qwen ? 4 : (kv->dtype == CS_BF16 ? 5 : 6);
-  if (cs_set_smem_attr(fn, slot, 160 * 1024)) return CS_ERR_CUDA;
-  if (qwen) kv_gather<uint16_t, 4, 128><<<grid, kGatherThreads, gsmem, stream>>>(P);
-  else if (kv->dtype == CS_BF16) kv_gather<uint16_t, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
-  else kv_gather<float, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  const int sms = cs_num_sms();
+  kv_prefix<<<1, 1024, 0, stream>>>(P);
+  if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+  if (tma_ok) {
+    // one CTA per SM, 8 warps, each warp an independent ring of nst x 8 KB stages (+ cos/sin table slots)
+    const unsigned stage_bytes = kTmaChunk;
+    const unsigned tab_bytes = static_cast<unsigned>(((8 * (P.D / 2)) + 127) & ~127);
+    int nst = static_cast<int>((200u * 1024u) / (kWarpsPerGather * (stage_bytes + tab_bytes)));
+    if (nst > kMaxStages) nst = kMaxStages;
+    if (nst < 3) return CS_ERR_UNSUPPORTED;
+    const size_t smem = static_cast<size_t>(kWarpsPerGather) * nst * (stage_bytes + tab_bytes);
+    const int grid = sms;
+    const void* fn = qwen ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 4, 128>)
+                          : (kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 0, 0>)
+                                                  : reinterpret_cast<const void*>(kv_gather_tma<float, 0, 0>));
+    const int slot = qwen ? 7 : (kv->dtype == CS_BF16 ? 8 : 9);
+    if (cs_set_smem_attr(fn, slot, 220 * 1024)) return CS_ERR_CUDA;
+    if (qwen)
+      kv_gather_tma<uint16_t, 4, 128><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+    else if (kv->dtype == CS_BF16)
+      kv_gather_tma<uint16_t, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+    else
+      kv_gather_tma<float, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+  } else {
+    const size_t gsmem = 8 * static_cast<size_t>((n_streams + 2) & ~1) + sizeof(KvSeg) * max_seg +
+                         8 * static_cast<size_t>(kv->head_dim / 2);
+    const int grid = sms * 4;
+    const void* fn = kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_ldg<uint16_t, 0, 0>)
+                                          : reinterpret_cast<const void*>(kv_gather_ldg<float, 0, 0>);
+    if (cs_set_smem_attr(fn, kv->dtype == CS_BF16 ? 5 : 6, 160 * 1024)) return CS_ERR_CUDA;
+    if (kv->dtype == CS_BF16) kv_gather_ldg<uint16_t, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+    else kv_gather_ldg<float, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  }
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
 }

@@ -1,0 +1,7 @@
+# quick GPU check: parity tests + smoke + bench (1 GPU)
+set -x
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -2 gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -15 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
