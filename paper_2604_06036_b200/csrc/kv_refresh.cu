@@ -66,7 +66,7 @@ __device__ __forceinline__ unsigned char* stream_ws(const KvParams& P, int s) { 
 
 // ------------------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ KvParams P) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_n[cs::kMaxWindowPlusStride];       // tokens per frame of [lo, hi)
   __shared__ uint8_t s_t[cs::kMaxWindowPlusStride];   // frame types
   __shared__ KvSeg s_seg[kMaxSeg];                    // index segments (unclamped), one per frame + prompt
@@ -377,7 +377,7 @@ __device__ __forceinline__ void copy_run_u32(const unsigned char* __restrict__ s
 
 template <typename T, int TH, int TD>
 __global__ void __launch_bounds__(kGatherThreads) kv_gather_ldg(const __grid_constant__ KvParams P) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   long long* s_pref = reinterpret_cast<long long*>(smem);                         // [n_streams + 1]
   KvSeg* s_seg = reinterpret_cast<KvSeg*>(smem + 8 * ((P.n_streams + 2) & ~1));  // [max_seg]
   float* s_c = reinterpret_cast<float*>(s_seg + P.max_seg);                       // [D/2]
@@ -819,7 +819,7 @@ int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window
     // one CTA per SM, 8 warps, each warp an independent ring of nst x 8 KB stages (+ cos/sin table slots)
     const unsigned stage_bytes = kTmaChunk;
     const unsigned tab_bytes = static_cast<unsigned>(((8 * (P.D / 2)) + 127) & ~127);
-    int nst = static_cast<int>((200u * 1024u) / (kWarpsPerGather * (stage_bytes + tab_bytes)));
+    int nst = static_cast<int>((216u * 1024u) / (kWarpsPerGather * (stage_bytes + tab_bytes)));
     if (nst > kMaxStages) nst = kMaxStages;
     if (nst < 3) return CS_ERR_UNSUPPORTED;
     const size_t smem = static_cast<size_t>(kWarpsPerGather) * nst * (stage_bytes + tab_bytes);
