@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--frame-layout", default="grouped", choices=["grouped", "planar"],
+                    help="layout of the preprocessed model-input frames handed to compact (DESIGN.md §6)")
     return ap.parse_args()
 
 
@@ -268,7 +270,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     S, w, s, gop = cfg["streams"], cfg["window"], cfg["stride"], cfg["gop"]
     global_ids = shard.stream_ids(rank, world, S)
     kvb = cfg["kv"]
-    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev)
+    layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
+    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     pipe.init_cache_fill(gen)
@@ -318,14 +321,15 @@ def run_ours(args, cfg, rank, world, local_rank):
             e[1].record(stream)
             abi.codecsight_compact(g, S, n, pipe.mask_ring[:, off:], pipe.ring, fidx_dev[k], ptrs, pipe.capacity,
                                    pipe.packed, pipe.pos_ids, pipe.src_index, pipe.frame_offsets[:S * n + 1],
-                                   pipe.counters, pipe.status)
+                                   pipe.counters, pipe.status, frame_layout=layout)
             e[2].record(stream)
-            win = dict(window=w, stride=s, step=k, ring_frames=pipe.ring)
-            old, new = pipe.cache_ptrs[pipe.cur], pipe.cache_ptrs[1 - pipe.cur]
-            abi.codecsight_kv_refresh(g, pipe.kv, win, S, pipe.mask_ring, pipe.type_ring, old, new,
-                                      pipe.refreshed_ptrs if k >= 1 else None, pipe.token_cap, pipe.disposition,
-                                      pipe.p_old, pipe.n_tokens, pipe.workspace, pipe.counters, pipe.status)
-            pipe.cur = 1 - pipe.cur
+            if pipe.kv is not None:
+                win = dict(window=w, stride=s, step=k, ring_frames=pipe.ring)
+                old, new = pipe.cache_ptrs[pipe.cur], pipe.cache_ptrs[1 - pipe.cur]
+                abi.codecsight_kv_refresh(g, pipe.kv, win, S, pipe.mask_ring, pipe.type_ring, old, new,
+                                          pipe.refreshed_ptrs if k >= 1 else None, pipe.token_cap, pipe.disposition,
+                                          pipe.p_old, pipe.n_tokens, pipe.workspace, pipe.counters, pipe.status)
+                pipe.cur = 1 - pipe.cur
             e[3].record(stream)
             ev["score"].append((e[0], e[1]))
             ev["compact"].append((e[1], e[2]))
@@ -362,6 +366,25 @@ def run_ours(args, cfg, rank, world, local_rank):
     per = {kname: [a.elapsed_time(b) for a, b in lst] for kname, lst in ev.items()}
     status = int(pipe.status.item())
 
+    # ---- compact alone on the last step's masks, both frame layouts (context for the layout choice) ---------
+    layouts = {}
+    k_last = args.warmup + args.steps - 1
+    off_l = pipe.ring_slot(k_last)
+    for lname, lid in (("grouped", abi.CS_LAYOUT_GROUPED), ("planar", abi.CS_LAYOUT_PLANAR)):
+        c0 = pipe.counters.clone()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        ea.record(stream)
+        for _ in range(reps):
+            abi.codecsight_compact(g, S, s, pipe.mask_ring[:, off_l:], pipe.ring, fidx_dev[k_last], ptr_s,
+                                   pipe.capacity, pipe.packed, pipe.pos_ids, pipe.src_index,
+                                   pipe.frame_offsets[:S * s + 1], pipe.counters, pipe.status, frame_layout=lid)
+        eb.record(stream)
+        torch.cuda.synchronize()
+        t_ms = ea.elapsed_time(eb) / reps
+        byt = float((pipe.counters - c0)[abi.CNT_BYTES_COMPACT].item()) / reps
+        layouts[lname] = {"ms": t_ms, "gbs": byt / (t_ms / 1e3) / 1e9}
+
     # ---- end-to-end through the public API with host buffers ----------------------------------------------
     e2e = None
     if not args.no_e2e:
@@ -390,7 +413,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             fidx_d = fi.to(dev, non_blocking=True)
             pipe.step(k, stage_mb, ptr_s, fidx_d, types_d)
             # D2H: the step's result (token counts per stream, kept counts, packed rows)
-            res_host[:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
+            if pipe.kv is not None:
+                res_host[:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
             res_host[S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
             res_host[-1:].copy_(pipe.frame_offsets[S * n:S * n + 1], non_blocking=True)
             stream.synchronize()                                          # the host consumes the result
@@ -415,9 +439,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     kv_ms = float(np.mean(per["kv"]))
     kv_bytes_launch = float(dcnt[abi.CNT_BYTES_KV].item()) / K
     peak, peak_kind = measured_peak_hbm()
-    achieved = kv_bytes_launch / (kv_ms / 1e3) / 1e9
+    achieved = kv_bytes_launch / (kv_ms / 1e3) / 1e9 if kvb else 0.0
     cmp_ms = float(np.mean(per["compact"]))
     cmp_bytes = float(dcnt[abi.CNT_BYTES_COMPACT].item()) / K
+    cmp_gbs = cmp_bytes / (cmp_ms / 1e3) / 1e9
     sc_ms = float(np.mean(per["score"]))
     sc_bytes = float(dcnt[abi.CNT_BYTES_SCORE].item()) / K
     kept_frac = float(dcnt[abi.CNT_KEPT].item()) / max(1.0, float(dcnt[abi.CNT_PATCHES].item()))
@@ -429,23 +454,33 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg["name"], "streams_per_gpu": S, "streams_total": S * world, "src": list(cfg["src"]),
                    "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": 0.25, "alpha": 0.0,
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
+                   "frame_layout": args.frame_layout,
                    "parallelism": f"stream-shard x{world}",
-                   "l2": "inputs larger than L2 (KV caches 121 GB/GPU, frames 1.2 GB, metadata 67 MB per step)"},
+                   "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
+                         "see per-step bytes)"},
         "streams_per_sec": stream_steps,
         "kv_refresh_gbs": achieved,
         "per_kernel_ms": {"score_patches": sc_ms, "compact": cmp_ms, "kv_refresh": kv_ms},
-        "per_kernel_gbs": {"score_patches": sc_bytes / (sc_ms / 1e3) / 1e9, "compact": cmp_bytes / (cmp_ms / 1e3) / 1e9,
+        "per_kernel_gbs": {"score_patches": sc_bytes / (sc_ms / 1e3) / 1e9, "compact": cmp_gbs,
                            "kv_refresh": achieved},
+        "frame_layout": args.frame_layout,
+        "compact_by_layout": layouts,
         "kept_fraction": kept_frac,
         "tokens_per_step": {"reuse": int(c[abi.CNT_TOK_REUSE]) // K, "anchor": int(c[abi.CNT_TOK_ANCHOR]) // K,
                             "new": int(c[abi.CNT_TOK_NEW]) // K},
         "near_tau_patches": int(c[abi.CNT_NEAR_TAU]),
         "status": status,
-        "roofline": {"bound": "hbm", "kernel": "codecsight_kv_refresh (kv_plan + kv_gather)", "achieved": achieved,
-                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic("kv_gather"),
-                     "algorithmic_bytes_per_launch": kv_bytes_launch},
-        "gpu_launches": K * 5,
+        "roofline": ({"bound": "hbm", "kernel": "codecsight_kv_refresh (kv_plan + kv_prefix + kv_gather_tma)",
+                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                      "frac": achieved / peak, "traffic": ncu_traffic("kv_gather"),
+                      "algorithmic_bytes_per_launch": kv_bytes_launch} if kvb else
+                     {"bound": "hbm", "kernel": "codecsight_compact (compact_scan + compact_gather)",
+                      "achieved": cmp_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                      "frac": cmp_gbs / peak, "traffic": ncu_traffic("compact_gather"),
+                      "algorithmic_bytes_per_launch": cmp_bytes}),
+        "secondary_roofline": {"kernel": "codecsight_compact", "achieved": cmp_gbs, "peak": peak,
+                               "frac": cmp_gbs / peak, "unit": "GB/s", "algorithmic_bytes_per_launch": cmp_bytes},
+        "gpu_launches": K * pipe.kernel_launches_per_step(1),
         "clocks": clk,
     }
     if e2e:

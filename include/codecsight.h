@@ -65,6 +65,7 @@ enum { CS_FRAME_I = 0, CS_FRAME_P = 1 };
 enum { CS_MB_INTER = 0, CS_MB_SKIP = 1, CS_MB_INTRA = 2 };
 enum { CS_DISP_NEW = 0, CS_DISP_ANCHOR = 1, CS_DISP_REUSE = 2 };
 enum { CS_BF16 = 0, CS_FP32 = 1 };
+enum { CS_LAYOUT_PLANAR = 0, CS_LAYOUT_GROUPED = 1 }; /* model-input frame layouts accepted by codecsight_compact */
 
 /* ---- counters (u64 each) -------------------------------------------------------------------------------- */
 enum {
@@ -165,8 +166,14 @@ int codecsight_score_patches(const cs_grid* g, int32_t n_streams, int32_t n_fram
  *   keep_mask         device [n_streams][mask_frame_stride][grid_words] u32, frame j of stream sigma at
  *                            sigma*mask_frame_stride + j (mask_frame_stride >= n_frames)
  *   frame_index       device [n_slots] i32 stream-local absolute frame index (pos id t)
- *   frames            device [n_slots] array of device pointers, each a [3][grid_h*patch][grid_w*patch] bf16
- *                            frame (the preprocessed model input); 16-B alignment enables wide loads
+ *   frames            device [n_slots] array of device pointers to bf16 model-input frames (the preprocessed
+ *                            frames) in `frame_layout`:
+ *                            CS_LAYOUT_PLANAR  [3][grid_h*patch][grid_w*patch] (the usual CHW tensor)
+ *                            CS_LAYOUT_GROUPED [n_groups][group*group][3][patch][patch]: groups row-major, the
+ *                              patches of a group (dy, dx) row-major -- i.e. already in packed order, so a kept
+ *                              group is one contiguous block (what a fused resize/normalise stage can emit, NEXT-2)
+ *                            8-B (planar) / 16-B (grouped) alignment enables wide loads
+ *   frame_layout      CS_LAYOUT_PLANAR | CS_LAYOUT_GROUPED (results are identical for both)
  *   capacity          rows available in packed / pos_ids / src_index
  *   packed            device [capacity][3*patch*patch] bf16 out
  *   pos_ids           device [capacity][3] i32 out
@@ -177,7 +184,7 @@ int codecsight_score_patches(const cs_grid* g, int32_t n_streams, int32_t n_fram
  * --------------------------------------------------------------------------------------------------------- */
 int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
                        int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
-                       int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                       int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
                        int32_t* frame_offsets, unsigned long long* counters, int32_t* status,
                        cudaStream_t stream);
 

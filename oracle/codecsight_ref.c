@@ -205,11 +205,12 @@ int codecsight_ref_score_patches(const ref_grid* g, int32_t n_streams, int32_t n
 /* ---------------------------------------------------------------------------------------------------- */
 int codecsight_ref_compact(const ref_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
                            int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
-                           int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                           int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
                            int32_t* frame_offsets, unsigned long long* counters, int32_t* status) {
   int rc = ref_grid_ok(g);
   if (rc) return rc;
   if (n_streams < 0 || n_frames < 1 || mask_frame_stride < n_frames || capacity < 0) return -1;
+  if (frame_layout != REF_LAYOUT_PLANAR && frame_layout != REF_LAYOUT_GROUPED) return -1;
   const int64_t np = (int64_t)g->grid_w * g->grid_h, nw = ref_words(g), G = g->group, p = g->patch;
   const int64_t n_slots = (int64_t)n_streams * n_frames;
   if (n_slots * np >= 2147483648LL) return -3;
@@ -239,8 +240,15 @@ int codecsight_ref_compact(const ref_grid* g, int32_t n_streams, int32_t n_frame
               if (n >= capacity) { *status |= REF_ST_CAPACITY; continue; }
               for (int64_t c = 0; c < 3; ++c)
                 for (int64_t y = 0; y < p; ++y)
-                  for (int64_t x = 0; x < p; ++x)
-                    out[n * row + c * p * p + y * p + x] = fr[c * fh * fw + (h * p + y) * fw + (w * p + x)];
+                  for (int64_t x = 0; x < p; ++x) {
+                    /* pixel (c, p*h + y, p*w + x) of the frame, in the frame's layout */
+                    int64_t src;
+                    if (frame_layout == REF_LAYOUT_PLANAR)
+                      src = c * fh * fw + (h * p + y) * fw + (w * p + x);
+                    else /* grouped: [group (gr,gc)][patch (dy,dx)][c][y][x] */
+                      src = (((gr * (g->grid_w / G) + gc) * G * G + dy * G + dx) * 3 + c) * p * p + y * p + x;
+                    out[n * row + c * p * p + y * p + x] = fr[src];
+                  }
               pos_ids[3 * n + 0] = frame_index[slot];
               pos_ids[3 * n + 1] = (int32_t)h;
               pos_ids[3 * n + 2] = (int32_t)w;

@@ -20,6 +20,8 @@
 #define REF_DISP_NEW 0
 #define REF_DISP_ANCHOR 1
 #define REF_DISP_REUSE 2
+#define REF_LAYOUT_PLANAR 0
+#define REF_LAYOUT_GROUPED 1
 #define REF_BF16 0
 #define REF_FP32 1
 
@@ -82,7 +84,7 @@ int codecsight_ref_score_patches(const ref_grid* g, int32_t n_streams, int32_t n
 
 int codecsight_ref_compact(const ref_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
                            int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
-                           int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                           int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
                            int32_t* frame_offsets, unsigned long long* counters, int32_t* status);
 
 int codecsight_ref_kv_refresh(const ref_grid* g, const ref_kv* kv, const ref_window* win, int32_t n_streams,

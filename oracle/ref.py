@@ -70,7 +70,7 @@ def lib():
                                                    P, P, P, P, P]
         L.codecsight_ref_compact.restype = C.c_int
         L.codecsight_ref_compact.argtypes = [C.POINTER(RefGrid), C.c_int32, C.c_int32, P, C.c_int64, P, P,
-                                             C.c_int64, P, P, P, P, P, P]
+                                             C.c_int32, C.c_int64, P, P, P, P, P, P]
         L.codecsight_ref_kv_refresh.restype = C.c_int
         L.codecsight_ref_kv_refresh.argtypes = [C.POINTER(RefGrid), C.POINTER(RefKv), C.POINTER(RefWindow),
                                                 C.c_int32, P, P, P, P, P, C.c_int64, P, P, P, P, P]
@@ -137,8 +137,9 @@ def score_patches(g: dict, mb: np.ndarray, frame_type: np.ndarray, gop_state: np
 
 def compact(g: dict, keep_mask: np.ndarray, frame_index: np.ndarray, frames: list, capacity: int,
             n_streams: int, n_frames: int, mask_frame_stride: int | None = None,
-            counters: np.ndarray | None = None):
-    """keep_mask [S][mask_frame_stride][words]; frames: list of n_slots uint16 arrays [3][H][W] (bf16 bits)."""
+            counters: np.ndarray | None = None, frame_layout: int = 0):
+    """keep_mask [S][mask_frame_stride][words]; frames: list of n_slots uint16 arrays (bf16 bits) in
+    ``frame_layout`` (0 planar [3][H][W], 1 grouped [groups][group^2][3][p][p])."""
     nw = grid_words(g)
     mfs = n_frames if mask_frame_stride is None else mask_frame_stride
     keep_mask = np.ascontiguousarray(keep_mask, dtype=np.uint32).reshape(n_streams, mfs, nw)
@@ -155,7 +156,8 @@ def compact(g: dict, keep_mask: np.ndarray, frame_index: np.ndarray, frames: lis
     counters = np.zeros(NCOUNTERS, np.uint64) if counters is None else counters
     status = np.zeros(1, np.int32)
     rc = lib().codecsight_ref_compact(C.byref(make_grid(g)), n_streams, n_frames, _p(keep_mask), mfs,
-                                      _p(frame_index), C.cast(ptrs, C.c_void_p), capacity, _p(packed), _p(pos),
+                                      _p(frame_index), C.cast(ptrs, C.c_void_p), frame_layout, capacity, _p(packed),
+                                      _p(pos),
                                       _p(src), _p(offs), _p(counters), _p(status))
     return dict(rc=rc, packed=packed, pos_ids=pos, src_index=src, frame_offsets=offs, counters=counters,
                 status=int(status[0]))

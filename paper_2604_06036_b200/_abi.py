@@ -24,6 +24,7 @@ CS_FRAME_I, CS_FRAME_P = 0, 1
 CS_MB_INTER, CS_MB_SKIP, CS_MB_INTRA = 0, 1, 2
 CS_DISP_NEW, CS_DISP_ANCHOR, CS_DISP_REUSE = 0, 1, 2
 CS_BF16, CS_FP32 = 0, 1
+CS_LAYOUT_PLANAR, CS_LAYOUT_GROUPED = 0, 1
 NCOUNTERS = 16
 (CNT_FRAMES, CNT_PFRAMES, CNT_PATCHES, CNT_KEPT, CNT_NEAR_TAU, CNT_TOK_REUSE, CNT_TOK_ANCHOR, CNT_TOK_NEW,
  CNT_BYTES_SCORE, CNT_BYTES_COMPACT, CNT_BYTES_KV, CNT_PACKED_ROWS, CNT_STREAM_STEPS) = range(13)
@@ -62,7 +63,7 @@ def lib():
         L.codecsight_score_patches.restype = C.c_int
         L.codecsight_score_patches.argtypes = [C.POINTER(CsGrid), I32, I32, P, P, P, I64, P, P, P, P, P, P]
         L.codecsight_compact.restype = C.c_int
-        L.codecsight_compact.argtypes = [C.POINTER(CsGrid), I32, I32, P, I64, P, P, I64, P, P, P, P, P, P, P]
+        L.codecsight_compact.argtypes = [C.POINTER(CsGrid), I32, I32, P, I64, P, P, I32, I64, P, P, P, P, P, P, P]
         L.codecsight_kv_refresh.restype = C.c_int
         L.codecsight_kv_refresh.argtypes = [C.POINTER(CsGrid), C.POINTER(CsKvDesc), C.POINTER(CsWindow), I32, P, P,
                                             P, P, P, I64, P, P, P, P, C.c_size_t, P, P, P]
@@ -136,9 +137,10 @@ def codecsight_score_patches(g: dict, n_streams: int, n_frames: int, mb, frame_t
 
 def codecsight_compact(g: dict, n_streams: int, n_frames: int, keep_mask, mask_frame_stride: int, frame_index,
                        frames_ptrs, capacity: int, packed, pos_ids, src_index, frame_offsets, counters, status,
-                       stream=None) -> None:
+                       stream=None, frame_layout: int = CS_LAYOUT_PLANAR) -> None:
     rc = lib().codecsight_compact(C.byref(make_grid(g)), n_streams, n_frames, _ptr(keep_mask), mask_frame_stride,
-                                  _ptr(frame_index), _ptr(frames_ptrs), capacity, _ptr(packed), _ptr(pos_ids),
+                                  _ptr(frame_index), _ptr(frames_ptrs), frame_layout, capacity, _ptr(packed),
+                                  _ptr(pos_ids),
                                   _ptr(src_index), _ptr(frame_offsets), _ptr(counters), _ptr(status),
                                   _stream(stream))
     _check(rc, "codecsight_compact")

@@ -98,13 +98,14 @@ int codecsight_score_patches(const cs_grid* g, int32_t n_streams, int32_t n_fram
 
 int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
                        int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
-                       int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                       int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
                        int32_t* frame_offsets, unsigned long long* counters, int32_t* status,
                        cudaStream_t stream) {
   int rc = grid_ok(g);
   if (rc) return rc;
   if (n_streams < 0 || n_frames < 1 || mask_frame_stride < n_frames || capacity < 0)
     return CS_ERR_INVALID_ARGUMENT;
+  if (frame_layout != CS_LAYOUT_PLANAR && frame_layout != CS_LAYOUT_GROUPED) return CS_ERR_INVALID_ARGUMENT;
   const long long n_slots = static_cast<long long>(n_streams) * n_frames;
   if (n_slots * g->grid_w * g->grid_h >= 2147483648LL) return CS_ERR_UNSUPPORTED;
   if (g->group * g->patch > 32) return CS_ERR_UNSUPPORTED;
@@ -112,7 +113,8 @@ int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, co
   if (n_slots > 0 && (!keep_mask || !frame_index || !frames)) return CS_ERR_INVALID_ARGUMENT;
   if (capacity > 0 && (!packed || !pos_ids || !src_index)) return CS_ERR_INVALID_ARGUMENT;
   if ((rc = device_ok())) return rc;
-  return cs_launch_compact(g, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, frames, capacity,
+  return cs_launch_compact(g, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, frames, frame_layout,
+                           capacity,
                            packed, pos_ids, src_index, frame_offsets, counters, status, stream);
 }
 

@@ -30,6 +30,7 @@ struct CompactParams {
   long long capacity;
   int FH, FW;  // model-input frame height / width in pixels
   int vec_out;
+  int layout;  // CS_LAYOUT_PLANAR | CS_LAYOUT_GROUPED
   const uint32_t* keep_mask;
   const int32_t* frame_index;
   const void* const* frames;
@@ -124,6 +125,47 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
   const long long FW = P.FW;
   const uint16_t* src0 = frame + (long long)(gr * gp) * FW + (long long)gc * gp;
   const long long plane = (long long)P.FH * FW;
+  if (P.layout == CS_LAYOUT_GROUPED) {
+    // the kept group is one contiguous block already in packed order: straight 16-B copy (no smem staging)
+    const int gs2 = G * G;
+    long long nvalid = P.capacity - n0;
+    nvalid = nvalid < 0 ? 0 : (nvalid > gs2 ? gs2 : nvalid);
+    const long long row_el = 3ll * pp;
+    const uint16_t* blk = frame + ((long long)gr * P.ngc + gc) * gs2 * row_el;
+    uint16_t* dst = P.packed + n0 * row_el;
+    if (vec_in && P.vec_out) {
+      const int n16 = static_cast<int>(nvalid * row_el * 2 / 16);
+      const uint4* s4 = reinterpret_cast<const uint4*>(blk);
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      constexpr int kU = 10;
+      for (int e0 = 0; e0 < n16; e0 += 32 * kU) {
+        uint4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int e = e0 + u * 32 + lane;
+          if (e < n16) v[u] = cs::ld_nc_v4(s4 + e);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int e = e0 + u * 32 + lane;
+          if (e < n16) d4[e] = v[u];
+        }
+      }
+    } else {
+      const int nel = static_cast<int>(nvalid * row_el);
+      for (int e = lane; e < nel; e += 32) dst[e] = blk[e];
+    }
+    if (lane < nvalid) {
+      const int dy = lane / G, dx = lane - dy * G;
+      const int h = gr * G + dy, w = gc * G + dx;
+      const long long n = n0 + lane;
+      P.pos_ids[3 * n + 0] = t_index;
+      P.pos_ids[3 * n + 1] = h;
+      P.pos_ids[3 * n + 2] = w;
+      P.src_index[n] = slot * P.np + h * P.grid_w + w;
+    }
+    return;
+  }
   if (vec_in) {
     // 8-byte loads: each group row segment is gp pixels = gp/4 pieces of 4 bf16.  Pairs of pixels never
     // straddle a patch boundary (p even), so the tile is written with 4-byte stores.
@@ -226,8 +268,10 @@ __global__ void __launch_bounds__(kGatherThreads) compact_gather(const __grid_co
     const uint16_t* frame = static_cast<const uint16_t*>(P.frames[slot]);
     const int t_index = __ldg(P.frame_index + slot);
     const int pe = TP > 0 ? TP : P.p;
-    const bool vec_in = ((reinterpret_cast<uintptr_t>(frame) & 7u) == 0) && ((P.FW & 3) == 0) &&
-                        (((G * pe) & 3) == 0) && ((pe & 1) == 0);
+    const bool vec_in = P.layout == CS_LAYOUT_GROUPED
+                            ? (((reinterpret_cast<uintptr_t>(frame) & 15u) == 0) && ((3 * G * G * pe * pe * 2) % 16 == 0))
+                            : (((reinterpret_cast<uintptr_t>(frame) & 7u) == 0) && ((P.FW & 3) == 0) &&
+                               (((G * pe) & 3) == 0) && ((pe & 1) == 0));
     __syncwarp();
     for (int base = 0; base < P.ngroups && q < q1; base += 32) {
       const int qq = base + lane;
@@ -261,7 +305,8 @@ __global__ void __launch_bounds__(kGatherThreads) compact_gather(const __grid_co
 
 int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
                       int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
-                      int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
+                      int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                      int32_t* frame_offsets,
                       unsigned long long* counters, int32_t* status, cudaStream_t stream) {
   CompactParams P{};
   P.grid_w = g->grid_w;
@@ -281,6 +326,7 @@ int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, con
   P.FW = g->grid_w * g->patch;
   const long long row_bytes = 3ll * g->patch * g->patch * 2ll;
   P.vec_out = ((reinterpret_cast<uintptr_t>(packed) & 15u) == 0 && (row_bytes % 16) == 0) ? 1 : 0;
+  P.layout = frame_layout;
   P.keep_mask = keep_mask;
   P.frame_index = frame_index;
   P.frames = frames;

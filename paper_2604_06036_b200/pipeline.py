@@ -25,8 +25,9 @@ from . import _abi as abi
 class Pipeline:
     def __init__(self, grid: dict, n_streams: int, window: int, stride: int, gop: int, kv: dict | None,
                  n_prompt: int = 0, device=None, want_score: bool = False, packed_capacity: int | None = None,
-                 with_refreshed: bool = True):
+                 with_refreshed: bool = True, frame_layout: int = abi.CS_LAYOUT_PLANAR):
         self.g = dict(grid)
+        self.frame_layout = frame_layout
         self.S, self.w, self.s, self.gop = n_streams, window, stride, gop
         self.ring = window + stride
         self.dev = torch.device(device if device is not None else "cuda")
@@ -108,7 +109,7 @@ class Pipeline:
         fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
         abi.codecsight_compact(g, self.S, n, self.mask_ring[:, off:], self.ring, fi, frame_ptrs, self.capacity,
                                self.packed, self.pos_ids, self.src_index, self.frame_offsets[: self.S * n + 1],
-                               self.counters, self.status, stream)
+                               self.counters, self.status, stream, frame_layout=self.frame_layout)
         if self.kv is not None and do_kv:
             win = dict(window=self.w, stride=self.s, step=k, ring_frames=self.ring)
             old, new = self.cache_ptrs[self.cur], self.cache_ptrs[1 - self.cur]
@@ -119,8 +120,8 @@ class Pipeline:
             self.cur = 1 - self.cur
 
     def kernel_launches_per_step(self, k: int) -> int:
-        """Kernels of this library launched by one step (score 1, compact 2, kv_refresh 2)."""
+        """Kernels of this library launched by one step (score 1, compact 2, kv_refresh 3)."""
         n = 1 + (2 if self.S > 0 else 1)
         if self.kv is not None:
-            n += 2
+            n += 3
         return n

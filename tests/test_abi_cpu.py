@@ -84,11 +84,12 @@ def test_compact_validation(abi):
     L = abi.lib()
     g = make_grid(448, 448)
 
-    def call(g, cap=16, n_streams=1, n_frames=1, mfs=1):
-        return L.codecsight_compact(C.byref(abi.make_grid(g)), n_streams, n_frames, FAKE, mfs, FAKE, FAKE, cap,
-                                    FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, None)
+    def call(g, cap=16, n_streams=1, n_frames=1, mfs=1, layout=0):
+        return L.codecsight_compact(C.byref(abi.make_grid(g)), n_streams, n_frames, FAKE, mfs, FAKE, FAKE, layout,
+                                    cap, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, None)
 
     assert call(g, cap=-1) == abi.CS_ERR_INVALID_ARGUMENT
+    assert call(g, layout=2) == abi.CS_ERR_INVALID_ARGUMENT
     assert call(g, mfs=0) == abi.CS_ERR_INVALID_ARGUMENT
     assert call(dict(g, patch=40)) == abi.CS_ERR_SHAPE
     assert call(dict(g, patch=20)) == abi.CS_ERR_UNSUPPORTED     # group * patch > 32

@@ -151,9 +151,18 @@ def test_score_full_size_batches(abi, ref, cfg_name):
 # ------------------------------------------------------------------------------------------------------------
 # compact
 # ------------------------------------------------------------------------------------------------------------
-def run_compact_both(abi, ref, g, keep_mask, frame_index, frames, capacity, S, n, mfs):
+def to_grouped(frame, g):
+    p, G = g["patch"], g["group"]
+    ngr, ngc = g["grid_h"] // G, g["grid_w"] // G
+    x = frame.reshape(3, ngr, G, p, ngc, G, p)
+    return np.ascontiguousarray(x.transpose(1, 4, 2, 5, 0, 3, 6)).reshape(-1)
+
+
+def run_compact_both(abi, ref, g, keep_mask, frame_index, frames, capacity, S, n, mfs, layout=0):
     nw = abi.grid_words(g)
     p = g["patch"]
+    if layout == 1:
+        frames = [to_grouped(f, g) for f in frames]
     km_d = torch.from_numpy(np.ascontiguousarray(keep_mask).view(np.int32)).to(DEV)
     fr_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in frames]
     fptr = abi.ptr_array(fr_d, DEV) if fr_d else torch.zeros(1, dtype=torch.int64, device=DEV)
@@ -165,8 +174,9 @@ def run_compact_both(abi, ref, g, keep_mask, frame_index, frames, capacity, S, n
     offs = torch.zeros(S * n + 1, dtype=torch.int32, device=DEV)
     cnt_d = torch.zeros(16, dtype=torch.int64, device=DEV)
     st_d = torch.zeros(1, dtype=torch.int32, device=DEV)
-    abi.codecsight_compact(g, S, n, km_d, mfs, fi_d, fptr, capacity, packed, pos, src, offs, cnt_d, st_d)
-    o = ref.compact(g, keep_mask, frame_index, frames, capacity, S, n, mask_frame_stride=mfs)
+    abi.codecsight_compact(g, S, n, km_d, mfs, fi_d, fptr, capacity, packed, pos, src, offs, cnt_d, st_d,
+                           frame_layout=layout)
+    o = ref.compact(g, keep_mask, frame_index, frames, capacity, S, n, mask_frame_stride=mfs, frame_layout=layout)
     torch.cuda.synchronize()
     rows = min(int(o["frame_offsets"][-1]), capacity)
     assert int(st_d.item()) == o["status"]
@@ -191,18 +201,20 @@ def scored_masks(ref, g, cfg, S, n, first):
     return ref.score_patches(g, mb, types, gs, want_score=False)["keep_mask"]
 
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("cfg_name,S,n", [("C1", 1, 8), ("C1", 5, 2), ("C2", 32, 4), ("C4", 8, 4)])
-def test_compact_configs(abi, ref, cfg_name, S, n):
+def test_compact_configs(abi, ref, cfg_name, S, n, layout):
     cfg = synth.CONFIGS[cfg_name]
     g = make_grid(*cfg["src"])
     km = scored_masks(ref, g, cfg, S, n, first=1)
     rng = np.random.default_rng(11)
     frames = synth.random_frames(S * n, 448, 448, rng)
     fidx = np.tile(np.arange(100, 100 + n, dtype=np.int32), S)
-    run_compact_both(abi, ref, g, km, fidx, frames, S * n * 1024, S, n, n)
+    run_compact_both(abi, ref, g, km, fidx, frames, S * n * 1024, S, n, n, layout)
 
 
-def test_compact_edge_cases(abi, ref):
+@pytest.mark.parametrize("layout", [0, 1])
+def test_compact_edge_cases(abi, ref, layout):
     g = make_grid(448, 448)
     rng = np.random.default_rng(3)
     S, n = 3, 3
@@ -211,23 +223,24 @@ def test_compact_edge_cases(abi, ref):
     km[2, 1] = 0xFFFFFFFF                       # a full frame
     frames = synth.random_frames(S * n, 448, 448, rng)
     fidx = np.arange(S * n, dtype=np.int32)
-    o = run_compact_both(abi, ref, g, km, fidx, frames, S * n * 1024, S, n, n)
+    o = run_compact_both(abi, ref, g, km, fidx, frames, S * n * 1024, S, n, n, layout)
     total = int(o["frame_offsets"][-1])
     # capacity overflow in the middle of a group, and exactly at a group boundary
-    run_compact_both(abi, ref, g, km, fidx, frames, total // 2 + 1, S, n, n)
-    run_compact_both(abi, ref, g, km, fidx, frames, (total // 8) * 4, S, n, n)
-    run_compact_both(abi, ref, g, km, fidx, frames, 0, S, n, n)
+    run_compact_both(abi, ref, g, km, fidx, frames, total // 2 + 1, S, n, n, layout)
+    run_compact_both(abi, ref, g, km, fidx, frames, (total // 8) * 4, S, n, n, layout)
+    run_compact_both(abi, ref, g, km, fidx, frames, 0, S, n, n, layout)
     # mask stride (ring) addressing
     ring = np.zeros((S, 7, 32), np.uint32)
     ring[:, 2:2 + n] = km
-    run_compact_both(abi, ref, g, ring[:, 2:].copy(), fidx, frames, S * n * 1024, S, n, 5)
+    run_compact_both(abi, ref, g, ring[:, 2:].copy(), fidx, frames, S * n * 1024, S, n, 5, layout)
     # empty batch
-    run_compact_both(abi, ref, g, np.zeros((0, n, 32), np.uint32), np.zeros(0, np.int32), [], 16, 0, n, n)
+    run_compact_both(abi, ref, g, np.zeros((0, n, 32), np.uint32), np.zeros(0, np.int32), [], 16, 0, n, n, layout)
 
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("geom", [(64, 48, 16, 8, 6, 2, 4), (30, 30, 8, 6, 6, 3, 6), (56, 56, 16, 4, 4, 1, 14),
                                   (100, 44, 16, 8, 8, 4, 8), (72, 40, 8, 12, 10, 2, 3)])
-def test_compact_generic_geometries(abi, ref, geom):
+def test_compact_generic_geometries(abi, ref, geom, layout):
     """Generic (runtime patch/group) path, odd patch size (scalar loads), group 1/3/4."""
     sw, sh, m, gw, gh, G, p = geom
     g = make_grid(sw, sh, mb_size=m, grid_w=gw, grid_h=gh, group=G, patch=p)
@@ -238,7 +251,7 @@ def test_compact_generic_geometries(abi, ref, geom):
     km &= rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
     frames = [rng.integers(0, 65536, size=(3, gh * p, gw * p), dtype=np.uint16) for _ in range(S * n)]
     fidx = np.arange(S * n, dtype=np.int32)
-    run_compact_both(abi, ref, g, km, fidx, frames, S * n * gw * gh, S, n, n)
+    run_compact_both(abi, ref, g, km, fidx, frames, S * n * gw * gh, S, n, n, layout)
 
 
 # ------------------------------------------------------------------------------------------------------------

@@ -328,6 +328,30 @@ def test_compact_round_trip_and_order(ref):
         assert h0 % 2 == 0 and w0 % 2 == 0 and hw == [(h0, w0), (h0, w0 + 1), (h0 + 1, w0), (h0 + 1, w0 + 1)]
 
 
+def to_grouped(frame, g):
+    """planar [3][gh*p][gw*p] -> grouped [groups][dy][dx][3][p][p] by a numpy permutation (independent of the
+    oracle's index arithmetic)."""
+    p, G = g["patch"], g["group"]
+    ngr, ngc = g["grid_h"] // G, g["grid_w"] // G
+    x = frame.reshape(3, ngr, G, p, ngc, G, p)            # c, gr, dy, y, gc, dx, x
+    return np.ascontiguousarray(x.transpose(1, 4, 2, 5, 0, 3, 6)).reshape(-1)
+
+
+@pytest.mark.parametrize("geom", [(448, 448, 14, 2, 32), (64, 48, 4, 2, 8), (30, 30, 5, 3, 6), (56, 56, 14, 1, 4)])
+def test_compact_grouped_layout_equals_planar(ref, geom):
+    sw, sh, p, G, gw = geom
+    g = make_grid(sw, sh, patch=p, group=G, grid_w=gw, grid_h=gw)
+    rng = np.random.default_rng(4)
+    nw = (gw * gw + 31) // 32
+    km = rng.integers(0, 2**32, size=(2, 3, nw), dtype=np.uint64).astype(np.uint32)
+    frames = [rng.integers(0, 65536, size=(3, gw * p, gw * p), dtype=np.uint16) for _ in range(6)]
+    a = ref.compact(g, km, np.arange(6, dtype=np.int32), frames, 6 * gw * gw, 2, 3)
+    b = ref.compact(g, km, np.arange(6, dtype=np.int32), [to_grouped(f, g) for f in frames], 6 * gw * gw, 2, 3,
+                    frame_layout=1)
+    for key in ("packed", "pos_ids", "src_index", "frame_offsets"):
+        assert (a[key] == b[key]).all(), key
+
+
 def test_compact_capacity_and_non_group_complete(ref):
     g = make_grid(128, 128, mb_size=16, grid_w=8, grid_h=8, patch=4, group=2)
     km = np.zeros((1, 1, 2), np.uint32)
