@@ -134,7 +134,9 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     const uint16_t* blk = frame + ((long long)gr * P.ngc + gc) * gs2 * row_el;
     uint16_t* dst = P.packed + n0 * row_el;
     if (vec_in && P.vec_out) {
-      const int n16 = static_cast<int>(nvalid * row_el * 2 / 16);
+      const int nel = static_cast<int>(nvalid * row_el);
+      const int n16 = nel / 8;
+      for (int e = n16 * 8 + lane; e < nel; e += 32) dst[e] = blk[e];  // tail of a truncated group
       const uint4* s4 = reinterpret_cast<const uint4*>(blk);
       uint4* d4 = reinterpret_cast<uint4*>(dst);
       constexpr int kU = 10;
@@ -171,7 +173,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     // straddle a patch boundary (p even), so the tile is written with 4-byte stores.
     const int cpr = gp / 4;
     const int total = 3 * gp * cpr;
-    constexpr int kUnroll = (TP > 0) ? ((3 * TG * TP * (TG * TP / 4) + 31) / 32) : 4;
+    constexpr int kUnroll = (TP > 0) ? 10 : 4;  // 588 8-B pieces of a 2x2 group of 14-px patches: 2 rounds
     for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
       uint2 v[kUnroll];
 #pragma unroll
@@ -216,10 +218,12 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
   const long long row_el = 3ll * pp;
   uint16_t* dst = P.packed + n0 * row_el;
   if (P.vec_out) {
-    const int n16 = static_cast<int>(nvalid * row_el * 2 / 16);
+    const int nel = static_cast<int>(nvalid * row_el);
+    const int n16 = nel / 8;
     const uint4* t4 = reinterpret_cast<const uint4*>(tile);
     uint4* d4 = reinterpret_cast<uint4*>(dst);
     for (int e = lane; e < n16; e += 32) d4[e] = t4[e];
+    for (int e = n16 * 8 + lane; e < nel; e += 32) dst[e] = tile[e];  // tail of a truncated group
   } else {
     const int nel = static_cast<int>(nvalid * row_el);
     for (int e = lane; e < nel; e += 32) dst[e] = tile[e];
@@ -237,7 +241,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
 }
 
 template <int TP, int TG>
-__global__ void __launch_bounds__(kGatherThreads) compact_gather(const __grid_constant__ CompactParams P) {
+__global__ void __launch_bounds__(kGatherThreads, 2) compact_gather(const __grid_constant__ CompactParams P) {
   extern __shared__ __align__(16) unsigned char g_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int G = TG > 0 ? TG : P.G;
@@ -325,7 +329,10 @@ int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, con
   P.FH = g->grid_h * g->patch;
   P.FW = g->grid_w * g->patch;
   const long long row_bytes = 3ll * g->patch * g->patch * 2ll;
-  P.vec_out = ((reinterpret_cast<uintptr_t>(packed) & 15u) == 0 && (row_bytes % 16) == 0) ? 1 : 0;
+  // every group starts at row n0 = q * group^2, i.e. at byte n0 * row_bytes: 16-B aligned iff a whole group is
+  // a multiple of 16 B (4,704 B for 2x2 groups of 14-px patches); a capacity-truncated group ends with a tail
+  P.vec_out = ((reinterpret_cast<uintptr_t>(packed) & 15u) == 0 &&
+               ((row_bytes * g->group * g->group) % 16) == 0) ? 1 : 0;
   P.layout = frame_layout;
   P.keep_mask = keep_mask;
   P.frame_index = frame_index;
