@@ -438,3 +438,174 @@ int codecsight_ref_kv_refresh(const ref_grid* g, const ref_kv* kv, const ref_win
   }
   return 0;
 }
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* kv_refresh_paged (NEXT-1): the same window step with the previous window's KV kept resident and        */
+/* updated IN PLACE ("maintains the previous window's KV cache resident in GPU memory and performs these  */
+/* updates in-place").  Each stream owns a pool of `capacity` physical rows; a token's rows live at */
+/* slot_map[p].  REUSE tokens keep their slot, their keys are rotated in place by R(dp) (Eq. 5) and their */
+/* values are not touched.  ANCHOR tokens keep their slot and are overwritten with their          */
+/* recomputed rows.  NEW tokens (new frames, prompt) take the free slots (slots not held by a token       */
+/* surviving from window k-1) in ascending slot order, in p_new order.                                    */
+/* ---------------------------------------------------------------------------------------------------- */
+int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const ref_window* win, int32_t n_streams,
+                                    const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                                    void* const* pool, const int32_t* slot_old, int32_t* slot_new, int64_t slot_cap,
+                                    const void* const* refreshed, int64_t token_cap, uint8_t* disposition,
+                                    int32_t* p_old, int32_t* n_tokens, unsigned long long* counters,
+                                    int32_t* status) {
+  int rc = ref_grid_ok(g);
+  if (rc) return rc;
+  if (!kv || !win) return -1;
+  if (n_streams < 0 || token_cap < 0 || slot_cap < 0) return -1;
+  if (kv->dtype != REF_BF16 && kv->dtype != REF_FP32) return -3;
+  if (kv->layers < 1 || kv->kv_heads < 1 || kv->head_dim < 2 || kv->head_dim > 512) return -3;
+  if (kv->head_dim % 2 != 0) return -3;
+  if (kv->capacity < 0 || kv->refresh_capacity < 0 || kv->n_prompt < 0) return -1;
+  if (!(kv->rope_base > 0.0)) return -1;
+  const int64_t w = win->window, s = win->stride, k = win->step;
+  if (w < 1 || s < 1 || k < 0) return -1;
+  if (s > w) return -3;
+  if (win->ring_frames < (k >= 1 ? w + s : w)) return -2;
+  if (n_streams == 0) return 0;
+  if (!keep_mask_ring || !frame_type_ring || !pool || !slot_new || !disposition || !p_old || !n_tokens ||
+      !counters || !status)
+    return -1;
+  if (k >= 1 && !slot_old) return -1;
+
+  const int64_t nw = ref_words(g), ring = win->ring_frames;
+  const int64_t L = kv->layers, H = kv->kv_heads, D = kv->head_dim, cap = kv->capacity;
+  const int64_t rowel = H * D, esz = (kv->dtype == REF_BF16) ? 2 : 4;
+  const int64_t ks = k * s, new_first = (k - 1) * s + w;
+  const int64_t max_tok = w * (g->grid_h / g->group) * (g->grid_w / g->group) + kv->n_prompt;
+  int32_t* tdisp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(max_tok + 1));
+  int64_t* tpold = (int64_t*)malloc(sizeof(int64_t) * (size_t)(max_tok + 1));
+  int64_t* tslot = (int64_t*)malloc(sizeof(int64_t) * (size_t)(max_tok + 1));
+  uint8_t* used = (uint8_t*)malloc((size_t)(cap + 1));
+  if (!tdisp || !tpold || !tslot || !used) { free(tdisp); free(tpold); free(tslot); free(used); return -1; }
+
+  for (int64_t sg = 0; sg < n_streams; ++sg) {
+    const uint32_t* mring = keep_mask_ring + sg * ring * nw;
+    const uint8_t* tring = frame_type_ring + sg * ring;
+    /* 1. the tokens of window k, in p_new order: disposition and p_old (same rules as kv_refresh) */
+    int64_t drop = 0, n_old = 0;
+    if (k >= 1) {
+      for (int64_t f = (k - 1) * s; f < ks; ++f) drop += ref_tokens_of(g, mring + (f % ring) * nw);
+      for (int64_t f = (k - 1) * s; f < (k - 1) * s + w; ++f) n_old += ref_tokens_of(g, mring + (f % ring) * nw);
+      n_old += kv->n_prompt; /* tokens of window k-1, prompt included */
+    }
+    int64_t nt = 0, before = 0;
+    for (int64_t f = ks; f < ks + w; ++f) {
+      const uint8_t type = tring[f % ring];
+      const int64_t nf = ref_tokens_of(g, mring + (f % ring) * nw);
+      for (int64_t t = 0; t < nf; ++t) {
+        if (k == 0 || f >= new_first) {
+          tdisp[nt] = REF_DISP_NEW;
+          tpold[nt] = -1;
+        } else {
+          tdisp[nt] = (type == REF_FRAME_I || f == ks) ? REF_DISP_ANCHOR : REF_DISP_REUSE;
+          tpold[nt] = drop + before + t;
+        }
+        ++nt;
+      }
+      before += nf;
+    }
+    const int64_t n_visual = nt;
+    for (int64_t j = 0; j < kv->n_prompt; ++j) {
+      tdisp[nt] = REF_DISP_NEW;
+      tpold[nt] = -1;
+      ++nt;
+    }
+    /* 2. slots held by tokens that survive from window k-1 (REUSE and ANCHOR keep their rows' slots) */
+    for (int64_t i = 0; i < cap; ++i) used[i] = 0;
+    for (int64_t p = 0; p < nt; ++p) {
+      tslot[p] = -1;
+      if (tdisp[p] == REF_DISP_NEW) continue;
+      const int64_t po = tpold[p];
+      const int64_t sl = (po < slot_cap && po < n_old) ? slot_old[sg * slot_cap + po] : -1;
+      if (sl < 0 || sl >= cap) { *status |= REF_ST_ORIGIN; continue; }
+      tslot[p] = sl;
+      used[sl] = 1;
+    }
+    /* 3. NEW tokens take the free slots in ascending order */
+    int64_t next_free = 0;
+    for (int64_t p = 0; p < nt; ++p) {
+      if (tdisp[p] != REF_DISP_NEW) continue;
+      while (next_free < cap && used[next_free]) ++next_free;
+      if (next_free >= cap) { *status |= REF_ST_CAPACITY; continue; }
+      tslot[p] = next_free;
+      used[next_free] = 1;
+    }
+    /* 4. outputs and row updates */
+    const uint8_t* rf = refreshed ? (const uint8_t*)refreshed[sg] : NULL;
+    uint8_t* pl = (uint8_t*)pool[sg];
+    int64_t n_reuse = 0, n_anchor = 0, n_new = 0, rrow = 0, rot = 0, cop = 0, dp = 0;
+    for (int64_t p = 0; p < nt; ++p) {
+      const int d = tdisp[p];
+      if (d == REF_DISP_REUSE) ++n_reuse;
+      else if (d == REF_DISP_ANCHOR) ++n_anchor;
+      else ++n_new;
+      if (p < token_cap) {
+        disposition[sg * token_cap + p] = (uint8_t)d;
+        p_old[sg * token_cap + p] = (int32_t)tpold[p];
+      } else {
+        *status |= REF_ST_CAPACITY;
+      }
+      if (p < slot_cap) slot_new[sg * slot_cap + p] = (int32_t)tslot[p];
+      else *status |= REF_ST_CAPACITY;
+      const int64_t sl = tslot[p];
+      if (d == REF_DISP_REUSE) {
+        if (sl < 0) continue;
+        dp = p - tpold[p];
+        for (int64_t l = 0; l < L; ++l)
+          for (int64_t h = 0; h < H; ++h)
+            for (int64_t i = 0; i < D / 2; ++i) {
+              const int64_t base = ((l * 2 + 0) * cap + sl) * rowel; /* the key row, rotated in place */
+              const int64_t e1 = base + h * D + i, e2 = base + h * D + i + D / 2;
+              float x1, x2, o1, o2;
+              if (esz == 2) {
+                x1 = ref_bf16_to_f32(((uint16_t*)pl)[e1]);
+                x2 = ref_bf16_to_f32(((uint16_t*)pl)[e2]);
+              } else {
+                x1 = ((float*)pl)[e1];
+                x2 = ((float*)pl)[e2];
+              }
+              ref_rot_pair(x1, x2, i, D, kv->rope_base, dp, &o1, &o2);
+              if (esz == 2) {
+                ((uint16_t*)pl)[e1] = ref_f32_to_bf16(o1);
+                ((uint16_t*)pl)[e2] = ref_f32_to_bf16(o2);
+              } else {
+                ((float*)pl)[e1] = o1;
+                ((float*)pl)[e2] = o2;
+              }
+            }
+        ++rot;
+      } else {
+        const int64_t r = rrow++;
+        if (!rf || sl < 0) continue;
+        if (r >= kv->refresh_capacity) { *status |= REF_ST_CAPACITY; continue; }
+        for (int64_t l = 0; l < L; ++l)
+          for (int64_t h2 = 0; h2 < 2; ++h2)
+            memcpy(pl + ((l * 2 + h2) * cap + sl) * rowel * esz,
+                   rf + ((l * 2 + h2) * kv->refresh_capacity + r) * rowel * esz, (size_t)(rowel * esz));
+        ++cop;
+      }
+    }
+    (void)dp;
+    n_tokens[sg * 4 + 0] = (int32_t)n_visual;
+    n_tokens[sg * 4 + 1] = (int32_t)n_reuse;
+    n_tokens[sg * 4 + 2] = (int32_t)n_anchor;
+    n_tokens[sg * 4 + 3] = (int32_t)n_new;
+    counters[REF_C_TOK_REUSE] += (unsigned long long)n_reuse;
+    counters[REF_C_TOK_ANCHOR] += (unsigned long long)n_anchor;
+    counters[REF_C_TOK_NEW] += (unsigned long long)n_new;
+    /* keys only for REUSE (read + write), keys and values for refreshed rows (read + write) */
+    counters[REF_C_BYTES_KV] += (unsigned long long)((rot * L * 1 + cop * L * 2) * rowel * esz * 2);
+    counters[REF_C_STREAM_STEPS] += 1;
+  }
+  free(tdisp);
+  free(tpold);
+  free(tslot);
+  free(used);
+  return 0;
+}

@@ -93,6 +93,14 @@ int codecsight_ref_kv_refresh(const ref_grid* g, const ref_kv* kv, const ref_win
                               const void* const* refreshed, int64_t token_cap, uint8_t* disposition,
                               int32_t* p_old, int32_t* n_tokens, unsigned long long* counters, int32_t* status);
 
+/* NEXT-1: in-place / paged variant (per-stream row pools + slot maps). */
+int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const ref_window* win, int32_t n_streams,
+                                    const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                                    void* const* pool, const int32_t* slot_old, int32_t* slot_new, int64_t slot_cap,
+                                    const void* const* refreshed, int64_t token_cap, uint8_t* disposition,
+                                    int32_t* p_old, int32_t* n_tokens, unsigned long long* counters,
+                                    int32_t* status);
+
 /* Eq. 5 on one fp32 key vector of n_heads x head_dim: out = R(dp) k (rotate_half pairing). */
 void codecsight_ref_rope_rotate_f32(const float* k, int32_t n_heads, int32_t head_dim, double base, int64_t dp,
                                     float* out);

@@ -74,6 +74,10 @@ def lib():
         L.codecsight_ref_kv_refresh.restype = C.c_int
         L.codecsight_ref_kv_refresh.argtypes = [C.POINTER(RefGrid), C.POINTER(RefKv), C.POINTER(RefWindow),
                                                 C.c_int32, P, P, P, P, P, C.c_int64, P, P, P, P, P]
+        L.codecsight_ref_kv_refresh_paged.restype = C.c_int
+        L.codecsight_ref_kv_refresh_paged.argtypes = [C.POINTER(RefGrid), C.POINTER(RefKv), C.POINTER(RefWindow),
+                                                      C.c_int32, P, P, P, P, P, C.c_int64, P, C.c_int64, P, P, P,
+                                                      P, P]
         L.codecsight_ref_rope_rotate_f32.restype = None
         L.codecsight_ref_rope_rotate_f32.argtypes = [P, C.c_int32, C.c_int32, C.c_double, C.c_int64, P]
         _lib = L
@@ -197,6 +201,37 @@ def kv_refresh(g: dict, kv: dict, win: dict, keep_mask_ring: np.ndarray, frame_t
                                          _p(frame_type_ring), olds, news, refs, token_cap, _p(disp), _p(pold),
                                          _p(ntok), _p(counters), _p(status))
     return dict(rc=rc, disposition=disp, p_old=pold, n_tokens=ntok, counters=counters, status=int(status[0]))
+
+
+def kv_refresh_paged(g: dict, kv: dict, win: dict, keep_mask_ring: np.ndarray, frame_type_ring: np.ndarray,
+                     pools: list, slot_old: np.ndarray | None, slot_cap: int, refreshed: list | None, token_cap: int,
+                     counters: np.ndarray | None = None):
+    """Pools are numpy arrays [L][2][capacity][H][D] updated in place; slot_old [S][slot_cap] (or None at k=0).
+    Returns dict(slot_new [S][slot_cap], disposition, p_old, n_tokens, counters, status, rc)."""
+    S = len(pools)
+    nw = grid_words(g)
+    keep_mask_ring = np.ascontiguousarray(keep_mask_ring, dtype=np.uint32).reshape(S, win["ring_frames"], nw)
+    frame_type_ring = np.ascontiguousarray(frame_type_ring, dtype=np.uint8).reshape(S, win["ring_frames"])
+    for c in pools:
+        assert c.flags.c_contiguous
+    pp = C.cast((C.c_void_p * S)(*[x.ctypes.data for x in pools]), C.c_void_p)
+    rp = None if refreshed is None else C.cast((C.c_void_p * S)(*[x.ctypes.data for x in refreshed]), C.c_void_p)
+    so = None if slot_old is None else np.ascontiguousarray(slot_old, dtype=np.int32)
+    sn = np.full((S, slot_cap), -7, np.int32)
+    disp = np.zeros((S, token_cap), np.uint8)
+    pold = np.zeros((S, token_cap), np.int32)
+    ntok = np.zeros((S, 4), np.int32)
+    counters = np.zeros(NCOUNTERS, np.uint64) if counters is None else counters
+    status = np.zeros(1, np.int32)
+    kvd = kv_desc(kv["layers"], kv["kv_heads"], kv["head_dim"], kv["dtype"], kv["capacity"],
+                  kv["refresh_capacity"], kv["rope_base"], kv["n_prompt"])
+    w = RefWindow(win["window"], win["stride"], win["step"], win["ring_frames"])
+    rc = lib().codecsight_ref_kv_refresh_paged(C.byref(make_grid(g)), C.byref(kvd), C.byref(w), S,
+                                               _p(keep_mask_ring), _p(frame_type_ring), pp, _p(so), _p(sn),
+                                               slot_cap, rp, token_cap, _p(disp), _p(pold), _p(ntok), _p(counters),
+                                               _p(status))
+    return dict(rc=rc, slot_new=sn, disposition=disp, p_old=pold, n_tokens=ntok, counters=counters,
+                status=int(status[0]))
 
 
 def rope_rotate_f32(k: np.ndarray, n_heads: int, head_dim: int, base: float, dp: int) -> np.ndarray:
