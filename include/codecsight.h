@@ -249,6 +249,39 @@ int codecsight_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_windo
                           void* workspace, size_t workspace_bytes, unsigned long long* counters,
                           int32_t* status, cudaStream_t stream);
 
+/* ------------------------------------------------------------------------------------------------------------
+ * codecsight_kv_refresh_paged — the same window step with the KV cache kept resident and updated IN PLACE
+ * ("maintains the previous window's KV cache resident in GPU memory and performs these updates in-place", P:363;
+ * SURVEY NEXT-1).  Each stream owns a pool of kv->capacity physical rows, laid out like a cache buffer
+ * [layers][2][capacity][H][D]; a window's token p lives in row slot_map[p].
+ *   tokens, dispositions, p_old, n_tokens: exactly as codecsight_kv_refresh.
+ *   REUSE  : keeps slot_old[p_old]; its key rows are rotated in place by R(p_new - p_old) (Eq. 5); values are not
+ *            touched.
+ *   ANCHOR : keeps slot_old[p_old]; its K and V rows are overwritten with refreshed row r (if refreshed != NULL).
+ *   NEW    : (new frames, then prompt rows) take the free slots -- slots not held by a REUSE/ANCHOR token --
+ *            in ascending slot order, in p_new order; rows copied from refreshed row r (if refreshed != NULL).
+ * Only keys of reused tokens move: 57,344 B per reused token instead of 114,688 B (Qwen2-VL-7B bf16).
+ *
+ *   pool        device array [n_streams] of device pointers to the row pools (in/out, 16-B aligned)
+ *   slot_old    device [n_streams][slot_cap] i32: slots of window k-1 (read when k >= 1; entries outside
+ *               [0, capacity) raise CS_STATUS_ORIGIN and the token gets no row)
+ *   slot_new    device [n_streams][slot_cap] i32 out: slots of window k (-1 = no row); must not alias slot_old
+ *   slot_cap    per-stream length of the slot maps
+ *   workspace   >= codecsight_kv_refresh_paged_workspace_size() bytes, 16-B aligned
+ *   other arguments as codecsight_kv_refresh.  CS_STATUS_CAPACITY when a NEW token finds no free slot.
+ * Limits: capacity <= 262144 rows per stream.
+ * --------------------------------------------------------------------------------------------------------- */
+int codecsight_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                                const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring, void* const* pool,
+                                const int32_t* slot_old, int32_t* slot_new, int64_t slot_cap,
+                                const void* const* refreshed, int64_t token_cap, uint8_t* disposition,
+                                int32_t* p_old, int32_t* n_tokens, void* workspace, size_t workspace_bytes,
+                                unsigned long long* counters, int32_t* status, cudaStream_t stream);
+
+/* Bytes of device workspace codecsight_kv_refresh_paged needs (0 on bad args). */
+size_t codecsight_kv_refresh_paged_workspace_size(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win,
+                                                  int32_t n_streams);
+
 /* Bytes of device workspace codecsight_kv_refresh needs for this window and stream count (0 on bad args). */
 size_t codecsight_kv_refresh_workspace_size(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams);
 

@@ -67,6 +67,12 @@ def lib():
         L.codecsight_kv_refresh.restype = C.c_int
         L.codecsight_kv_refresh.argtypes = [C.POINTER(CsGrid), C.POINTER(CsKvDesc), C.POINTER(CsWindow), I32, P, P,
                                             P, P, P, I64, P, P, P, P, C.c_size_t, P, P, P]
+        L.codecsight_kv_refresh_paged.restype = C.c_int
+        L.codecsight_kv_refresh_paged.argtypes = [C.POINTER(CsGrid), C.POINTER(CsKvDesc), C.POINTER(CsWindow), I32,
+                                                  P, P, P, P, P, I64, P, I64, P, P, P, P, C.c_size_t, P, P, P]
+        L.codecsight_kv_refresh_paged_workspace_size.restype = C.c_size_t
+        L.codecsight_kv_refresh_paged_workspace_size.argtypes = [C.POINTER(CsGrid), C.POINTER(CsKvDesc),
+                                                                 C.POINTER(CsWindow), I32]
         L.codecsight_kv_refresh_workspace_size.restype = C.c_size_t
         L.codecsight_kv_refresh_workspace_size.argtypes = [C.POINTER(CsKvDesc), C.POINTER(CsWindow), I32]
         L.codecsight_strerror.restype = C.c_char_p
@@ -163,7 +169,25 @@ def codecsight_kv_refresh(g: dict, kv: dict, win: dict, n_streams: int, keep_mas
     _check(rc, "codecsight_kv_refresh")
 
 
+def kv_paged_workspace_size(g: dict, kv: dict, win: dict, n_streams: int) -> int:
+    return int(lib().codecsight_kv_refresh_paged_workspace_size(C.byref(make_grid(g)), C.byref(make_kv(kv)),
+                                                                C.byref(make_window(win)), n_streams))
+
+
+def codecsight_kv_refresh_paged(g: dict, kv: dict, win: dict, n_streams: int, keep_mask_ring, frame_type_ring,
+                                pool_ptrs, slot_old, slot_new, slot_cap: int, refreshed_ptrs, token_cap: int,
+                                disposition, p_old, n_tokens, workspace, counters, status, stream=None) -> None:
+    ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    rc = lib().codecsight_kv_refresh_paged(C.byref(make_grid(g)), C.byref(make_kv(kv)), C.byref(make_window(win)),
+                                           n_streams, _ptr(keep_mask_ring), _ptr(frame_type_ring), _ptr(pool_ptrs),
+                                           _ptr(slot_old), _ptr(slot_new), slot_cap, _ptr(refreshed_ptrs), token_cap,
+                                           _ptr(disposition), _ptr(p_old), _ptr(n_tokens), _ptr(workspace), ws_bytes,
+                                           _ptr(counters), _ptr(status), _stream(stream))
+    _check(rc, "codecsight_kv_refresh_paged")
+
+
 # short aliases
+kv_refresh_paged = codecsight_kv_refresh_paged
 score_patches = codecsight_score_patches
 compact = codecsight_compact
 kv_refresh = codecsight_kv_refresh

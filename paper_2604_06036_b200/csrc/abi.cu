@@ -64,6 +64,9 @@ int cs_set_smem_attr(const void* func, int slot, int bytes) {
 
 extern "C" {
 
+static int kv_args_ok(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                      int64_t token_cap);
+
 int codecsight_version(void) { return 100; }
 
 const char* codecsight_strerror(int code) {
@@ -118,18 +121,45 @@ int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, co
                            packed, pos_ids, src_index, frame_offsets, counters, status, stream);
 }
 
+int codecsight_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                                const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring, void* const* pool,
+                                const int32_t* slot_old, int32_t* slot_new, int64_t slot_cap,
+                                const void* const* refreshed, int64_t token_cap, uint8_t* disposition,
+                                int32_t* p_old, int32_t* n_tokens, void* workspace, size_t workspace_bytes,
+                                unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+  int rc = kv_args_ok(g, kv, win, n_streams, token_cap);
+  if (rc == 1) return CS_OK;
+  if (rc) return rc;
+  if (slot_cap < 0) return CS_ERR_INVALID_ARGUMENT;
+  if (kv->capacity > 262144) return CS_ERR_UNSUPPORTED;
+  if (!keep_mask_ring || !frame_type_ring || !pool || !slot_new || !disposition || !p_old || !n_tokens ||
+      !counters || !status || !workspace)
+    return CS_ERR_INVALID_ARGUMENT;
+  if (win->step >= 1 && !slot_old) return CS_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15u) != 0) return CS_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < cs_kv_paged_workspace_bytes(g, kv, win, n_streams)) return CS_ERR_INVALID_ARGUMENT;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_kv_refresh_paged(g, kv, win, n_streams, keep_mask_ring, frame_type_ring, pool, slot_old,
+                                    slot_new, slot_cap, refreshed, token_cap, disposition, p_old, n_tokens,
+                                    workspace, counters, status, stream);
+}
+
+size_t codecsight_kv_refresh_paged_workspace_size(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win,
+                                                  int32_t n_streams) {
+  if (!g || !kv || !win || n_streams < 0 || win->window < 1 || kv->head_dim < 2 || kv->head_dim > cs::kMaxHeadDim ||
+      g->group < 1 || kv->n_prompt < 0)
+    return 0;
+  return cs_kv_paged_workspace_bytes(g, kv, win, n_streams);
+}
+
 size_t codecsight_kv_refresh_workspace_size(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams) {
   if (!kv || !win || n_streams < 0 || win->window < 1 || kv->head_dim < 2 || kv->head_dim > cs::kMaxHeadDim)
     return 0;
   return cs_kv_workspace_bytes(kv, win, n_streams);
 }
 
-int codecsight_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
-                          const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
-                          const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
-                          int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens,
-                          void* workspace, size_t workspace_bytes, unsigned long long* counters,
-                          int32_t* status, cudaStream_t stream) {
+static int kv_args_ok(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                      int64_t token_cap) {
   int rc = grid_ok(g);
   if (rc) return rc;
   if (!kv || !win) return CS_ERR_INVALID_ARGUMENT;
@@ -145,7 +175,7 @@ int codecsight_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_windo
   if (s > w) return CS_ERR_UNSUPPORTED;
   if (win->ring_frames < (k >= 1 ? w + s : w)) return CS_ERR_SHAPE;
   if (w + s > cs::kMaxWindowPlusStride) return CS_ERR_UNSUPPORTED;
-  if (n_streams == 0) return CS_OK;
+  if (n_streams == 0) return 1;  /* nothing to do */
   if (n_streams > 8192) return CS_ERR_UNSUPPORTED;
   const long long nw = (static_cast<long long>(g->grid_w) * g->grid_h + 31) / 32;
   if ((w + s) * nw * 4 > 96 * 1024) return CS_ERR_UNSUPPORTED;
@@ -153,6 +183,19 @@ int codecsight_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_windo
   if (w * ngroups + kv->n_prompt >= 2147483647LL || kv->capacity >= 2147483647LL ||
       kv->refresh_capacity >= 2147483647LL || (k * s + w) >= 2147483647LL)
     return CS_ERR_UNSUPPORTED;
+  return CS_OK;
+}
+
+int codecsight_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                          const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                          const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
+                          int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens,
+                          void* workspace, size_t workspace_bytes, unsigned long long* counters,
+                          int32_t* status, cudaStream_t stream) {
+  int rc = kv_args_ok(g, kv, win, n_streams, token_cap);
+  if (rc == 1) return CS_OK;
+  if (rc) return rc;
+  const long long k = win->step;
   if (!keep_mask_ring || !frame_type_ring || !new_cache || !disposition || !p_old || !n_tokens || !counters ||
       !status || !workspace)
     return CS_ERR_INVALID_ARGUMENT;

@@ -158,6 +158,14 @@ int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window
                          void* workspace, size_t workspace_bytes, unsigned long long* counters, int32_t* status,
                          cudaStream_t stream);
 size_t cs_kv_workspace_bytes(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams);
+int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                               const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring, void* const* pool,
+                               const int32_t* slot_old, int32_t* slot_new, int64_t slot_cap,
+                               const void* const* refreshed, int64_t token_cap, uint8_t* disposition,
+                               int32_t* p_old, int32_t* n_tokens, void* workspace, unsigned long long* counters,
+                               int32_t* status, cudaStream_t stream);
+size_t cs_kv_paged_workspace_bytes(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win,
+                                   int32_t n_streams);
 int cs_num_sms();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel slot, device); 0 on success
 int cs_set_smem_attr(const void* func, int slot, int bytes);

@@ -59,6 +59,14 @@ struct KvParams {
   unsigned char* ws;
   unsigned long long* counters;
   int32_t* status;
+  // paged (in-place) variant
+  void* const* pool;
+  const int32_t* slot_old;
+  int32_t* slot_new;
+  long long slot_cap;
+  int max_tok;      // w * groups + n_prompt: entries of the per-stream move list
+  int prefix_mode;  // kv_prefix items: 0 = (stream, 128-row block, layer, K|V), 1 = tokens
+  long long mv_off;  // byte offset of the move list inside a stream's workspace slice
   double inv_freq[cs::kMaxHeadDim / 2];  // base^(-2i/D), computed on the host
 };
 
@@ -592,8 +600,12 @@ __global__ void __launch_bounds__(1024) kv_prefix(const __grid_constant__ KvPara
     int v = 0;
     if (si < P.n_streams) {
       const KvHdr* h = reinterpret_cast<const KvHdr*>(stream_ws(P, si));
-      const int rows = h->n_seg > 0 ? h->n_rows : 0;
-      v = (rows + kRowBlock - 1) / kRowBlock * ipb;
+      if (P.prefix_mode == 1) {
+        v = h->n_rows;  // paged: one item per token (all layers)
+      } else {
+        const int rows = h->n_seg > 0 ? h->n_rows : 0;
+        v = (rows + kRowBlock - 1) / kRowBlock * ipb;
+      }
     }
     int inc = v;
 #pragma unroll
@@ -742,6 +754,419 @@ __global__ void __launch_bounds__(kGatherThreads, 1) kv_gather_tma(const __grid_
   }
   if (lane == 0) cs::bulk_wait_all<0>();
 }
+
+// ============================================================================================================
+// Paged / in-place variant (NEXT-1; "maintains the previous window's KV cache resident in GPU memory and
+// performs these updates in-place").  Rows live in a per-stream pool; slot maps give each token's row.
+// REUSE: key rotated in place, value untouched.  ANCHOR: keeps its slot, rows overwritten from `refreshed`.
+// NEW (new frames + prompt): the free slots in ascending order.
+// ============================================================================================================
+struct MoveEntry {
+  int slot;  // pool row, -1 = none
+  int src;   // -1: rotate the key in place (REUSE); >= 0: copy K and V from refreshed row src; -2: nothing
+};
+
+__device__ __forceinline__ MoveEntry* stream_moves(const KvParams& P, int s) {
+  return reinterpret_cast<MoveEntry*>(stream_ws(P, s) + P.mv_off);
+}
+
+// exclusive scan of n ints in shared memory (in place), block-wide; returns the total
+__device__ int block_exclusive_scan(int* a, int n) {
+  __shared__ int s_part[33];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  const int b = tid * per, e = min(n, b + per);
+  int sum = 0;
+  for (int i = b; i < e; ++i) sum += a[i];
+  // warp scan of the per-thread sums, then of the warp totals
+  const int lane = tid & 31, warp = tid >> 5;
+  int inc = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += u;
+  }
+  if (lane == 31) s_part[warp] = inc;
+  __syncthreads();
+  if (tid == 0) {
+    int c = 0;
+    for (int q = 0; q < (nt + 31) / 32; ++q) {
+      const int v = s_part[q];
+      s_part[q] = c;
+      c += v;
+    }
+    s_part[32] = c;
+  }
+  __syncthreads();
+  int run = s_part[warp] + inc - sum;
+  for (int i = b; i < e; ++i) {
+    const int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  __syncthreads();
+  return s_part[32];
+}
+
+__global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_constant__ KvParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int s_n[cs::kMaxWindowPlusStride];
+  __shared__ uint8_t s_t[cs::kMaxWindowPlusStride];
+  __shared__ KvSeg s_seg[kMaxSeg];
+  __shared__ int s_pold[kMaxSeg];
+  __shared__ int s_disp[kMaxSeg];
+  __shared__ int s_nseg, s_dp, s_ntotal, s_p0, s_n_old, s_r0, s_st;
+  __shared__ unsigned long long s_rot, s_cop;
+
+  const int sidx = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int k = P.k, w = P.w, s = P.s;
+  const int lo = k >= 1 ? (k - 1) * s : 0;
+  const int ks = k * s, hi = ks + w;
+  const int nfr = hi - lo;
+  const int nw = P.nw;
+  const int cw = static_cast<int>((P.cap + 31) / 32);  // words of the slot bitmap
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(smem);                 // [nfr][nw]
+  uint32_t* s_used = s_mask + nfr * nw;                                 // [cw]
+  int* s_free = reinterpret_cast<int*>(s_used + cw);                    // [cw + 1] free-slot prefix
+
+  for (int e = tid; e < nfr * nw; e += blockDim.x) {
+    const int fi = e / nw, t = e - fi * nw;
+    s_mask[e] = __ldg(P.mring + ((long long)sidx * P.ring + ((lo + fi) % P.ring)) * nw + t);
+  }
+  for (int fi = tid; fi < nfr; fi += blockDim.x) s_t[fi] = __ldg(P.tring + (long long)sidx * P.ring + ((lo + fi) % P.ring));
+  for (int i = tid; i < cw; i += blockDim.x) s_used[i] = 0u;
+  if (tid == 0) {
+    s_rot = 0ull;
+    s_cop = 0ull;
+    s_st = 0;
+  }
+  __syncthreads();
+  for (int fi = warp; fi < nfr; fi += nwarp) {
+    int n = 0;
+    for (int base = 0; base < P.ngroups; base += 32) {
+      const int q = base + lane;
+      const bool kept = q < P.ngroups && cs::group_kept(s_mask + fi * nw, q, P.ngc, P.G, P.grid_w);
+      n += __popc(__ballot_sync(0xffffffffu, kept));
+    }
+    if (lane == 0) s_n[fi] = n;
+  }
+  __syncthreads();
+
+  if (tid == 0) {
+    long long drop = 0, n_old = 0;
+    if (k >= 1) {
+      for (int f = lo; f < ks; ++f) drop += s_n[f - lo];
+      for (int f = lo; f < lo + w; ++f) n_old += s_n[f - lo];
+      n_old += P.n_prompt;
+    }
+    const int new_first = (k - 1) * s + w;
+    long long pnew = 0, rrow = 0, n_reuse = 0, n_anchor = 0, n_new = 0, p0 = -1, r0 = 0;
+    int nseg = 0;
+    for (int f = ks; f < hi; ++f) {
+      const int n = s_n[f - lo];
+      int disp, pold;
+      if (k == 0 || f >= new_first) {
+        disp = CS_DISP_NEW;
+        pold = -1;
+      } else {
+        disp = (s_t[f - lo] != CS_FRAME_P || f == ks) ? CS_DISP_ANCHOR : CS_DISP_REUSE;
+        pold = static_cast<int>(drop + pnew);
+      }
+      if (disp == CS_DISP_NEW && p0 < 0) {
+        p0 = pnew;
+        r0 = rrow;
+      }
+      s_seg[nseg].p_new = static_cast<int>(pnew);
+      s_seg[nseg].len = n;
+      s_seg[nseg].kind = disp;
+      s_seg[nseg].src = static_cast<int>(rrow);
+      s_pold[nseg] = pold;
+      s_disp[nseg] = disp;
+      ++nseg;
+      if (disp != CS_DISP_REUSE) rrow += n;
+      if (disp == CS_DISP_REUSE) n_reuse += n;
+      else if (disp == CS_DISP_ANCHOR) n_anchor += n;
+      else n_new += n;
+      pnew += n;
+    }
+    const long long n_visual = pnew;
+    if (p0 < 0) {
+      p0 = pnew;
+      r0 = rrow;
+    }
+    s_seg[nseg].p_new = static_cast<int>(pnew);
+    s_seg[nseg].len = P.n_prompt;
+    s_seg[nseg].kind = CS_DISP_NEW;
+    s_seg[nseg].src = static_cast<int>(rrow);
+    s_pold[nseg] = -1;
+    s_disp[nseg] = CS_DISP_NEW;
+    ++nseg;
+    n_new += P.n_prompt;
+    const long long n_total = n_visual + P.n_prompt;
+    s_nseg = nseg;
+    s_dp = static_cast<int>(-drop);
+    s_ntotal = static_cast<int>(n_total);
+    s_p0 = static_cast<int>(p0);
+    s_r0 = static_cast<int>(r0);
+    s_n_old = static_cast<int>(n_old);
+    int* nt = P.n_tokens + (long long)sidx * 4;
+    nt[0] = static_cast<int>(n_visual);
+    nt[1] = static_cast<int>(n_reuse);
+    nt[2] = static_cast<int>(n_anchor);
+    nt[3] = static_cast<int>(n_new);
+    int st = 0;
+    if (n_total > P.token_cap || n_total > P.slot_cap) st |= CS_STATUS_CAPACITY;
+    s_st = st;
+    KvHdr* hdr = reinterpret_cast<KvHdr*>(stream_ws(P, sidx));
+    hdr->n_rows = static_cast<int>(n_total < P.max_tok ? n_total : P.max_tok);
+    hdr->n_seg = nseg;
+    hdr->dp = static_cast<int>(-drop);
+    hdr->pad = 0;
+    cs::atomic_add_u64(&P.counters[CS_CNT_TOK_REUSE], static_cast<unsigned long long>(n_reuse));
+    cs::atomic_add_u64(&P.counters[CS_CNT_TOK_ANCHOR], static_cast<unsigned long long>(n_anchor));
+    cs::atomic_add_u64(&P.counters[CS_CNT_TOK_NEW], static_cast<unsigned long long>(n_new));
+    cs::atomic_add_u64(&P.counters[CS_CNT_STREAM_STEPS], 1ull);
+  }
+  __syncthreads();
+
+  const int nseg = s_nseg, n_total = s_ntotal, p0 = s_p0, n_old = s_n_old;
+  MoveEntry* mv = stream_moves(P, sidx);
+  int32_t* slot_new = P.slot_new + (long long)sidx * P.slot_cap;
+  uint8_t* dsp = P.disposition + (long long)sidx * P.token_cap;
+  int32_t* po_out = P.p_old + (long long)sidx * P.token_cap;
+  int st_local = 0;
+  unsigned long long rot = 0, cop = 0;
+  // ---- surviving tokens (REUSE, ANCHOR) keep their slots; index outputs of every token ---------------------
+  for (int i = warp; i < nseg; i += nwarp) {
+    const KvSeg sg = s_seg[i];
+    const int d = s_disp[i], pold = s_pold[i];
+    for (int t = lane; t < sg.len; t += 32) {
+      const long long p = (long long)sg.p_new + t;
+      if (p < P.token_cap) {
+        dsp[p] = static_cast<uint8_t>(d);
+        po_out[p] = d == CS_DISP_NEW ? -1 : pold + t;
+      }
+      if (d == CS_DISP_NEW) continue;
+      const long long q = (long long)pold + t;
+      int sl = -1;
+      if (q < P.slot_cap && q < n_old) sl = __ldg(P.slot_old + (long long)sidx * P.slot_cap + q);
+      if (sl < 0 || sl >= P.cap) {
+        sl = -1;
+        st_local |= CS_STATUS_ORIGIN;
+      } else {
+        atomicOr(&s_used[sl >> 5], 1u << (sl & 31));
+      }
+      if (p < P.slot_cap) slot_new[p] = sl;
+      MoveEntry me;
+      me.slot = sl;
+      if (d == CS_DISP_REUSE) {
+        me.src = sl >= 0 ? -1 : -2;
+        rot += sl >= 0;
+      } else {
+        const long long r = (long long)sg.src + t;
+        const bool ok = P.has_refreshed && sl >= 0 && r < P.rcap;
+        if (P.has_refreshed && sl >= 0 && r >= P.rcap) st_local |= CS_STATUS_CAPACITY;
+        me.src = ok ? static_cast<int>(r) : -2;
+        cop += ok;
+      }
+      if (p < P.max_tok) mv[p] = me;
+    }
+  }
+  __syncthreads();
+  // ---- free slots (not held by a survivor), ascending -> NEW tokens in p_new order -------------------------
+  for (int i = tid; i < cw; i += blockDim.x) {
+    uint32_t valid = 0xffffffffu;
+    if ((long long)(i + 1) * 32 > P.cap) valid = (1u << (P.cap - (long long)i * 32)) - 1u;
+    s_free[i] = __popc(~s_used[i] & valid);
+  }
+  __syncthreads();
+  const int total_free = block_exclusive_scan(s_free, cw);
+  if (tid == 0) s_free[cw] = total_free;
+  __syncthreads();
+  for (int p = p0 + tid; p < n_total; p += blockDim.x) {
+    const int i = p - p0;  // index among the NEW tokens
+    int sl = -1;
+    if (i < total_free) {
+      int a = 0, b = cw;  // s_free[a] <= i < s_free[b]
+      while (b - a > 1) {
+        const int m = (a + b) >> 1;
+        if (s_free[m] <= i) a = m; else b = m;
+      }
+      const uint32_t fr = ~s_used[a];
+      const int j = i - s_free[a];
+      sl = a * 32 + static_cast<int>(__fns(fr, 0, j + 1));
+    } else {
+      st_local |= CS_STATUS_CAPACITY;
+    }
+    if (p < P.slot_cap) slot_new[p] = sl;
+    const long long r = (long long)s_r0 + i;
+    const bool ok = P.has_refreshed && sl >= 0 && r < P.rcap;
+    if (P.has_refreshed && sl >= 0 && r >= P.rcap) st_local |= CS_STATUS_CAPACITY;
+    MoveEntry me;
+    me.slot = sl;
+    me.src = ok ? static_cast<int>(r) : -2;
+    cop += ok;
+    if (p < P.max_tok) mv[p] = me;
+  }
+  // ---- (cos, sin) of R(dp) ----------------------------------------------------------------------------------
+  float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
+  for (int i = tid; i < P.D / 2; i += blockDim.x) {
+    const double ang = static_cast<double>(s_dp) * P.inv_freq[i];
+    cs_tab[i] = make_float2(__double2float_rn(cos(ang)), __double2float_rn(sin(ang)));
+  }
+  if (st_local) atomicOr(&s_st, st_local);
+  if (rot) atomicAdd(&s_rot, rot);
+  if (cop) atomicAdd(&s_cop, cop);
+  __syncthreads();
+  if (tid == 0) {
+    cs::atomic_or_status(P.status, s_st);
+    const unsigned long long rowb = (unsigned long long)(P.H * P.D * P.esz);
+    cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_KV], (s_rot * P.L + s_cop * P.L * 2ull) * rowb * 2ull);
+  }
+}
+
+// One token per warp iteration: REUSE -> rotate the key rows of all layers in place; copy -> K and V rows of all
+// layers from the refreshed buffer.  Layers are unrolled by 4 for memory-level parallelism.
+template <typename T, int TH, int TD>
+__global__ void __launch_bounds__(kGatherThreads) kv_gather_paged(const __grid_constant__ KvParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int VE = Vec<T>::N;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int H = TH > 0 ? TH : P.H;
+  const int D = TD > 0 ? TD : P.D;
+  const int half = D / 2, vph = half / VE, upr = H * vph;
+  const int rowb = H * D * static_cast<int>(sizeof(T));
+  float2* tab = reinterpret_cast<float2*>(smem) + wib * (P.D / 2);  // this warp's (cos, sin) table
+  const int* pref = ws_prefix(P);
+  const long long V = __ldg(pref + P.n_streams);
+  const long long nwarps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const long long gw = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + wib;
+  long long it = V * gw / nwarps;
+  const long long it1 = V * (gw + 1) / nwarps;
+  if (it >= it1) return;
+  int sidx = 0;
+  {
+    int lo = 0, hi = P.n_streams;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(pref + mid) <= it) lo = mid; else hi = mid;
+    }
+    sidx = lo;
+  }
+  int cur = -1;
+  const long long plane = P.cap * rowb;       // bytes of one (layer, K|V) plane of the pool
+  const long long rplane = P.rcap * rowb;     // ... of the refreshed buffer
+  unsigned char* pl = nullptr;
+  const unsigned char* rf = nullptr;
+  const MoveEntry* mv = nullptr;
+  for (; it < it1; ++it) {
+    while (__ldg(pref + sidx + 1) <= it) ++sidx;
+    if (sidx != cur) {
+      cur = sidx;
+      pl = static_cast<unsigned char*>(P.pool[sidx]);
+      rf = P.has_refreshed ? static_cast<const unsigned char*>(P.refreshed[sidx]) : nullptr;
+      mv = stream_moves(P, sidx);
+      const float2* g = reinterpret_cast<const float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
+      __syncwarp();
+      for (int i = lane; i < P.D / 2; i += 32) tab[i] = g[i];
+      __syncwarp();
+    }
+    const int p = static_cast<int>(it - __ldg(pref + sidx));
+    const MoveEntry me = mv[p];
+    if (me.src == -2 || me.slot < 0) continue;
+    if (me.src == -1) {
+      // Eq. 5 in place on the key rows (plane 2l) of every layer
+      unsigned char* base = pl + (long long)me.slot * rowb;
+      if (P.vec_rot && P.vec_copy) {
+        const int total = upr;  // units per row
+        for (int l0 = 0; l0 < P.L; l0 += 4) {
+          for (int e = lane; e < total; e += 32) {
+            const int h = e / vph, j = e - h * vph;
+            const int off1 = (h * D + j * VE) * static_cast<int>(sizeof(T));
+            const int off2 = off1 + half * static_cast<int>(sizeof(T));
+            uint4 a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (l0 + u < P.L) {
+                unsigned char* r = base + (long long)(2 * (l0 + u)) * plane;
+                a[u] = *reinterpret_cast<const uint4*>(r + off1);
+                b[u] = *reinterpret_cast<const uint4*>(r + off2);
+              }
+            }
+            float c[VE], sn[VE];
+#pragma unroll
+            for (int v = 0; v < VE; ++v) {
+              const float2 cs2 = tab[j * VE + v];
+              c[v] = cs2.x;
+              sn[v] = cs2.y;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (l0 + u < P.L) {
+                if constexpr (sizeof(T) == 2) rot8_bf16_pack(a[u], b[u], c, sn);
+                else rot4_f32(a[u], b[u], c, sn);
+                unsigned char* r = base + (long long)(2 * (l0 + u)) * plane;
+                *reinterpret_cast<uint4*>(r + off1) = a[u];
+                *reinterpret_cast<uint4*>(r + off2) = b[u];
+              }
+            }
+          }
+        }
+      } else {
+        for (int l = 0; l < P.L; ++l) {
+          T* r = reinterpret_cast<T*>(base + (long long)(2 * l) * plane);
+          for (int e = lane; e < H * half; e += 32) {
+            const int h = e / half, i = e - h * half;
+            float x1, x2;
+            if constexpr (sizeof(T) == 2) {
+              x1 = __uint_as_float(static_cast<uint32_t>(r[h * D + i]) << 16);
+              x2 = __uint_as_float(static_cast<uint32_t>(r[h * D + i + half]) << 16);
+            } else {
+              x1 = r[h * D + i];
+              x2 = r[h * D + i + half];
+            }
+            const float2 cs2 = tab[i];
+            const float y1 = __fmaf_rn(x1, cs2.x, -__fmul_rn(x2, cs2.y));
+            const float y2 = __fmaf_rn(x2, cs2.x, __fmul_rn(x1, cs2.y));
+            if constexpr (sizeof(T) == 2) {
+              r[h * D + i] = static_cast<T>(cs::f32_to_bf16_rne(y1));
+              r[h * D + i + half] = static_cast<T>(cs::f32_to_bf16_rne(y2));
+            } else {
+              r[h * D + i] = y1;
+              r[h * D + i + half] = y2;
+            }
+          }
+        }
+      }
+    } else {
+      // refreshed rows -> slot, K and V of every layer
+      unsigned char* dst = pl + (long long)me.slot * rowb;
+      const unsigned char* src = rf + (long long)me.src * rowb;
+      if (P.vec_copy) {
+        const int n16 = rowb / 16;
+        for (int l0 = 0; l0 < 2 * P.L; l0 += 4) {
+          for (int e = lane; e < n16; e += 32) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (l0 + u < 2 * P.L) v[u] = cs::ld_nc_v4(src + (long long)(l0 + u) * rplane + e * 16);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (l0 + u < 2 * P.L) *reinterpret_cast<uint4*>(dst + (long long)(l0 + u) * plane + e * 16) = v[u];
+          }
+        }
+      } else {
+        for (int l = 0; l < 2 * P.L; ++l) {
+          const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src + (long long)l * rplane);
+          uint32_t* d4 = reinterpret_cast<uint32_t*>(dst + (long long)l * plane);
+          for (int e = lane; e < rowb / 4; e += 32) d4[e] = s4[e];
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 size_t cs_kv_workspace_bytes(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams) {
@@ -751,14 +1176,11 @@ size_t cs_kv_workspace_bytes(const cs_kv_desc* kv, const cs_window* win, int32_t
   return 16 + stride * static_cast<size_t>(n_streams) + 4 * (static_cast<size_t>(n_streams) + 1);
 }
 
-int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
-                         const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
-                         const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
-                         int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens,
-                         void* workspace, size_t workspace_bytes, unsigned long long* counters, int32_t* status,
-                         cudaStream_t stream) {
-  (void)workspace_bytes;
-  KvParams P{};
+static void fill_params(KvParams& P, const cs_grid* g, const cs_kv_desc* kv, const cs_window* win,
+                        int32_t n_streams, const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                        const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
+                        int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens, void* workspace,
+                        unsigned long long* counters, int32_t* status) {
   P.grid_w = g->grid_w;
   P.grid_h = g->grid_h;
   P.G = g->group;
@@ -802,6 +1224,19 @@ int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window
   for (int i = 0; i < kv->head_dim / 2; ++i)
     P.inv_freq[i] = pow(kv->rope_base, -2.0 * static_cast<double>(i) / static_cast<double>(kv->head_dim));
 
+}
+
+int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                         const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
+                         const void* const* old_cache, void* const* new_cache, const void* const* refreshed,
+                         int64_t token_cap, uint8_t* disposition, int32_t* p_old, int32_t* n_tokens,
+                         void* workspace, size_t workspace_bytes, unsigned long long* counters, int32_t* status,
+                         cudaStream_t stream) {
+  (void)workspace_bytes;
+  KvParams P{};
+  fill_params(P, g, kv, win, n_streams, keep_mask_ring, frame_type_ring, old_cache, new_cache, refreshed, token_cap,
+              disposition, p_old, n_tokens, workspace, counters, status);
+  const size_t max_seg = static_cast<size_t>(P.max_seg);
   const int lo = win->step >= 1 ? (win->step - 1) * win->stride : 0;
   const int nfr = win->step * win->stride + win->window - lo;
   const size_t plan_smem = static_cast<size_t>(nfr) * P.nw * 4;
@@ -845,6 +1280,61 @@ int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window
     if (kv->dtype == CS_BF16) kv_gather_ldg<uint16_t, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
     else kv_gather_ldg<float, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
   }
+  if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+  return CS_OK;
+}
+
+static size_t paged_stride(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, long long* mv_off,
+                           int* max_tok) {
+  const long long groups = static_cast<long long>(g->grid_w / g->group) * (g->grid_h / g->group);
+  const long long mt = static_cast<long long>(win->window) * groups + kv->n_prompt;
+  size_t off = sizeof(KvHdr) + sizeof(KvSeg) * (static_cast<size_t>(win->window) + 1) +
+               8 * static_cast<size_t>(kv->head_dim / 2);
+  off = (off + 15) & ~static_cast<size_t>(15);
+  if (mv_off) *mv_off = static_cast<long long>(off);
+  if (max_tok) *max_tok = static_cast<int>(mt);
+  size_t stride = off + sizeof(MoveEntry) * static_cast<size_t>(mt);
+  return (stride + 15) & ~static_cast<size_t>(15);
+}
+
+size_t cs_kv_paged_workspace_bytes(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win,
+                                   int32_t n_streams) {
+  const size_t stride = paged_stride(g, kv, win, nullptr, nullptr);
+  return 16 + stride * static_cast<size_t>(n_streams) + 4 * (static_cast<size_t>(n_streams) + 1);
+}
+
+int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
+                               const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring, void* const* pool,
+                               const int32_t* slot_old, int32_t* slot_new, int64_t slot_cap,
+                               const void* const* refreshed, int64_t token_cap, uint8_t* disposition,
+                               int32_t* p_old, int32_t* n_tokens, void* workspace, unsigned long long* counters,
+                               int32_t* status, cudaStream_t stream) {
+  KvParams P{};
+  fill_params(P, g, kv, win, n_streams, keep_mask_ring, frame_type_ring, nullptr, nullptr, refreshed, token_cap,
+              disposition, p_old, n_tokens, workspace, counters, status);
+  P.pool = pool;
+  P.slot_old = slot_old;
+  P.slot_new = slot_new;
+  P.slot_cap = slot_cap;
+  P.ws_stride = static_cast<long long>(paged_stride(g, kv, win, &P.mv_off, &P.max_tok));
+  P.prefix_mode = 1;
+  const int lo = win->step >= 1 ? (win->step - 1) * win->stride : 0;
+  const int nfr = win->step * win->stride + win->window - lo;
+  const long long cw = (kv->capacity + 31) / 32;
+  const size_t plan_smem = static_cast<size_t>(nfr) * P.nw * 4 + static_cast<size_t>(cw) * 4 +
+                           static_cast<size_t>(cw + 1) * 4;
+  if (plan_smem > 160 * 1024) return CS_ERR_UNSUPPORTED;
+  if (cs_set_smem_attr(reinterpret_cast<const void*>(kv_plan_paged), 10, 160 * 1024)) return CS_ERR_CUDA;
+  kv_plan_paged<<<n_streams, kPlanThreads, plan_smem, stream>>>(P);
+  if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+  kv_prefix<<<1, 1024, 0, stream>>>(P);
+  if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+  const int grid = cs_num_sms() * 4;
+  const size_t gsmem = static_cast<size_t>(kGatherThreads / 32) * 8 * static_cast<size_t>(kv->head_dim / 2);
+  const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
+  if (qwen) kv_gather_paged<uint16_t, 4, 128><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  else if (kv->dtype == CS_BF16) kv_gather_paged<uint16_t, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  else kv_gather_paged<float, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
 }

@@ -530,3 +530,131 @@ def test_pipeline_end_to_end_c4_shape(abi, ref):
             fb = (b[:, 0, :nt].astype(np.uint32) << 16).view(np.float32)
             assert np.abs(fa - fb).max() <= 1e-2
     assert int(pipe.status.item()) == 0
+
+
+# ------------------------------------------------------------------------------------------------------------
+# kv_refresh_paged (NEXT-1: in place, slot maps)
+# ------------------------------------------------------------------------------------------------------------
+def run_paged_both(abi, ref, g, kv, win, mring, tring, pools_d, slot_old_h, slot_cap, ref_d, token_cap):
+    S = mring.shape[0]
+    pools_h = [_host_cache(t).copy() for t in pools_d]
+    ref_h = [_host_cache(t) for t in ref_d] if ref_d is not None else None
+    m_d = torch.from_numpy(np.ascontiguousarray(mring).view(np.int32)).to(DEV)
+    t_d = torch.from_numpy(np.ascontiguousarray(tring)).to(DEV)
+    so_d = torch.from_numpy(slot_old_h).to(DEV) if slot_old_h is not None else None
+    sn_d = torch.full((S, slot_cap), -7, dtype=torch.int32, device=DEV)
+    disp = torch.full((S, token_cap), 9, dtype=torch.uint8, device=DEV)
+    pold = torch.full((S, token_cap), -9, dtype=torch.int32, device=DEV)
+    ntok = torch.zeros(S, 4, dtype=torch.int32, device=DEV)
+    ws = torch.empty(abi.kv_paged_workspace_size(g, kv, win, S), dtype=torch.uint8, device=DEV)
+    cnt = torch.zeros(16, dtype=torch.int64, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    abi.codecsight_kv_refresh_paged(g, kv, win, S, m_d, t_d, abi.ptr_array(pools_d, DEV), so_d, sn_d, slot_cap,
+                                    abi.ptr_array(ref_d, DEV) if ref_d is not None else None, token_cap, disp, pold,
+                                    ntok, ws, cnt, st)
+    o = ref.kv_refresh_paged(g, kv, win, mring, tring, pools_h, slot_old_h, slot_cap, ref_h, token_cap)
+    torch.cuda.synchronize()
+    assert int(st.item()) == o["status"]
+    assert (ntok.cpu().numpy() == o["n_tokens"]).all()
+    assert (cnt.cpu().numpy().view(np.uint64) == o["counters"]).all(), (cnt.cpu().numpy(), o["counters"])
+    sn = sn_d.cpu().numpy()
+    stats = {"not_bit_exact": 0, "max_diff": 0.0}
+    for s in range(S):
+        nt = min(int(o["n_tokens"][s, 0]) + kv["n_prompt"], token_cap)
+        assert (disp.cpu().numpy()[s, :nt] == o["disposition"][s, :nt]).all()
+        assert (pold.cpu().numpy()[s, :nt] == o["p_old"][s, :nt]).all()
+        nsl = min(int(o["n_tokens"][s, 0]) + kv["n_prompt"], slot_cap)
+        assert (sn[s, :nsl] == o["slot_new"][s, :nsl]).all()
+        a, b = _host_cache(pools_d[s]), pools_h[s]
+        # values and every row that is not a rotated key: bit-identical
+        assert (a[:, 1] == b[:, 1]).all()
+        if kv["dtype"] == 0:
+            fa = (a[:, 0].astype(np.uint32) << 16).view(np.float32)
+            fb = (b[:, 0].astype(np.uint32) << 16).view(np.float32)
+            tol = 1e-2
+        else:
+            fa, fb, tol = a[:, 0], b[:, 0], 1e-5
+        d = float(np.abs(fa - fb).max())
+        assert d <= tol, d
+        stats["max_diff"] = max(stats["max_diff"], d)
+        stats["not_bit_exact"] += int((a[:, 0] != b[:, 0]).sum())
+    return sn, o, stats
+
+
+@pytest.mark.parametrize("dtype", [1, 0])
+def test_paged_c1_windows(abi, ref, dtype):
+    """C1 streams of all 5 scene kinds, 14 consecutive windows, slot maps carried from step to step."""
+    cfg = synth.CONFIGS["C1"]
+    g = make_grid(448, 448)
+    w, s, ring = 8, 2, 10
+    base = synth.TOY_KV if dtype == 1 else dict(synth.QWEN_KV, layers=2)
+    cap = w * 256 + 32
+    kv = dict(base, capacity=cap + 64, refresh_capacity=cap, n_prompt=32)
+    S = 5
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(5)
+    dt = torch.bfloat16 if dtype == 0 else torch.float32
+    shape = (kv["layers"], 2, kv["capacity"], kv["kv_heads"], kv["head_dim"])
+    pools = [torch.randn(shape, generator=gen, device=DEV).to(dt) for _ in range(S)]
+    slot = None
+    tot = {"not_bit_exact": 0, "max_diff": 0.0}
+    for k in range(14):
+        mring, tring = stream_rings(ref, g, cfg, S, ring, k, w, s)
+        _, _, refr = make_caches(kv, S, gen)
+        sn, o, st = run_paged_both(abi, ref, g, kv, dict(window=w, stride=s, step=k, ring_frames=ring), mring, tring,
+                                   pools, slot, cap, refr, cap)
+        slot = sn
+        tot["not_bit_exact"] += st["not_bit_exact"]
+        tot["max_diff"] = max(tot["max_diff"], st["max_diff"])
+    print("paged C1", dtype, tot)
+
+
+def test_paged_c5_shape(abi, ref):
+    """C5 shape: 4K traffic masks, w=64, s=8, GOP 16, Qwen2-VL-7B rows (2 layers to bound the oracle), 2 streams,
+    windows 0 and 1."""
+    cfg = synth.CONFIGS["C5"]
+    g = make_grid(3840, 2160)
+    w, s, ring = 64, 8, 72
+    cap = w * 256 + 32
+    kv = dict(synth.QWEN_KV, layers=2, capacity=cap, refresh_capacity=13 * 256 + 32, n_prompt=32)
+    S = 2
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(6)
+    shape = (kv["layers"], 2, cap, 4, 128)
+    pools = [torch.randn(shape, generator=gen, device=DEV).to(torch.bfloat16) for _ in range(S)]
+    slot = None
+    for k in range(2):
+        mring, tring = stream_rings(ref, g, cfg, S, ring, k, w, s)
+        _, _, refr = make_caches(dict(kv, refresh_capacity=cap) if k == 0 else kv, S, gen)
+        sn, o, st = run_paged_both(abi, ref, g, dict(kv, refresh_capacity=cap) if k == 0 else kv,
+                                   dict(window=w, stride=s, step=k, ring_frames=ring), mring, tring, pools, slot, cap,
+                                   refr, cap)
+        slot = sn
+
+
+def test_paged_edge_cases(abi, ref):
+    cfg = synth.CONFIGS["C1"]
+    g = make_grid(448, 448)
+    w, s, ring = 8, 2, 10
+    S = 5
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(8)
+    mring, tring = stream_rings(ref, g, cfg, S, ring, 3, w, s)
+    win = dict(window=w, stride=s, step=3, ring_frames=ring)
+    cap = w * 256 + 32
+    rng = np.random.default_rng(2)
+    for kvb, slot_cap, tc, pool_cap, with_ref in [
+            (synth.TOY_KV, cap, cap, cap + 10, True),          # plain
+            (synth.TOY_KV, cap, cap, cap + 10, False),         # refreshed = NULL
+            (synth.TOY_KV, 300, 250, 400, True),               # small slot map / index / pool: CAPACITY
+            (dict(layers=3, kv_heads=1, head_dim=2, dtype=1, rope_base=1e4), cap, cap, cap, True),   # scalar paths
+            (dict(layers=2, kv_heads=2, head_dim=8, dtype=0, rope_base=1e6), cap, cap, cap, True)]:
+        kv = dict(kvb, capacity=pool_cap, refresh_capacity=min(cap, 900), n_prompt=32)
+        dt = torch.bfloat16 if kv["dtype"] == 0 else torch.float32
+        shape = (kv["layers"], 2, pool_cap, kv["kv_heads"], kv["head_dim"])
+        pools = [torch.randn(shape, generator=gen, device=DEV).to(dt) for _ in range(S)]
+        # an arbitrary permutation of slots for window k-1 (some out of range -> ORIGIN)
+        slot_old = np.stack([rng.permutation(pool_cap)[:slot_cap] for _ in range(S)]).astype(np.int32)
+        slot_old[0, 5] = pool_cap + 3
+        _, _, refr = make_caches(kv, S, gen)
+        run_paged_both(abi, ref, g, kv, win, mring, tring, pools, slot_old, slot_cap, refr if with_ref else None, tc)
