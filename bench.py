@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--kv-mode", default="paged", choices=["paged", "copy"],
+                    help="paged: codecsight_kv_refresh_paged (in place, NEXT-1); copy: out-of-place double buffer")
     ap.add_argument("--frame-layout", default="grouped", choices=["grouped", "planar"],
                     help="layout of the preprocessed model-input frames handed to compact (DESIGN.md §6)")
     return ap.parse_args()
@@ -56,13 +58,16 @@ def log(*a):
 # --------------------------------------------------------------------------------------------------------------
 # workload
 # --------------------------------------------------------------------------------------------------------------
-def workload(name: str, streams: int | None):
+def workload(name: str, streams: int | None, kv_mode: str = "paged"):
     cfg = dict(synth.CONFIGS[name])
     if cfg["kv"] is None and name != "C2":
         raise SystemExit(f"workload {name} has no KV shape")
     if name == "C5":
-        raise SystemExit("C5 (1,024 4K streams, w=64) needs the in-place / paged KV refresh (NEXT-1): 128 streams x "
-                         "2 out-of-place 941 MB caches exceed one GPU's 180 GB")
+        # BASELINE: 1,024 streams on 8 B200 -> 128 streams per GPU (weak scaling unit).  Out of place, 128 x 2 x
+        # 941 MB caches exceed 180 GB: C5 runs with the in-place / paged refresh only.
+        cfg["streams"] = 128
+        if kv_mode != "paged":
+            raise SystemExit("C5 needs --kv-mode paged (out-of-place caches do not fit one GPU)")
     if streams is not None:
         cfg["streams"] = streams
     return cfg
@@ -73,15 +78,16 @@ def step_frames(cfg, k):
     return (0, w) if k == 0 else ((k - 1) * s + w, s)
 
 
-def gen_metadata(cfg, global_ids, n_steps):
-    """Per-step MB metadata [S][n][rows][cols] for steps 0..n_steps-1 (each stream's scene evolves in time)."""
+def gen_metadata(cfg, global_ids, n_pool):
+    """MB metadata: entry 0 = the first window (w frames), entries 1..n_pool = stride steps (s frames each) that
+    the timed loop cycles through.  Each stream's scene evolves in time; the first window re-uses the pool's
+    frames (it is warm-up only)."""
     sw, sh = cfg["src"]
+    w, s = cfg["window"], cfg["stride"]
     gens = [synth.StreamGen(sw, sh, synth.scene_of(cfg, gid), synth.stream_seed(cfg, gid)) for gid in global_ids]
-    out = []
-    for k in range(n_steps):
-        _, n = step_frames(cfg, k)
-        out.append(np.stack([np.stack([gn.next_frame() for _ in range(n)]) for gn in gens]))
-    return out
+    pool = [np.stack([np.stack([gn.next_frame() for _ in range(s)]) for gn in gens]) for _ in range(n_pool)]
+    first = np.concatenate([pool[i % n_pool] for i in range(-(-w // s))], axis=1)[:, :w]
+    return [np.ascontiguousarray(first)] + pool
 
 
 class ClockSampler:
@@ -161,7 +167,7 @@ def ncu_traffic(kernel: str):
 # --------------------------------------------------------------------------------------------------------------
 # CPU oracle (baseline / reference arm)
 # --------------------------------------------------------------------------------------------------------------
-def oracle_sample(cfg, budget_s: float, max_steps: int = 64):
+def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "paged"):
     """Run the oracle, as it stands, on a bounded sample of the workload: whole stream-steps (score + compact +
     kv_refresh) of alternating streams, until ~budget_s seconds of single-threaded CPU work are spent."""
     import oracle.ref as ref
@@ -216,9 +222,15 @@ def oracle_sample(cfg, budget_s: float, max_steps: int = 64):
             new = np.zeros(shape, dtp)
             refr = np.zeros(rshape, dtp)
             win = dict(window=w, stride=s, step=k_meas, ring_frames=ring)
-            t0 = time.perf_counter()
-            ref.kv_refresh(g, kv, win, mring, tring, [old], [new], [refr], cap)
-            dt += time.perf_counter() - t0
+            if kv_mode == "paged":
+                slot_old = np.arange(cap, dtype=np.int32)[None]     # any valid slot map of window k-1
+                t0 = time.perf_counter()
+                ref.kv_refresh_paged(g, kv, win, mring, tring, [old], slot_old, cap, [refr], cap)
+                dt += time.perf_counter() - t0
+            else:
+                t0 = time.perf_counter()
+                ref.kv_refresh(g, kv, win, mring, tring, [old], [new], [refr], cap)
+                dt += time.perf_counter() - t0
         t_total += dt
         frames_done += s
         steps_done += 1
@@ -231,10 +243,10 @@ def run_reference(args, cfg, rank, world):
         return
     per_step = max(1.0, args.cpu_seconds / max(1, args.steps))
     for _ in range(args.warmup):
-        oracle_sample(cfg, 0.0, max_steps=1)
+        oracle_sample(cfg, 0.0, max_steps=1, kv_mode=args.kv_mode)
     tot = dict(seconds=0.0, frames=0, stream_steps=0)
     for _ in range(args.steps):
-        r = oracle_sample(cfg, per_step, max_steps=4)
+        r = oracle_sample(cfg, per_step, max_steps=4, kv_mode=args.kv_mode)
         for kk in tot:
             tot[kk] += r[kk]
     fps = tot["frames"] / tot["seconds"]
@@ -271,14 +283,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     global_ids = shard.stream_ids(rank, world, S)
     kvb = cfg["kv"]
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
-    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout)
+    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
+                    kv_mode=args.kv_mode, compact_chunk=s)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     pipe.init_cache_fill(gen)
     t_setup = time.time()
     # metadata pool: step 0 (w frames) + `pool` stride steps, cycled during the run
-    n_pool = max(1, min(args.pool, args.warmup + args.steps))
-    md = gen_metadata(cfg, global_ids, n_pool + 1)
+    n_pool = max(1, min(args.pool if cfg["src"][0] < 3000 else min(args.pool, 3), args.warmup + args.steps))
+    md = gen_metadata(cfg, global_ids, n_pool)
     mb_host = [torch.from_numpy(m.view(np.uint8).copy()).pin_memory() for m in md]
     mb_dev = [t.to(dev) for t in mb_host]
     # frames: S*s distinct model-input frames [3][448][448] bf16 (pointer array aliases them for the first window)
@@ -312,24 +325,17 @@ def run_ours(args, cfg, rank, world, local_rank):
         ptrs = ptr_w if k == 0 else ptr_s
         if timed:
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            pipe.type_ring[:, pipe.ring_slot(k):pipe.ring_slot(k) + n].copy_(types_dev[k], non_blocking=True)
-            e[0].record(stream)
             off = pipe.ring_slot(k)
+            pipe.type_ring[:, off:off + n].copy_(types_dev[k], non_blocking=True)
+            e[0].record(stream)
             abi.codecsight_score_patches(g, S, n, md_for(k), pipe.type_ring[:, off:], pipe.mask_ring[:, off:],
                                          pipe.ring, pipe.gop_state, None, pipe.kept_count[:, :n], pipe.counters,
                                          pipe.status)
             e[1].record(stream)
-            abi.codecsight_compact(g, S, n, pipe.mask_ring[:, off:], pipe.ring, fidx_dev[k], ptrs, pipe.capacity,
-                                   pipe.packed, pipe.pos_ids, pipe.src_index, pipe.frame_offsets[:S * n + 1],
-                                   pipe.counters, pipe.status, frame_layout=layout)
+            pipe.compact(k, n, off, ptrs, fidx_dev[k])
             e[2].record(stream)
             if pipe.kv is not None:
-                win = dict(window=w, stride=s, step=k, ring_frames=pipe.ring)
-                old, new = pipe.cache_ptrs[pipe.cur], pipe.cache_ptrs[1 - pipe.cur]
-                abi.codecsight_kv_refresh(g, pipe.kv, win, S, pipe.mask_ring, pipe.type_ring, old, new,
-                                          pipe.refreshed_ptrs if k >= 1 else None, pipe.token_cap, pipe.disposition,
-                                          pipe.p_old, pipe.n_tokens, pipe.workspace, pipe.counters, pipe.status)
-                pipe.cur = 1 - pipe.cur
+                pipe.kv_refresh(k)
             e[3].record(stream)
             ev["score"].append((e[0], e[1]))
             ev["compact"].append((e[1], e[2]))
@@ -454,7 +460,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg["name"], "streams_per_gpu": S, "streams_total": S * world, "src": list(cfg["src"]),
                    "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": 0.25, "alpha": 0.0,
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
-                   "frame_layout": args.frame_layout,
+                   "frame_layout": args.frame_layout, "kv_mode": args.kv_mode,
                    "parallelism": f"stream-shard x{world}",
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
                          "see per-step bytes)"},
@@ -470,9 +476,13 @@ def run_ours(args, cfg, rank, world, local_rank):
                             "new": int(c[abi.CNT_TOK_NEW]) // K},
         "near_tau_patches": int(c[abi.CNT_NEAR_TAU]),
         "status": status,
-        "roofline": ({"bound": "hbm", "kernel": "codecsight_kv_refresh (kv_plan + kv_prefix + kv_gather_tma)",
+        "kv_mode": args.kv_mode,
+        "roofline": ({"bound": "hbm", "kernel": ("codecsight_kv_refresh_paged (kv_plan_paged + kv_prefix + "
+                                                 "kv_gather_paged)") if args.kv_mode == "paged" else
+                      "codecsight_kv_refresh (kv_plan + kv_prefix + kv_gather_tma)",
                       "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                      "frac": achieved / peak, "traffic": ncu_traffic("kv_gather"),
+                      "frac": achieved / peak,
+                      "traffic": ncu_traffic("kv_gather_paged" if args.kv_mode == "paged" else "kv_gather"),
                       "algorithmic_bytes_per_launch": kv_bytes_launch} if kvb else
                      {"bound": "hbm", "kernel": "codecsight_compact (compact_scan + compact_gather)",
                       "achieved": cmp_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
@@ -488,7 +498,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                       "h2d_bytes_per_step": e2e["h2d"] * world, "d2h_bytes_per_step": e2e["d2h"] * world}
     if not args.no_cpu_baseline:
         log("[rank 0] timing the CPU oracle on a bounded sample ...")
-        r = oracle_sample(cfg, args.cpu_seconds)
+        r = oracle_sample(cfg, args.cpu_seconds, kv_mode=args.kv_mode)
         out["cpu_baseline"] = {"value": r["frames"] / r["seconds"], "unit": "frames/s", "cores": 1, "kind": "oracle",
                                "sample": f"{r['stream_steps']} whole stream-steps (window k=4: {s} new frames + "
                                          f"KV refresh) of streams {r['scenes'][:4]}..., single-threaded C oracle, "
@@ -501,7 +511,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = workload(args.workload, args.streams)
+    cfg = workload(args.workload, args.streams, args.kv_mode)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

@@ -6,7 +6,8 @@ One ``Pipeline`` owns, for its shard of camera streams, everything the path keep
   gop_state   [S][grid_words + 1]      GOP accumulation state
   mask_ring   [S][ring][grid_words]    keep masks of the last ring = w + s frames (decode-once)
   type_ring   [S][ring]                I/P frame types
-  caches      2 x S buffers [L][2][capacity][H][D] (window k-1 / window k, swapped every step)
+  caches      kv_mode "copy":  2 x S buffers [L][2][capacity][H][D] (window k-1 / window k, swapped every step)
+              kv_mode "paged": S row pools [L][2][capacity][H][D] updated in place + 2 x [S][capacity] slot maps
   refreshed   S buffers [L][2][refresh_capacity][H][D] (rows the prefill recomputes: anchors, new, prompt)
 
 ``step(k, ...)`` enqueues, on the current CUDA stream and without any host synchronisation:
@@ -25,9 +26,13 @@ from . import _abi as abi
 class Pipeline:
     def __init__(self, grid: dict, n_streams: int, window: int, stride: int, gop: int, kv: dict | None,
                  n_prompt: int = 0, device=None, want_score: bool = False, packed_capacity: int | None = None,
-                 with_refreshed: bool = True, frame_layout: int = abi.CS_LAYOUT_PLANAR):
+                 with_refreshed: bool = True, frame_layout: int = abi.CS_LAYOUT_PLANAR, kv_mode: str = "copy",
+                 compact_chunk: int | None = None):
         self.g = dict(grid)
         self.frame_layout = frame_layout
+        self.kv_mode = kv_mode
+        # frames per compaction call (the first window's w frames are compacted s at a time when set)
+        self.compact_chunk = compact_chunk
         self.S, self.w, self.s, self.gop = n_streams, window, stride, gop
         self.ring = window + stride
         self.dev = torch.device(device if device is not None else "cuda")
@@ -45,7 +50,8 @@ class Pipeline:
         self.status = torch.zeros(1, dtype=torch.int32, device=d)
         # packed ViT input: enough rows for the first window (every patch kept)
         p = grid["patch"]
-        self.capacity = packed_capacity if packed_capacity is not None else S * window * self.np
+        chunk = compact_chunk if compact_chunk is not None else window
+        self.capacity = packed_capacity if packed_capacity is not None else S * chunk * self.np
         self.packed = torch.empty(self.capacity, 3 * p * p, dtype=torch.bfloat16, device=d)
         self.pos_ids = torch.empty(self.capacity, 3, dtype=torch.int32, device=d)
         self.src_index = torch.empty(self.capacity, dtype=torch.int32, device=d)
@@ -60,8 +66,11 @@ class Pipeline:
             self.kv = dict(kv, capacity=cap, refresh_capacity=rcap, n_prompt=n_prompt)
             dt = torch.bfloat16 if kv["dtype"] == abi.CS_BF16 else torch.float32
             shape = (kv["layers"], 2, cap, kv["kv_heads"], kv["head_dim"])
-            self.caches = [[torch.empty(shape, dtype=dt, device=d) for _ in range(S)] for _ in range(2)]
+            n_sets = 1 if kv_mode == "paged" else 2
+            self.caches = [[torch.empty(shape, dtype=dt, device=d) for _ in range(S)] for _ in range(n_sets)]
             self.cache_ptrs = [abi.ptr_array(c, d) for c in self.caches]
+            if kv_mode == "paged":
+                self.slots = [torch.full((S, cap), -1, dtype=torch.int32, device=d) for _ in range(2)]
             rshape = (kv["layers"], 2, rcap, kv["kv_heads"], kv["head_dim"])
             self.refreshed = [torch.empty(rshape, dtype=dt, device=d) for _ in range(S)] if with_refreshed else None
             self.refreshed_ptrs = abi.ptr_array(self.refreshed, d) if with_refreshed else None
@@ -69,7 +78,9 @@ class Pipeline:
             self.disposition = torch.zeros(S, cap, dtype=torch.uint8, device=d)
             self.p_old = torch.zeros(S, cap, dtype=torch.int32, device=d)
             self.n_tokens = torch.zeros(S, 4, dtype=torch.int32, device=d)
-            nbytes = abi.kv_workspace_size(self.kv, dict(window=window, stride=stride, step=1, ring_frames=ring), S)
+            win1 = dict(window=window, stride=stride, step=1, ring_frames=ring)
+            nbytes = (abi.kv_paged_workspace_size(grid, self.kv, win1, S) if kv_mode == "paged"
+                      else abi.kv_workspace_size(self.kv, win1, S))
             self.workspace = torch.empty((nbytes + 15) // 16 * 16, dtype=torch.uint8, device=d)
         self.cur = 0  # which cache set holds window k-1
 
@@ -106,22 +117,51 @@ class Pipeline:
         abi.codecsight_score_patches(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:], self.ring,
                                      self.gop_state, None if self.score is None else self.score[:, :n],
                                      self.kept_count[:, :n], self.counters, self.status, stream)
-        fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
-        abi.codecsight_compact(g, self.S, n, self.mask_ring[:, off:], self.ring, fi, frame_ptrs, self.capacity,
-                               self.packed, self.pos_ids, self.src_index, self.frame_offsets[: self.S * n + 1],
-                               self.counters, self.status, stream, frame_layout=self.frame_layout)
+        self.compact(k, n, off, frame_ptrs, frame_index, stream)
         if self.kv is not None and do_kv:
-            win = dict(window=self.w, stride=self.s, step=k, ring_frames=self.ring)
+            self.kv_refresh(k, use_refreshed, stream)
+
+    def compact(self, k, n, off, frame_ptrs, frame_index=None, stream=None):
+        """codecsight_compact of the step's n new frames, in chunks of compact_chunk frames when set (the packed
+        buffer then holds one chunk at a time, as a streaming ViT would consume it)."""
+        g = self.g
+        fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
+        c = n if self.compact_chunk is None else min(n, self.compact_chunk)
+        for j0 in range(0, n, c):
+            nj = min(c, n - j0)
+            if nj == n:
+                fptr, fidx = frame_ptrs, fi
+            else:  # frames / indices of the chunk: per stream the slots j0..j0+nj-1 of [S][n]
+                fptr = frame_ptrs.view(self.S, n)[:, j0:j0 + nj].contiguous().view(-1)
+                fidx = fi.view(self.S, n)[:, j0:j0 + nj].contiguous().view(-1)
+            abi.codecsight_compact(g, self.S, nj, self.mask_ring[:, off + j0:], self.ring, fidx, fptr,
+                                   self.capacity, self.packed, self.pos_ids, self.src_index,
+                                   self.frame_offsets[: self.S * nj + 1], self.counters, self.status, stream,
+                                   frame_layout=self.frame_layout)
+
+    def kv_refresh(self, k, use_refreshed=None, stream=None):
+        g = self.g
+        win = dict(window=self.w, stride=self.s, step=k, ring_frames=self.ring)
+        use_r = (k >= 1) if use_refreshed is None else use_refreshed
+        ref = self.refreshed_ptrs if use_r else None
+        if self.kv_mode == "paged":
+            so, sn = self.slots[self.cur], self.slots[1 - self.cur]
+            abi.codecsight_kv_refresh_paged(g, self.kv, win, self.S, self.mask_ring, self.type_ring,
+                                            self.cache_ptrs[0], so if k >= 1 else None, sn, self.token_cap, ref,
+                                            self.token_cap, self.disposition, self.p_old, self.n_tokens,
+                                            self.workspace, self.counters, self.status, stream)
+        else:
             old, new = self.cache_ptrs[self.cur], self.cache_ptrs[1 - self.cur]
-            use_r = (k >= 1) if use_refreshed is None else use_refreshed
-            abi.codecsight_kv_refresh(g, self.kv, win, self.S, self.mask_ring, self.type_ring, old, new,
-                                      self.refreshed_ptrs if use_r else None, self.token_cap, self.disposition,
-                                      self.p_old, self.n_tokens, self.workspace, self.counters, self.status, stream)
-            self.cur = 1 - self.cur
+            abi.codecsight_kv_refresh(g, self.kv, win, self.S, self.mask_ring, self.type_ring, old, new, ref,
+                                      self.token_cap, self.disposition, self.p_old, self.n_tokens, self.workspace,
+                                      self.counters, self.status, stream)
+        self.cur = 1 - self.cur
 
     def kernel_launches_per_step(self, k: int) -> int:
-        """Kernels of this library launched by one step (score 1, compact 2, kv_refresh 3)."""
-        n = 1 + (2 if self.S > 0 else 1)
+        """Kernels of this library launched by one step (score 1, compact 2 per chunk, kv_refresh 3)."""
+        _, nf = self.new_frames(k)
+        c = nf if self.compact_chunk is None else min(nf, self.compact_chunk)
+        n = 1 + 2 * ((nf + c - 1) // c)
         if self.kv is not None:
             n += 3
         return n

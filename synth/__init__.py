@@ -156,18 +156,23 @@ class StreamGen:
             x, y, w, h, vx, vy = o
             if vx == 0.0 and vy == 0.0:
                 continue
-            inside = (np.abs(self.cx - x) <= w / 2) & (np.abs(self.cy - y) <= h / 2)
-            k = int(inside.sum())
-            if k == 0:
+            # MBs whose centre (16 i + 8, 16 j + 8) lies inside the box: a slice of the MB grid
+            m = self.mb
+            i0 = max(0, int(np.ceil((x - w / 2 - m / 2) / m)))
+            i1 = min(self.cols - 1, int(np.floor((x + w / 2 - m / 2) / m)))
+            j0 = max(0, int(np.ceil((y - h / 2 - m / 2) / m)))
+            j1 = min(self.rows - 1, int(np.floor((y + h / 2 - m / 2) / m)))
+            if i1 < i0 or j1 < j0:
                 continue
-            jit = (r.random((k, 2)) < 0.2) * r.choice(np.array([-1, 1]), size=(k, 2))
-            rec["mvx"][inside] = np.clip(np.round(4 * vx) + jit[:, 0], -32768, 32767).astype(np.int16)
-            rec["mvy"][inside] = np.clip(np.round(4 * vy) + jit[:, 1], -32768, 32767).astype(np.int16)
-            rec["sad"][inside] = (256 * r.uniform(8, 40, size=k)).astype(np.uint16)
-            intra = r.random(k) < 0.02
-            t = np.full(k, MB_INTER, np.uint8)
-            t[intra] = MB_INTRA
-            rec["type"][inside] = t
+            sl = rec[j0:j1 + 1, i0:i1 + 1]
+            shp = sl.shape
+            jit = (r.random(shp + (2,)) < 0.2) * r.choice(np.array([-1, 1]), size=shp + (2,))
+            sl["mvx"] = np.clip(np.round(4 * vx) + jit[..., 0], -32768, 32767).astype(np.int16)
+            sl["mvy"] = np.clip(np.round(4 * vy) + jit[..., 1], -32768, 32767).astype(np.int16)
+            sl["sad"] = (256 * r.uniform(8, 40, size=shp)).astype(np.uint16)
+            t = np.full(shp, MB_INTER, np.uint8)
+            t[r.random(shp) < 0.02] = MB_INTRA
+            sl["type"] = t
         if "p_cut" in sc and r.random() < sc["p_cut"]:
             cut = r.random((self.rows, self.cols)) < 0.85
             rec["type"][cut] = MB_INTRA
