@@ -34,10 +34,16 @@ struct KvHdr {
   int pad;
 };
 struct KvSeg {
-  int p_new;  // first row in the new cache
-  int len;    // rows (already clamped to the capacities)
-  int kind;   // SEG_COPY (refreshed rows) | SEG_REUSE (old cache, K rotated, V copied)
-  int src;    // first source row (old cache row for REUSE, refreshed-buffer row for COPY)
+  int p_new;  // first token (p_new) of the run
+  int len;    // tokens (already clamped to the capacities)
+  int kind;   // SEG_COPY (refreshed rows) | SEG_REUSE (old cache, K rotated, V copied) | SEG_SKIP
+  int src;    // first source row (old cache / pool row for REUSE, refreshed-buffer row for COPY)
+  int dst;    // first destination row (= p_new out of place; the pool slot in the paged variant)
+  int pad[3];  // 32 B: keeps the cos/sin table that follows the run list 16-B aligned (TMA source)
+};
+static_assert(sizeof(KvSeg) == 32, "KvSeg must stay 32 bytes");
+struct PlanSeg {  // per-frame index segment inside the plan kernels (shared memory)
+  int p_new, len, kind, src;
 };
 
 struct KvParams {
@@ -66,6 +72,7 @@ struct KvParams {
   long long slot_cap;
   int max_tok;      // w * groups + n_prompt: entries of the per-stream move list
   int prefix_mode;  // kv_prefix items: 0 = (stream, 128-row block, layer, K|V), 1 = tokens
+  int paged;        // 1: REUSE runs rotate keys in place and leave values alone
   long long mv_off;  // byte offset of the move list inside a stream's workspace slice
   double inv_freq[cs::kMaxHeadDim / 2];  // base^(-2i/D), computed on the host
 };
@@ -77,7 +84,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_n[cs::kMaxWindowPlusStride];       // tokens per frame of [lo, hi)
   __shared__ uint8_t s_t[cs::kMaxWindowPlusStride];   // frame types
-  __shared__ KvSeg s_seg[kMaxSeg];                    // index segments (unclamped), one per frame + prompt
+  __shared__ PlanSeg s_seg[kMaxSeg];                  // index segments (unclamped), one per frame + prompt
   __shared__ int s_pold[kMaxSeg];                     // p_old of the first token of the segment (-1: NEW)
   __shared__ int s_disp[kMaxSeg];
   __shared__ int s_nseg, s_dp;
@@ -193,6 +200,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
         wseg[nout].len = static_cast<int>(valid);
         wseg[nout].kind = kind;
         wseg[nout].src = static_cast<int>(src);
+        wseg[nout].dst = static_cast<int>(pn);
         ++nout;
         moved += valid;
       }
@@ -544,7 +552,14 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
       g.nc = static_cast<unsigned char*>(P.new_cache[g.sidx]);
       g.oc = P.k >= 1 ? static_cast<const unsigned char*>(P.old_cache[g.sidx]) : nullptr;
       g.rf = P.has_refreshed ? static_cast<const unsigned char*>(P.refreshed[g.sidx]) : nullptr;
-      g.seg = 0;
+      // first run that ends after the block start (runs are sorted by p_new and disjoint)
+      int lo = 0, hi = g.nseg;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const KvSeg m = g.segs[mid];
+        if (m.p_new + m.len <= g.a) lo = mid + 1; else hi = mid;
+      }
+      g.seg = lo;
       g.x = g.a;
       g.active = 1;
     }
@@ -555,14 +570,15 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
         break;
       }
       const int x0 = max(g.x, sg.p_new), x1 = min(g.b, sg.p_new + sg.len);
-      if (x0 >= x1) {
+      if (x0 >= x1 || sg.kind == SEG_SKIP || (P.paged && sg.kind == SEG_REUSE && g.kv == 1)) {
         ++g.seg;
         continue;
       }
       const int n = min(cr, x1 - x0);
       const long long plane = static_cast<long long>(g.l * 2 + g.kv);
       const long long srow = sg.src + (x0 - sg.p_new);
-      d.dst = g.nc + (plane * P.cap + x0) * row_bytes;
+      const long long drow = sg.dst + (x0 - sg.p_new);
+      d.dst = g.nc + (plane * P.cap + drow) * row_bytes;
       d.bytes = static_cast<uint32_t>(n * row_bytes);
       d.rows = n;
       if (sg.kind == SEG_REUSE) {
@@ -812,7 +828,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_n[cs::kMaxWindowPlusStride];
   __shared__ uint8_t s_t[cs::kMaxWindowPlusStride];
-  __shared__ KvSeg s_seg[kMaxSeg];
+  __shared__ PlanSeg s_seg[kMaxSeg];
   __shared__ int s_pold[kMaxSeg];
   __shared__ int s_disp[kMaxSeg];
   __shared__ int s_nseg, s_dp, s_ntotal, s_p0, s_n_old, s_r0, s_st;
@@ -939,7 +955,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   unsigned long long rot = 0, cop = 0;
   // ---- surviving tokens (REUSE, ANCHOR) keep their slots; index outputs of every token ---------------------
   for (int i = warp; i < nseg; i += nwarp) {
-    const KvSeg sg = s_seg[i];
+    const PlanSeg sg = s_seg[i];
     const int d = s_disp[i], pold = s_pold[i];
     for (int t = lane; t < sg.len; t += 32) {
       const long long p = (long long)sg.p_new + t;
@@ -1008,6 +1024,47 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     me.src = ok ? static_cast<int>(r) : -2;
     cop += ok;
     if (p < P.max_tok) mv[p] = me;
+  }
+  // ---- runs for the bulk-copy gather: maximal token ranges with one action and consecutive slots (and
+  //      consecutive refreshed rows for copies); skipped tokens form SKIP runs so runs tile [0, n_total) -------
+  __syncthreads();  // move entries of every token written
+  {
+    __shared__ int s_cnt[kPlanThreads];
+    const int nmv = min(n_total, P.max_tok);
+    const int per = (nmv + blockDim.x - 1) / blockDim.x;
+    const int b = tid * per, e = min(nmv, b + per);
+    auto cls = [](const MoveEntry& m) { return (m.slot < 0 || m.src == -2) ? 0 : (m.src == -1 ? 1 : 2); };
+    auto starts = [&](int p) {
+      if (p == 0) return true;
+      const MoveEntry a = mv[p - 1], c = mv[p];
+      const int ca = cls(a), cc = cls(c);
+      if (ca != cc) return true;
+      if (cc == 0) return false;
+      if (c.slot != a.slot + 1) return true;
+      return cc == 2 && c.src != a.src + 1;
+    };
+    int cnt = 0;
+    for (int p = b; p < e; ++p) cnt += starts(p) ? 1 : 0;
+    s_cnt[tid] = cnt;
+    __syncthreads();
+    const int nruns = block_exclusive_scan(s_cnt, blockDim.x);
+    KvSeg* runs = reinterpret_cast<KvSeg*>(stream_ws(P, sidx) + sizeof(KvHdr));
+    int idx = s_cnt[tid];
+    for (int p = b; p < e; ++p) {
+      if (!starts(p)) continue;
+      const MoveEntry m = mv[p];
+      const int c = cls(m);
+      KvSeg r;
+      r.p_new = p;
+      r.len = 0;
+      r.kind = c == 0 ? SEG_SKIP : (c == 1 ? SEG_REUSE : SEG_COPY);
+      r.src = c == 2 ? m.src : m.slot;
+      r.dst = m.slot;
+      runs[idx++] = r;
+    }
+    __syncthreads();
+    for (int i = tid; i < nruns; i += blockDim.x) runs[i].len = (i + 1 < nruns ? runs[i + 1].p_new : nmv) - runs[i].p_new;
+    if (tid == 0) reinterpret_cast<KvHdr*>(stream_ws(P, sidx))->n_seg = nruns;
   }
   // ---- (cos, sin) of R(dp) ----------------------------------------------------------------------------------
   float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
@@ -1288,7 +1345,7 @@ static size_t paged_stride(const cs_grid* g, const cs_kv_desc* kv, const cs_wind
                            int* max_tok) {
   const long long groups = static_cast<long long>(g->grid_w / g->group) * (g->grid_h / g->group);
   const long long mt = static_cast<long long>(win->window) * groups + kv->n_prompt;
-  size_t off = sizeof(KvHdr) + sizeof(KvSeg) * (static_cast<size_t>(win->window) + 1) +
+  size_t off = sizeof(KvHdr) + sizeof(KvSeg) * (static_cast<size_t>(mt) + 1) +
                8 * static_cast<size_t>(kv->head_dim / 2);
   off = (off + 15) & ~static_cast<size_t>(15);
   if (mv_off) *mv_off = static_cast<long long>(off);
@@ -1317,7 +1374,13 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   P.slot_new = slot_new;
   P.slot_cap = slot_cap;
   P.ws_stride = static_cast<long long>(paged_stride(g, kv, win, &P.mv_off, &P.max_tok));
-  P.prefix_mode = 1;
+  P.max_seg = P.max_tok + 1;  // run list capacity (also locates the cos/sin table)
+  P.paged = 1;
+  P.old_cache = pool;  // REUSE runs read and write the same pool rows
+  P.new_cache = pool;
+  const long long row_bytes = static_cast<long long>(P.H) * P.D * P.esz;
+  const bool tma_ok = P.vec_rot && P.vec_copy && row_bytes <= kTmaChunk && (P.D % 4) == 0;
+  P.prefix_mode = tma_ok ? 0 : 1;
   const int lo = win->step >= 1 ? (win->step - 1) * win->stride : 0;
   const int nfr = win->step * win->stride + win->window - lo;
   const long long cw = (kv->capacity + 31) / 32;
@@ -1329,12 +1392,32 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   kv_prefix<<<1, 1024, 0, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
-  const int grid = cs_num_sms() * 4;
-  const size_t gsmem = static_cast<size_t>(kGatherThreads / 32) * 8 * static_cast<size_t>(kv->head_dim / 2);
   const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
-  if (qwen) kv_gather_paged<uint16_t, 4, 128><<<grid, kGatherThreads, gsmem, stream>>>(P);
-  else if (kv->dtype == CS_BF16) kv_gather_paged<uint16_t, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
-  else kv_gather_paged<float, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  if (tma_ok) {
+    const unsigned stage_bytes = kTmaChunk;
+    const unsigned tab_bytes = static_cast<unsigned>(((8 * (P.D / 2)) + 127) & ~127);
+    int nst = static_cast<int>((216u * 1024u) / (kWarpsPerGather * (stage_bytes + tab_bytes)));
+    if (nst > kMaxStages) nst = kMaxStages;
+    if (nst < 3) return CS_ERR_UNSUPPORTED;
+    const size_t smem = static_cast<size_t>(kWarpsPerGather) * nst * (stage_bytes + tab_bytes);
+    const int grid = cs_num_sms();
+    const void* fn = qwen ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 4, 128>)
+                          : (kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 0, 0>)
+                                                  : reinterpret_cast<const void*>(kv_gather_tma<float, 0, 0>));
+    const int slot = qwen ? 7 : (kv->dtype == CS_BF16 ? 8 : 9);
+    if (cs_set_smem_attr(fn, slot, 220 * 1024)) return CS_ERR_CUDA;
+    if (qwen)
+      kv_gather_tma<uint16_t, 4, 128><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+    else if (kv->dtype == CS_BF16)
+      kv_gather_tma<uint16_t, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+    else
+      kv_gather_tma<float, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+  } else {
+    const int grid = cs_num_sms() * 4;
+    const size_t gsmem = static_cast<size_t>(kGatherThreads / 32) * 8 * static_cast<size_t>(kv->head_dim / 2);
+    if (kv->dtype == CS_BF16) kv_gather_paged<uint16_t, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+    else kv_gather_paged<float, 0, 0><<<grid, kGatherThreads, gsmem, stream>>>(P);
+  }
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
 }
