@@ -482,7 +482,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                       "codecsight_kv_refresh (kv_plan + kv_prefix + kv_gather_tma)",
                       "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                       "frac": achieved / peak,
-                      "traffic": ncu_traffic("kv_gather_paged" if args.kv_mode == "paged" else "kv_gather"),
+                      "traffic": ncu_traffic("kv_refresh_paged" if args.kv_mode == "paged" else "kv_refresh_copy"),
                       "algorithmic_bytes_per_launch": kv_bytes_launch} if kvb else
                      {"bound": "hbm", "kernel": "codecsight_compact (compact_scan + compact_gather)",
                       "achieved": cmp_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
