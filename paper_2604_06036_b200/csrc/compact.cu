@@ -66,15 +66,42 @@ __device__ int count_groups(const CompactParams& P, const uint32_t* m) {
 
 __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_constant__ CompactParams P) {
   __shared__ int s_warp[kScanThreads / 32];
+  __shared__ int s_cnt[kScanThreads];
   __shared__ int s_carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gs2 = P.G * P.G;
+  const bool fast = (P.G == 2 && P.grid_w == 32);
   if (tid == 0) s_carry = 0;
   __syncthreads();
   for (int base = 0; base < P.n_slots; base += kScanThreads) {
+    // counts of this tile of slots: one warp per slot (coalesced 128-B mask loads)
+    for (int j = warp; j < kScanThreads; j += kScanThreads / 32) {
+      const int slot = base + j;
+      int cnt = 0;
+      if (slot < P.n_slots) {
+        const uint32_t* m = slot_mask(P, slot);
+        if (fast) {
+          // word r = patch row r; group row g = rows 2g, 2g+1; fold horizontal pairs onto even bits
+          const uint32_t wv = lane < P.nw ? __ldg(m + lane) : 0u;
+          const uint32_t x = wv | __shfl_down_sync(0xffffffffu, wv, 1);
+          int c = (lane & 1) == 0 ? __popc((x | (x >> 1)) & 0x55555555u) : 0;
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
+          cnt = c;
+        } else {
+          int c = 0;
+          for (int q0 = 0; q0 < P.ngroups; q0 += 32) {
+            const int q = q0 + lane;
+            c += __popc(__ballot_sync(0xffffffffu, q < P.ngroups && cs::group_kept(m, q, P.ngc, P.G, P.grid_w)));
+          }
+          cnt = c;
+        }
+      }
+      if (lane == 0) s_cnt[j] = cnt * gs2;
+    }
+    __syncthreads();
     const int slot = base + tid;
-    int cnt = 0;
-    if (slot < P.n_slots) cnt = count_groups(P, slot_mask(P, slot)) * gs2;
+    const int cnt = s_cnt[tid];
     int inc = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {

@@ -24,6 +24,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kThreads = 256;
+constexpr uint32_t kIntraSq = 0xffffffffu;  // > any |mv|^2 (<= 2^31)
 
 struct ScoreParams {
   int src_w, src_h, mb, mb_cols, mb_rows, grid_w, grid_h, G;
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   const int nthr = blockDim.x;
 
   unsigned char* stage = smem;
-  float* Vrow = reinterpret_cast<float*>(smem + P.off_vrow);
+  uint32_t* Vrow = reinterpret_cast<uint32_t*>(smem + P.off_vrow);  // max |mv|^2 per (MB row, patch col)
   uint32_t* Srow = reinterpret_cast<uint32_t*>(smem + P.off_srow);
   uint32_t* dyn = reinterpret_cast<uint32_t*>(smem + P.off_dyn);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.off_bar);
@@ -127,37 +128,37 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       for (int e = tid; e < nrows * P.mb_cols; e += nthr) d[e] = g[e];
       __syncthreads();
     }
-    // ---- pass 1: MB row j -> per patch column c: max v_m and sum_i ox(c,i) * sad_m (exact, u32) ----------
+    // ---- pass 1: MB row j -> per patch column c: max |mv|^2 and sum_i ox(c,i) * sad_m (exact, u32) --------
+    // v = fl(sqrt(fl(dx^2 + dy^2))) / 4 is monotone in dx^2 + dy^2, so max_m v_m = v(max_m |mv_m|^2): the sqrt
+    // is taken once per patch in pass 2 (bit-identical to the max of per-MB magnitudes).  INTRA -> sentinel.
     int badmb = 0;
-    for (int it = tid; it < nrows * P.grid_w; it += nthr) {
-      const int row = it / P.grid_w;
-      const int c = it - row * P.grid_w;
+    const int lane_w = tid >> 5, nwarps = nthr >> 5;
+    const int cw = P.mb * P.grid_w;  // MB width in scaled x units
+    for (int c = lane; c < P.grid_w; c += 32) {
       const int px0 = c * P.src_w, px1 = px0 + P.src_w;
-      const int cw = P.mb * P.grid_w;  // MB width in scaled x units
       const int i0 = px0 / cw, i1 = (px1 - 1) / cw;
-      float vmax = -CUDART_INF_F;
-      uint32_t ssum = 0;
-      for (int i = i0; i <= i1; ++i) {
-        const uint2 rec = buf[row * P.mb_cols + i];
-        const int dx = static_cast<int16_t>(rec.x & 0xffffu);
-        const int dy = static_cast<int16_t>(rec.x >> 16);
-        const uint32_t sad = rec.y & 0xffffu;
-        const uint32_t type = (rec.y >> 16) & 0xffu;
-        float v;
-        if (type <= CS_MB_SKIP) {
-          const uint32_t sq = static_cast<uint32_t>(dx * dx) + static_cast<uint32_t>(dy * dy);
-          v = __fmul_rn(__fsqrt_rn(__uint2float_rn(sq)), 0.25f);  // Eq. 1 in source px (qpel / 4)
-        } else {
-          v = CUDART_INF_F;  // INTRA (or unknown) -> maximally dynamic (Q9)
-          badmb |= (type > CS_MB_INTRA);
+      for (int row = lane_w; row < nrows; row += nwarps) {
+        uint32_t msq = 0u, ssum = 0u;
+        for (int i = i0; i <= i1; ++i) {
+          const uint2 rec = buf[row * P.mb_cols + i];
+          const int dx = static_cast<int16_t>(rec.x & 0xffffu);
+          const int dy = static_cast<int16_t>(rec.x >> 16);
+          const uint32_t sad = rec.y & 0xffffu;
+          const uint32_t type = (rec.y >> 16) & 0xffu;
+          if (type <= CS_MB_SKIP) {
+            const uint32_t sq = static_cast<uint32_t>(dx * dx) + static_cast<uint32_t>(dy * dy);
+            msq = sq > msq ? sq : msq;
+          } else {
+            msq = kIntraSq;  // INTRA (or unknown) -> maximally dynamic (Q9)
+            badmb |= (type > CS_MB_INTRA);
+          }
+          const int ox = min(px1, cw * (i + 1)) - max(px0, cw * i);
+          ssum += static_cast<uint32_t>(ox) * sad;
         }
-        vmax = (v > vmax) ? v : vmax;
-        const int ox = min(px1, cw * (i + 1)) - max(px0, cw * i);
-        ssum += static_cast<uint32_t>(ox) * sad;
+        const int j = r0 + row;
+        Vrow[j * P.grid_w + c] = msq;
+        Srow[j * P.grid_w + c] = ssum;
       }
-      const int j = r0 + row;
-      Vrow[j * P.grid_w + c] = vmax;
-      Srow[j * P.grid_w + c] = ssum;
     }
     if (badmb) s_badmb = 1;
     __syncthreads();  // chunk fully consumed, Vrow/Srow rows complete
@@ -169,28 +170,34 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       const int lf = f - f_begin;
       const int ch = P.mb * P.grid_h;  // MB height in scaled y units
       for (int i = tid; i < nw * 32; i += nthr) {
-        bool d = false;
+        bool d = false, nr = false;
         if (i < P.np) {
           const int r = i / P.grid_w;
           const int c = i - r * P.grid_w;
           const int py0 = r * P.src_h, py1 = py0 + P.src_h;
           const int j0 = py0 / ch, j1 = (py1 - 1) / ch;
-          float V = -CUDART_INF_F;
+          uint32_t msq = 0u;
           unsigned long long S = 0ull;
           for (int j = j0; j <= j1; ++j) {
             const int oy = min(py1, ch * (j + 1)) - max(py0, ch * j);
-            const float vj = Vrow[j * P.grid_w + c];
-            V = (vj > V) ? vj : V;
+            const uint32_t mj = Vrow[j * P.grid_w + c];
+            msq = mj > msq ? mj : msq;
             S += static_cast<unsigned long long>(oy) * Srow[j * P.grid_w + c];
           }
+          // Eq. 1: V(i) = max over overlapping MBs of |mv| / 4 px
+          const float V = msq == kIntraSq ? CUDART_INF_F : __fmul_rn(__fsqrt_rn(__uint2float_rn(msq)), 0.25f);
           const float R = __double2float_rn(__ddiv_rn(static_cast<double>(S), P.denom));
           const float M = isinf(V) ? CUDART_INF_F : __fmaf_rn(P.alpha, R, V);  // Eq. 3
           d = (M >= P.tau);                                                  // Eq. 4 (inclusive, Q1)
-          if (isfinite(M) && fabsf(__fsub_rn(M, P.tau)) <= 1e-5f) ++near_local;
+          nr = isfinite(M) && fabsf(__fsub_rn(M, P.tau)) <= 1e-5f;
           if (P.want_score) P.score[((long long)sidx * P.n_frames + f) * P.np + i] = M;
         }
         const uint32_t word = __ballot_sync(0xffffffffu, d);
-        if (lane == 0) dyn[lf * nw + (i >> 5)] = word;
+        const uint32_t nword = __ballot_sync(0xffffffffu, nr);
+        if (lane == 0) {
+          dyn[lf * nw + (i >> 5)] = word;
+          near_local += __popc(nword);
+        }
       }
       __syncthreads();  // Vrow/Srow free for the next frame
     }
@@ -321,12 +328,12 @@ int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const
   P.frame_stride = frame_stride;
   P.row_bytes = static_cast<unsigned>(g->mb_cols) * 8u;
   P.use_bulk = ((reinterpret_cast<uintptr_t>(mb) & 15u) == 0 && (P.row_bytes % 16u) == 0) ? 1 : 0;
-  const unsigned target = 16384u;
+  const unsigned target = 8192u;
   P.chunk_rows = static_cast<int>(P.row_bytes >= target ? 1u : target / P.row_bytes);
   if (P.chunk_rows > P.mb_rows) P.chunk_rows = P.mb_rows;
   P.n_chunks = (P.mb_rows + P.chunk_rows - 1) / P.chunk_rows;
   P.chunk_alloc = (static_cast<unsigned>(P.chunk_rows) * P.row_bytes + 127u) & ~127u;
-  P.nstage = P.chunk_alloc <= 16384u ? 4 : 2;
+  P.nstage = P.chunk_alloc <= 8192u ? 4 : 2;
   if (!P.use_bulk) P.nstage = 1;
   P.want_score = score != nullptr;
   P.mb_ptr = mb;
