@@ -47,23 +47,6 @@ __device__ __forceinline__ const uint32_t* slot_mask(const CompactParams& P, int
   return P.keep_mask + ((long long)s * P.mask_frame_stride + j) * P.nw;
 }
 
-// emitted groups of one slot
-__device__ int count_groups(const CompactParams& P, const uint32_t* m) {
-  if (P.G == 2 && P.grid_w == 32) {
-    // fast path (32 x 32 grid, 2 x 2 groups): one word per patch row; OR the two rows of a group row, fold
-    // horizontal pairs onto even bits, popcount.
-    int n = 0;
-    for (int r = 0; r < P.grid_h; r += 2) {
-      const uint32_t x = __ldg(m + r) | __ldg(m + r + 1);
-      n += __popc((x | (x >> 1)) & 0x55555555u);
-    }
-    return n;
-  }
-  int n = 0;
-  for (int q = 0; q < P.ngroups; ++q) n += cs::group_kept(m, q, P.ngc, P.G, P.grid_w) ? 1 : 0;
-  return n;
-}
-
 __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_constant__ CompactParams P) {
   __shared__ int s_warp[kScanThreads / 32];
   __shared__ int s_cnt[kScanThreads];

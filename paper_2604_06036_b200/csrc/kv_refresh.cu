@@ -15,6 +15,8 @@
 //              REUSE V runs and refreshed rows are contiguous 16-B vector copies.  No tensor cores: nothing here
 //              is a contraction; the kernel is HBM-bound.
 #include <math_constants.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "cs_internal.cuh"
 
@@ -520,6 +522,7 @@ struct ChunkGen {  // generator state, owned by lane 0 of a warp
   long long it, it1;
   int sidx, seg, x, active;
   int nseg, a, b, l, kv;
+  int c_sidx, c_blk, c_seg;  // cache: stream whose pointers are loaded; (stream, block) of the last run search
   const KvSeg* segs;
   unsigned char* nc;
   const unsigned char* oc;
@@ -537,6 +540,8 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
   const int ipb = P.L * 2;
   while (g.it < g.it1) {
     if (!g.active) {
+      // items of one stream are contiguous and ordered (block, layer, K|V): stream pointers and the run search
+      // of a block are cached across the 2L items that share them
       while (__ldg(pref + g.sidx + 1) <= g.it) ++g.sidx;
       const long long local = g.it - __ldg(pref + g.sidx);
       const int blk = static_cast<int>(local / ipb);
@@ -545,21 +550,29 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
       g.kv = lk & 1;
       g.a = blk * kRowBlock;
       g.b = g.a + kRowBlock;
-      const unsigned char* ws = stream_ws(P, g.sidx);
-      g.nseg = reinterpret_cast<const KvHdr*>(ws)->n_seg;
-      g.segs = reinterpret_cast<const KvSeg*>(ws + sizeof(KvHdr));
-      g.tab = ws + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg;
-      g.nc = static_cast<unsigned char*>(P.new_cache[g.sidx]);
-      g.oc = P.k >= 1 ? static_cast<const unsigned char*>(P.old_cache[g.sidx]) : nullptr;
-      g.rf = P.has_refreshed ? static_cast<const unsigned char*>(P.refreshed[g.sidx]) : nullptr;
-      // first run that ends after the block start (runs are sorted by p_new and disjoint)
-      int lo = 0, hi = g.nseg;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const KvSeg m = g.segs[mid];
-        if (m.p_new + m.len <= g.a) lo = mid + 1; else hi = mid;
+      if (g.sidx != g.c_sidx) {
+        const unsigned char* ws = stream_ws(P, g.sidx);
+        g.nseg = reinterpret_cast<const KvHdr*>(ws)->n_seg;
+        g.segs = reinterpret_cast<const KvSeg*>(ws + sizeof(KvHdr));
+        g.tab = ws + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg;
+        g.nc = static_cast<unsigned char*>(P.new_cache[g.sidx]);
+        g.oc = P.k >= 1 ? static_cast<const unsigned char*>(P.old_cache[g.sidx]) : nullptr;
+        g.rf = P.has_refreshed ? static_cast<const unsigned char*>(P.refreshed[g.sidx]) : nullptr;
+        g.c_sidx = g.sidx;
+        g.c_blk = -1;
       }
-      g.seg = lo;
+      if (blk != g.c_blk) {
+        // first run that ends after the block start (runs are sorted by p_new and disjoint)
+        int lo = 0, hi = g.nseg;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const KvSeg m = g.segs[mid];
+          if (m.p_new + m.len <= g.a) lo = mid + 1; else hi = mid;
+        }
+        g.c_blk = blk;
+        g.c_seg = lo;
+      }
+      g.seg = g.c_seg;
       g.x = g.a;
       g.active = 1;
     }
@@ -704,15 +717,17 @@ __global__ void __launch_bounds__(kGatherThreads, 1) kv_gather_tma(const __grid_
   uint64_t* full = s_full[wib];
   ChunkDesc* desc = s_desc[wib];
   const long long row_bytes = (long long)P.H * P.D * sizeof(T);
-  const int cr = static_cast<int>(kTmaChunk / row_bytes);
+  const int cr = static_cast<int>(stage_bytes / row_bytes);
   const int* pref = ws_prefix(P);
 
   const long long V = __ldg(pref + P.n_streams);
-  const long long nwarps = static_cast<long long>(gridDim.x) * kWarpsPerGather;
-  const long long gw = static_cast<long long>(blockIdx.x) * kWarpsPerGather + wib;
+  const long long nwarps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const long long gw = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + wib;
   ChunkGen gen{};
   gen.it = V * gw / nwarps;
   gen.it1 = V * (gw + 1) / nwarps;
+  gen.c_sidx = -1;
+  gen.c_blk = -1;
   if (gen.it >= gen.it1) return;  // warp-uniform
   if (lane == 0) {
     // first stream of this warp's range: binary search over the prefix
@@ -1224,6 +1239,37 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather_paged(const __grid_c
   }
 }
 
+
+// Launch the TMA ring gather.  Geometry: warps per CTA x stages x stage bytes (one CTA per SM); default 8 warps x
+// 8 KB stages, as many stages (<= 6) as fit.  CS_KV_TMA="warps,stage_kb,stages" overrides (tuning experiments).
+static int launch_gather_tma(const KvParams& P, const cs_kv_desc* kv, cudaStream_t stream) {
+  int warps = 8, stage_kb = 8, nst = 0;
+  if (const char* e = getenv("CS_KV_TMA")) sscanf(e, "%d,%d,%d", &warps, &stage_kb, &nst);
+  if (warps < 1 || warps > kWarpsPerGather) warps = kWarpsPerGather;
+  const unsigned stage_bytes = static_cast<unsigned>(stage_kb) * 1024u;
+  const unsigned tab_bytes = static_cast<unsigned>(((8 * (P.D / 2)) + 127) & ~127);
+  const int fit = static_cast<int>((216u * 1024u) / (warps * (stage_bytes + tab_bytes)));
+  if (nst <= 0 || nst > fit) nst = fit;
+  if (nst > kMaxStages) nst = kMaxStages;
+  if (nst < 3) return CS_ERR_UNSUPPORTED;
+  const size_t smem = static_cast<size_t>(warps) * nst * (stage_bytes + tab_bytes);
+  const int grid = cs_num_sms();
+  const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
+  const void* fn = qwen ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 4, 128>)
+                        : (kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 0, 0>)
+                                                : reinterpret_cast<const void*>(kv_gather_tma<float, 0, 0>));
+  const int slot = qwen ? 7 : (kv->dtype == CS_BF16 ? 8 : 9);
+  if (cs_set_smem_attr(fn, slot, 220 * 1024)) return CS_ERR_CUDA;
+  const int threads = warps * 32;
+  if (qwen)
+    kv_gather_tma<uint16_t, 4, 128><<<grid, threads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+  else if (kv->dtype == CS_BF16)
+    kv_gather_tma<uint16_t, 0, 0><<<grid, threads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+  else
+    kv_gather_tma<float, 0, 0><<<grid, threads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+  return CS_OK;
+}
+
 }  // namespace
 
 size_t cs_kv_workspace_bytes(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams) {
@@ -1308,25 +1354,8 @@ int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window
   kv_prefix<<<1, 1024, 0, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   if (tma_ok) {
-    // one CTA per SM, 8 warps, each warp an independent ring of nst x 8 KB stages (+ cos/sin table slots)
-    const unsigned stage_bytes = kTmaChunk;
-    const unsigned tab_bytes = static_cast<unsigned>(((8 * (P.D / 2)) + 127) & ~127);
-    int nst = static_cast<int>((216u * 1024u) / (kWarpsPerGather * (stage_bytes + tab_bytes)));
-    if (nst > kMaxStages) nst = kMaxStages;
-    if (nst < 3) return CS_ERR_UNSUPPORTED;
-    const size_t smem = static_cast<size_t>(kWarpsPerGather) * nst * (stage_bytes + tab_bytes);
-    const int grid = sms;
-    const void* fn = qwen ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 4, 128>)
-                          : (kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 0, 0>)
-                                                  : reinterpret_cast<const void*>(kv_gather_tma<float, 0, 0>));
-    const int slot = qwen ? 7 : (kv->dtype == CS_BF16 ? 8 : 9);
-    if (cs_set_smem_attr(fn, slot, 220 * 1024)) return CS_ERR_CUDA;
-    if (qwen)
-      kv_gather_tma<uint16_t, 4, 128><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
-    else if (kv->dtype == CS_BF16)
-      kv_gather_tma<uint16_t, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
-    else
-      kv_gather_tma<float, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+    const int rc = launch_gather_tma(P, kv, stream);
+    if (rc) return rc;
   } else {
     const size_t gsmem = 8 * static_cast<size_t>((n_streams + 2) & ~1) + sizeof(KvSeg) * max_seg +
                          8 * static_cast<size_t>(kv->head_dim / 2);
@@ -1394,24 +1423,8 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
   if (tma_ok) {
-    const unsigned stage_bytes = kTmaChunk;
-    const unsigned tab_bytes = static_cast<unsigned>(((8 * (P.D / 2)) + 127) & ~127);
-    int nst = static_cast<int>((216u * 1024u) / (kWarpsPerGather * (stage_bytes + tab_bytes)));
-    if (nst > kMaxStages) nst = kMaxStages;
-    if (nst < 3) return CS_ERR_UNSUPPORTED;
-    const size_t smem = static_cast<size_t>(kWarpsPerGather) * nst * (stage_bytes + tab_bytes);
-    const int grid = cs_num_sms();
-    const void* fn = qwen ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 4, 128>)
-                          : (kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 0, 0>)
-                                                  : reinterpret_cast<const void*>(kv_gather_tma<float, 0, 0>));
-    const int slot = qwen ? 7 : (kv->dtype == CS_BF16 ? 8 : 9);
-    if (cs_set_smem_attr(fn, slot, 220 * 1024)) return CS_ERR_CUDA;
-    if (qwen)
-      kv_gather_tma<uint16_t, 4, 128><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
-    else if (kv->dtype == CS_BF16)
-      kv_gather_tma<uint16_t, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
-    else
-      kv_gather_tma<float, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P, nst, stage_bytes, tab_bytes);
+    const int rc = launch_gather_tma(P, kv, stream);
+    if (rc) return rc;
   } else {
     const int grid = cs_num_sms() * 4;
     const size_t gsmem = static_cast<size_t>(kGatherThreads / 32) * 8 * static_cast<size_t>(kv->head_dim / 2);

@@ -1,0 +1,122 @@
+"""Full-size parity in the bench's own launch configuration (BASELINE configs C4 and C5 shapes).
+
+The GPU runs the whole batch of streams exactly as bench.py does (Pipeline, paged KV, grouped frames); the oracle,
+which is per-stream independent, re-runs a deterministic sample of streams from the same inputs and every output of
+those streams is compared (masks, GOP state, compaction rows of their frames, dispositions, p_old, slot maps and the
+pool rows).  Sizes: C4 = 256 1080p streams (w=16, s=4, 28-layer Qwen2-VL-7B KV); C5 = 128 4K streams (w=64, s=8).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from synth import make_grid
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _host(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16) if t.dtype == torch.bfloat16 else t.cpu().numpy()
+
+
+def to_grouped(frame, g):
+    p, G = g["patch"], g["group"]
+    ngr, ngc = g["grid_h"] // G, g["grid_w"] // G
+    x = frame.reshape(3, ngr, G, p, ngc, G, p)
+    return np.ascontiguousarray(x.transpose(1, 4, 2, 5, 0, 3, 6)).reshape(-1)
+
+
+@pytest.mark.parametrize("cfg_name,S,steps,sample", [("C4", 256, 3, [0, 1, 254, 255]), ("C5", 128, 2, [0, 127])])
+def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample):
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    from paper_2604_06036_b200 import _abi as abi
+    from paper_2604_06036_b200.pipeline import Pipeline
+    cfg = synth.CONFIGS[cfg_name]
+    sw, sh = cfg["src"]
+    g = make_grid(sw, sh)
+    w, s, gop = cfg["window"], cfg["stride"], cfg["gop"]
+    ring = w + s
+    kvb = cfg["kv"]
+    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=DEV,
+                    frame_layout=abi.CS_LAYOUT_GROUPED, kv_mode="paged", compact_chunk=s)
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(11)
+    pipe.init_cache_fill(gen)
+    gens = [synth.StreamGen(sw, sh, synth.scene_of(cfg, i), synth.stream_seed(cfg, i)) for i in range(S)]
+    rng = np.random.default_rng(3)
+    # distinct frames for the sampled streams, one shared frame for the others (their pixels are not checked)
+    planar = {si: synth.random_frames(w, 448, 448, rng) for si in sample}
+    shared = torch.from_numpy(to_grouped(synth.random_frames(1, 448, 448, rng)[0], g).view(np.int16)).to(DEV)
+    dev_frames = {si: [torch.from_numpy(to_grouped(f, g).view(np.int16)).to(DEV) for f in planar[si]]
+                  for si in sample}
+    nw = 32
+    st_h = {si: dict(gop=np.zeros((1, nw + 1), np.uint32), mring=np.zeros((1, ring, nw), np.uint32),
+                     tring=np.zeros((1, ring), np.uint8), slot=None) for si in sample}
+    L = kvb["layers"]
+    for k in range(steps):
+        f0, n = pipe.new_frames(k)
+        mb = np.stack([np.stack([gn.next_frame() for _ in range(n)]) for gn in gens])
+        types = np.stack([synth.frame_types(n, gop, f0)] * S)
+        ptr_list = []
+        for si in range(S):
+            for j in range(n):
+                ptr_list.append(dev_frames[si][j % w] if si in sample else shared)
+        fptr = abi.ptr_array(ptr_list, DEV)
+        fidx = np.tile(np.arange(f0, f0 + n, dtype=np.int32), S)
+        pool_before = {si: _host(pipe.caches[0][si]).copy() for si in sample}
+        refr = {si: _host(pipe.refreshed[si]) for si in sample}
+        pipe.step(k, torch.from_numpy(mb.view(np.uint8)).to(DEV), fptr, torch.from_numpy(fidx).to(DEV),
+                  torch.from_numpy(types).to(DEV))
+        torch.cuda.synchronize()
+        assert int(pipe.status.item()) == 0
+        off = f0 % ring
+        mring_d = pipe.mask_ring.cpu().numpy().view(np.uint32)
+        gop_d = pipe.gop_state.cpu().numpy().view(np.uint32)
+        slot_d = pipe.slots[pipe.cur].cpu().numpy()          # after the swap: window k
+        disp_d, pold_d, nt_d = pipe.disposition.cpu().numpy(), pipe.p_old.cpu().numpy(), pipe.n_tokens.cpu().numpy()
+        for si in sample:
+            h = st_h[si]
+            h["tring"][0, off:off + n] = types[si]
+            so = ref.score_patches(g, mb[si:si + 1], np.ascontiguousarray(h["tring"][:, off:]), h["gop"],
+                                   frame_stride=ring - off, want_score=False)
+            h["mring"][0, off:off + n] = so["keep_mask"][0, :n]
+            assert (mring_d[si] == h["mring"][0]).all()
+            assert (gop_d[si] == h["gop"][0]).all()
+            # kv refresh of this stream (paged), pool rows compared in full
+            kv = pipe.kv
+            win = dict(window=w, stride=s, step=k, ring_frames=ring)
+            pool = pool_before[si]
+            ko = ref.kv_refresh_paged(g, kv, win, h["mring"], h["tring"], [pool], h["slot"], pipe.token_cap,
+                                      [refr[si]] if k >= 1 else None, pipe.token_cap)
+            ntok = int(ko["n_tokens"][0, 0]) + cfg["n_prompt"]
+            assert (nt_d[si] == ko["n_tokens"][0]).all()
+            assert (disp_d[si, :ntok] == ko["disposition"][0, :ntok]).all()
+            assert (pold_d[si, :ntok] == ko["p_old"][0, :ntok]).all()
+            assert (slot_d[si, :ntok] == ko["slot_new"][0, :ntok]).all()
+            got = _host(pipe.caches[0][si])
+            assert (got[:, 1] == pool[:, 1]).all()                 # values: bit copies / untouched
+            fa = (got[:, 0].astype(np.uint32) << 16).view(np.float32)
+            fb = (pool[:, 0].astype(np.uint32) << 16).view(np.float32)
+            assert np.abs(fa - fb).max() <= 1e-2                   # keys: rotated within the bf16 bound
+            h["slot"] = ko["slot_new"]
+        # compaction of the last chunk (the packed buffer holds the last s frames of the step)
+        last0 = n - min(n, s)
+        nl = n - last0
+        offs = pipe.frame_offsets[:S * nl + 1].cpu().numpy()
+        src_d = pipe.src_index.cpu().numpy()
+        pos_d = pipe.pos_ids.cpu().numpy()
+        packed_d = pipe.packed.view(torch.int16).cpu().numpy().view(np.uint16)
+        for si in sample:
+            mask = st_h[si]["mring"][:, off + last0:off + n]
+            fr = [to_grouped(planar[si][(last0 + j) % w], g) for j in range(nl)]
+            co = ref.compact(g, mask.copy(), np.arange(f0 + last0, f0 + n, dtype=np.int32), fr, nl * 1024, 1, nl,
+                             frame_layout=1)
+            a, b = int(offs[si * nl]), int(offs[si * nl + nl])
+            cnt = int(co["frame_offsets"][-1])
+            assert b - a == cnt
+            assert (packed_d[a:b] == co["packed"][:cnt]).all()
+            assert (pos_d[a:b] == co["pos_ids"][:cnt]).all()
+            assert (src_d[a:b] - si * nl * 1024 == co["src_index"][:cnt]).all()
