@@ -1254,7 +1254,6 @@ static int launch_gather_tma(const KvParams& P, const cs_kv_desc* kv, cudaStream
   if (nst < 3) return CS_ERR_UNSUPPORTED;
   const size_t smem = static_cast<size_t>(warps) * nst * (stage_bytes + tab_bytes);
   const int grid = cs_num_sms();
-  const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
   const void* fn = qwen ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 4, 128>)
                         : (kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 0, 0>)
                                                 : reinterpret_cast<const void*>(kv_gather_tma<float, 0, 0>));
@@ -1349,7 +1348,6 @@ int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window
 
   const long long row_bytes = static_cast<long long>(P.H) * P.D * P.esz;
   const bool tma_ok = P.vec_rot && P.vec_copy && row_bytes <= kTmaChunk && (P.D % 4) == 0;
-  const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
   const int sms = cs_num_sms();
   kv_prefix<<<1, 1024, 0, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
@@ -1421,7 +1419,6 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   kv_prefix<<<1, 1024, 0, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
-  const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
   if (tma_ok) {
     const int rc = launch_gather_tma(P, kv, stream);
     if (rc) return rc;
