@@ -1254,6 +1254,7 @@ static int launch_gather_tma(const KvParams& P, const cs_kv_desc* kv, cudaStream
   if (nst < 3) return CS_ERR_UNSUPPORTED;
   const size_t smem = static_cast<size_t>(warps) * nst * (stage_bytes + tab_bytes);
   const int grid = cs_num_sms();
+  const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
   const void* fn = qwen ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 4, 128>)
                         : (kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 0, 0>)
                                                 : reinterpret_cast<const void*>(kv_gather_tma<float, 0, 0>));
