@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--kv-mode", default="paged", choices=["paged", "copy"],
                     help="paged: codecsight_kv_refresh_paged (in place, NEXT-1); copy: out-of-place double buffer")
+    ap.add_argument("--rope", default="1d", choices=["1d", "mrope"],
+                    help="key position scheme: 1-D on compacted sequence indices (Q16) or Qwen2-VL M-RoPE (NEXT-3)")
     ap.add_argument("--frame-layout", default="grouped", choices=["grouped", "planar"],
                     help="layout of the preprocessed model-input frames handed to compact (DESIGN.md §6)")
     return ap.parse_args()
@@ -282,6 +284,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     S, w, s, gop = cfg["streams"], cfg["window"], cfg["stride"], cfg["gop"]
     global_ids = shard.stream_ids(rank, world, S)
     kvb = cfg["kv"]
+    if kvb is not None and args.rope == "mrope":
+        kvb = dict(kvb, rope_mode=1, mrope_section=(16, 24, 24), t_per_frame=1)
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
                     kv_mode=args.kv_mode, compact_chunk=s)
@@ -483,7 +487,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg["name"], "streams_per_gpu": S, "streams_total": S * world, "src": list(cfg["src"]),
                    "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": 0.25, "alpha": 0.0,
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
-                   "frame_layout": args.frame_layout, "kv_mode": args.kv_mode,
+                   "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
                    "parallelism": f"stream-shard x{world}",
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
                          "see per-step bytes)"},

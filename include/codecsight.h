@@ -198,8 +198,20 @@ typedef struct {
   int64_t refresh_capacity;           /* token rows per refreshed (recompute) buffer                          */
   double rope_base;                   /* 1e4 (S:355 default) | 1e6 (Qwen2)                                    */
   int32_t n_prompt;                   /* prompt rows after the visual tokens; always NEW        */
-  int32_t reserved;
+  int32_t rope_mode;                  /* CS_ROPE_1D | CS_ROPE_MROPE (below)                                   */
+  int32_t mrope_section[3];           /* M-RoPE: frequency pairs of the t / h / w sections, sum = head_dim/2
+                                         (Qwen2-VL: 16, 24, 24)                                               */
+  int32_t t_per_frame;                /* M-RoPE: temporal position units per consumed frame (>= 1)            */
 } cs_kv_desc;
+
+/* Rotary position schemes of the cached keys (Eq. 5; reading Q19 and NEXT-3):
+ *   CS_ROPE_1D    one position per token = its compacted sequence index (reading Q16); R(dp) rotates every
+ *                 frequency pair i by dp * base^(-2i/D), dp = p_new - p_old.
+ *   CS_ROPE_MROPE multimodal RoPE (Qwen2-VL / Qwen3-VL): a visual token of frame f, group (gr, gc) has position
+ *                 (t, h, w) = ((f - ks) * t_per_frame, gr, gc) in window k, pair i < s_t rotates with t, the next
+ *                 s_h pairs with h, the last s_w with w.  A reused token keeps (h, w) and moves in time by
+ *                 dt = -stride * t_per_frame, so only the temporal section is rotated.                          */
+enum { CS_ROPE_1D = 0, CS_ROPE_MROPE = 1 };
 
 /* Sliding window: window k covers frames [k*stride, k*stride + window).                   */
 typedef struct {

@@ -275,6 +275,25 @@ static void ref_rot_pair(float x1, float x2, int64_t i, int64_t D, double base, 
   *o2 = fmaf(x2, c, x1 * s);
 }
 
+/* The position difference that rotates frequency pair i (Eq. 5): 1-D RoPE rotates every pair by the
+ * sequence-position difference; M-RoPE (reading NEXT-3) rotates pair i by the difference of the position component
+ * its section belongs to: i < s_t -> t, next s_h -> h, last s_w -> w. */
+static int64_t ref_pair_delta(const ref_kv* kv, int64_t i, int64_t dp_seq, const int64_t dpos[3]) {
+  if (kv->rope_mode != REF_ROPE_MROPE) return dp_seq;
+  if (i < kv->mrope_section[0]) return dpos[0];
+  if (i < kv->mrope_section[0] + kv->mrope_section[1]) return dpos[1];
+  return dpos[2];
+}
+
+static int ref_rope_ok(const ref_kv* kv) {
+  if (kv->rope_mode == REF_ROPE_1D) return 0;
+  if (kv->rope_mode != REF_ROPE_MROPE) return -3;
+  if (kv->mrope_section[0] < 0 || kv->mrope_section[1] < 0 || kv->mrope_section[2] < 0) return -1;
+  if (kv->mrope_section[0] + kv->mrope_section[1] + kv->mrope_section[2] != kv->head_dim / 2) return -2;
+  if (kv->t_per_frame < 1) return -1;
+  return 0;
+}
+
 void codecsight_ref_rope_rotate_f32(const float* k, int32_t n_heads, int32_t head_dim, double base, int64_t dp,
                                     float* out) {
   const int64_t half = head_dim / 2;
@@ -315,6 +334,7 @@ int codecsight_ref_kv_refresh(const ref_grid* g, const ref_kv* kv, const ref_win
   if (kv->head_dim % 2 != 0) return -3;
   if (kv->capacity < 0 || kv->refresh_capacity < 0 || kv->n_prompt < 0) return -1;
   if (!(kv->rope_base > 0.0)) return -1;
+  if ((rc = ref_rope_ok(kv))) return rc;
   const int64_t w = win->window, s = win->stride, k = win->step;
   if (w < 1 || s < 1 || k < 0) return -1;
   if (s > w) return -3;
@@ -384,6 +404,11 @@ int codecsight_ref_kv_refresh(const ref_grid* g, const ref_kv* kv, const ref_win
           if (p_new >= cap) { *status |= REF_ST_CAPACITY; continue; }
           if (po >= cap) { *status |= REF_ST_ORIGIN; continue; }
           const int64_t dp = p_new - po;
+          /* M-RoPE positions of this token in windows k-1 and k: (t, h, w) = (frame offset * t_per_frame, gr, gc) */
+          const int64_t gr = q / (g->grid_w / G), gc = q % (g->grid_w / G);
+          const int64_t pos_old[3] = {(f - (k - 1) * s) * kv->t_per_frame, gr, gc};
+          const int64_t pos_new[3] = {(f - ks) * kv->t_per_frame, gr, gc};
+          const int64_t dpos[3] = {pos_new[0] - pos_old[0], pos_new[1] - pos_old[1], pos_new[2] - pos_old[2]};
           for (int64_t l = 0; l < L; ++l) {
             /* value reuse: V^_t(j) = V_{t-1}(j) */
             memcpy(nc + ((l * 2 + 1) * cap + p_new) * rowel * esz, oc + ((l * 2 + 1) * cap + po) * rowel * esz,
@@ -401,7 +426,7 @@ int codecsight_ref_kv_refresh(const ref_grid* g, const ref_kv* kv, const ref_win
                   x1 = ((const float*)oc)[src + e1];
                   x2 = ((const float*)oc)[src + e2];
                 }
-                ref_rot_pair(x1, x2, i, D, kv->rope_base, dp, &o1, &o2);
+                ref_rot_pair(x1, x2, i, D, kv->rope_base, ref_pair_delta(kv, i, dp, dpos), &o1, &o2);
                 if (esz == 2) {
                   ((uint16_t*)nc)[dst + e1] = ref_f32_to_bf16(o1);
                   ((uint16_t*)nc)[dst + e2] = ref_f32_to_bf16(o2);
@@ -463,6 +488,7 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
   if (kv->head_dim % 2 != 0) return -3;
   if (kv->capacity < 0 || kv->refresh_capacity < 0 || kv->n_prompt < 0) return -1;
   if (!(kv->rope_base > 0.0)) return -1;
+  if ((rc = ref_rope_ok(kv))) return rc;
   const int64_t w = win->window, s = win->stride, k = win->step;
   if (w < 1 || s < 1 || k < 0) return -1;
   if (s > w) return -3;
@@ -481,8 +507,12 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
   int32_t* tdisp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(max_tok + 1));
   int64_t* tpold = (int64_t*)malloc(sizeof(int64_t) * (size_t)(max_tok + 1));
   int64_t* tslot = (int64_t*)malloc(sizeof(int64_t) * (size_t)(max_tok + 1));
+  int64_t* tfrm = (int64_t*)malloc(sizeof(int64_t) * (size_t)(max_tok + 1));
   uint8_t* used = (uint8_t*)malloc((size_t)(cap + 1));
-  if (!tdisp || !tpold || !tslot || !used) { free(tdisp); free(tpold); free(tslot); free(used); return -1; }
+  if (!tdisp || !tpold || !tslot || !used || !tfrm) {
+    free(tdisp); free(tpold); free(tslot); free(used); free(tfrm);
+    return -1;
+  }
 
   for (int64_t sg = 0; sg < n_streams; ++sg) {
     const uint32_t* mring = keep_mask_ring + sg * ring * nw;
@@ -506,6 +536,7 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
           tdisp[nt] = (type == REF_FRAME_I || f == ks) ? REF_DISP_ANCHOR : REF_DISP_REUSE;
           tpold[nt] = drop + before + t;
         }
+        tfrm[nt] = f;
         ++nt;
       }
       before += nf;
@@ -557,6 +588,8 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
       if (d == REF_DISP_REUSE) {
         if (sl < 0) continue;
         dp = p - tpold[p];
+        /* M-RoPE: t moves with the window, (h, w) of a reused token (same frame, same group) do not */
+        const int64_t dpos[3] = {((tfrm[p] - ks) - (tfrm[p] - (k - 1) * s)) * kv->t_per_frame, 0, 0};
         for (int64_t l = 0; l < L; ++l)
           for (int64_t h = 0; h < H; ++h)
             for (int64_t i = 0; i < D / 2; ++i) {
@@ -570,7 +603,7 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
                 x1 = ((float*)pl)[e1];
                 x2 = ((float*)pl)[e2];
               }
-              ref_rot_pair(x1, x2, i, D, kv->rope_base, dp, &o1, &o2);
+              ref_rot_pair(x1, x2, i, D, kv->rope_base, ref_pair_delta(kv, i, dp, dpos), &o1, &o2);
               if (esz == 2) {
                 ((uint16_t*)pl)[e1] = ref_f32_to_bf16(o1);
                 ((uint16_t*)pl)[e2] = ref_f32_to_bf16(o2);
@@ -607,5 +640,6 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
   free(tpold);
   free(tslot);
   free(used);
+  free(tfrm);
   return 0;
 }

@@ -62,8 +62,12 @@ typedef struct {
   int32_t layers, kv_heads, head_dim, dtype;
   int64_t capacity, refresh_capacity;
   double rope_base;
-  int32_t n_prompt, reserved;
+  int32_t n_prompt, rope_mode;
+  int32_t mrope_section[3];
+  int32_t t_per_frame;
 } ref_kv;
+#define REF_ROPE_1D 0
+#define REF_ROPE_MROPE 1
 
 typedef struct {
   int32_t window, stride, step, ring_frames;

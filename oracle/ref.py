@@ -37,7 +37,8 @@ class RefGrid(C.Structure):
 class RefKv(C.Structure):
     _fields_ = [("layers", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32),
                 ("capacity", C.c_int64), ("refresh_capacity", C.c_int64), ("rope_base", C.c_double),
-                ("n_prompt", C.c_int32), ("reserved", C.c_int32)]
+                ("n_prompt", C.c_int32), ("rope_mode", C.c_int32), ("mrope_section", C.c_int32 * 3),
+                ("t_per_frame", C.c_int32)]
 
 
 class RefWindow(C.Structure):
@@ -167,8 +168,16 @@ def compact(g: dict, keep_mask: np.ndarray, frame_index: np.ndarray, frames: lis
                 status=int(status[0]))
 
 
-def kv_desc(layers, kv_heads, head_dim, dtype, capacity, refresh_capacity, rope_base, n_prompt) -> RefKv:
-    return RefKv(layers, kv_heads, head_dim, dtype, capacity, refresh_capacity, rope_base, n_prompt, 0)
+def kv_desc(layers, kv_heads, head_dim, dtype, capacity, refresh_capacity, rope_base, n_prompt, rope_mode=0,
+            mrope_section=(0, 0, 0), t_per_frame=1) -> RefKv:
+    return RefKv(layers, kv_heads, head_dim, dtype, capacity, refresh_capacity, rope_base, n_prompt, rope_mode,
+                 (C.c_int32 * 3)(*mrope_section), t_per_frame)
+
+
+def _kvd(kv: dict) -> RefKv:
+    return kv_desc(kv["layers"], kv["kv_heads"], kv["head_dim"], kv["dtype"], kv["capacity"],
+                   kv["refresh_capacity"], kv["rope_base"], kv["n_prompt"], kv.get("rope_mode", 0),
+                   tuple(kv.get("mrope_section", (0, 0, 0))), kv.get("t_per_frame", 1))
 
 
 def kv_refresh(g: dict, kv: dict, win: dict, keep_mask_ring: np.ndarray, frame_type_ring: np.ndarray,
@@ -193,8 +202,7 @@ def kv_refresh(g: dict, kv: dict, win: dict, keep_mask_ring: np.ndarray, frame_t
     ntok = np.zeros((S, 4), np.int32)
     counters = np.zeros(NCOUNTERS, np.uint64) if counters is None else counters
     status = np.zeros(1, np.int32)
-    kvd = kv_desc(kv["layers"], kv["kv_heads"], kv["head_dim"], kv["dtype"], kv["capacity"],
-                  kv["refresh_capacity"], kv["rope_base"], kv["n_prompt"])
+    kvd = _kvd(kv)
     w = RefWindow(win["window"], win["stride"], win["step"], win["ring_frames"])
     olds, news, refs = arr(old_cache), arr(new_cache), arr(refreshed)
     rc = lib().codecsight_ref_kv_refresh(C.byref(make_grid(g)), C.byref(kvd), C.byref(w), S, _p(keep_mask_ring),
@@ -223,8 +231,7 @@ def kv_refresh_paged(g: dict, kv: dict, win: dict, keep_mask_ring: np.ndarray, f
     ntok = np.zeros((S, 4), np.int32)
     counters = np.zeros(NCOUNTERS, np.uint64) if counters is None else counters
     status = np.zeros(1, np.int32)
-    kvd = kv_desc(kv["layers"], kv["kv_heads"], kv["head_dim"], kv["dtype"], kv["capacity"],
-                  kv["refresh_capacity"], kv["rope_base"], kv["n_prompt"])
+    kvd = _kvd(kv)
     w = RefWindow(win["window"], win["stride"], win["step"], win["ring_frames"])
     rc = lib().codecsight_ref_kv_refresh_paged(C.byref(make_grid(g)), C.byref(kvd), C.byref(w), S,
                                                _p(keep_mask_ring), _p(frame_type_ring), pp, _p(so), _p(sn),

@@ -42,7 +42,11 @@ class CsGrid(C.Structure):
 class CsKvDesc(C.Structure):
     _fields_ = [("layers", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32),
                 ("capacity", C.c_int64), ("refresh_capacity", C.c_int64), ("rope_base", C.c_double),
-                ("n_prompt", C.c_int32), ("reserved", C.c_int32)]
+                ("n_prompt", C.c_int32), ("rope_mode", C.c_int32), ("mrope_section", C.c_int32 * 3),
+                ("t_per_frame", C.c_int32)]
+
+
+CS_ROPE_1D, CS_ROPE_MROPE = 0, 1
 
 
 class CsWindow(C.Structure):
@@ -96,7 +100,8 @@ def make_grid(g: dict) -> CsGrid:
 
 def make_kv(kv: dict) -> CsKvDesc:
     return CsKvDesc(kv["layers"], kv["kv_heads"], kv["head_dim"], kv["dtype"], kv["capacity"],
-                    kv["refresh_capacity"], kv["rope_base"], kv["n_prompt"], 0)
+                    kv["refresh_capacity"], kv["rope_base"], kv["n_prompt"], kv.get("rope_mode", CS_ROPE_1D),
+                    (C.c_int32 * 3)(*kv.get("mrope_section", (0, 0, 0))), kv.get("t_per_frame", 1))
 
 
 def make_window(win: dict) -> CsWindow:

@@ -170,6 +170,12 @@ static int kv_args_ok(const cs_grid* g, const cs_kv_desc* kv, const cs_window* w
   if (kv->head_dim % 2 != 0) return CS_ERR_UNSUPPORTED;  // S:376 "odd head_dim"
   if (kv->capacity < 0 || kv->refresh_capacity < 0 || kv->n_prompt < 0) return CS_ERR_INVALID_ARGUMENT;
   if (!(kv->rope_base > 0.0)) return CS_ERR_INVALID_ARGUMENT;
+  if (kv->rope_mode != CS_ROPE_1D && kv->rope_mode != CS_ROPE_MROPE) return CS_ERR_UNSUPPORTED;
+  if (kv->rope_mode == CS_ROPE_MROPE) {
+    if (kv->mrope_section[0] < 0 || kv->mrope_section[1] < 0 || kv->mrope_section[2] < 0 || kv->t_per_frame < 1)
+      return CS_ERR_INVALID_ARGUMENT;
+    if (kv->mrope_section[0] + kv->mrope_section[1] + kv->mrope_section[2] != kv->head_dim / 2) return CS_ERR_SHAPE;
+  }
   const long long w = win->window, s = win->stride, k = win->step;
   if (w < 1 || s < 1 || k < 0) return CS_ERR_INVALID_ARGUMENT;
   if (s > w) return CS_ERR_UNSUPPORTED;

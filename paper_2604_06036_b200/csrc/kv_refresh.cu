@@ -75,6 +75,9 @@ struct KvParams {
   int max_tok;      // w * groups + n_prompt: entries of the per-stream move list
   int prefix_mode;  // kv_prefix items: 0 = (stream, 128-row block, layer, K|V), 1 = tokens
   int paged;        // 1: REUSE runs rotate keys in place and leave values alone
+  int rope_mode;    // CS_ROPE_1D | CS_ROPE_MROPE
+  int mrope_t;      // M-RoPE: pairs of the temporal section (rotated by dt); the h / w sections stay
+  long long mrope_dt;  // M-RoPE: temporal position change of a reused token (-stride * t_per_frame)
   long long mv_off;  // byte offset of the move list inside a stream's workspace slice
   double inv_freq[cs::kMaxHeadDim / 2];  // base^(-2i/D), computed on the host
 };
@@ -240,7 +243,9 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
   // ---- (cos, sin) of R(dp), fp64 angle rounded to fp32 (reading Q20) -------------------------------------
   float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
   for (int i = tid; i < P.D / 2; i += blockDim.x) {
-    const double ang = static_cast<double>(s_dp) * P.inv_freq[i];
+    // position change of pair i: the sequence-index change (1-D RoPE) or its section's component (M-RoPE)
+    const long long delta = P.rope_mode == CS_ROPE_MROPE ? (i < P.mrope_t ? P.mrope_dt : 0ll) : (long long)s_dp;
+    const double ang = static_cast<double>(delta) * P.inv_freq[i];
     cs_tab[i] = make_float2(__double2float_rn(cos(ang)), __double2float_rn(sin(ang)));
   }
 }
@@ -1084,7 +1089,9 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   // ---- (cos, sin) of R(dp) ----------------------------------------------------------------------------------
   float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
   for (int i = tid; i < P.D / 2; i += blockDim.x) {
-    const double ang = static_cast<double>(s_dp) * P.inv_freq[i];
+    // position change of pair i: the sequence-index change (1-D RoPE) or its section's component (M-RoPE)
+    const long long delta = P.rope_mode == CS_ROPE_MROPE ? (i < P.mrope_t ? P.mrope_dt : 0ll) : (long long)s_dp;
+    const double ang = static_cast<double>(delta) * P.inv_freq[i];
     cs_tab[i] = make_float2(__double2float_rn(cos(ang)), __double2float_rn(sin(ang)));
   }
   if (st_local) atomicOr(&s_st, st_local);
@@ -1326,6 +1333,9 @@ static void fill_params(KvParams& P, const cs_grid* g, const cs_kv_desc* kv, con
   P.status = status;
   for (int i = 0; i < kv->head_dim / 2; ++i)
     P.inv_freq[i] = pow(kv->rope_base, -2.0 * static_cast<double>(i) / static_cast<double>(kv->head_dim));
+  P.rope_mode = kv->rope_mode;
+  P.mrope_t = kv->mrope_section[0];
+  P.mrope_dt = -static_cast<long long>(win->stride) * kv->t_per_frame;
 
 }
 

@@ -28,6 +28,8 @@ def make_grid(src_w: int, src_h: int, tau: float = 0.25, alpha: float = 0.0, mb_
 
 QWEN_KV = dict(layers=28, kv_heads=4, head_dim=128, dtype=0, rope_base=1e6)  # Qwen2-VL-7B shape, bf16
 TOY_KV = dict(layers=2, kv_heads=2, head_dim=16, dtype=1, rope_base=1e4)     # SPEC toy scale, fp32
+# Qwen2-VL multimodal RoPE: 64 frequency pairs split t/h/w = 16/24/24, one temporal position per frame (NEXT-3)
+QWEN_MROPE_KV = dict(QWEN_KV, rope_mode=1, mrope_section=(16, 24, 24), t_per_frame=1)
 
 # BASELINE.json configs with SURVEY §8(d) readings.  "scenes" is either a list cycled over stream ids or
 # the string "mixed" (even ids static, odd ids high-motion: C4).

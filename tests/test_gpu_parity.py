@@ -658,3 +658,36 @@ def test_paged_edge_cases(abi, ref):
         slot_old[0, 5] = pool_cap + 3
         _, _, refr = make_caches(kv, S, gen)
         run_paged_both(abi, ref, g, kv, win, mring, tring, pools, slot_old, slot_cap, refr if with_ref else None, tc)
+
+
+# ------------------------------------------------------------------------------------------------------------
+# M-RoPE position correction (NEXT-3), both KV modes
+# ------------------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [1, 0])
+def test_mrope_gpu_both_modes(abi, ref, dtype):
+    cfg = synth.CONFIGS["C1"]
+    g = make_grid(448, 448)
+    w, s, ring = 8, 2, 10
+    cap = w * 256 + 32
+    if dtype == 0:
+        base = dict(synth.QWEN_MROPE_KV, layers=2)
+    else:
+        base = dict(synth.TOY_KV, rope_mode=1, mrope_section=(2, 3, 3), t_per_frame=3)
+    kv = dict(base, capacity=cap, refresh_capacity=cap, n_prompt=32)
+    S = 5
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(12)
+    dt = torch.bfloat16 if dtype == 0 else torch.float32
+    shape = (kv["layers"], 2, cap, kv["kv_heads"], kv["head_dim"])
+    pools = [torch.randn(shape, generator=gen, device=DEV).to(dt) for _ in range(S)]
+    slot = None
+    stats = {}
+    for k in range(6):
+        mring, tring = stream_rings(ref, g, cfg, S, ring, k, w, s)
+        old, new, refr = make_caches(kv, S, gen)
+        win = dict(window=w, stride=s, step=k, ring_frames=ring)
+        gpu, o, new_h = run_kv_both(abi, ref, g, kv, win, mring, tring, old if k else None, new, refr, cap)
+        assert_kv_equal(gpu, o, new, new_h, kv, stats)
+        sn, _, st = run_paged_both(abi, ref, g, kv, win, mring, tring, pools, slot, cap, refr, cap)
+        slot = sn
+    print("mrope", dtype, stats)
