@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
 }
 
 // Gather one kept group (gr, gc) of `frame` into the warp tile and write it to packed rows [n0, n0 + G^2).
-template <int TP, int TG>
+template <int TP, int TG, int LAYOUT>
 __device__ __forceinline__ void gather_group(const CompactParams& P, const uint16_t* __restrict__ frame,
                                              bool vec_in, int gr, int gc, long long n0, int slot, int t_index,
                                              uint16_t* tile, int lane) {
@@ -135,7 +135,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
   const long long FW = P.FW;
   const uint16_t* src0 = frame + (long long)(gr * gp) * FW + (long long)gc * gp;
   const long long plane = (long long)P.FH * FW;
-  if (P.layout == CS_LAYOUT_GROUPED) {
+  if (LAYOUT == CS_LAYOUT_GROUPED) {
     // the kept group is one contiguous block already in packed order: straight 16-B copy (no smem staging)
     const int gs2 = G * G;
     long long nvalid = P.capacity - n0;
@@ -149,7 +149,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
       for (int e = n16 * 8 + lane; e < nel; e += 32) dst[e] = blk[e];  // tail of a truncated group
       const uint4* s4 = reinterpret_cast<const uint4*>(blk);
       uint4* d4 = reinterpret_cast<uint4*>(dst);
-      constexpr int kU = 10;
+      constexpr int kU = 5;
       for (int e0 = 0; e0 < n16; e0 += 32 * kU) {
         uint4 v[kU];
 #pragma unroll
@@ -250,8 +250,9 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
   __syncwarp();  // tile reusable
 }
 
-template <int TP, int TG>
-__global__ void __launch_bounds__(kGatherThreads, 2) compact_gather(const __grid_constant__ CompactParams P) {
+template <int TP, int TG, int LAYOUT>
+__global__ void __launch_bounds__(kGatherThreads, LAYOUT == CS_LAYOUT_GROUPED ? 4 : 2)
+    compact_gather(const __grid_constant__ CompactParams P) {
   extern __shared__ __align__(16) unsigned char g_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int G = TG > 0 ? TG : P.G;
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kGatherThreads, 2) compact_gather(const __grid
   long long q = total_groups * wid / nwarps;
   const long long q1 = total_groups * (wid + 1) / nwarps;
   if (q >= q1) return;
-  const int tile_bytes = tile_bytes_of(TP > 0 ? TP : P.p, G);
+  const int tile_bytes = LAYOUT == CS_LAYOUT_GROUPED ? 0 : tile_bytes_of(TP > 0 ? TP : P.p, G);
   uint16_t* tile = reinterpret_cast<uint16_t*>(g_smem + (size_t)wib * tile_bytes);
   uint32_t* mask = reinterpret_cast<uint32_t*>(g_smem + (size_t)kWarpsPerCta * tile_bytes) + wib * P.nw;
 
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kGatherThreads, 2) compact_gather(const __grid
     const uint16_t* frame = static_cast<const uint16_t*>(P.frames[slot]);
     const int t_index = __ldg(P.frame_index + slot);
     const int pe = TP > 0 ? TP : P.p;
-    const bool vec_in = P.layout == CS_LAYOUT_GROUPED
+    const bool vec_in = LAYOUT == CS_LAYOUT_GROUPED
                             ? (((reinterpret_cast<uintptr_t>(frame) & 15u) == 0) && ((3 * G * G * pe * pe * 2) % 16 == 0))
                             : (((reinterpret_cast<uintptr_t>(frame) & 7u) == 0) && ((P.FW & 3) == 0) &&
                                (((G * pe) & 3) == 0) && ((pe & 1) == 0));
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(kGatherThreads, 2) compact_gather(const __grid
         const int gi = base + b;
         const int gr = gi / P.ngc, gc = gi - gr * P.ngc;
         const long long n0 = q * gs2;
-        if (n0 < P.capacity) gather_group<TP, TG>(P, frame, vec_in, gr, gc, n0, slot, t_index, tile, lane);
+        if (n0 < P.capacity) gather_group<TP, TG, LAYOUT>(P, frame, vec_in, gr, gc, n0, slot, t_index, tile, lane);
         ++q;
       }
     }
@@ -357,15 +358,20 @@ int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, con
   compact_scan<<<1, kScanThreads, 0, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   if (P.n_slots == 0 || capacity == 0) return CS_OK;
-  const int grid = cs_num_sms() * 4;
-  const size_t smem = (size_t)kWarpsPerCta * (tile_bytes_of(g->patch, g->group) + 4 * P.nw);
-  if (g->patch == 14 && g->group == 2) {
-    if (cs_set_smem_attr(reinterpret_cast<const void*>(compact_gather<14, 2>), 1, 96 * 1024)) return CS_ERR_CUDA;
-    compact_gather<14, 2><<<grid, kGatherThreads, smem, stream>>>(P);
-  } else {
-    if (cs_set_smem_attr(reinterpret_cast<const void*>(compact_gather<0, 0>), 2, 96 * 1024)) return CS_ERR_CUDA;
-    compact_gather<0, 0><<<grid, kGatherThreads, smem, stream>>>(P);
-  }
+  const bool grouped = frame_layout == CS_LAYOUT_GROUPED;
+  const size_t smem = (size_t)kWarpsPerCta * ((grouped ? 0 : tile_bytes_of(g->patch, g->group)) + 4 * P.nw);
+  const bool fast = g->patch == 14 && g->group == 2;
+  const void* fn = fast ? (grouped ? reinterpret_cast<const void*>(compact_gather<14, 2, 1>)
+                                   : reinterpret_cast<const void*>(compact_gather<14, 2, 0>))
+                        : (grouped ? reinterpret_cast<const void*>(compact_gather<0, 0, 1>)
+                                   : reinterpret_cast<const void*>(compact_gather<0, 0, 0>));
+  const int slot = 1 + (fast ? 0 : 2) + (grouped ? 1 : 0) + 10;
+  if (cs_set_smem_attr(fn, slot, 96 * 1024)) return CS_ERR_CUDA;
+  const int grid = cs_num_sms() * (grouped ? 8 : 4);
+  if (fast && grouped) compact_gather<14, 2, 1><<<grid, kGatherThreads, smem, stream>>>(P);
+  else if (fast) compact_gather<14, 2, 0><<<grid, kGatherThreads, smem, stream>>>(P);
+  else if (grouped) compact_gather<0, 0, 1><<<grid, kGatherThreads, smem, stream>>>(P);
+  else compact_gather<0, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
 }
