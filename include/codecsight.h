@@ -188,6 +188,39 @@ int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, co
                        int32_t* frame_offsets, unsigned long long* counters, int32_t* status,
                        cudaStream_t stream);
 
+/* ------------------------------------------------------------------------------------------------------------
+ * codecsight_compact_nv12 — NEXT-2: the GPU preprocessing fused into the compaction ("Resizing, color-space
+ * conversion, and normalization are fused into a single batched operation over all frames"): the frames are the
+ * decoder's NV12 output and only the kept groups are converted, resized and normalised -- pruned patches are never
+ * preprocessed.  A model-input pixel (c, y, x) of the (grid_h*patch) x (grid_w*patch) input is, in fp32 and in
+ * this order:
+ *   colour  BT.601 limited range: R = 1.164383(Y-16) + 1.596027(V-128), G = (1.164383(Y-16) - 0.391762(U-128))
+ *           - 0.812968(V-128), B = 1.164383(Y-16) + 2.017232(U-128), each clamped to [0, 255]; the chroma of
+ *           source pixel (y, x) is UV[y/2][2(x/2)], UV[y/2][2(x/2)+1]
+ *   resize  bilinear with half-pixel centres (PyTorch interpolate, align_corners=False, no antialias):
+ *           f = (o + 0.5)(src/M) - 0.5 clamped at 0, i0 = floor f, i1 = i0 + (i0 < src-1), l = f - i0,
+ *           v = (1-ly)((1-lx)p00 + lx p01) + ly((1-lx)p10 + lx p11)
+ *   scale   out = (v/255 - mean[c]) / std[c], stored bf16 (RNE)
+ * Outputs, order and capacity semantics are those of codecsight_compact.
+ *   pp         host  source geometry and normalisation
+ *   y_planes   device [n_slots] device pointers to Y planes   [src_h][y_pitch] u8
+ *   uv_planes  device [n_slots] device pointers to UV planes  [src_h/2][uv_pitch] u8 (U, V interleaved)
+ * --------------------------------------------------------------------------------------------------------- */
+enum { CS_COLOR_BT601_LIMITED = 0 };
+typedef struct {
+  int32_t src_w, src_h;      /* decoded frame size in px, even, <= 16384                                     */
+  int32_t y_pitch, uv_pitch; /* bytes per row of the Y and UV planes (>= src_w)                              */
+  int32_t color;             /* CS_COLOR_BT601_LIMITED                                                       */
+  float mean[3], std[3];     /* per-channel normalisation of v/255 (Qwen2-VL / CLIP: 0.4815 0.4578 0.4082,
+                                0.2686 0.2613 0.2758)                                                        */
+} cs_preprocess;
+
+int codecsight_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n_streams, int32_t n_frames,
+                            const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* frame_index,
+                            const void* const* y_planes, const void* const* uv_planes, int64_t capacity,
+                            void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
+                            unsigned long long* counters, int32_t* status, cudaStream_t stream);
+
 /* KV cache description.  One cache buffer (one stream, one window) is laid out as
  *   [layers][2 (K, V)][capacity][kv_heads][head_dim]  of dtype,
  * so one (token, layer, K-or-V) row is kv_heads*head_dim contiguous elements.                                */

@@ -643,3 +643,137 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
   free(tfrm);
   return 0;
 }
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* NEXT-2: GPU preprocessing fused into the compaction ("Resizing, color-space conversion, and      */
+/* normalization are fused into a single batched operation over all frames").  Decoded frames arrive as   */
+/* NV12 (NVDEC's output: a Y plane and an interleaved 2x2-subsampled UV plane).  A model-input pixel      */
+/* (c, y, x) of the MH x MW input (MH = grid_h*patch, MW = grid_w*patch) is defined, in fp32 and in this   */
+/* order (reading NEXT-2):                                                                                 */
+/*   colour  BT.601 limited range: R = kY(Y-16) + kRV(V-128), G = (kY(Y-16) - kGU(U-128)) - kGV(V-128),     */
+/*           B = kY(Y-16) + kBU(U-128), clamped to [0, 255]; chroma of pixel (y, x) at UV row y/2, col x/2  */
+/*   resize  bilinear, half-pixel centres (PyTorch interpolate align_corners=False, antialias=False):      */
+/*           f = (o + 0.5) * (src/M) - 0.5, clamped at 0; i0 = floor(f), i1 = i0 + (i0 < src-1),           */
+/*           l = f - i0; value = (1-ly)((1-lx) p00 + lx p01) + ly((1-lx) p10 + lx p11)                     */
+/*   scale   t = value / 255; out = (t - mean_c) / std_c; stored as bf16 (RNE).                            */
+/* ---------------------------------------------------------------------------------------------------- */
+static const float REF_KY = 1.164383f, REF_KRV = 1.596027f, REF_KGU = 0.391762f, REF_KGV = 0.812968f,
+                   REF_KBU = 2.017232f;
+
+static float ref_clamp255(float v) { return v < 0.0f ? 0.0f : (v > 255.0f ? 255.0f : v); }
+
+void codecsight_ref_nv12_rgb(const uint8_t* Y, const uint8_t* UV, const ref_pre* pp, int64_t y, int64_t x,
+                             float rgb[3]) {
+  const float c = (float)((int32_t)Y[y * pp->y_pitch + x] - 16);
+  const float d = (float)((int32_t)UV[(y / 2) * pp->uv_pitch + 2 * (x / 2)] - 128);
+  const float e = (float)((int32_t)UV[(y / 2) * pp->uv_pitch + 2 * (x / 2) + 1] - 128);
+  rgb[0] = ref_clamp255(REF_KY * c + REF_KRV * e);
+  rgb[1] = ref_clamp255((REF_KY * c - REF_KGU * d) - REF_KGV * e);
+  rgb[2] = ref_clamp255(REF_KY * c + REF_KBU * d);
+}
+
+/* source index pair and weight of model coordinate o along an axis of `src` source and `m` model pixels */
+static void ref_axis(int64_t o, int64_t src, int64_t m, int64_t* i0, int64_t* i1, float* l) {
+  const float scale = (float)src / (float)m;
+  float f = ((float)o + 0.5f) * scale - 0.5f;
+  if (f < 0.0f) f = 0.0f;
+  *i0 = (int64_t)f; /* f >= 0: truncation is floor */
+  *i1 = *i0 + (*i0 < src - 1 ? 1 : 0);
+  *l = f - (float)*i0;
+}
+
+float codecsight_ref_model_pixel(const ref_grid* g, const ref_pre* pp, const uint8_t* Y, const uint8_t* UV, int64_t c,
+                                 int64_t yo, int64_t xo) {
+  const int64_t MH = (int64_t)g->grid_h * g->patch, MW = (int64_t)g->grid_w * g->patch;
+  int64_t y0, y1, x0, x1;
+  float ly, lx;
+  ref_axis(yo, pp->src_h, MH, &y0, &y1, &ly);
+  ref_axis(xo, pp->src_w, MW, &x0, &x1, &lx);
+  float p00[3], p01[3], p10[3], p11[3];
+  codecsight_ref_nv12_rgb(Y, UV, pp, y0, x0, p00);
+  codecsight_ref_nv12_rgb(Y, UV, pp, y0, x1, p01);
+  codecsight_ref_nv12_rgb(Y, UV, pp, y1, x0, p10);
+  codecsight_ref_nv12_rgb(Y, UV, pp, y1, x1, p11);
+  const float hx = 1.0f - lx, hy = 1.0f - ly;
+  const float top = hx * p00[c] + lx * p01[c];
+  const float bot = hx * p10[c] + lx * p11[c];
+  const float v = hy * top + ly * bot;
+  const float t = v / 255.0f;
+  return (t - pp->mean[c]) / pp->stdv[c];
+}
+
+static int ref_pre_ok(const ref_pre* pp) {
+  if (!pp) return -1;
+  if (pp->src_w < 2 || pp->src_h < 2 || pp->src_w % 2 || pp->src_h % 2 || pp->src_w > 16384 || pp->src_h > 16384)
+    return -2;
+  if (pp->y_pitch < pp->src_w || pp->uv_pitch < pp->src_w) return -2;
+  if (pp->color != 0) return -3;
+  for (int c = 0; c < 3; ++c)
+    if (!(pp->stdv[c] > 0.0f) || isnan(pp->mean[c])) return -1;
+  return 0;
+}
+
+void codecsight_ref_preprocess_frame(const ref_grid* g, const ref_pre* pp, const uint8_t* Y, const uint8_t* UV,
+                                     uint16_t* out) {
+  const int64_t MH = (int64_t)g->grid_h * g->patch, MW = (int64_t)g->grid_w * g->patch;
+  for (int64_t c = 0; c < 3; ++c)
+    for (int64_t y = 0; y < MH; ++y)
+      for (int64_t x = 0; x < MW; ++x)
+        out[(c * MH + y) * MW + x] = ref_f32_to_bf16(codecsight_ref_model_pixel(g, pp, Y, UV, c, y, x));
+}
+
+int codecsight_ref_compact_nv12(const ref_grid* g, const ref_pre* pp, int32_t n_streams, int32_t n_frames,
+                                const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* frame_index,
+                                const void* const* y_planes, const void* const* uv_planes, int64_t capacity,
+                                void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
+                                unsigned long long* counters, int32_t* status) {
+  int rc = ref_grid_ok(g);
+  if (rc) return rc;
+  if ((rc = ref_pre_ok(pp))) return rc;
+  if (n_streams < 0 || n_frames < 1 || mask_frame_stride < n_frames || capacity < 0) return -1;
+  const int64_t np = (int64_t)g->grid_w * g->grid_h, nw = ref_words(g), G = g->group, p = g->patch;
+  const int64_t n_slots = (int64_t)n_streams * n_frames;
+  if (n_slots * np >= 2147483648LL) return -3;
+  if (!frame_offsets || !counters || !status) return -1;
+  if (n_slots > 0 && (!keep_mask || !frame_index || !y_planes || !uv_planes)) return -1;
+  if (capacity > 0 && (!packed || !pos_ids || !src_index)) return -1;
+  const int64_t row = 3 * p * p;
+  uint16_t* out = (uint16_t*)packed;
+  int64_t off = 0, written = 0;
+  for (int64_t s = 0; s < n_streams; ++s)
+    for (int64_t j = 0; j < n_frames; ++j) {
+      const int64_t slot = s * n_frames + j;
+      const uint32_t* m = keep_mask + (s * mask_frame_stride + j) * nw;
+      const uint8_t* Y = (const uint8_t*)y_planes[slot];
+      const uint8_t* UV = (const uint8_t*)uv_planes[slot];
+      frame_offsets[slot] = (int32_t)off;
+      for (int64_t gr = 0; gr < g->grid_h / G; ++gr)
+        for (int64_t gc = 0; gc < g->grid_w / G; ++gc) {
+          int any = 0;
+          for (int64_t dy = 0; dy < G; ++dy)
+            for (int64_t dx = 0; dx < G; ++dx) any |= ref_bit(m, (gr * G + dy) * g->grid_w + gc * G + dx);
+          if (!any) continue;
+          for (int64_t dy = 0; dy < G; ++dy)
+            for (int64_t dx = 0; dx < G; ++dx) {
+              const int64_t h = gr * G + dy, w = gc * G + dx, n = off++;
+              if (n >= capacity) { *status |= REF_ST_CAPACITY; continue; }
+              for (int64_t c = 0; c < 3; ++c)
+                for (int64_t y = 0; y < p; ++y)
+                  for (int64_t x = 0; x < p; ++x)
+                    out[n * row + c * p * p + y * p + x] =
+                        ref_f32_to_bf16(codecsight_ref_model_pixel(g, pp, Y, UV, c, h * p + y, w * p + x));
+              pos_ids[3 * n + 0] = frame_index[slot];
+              pos_ids[3 * n + 1] = (int32_t)h;
+              pos_ids[3 * n + 2] = (int32_t)w;
+              src_index[n] = (int32_t)(slot * np + h * g->grid_w + w);
+              ++written;
+            }
+        }
+    }
+  frame_offsets[n_slots] = (int32_t)off;
+  counters[REF_C_PACKED_ROWS] += (unsigned long long)written;
+  /* algorithmic bytes: masks + offsets, and per written row its output (+16 B of ids); the source pixels a row
+     needs are counted by the caller (they depend on the scale) */
+  counters[REF_C_BYTES_COMPACT] += (unsigned long long)(n_slots * (4 * nw + 4) + written * (row * 2 + 16));
+  return 0;
+}

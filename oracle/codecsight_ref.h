@@ -105,6 +105,24 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
                                     int32_t* p_old, int32_t* n_tokens, unsigned long long* counters,
                                     int32_t* status);
 
+/* NEXT-2: NV12 -> RGB -> bilinear resize -> normalise, fused into the compaction. */
+typedef struct {
+  int32_t src_w, src_h, y_pitch, uv_pitch;
+  int32_t color; /* 0 = BT.601 limited range */
+  float mean[3], stdv[3];
+} ref_pre;
+void codecsight_ref_nv12_rgb(const uint8_t* Y, const uint8_t* UV, const ref_pre* pp, int64_t y, int64_t x,
+                             float rgb[3]);
+float codecsight_ref_model_pixel(const ref_grid* g, const ref_pre* pp, const uint8_t* Y, const uint8_t* UV, int64_t c,
+                                 int64_t yo, int64_t xo);
+void codecsight_ref_preprocess_frame(const ref_grid* g, const ref_pre* pp, const uint8_t* Y, const uint8_t* UV,
+                                     uint16_t* out);
+int codecsight_ref_compact_nv12(const ref_grid* g, const ref_pre* pp, int32_t n_streams, int32_t n_frames,
+                                const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* frame_index,
+                                const void* const* y_planes, const void* const* uv_planes, int64_t capacity,
+                                void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
+                                unsigned long long* counters, int32_t* status);
+
 /* Eq. 5 on one fp32 key vector of n_heads x head_dim: out = R(dp) k (rotate_half pairing). */
 void codecsight_ref_rope_rotate_f32(const float* k, int32_t n_heads, int32_t head_dim, double base, int64_t dp,
                                     float* out);

@@ -41,6 +41,20 @@ class RefKv(C.Structure):
                 ("t_per_frame", C.c_int32)]
 
 
+class RefPre(C.Structure):
+    _fields_ = [("src_w", C.c_int32), ("src_h", C.c_int32), ("y_pitch", C.c_int32), ("uv_pitch", C.c_int32),
+                ("color", C.c_int32), ("mean", C.c_float * 3), ("stdv", C.c_float * 3)]
+
+
+CLIP_MEAN = (0.48145466, 0.4578275, 0.40821073)   # Qwen2-VL / CLIP image normalisation
+CLIP_STD = (0.26862954, 0.26130258, 0.27577711)
+
+
+def make_pre(src_w, src_h, y_pitch=None, uv_pitch=None, mean=CLIP_MEAN, std=CLIP_STD, color=0) -> RefPre:
+    return RefPre(src_w, src_h, y_pitch or src_w, uv_pitch or src_w, color, (C.c_float * 3)(*mean),
+                  (C.c_float * 3)(*std))
+
+
 class RefWindow(C.Structure):
     _fields_ = [("window", C.c_int32), ("stride", C.c_int32), ("step", C.c_int32), ("ring_frames", C.c_int32)]
 
@@ -79,6 +93,16 @@ def lib():
         L.codecsight_ref_kv_refresh_paged.argtypes = [C.POINTER(RefGrid), C.POINTER(RefKv), C.POINTER(RefWindow),
                                                       C.c_int32, P, P, P, P, P, C.c_int64, P, C.c_int64, P, P, P,
                                                       P, P]
+        L.codecsight_ref_nv12_rgb.restype = None
+        L.codecsight_ref_nv12_rgb.argtypes = [P, P, C.POINTER(RefPre), C.c_int64, C.c_int64, P]
+        L.codecsight_ref_model_pixel.restype = C.c_float
+        L.codecsight_ref_model_pixel.argtypes = [C.POINTER(RefGrid), C.POINTER(RefPre), P, P, C.c_int64, C.c_int64,
+                                                 C.c_int64]
+        L.codecsight_ref_preprocess_frame.restype = None
+        L.codecsight_ref_preprocess_frame.argtypes = [C.POINTER(RefGrid), C.POINTER(RefPre), P, P, P]
+        L.codecsight_ref_compact_nv12.restype = C.c_int
+        L.codecsight_ref_compact_nv12.argtypes = [C.POINTER(RefGrid), C.POINTER(RefPre), C.c_int32, C.c_int32, P,
+                                                  C.c_int64, P, P, P, C.c_int64, P, P, P, P, P, P]
         L.codecsight_ref_rope_rotate_f32.restype = None
         L.codecsight_ref_rope_rotate_f32.argtypes = [P, C.c_int32, C.c_int32, C.c_double, C.c_int64, P]
         _lib = L
@@ -246,3 +270,45 @@ def rope_rotate_f32(k: np.ndarray, n_heads: int, head_dim: int, base: float, dp:
     out = np.zeros_like(k)
     lib().codecsight_ref_rope_rotate_f32(_p(k), n_heads, head_dim, base, dp, _p(out))
     return out
+
+
+def nv12_rgb(Y: np.ndarray, UV: np.ndarray, pre: RefPre, y: int, x: int) -> np.ndarray:
+    out = np.zeros(3, np.float32)
+    lib().codecsight_ref_nv12_rgb(_p(Y), _p(UV), C.byref(pre), y, x, _p(out))
+    return out
+
+
+def preprocess_frame(g: dict, pre: RefPre, Y: np.ndarray, UV: np.ndarray) -> np.ndarray:
+    """Full-frame preprocessing -> planar [3][MH][MW] bf16 bits."""
+    MH, MW = g["grid_h"] * g["patch"], g["grid_w"] * g["patch"]
+    out = np.zeros((3, MH, MW), np.uint16)
+    lib().codecsight_ref_preprocess_frame(C.byref(make_grid(g)), C.byref(pre), _p(np.ascontiguousarray(Y)),
+                                          _p(np.ascontiguousarray(UV)), _p(out))
+    return out
+
+
+def compact_nv12(g: dict, pre: RefPre, keep_mask: np.ndarray, frame_index: np.ndarray, y_planes: list,
+                 uv_planes: list, capacity: int, n_streams: int, n_frames: int,
+                 mask_frame_stride: int | None = None, counters: np.ndarray | None = None):
+    nw = grid_words(g)
+    mfs = n_frames if mask_frame_stride is None else mask_frame_stride
+    keep_mask = np.ascontiguousarray(keep_mask, dtype=np.uint32).reshape(n_streams, mfs, nw)
+    n_slots = n_streams * n_frames
+    frame_index = np.ascontiguousarray(frame_index, dtype=np.int32).reshape(n_slots)
+    ys = [np.ascontiguousarray(a, dtype=np.uint8) for a in y_planes]
+    uvs = [np.ascontiguousarray(a, dtype=np.uint8) for a in uv_planes]
+    yp = (C.c_void_p * max(1, n_slots))(*[a.ctypes.data for a in ys])
+    uvp = (C.c_void_p * max(1, n_slots))(*[a.ctypes.data for a in uvs])
+    row = 3 * g["patch"] * g["patch"]
+    packed = np.zeros((max(capacity, 0), row), np.uint16)
+    pos = np.zeros((max(capacity, 0), 3), np.int32)
+    src = np.zeros(max(capacity, 0), np.int32)
+    offs = np.zeros(n_slots + 1, np.int32)
+    counters = np.zeros(NCOUNTERS, np.uint64) if counters is None else counters
+    status = np.zeros(1, np.int32)
+    rc = lib().codecsight_ref_compact_nv12(C.byref(make_grid(g)), C.byref(pre), n_streams, n_frames, _p(keep_mask),
+                                           mfs, _p(frame_index), C.cast(yp, C.c_void_p), C.cast(uvp, C.c_void_p),
+                                           capacity, _p(packed), _p(pos), _p(src), _p(offs), _p(counters),
+                                           _p(status))
+    return dict(rc=rc, packed=packed, pos_ids=pos, src_index=src, frame_offsets=offs, counters=counters,
+                status=int(status[0]))

@@ -49,6 +49,21 @@ class CsKvDesc(C.Structure):
 CS_ROPE_1D, CS_ROPE_MROPE = 0, 1
 
 
+class CsPreprocess(C.Structure):
+    _fields_ = [("src_w", C.c_int32), ("src_h", C.c_int32), ("y_pitch", C.c_int32), ("uv_pitch", C.c_int32),
+                ("color", C.c_int32), ("mean", C.c_float * 3), ("std", C.c_float * 3)]
+
+
+CLIP_MEAN = (0.48145466, 0.4578275, 0.40821073)
+CLIP_STD = (0.26862954, 0.26130258, 0.27577711)
+
+
+def make_preprocess(pre: dict) -> CsPreprocess:
+    return CsPreprocess(pre["src_w"], pre["src_h"], pre.get("y_pitch", pre["src_w"]), pre.get("uv_pitch", pre["src_w"]),
+                        pre.get("color", 0), (C.c_float * 3)(*pre.get("mean", CLIP_MEAN)),
+                        (C.c_float * 3)(*pre.get("std", CLIP_STD)))
+
+
 class CsWindow(C.Structure):
     _fields_ = [("window", C.c_int32), ("stride", C.c_int32), ("step", C.c_int32), ("ring_frames", C.c_int32)]
 
@@ -68,6 +83,9 @@ def lib():
         L.codecsight_score_patches.argtypes = [C.POINTER(CsGrid), I32, I32, P, P, P, I64, P, P, P, P, P, P]
         L.codecsight_compact.restype = C.c_int
         L.codecsight_compact.argtypes = [C.POINTER(CsGrid), I32, I32, P, I64, P, P, I32, I64, P, P, P, P, P, P, P]
+        L.codecsight_compact_nv12.restype = C.c_int
+        L.codecsight_compact_nv12.argtypes = [C.POINTER(CsGrid), C.POINTER(CsPreprocess), I32, I32, P, I64, P, P, P,
+                                              I64, P, P, P, P, P, P, P]
         L.codecsight_kv_refresh.restype = C.c_int
         L.codecsight_kv_refresh.argtypes = [C.POINTER(CsGrid), C.POINTER(CsKvDesc), C.POINTER(CsWindow), I32, P, P,
                                             P, P, P, I64, P, P, P, P, C.c_size_t, P, P, P]
@@ -157,6 +175,16 @@ def codecsight_compact(g: dict, n_streams: int, n_frames: int, keep_mask, mask_f
     _check(rc, "codecsight_compact")
 
 
+def codecsight_compact_nv12(g: dict, pre: dict, n_streams: int, n_frames: int, keep_mask, mask_frame_stride: int,
+                            frame_index, y_ptrs, uv_ptrs, capacity: int, packed, pos_ids, src_index, frame_offsets,
+                            counters, status, stream=None) -> None:
+    rc = lib().codecsight_compact_nv12(C.byref(make_grid(g)), C.byref(make_preprocess(pre)), n_streams, n_frames,
+                                       _ptr(keep_mask), mask_frame_stride, _ptr(frame_index), _ptr(y_ptrs),
+                                       _ptr(uv_ptrs), capacity, _ptr(packed), _ptr(pos_ids), _ptr(src_index),
+                                       _ptr(frame_offsets), _ptr(counters), _ptr(status), _stream(stream))
+    _check(rc, "codecsight_compact_nv12")
+
+
 def kv_workspace_size(kv: dict, win: dict, n_streams: int) -> int:
     return int(lib().codecsight_kv_refresh_workspace_size(C.byref(make_kv(kv)), C.byref(make_window(win)),
                                                           n_streams))
@@ -195,4 +223,5 @@ def codecsight_kv_refresh_paged(g: dict, kv: dict, win: dict, n_streams: int, ke
 kv_refresh_paged = codecsight_kv_refresh_paged
 score_patches = codecsight_score_patches
 compact = codecsight_compact
+compact_nv12 = codecsight_compact_nv12
 kv_refresh = codecsight_kv_refresh

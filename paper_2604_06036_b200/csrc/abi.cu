@@ -152,6 +152,33 @@ size_t codecsight_kv_refresh_paged_workspace_size(const cs_grid* g, const cs_kv_
   return cs_kv_paged_workspace_bytes(g, kv, win, n_streams);
 }
 
+int codecsight_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n_streams, int32_t n_frames,
+                            const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* frame_index,
+                            const void* const* y_planes, const void* const* uv_planes, int64_t capacity,
+                            void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
+                            unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+  int rc = grid_ok(g);
+  if (rc) return rc;
+  if (!pp) return CS_ERR_INVALID_ARGUMENT;
+  if (pp->src_w < 2 || pp->src_h < 2 || (pp->src_w & 1) || (pp->src_h & 1) || pp->src_w > 16384 ||
+      pp->src_h > 16384 || pp->y_pitch < pp->src_w || pp->uv_pitch < pp->src_w)
+    return CS_ERR_SHAPE;
+  if (pp->color != CS_COLOR_BT601_LIMITED) return CS_ERR_UNSUPPORTED;
+  for (int c = 0; c < 3; ++c)
+    if (!(pp->std[c] > 0.0f) || isnan(pp->mean[c])) return CS_ERR_INVALID_ARGUMENT;
+  if (n_streams < 0 || n_frames < 1 || mask_frame_stride < n_frames || capacity < 0) return CS_ERR_INVALID_ARGUMENT;
+  const long long n_slots = static_cast<long long>(n_streams) * n_frames;
+  if (n_slots * g->grid_w * g->grid_h >= 2147483648LL) return CS_ERR_UNSUPPORTED;
+  if (g->group * g->patch > 32) return CS_ERR_UNSUPPORTED;
+  if (!frame_offsets || !counters || !status) return CS_ERR_INVALID_ARGUMENT;
+  if (n_slots > 0 && (!keep_mask || !frame_index || !y_planes || !uv_planes)) return CS_ERR_INVALID_ARGUMENT;
+  if (capacity > 0 && (!packed || !pos_ids || !src_index)) return CS_ERR_INVALID_ARGUMENT;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_compact_nv12(g, pp, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, y_planes,
+                                uv_planes, capacity, packed, pos_ids, src_index, frame_offsets, counters, status,
+                                stream);
+}
+
 size_t codecsight_kv_refresh_workspace_size(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams) {
   if (!kv || !win || n_streams < 0 || win->window < 1 || kv->head_dim < 2 || kv->head_dim > cs::kMaxHeadDim)
     return 0;

@@ -20,6 +20,8 @@ constexpr int kScanThreads = 1024;
 constexpr int kGatherThreads = 256;
 constexpr int kWarpsPerCta = kGatherThreads / 32;
 
+constexpr int kLayoutNV12 = 2;  // internal: frames are decoded NV12 planes, preprocessing fused (NEXT-2)
+
 // per-warp tile of one group in packed order: 3 x (group*patch)^2 bf16, padded to 16 B
 __host__ __device__ __forceinline__ int tile_bytes_of(int p, int G) { return ((3 * G * G * p * p * 2) + 15) & ~15; }
 
@@ -30,7 +32,12 @@ struct CompactParams {
   long long capacity;
   int FH, FW;  // model-input frame height / width in pixels
   int vec_out;
-  int layout;  // CS_LAYOUT_PLANAR | CS_LAYOUT_GROUPED
+  int layout;  // CS_LAYOUT_PLANAR | CS_LAYOUT_GROUPED | kLayoutNV12
+  // NV12 source (fused preprocessing, NEXT-2)
+  int src_w, src_h, y_pitch, uv_pitch;
+  float scale_y, scale_x;  // src / model, fp32 (computed once on the host, IEEE division)
+  float mean[3], stdv[3];
+  const void* const* uv_planes;
   const uint32_t* keep_mask;
   const int32_t* frame_index;
   const void* const* frames;
@@ -123,6 +130,29 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
   }
 }
 
+
+// ---- fused preprocessing (NEXT-2): NV12 -> RGB (BT.601 limited) -> bilinear resize -> /255 -> normalise ------
+// Same fp32 operations in the same order as the oracle (oracle/codecsight_ref.c, codecsight_ref_model_pixel).
+__device__ __forceinline__ void nv12_rgb(const uint8_t* __restrict__ Y, const uint8_t* __restrict__ UV,
+                                         const CompactParams& P, int y, int x, float rgb[3]) {
+  const float c = static_cast<float>(static_cast<int>(__ldg(Y + (long long)y * P.y_pitch + x)) - 16);
+  const uint8_t* uv = UV + (long long)(y >> 1) * P.uv_pitch + 2 * (x >> 1);
+  const float d = static_cast<float>(static_cast<int>(__ldg(uv)) - 128);
+  const float e = static_cast<float>(static_cast<int>(__ldg(uv + 1)) - 128);
+  const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
+  rgb[0] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kRV, e)), 0.0f), 255.0f);
+  rgb[1] = fminf(fmaxf(__fsub_rn(__fsub_rn(__fmul_rn(kY, c), __fmul_rn(kGU, d)), __fmul_rn(kGV, e)), 0.0f), 255.0f);
+  rgb[2] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kBU, d)), 0.0f), 255.0f);
+}
+
+__device__ __forceinline__ void nv12_axis(int o, int src, float scale, int& i0, int& i1, float& l) {
+  float f = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(o), 0.5f), scale), 0.5f);
+  f = f < 0.0f ? 0.0f : f;
+  i0 = static_cast<int>(f);
+  i1 = i0 + (i0 < src - 1 ? 1 : 0);
+  l = __fsub_rn(f, static_cast<float>(i0));
+}
+
 // Gather one kept group (gr, gc) of `frame` into the warp tile and write it to packed rows [n0, n0 + G^2).
 template <int TP, int TG, int LAYOUT>
 __device__ __forceinline__ void gather_group(const CompactParams& P, const uint16_t* __restrict__ frame,
@@ -178,7 +208,34 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     }
     return;
   }
-  if (vec_in) {
+  if (LAYOUT == kLayoutNV12) {
+    // preprocess only the kept group's 3 x gp x gp model pixels straight from the decoded NV12 frame
+    const uint8_t* Yp = reinterpret_cast<const uint8_t*>(frame);
+    const uint8_t* UVp = static_cast<const uint8_t*>(P.uv_planes[slot]);
+    for (int e = lane; e < gp * gp; e += 32) {
+      const int yy = e / gp, xx = e - yy * gp;
+      int y0, y1, x0, x1;
+      float ly, lx;
+      nv12_axis(gr * gp + yy, P.src_h, P.scale_y, y0, y1, ly);
+      nv12_axis(gc * gp + xx, P.src_w, P.scale_x, x0, x1, lx);
+      float p00[3], p01[3], p10[3], p11[3];
+      nv12_rgb(Yp, UVp, P, y0, x0, p00);
+      nv12_rgb(Yp, UVp, P, y0, x1, p01);
+      nv12_rgb(Yp, UVp, P, y1, x0, p10);
+      nv12_rgb(Yp, UVp, P, y1, x1, p11);
+      const float hx = __fsub_rn(1.0f, lx), hy = __fsub_rn(1.0f, ly);
+      const int dy = yy / p, y = yy - dy * p, dx = xx / p, x = xx - dx * p;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float top = __fadd_rn(__fmul_rn(hx, p00[c]), __fmul_rn(lx, p01[c]));
+        const float bot = __fadd_rn(__fmul_rn(hx, p10[c]), __fmul_rn(lx, p11[c]));
+        const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
+        const float t = __fdiv_rn(v, 255.0f);
+        const float o = __fdiv_rn(__fsub_rn(t, P.mean[c]), P.stdv[c]);
+        tile[((dy * G + dx) * 3 + c) * pp + y * p + x] = static_cast<uint16_t>(cs::f32_to_bf16_rne(o));
+      }
+    }
+  } else if (vec_in) {
     // 8-byte loads: each group row segment is gp pixels = gp/4 pieces of 4 bf16.  Pairs of pixels never
     // straddle a patch boundary (p even), so the tile is written with 4-byte stores.
     const int cpr = gp / 4;
@@ -318,10 +375,11 @@ __global__ void __launch_bounds__(kGatherThreads, LAYOUT == CS_LAYOUT_GROUPED ? 
 
 }  // namespace
 
-int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
-                      int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
-                      int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
-                      int32_t* frame_offsets,
+static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t n_streams, int32_t n_frames,
+                          const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* frame_index,
+                          const void* const* frames, const void* const* uv_planes, int32_t frame_layout,
+                          int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                          int32_t* frame_offsets,
                       unsigned long long* counters, int32_t* status, cudaStream_t stream) {
   CompactParams P{};
   P.grid_w = g->grid_w;
@@ -345,6 +403,19 @@ int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, con
   P.vec_out = ((reinterpret_cast<uintptr_t>(packed) & 15u) == 0 &&
                ((row_bytes * g->group * g->group) % 16) == 0) ? 1 : 0;
   P.layout = frame_layout;
+  if (pre) {
+    P.src_w = pre->src_w;
+    P.src_h = pre->src_h;
+    P.y_pitch = pre->y_pitch;
+    P.uv_pitch = pre->uv_pitch;
+    P.scale_y = static_cast<float>(pre->src_h) / static_cast<float>(P.FH);
+    P.scale_x = static_cast<float>(pre->src_w) / static_cast<float>(P.FW);
+    for (int c = 0; c < 3; ++c) {
+      P.mean[c] = pre->mean[c];
+      P.stdv[c] = pre->std[c];
+    }
+    P.uv_planes = uv_planes;
+  }
   P.keep_mask = keep_mask;
   P.frame_index = frame_index;
   P.frames = frames;
@@ -359,19 +430,45 @@ int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, con
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   if (P.n_slots == 0 || capacity == 0) return CS_OK;
   const bool grouped = frame_layout == CS_LAYOUT_GROUPED;
+  const bool nv12 = frame_layout == kLayoutNV12;
   const size_t smem = (size_t)kWarpsPerCta * ((grouped ? 0 : tile_bytes_of(g->patch, g->group)) + 4 * P.nw);
   const bool fast = g->patch == 14 && g->group == 2;
-  const void* fn = fast ? (grouped ? reinterpret_cast<const void*>(compact_gather<14, 2, 1>)
-                                   : reinterpret_cast<const void*>(compact_gather<14, 2, 0>))
-                        : (grouped ? reinterpret_cast<const void*>(compact_gather<0, 0, 1>)
-                                   : reinterpret_cast<const void*>(compact_gather<0, 0, 0>));
-  const int slot = 1 + (fast ? 0 : 2) + (grouped ? 1 : 0) + 10;
-  if (cs_set_smem_attr(fn, slot, 96 * 1024)) return CS_ERR_CUDA;
   const int grid = cs_num_sms() * (grouped ? 8 : 4);
-  if (fast && grouped) compact_gather<14, 2, 1><<<grid, kGatherThreads, smem, stream>>>(P);
-  else if (fast) compact_gather<14, 2, 0><<<grid, kGatherThreads, smem, stream>>>(P);
-  else if (grouped) compact_gather<0, 0, 1><<<grid, kGatherThreads, smem, stream>>>(P);
-  else compact_gather<0, 0, 0><<<grid, kGatherThreads, smem, stream>>>(P);
+  const void* fn;
+  int slot;
+#define CS_PICK(TP, TG, LY, SL) \
+  do {                                                                                   \
+    fn = reinterpret_cast<const void*>(compact_gather<TP, TG, LY>);                      \
+    slot = SL;                                                                           \
+  } while (0)
+  if (nv12) {
+    if (fast) CS_PICK(14, 2, kLayoutNV12, 15); else CS_PICK(0, 0, kLayoutNV12, 16);
+  } else if (grouped) {
+    if (fast) CS_PICK(14, 2, 1, 12); else CS_PICK(0, 0, 1, 14);
+  } else {
+    if (fast) CS_PICK(14, 2, 0, 11); else CS_PICK(0, 0, 0, 13);
+  }
+#undef CS_PICK
+  if (cs_set_smem_attr(fn, slot, 96 * 1024)) return CS_ERR_CUDA;
+  void* args[] = {&P};
+  if (cudaLaunchKernel(fn, dim3(grid), dim3(kGatherThreads), args, smem, stream) != cudaSuccess) return CS_ERR_CUDA;
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
+}
+
+int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
+                      int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
+                      int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                      int32_t* frame_offsets, unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+  return launch_compact(g, nullptr, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, frames, nullptr,
+                        frame_layout, capacity, packed, pos_ids, src_index, frame_offsets, counters, status, stream);
+}
+
+int cs_launch_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n_streams, int32_t n_frames,
+                           const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* frame_index,
+                           const void* const* y_planes, const void* const* uv_planes, int64_t capacity,
+                           void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
+                           unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+  return launch_compact(g, pp, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, y_planes, uv_planes,
+                        kLayoutNV12, capacity, packed, pos_ids, src_index, frame_offsets, counters, status, stream);
 }

@@ -27,10 +27,13 @@ class Pipeline:
     def __init__(self, grid: dict, n_streams: int, window: int, stride: int, gop: int, kv: dict | None,
                  n_prompt: int = 0, device=None, want_score: bool = False, packed_capacity: int | None = None,
                  with_refreshed: bool = True, frame_layout: int = abi.CS_LAYOUT_PLANAR, kv_mode: str = "copy",
-                 compact_chunk: int | None = None):
+                 compact_chunk: int | None = None, preprocess: dict | None = None):
         self.g = dict(grid)
         self.frame_layout = frame_layout
         self.kv_mode = kv_mode
+        # preprocess set: frames are decoded NV12 (frame_ptrs = (y_ptrs, uv_ptrs)) and compaction runs the fused
+        # NV12 -> RGB -> resize -> normalise kernel (codecsight_compact_nv12, NEXT-2)
+        self.preprocess = preprocess
         # frames per compaction call (the first window's w frames are compacted s at a time when set)
         self.compact_chunk = compact_chunk
         self.S, self.w, self.s, self.gop = n_streams, window, stride, gop
@@ -129,15 +132,22 @@ class Pipeline:
         c = n if self.compact_chunk is None else min(n, self.compact_chunk)
         for j0 in range(0, n, c):
             nj = min(c, n - j0)
+            ptrs = frame_ptrs if isinstance(frame_ptrs, (tuple, list)) else (frame_ptrs,)
             if nj == n:
-                fptr, fidx = frame_ptrs, fi
+                fptrs, fidx = ptrs, fi
             else:  # frames / indices of the chunk: per stream the slots j0..j0+nj-1 of [S][n]
-                fptr = frame_ptrs.view(self.S, n)[:, j0:j0 + nj].contiguous().view(-1)
+                fptrs = tuple(p.view(self.S, n)[:, j0:j0 + nj].contiguous().view(-1) for p in ptrs)
                 fidx = fi.view(self.S, n)[:, j0:j0 + nj].contiguous().view(-1)
-            abi.codecsight_compact(g, self.S, nj, self.mask_ring[:, off + j0:], self.ring, fidx, fptr,
-                                   self.capacity, self.packed, self.pos_ids, self.src_index,
-                                   self.frame_offsets[: self.S * nj + 1], self.counters, self.status, stream,
-                                   frame_layout=self.frame_layout)
+            if self.preprocess is not None:
+                abi.codecsight_compact_nv12(g, self.preprocess, self.S, nj, self.mask_ring[:, off + j0:], self.ring,
+                                            fidx, fptrs[0], fptrs[1], self.capacity, self.packed, self.pos_ids,
+                                            self.src_index, self.frame_offsets[: self.S * nj + 1], self.counters,
+                                            self.status, stream)
+            else:
+                abi.codecsight_compact(g, self.S, nj, self.mask_ring[:, off + j0:], self.ring, fidx, fptrs[0],
+                                       self.capacity, self.packed, self.pos_ids, self.src_index,
+                                       self.frame_offsets[: self.S * nj + 1], self.counters, self.status, stream,
+                                       frame_layout=self.frame_layout)
 
     def kv_refresh(self, k, use_refreshed=None, stream=None):
         g = self.g

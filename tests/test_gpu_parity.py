@@ -691,3 +691,46 @@ def test_mrope_gpu_both_modes(abi, ref, dtype):
         sn, _, st = run_paged_both(abi, ref, g, kv, win, mring, tring, pools, slot, cap, refr, cap)
         slot = sn
     print("mrope", dtype, stats)
+
+
+# ------------------------------------------------------------------------------------------------------------
+# fused preprocessing + compaction from NV12 (NEXT-2)
+# ------------------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("geom", [(448, 448, 14, 2, 32, 32), (1920, 1080, 14, 2, 32, 32),
+                                  (3840, 2160, 14, 2, 32, 32), (120, 90, 6, 2, 8, 6), (64, 48, 8, 2, 4, 4)])
+def test_compact_nv12(abi, ref, geom):
+    sw, sh, p, G, gw, gh = geom
+    g = make_grid(sw, sh, patch=p, group=G, grid_w=gw, grid_h=gh)
+    rng = np.random.default_rng(sw + sh)
+    S, n = 2, 3
+    nw = abi.grid_words(g)
+    km = rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
+    km &= rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
+    pitch = sw + 64                                  # padded planes, as NVDEC allocates them
+    ys = [rng.integers(16, 236, size=(sh, pitch), dtype=np.uint8) for _ in range(S * n)]
+    uvs = [rng.integers(16, 241, size=(sh // 2, pitch), dtype=np.uint8) for _ in range(S * n)]
+    pre_h = ref.make_pre(sw, sh, pitch, pitch)
+    pre = dict(src_w=sw, src_h=sh, y_pitch=pitch, uv_pitch=pitch)
+    fidx = np.arange(S * n, dtype=np.int32) + 7
+    for cap in (S * n * gw * gh, S * n * gw * gh // 3 + 1):
+        y_d = [torch.from_numpy(a).to(DEV) for a in ys]
+        uv_d = [torch.from_numpy(a).to(DEV) for a in uvs]
+        km_d = torch.from_numpy(km.view(np.int32)).to(DEV)
+        packed = torch.full((cap, 3 * p * p), -1, dtype=torch.int16, device=DEV)
+        pos = torch.zeros(cap, 3, dtype=torch.int32, device=DEV)
+        src = torch.zeros(cap, dtype=torch.int32, device=DEV)
+        offs = torch.zeros(S * n + 1, dtype=torch.int32, device=DEV)
+        cnt = torch.zeros(16, dtype=torch.int64, device=DEV)
+        st = torch.zeros(1, dtype=torch.int32, device=DEV)
+        abi.codecsight_compact_nv12(g, pre, S, n, km_d, n, torch.from_numpy(fidx).to(DEV), abi.ptr_array(y_d, DEV),
+                                    abi.ptr_array(uv_d, DEV), cap, packed, pos, src, offs, cnt, st)
+        o = ref.compact_nv12(g, pre_h, km, fidx, ys, uvs, cap, S, n)
+        torch.cuda.synchronize()
+        rows = min(int(o["frame_offsets"][-1]), cap)
+        assert int(st.item()) == o["status"]
+        assert (offs.cpu().numpy() == o["frame_offsets"]).all()
+        assert (pos.cpu().numpy()[:rows] == o["pos_ids"][:rows]).all()
+        assert (src.cpu().numpy()[:rows] == o["src_index"][:rows]).all()
+        got = packed.cpu().numpy().view(np.uint16)[:rows]
+        assert (got == o["packed"][:rows]).all(), int((got != o["packed"][:rows]).sum())
+        assert (cnt.cpu().numpy().view(np.uint64) == o["counters"]).all()
