@@ -48,6 +48,9 @@ def parse():
                     help="paged: codecsight_kv_refresh_paged (in place, NEXT-1); copy: out-of-place double buffer")
     ap.add_argument("--rope", default="1d", choices=["1d", "mrope"],
                     help="key position scheme: 1-D on compacted sequence indices (Q16) or Qwen2-VL M-RoPE (NEXT-3)")
+    ap.add_argument("--frames", default="model", choices=["model", "nv12"],
+                    help="model: preprocessed model-input frames; nv12: decoded NV12 frames, preprocessing fused into "
+                         "the compaction (codecsight_compact_nv12, NEXT-2)")
     ap.add_argument("--frame-layout", default="grouped", choices=["grouped", "planar"],
                     help="layout of the preprocessed model-input frames handed to compact (DESIGN.md §6)")
     return ap.parse_args()
@@ -287,8 +290,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     if kvb is not None and args.rope == "mrope":
         kvb = dict(kvb, rope_mode=1, mrope_section=(16, 24, 24), t_per_frame=1)
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
+    pre = dict(src_w=sw, src_h=sh, y_pitch=sw, uv_pitch=sw) if args.frames == "nv12" else None
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
-                    kv_mode=args.kv_mode, compact_chunk=s)
+                    kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     pipe.init_cache_fill(gen)
@@ -300,9 +304,18 @@ def run_ours(args, cfg, rank, world, local_rank):
     mb_dev = [t.to(dev) for t in mb_host]
     # frames: S*s distinct model-input frames [3][448][448] bf16 (pointer array aliases them for the first window)
     H, W = g["grid_h"] * g["patch"], g["grid_w"] * g["patch"]
-    frames = [torch.randn(3, H, W, generator=gen, device=dev).to(torch.bfloat16) for _ in range(S * s)]
-    ptr_w = abi.ptr_array([frames[i % len(frames)] for i in range(S * w)], dev)
-    ptr_s = abi.ptr_array(frames, dev)
+    if args.frames == "nv12":
+        # decoded frames as NVDEC delivers them: Y [sh][sw] + interleaved UV [sh/2][sw], u8
+        ys = [torch.randint(16, 236, (sh, sw), dtype=torch.uint8, device=dev, generator=gen) for _ in range(S * s)]
+        uvs = [torch.randint(16, 241, (sh // 2, sw), dtype=torch.uint8, device=dev, generator=gen)
+               for _ in range(S * s)]
+        ptr_w = (abi.ptr_array([ys[i % len(ys)] for i in range(S * w)], dev),
+                 abi.ptr_array([uvs[i % len(uvs)] for i in range(S * w)], dev))
+        ptr_s = (abi.ptr_array(ys, dev), abi.ptr_array(uvs, dev))
+    else:
+        frames = [torch.randn(3, H, W, generator=gen, device=dev).to(torch.bfloat16) for _ in range(S * s)]
+        ptr_w = abi.ptr_array([frames[i % len(frames)] for i in range(S * w)], dev)
+        ptr_s = abi.ptr_array(frames, dev)
     total_steps = args.warmup + args.steps
     types_dev, fidx_dev, types_host = [], [], []
     for k in range(total_steps + 1):
@@ -380,20 +393,52 @@ def run_ours(args, cfg, rank, world, local_rank):
     layouts = {}
     k_last = args.warmup + args.steps - 1
     off_l = pipe.ring_slot(k_last)
-    for lname, lid in (("grouped", abi.CS_LAYOUT_GROUPED), ("planar", abi.CS_LAYOUT_PLANAR)):
+
+    def time_compact(fn, reps=10):
         c0 = pipe.counters.clone()
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 10
         ea.record(stream)
         for _ in range(reps):
-            abi.codecsight_compact(g, S, s, pipe.mask_ring[:, off_l:], pipe.ring, fidx_dev[k_last], ptr_s,
-                                   pipe.capacity, pipe.packed, pipe.pos_ids, pipe.src_index,
-                                   pipe.frame_offsets[:S * s + 1], pipe.counters, pipe.status, frame_layout=lid)
+            fn()
         eb.record(stream)
         torch.cuda.synchronize()
         t_ms = ea.elapsed_time(eb) / reps
         byt = float((pipe.counters - c0)[abi.CNT_BYTES_COMPACT].item()) / reps
-        layouts[lname] = {"ms": t_ms, "gbs": byt / (t_ms / 1e3) / 1e9}
+        return {"ms": t_ms, "gbs": byt / (t_ms / 1e3) / 1e9}
+
+    if args.frames == "nv12":
+        # fused (kept groups only) vs unfused (preprocess every group of every frame into grouped model frames,
+        # then compact them) on the last step's frames and masks
+        full = torch.full((S, s, abi.grid_words(g)), -1, dtype=torch.int32, device=dev)
+        model_frames = torch.empty(S * s, 3 * H * W, dtype=torch.bfloat16, device=dev)
+        mf_ptrs = abi.ptr_array([model_frames[i] for i in range(S * s)], dev)
+        offs_full = torch.zeros(S * s + 1, dtype=torch.int32, device=dev)
+        pos_full = torch.empty(S * s * pipe.np, 3, dtype=torch.int32, device=dev)
+        src_full = torch.empty(S * s * pipe.np, dtype=torch.int32, device=dev)
+
+        def fused():
+            abi.codecsight_compact_nv12(g, pre, S, s, pipe.mask_ring[:, off_l:], pipe.ring, fidx_dev[k_last],
+                                        ptr_s[0], ptr_s[1], pipe.capacity, pipe.packed, pipe.pos_ids,
+                                        pipe.src_index, pipe.frame_offsets[:S * s + 1], pipe.counters, pipe.status)
+
+        def unfused():
+            abi.codecsight_compact_nv12(g, pre, S, s, full, s, fidx_dev[k_last], ptr_s[0], ptr_s[1],
+                                        S * s * pipe.np, model_frames, pos_full, src_full, offs_full, pipe.counters,
+                                        pipe.status)
+            abi.codecsight_compact(g, S, s, pipe.mask_ring[:, off_l:], pipe.ring, fidx_dev[k_last], mf_ptrs,
+                                   pipe.capacity, pipe.packed, pipe.pos_ids, pipe.src_index,
+                                   pipe.frame_offsets[:S * s + 1], pipe.counters, pipe.status,
+                                   frame_layout=abi.CS_LAYOUT_GROUPED)
+
+        layouts["nv12_fused"] = time_compact(fused)
+        layouts["nv12_preprocess_all_then_compact"] = time_compact(unfused)
+        del model_frames
+    else:
+        for lname, lid in (("grouped", abi.CS_LAYOUT_GROUPED), ("planar", abi.CS_LAYOUT_PLANAR)):
+            layouts[lname] = time_compact(lambda lid=lid: abi.codecsight_compact(
+                g, S, s, pipe.mask_ring[:, off_l:], pipe.ring, fidx_dev[k_last], ptr_s, pipe.capacity, pipe.packed,
+                pipe.pos_ids, pipe.src_index, pipe.frame_offsets[:S * s + 1], pipe.counters, pipe.status,
+                frame_layout=lid))
 
     # ---- end-to-end through the public API with host buffers ----------------------------------------------
     # Every step: the step's codec metadata, frame types and frame indices go H2D from pinned host memory (copy
@@ -488,6 +533,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": 0.25, "alpha": 0.0,
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
+                   "frames": args.frames,
                    "parallelism": f"stream-shard x{world}",
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
                          "see per-step bytes)"},

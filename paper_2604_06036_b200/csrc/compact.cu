@@ -124,9 +124,12 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
     if (total > P.capacity) cs::atomic_or_status(P.status, CS_STATUS_CAPACITY);
     const unsigned long long row_bytes = 3ull * P.p * P.p * 2ull;
     cs::atomic_add_u64(&P.counters[CS_CNT_PACKED_ROWS], static_cast<unsigned long long>(rows));
+    // per packed row: its bytes read from the frame and written (+16 B of ids); with the fused NV12 path the
+    // source pixels depend on the scale and are not counted here (write side only, as in the oracle)
+    const unsigned long long per_row = (P.layout == kLayoutNV12 ? 1ull : 2ull) * row_bytes + 16ull;
     cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_COMPACT],
                        static_cast<unsigned long long>(P.n_slots) * (4ull * P.nw + 4ull) +
-                           static_cast<unsigned long long>(rows) * (2ull * row_bytes + 16ull));
+                           static_cast<unsigned long long>(rows) * per_row);
   }
 }
 
