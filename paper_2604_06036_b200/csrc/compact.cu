@@ -215,27 +215,58 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     // preprocess only the kept group's 3 x gp x gp model pixels straight from the decoded NV12 frame
     const uint8_t* Yp = reinterpret_cast<const uint8_t*>(frame);
     const uint8_t* UVp = static_cast<const uint8_t*>(P.uv_planes[slot]);
-    for (int e = lane; e < gp * gp; e += 32) {
-      const int yy = e / gp, xx = e - yy * gp;
-      int y0, y1, x0, x1;
-      float ly, lx;
-      nv12_axis(gr * gp + yy, P.src_h, P.scale_y, y0, y1, ly);
-      nv12_axis(gc * gp + xx, P.src_w, P.scale_x, x0, x1, lx);
-      float p00[3], p01[3], p10[3], p11[3];
-      nv12_rgb(Yp, UVp, P, y0, x0, p00);
-      nv12_rgb(Yp, UVp, P, y0, x1, p01);
-      nv12_rgb(Yp, UVp, P, y1, x0, p10);
-      nv12_rgb(Yp, UVp, P, y1, x1, p11);
-      const float hx = __fsub_rn(1.0f, lx), hy = __fsub_rn(1.0f, ly);
-      const int dy = yy / p, y = yy - dy * p, dx = xx / p, x = xx - dx * p;
+    // batches of 4 output pixels per lane: the 4 x (4 luma bytes + 4 chroma pairs) loads of a batch are all
+    // issued before any is consumed (memory-level parallelism), then converted, interpolated and normalised
+    constexpr int kB = 4;
+    const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
+    for (int e0 = 0; e0 < gp * gp; e0 += 32 * kB) {
+      uint32_t yv[kB][4], uvv[kB][4];
+      float lyv[kB], lxv[kB];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float top = __fadd_rn(__fmul_rn(hx, p00[c]), __fmul_rn(lx, p01[c]));
-        const float bot = __fadd_rn(__fmul_rn(hx, p10[c]), __fmul_rn(lx, p11[c]));
-        const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
-        const float t = __fdiv_rn(v, 255.0f);
-        const float o = __fdiv_rn(__fsub_rn(t, P.mean[c]), P.stdv[c]);
-        tile[((dy * G + dx) * 3 + c) * pp + y * p + x] = static_cast<uint16_t>(cs::f32_to_bf16_rne(o));
+      for (int b = 0; b < kB; ++b) {
+        const int e = e0 + b * 32 + lane;
+        if (e < gp * gp) {
+          const int yy = e / gp, xx = e - yy * gp;
+          int y0, y1, x0, x1;
+          nv12_axis(gr * gp + yy, P.src_h, P.scale_y, y0, y1, lyv[b]);
+          nv12_axis(gc * gp + xx, P.src_w, P.scale_x, x0, x1, lxv[b]);
+          const int ys[4] = {y0, y0, y1, y1}, xs[4] = {x0, x1, x0, x1};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            yv[b][q] = __ldg(Yp + (long long)ys[q] * P.y_pitch + xs[q]);
+            uvv[b][q] = __ldg(reinterpret_cast<const uint16_t*>(UVp + (long long)(ys[q] >> 1) * P.uv_pitch +
+                                                                2 * (xs[q] >> 1)));
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int e = e0 + b * 32 + lane;
+        if (e >= gp * gp) continue;
+        float rgb[4][3];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float c = static_cast<float>(static_cast<int>(yv[b][q]) - 16);
+          const float d = static_cast<float>(static_cast<int>(uvv[b][q] & 0xffu) - 128);
+          const float ee = static_cast<float>(static_cast<int>(uvv[b][q] >> 8) - 128);
+          rgb[q][0] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kRV, ee)), 0.0f), 255.0f);
+          rgb[q][1] = fminf(fmaxf(__fsub_rn(__fsub_rn(__fmul_rn(kY, c), __fmul_rn(kGU, d)), __fmul_rn(kGV, ee)), 0.0f),
+                            255.0f);
+          rgb[q][2] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kBU, d)), 0.0f), 255.0f);
+        }
+        const float lx = lxv[b], ly = lyv[b];
+        const float hx = __fsub_rn(1.0f, lx), hy = __fsub_rn(1.0f, ly);
+        const int yy = e / gp, xx = e - yy * gp;
+        const int dy = yy / p, y = yy - dy * p, dx = xx / p, x = xx - dx * p;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float top = __fadd_rn(__fmul_rn(hx, rgb[0][c]), __fmul_rn(lx, rgb[1][c]));
+          const float bot = __fadd_rn(__fmul_rn(hx, rgb[2][c]), __fmul_rn(lx, rgb[3][c]));
+          const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
+          const float t = __fdiv_rn(v, 255.0f);
+          const float o = __fdiv_rn(__fsub_rn(t, P.mean[c]), P.stdv[c]);
+          tile[((dy * G + dx) * 3 + c) * pp + y * p + x] = static_cast<uint16_t>(cs::f32_to_bf16_rne(o));
+        }
       }
     }
   } else if (vec_in) {
