@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather_ldg(const __grid_con
 // the issue overhead off the critical path and ~8 x NST x 8 KB in flight per SM without register staging.
 // ------------------------------------------------------------------------------------------------------------
 constexpr int kTmaChunk = 8192;
+constexpr int kClaim = 4;  // items per dynamic work claim
 constexpr int kWarpsPerGather = kGatherThreads / 32;
 constexpr int kMaxStages = 6;
 
@@ -528,6 +529,9 @@ struct ChunkGen {  // generator state, owned by lane 0 of a warp
   int sidx, seg, x, active;
   int nseg, a, b, l, kv;
   int c_sidx, c_blk, c_seg;  // cache: stream whose pointers are loaded; (stream, block) of the last run search
+  long long V;               // total items
+  long long next_claim;      // start of the next claimed range (claimed one range ahead), >= V when exhausted
+  unsigned long long* ctr;   // work counter in the workspace header (zeroed by kv_prefix)
   const KvSeg* segs;
   unsigned char* nc;
   const unsigned char* oc;
@@ -543,11 +547,28 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
                                          long long row_bytes, const unsigned char*& src, ChunkDesc& d,
                                          const void*& tab) {
   const int ipb = P.L * 2;
-  while (g.it < g.it1) {
+  for (;;) {
+    if (g.it >= g.it1) {
+      // dynamic balancing: take the range claimed earlier, claim the next one now (latency hidden by the ring)
+      if (g.next_claim >= g.V) return false;
+      g.it = g.next_claim;
+      g.it1 = min(g.V, g.it + kClaim);
+      g.next_claim = static_cast<long long>(atomicAdd(g.ctr, static_cast<unsigned long long>(kClaim)));
+      if (__ldg(pref + g.sidx) > g.it) g.sidx = 0;  // (claims only increase; defensive)
+      g.active = 0;
+    }
     if (!g.active) {
       // items of one stream are contiguous and ordered (block, layer, K|V): stream pointers and the run search
       // of a block are cached across the 2L items that share them
-      while (__ldg(pref + g.sidx + 1) <= g.it) ++g.sidx;
+      if (__ldg(pref + g.sidx + 1) <= g.it) {  // find the stream of item g.it: pref[s] <= it < pref[s + 1]
+        int lo = g.sidx + 1, hi = P.n_streams;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (__ldg(pref + mid) <= g.it) lo = mid; else hi = mid;
+        }
+        g.sidx = lo;
+        while (__ldg(pref + g.sidx + 1) <= g.it) ++g.sidx;
+      }
       const long long local = g.it - __ldg(pref + g.sidx);
       const int blk = static_cast<int>(local / ipb);
       const int lk = static_cast<int>(local - (long long)blk * ipb);
@@ -614,7 +635,6 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
     ++g.it;
     g.active = 0;
   }
-  return false;
 }
 
 // 1 CTA: item prefix over streams into the workspace (item = stream x 128-row block x layer x K|V)
@@ -627,6 +647,7 @@ __global__ void __launch_bounds__(1024) kv_prefix(const __grid_constant__ KvPara
   if (tid == 0) {
     s_carry = 0;
     pref[0] = 0;
+    *reinterpret_cast<unsigned long long*>(P.ws) = 0ull;  // work counter of the gather (dynamic claims)
   }
   __syncthreads();
   for (int base = 0; base < P.n_streams; base += blockDim.x) {
@@ -726,22 +747,15 @@ __global__ void __launch_bounds__(kGatherThreads, 1) kv_gather_tma(const __grid_
   const int* pref = ws_prefix(P);
 
   const long long V = __ldg(pref + P.n_streams);
-  const long long nwarps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-  const long long gw = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + wib;
   ChunkGen gen{};
-  gen.it = V * gw / nwarps;
-  gen.it1 = V * (gw + 1) / nwarps;
+  gen.V = V;
+  gen.ctr = reinterpret_cast<unsigned long long*>(P.ws);
   gen.c_sidx = -1;
   gen.c_blk = -1;
-  if (gen.it >= gen.it1) return;  // warp-uniform
+  gen.sidx = 0;
   if (lane == 0) {
-    // first stream of this warp's range: binary search over the prefix
-    int lo = 0, hi = P.n_streams;  // pref[lo] <= it < pref[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(pref + mid) <= gen.it) lo = mid; else hi = mid;
-    }
-    gen.sidx = lo;
+    gen.next_claim = static_cast<long long>(atomicAdd(gen.ctr, static_cast<unsigned long long>(kClaim)));
+    gen.it = gen.it1 = 0;  // empty: the first gen_next takes the claimed range
     for (int s = 0; s < nst; ++s) cs::mbar_init(&full[s], 1);
     cs::fence_mbar_init();
   }
