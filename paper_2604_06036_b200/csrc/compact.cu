@@ -60,34 +60,41 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
   __shared__ int s_carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gs2 = P.G * P.G;
-  const bool fast = (P.G == 2 && P.grid_w == 32);
+  const bool fast = (P.G == 2 && P.grid_w == 32 && P.nw <= 32);  // one mask word per patch row, one per lane
   if (tid == 0) s_carry = 0;
   __syncthreads();
   for (int base = 0; base < P.n_slots; base += kScanThreads) {
-    // counts of this tile of slots: one warp per slot (coalesced 128-B mask loads)
-    for (int j = warp; j < kScanThreads; j += kScanThreads / 32) {
-      const int slot = base + j;
-      int cnt = 0;
-      if (slot < P.n_slots) {
-        const uint32_t* m = slot_mask(P, slot);
-        if (fast) {
-          // word r = patch row r; group row g = rows 2g, 2g+1; fold horizontal pairs onto even bits
-          const uint32_t wv = lane < P.nw ? __ldg(m + lane) : 0u;
-          const uint32_t x = wv | __shfl_down_sync(0xffffffffu, wv, 1);
-          int c = (lane & 1) == 0 ? __popc((x | (x >> 1)) & 0x55555555u) : 0;
+    // counts of this tile of slots: warp w handles slots w, w + 32, ...; lane l holds word l of the slot's mask
+    if (fast) {
+      // all 32 masks of the warp are loaded before any is reduced (32 coalesced 128-B loads in flight)
+      uint32_t wv[kScanThreads / 32];
 #pragma unroll
-          for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
-          cnt = c;
-        } else {
-          int c = 0;
+      for (int i = 0; i < kScanThreads / 32; ++i) {
+        const int slot = base + warp + 32 * i;
+        wv[i] = (slot < P.n_slots && lane < P.nw) ? __ldg(slot_mask(P, slot) + lane) : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < kScanThreads / 32; ++i) {
+        // word r = patch row r; group row g = rows 2g, 2g+1; fold horizontal pairs onto even bits
+        const uint32_t x = wv[i] | __shfl_down_sync(0xffffffffu, wv[i], 1);
+        int c = (lane & 1) == 0 ? __popc((x | (x >> 1)) & 0x55555555u) : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
+        if (lane == 0) s_cnt[warp + 32 * i] = c * gs2;
+      }
+    } else {
+      for (int j = warp; j < kScanThreads; j += kScanThreads / 32) {
+        const int slot = base + j;
+        int c = 0;
+        if (slot < P.n_slots) {
+          const uint32_t* m = slot_mask(P, slot);
           for (int q0 = 0; q0 < P.ngroups; q0 += 32) {
             const int q = q0 + lane;
             c += __popc(__ballot_sync(0xffffffffu, q < P.ngroups && cs::group_kept(m, q, P.ngc, P.G, P.grid_w)));
           }
-          cnt = c;
         }
+        if (lane == 0) s_cnt[j] = c * gs2;
       }
-      if (lane == 0) s_cnt[j] = cnt * gs2;
     }
     __syncthreads();
     const int slot = base + tid;
