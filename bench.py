@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="run score, compact and kv_refresh back to back on one stream (default: three streams)")
     ap.add_argument("--kv-mode", default="paged", choices=["paged", "copy"],
                     help="paged: codecsight_kv_refresh_paged (in place, NEXT-1); copy: out-of-place double buffer")
     ap.add_argument("--rope", default="1d", choices=["1d", "mrope"],
@@ -292,7 +294,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
     pre = dict(src_w=sw, src_h=sh, y_pitch=sw, uv_pitch=sw) if args.frames == "nv12" else None
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
-                    kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre)
+                    kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre, overlap=not args.no_overlap)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     pipe.init_cache_fill(gen)
@@ -340,28 +342,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     def run_step(k, timed):
         _, n = step_frames(cfg, k)
         ptrs = ptr_w if k == 0 else ptr_s
+        evs = pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k], timing=timed)
         if timed:
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            off = pipe.ring_slot(k)
-            pipe.type_ring[:, off:off + n].copy_(types_dev[k], non_blocking=True)
-            e[0].record(stream)
-            abi.codecsight_score_patches(g, S, n, md_for(k), pipe.type_ring[:, off:], pipe.mask_ring[:, off:],
-                                         pipe.ring, pipe.gop_state, None, pipe.kept_count[:, :n], pipe.counters,
-                                         pipe.status)
-            e[1].record(stream)
-            pipe.compact(k, n, off, ptrs, fidx_dev[k])
-            e[2].record(stream)
-            if pipe.kv is not None:
-                pipe.kv_refresh(k)
-            e[3].record(stream)
-            ev["score"].append((e[0], e[1]))
-            ev["compact"].append((e[1], e[2]))
-            ev["kv"].append((e[2], e[3]))
-        else:
-            pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k])
+            for name in ("score", "compact", "kv"):
+                if name in evs:
+                    ev[name].append(evs[name])
 
     for k in range(args.warmup):
         run_step(k, False)
+    pipe.join(stream)
     torch.cuda.synchronize()
     cnt0 = pipe.counters.clone()
     if world > 1:
@@ -378,6 +367,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     t_start.record(stream)
     for k in range(args.warmup, args.warmup + args.steps):
         run_step(k, True)
+    pipe.join(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -471,6 +461,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         checksum = 0
         t0 = time.perf_counter()
         e_a.record(copy_stream)
+        res_stream = torch.cuda.Stream(dev)
         for i in range(nsteps):
             k = k0 + i
             b = i & 1
@@ -483,16 +474,22 @@ def run_ours(args, cfg, rank, world, local_rank):
                 st_fi[b].copy_(in_fi[i], non_blocking=True)
                 loaded[b].record(copy_stream)
             stream.wait_event(loaded[b])
-            pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b])
-            consumed[b].record(stream)
-            if pipe.kv is not None:                                        # D2H: the step's results
-                res[b][:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
-            res[b][S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
-            res[b][-1:].copy_(pipe.frame_offsets[S * n:S * n + 1], non_blocking=True)
-            done[b].record(stream)
+            evs = pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b])
+            # results stream: waits for the step's kernels, reads the results back (D2H), releases the staging slot
+            for name in ("score", "compact", "kv"):
+                if name in evs:
+                    res_stream.wait_event(evs[name][1])
+            with torch.cuda.stream(res_stream):
+                if pipe.kv is not None:                                    # D2H: the step's results
+                    res[b][:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
+                res[b][S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
+                res[b][-1:].copy_(pipe.frame_offsets[S * n:S * n + 1], non_blocking=True)
+                consumed[b].record(res_stream)
+                done[b].record(res_stream)
             if i >= 1:
                 done[1 - b].synchronize()                                  # the host consumes step k-1's result
                 checksum += int(res[1 - b][-1])
+        stream.wait_stream(res_stream)
         e_b.record(stream)
         done[(nsteps - 1) & 1].synchronize()
         checksum += int(res[(nsteps - 1) & 1][-1])
@@ -514,7 +511,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     frames_total = S * world * s * K
     value = frames_total / (ms_max / 1e3)
     stream_steps = S * world * K / (ms_max / 1e3)
-    kv_ms = float(np.mean(per["kv"]))
+    kv_ms = float(np.mean(per["kv"])) if per["kv"] else 0.0
     kv_bytes_launch = float(dcnt[abi.CNT_BYTES_KV].item()) / K
     peak, peak_kind = measured_peak_hbm()
     achieved = kv_bytes_launch / (kv_ms / 1e3) / 1e9 if kvb else 0.0

@@ -27,7 +27,7 @@ class Pipeline:
     def __init__(self, grid: dict, n_streams: int, window: int, stride: int, gop: int, kv: dict | None,
                  n_prompt: int = 0, device=None, want_score: bool = False, packed_capacity: int | None = None,
                  with_refreshed: bool = True, frame_layout: int = abi.CS_LAYOUT_PLANAR, kv_mode: str = "copy",
-                 compact_chunk: int | None = None, preprocess: dict | None = None):
+                 compact_chunk: int | None = None, preprocess: dict | None = None, overlap: bool = False):
         self.g = dict(grid)
         self.frame_layout = frame_layout
         self.kv_mode = kv_mode
@@ -37,7 +37,11 @@ class Pipeline:
         # frames per compaction call (the first window's w frames are compacted s at a time when set)
         self.compact_chunk = compact_chunk
         self.S, self.w, self.s, self.gop = n_streams, window, stride, gop
-        self.ring = window + stride
+        # overlap: compact and kv_refresh of step k run on their own streams concurrently with the scoring of step
+        # k+1; the ring then holds w + 2s frames so that step k+1's new masks never land on slots kv_refresh(k)
+        # still reads (frames [(k-1)s, ks+w) and the next s frames are w + 2s distinct slots)
+        self.overlap = overlap
+        self.ring = window + (2 * stride if overlap else stride)
         self.dev = torch.device(device if device is not None else "cuda")
         self.nw = abi.grid_words(grid)
         self.np = grid["grid_w"] * grid["grid_h"]
@@ -86,6 +90,9 @@ class Pipeline:
                       else abi.kv_workspace_size(self.kv, win1, S))
             self.workspace = torch.empty((nbytes + 15) // 16 * 16, dtype=torch.uint8, device=d)
         self.cur = 0  # which cache set holds window k-1
+        if overlap:
+            self.stream_compact = torch.cuda.Stream(d)
+            self.stream_kv = torch.cuda.Stream(d)
 
     # ------------------------------------------------------------------------------------------------------
     def new_frames(self, k: int) -> tuple[int, int]:
@@ -108,21 +115,54 @@ class Pipeline:
 
     def step(self, k: int, mb: torch.Tensor, frame_ptrs: torch.Tensor, frame_index: torch.Tensor | None = None,
              types: torch.Tensor | None = None, use_refreshed: bool | None = None, do_kv: bool = True,
-             stream=None):
+             stream=None, timing: bool = False):
         """Enqueue one sliding-window step.  ``mb``: [S][n_new][mb_rows][mb_cols] cs_mb records (uint8 view or any
         dtype, contiguous, device); ``types``: [S][n_new] uint8 written into the ring (None = already there);
-        ``frame_ptrs``: device int64 [S*n_new] pointers to [3][H][W] bf16 frames."""
+        ``frame_ptrs``: device int64 [S*n_new] pointers to [3][H][W] bf16 frames (a (Y, UV) pair with NV12).
+        Returns {"score"|"compact"|"kv": (start_event, end_event)} (timing events when ``timing``)."""
         g = self.g
         f0, n = self.new_frames(k)
         off = f0 % self.ring
-        if types is not None:
-            self.type_ring[:, off:off + n].copy_(types, non_blocking=True)
-        abi.codecsight_score_patches(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:], self.ring,
-                                     self.gop_state, None if self.score is None else self.score[:, :n],
-                                     self.kept_count[:, :n], self.counters, self.status, stream)
-        self.compact(k, n, off, frame_ptrs, frame_index, stream)
+        main = torch.cuda.current_stream(self.dev) if stream is None else stream
+
+        def ev(st):
+            e = torch.cuda.Event(enable_timing=timing)
+            e.record(st)
+            return e
+
+        out = {}
+        with torch.cuda.stream(main):
+            if types is not None:
+                self.type_ring[:, off:off + n].copy_(types, non_blocking=True)
+            s0 = ev(main)
+            abi.codecsight_score_patches(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:],
+                                         self.ring, self.gop_state, None if self.score is None else self.score[:, :n],
+                                         self.kept_count[:, :n], self.counters, self.status, main)
+            out["score"] = (s0, ev(main))
+        cs_stream = self.stream_compact if self.overlap else main
+        kv_stream = self.stream_kv if self.overlap else main
+        if self.overlap:
+            cs_stream.wait_event(out["score"][1])
+        with torch.cuda.stream(cs_stream):
+            c0 = ev(cs_stream)
+            self.compact(k, n, off, frame_ptrs, frame_index, cs_stream)
+            out["compact"] = (c0, ev(cs_stream))
         if self.kv is not None and do_kv:
-            self.kv_refresh(k, use_refreshed, stream)
+            if self.overlap:
+                kv_stream.wait_event(out["score"][1])
+            with torch.cuda.stream(kv_stream):
+                k0 = ev(kv_stream)
+                self.kv_refresh(k, use_refreshed, kv_stream)
+                out["kv"] = (k0, ev(kv_stream))
+        return out
+
+    def join(self, stream=None):
+        """Make `stream` (default: current) wait for everything enqueued on the side streams."""
+        if not self.overlap:
+            return
+        main = torch.cuda.current_stream(self.dev) if stream is None else stream
+        main.wait_stream(self.stream_compact)
+        main.wait_stream(self.stream_kv)
 
     def compact(self, k, n, off, frame_ptrs, frame_index=None, stream=None):
         """codecsight_compact of the step's n new frames, in chunks of compact_chunk frames when set (the packed

@@ -465,7 +465,8 @@ def test_kv_zero_slide_bit_exact(abi, ref):
     assert re.size and (a[:, :, re] == b[:, :, re]).all()
 
 
-def test_pipeline_end_to_end_c4_shape(abi, ref):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_pipeline_end_to_end_c4_shape(abi, ref, overlap):
     """Pipeline (score -> compact -> kv_refresh) on a C4-shaped shard (4 streams: 2 static, 2 high-motion, 1080p,
     w=16, s=4, GOP 16) for 4 steps, every output compared with the oracle driven the same way."""
     from paper_2604_06036_b200.pipeline import Pipeline
@@ -473,12 +474,12 @@ def test_pipeline_end_to_end_c4_shape(abi, ref):
     g = make_grid(1920, 1080)
     S, w, s, gop = 4, 16, 4, 16
     kvb = dict(synth.QWEN_KV, layers=2)
-    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=32, device=DEV)
+    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=32, device=DEV, overlap=overlap)
     gen = torch.Generator(device=DEV)
     gen.manual_seed(4)
     pipe.init_cache_fill(gen)
     nw = 32
-    ring = w + s
+    ring = pipe.ring
     gens = [synth.StreamGen(1920, 1080, synth.scene_of(cfg, si), synth.stream_seed(cfg, si)) for si in range(S)]
     gop_h = np.zeros((S, nw + 1), np.uint32)
     mring_h = np.zeros((S, ring, nw), np.uint32)
@@ -486,7 +487,7 @@ def test_pipeline_end_to_end_c4_shape(abi, ref):
     rng = np.random.default_rng(0)
     frames_h = synth.random_frames(S * w, 448, 448, rng)
     frames_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in frames_h]
-    for k in range(4):
+    for k in range(6 if overlap else 4):
         f0, n = pipe.new_frames(k)
         mb = np.stack([np.stack([gens[si].next_frame() for _ in range(n)]) for si in range(S)])
         types = np.stack([synth.frame_types(n, gop, f0) for _ in range(S)])
