@@ -474,7 +474,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                 st_fi[b].copy_(in_fi[i], non_blocking=True)
                 loaded[b].record(copy_stream)
             stream.wait_event(loaded[b])
-            evs = pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b])
+            # the step's output buffers (parity b) were last read back by step i-2's results copy
+            evs = pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b], wait_events=[done[b]] if i >= 2 else [])
             # results stream: waits for the step's kernels, reads the results back (D2H), releases the staging slot
             for name in ("score", "compact", "kv"):
                 if name in evs:

@@ -51,7 +51,9 @@ class Pipeline:
         self.gop_state = torch.zeros(S, nw + 1, dtype=torch.int32, device=d)
         self.mask_ring = torch.zeros(S, ring, nw, dtype=torch.int32, device=d)
         self.type_ring = torch.zeros(S, ring, dtype=torch.uint8, device=d)
-        self.kept_count = torch.zeros(S, window, dtype=torch.int32, device=d)
+        nb = 2 if overlap else 1  # per-step outputs alternate between nb buffer sets (step parity)
+        self._kept_count = [torch.zeros(S, window, dtype=torch.int32, device=d) for _ in range(nb)]
+        self.kept_count = self._kept_count[0]
         self.score = torch.zeros(S, window, self.np, dtype=torch.float32, device=d) if want_score else None
         self.counters = torch.zeros(abi.NCOUNTERS, dtype=torch.int64, device=d)
         self.status = torch.zeros(1, dtype=torch.int32, device=d)
@@ -59,10 +61,12 @@ class Pipeline:
         p = grid["patch"]
         chunk = compact_chunk if compact_chunk is not None else window
         self.capacity = packed_capacity if packed_capacity is not None else S * chunk * self.np
-        self.packed = torch.empty(self.capacity, 3 * p * p, dtype=torch.bfloat16, device=d)
-        self.pos_ids = torch.empty(self.capacity, 3, dtype=torch.int32, device=d)
-        self.src_index = torch.empty(self.capacity, dtype=torch.int32, device=d)
-        self.frame_offsets = torch.zeros(S * window + 1, dtype=torch.int32, device=d)
+        self._packed = [torch.empty(self.capacity, 3 * p * p, dtype=torch.bfloat16, device=d) for _ in range(nb)]
+        self._pos_ids = [torch.empty(self.capacity, 3, dtype=torch.int32, device=d) for _ in range(nb)]
+        self._src_index = [torch.empty(self.capacity, dtype=torch.int32, device=d) for _ in range(nb)]
+        self._frame_offsets = [torch.zeros(S * window + 1, dtype=torch.int32, device=d) for _ in range(nb)]
+        self.packed, self.pos_ids = self._packed[0], self._pos_ids[0]
+        self.src_index, self.frame_offsets = self._src_index[0], self._frame_offsets[0]
         self.frame_index = torch.zeros(S * window, dtype=torch.int32, device=d)
         self.kv = None
         if kv is not None:
@@ -82,14 +86,16 @@ class Pipeline:
             self.refreshed = [torch.empty(rshape, dtype=dt, device=d) for _ in range(S)] if with_refreshed else None
             self.refreshed_ptrs = abi.ptr_array(self.refreshed, d) if with_refreshed else None
             self.token_cap = cap
-            self.disposition = torch.zeros(S, cap, dtype=torch.uint8, device=d)
-            self.p_old = torch.zeros(S, cap, dtype=torch.int32, device=d)
-            self.n_tokens = torch.zeros(S, 4, dtype=torch.int32, device=d)
+            self._disposition = [torch.zeros(S, cap, dtype=torch.uint8, device=d) for _ in range(nb)]
+            self._p_old = [torch.zeros(S, cap, dtype=torch.int32, device=d) for _ in range(nb)]
+            self._n_tokens = [torch.zeros(S, 4, dtype=torch.int32, device=d) for _ in range(nb)]
+            self.disposition, self.p_old, self.n_tokens = self._disposition[0], self._p_old[0], self._n_tokens[0]
             win1 = dict(window=window, stride=stride, step=1, ring_frames=ring)
             nbytes = (abi.kv_paged_workspace_size(grid, self.kv, win1, S) if kv_mode == "paged"
                       else abi.kv_workspace_size(self.kv, win1, S))
             self.workspace = torch.empty((nbytes + 15) // 16 * 16, dtype=torch.uint8, device=d)
         self.cur = 0  # which cache set holds window k-1
+        self._side_done = {}  # step -> events closing its compact / kv_refresh work (overlap mode)
         if overlap:
             self.stream_compact = torch.cuda.Stream(d)
             self.stream_kv = torch.cuda.Stream(d)
@@ -115,7 +121,7 @@ class Pipeline:
 
     def step(self, k: int, mb: torch.Tensor, frame_ptrs: torch.Tensor, frame_index: torch.Tensor | None = None,
              types: torch.Tensor | None = None, use_refreshed: bool | None = None, do_kv: bool = True,
-             stream=None, timing: bool = False):
+             stream=None, timing: bool = False, wait_events=()):
         """Enqueue one sliding-window step.  ``mb``: [S][n_new][mb_rows][mb_cols] cs_mb records (uint8 view or any
         dtype, contiguous, device); ``types``: [S][n_new] uint8 written into the ring (None = already there);
         ``frame_ptrs``: device int64 [S*n_new] pointers to [3][H][W] bf16 frames (a (Y, UV) pair with NV12).
@@ -131,6 +137,16 @@ class Pipeline:
             return e
 
         out = {}
+        if self.overlap:
+            # this step's output buffers (parity k & 1) and ring slots were last used by step k-2: wait for its
+            # side-stream work (and any consumer events the caller passes) before writing them again
+            b = k & 1
+            self.kept_count, self.packed, self.pos_ids = self._kept_count[b], self._packed[b], self._pos_ids[b]
+            self.src_index, self.frame_offsets = self._src_index[b], self._frame_offsets[b]
+            if self.kv is not None:
+                self.disposition, self.p_old, self.n_tokens = self._disposition[b], self._p_old[b], self._n_tokens[b]
+            for e in self._side_done.pop(k - 2, []) + list(wait_events):
+                main.wait_event(e)
         with torch.cuda.stream(main):
             if types is not None:
                 self.type_ring[:, off:off + n].copy_(types, non_blocking=True)
@@ -154,6 +170,8 @@ class Pipeline:
                 k0 = ev(kv_stream)
                 self.kv_refresh(k, use_refreshed, kv_stream)
                 out["kv"] = (k0, ev(kv_stream))
+        if self.overlap:
+            self._side_done[k] = [out[x][1] for x in ("compact", "kv") if x in out]
         return out
 
     def join(self, stream=None):
