@@ -44,8 +44,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quiet", action="store_true")
-    ap.add_argument("--no-overlap", action="store_true",
-                    help="run score, compact and kv_refresh back to back on one stream (default: three streams)")
+    ap.add_argument("--overlap", action="store_true",
+                    help="run compact and kv_refresh on side streams concurrently with the next step's scoring "
+                         "(measured: no gain -- kv_refresh already saturates HBM and holds every SM; default off)")
     ap.add_argument("--kv-mode", default="paged", choices=["paged", "copy"],
                     help="paged: codecsight_kv_refresh_paged (in place, NEXT-1); copy: out-of-place double buffer")
     ap.add_argument("--rope", default="1d", choices=["1d", "mrope"],
@@ -294,7 +295,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
     pre = dict(src_w=sw, src_h=sh, y_pitch=sw, uv_pitch=sw) if args.frames == "nv12" else None
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
-                    kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre, overlap=not args.no_overlap)
+                    kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre, overlap=args.overlap)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     pipe.init_cache_fill(gen)
@@ -531,7 +532,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": 0.25, "alpha": 0.0,
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
-                   "frames": args.frames,
+                   "frames": args.frames, "overlap": args.overlap,
                    "parallelism": f"stream-shard x{world}",
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
                          "see per-step bytes)"},
