@@ -36,6 +36,9 @@ struct ScoreParams {
   int use_bulk, chunk_rows, n_chunks, nstage;
   unsigned row_bytes, chunk_alloc;
   int want_score;
+  int use_r;     // alpha != 0: R(i) is needed (with alpha == 0, M = fma(0, R, V) = V exactly, R is skipped)
+  int gw_shift;  // log2(grid_w) when grid_w is a power of two, else -1
+  unsigned off_col, off_row;  // smem: per patch column (i0, i1), per patch row (j0, j1)
   const cs_mb* mb_ptr;
   const uint8_t* frame_type;
   uint32_t* keep_mask;
@@ -94,37 +97,45 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
 
   const int T = s_np * P.n_chunks;  // chunk sequence over this CTA's P-frames
   const cs_mb* stream_mb = P.mb_ptr + (long long)sidx * P.n_frames * P.mb_rows * P.mb_cols;
+  int2* s_col = reinterpret_cast<int2*>(smem + P.off_col);  // [grid_w] MB column range of each patch column
+  int2* s_row = reinterpret_cast<int2*>(smem + P.off_row);  // [grid_h] MB row range of each patch row
+  {
+    const int cw = P.mb * P.grid_w, ch = P.mb * P.grid_h;  // MB width / height in scaled units
+    for (int c = tid; c < P.grid_w; c += nthr) s_col[c] = make_int2((c * P.src_w) / cw, ((c + 1) * P.src_w - 1) / cw);
+    for (int r = tid; r < P.grid_h; r += nthr) s_row[r] = make_int2((r * P.src_h) / ch, ((r + 1) * P.src_h - 1) / ch);
+  }
+  __syncthreads();
 
-  auto chunk_src = [&](int q, int& r0, int& nrows) -> const cs_mb* {
-    const int f = s_plist[q / P.n_chunks];
-    const int c = q % P.n_chunks;
-    r0 = c * P.chunk_rows;
-    nrows = min(P.chunk_rows, P.mb_rows - r0);
-    return stream_mb + ((long long)f * P.mb_rows + r0) * P.mb_cols;
-  };
-  auto issue = [&](int q) {
-    int r0, nrows;
-    const cs_mb* src = chunk_src(q, r0, nrows);
-    const int s = q % P.nstage;
+  // producer (thread 0) walks the chunk sequence with its own counters: frame list index, chunk in frame, stage
+  int pf = 0, pc = 0, ps = 0;
+  auto issue_next = [&]() {
+    const int f = s_plist[pf];
+    const int r0 = pc * P.chunk_rows;
+    const int nrows = min(P.chunk_rows, P.mb_rows - r0);
     const uint32_t bytes = static_cast<uint32_t>(nrows) * P.row_bytes;
-    cs::mbar_arrive_expect_tx(&bars[s], bytes);
-    cs::bulk_g2s(stage + (size_t)s * P.chunk_alloc, src, bytes, &bars[s]);
+    cs::mbar_arrive_expect_tx(&bars[ps], bytes);
+    cs::bulk_g2s(stage + (size_t)ps * P.chunk_alloc, stream_mb + ((long long)f * P.mb_rows + r0) * P.mb_cols, bytes,
+                 &bars[ps]);
+    if (++pc == P.n_chunks) { pc = 0; ++pf; }
+    if (++ps == P.nstage) ps = 0;
   };
-
   if (P.use_bulk && tid == 0)
-    for (int q = 0; q < min(T, P.nstage); ++q) issue(q);
+    for (int q = 0; q < min(T, P.nstage); ++q) issue_next();
 
   unsigned long long near_local = 0;
+  const int lane_w = tid >> 5, nwarps = nthr >> 5;
+  const int cw = P.mb * P.grid_w;
+  int cf = 0, cc = 0, cs_ = 0, cph = 0;  // consumer: frame list index, chunk in frame, stage, stage phase
   for (int q = 0; q < T; ++q) {
-    const int s = q % P.nstage;
-    int r0, nrows;
-    const cs_mb* src = chunk_src(q, r0, nrows);
-    const uint2* buf = reinterpret_cast<const uint2*>(stage + (size_t)s * P.chunk_alloc);
+    const int f = s_plist[cf];
+    const int r0 = cc * P.chunk_rows;
+    const int nrows = min(P.chunk_rows, P.mb_rows - r0);
+    const uint2* buf = reinterpret_cast<const uint2*>(stage + (size_t)cs_ * P.chunk_alloc);
     if (P.use_bulk) {
-      cs::mbar_wait(&bars[s], (q / P.nstage) & 1);
+      cs::mbar_wait(&bars[cs_], cph);
     } else {
-      const uint2* g = reinterpret_cast<const uint2*>(src);
-      uint2* d = reinterpret_cast<uint2*>(stage + (size_t)s * P.chunk_alloc);
+      const uint2* g = reinterpret_cast<const uint2*>(stream_mb + ((long long)f * P.mb_rows + r0) * P.mb_cols);
+      uint2* d = reinterpret_cast<uint2*>(stage + (size_t)cs_ * P.chunk_alloc);
       for (int e = tid; e < nrows * P.mb_cols; e += nthr) d[e] = g[e];
       __syncthreads();
     }
@@ -132,18 +143,16 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     // v = fl(sqrt(fl(dx^2 + dy^2))) / 4 is monotone in dx^2 + dy^2, so max_m v_m = v(max_m |mv_m|^2): the sqrt
     // is taken once per patch in pass 2 (bit-identical to the max of per-MB magnitudes).  INTRA -> sentinel.
     int badmb = 0;
-    const int lane_w = tid >> 5, nwarps = nthr >> 5;
-    const int cw = P.mb * P.grid_w;  // MB width in scaled x units
     for (int c = lane; c < P.grid_w; c += 32) {
       const int px0 = c * P.src_w, px1 = px0 + P.src_w;
-      const int i0 = px0 / cw, i1 = (px1 - 1) / cw;
+      const int2 ic = s_col[c];
       for (int row = lane_w; row < nrows; row += nwarps) {
         uint32_t msq = 0u, ssum = 0u;
-        for (int i = i0; i <= i1; ++i) {
-          const uint2 rec = buf[row * P.mb_cols + i];
+        const uint2* rr = buf + row * P.mb_cols;
+        for (int i = ic.x; i <= ic.y; ++i) {
+          const uint2 rec = rr[i];
           const int dx = static_cast<int16_t>(rec.x & 0xffffu);
           const int dy = static_cast<int16_t>(rec.x >> 16);
-          const uint32_t sad = rec.y & 0xffffu;
           const uint32_t type = (rec.y >> 16) & 0xffu;
           if (type <= CS_MB_SKIP) {
             const uint32_t sq = static_cast<uint32_t>(dx * dx) + static_cast<uint32_t>(dy * dy);
@@ -152,43 +161,56 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
             msq = kIntraSq;  // INTRA (or unknown) -> maximally dynamic (Q9)
             badmb |= (type > CS_MB_INTRA);
           }
-          const int ox = min(px1, cw * (i + 1)) - max(px0, cw * i);
-          ssum += static_cast<uint32_t>(ox) * sad;
+          if (P.use_r) {
+            const int ox = min(px1, cw * (i + 1)) - max(px0, cw * i);
+            ssum += static_cast<uint32_t>(ox) * (rec.y & 0xffffu);
+          }
         }
         const int j = r0 + row;
         Vrow[j * P.grid_w + c] = msq;
-        Srow[j * P.grid_w + c] = ssum;
+        if (P.use_r) Srow[j * P.grid_w + c] = ssum;
       }
     }
     if (badmb) s_badmb = 1;
     __syncthreads();  // chunk fully consumed, Vrow/Srow rows complete
-    if (P.use_bulk && tid == 0 && q + P.nstage < T) issue(q + P.nstage);
+    if (P.use_bulk && tid == 0 && q + P.nstage < T) issue_next();
+    if (++cs_ == P.nstage) { cs_ = 0; cph ^= 1; }
 
-    if (q % P.n_chunks == P.n_chunks - 1) {
+    if (++cc == P.n_chunks) {
+      cc = 0;
+      ++cf;
       // ---- pass 2: patch rows; Eq. 3 and Eq. 4; ballot into dynamic words ------------------------------
-      const int f = s_plist[q / P.n_chunks];
       const int lf = f - f_begin;
       const int ch = P.mb * P.grid_h;  // MB height in scaled y units
       for (int i = tid; i < nw * 32; i += nthr) {
         bool d = false, nr = false;
         if (i < P.np) {
-          const int r = i / P.grid_w;
+          const int r = P.gw_shift >= 0 ? (i >> P.gw_shift) : i / P.grid_w;
           const int c = i - r * P.grid_w;
           const int py0 = r * P.src_h, py1 = py0 + P.src_h;
-          const int j0 = py0 / ch, j1 = (py1 - 1) / ch;
+          const int2 jr = s_row[r];
           uint32_t msq = 0u;
           unsigned long long S = 0ull;
-          for (int j = j0; j <= j1; ++j) {
-            const int oy = min(py1, ch * (j + 1)) - max(py0, ch * j);
+          for (int j = jr.x; j <= jr.y; ++j) {
             const uint32_t mj = Vrow[j * P.grid_w + c];
             msq = mj > msq ? mj : msq;
-            S += static_cast<unsigned long long>(oy) * Srow[j * P.grid_w + c];
+            if (P.use_r) {
+              const int oy = min(py1, ch * (j + 1)) - max(py0, ch * j);
+              S += static_cast<unsigned long long>(oy) * Srow[j * P.grid_w + c];
+            }
           }
           // Eq. 1: V(i) = max over overlapping MBs of |mv| / 4 px
           const float V = msq == kIntraSq ? CUDART_INF_F : __fmul_rn(__fsqrt_rn(__uint2float_rn(msq)), 0.25f);
-          const float R = __double2float_rn(__ddiv_rn(static_cast<double>(S), P.denom));
-          const float M = isinf(V) ? CUDART_INF_F : __fmaf_rn(P.alpha, R, V);  // Eq. 3
-          d = (M >= P.tau);                                                  // Eq. 4 (inclusive, Q1)
+          float M;
+          if (isinf(V)) {
+            M = CUDART_INF_F;
+          } else if (P.use_r) {
+            const float R = __double2float_rn(__ddiv_rn(static_cast<double>(S), P.denom));
+            M = __fmaf_rn(P.alpha, R, V);  // Eq. 3
+          } else {
+            M = V;  // alpha == 0: fma(0, R, V) == V for every finite R >= 0 and V >= 0
+          }
+          d = (M >= P.tau);  // Eq. 4 (inclusive, Q1)
           nr = isfinite(M) && fabsf(__fsub_rn(M, P.tau)) <= 1e-5f;
           if (P.want_score) P.score[((long long)sidx * P.n_frames + f) * P.np + i] = M;
         }
@@ -255,17 +277,29 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     }
     if (tid == 0) s_kept = 0;
     __syncthreads();
-    const int ngc = P.grid_w / P.G;
-    for (int i = tid; i < nw * 32; i += nthr) {
-      bool k = false;
-      if (i < P.np) {
-        const int h = i / P.grid_w, w = i - h * P.grid_w;
-        k = cs::group_kept(s_out, (h / P.G) * ngc + (w / P.G), ngc, P.G, P.grid_w);
+    if (P.G == 2 && P.grid_w == 32) {
+      // word r = patch row r: a group row is rows 2g, 2g+1; fold horizontal pairs, spread back to both columns
+      for (int gr = tid; gr < P.grid_h / 2; gr += nthr) {
+        const uint32_t x = s_out[2 * gr] | s_out[2 * gr + 1];
+        const uint32_t y = (x | (x >> 1)) & 0x55555555u;
+        const uint32_t kw = y | (y << 1);
+        s_keep[2 * gr] = kw;
+        s_keep[2 * gr + 1] = kw;
+        atomicAdd(&s_kept, 2 * __popc(kw));
       }
-      const uint32_t word = __ballot_sync(0xffffffffu, k);
-      if (lane == 0) {
-        s_keep[i >> 5] = word;
-        atomicAdd(&s_kept, __popc(word));
+    } else {
+      const int ngc = P.grid_w / P.G;
+      for (int i = tid; i < nw * 32; i += nthr) {
+        bool k = false;
+        if (i < P.np) {
+          const int h = i / P.grid_w, w = i - h * P.grid_w;
+          k = cs::group_kept(s_out, (h / P.G) * ngc + (w / P.G), ngc, P.G, P.grid_w);
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, k);
+        if (lane == 0) {
+          s_keep[i >> 5] = word;
+          atomicAdd(&s_kept, __popc(word));
+        }
       }
     }
     __syncthreads();
@@ -336,6 +370,10 @@ int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const
   P.nstage = P.chunk_alloc <= 8192u ? 4 : 2;
   if (!P.use_bulk) P.nstage = 1;
   P.want_score = score != nullptr;
+  P.use_r = g->alpha != 0.0f;
+  P.gw_shift = -1;
+  for (int sh = 0; sh < 13; ++sh)
+    if ((1 << sh) == g->grid_w) P.gw_shift = sh;
   P.mb_ptr = mb;
   P.frame_type = frame_type;
   P.keep_mask = keep_mask;
@@ -353,6 +391,10 @@ int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const
   off += ((static_cast<unsigned>(P.fpc * P.nw) * 4u + 127u) & ~127u);
   P.off_bar = off;
   off += 64u;
+  P.off_col = off;
+  off += ((static_cast<unsigned>(g->grid_w) * 8u + 127u) & ~127u);
+  P.off_row = off;
+  off += ((static_cast<unsigned>(g->grid_h) * 8u + 127u) & ~127u);
   const size_t smem = off;
 
   if (smem > 200 * 1024) return CS_ERR_UNSUPPORTED;
