@@ -327,6 +327,45 @@ int codecsight_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs
 size_t codecsight_kv_refresh_paged_workspace_size(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win,
                                                   int32_t n_streams);
 
+/* ------------------------------------------------------------------------------------------------------------
+ * NEXT-4 — real H.264 metadata ingest and the similar-patch analysis.
+ *
+ * cs_av_mv is FFmpeg's AVMotionVector (libavutil/motion_vector.h, 40 bytes): the per-partition motion a software
+ * H.264 decoder exports (the "MV extraction" of the Codec Processor).
+ *
+ * codecsight_mv_rasterize: frame f's records mvs[mv_offsets[f] .. mv_offsets[f+1]) -> out[f] = its
+ * [mb_rows][mb_cols] cs_mb grid (the input of codecsight_score_patches).  Partition = destination rectangle
+ * [dst_x - w/2, dst_x - w/2 + w) x [dst_y - h/2, ...) px; an MB takes the motion vector of largest magnitude among
+ * the past-reference partitions (source < 0) overlapping it with positive area (ties: the earliest record) -- the
+ * conservative max of the patch resampling -- in quarter pel, trunc(4 * motion / motion_scale) clamped to
+ * int16, type INTER; an MB no partition covers was intra coded (FFmpeg exports no motion for it): INTRA.  SAD is not
+ * exported by FFmpeg: 0 (use alpha = 0).
+ *   mvs         device cs_av_mv records;  mv_offsets device [n_frames+1] i64;  out device [n_frames][rows][cols],
+ *               8-B aligned (used as scratch while arbitrating).
+ *
+ * codecsight_similar_hist: fig:mv_residual_analysis_cdf.  For every P-frame f and threshold
+ * taus[t]: count = #{i : score[f][i] < taus[t]} ("similar" patches), bin = min(count * n_bins / n_patches,
+ * n_bins - 1), hist[t][bin] += 1 (u64, accumulated).  The CDF over frames is the running sum of a row.
+ *   score device [n_frames][n_patches] fp32 (codecsight_score_patches' optional output); frame_type device
+ *   [n_frames]; taus device [n_tau] fp32; hist device [n_tau][n_bins] u64.
+ * --------------------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t source;       /* < 0: past reference, > 0: future (B-frames, ignored)                            */
+  uint8_t w, h;         /* partition size in px                                                           */
+  int16_t src_x, src_y; /* source position (unused)                                                      */
+  int16_t dst_x, dst_y; /* centre of the partition in the current frame, px                              */
+  uint64_t flags;
+  int32_t motion_x, motion_y; /* motion in 1/motion_scale px                                             */
+  uint16_t motion_scale;
+} cs_av_mv;
+
+int codecsight_mv_rasterize(const cs_grid* g, int32_t n_frames, const cs_av_mv* mvs, const int64_t* mv_offsets,
+                            cs_mb* out, cudaStream_t stream);
+
+int codecsight_similar_hist(const float* score, const uint8_t* frame_type, int64_t n_frames, int32_t n_patches,
+                            const float* taus, int32_t n_tau, int32_t n_bins, unsigned long long* hist,
+                            cudaStream_t stream);
+
 /* Bytes of device workspace codecsight_kv_refresh needs for this window and stream count (0 on bad args). */
 size_t codecsight_kv_refresh_workspace_size(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams);
 

@@ -777,3 +777,79 @@ int codecsight_ref_compact_nv12(const ref_grid* g, const ref_pre* pp, int32_t n_
   counters[REF_C_BYTES_COMPACT] += (unsigned long long)(n_slots * (4 * nw + 4) + written * (row * 2 + 16));
   return 0;
 }
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* NEXT-4 (a): real H.264 metadata ingest.  FFmpeg exports a frame's motion as AVMotionVector records      */
+/* (libavutil/motion_vector.h) per coded partition (4x4 .. 16x16, the decoder's "MV extraction"):  */
+/* destination centre (dst_x, dst_y), size w x h, motion (motion_x, motion_y) / motion_scale pixels.       */
+/* Rasterised onto the 16x16 MB grid (reading NEXT-4): an MB takes the motion vector of largest magnitude  */
+/* among the past-reference partitions (source < 0) overlapping it with positive area (ties: the first     */
+/* record) -- the same conservative max that the patch resampling uses -- converted to quarter     */
+/* pel, mv_q = trunc(4 * motion / motion_scale) clamped to int16, type INTER; an MB that no partition      */
+/* covers was intra coded (no motion exported): type INTRA.  SAD is not exported by FFmpeg: 0.             */
+/* ---------------------------------------------------------------------------------------------------- */
+static int32_t ref_qpel(int32_t motion, int32_t scale) {
+  int64_t v = ((int64_t)motion * 4) / (scale > 0 ? scale : 1); /* C division truncates toward zero */
+  if (v > 32767) v = 32767;
+  if (v < -32768) v = -32768;
+  return (int32_t)v;
+}
+
+int codecsight_ref_mv_rasterize(const ref_grid* g, int32_t n_frames, const ref_av_mv* mvs, const int64_t* mv_offsets,
+                                ref_mb* out) {
+  if (!g || n_frames < 0 || (n_frames > 0 && (!mvs || !mv_offsets || !out))) return -1;
+  const int64_t cols = g->mb_cols, rows = g->mb_rows, mb = g->mb_size;
+  for (int64_t f = 0; f < n_frames; ++f) {
+    for (int64_t j = 0; j < rows; ++j)
+      for (int64_t i = 0; i < cols; ++i) {
+        int64_t best = -1, best_sq = -1;
+        for (int64_t r = mv_offsets[f]; r < mv_offsets[f + 1]; ++r) {
+          const ref_av_mv* m = &mvs[r];
+          if (m->source >= 0) continue;
+          /* partition rectangle [dst - size/2, dst - size/2 + size) in pixels */
+          const int64_t x0 = (int64_t)m->dst_x - m->w / 2, y0 = (int64_t)m->dst_y - m->h / 2;
+          const int64_t ox = (x0 + m->w < mb * (i + 1) ? x0 + m->w : mb * (i + 1)) - (x0 > mb * i ? x0 : mb * i);
+          const int64_t oy = (y0 + m->h < mb * (j + 1) ? y0 + m->h : mb * (j + 1)) - (y0 > mb * j ? y0 : mb * j);
+          if (ox <= 0 || oy <= 0) continue;
+          const int64_t qx = ref_qpel(m->motion_x, m->motion_scale), qy = ref_qpel(m->motion_y, m->motion_scale);
+          const int64_t sq = qx * qx + qy * qy;
+          if (sq > best_sq) { best_sq = sq; best = r; }
+        }
+        ref_mb* o = &out[(f * rows + j) * cols + i];
+        o->sad = 0;
+        o->reserved = 0;
+        if (best < 0) {
+          o->mvx_qpel = 0;
+          o->mvy_qpel = 0;
+          o->mb_type = REF_MB_INTRA;
+        } else {
+          o->mvx_qpel = (int16_t)ref_qpel(mvs[best].motion_x, mvs[best].motion_scale);
+          o->mvy_qpel = (int16_t)ref_qpel(mvs[best].motion_y, mvs[best].motion_scale);
+          o->mb_type = REF_MB_INTER;
+        }
+      }
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------------- */
+/* NEXT-4 (b): the similar-patch-ratio distribution of fig:mv_residual_analysis_cdf: */
+/* for every P-frame and threshold tau_t, the ratio of patches whose score is below tau_t ("similar") --   */
+/* count / n_patches -- falls in bin floor(count * n_bins / n_patches) (the last bin holds ratio 1);        */
+/* hist[t][bin] counts frames.  The CDF is the running sum of a row.                                       */
+/* ---------------------------------------------------------------------------------------------------- */
+int codecsight_ref_similar_hist(const float* score, const uint8_t* frame_type, int64_t n_frames, int32_t n_patches,
+                                const float* taus, int32_t n_tau, int32_t n_bins, unsigned long long* hist) {
+  if (n_frames < 0 || n_patches < 1 || n_tau < 1 || n_bins < 1) return -1;
+  for (int64_t f = 0; f < n_frames; ++f) {
+    if (frame_type[f] != REF_FRAME_P) continue;
+    for (int32_t t = 0; t < n_tau; ++t) {
+      int64_t cnt = 0;
+      for (int32_t i = 0; i < n_patches; ++i) cnt += (score[f * n_patches + i] < taus[t]) ? 1 : 0;
+      int64_t bin = cnt * n_bins / n_patches;
+      if (bin >= n_bins) bin = n_bins - 1;
+      hist[(int64_t)t * n_bins + bin] += 1;
+    }
+  }
+  return 0;
+}

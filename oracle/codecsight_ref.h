@@ -123,6 +123,20 @@ int codecsight_ref_compact_nv12(const ref_grid* g, const ref_pre* pp, int32_t n_
                                 void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
                                 unsigned long long* counters, int32_t* status);
 
+/* NEXT-4: FFmpeg AVMotionVector records -> MB grid; similar-patch-ratio histogram. */
+typedef struct {
+  int32_t source;
+  uint8_t w, h;
+  int16_t src_x, src_y, dst_x, dst_y;
+  uint64_t flags;
+  int32_t motion_x, motion_y;
+  uint16_t motion_scale;
+} ref_av_mv;
+int codecsight_ref_mv_rasterize(const ref_grid* g, int32_t n_frames, const ref_av_mv* mvs, const int64_t* mv_offsets,
+                                ref_mb* out);
+int codecsight_ref_similar_hist(const float* score, const uint8_t* frame_type, int64_t n_frames, int32_t n_patches,
+                                const float* taus, int32_t n_tau, int32_t n_bins, unsigned long long* hist);
+
 /* Eq. 5 on one fp32 key vector of n_heads x head_dim: out = R(dp) k (rotate_half pairing). */
 void codecsight_ref_rope_rotate_f32(const float* k, int32_t n_heads, int32_t head_dim, double base, int64_t dp,
                                     float* out);

@@ -103,6 +103,10 @@ def lib():
         L.codecsight_ref_compact_nv12.restype = C.c_int
         L.codecsight_ref_compact_nv12.argtypes = [C.POINTER(RefGrid), C.POINTER(RefPre), C.c_int32, C.c_int32, P,
                                                   C.c_int64, P, P, P, C.c_int64, P, P, P, P, P, P]
+        L.codecsight_ref_mv_rasterize.restype = C.c_int
+        L.codecsight_ref_mv_rasterize.argtypes = [C.POINTER(RefGrid), C.c_int32, P, P, P]
+        L.codecsight_ref_similar_hist.restype = C.c_int
+        L.codecsight_ref_similar_hist.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int32, C.c_int32, P]
         L.codecsight_ref_rope_rotate_f32.restype = None
         L.codecsight_ref_rope_rotate_f32.argtypes = [P, C.c_int32, C.c_int32, C.c_double, C.c_int64, P]
         _lib = L
@@ -312,3 +316,29 @@ def compact_nv12(g: dict, pre: RefPre, keep_mask: np.ndarray, frame_index: np.nd
                                            _p(status))
     return dict(rc=rc, packed=packed, pos_ids=pos, src_index=src, frame_offsets=offs, counters=counters,
                 status=int(status[0]))
+
+
+AV_MV_DTYPE = np.dtype([("source", "<i4"), ("w", "u1"), ("h", "u1"), ("src_x", "<i2"), ("src_y", "<i2"),
+                        ("dst_x", "<i2"), ("dst_y", "<i2"), ("pad0", "<u2"), ("flags", "<u8"), ("motion_x", "<i4"),
+                        ("motion_y", "<i4"), ("motion_scale", "<u2"), ("pad1", "u1", (6,))])
+assert AV_MV_DTYPE.itemsize == 40
+
+
+def mv_rasterize(g: dict, mvs: np.ndarray, mv_offsets: np.ndarray, n_frames: int) -> np.ndarray:
+    out = np.zeros((n_frames, g["mb_rows"], g["mb_cols"]), MB_DTYPE)
+    mvs = np.ascontiguousarray(mvs, dtype=AV_MV_DTYPE)
+    offs = np.ascontiguousarray(mv_offsets, dtype=np.int64)
+    rc = lib().codecsight_ref_mv_rasterize(C.byref(make_grid(g)), n_frames, _p(mvs), _p(offs), _p(out))
+    assert rc == 0
+    return out
+
+
+def similar_hist(score: np.ndarray, frame_type: np.ndarray, taus, n_bins: int) -> np.ndarray:
+    score = np.ascontiguousarray(score, dtype=np.float32)
+    n_frames, n_patches = score.shape
+    taus = np.ascontiguousarray(taus, dtype=np.float32)
+    hist = np.zeros((len(taus), n_bins), np.uint64)
+    rc = lib().codecsight_ref_similar_hist(_p(score), _p(np.ascontiguousarray(frame_type, dtype=np.uint8)), n_frames,
+                                           n_patches, _p(taus), len(taus), n_bins, _p(hist))
+    assert rc == 0
+    return hist

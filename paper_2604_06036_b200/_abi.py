@@ -86,6 +86,10 @@ def lib():
         L.codecsight_compact_nv12.restype = C.c_int
         L.codecsight_compact_nv12.argtypes = [C.POINTER(CsGrid), C.POINTER(CsPreprocess), I32, I32, P, I64, P, P, P,
                                               I64, P, P, P, P, P, P, P]
+        L.codecsight_mv_rasterize.restype = C.c_int
+        L.codecsight_mv_rasterize.argtypes = [C.POINTER(CsGrid), I32, P, P, P, P]
+        L.codecsight_similar_hist.restype = C.c_int
+        L.codecsight_similar_hist.argtypes = [P, P, I64, I32, P, I32, I32, P, P]
         L.codecsight_kv_refresh.restype = C.c_int
         L.codecsight_kv_refresh.argtypes = [C.POINTER(CsGrid), C.POINTER(CsKvDesc), C.POINTER(CsWindow), I32, P, P,
                                             P, P, P, I64, P, P, P, P, C.c_size_t, P, P, P]
@@ -185,6 +189,19 @@ def codecsight_compact_nv12(g: dict, pre: dict, n_streams: int, n_frames: int, k
     _check(rc, "codecsight_compact_nv12")
 
 
+def codecsight_mv_rasterize(g: dict, n_frames: int, mvs, mv_offsets, out, stream=None) -> None:
+    rc = lib().codecsight_mv_rasterize(C.byref(make_grid(g)), n_frames, _ptr(mvs), _ptr(mv_offsets), _ptr(out),
+                                       _stream(stream))
+    _check(rc, "codecsight_mv_rasterize")
+
+
+def codecsight_similar_hist(score, frame_type, n_frames: int, n_patches: int, taus, n_tau: int, n_bins: int, hist,
+                            stream=None) -> None:
+    rc = lib().codecsight_similar_hist(_ptr(score), _ptr(frame_type), n_frames, n_patches, _ptr(taus), n_tau, n_bins,
+                                       _ptr(hist), _stream(stream))
+    _check(rc, "codecsight_similar_hist")
+
+
 def kv_workspace_size(kv: dict, win: dict, n_streams: int) -> int:
     return int(lib().codecsight_kv_refresh_workspace_size(C.byref(make_kv(kv)), C.byref(make_window(win)),
                                                           n_streams))
@@ -224,4 +241,6 @@ kv_refresh_paged = codecsight_kv_refresh_paged
 score_patches = codecsight_score_patches
 compact = codecsight_compact
 compact_nv12 = codecsight_compact_nv12
+mv_rasterize = codecsight_mv_rasterize
+similar_hist = codecsight_similar_hist
 kv_refresh = codecsight_kv_refresh

@@ -179,6 +179,30 @@ int codecsight_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n
                                 stream);
 }
 
+int codecsight_mv_rasterize(const cs_grid* g, int32_t n_frames, const cs_av_mv* mvs, const int64_t* mv_offsets,
+                            cs_mb* out, cudaStream_t stream) {
+  int rc = grid_ok(g);
+  if (rc) return rc;
+  if (n_frames < 0) return CS_ERR_INVALID_ARGUMENT;
+  if (n_frames == 0) return CS_OK;
+  if (!mvs || !mv_offsets || !out) return CS_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(out) & 7u) != 0) return CS_ERR_INVALID_ARGUMENT;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_mv_rasterize(g, n_frames, mvs, mv_offsets, out, stream);
+}
+
+int codecsight_similar_hist(const float* score, const uint8_t* frame_type, int64_t n_frames, int32_t n_patches,
+                            const float* taus, int32_t n_tau, int32_t n_bins, unsigned long long* hist,
+                            cudaStream_t stream) {
+  if (n_frames < 0 || n_patches < 1 || n_tau < 1 || n_bins < 1) return CS_ERR_INVALID_ARGUMENT;
+  if (n_frames == 0) return CS_OK;
+  if (!score || !frame_type || !taus || !hist) return CS_ERR_INVALID_ARGUMENT;
+  if (n_frames * n_tau > (1ll << 40)) return CS_ERR_UNSUPPORTED;
+  int rc;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_similar_hist(score, frame_type, n_frames, n_patches, taus, n_tau, n_bins, hist, stream);
+}
+
 size_t codecsight_kv_refresh_workspace_size(const cs_kv_desc* kv, const cs_window* win, int32_t n_streams) {
   if (!kv || !win || n_streams < 0 || win->window < 1 || kv->head_dim < 2 || kv->head_dim > cs::kMaxHeadDim)
     return 0;

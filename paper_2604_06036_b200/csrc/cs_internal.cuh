@@ -171,6 +171,11 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
                                int32_t* status, cudaStream_t stream);
 size_t cs_kv_paged_workspace_bytes(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win,
                                    int32_t n_streams);
+int cs_launch_mv_rasterize(const cs_grid* g, int32_t n_frames, const cs_av_mv* mvs, const int64_t* mv_offsets,
+                           cs_mb* out, cudaStream_t stream);
+int cs_launch_similar_hist(const float* score, const uint8_t* frame_type, int64_t n_frames, int32_t n_patches,
+                           const float* taus, int32_t n_tau, int32_t n_bins, unsigned long long* hist,
+                           cudaStream_t stream);
 int cs_num_sms();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel slot, device); 0 on success
 int cs_set_smem_attr(const void* func, int slot, int bytes);

@@ -735,3 +735,58 @@ def test_compact_nv12(abi, ref, geom):
         got = packed.cpu().numpy().view(np.uint16)[:rows]
         assert (got == o["packed"][:rows]).all(), int((got != o["packed"][:rows]).sum())
         assert (cnt.cpu().numpy().view(np.uint64) == o["counters"]).all()
+
+
+# ------------------------------------------------------------------------------------------------------------
+# NEXT-4: AVMotionVector rasterisation and the similar-patch histogram
+# ------------------------------------------------------------------------------------------------------------
+def _random_avmv(ref, g, n_frames, rng):
+    recs = []
+    offs = [0]
+    for f in range(n_frames):
+        n = int(rng.integers(0, 3 * g["mb_rows"] * g["mb_cols"]))
+        a = np.zeros(n, ref.AV_MV_DTYPE)
+        a["source"] = rng.choice([-1, -1, -1, 1], size=n)
+        a["w"] = rng.choice([4, 8, 16], size=n)
+        a["h"] = rng.choice([4, 8, 16], size=n)
+        a["dst_x"] = rng.integers(-8, g["src_w"] + 8, size=n)
+        a["dst_y"] = rng.integers(-8, g["src_h"] + 8, size=n)
+        a["motion_x"] = rng.integers(-40, 41, size=n)
+        a["motion_y"] = rng.integers(-40, 41, size=n)
+        a["motion_scale"] = rng.choice([1, 2, 4], size=n)
+        recs.append(a)
+        offs.append(offs[-1] + n)
+    return np.concatenate(recs), np.array(offs, np.int64)
+
+
+@pytest.mark.parametrize("src", [(448, 448), (1920, 1080), (100, 60)])
+def test_mv_rasterize_gpu(abi, ref, src):
+    g = make_grid(*src)
+    rng = np.random.default_rng(src[0])
+    n = 5
+    mvs, offs = _random_avmv(ref, g, n, rng)
+    out_d = torch.zeros(n * g["mb_rows"] * g["mb_cols"], dtype=torch.int64, device=DEV)
+    abi.codecsight_mv_rasterize(g, n, torch.from_numpy(mvs.view(np.uint8)).to(DEV), torch.from_numpy(offs).to(DEV),
+                                out_d)
+    exp = ref.mv_rasterize(g, mvs, offs, n)
+    torch.cuda.synchronize()
+    got = out_d.cpu().numpy().view(MB_DTYPE).reshape(exp.shape)
+    for f in ("mvx", "mvy", "sad", "type"):
+        assert (got[f] == exp[f]).all(), f
+
+
+def test_similar_hist_gpu(abi, ref):
+    g = make_grid(1920, 1080)
+    S, n = 8, 8
+    mb = np.stack([synth.stream_metadata(1920, 1080, sc, 40 + i, n) for i, sc in
+                   enumerate(["low", "medium", "high", "noise"] * 2)])
+    types = np.stack([synth.frame_types(n, 16, 5)] * S)
+    sc = ref.score_patches(g, mb, types, np.zeros((S, 33), np.uint32))["score"]
+    taus = np.array([0.25, 0.5, 1.0, 2.0, 5.0], np.float32)
+    hist_d = torch.zeros(5, 50, dtype=torch.int64, device=DEV)
+    abi.codecsight_similar_hist(torch.from_numpy(sc.reshape(S * n, -1)).to(DEV),
+                                torch.from_numpy(types.reshape(-1)).to(DEV), S * n, 1024,
+                                torch.from_numpy(taus).to(DEV), 5, 50, hist_d)
+    exp = ref.similar_hist(sc.reshape(S * n, -1), types.reshape(-1), taus, 50)
+    torch.cuda.synchronize()
+    assert (hist_d.cpu().numpy().view(np.uint64) == exp).all()
