@@ -265,6 +265,86 @@ int codecsight_ref_compact(const ref_grid* g, int32_t n_streams, int32_t n_frame
 }
 
 /* ---------------------------------------------------------------------------------------------------- */
+/* NEXT-3: temporal patches.  Qwen2-VL embeds video with temporal_patch_size = 2 (P:399 names the
+ * Qwen-VL models): one visual token covers tp consecutive frames and its patch row is [3][tp][p][p] (channel, then
+ * frame, then pixels -- the Hugging Face processor's flatten order).  Pruning reading: a group of a unit is emitted
+ * iff any of its patches is kept in ANY of the unit's frames (the union keeps every dynamic pixel).  Unit u of
+ * stream s uses frames[(s*n_units + u)*tp + f] and masks keep_mask[s][u*tp + f], f < tp.                     */
+/* ---------------------------------------------------------------------------------------------------- */
+int codecsight_ref_compact_tp(const ref_grid* g, int32_t tp, int32_t n_streams, int32_t n_units,
+                              const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* unit_index,
+                              const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
+                              int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, uint32_t* unit_mask,
+                              int64_t unit_mask_stride, unsigned long long* counters, int32_t* status) {
+  int rc = ref_grid_ok(g);
+  if (rc) return rc;
+  if (tp < 1 || tp > 4) return -3;
+  if (n_streams < 0 || n_units < 1 || mask_frame_stride < (int64_t)n_units * tp || capacity < 0) return -1;
+  if (unit_mask && unit_mask_stride < n_units) return -1;
+  if (frame_layout != REF_LAYOUT_PLANAR && frame_layout != REF_LAYOUT_GROUPED) return -1;
+  const int64_t np = (int64_t)g->grid_w * g->grid_h, nw = ref_words(g), G = g->group, p = g->patch;
+  const int64_t n_slots = (int64_t)n_streams * n_units;
+  if (n_slots * np >= 2147483648LL) return -3;
+  if (!frame_offsets || !counters || !status) return -1;
+  if (n_slots > 0 && (!keep_mask || !unit_index || !frames)) return -1;
+  if (capacity > 0 && (!packed || !pos_ids || !src_index)) return -1;
+
+  const int64_t fh = g->grid_h * p, fw = g->grid_w * p;
+  const int64_t row = 3 * tp * p * p; /* elements of one packed row: [3][tp][p][p] */
+  uint16_t* out = (uint16_t*)packed;
+  int64_t off = 0, written = 0;
+  for (int64_t s = 0; s < n_streams; ++s)
+    for (int64_t u = 0; u < n_units; ++u) {
+      const int64_t slot = s * n_units + u;
+      frame_offsets[slot] = (int32_t)off;
+      if (unit_mask)
+        for (int64_t t = 0; t < nw; ++t) {
+          uint32_t w = 0;
+          for (int64_t f = 0; f < tp; ++f) w |= keep_mask[(s * mask_frame_stride + u * tp + f) * nw + t];
+          unit_mask[(s * unit_mask_stride + u) * nw + t] = w;
+        }
+      for (int64_t gr = 0; gr < g->grid_h / G; ++gr)
+        for (int64_t gc = 0; gc < g->grid_w / G; ++gc) {
+          int any = 0;
+          for (int64_t f = 0; f < tp; ++f) {
+            const uint32_t* m = keep_mask + (s * mask_frame_stride + u * tp + f) * nw;
+            for (int64_t dy = 0; dy < G; ++dy)
+              for (int64_t dx = 0; dx < G; ++dx) any |= ref_bit(m, (gr * G + dy) * g->grid_w + gc * G + dx);
+          }
+          if (!any) continue;
+          for (int64_t dy = 0; dy < G; ++dy)
+            for (int64_t dx = 0; dx < G; ++dx) {
+              const int64_t h = gr * G + dy, w = gc * G + dx, n = off++;
+              if (n >= capacity) { *status |= REF_ST_CAPACITY; continue; }
+              for (int64_t c = 0; c < 3; ++c)
+                for (int64_t f = 0; f < tp; ++f) {
+                  const uint16_t* fr = (const uint16_t*)frames[slot * tp + f];
+                  for (int64_t y = 0; y < p; ++y)
+                    for (int64_t x = 0; x < p; ++x) {
+                      int64_t src;
+                      if (frame_layout == REF_LAYOUT_PLANAR)
+                        src = c * fh * fw + (h * p + y) * fw + (w * p + x);
+                      else
+                        src = (((gr * (g->grid_w / G) + gc) * G * G + dy * G + dx) * 3 + c) * p * p + y * p + x;
+                      out[n * row + ((c * tp + f) * p + y) * p + x] = fr[src];
+                    }
+                }
+              pos_ids[3 * n + 0] = unit_index[slot];
+              pos_ids[3 * n + 1] = (int32_t)h;
+              pos_ids[3 * n + 2] = (int32_t)w;
+              src_index[n] = (int32_t)(slot * np + h * g->grid_w + w);
+              ++written;
+            }
+        }
+    }
+  frame_offsets[n_slots] = (int32_t)off;
+  counters[REF_C_PACKED_ROWS] += (unsigned long long)written;
+  counters[REF_C_BYTES_COMPACT] += (unsigned long long)(n_slots * (4 * nw * tp + 4) + written * (2 * row * 2 + 16) +
+                                                        (unit_mask ? n_slots * 4 * nw : 0));
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------------- */
 /* Eq. 5: K^_t(j) = R(p_new - p_old) K_{t-1}(j), rotate_half pairing (reading Q19-Q21).      */
 /* ---------------------------------------------------------------------------------------------------- */
 static void ref_rot_pair(float x1, float x2, int64_t i, int64_t D, double base, int64_t dp, float* o1, float* o2) {

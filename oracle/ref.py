@@ -86,6 +86,9 @@ def lib():
         L.codecsight_ref_compact.restype = C.c_int
         L.codecsight_ref_compact.argtypes = [C.POINTER(RefGrid), C.c_int32, C.c_int32, P, C.c_int64, P, P,
                                              C.c_int32, C.c_int64, P, P, P, P, P, P]
+        L.codecsight_ref_compact_tp.restype = C.c_int
+        L.codecsight_ref_compact_tp.argtypes = [C.POINTER(RefGrid), C.c_int32, C.c_int32, C.c_int32, P, C.c_int64, P,
+                                                P, C.c_int32, C.c_int64, P, P, P, P, P, C.c_int64, P, P]
         L.codecsight_ref_kv_refresh.restype = C.c_int
         L.codecsight_ref_kv_refresh.argtypes = [C.POINTER(RefGrid), C.POINTER(RefKv), C.POINTER(RefWindow),
                                                 C.c_int32, P, P, P, P, P, C.c_int64, P, P, P, P, P]
@@ -194,6 +197,34 @@ def compact(g: dict, keep_mask: np.ndarray, frame_index: np.ndarray, frames: lis
                                       _p(src), _p(offs), _p(counters), _p(status))
     return dict(rc=rc, packed=packed, pos_ids=pos, src_index=src, frame_offsets=offs, counters=counters,
                 status=int(status[0]))
+
+
+def compact_tp(g: dict, tp: int, keep_mask: np.ndarray, unit_index: np.ndarray, frames: list, capacity: int,
+               n_streams: int, n_units: int, mask_frame_stride: int | None = None, frame_layout: int = 0,
+               want_unit_mask: bool = False, counters: np.ndarray | None = None):
+    """NEXT-3 temporal patches: keep_mask [S][mask_frame_stride][words] (per frame); frames: n_slots*tp arrays."""
+    nw = grid_words(g)
+    mfs = n_units * tp if mask_frame_stride is None else mask_frame_stride
+    keep_mask = np.ascontiguousarray(keep_mask, dtype=np.uint32).reshape(n_streams, mfs, nw)
+    n_slots = n_streams * n_units
+    unit_index = np.ascontiguousarray(unit_index, dtype=np.int32).reshape(n_slots)
+    frames = [np.ascontiguousarray(f, dtype=np.uint16) for f in frames]
+    assert len(frames) == n_slots * tp
+    ptrs = (C.c_void_p * max(1, len(frames)))(*[f.ctypes.data for f in frames])
+    row = 3 * tp * g["patch"] * g["patch"]
+    packed = np.zeros((max(capacity, 0), row), np.uint16)
+    pos = np.zeros((max(capacity, 0), 3), np.int32)
+    src = np.zeros(max(capacity, 0), np.int32)
+    offs = np.zeros(n_slots + 1, np.int32)
+    um = np.zeros((n_streams, n_units, nw), np.uint32) if want_unit_mask else None
+    counters = np.zeros(NCOUNTERS, np.uint64) if counters is None else counters
+    status = np.zeros(1, np.int32)
+    rc = lib().codecsight_ref_compact_tp(C.byref(make_grid(g)), tp, n_streams, n_units, _p(keep_mask), mfs,
+                                         _p(unit_index), C.cast(ptrs, C.c_void_p), frame_layout, capacity,
+                                         _p(packed), _p(pos), _p(src), _p(offs), _p(um) if um is not None else None,
+                                         n_units, _p(counters), _p(status))
+    return dict(rc=rc, packed=packed, pos_ids=pos, src_index=src, frame_offsets=offs, unit_mask=um,
+                counters=counters, status=int(status[0]))
 
 
 def kv_desc(layers, kv_heads, head_dim, dtype, capacity, refresh_capacity, rope_base, n_prompt, rope_mode=0,
