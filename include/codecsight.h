@@ -189,6 +189,30 @@ int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, co
                        cudaStream_t stream);
 
 /* ------------------------------------------------------------------------------------------------------------
+ * codecsight_compact_tp — NEXT-3: temporal patches.  Qwen2-VL / Qwen3-VL embed video with
+ * temporal_patch_size 2: one visual token covers `temporal_patch` consecutive frames and its patch row is
+ * [3][temporal_patch][patch][patch] (channel, frame, y, x -- the Hugging Face processor's flatten order).
+ * Token unit u of stream sigma = frames u*tp .. u*tp+tp-1 of the stream: their bf16 frames are
+ * frames[(sigma*n_units + u)*tp + f] and their masks keep_mask[sigma][u*tp + f] (f < tp).  Reading: a group of the
+ * unit is emitted iff any of its patches is kept in ANY frame of the unit (the union keeps every dynamic pixel).
+ *   packed[n][c][f][y][x] = frame f of the unit, pixel (c, patch*h + y, patch*w + x)
+ *   pos_ids[n] = (unit_index[slot], h, w); src_index[n] = slot*grid_h*grid_w + h*grid_w + w; slot = sigma*n_units+u
+ *   unit_mask  optional device [n_streams][unit_mask_stride][grid_words] u32 out: OR of the unit's frame masks
+ *              (the per-unit mask a token-unit KV ring is built from); NULL = not written
+ * Order, offsets, capacity and status as codecsight_compact (rows of 3*tp*patch^2 bf16); temporal_patch = 1 is
+ * codecsight_compact.  A clip whose length is not a multiple of tp repeats its last frame (pass the same pointer
+ * and mask twice), as the Hugging Face processor does.  Limits: 1 <= temporal_patch <= 4; 8 tiles of
+ * 3*tp*(group*patch)^2 bf16 fit 227 KB of shared memory (else CS_ERR_UNSUPPORTED).
+ *   counters: BYTES_COMPACT (+ 4*tp*grid_words+4 per unit, + 4*grid_words per unit mask written), PACKED_ROWS
+ * --------------------------------------------------------------------------------------------------------- */
+int codecsight_compact_tp(const cs_grid* g, int32_t temporal_patch, int32_t n_streams, int32_t n_units,
+                          const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* unit_index,
+                          const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
+                          int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, uint32_t* unit_mask,
+                          int64_t unit_mask_stride, unsigned long long* counters, int32_t* status,
+                          cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------------------------------
  * codecsight_compact_nv12 — NEXT-2: the GPU preprocessing fused into the compaction ("Resizing, color-space
  * conversion, and normalization are fused into a single batched operation over all frames"): the frames are the
  * decoder's NV12 output and only the kept groups are converted, resized and normalised -- pruned patches are never

@@ -121,6 +121,34 @@ int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, co
                            packed, pos_ids, src_index, frame_offsets, counters, status, stream);
 }
 
+int codecsight_compact_tp(const cs_grid* g, int32_t temporal_patch, int32_t n_streams, int32_t n_units,
+                          const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* unit_index,
+                          const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
+                          int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, uint32_t* unit_mask,
+                          int64_t unit_mask_stride, unsigned long long* counters, int32_t* status,
+                          cudaStream_t stream) {
+  int rc = grid_ok(g);
+  if (rc) return rc;
+  if (temporal_patch < 1 || temporal_patch > 4) return CS_ERR_UNSUPPORTED;
+  if (n_streams < 0 || n_units < 1 || capacity < 0) return CS_ERR_INVALID_ARGUMENT;
+  if (mask_frame_stride < static_cast<long long>(n_units) * temporal_patch) return CS_ERR_INVALID_ARGUMENT;
+  if (unit_mask && unit_mask_stride < n_units) return CS_ERR_INVALID_ARGUMENT;
+  if (frame_layout != CS_LAYOUT_PLANAR && frame_layout != CS_LAYOUT_GROUPED) return CS_ERR_INVALID_ARGUMENT;
+  const long long n_slots = static_cast<long long>(n_streams) * n_units;
+  if (n_slots * g->grid_w * g->grid_h >= 2147483648LL) return CS_ERR_UNSUPPORTED;
+  if (g->group * g->patch > 32) return CS_ERR_UNSUPPORTED;
+  // per-warp staging tile of one group (x 8 warps) must fit the 227 KB of shared memory
+  const long long tile = (3ll * temporal_patch * g->group * g->group * g->patch * g->patch * 2 + 15) & ~15ll;
+  if (8 * (tile + 4ll * ((g->grid_w * g->grid_h + 31) / 32)) > 227 * 1024) return CS_ERR_UNSUPPORTED;
+  if (!frame_offsets || !counters || !status) return CS_ERR_INVALID_ARGUMENT;
+  if (n_slots > 0 && (!keep_mask || !unit_index || !frames)) return CS_ERR_INVALID_ARGUMENT;
+  if (capacity > 0 && (!packed || !pos_ids || !src_index)) return CS_ERR_INVALID_ARGUMENT;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_compact_tp(g, temporal_patch, n_streams, n_units, keep_mask, mask_frame_stride, unit_index, frames,
+                              frame_layout, capacity, packed, pos_ids, src_index, frame_offsets, unit_mask,
+                              unit_mask_stride, counters, status, stream);
+}
+
 int codecsight_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
                                 const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring, void* const* pool,
                                 const int32_t* slot_old, int32_t* slot_new, int64_t slot_cap,

@@ -22,13 +22,18 @@ constexpr int kWarpsPerCta = kGatherThreads / 32;
 
 constexpr int kLayoutNV12 = 2;  // internal: frames are decoded NV12 planes, preprocessing fused (NEXT-2)
 
-// per-warp tile of one group in packed order: 3 x (group*patch)^2 bf16, padded to 16 B
-__host__ __device__ __forceinline__ int tile_bytes_of(int p, int G) { return ((3 * G * G * p * p * 2) + 15) & ~15; }
+// per-warp tile of one group in packed order: 3 x tp x (group*patch)^2 bf16, padded to 16 B
+__host__ __device__ __forceinline__ int tile_bytes_of(int p, int G, int tp = 1) {
+  return ((3 * tp * G * G * p * p * 2) + 15) & ~15;
+}
 
 struct CompactParams {
   int grid_w, grid_h, G, p, np, nw, ngc, ngroups;
-  int n_streams, n_frames, n_slots;
+  int n_streams, n_frames, n_slots;  // n_frames = token units per stream (frames when tp == 1)
+  int tp;                             // temporal patch: frames per token unit (NEXT-3, Qwen2-VL: 2)
   long long mask_frame_stride;
+  uint32_t* unit_mask;                // optional [n_streams][unit_mask_stride][nw] OR of the unit's masks
+  long long unit_mask_stride;
   long long capacity;
   int FH, FW;  // model-input frame height / width in pixels
   int vec_out;
@@ -49,15 +54,30 @@ struct CompactParams {
   int32_t* status;
 };
 
-__device__ __forceinline__ const uint32_t* slot_mask(const CompactParams& P, int slot) {
+// mask of frame f of token unit `slot` (frame j*tp + f of its stream)
+__device__ __forceinline__ const uint32_t* slot_mask(const CompactParams& P, int slot, int f = 0) {
   const int s = slot / P.n_frames, j = slot - s * P.n_frames;
-  return P.keep_mask + ((long long)s * P.mask_frame_stride + j) * P.nw;
+  return P.keep_mask + ((long long)s * P.mask_frame_stride + (long long)j * P.tp + f) * P.nw;
+}
+
+// word t of the unit mask: OR over the unit's tp frames (a group is emitted iff kept in any of them)
+__device__ __forceinline__ uint32_t unit_word(const CompactParams& P, int slot, int t) {
+  const uint32_t* m = slot_mask(P, slot);
+  uint32_t w = __ldg(m + t);
+  for (int f = 1; f < P.tp; ++f) w |= __ldg(m + (long long)f * P.nw + t);
+  return w;
+}
+
+__device__ __forceinline__ void put_unit_word(const CompactParams& P, int slot, int t, uint32_t w) {
+  const int s = slot / P.n_frames, j = slot - s * P.n_frames;
+  P.unit_mask[((long long)s * P.unit_mask_stride + j) * P.nw + t] = w;
 }
 
 __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_constant__ CompactParams P) {
   __shared__ int s_warp[kScanThreads / 32];
   __shared__ int s_cnt[kScanThreads];
   __shared__ int s_carry;
+  __shared__ uint32_t s_m[kScanThreads / 32][128];  // per-warp unit mask (grid_words <= 128)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gs2 = P.G * P.G;
   const bool fast = (P.G == 2 && P.grid_w == 32 && P.nw <= 32);  // one mask word per patch row, one per lane
@@ -71,7 +91,16 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
 #pragma unroll
       for (int i = 0; i < kScanThreads / 32; ++i) {
         const int slot = base + warp + 32 * i;
-        wv[i] = (slot < P.n_slots && lane < P.nw) ? __ldg(slot_mask(P, slot) + lane) : 0u;
+        wv[i] = (slot < P.n_slots && lane < P.nw) ? (P.tp == 1 ? __ldg(slot_mask(P, slot) + lane)
+                                                                  : unit_word(P, slot, lane))
+                                                  : 0u;
+      }
+      if (P.unit_mask) {
+#pragma unroll
+        for (int i = 0; i < kScanThreads / 32; ++i) {
+          const int slot = base + warp + 32 * i;
+          if (slot < P.n_slots && lane < P.nw) put_unit_word(P, slot, lane, wv[i]);
+        }
       }
 #pragma unroll
       for (int i = 0; i < kScanThreads / 32; ++i) {
@@ -88,12 +117,22 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
         int c = 0;
         if (slot < P.n_slots) {
           const uint32_t* m = slot_mask(P, slot);
+          if (P.tp > 1 || P.unit_mask) {
+            for (int t = lane; t < P.nw; t += 32) {
+              const uint32_t w = unit_word(P, slot, t);
+              s_m[warp][t] = w;
+              if (P.unit_mask) put_unit_word(P, slot, t, w);
+            }
+            __syncwarp();
+            m = s_m[warp];
+          }
           for (int q0 = 0; q0 < P.ngroups; q0 += 32) {
             const int q = q0 + lane;
             c += __popc(__ballot_sync(0xffffffffu, q < P.ngroups && cs::group_kept(m, q, P.ngc, P.G, P.grid_w)));
           }
         }
         if (lane == 0) s_cnt[j] = c * gs2;
+        __syncwarp();
       }
     }
     __syncthreads();
@@ -129,13 +168,14 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
     P.frame_offsets[P.n_slots] = static_cast<int32_t>(total);
     const long long rows = total < P.capacity ? total : P.capacity;
     if (total > P.capacity) cs::atomic_or_status(P.status, CS_STATUS_CAPACITY);
-    const unsigned long long row_bytes = 3ull * P.p * P.p * 2ull;
+    const unsigned long long row_bytes = 3ull * P.tp * P.p * P.p * 2ull;
     cs::atomic_add_u64(&P.counters[CS_CNT_PACKED_ROWS], static_cast<unsigned long long>(rows));
     // per packed row: its bytes read from the frame and written (+16 B of ids); with the fused NV12 path the
     // source pixels depend on the scale and are not counted here (write side only, as in the oracle)
     const unsigned long long per_row = (P.layout == kLayoutNV12 ? 1ull : 2ull) * row_bytes + 16ull;
     cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_COMPACT],
-                       static_cast<unsigned long long>(P.n_slots) * (4ull * P.nw + 4ull) +
+                       static_cast<unsigned long long>(P.n_slots) * (4ull * P.nw * P.tp + 4ull) +
+                           (P.unit_mask ? static_cast<unsigned long long>(P.n_slots) * 4ull * P.nw : 0ull) +
                            static_cast<unsigned long long>(rows) * per_row);
   }
 }
@@ -143,18 +183,6 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
 
 // ---- fused preprocessing (NEXT-2): NV12 -> RGB (BT.601 limited) -> bilinear resize -> /255 -> normalise ------
 // Same fp32 operations in the same order as the oracle (oracle/codecsight_ref.c, codecsight_ref_model_pixel).
-__device__ __forceinline__ void nv12_rgb(const uint8_t* __restrict__ Y, const uint8_t* __restrict__ UV,
-                                         const CompactParams& P, int y, int x, float rgb[3]) {
-  const float c = static_cast<float>(static_cast<int>(__ldg(Y + (long long)y * P.y_pitch + x)) - 16);
-  const uint8_t* uv = UV + (long long)(y >> 1) * P.uv_pitch + 2 * (x >> 1);
-  const float d = static_cast<float>(static_cast<int>(__ldg(uv)) - 128);
-  const float e = static_cast<float>(static_cast<int>(__ldg(uv + 1)) - 128);
-  const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
-  rgb[0] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kRV, e)), 0.0f), 255.0f);
-  rgb[1] = fminf(fmaxf(__fsub_rn(__fsub_rn(__fmul_rn(kY, c), __fmul_rn(kGU, d)), __fmul_rn(kGV, e)), 0.0f), 255.0f);
-  rgb[2] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kBU, d)), 0.0f), 255.0f);
-}
-
 __device__ __forceinline__ void nv12_axis(int o, int src, float scale, int& i0, int& i1, float& l) {
   float f = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(o), 0.5f), scale), 0.5f);
   f = f < 0.0f ? 0.0f : f;
@@ -164,18 +192,54 @@ __device__ __forceinline__ void nv12_axis(int o, int src, float scale, int& i0, 
 }
 
 // Gather one kept group (gr, gc) of `frame` into the warp tile and write it to packed rows [n0, n0 + G^2).
-template <int TP, int TG, int LAYOUT>
+// TT = frames per token unit (temporal patch, NEXT-3); 0 = runtime P.tp.  With TT > 1 the packed row is
+// [3][TT][p][p] and tile element (patch q, c, f, y, x) sits at ((q*3 + c)*TT + f)*p*p + y*p + x.
+template <int TP, int TG, int LAYOUT, int TT>
 __device__ __forceinline__ void gather_group(const CompactParams& P, const uint16_t* __restrict__ frame,
                                              bool vec_in, int gr, int gc, long long n0, int slot, int t_index,
                                              uint16_t* tile, int lane) {
   const int p = TP > 0 ? TP : P.p;
   const int G = TG > 0 ? TG : P.G;
+  const int tp = TT > 0 ? TT : P.tp;
   const int gp = G * p;  // group edge in pixels
   const int pp = p * p;
   const long long FW = P.FW;
-  const uint16_t* src0 = frame + (long long)(gr * gp) * FW + (long long)gc * gp;
   const long long plane = (long long)P.FH * FW;
-  if (LAYOUT == CS_LAYOUT_GROUPED) {
+  if (LAYOUT == CS_LAYOUT_GROUPED && tp > 1) {
+    // the unit's frames hold the group as contiguous blocks [q][3][p][p]; interleave them per (q, c) into the
+    // tile in 8-B pieces (a p*p segment is 392 B = 49 x 8 B for 14-px patches; pp % 4 == 0 is checked by vec_in)
+    const int gs2 = G * G;
+    const long long blk_el = (long long)gs2 * 3 * pp;
+    const long long goff = ((long long)gr * P.ngc + gc) * blk_el;
+    for (int f = 0; f < tp; ++f) {
+      const uint16_t* blk = (f == 0 ? frame : static_cast<const uint16_t*>(P.frames[(long long)slot * tp + f])) + goff;
+      if (vec_in) {
+        const int n8 = static_cast<int>(blk_el / 4);
+        constexpr int kU = 4;
+        for (int e0 = 0; e0 < n8; e0 += 32 * kU) {
+          uint2 v[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int e = e0 + u * 32 + lane;
+            if (e < n8) v[u] = cs::ld_nc_v2(blk + 4 * e);
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int e = e0 + u * 32 + lane;
+            if (e < n8) {
+              const int el = 4 * e, seg = el / pp, r = el - seg * pp;
+              *reinterpret_cast<uint2*>(tile + (seg * tp + f) * pp + r) = v[u];
+            }
+          }
+        }
+      } else {
+        for (int el = lane; el < blk_el; el += 32) {
+          const int seg = el / pp, r = el - seg * pp;
+          tile[(seg * tp + f) * pp + r] = blk[el];
+        }
+      }
+    }
+  } else if (LAYOUT == CS_LAYOUT_GROUPED) {
     // the kept group is one contiguous block already in packed order: straight 16-B copy (no smem staging)
     const int gs2 = G * G;
     long long nvalid = P.capacity - n0;
@@ -218,7 +282,9 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     }
     return;
   }
-  if (LAYOUT == kLayoutNV12) {
+  if (LAYOUT == CS_LAYOUT_GROUPED) {
+    // tp > 1: the tile was filled above
+  } else if (LAYOUT == kLayoutNV12) {
     // preprocess only the kept group's 3 x gp x gp model pixels straight from the decoded NV12 frame
     const uint8_t* Yp = reinterpret_cast<const uint8_t*>(frame);
     const uint8_t* UVp = static_cast<const uint8_t*>(P.uv_planes[slot]);
@@ -279,6 +345,9 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
   } else if (vec_in) {
     // 8-byte loads: each group row segment is gp pixels = gp/4 pieces of 4 bf16.  Pairs of pixels never
     // straddle a patch boundary (p even), so the tile is written with 4-byte stores.
+   for (int f = 0; f < tp; ++f) {
+    const uint16_t* src0 = (f == 0 ? frame : static_cast<const uint16_t*>(P.frames[(long long)slot * tp + f])) +
+                           (long long)(gr * gp) * FW + (long long)gc * gp;
     const int cpr = gp / 4;
     const int total = 3 * gp * cpr;
     constexpr int kUnroll = (TP > 0) ? 10 : 4;  // 588 8-B pieces of a 2x2 group of 14-px patches: 2 rounds
@@ -304,26 +373,31 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
           for (int k = 0; k < 2; ++k) {
             const int x = piece * 4 + 2 * k;
             const int dx = x / p, xx = x - dx * p;
-            const int idx = ((dy * G + dx) * 3 + c) * pp + y * p + xx;
+            const int idx = (((dy * G + dx) * 3 + c) * tp + f) * pp + y * p + xx;
             *reinterpret_cast<uint32_t*>(tile + idx) = k == 0 ? v[u].x : v[u].y;
           }
         }
       }
     }
+   }
   } else {
-    const int total = 3 * gp * gp;
-    for (int e = lane; e < total; e += 32) {
-      const int row = e / gp, x = e - row * gp;
-      const int c = row / gp, yy = row - c * gp;
-      const int dy = yy / p, y = yy - dy * p, dx = x / p, xx = x - dx * p;
-      tile[((dy * G + dx) * 3 + c) * pp + y * p + xx] = src0[c * plane + (long long)yy * FW + x];
+    for (int f = 0; f < tp; ++f) {
+      const uint16_t* src0 = (f == 0 ? frame : static_cast<const uint16_t*>(P.frames[(long long)slot * tp + f])) +
+                             (long long)(gr * gp) * FW + (long long)gc * gp;
+      const int total = 3 * gp * gp;
+      for (int e = lane; e < total; e += 32) {
+        const int row = e / gp, x = e - row * gp;
+        const int c = row / gp, yy = row - c * gp;
+        const int dy = yy / p, y = yy - dy * p, dx = x / p, xx = x - dx * p;
+        tile[(((dy * G + dx) * 3 + c) * tp + f) * pp + y * p + xx] = src0[c * plane + (long long)yy * FW + x];
+      }
     }
   }
   __syncwarp();
   const int gs2 = G * G;
   long long nvalid = P.capacity - n0;
   nvalid = nvalid < 0 ? 0 : (nvalid > gs2 ? gs2 : nvalid);
-  const long long row_el = 3ll * pp;
+  const long long row_el = 3ll * tp * pp;
   uint16_t* dst = P.packed + n0 * row_el;
   if (P.vec_out) {
     const int nel = static_cast<int>(nvalid * row_el);
@@ -348,8 +422,8 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
   __syncwarp();  // tile reusable
 }
 
-template <int TP, int TG, int LAYOUT>
-__global__ void __launch_bounds__(kGatherThreads, LAYOUT == CS_LAYOUT_GROUPED ? 4 : 2)
+template <int TP, int TG, int LAYOUT, int TT>
+__global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED && TT == 1) ? 4 : 2)
     compact_gather(const __grid_constant__ CompactParams P) {
   extern __shared__ __align__(16) unsigned char g_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -361,7 +435,8 @@ __global__ void __launch_bounds__(kGatherThreads, LAYOUT == CS_LAYOUT_GROUPED ? 
   long long q = total_groups * wid / nwarps;
   const long long q1 = total_groups * (wid + 1) / nwarps;
   if (q >= q1) return;
-  const int tile_bytes = LAYOUT == CS_LAYOUT_GROUPED ? 0 : tile_bytes_of(TP > 0 ? TP : P.p, G);
+  const int tp = TT > 0 ? TT : P.tp;
+  const int tile_bytes = (LAYOUT == CS_LAYOUT_GROUPED && tp == 1) ? 0 : tile_bytes_of(TP > 0 ? TP : P.p, G, tp);
   uint16_t* tile = reinterpret_cast<uint16_t*>(g_smem + (size_t)wib * tile_bytes);
   uint32_t* mask = reinterpret_cast<uint32_t*>(g_smem + (size_t)kWarpsPerCta * tile_bytes) + wib * P.nw;
 
@@ -376,15 +451,17 @@ __global__ void __launch_bounds__(kGatherThreads, LAYOUT == CS_LAYOUT_GROUPED ? 
   long long skip = q - __ldg(P.frame_offsets + slot) / gs2;  // kept groups of the slot before q
 
   while (q < q1 && slot < P.n_slots) {
-    const uint32_t* m = slot_mask(P, slot);
-    for (int t = lane; t < P.nw; t += 32) mask[t] = __ldg(m + t);
-    const uint16_t* frame = static_cast<const uint16_t*>(P.frames[slot]);
+    for (int t = lane; t < P.nw; t += 32) mask[t] = tp == 1 ? __ldg(slot_mask(P, slot) + t) : unit_word(P, slot, t);
+    const uint16_t* frame = static_cast<const uint16_t*>(P.frames[(long long)slot * tp]);
     const int t_index = __ldg(P.frame_index + slot);
     const int pe = TP > 0 ? TP : P.p;
-    const bool vec_in = LAYOUT == CS_LAYOUT_GROUPED
-                            ? (((reinterpret_cast<uintptr_t>(frame) & 15u) == 0) && ((3 * G * G * pe * pe * 2) % 16 == 0))
-                            : (((reinterpret_cast<uintptr_t>(frame) & 7u) == 0) && ((P.FW & 3) == 0) &&
-                               (((G * pe) & 3) == 0) && ((pe & 1) == 0));
+    uintptr_t align_or = reinterpret_cast<uintptr_t>(frame);
+    for (int f = 1; f < tp; ++f) align_or |= reinterpret_cast<uintptr_t>(P.frames[(long long)slot * tp + f]);
+    const bool vec_in =
+        LAYOUT == CS_LAYOUT_GROUPED
+            ? (tp == 1 ? (((align_or & 15u) == 0) && ((3 * G * G * pe * pe * 2) % 16 == 0))
+                       : (((align_or & 7u) == 0) && ((pe * pe) % 4 == 0)))
+            : (((align_or & 7u) == 0) && ((P.FW & 3) == 0) && (((G * pe) & 3) == 0) && ((pe & 1) == 0));
     __syncwarp();
     for (int base = 0; base < P.ngroups && q < q1; base += 32) {
       const int qq = base + lane;
@@ -405,7 +482,7 @@ __global__ void __launch_bounds__(kGatherThreads, LAYOUT == CS_LAYOUT_GROUPED ? 
         const int gi = base + b;
         const int gr = gi / P.ngc, gc = gi - gr * P.ngc;
         const long long n0 = q * gs2;
-        if (n0 < P.capacity) gather_group<TP, TG, LAYOUT>(P, frame, vec_in, gr, gc, n0, slot, t_index, tile, lane);
+        if (n0 < P.capacity) gather_group<TP, TG, LAYOUT, TT>(P, frame, vec_in, gr, gc, n0, slot, t_index, tile, lane);
         ++q;
       }
     }
@@ -416,12 +493,12 @@ __global__ void __launch_bounds__(kGatherThreads, LAYOUT == CS_LAYOUT_GROUPED ? 
 
 }  // namespace
 
-static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t n_streams, int32_t n_frames,
-                          const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* frame_index,
-                          const void* const* frames, const void* const* uv_planes, int32_t frame_layout,
-                          int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
-                          int32_t* frame_offsets,
-                      unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp, int32_t n_streams,
+                          int32_t n_frames, const uint32_t* keep_mask, int64_t mask_frame_stride,
+                          const int32_t* frame_index, const void* const* frames, const void* const* uv_planes,
+                          int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                          int32_t* frame_offsets, uint32_t* unit_mask, int64_t unit_mask_stride,
+                          unsigned long long* counters, int32_t* status, cudaStream_t stream) {
   CompactParams P{};
   P.grid_w = g->grid_w;
   P.grid_h = g->grid_h;
@@ -434,11 +511,14 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t n_
   P.n_streams = n_streams;
   P.n_frames = n_frames;
   P.n_slots = n_streams * n_frames;
+  P.tp = tp;
+  P.unit_mask = unit_mask;
+  P.unit_mask_stride = unit_mask_stride;
   P.mask_frame_stride = mask_frame_stride;
   P.capacity = capacity;
   P.FH = g->grid_h * g->patch;
   P.FW = g->grid_w * g->patch;
-  const long long row_bytes = 3ll * g->patch * g->patch * 2ll;
+  const long long row_bytes = 3ll * tp * g->patch * g->patch * 2ll;
   // every group starts at row n0 = q * group^2, i.e. at byte n0 * row_bytes: 16-B aligned iff a whole group is
   // a multiple of 16 B (4,704 B for 2x2 groups of 14-px patches); a capacity-truncated group ends with a tail
   P.vec_out = ((reinterpret_cast<uintptr_t>(packed) & 15u) == 0 &&
@@ -472,25 +552,34 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t n_
   if (P.n_slots == 0 || capacity == 0) return CS_OK;
   const bool grouped = frame_layout == CS_LAYOUT_GROUPED;
   const bool nv12 = frame_layout == kLayoutNV12;
-  const size_t smem = (size_t)kWarpsPerCta * ((grouped ? 0 : tile_bytes_of(g->patch, g->group)) + 4 * P.nw);
-  const bool fast = g->patch == 14 && g->group == 2;
-  const int grid = cs_num_sms() * (grouped ? 8 : 4);
+  const size_t smem =
+      (size_t)kWarpsPerCta * (((grouped && tp == 1) ? 0 : tile_bytes_of(g->patch, g->group, tp)) + 4 * P.nw);
+  const bool fast = g->patch == 14 && g->group == 2 && (tp == 1 || tp == 2);
+  const int grid = cs_num_sms() * ((grouped && tp == 1) ? 8 : 4);
   const void* fn;
   int slot;
-#define CS_PICK(TP, TG, LY, SL) \
+#define CS_PICK(TP, TG, LY, TT, SL) \
   do {                                                                                   \
-    fn = reinterpret_cast<const void*>(compact_gather<TP, TG, LY>);                      \
+    fn = reinterpret_cast<const void*>(compact_gather<TP, TG, LY, TT>);                  \
     slot = SL;                                                                           \
   } while (0)
   if (nv12) {
-    if (fast) CS_PICK(14, 2, kLayoutNV12, 15); else CS_PICK(0, 0, kLayoutNV12, 16);
+    if (fast) CS_PICK(14, 2, kLayoutNV12, 1, 15); else CS_PICK(0, 0, kLayoutNV12, 1, 16);
   } else if (grouped) {
-    if (fast) CS_PICK(14, 2, 1, 12); else CS_PICK(0, 0, 1, 14);
+    if (fast) {
+      if (tp == 1) CS_PICK(14, 2, 1, 1, 12); else CS_PICK(14, 2, 1, 2, 17);
+    } else {
+      CS_PICK(0, 0, 1, 0, 14);
+    }
   } else {
-    if (fast) CS_PICK(14, 2, 0, 11); else CS_PICK(0, 0, 0, 13);
+    if (fast) {
+      if (tp == 1) CS_PICK(14, 2, 0, 1, 11); else CS_PICK(14, 2, 0, 2, 18);
+    } else {
+      CS_PICK(0, 0, 0, 0, 13);
+    }
   }
 #undef CS_PICK
-  if (cs_set_smem_attr(fn, slot, 96 * 1024)) return CS_ERR_CUDA;
+  if (cs_set_smem_attr(fn, slot, 227 * 1024)) return CS_ERR_CUDA;
   void* args[] = {&P};
   if (cudaLaunchKernel(fn, dim3(grid), dim3(kGatherThreads), args, smem, stream) != cudaSuccess) return CS_ERR_CUDA;
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
@@ -501,8 +590,19 @@ int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, con
                       int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
                       int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
                       int32_t* frame_offsets, unsigned long long* counters, int32_t* status, cudaStream_t stream) {
-  return launch_compact(g, nullptr, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, frames, nullptr,
-                        frame_layout, capacity, packed, pos_ids, src_index, frame_offsets, counters, status, stream);
+  return launch_compact(g, nullptr, 1, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, frames,
+                        nullptr, frame_layout, capacity, packed, pos_ids, src_index, frame_offsets, nullptr, 0,
+                        counters, status, stream);
+}
+
+int cs_launch_compact_tp(const cs_grid* g, int32_t tp, int32_t n_streams, int32_t n_units, const uint32_t* keep_mask,
+                         int64_t mask_frame_stride, const int32_t* unit_index, const void* const* frames,
+                         int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                         int32_t* frame_offsets, uint32_t* unit_mask, int64_t unit_mask_stride,
+                         unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+  return launch_compact(g, nullptr, tp, n_streams, n_units, keep_mask, mask_frame_stride, unit_index, frames,
+                        nullptr, frame_layout, capacity, packed, pos_ids, src_index, frame_offsets, unit_mask,
+                        unit_mask_stride, counters, status, stream);
 }
 
 int cs_launch_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n_streams, int32_t n_frames,
@@ -510,6 +610,7 @@ int cs_launch_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n_
                            const void* const* y_planes, const void* const* uv_planes, int64_t capacity,
                            void* packed, int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets,
                            unsigned long long* counters, int32_t* status, cudaStream_t stream) {
-  return launch_compact(g, pp, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, y_planes, uv_planes,
-                        kLayoutNV12, capacity, packed, pos_ids, src_index, frame_offsets, counters, status, stream);
+  return launch_compact(g, pp, 1, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, y_planes,
+                        uv_planes, kLayoutNV12, capacity, packed, pos_ids, src_index, frame_offsets, nullptr, 0,
+                        counters, status, stream);
 }

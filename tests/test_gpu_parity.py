@@ -255,6 +255,80 @@ def test_compact_generic_geometries(abi, ref, geom, layout):
 
 
 # ------------------------------------------------------------------------------------------------------------
+# compact_tp (NEXT-3 temporal patches)
+# ------------------------------------------------------------------------------------------------------------
+def run_compact_tp_both(abi, ref, g, tp, keep_mask, unit_index, frames, capacity, S, nu, mfs, layout=0,
+                        want_unit_mask=True):
+    nw = abi.grid_words(g)
+    p = g["patch"]
+    if layout == 1:
+        frames = [to_grouped(f, g) for f in frames]
+    km_d = torch.from_numpy(np.ascontiguousarray(keep_mask).view(np.int32)).to(DEV)
+    fr_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in frames]
+    fptr = abi.ptr_array(fr_d, DEV) if fr_d else torch.zeros(1, dtype=torch.int64, device=DEV)
+    ui_d = torch.from_numpy(np.ascontiguousarray(unit_index, dtype=np.int32)).to(DEV)
+    cap = max(capacity, 1)
+    packed = torch.full((cap, 3 * tp * p * p), -1, dtype=torch.int16, device=DEV)
+    pos = torch.full((cap, 3), -7, dtype=torch.int32, device=DEV)
+    src = torch.full((cap,), -7, dtype=torch.int32, device=DEV)
+    offs = torch.zeros(S * nu + 1, dtype=torch.int32, device=DEV)
+    um = torch.full((max(S, 1), nu, nw), -1, dtype=torch.int32, device=DEV) if want_unit_mask else None
+    cnt_d = torch.zeros(16, dtype=torch.int64, device=DEV)
+    st_d = torch.zeros(1, dtype=torch.int32, device=DEV)
+    abi.codecsight_compact_tp(g, tp, S, nu, km_d, mfs, ui_d, fptr, capacity, packed, pos, src, offs, cnt_d, st_d,
+                              frame_layout=layout, unit_mask=um, unit_mask_stride=nu)
+    o = ref.compact_tp(g, tp, keep_mask, unit_index, frames, capacity, S, nu, mask_frame_stride=mfs,
+                       frame_layout=layout, want_unit_mask=want_unit_mask)
+    torch.cuda.synchronize()
+    rows = min(int(o["frame_offsets"][-1]), capacity)
+    assert int(st_d.item()) == o["status"]
+    assert (offs.cpu().numpy() == o["frame_offsets"]).all()
+    assert (packed.cpu().numpy().view(np.uint16)[:rows] == o["packed"][:rows]).all()
+    assert (pos.cpu().numpy()[:rows] == o["pos_ids"][:rows]).all()
+    assert (src.cpu().numpy()[:rows] == o["src_index"][:rows]).all()
+    assert (cnt_d.cpu().numpy().view(np.uint64) == o["counters"]).all()
+    if want_unit_mask and S > 0:
+        assert (um.cpu().numpy().view(np.uint32) == o["unit_mask"]).all()
+    if rows < cap:
+        assert (src.cpu().numpy()[rows:] == -7).all()
+    return o
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("cfg_name,S,nu", [("C1", 2, 4), ("C4", 8, 2)])
+def test_compact_tp2_configs(abi, ref, cfg_name, S, nu, layout):
+    cfg = synth.CONFIGS[cfg_name]
+    g = make_grid(*cfg["src"])
+    km = scored_masks(ref, g, cfg, S, 2 * nu, first=1)
+    rng = np.random.default_rng(12)
+    frames = synth.random_frames(S * 2 * nu, 448, 448, rng)
+    ui = np.tile(np.arange(50, 50 + nu, dtype=np.int32), S)
+    o = run_compact_tp_both(abi, ref, g, 2, km, ui, frames, S * nu * 1024, S, nu, 2 * nu, layout)
+    total = int(o["frame_offsets"][-1])
+    run_compact_tp_both(abi, ref, g, 2, km, ui, frames, total // 2 + 1, S, nu, 2 * nu, layout)
+    run_compact_tp_both(abi, ref, g, 2, km, ui, frames, 0, S, nu, 2 * nu, layout, want_unit_mask=False)
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("tp", [1, 2, 3])
+@pytest.mark.parametrize("geom", [(64, 48, 16, 8, 6, 2, 4), (30, 30, 8, 6, 6, 3, 6), (56, 56, 16, 4, 4, 1, 14),
+                                  (72, 40, 8, 12, 10, 2, 3)])
+def test_compact_tp_generic(abi, ref, geom, tp, layout):
+    sw, sh, m, gw, gh, G, p = geom
+    g = make_grid(sw, sh, mb_size=m, grid_w=gw, grid_h=gh, group=G, patch=p)
+    rng = np.random.default_rng(15 + tp)
+    S, nu = 2, 2
+    nw = abi.grid_words(g)
+    mfs = nu * tp + 1
+    km = rng.integers(0, 2**32, size=(S, mfs, nw), dtype=np.uint64).astype(np.uint32)
+    km &= rng.integers(0, 2**32, size=(S, mfs, nw), dtype=np.uint64).astype(np.uint32)
+    km &= rng.integers(0, 2**32, size=(S, mfs, nw), dtype=np.uint64).astype(np.uint32)
+    frames = [rng.integers(0, 65536, size=(3, gh * p, gw * p), dtype=np.uint16) for _ in range(S * nu * tp)]
+    ui = np.arange(S * nu, dtype=np.int32)
+    run_compact_tp_both(abi, ref, g, tp, km, ui, frames, S * nu * gw * gh, S, nu, mfs, layout)
+
+
+# ------------------------------------------------------------------------------------------------------------
 # kv_refresh
 # ------------------------------------------------------------------------------------------------------------
 def _host_cache(t):
