@@ -199,18 +199,22 @@ int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, co
  *   pos_ids[n] = (unit_index[slot], h, w); src_index[n] = slot*grid_h*grid_w + h*grid_w + w; slot = sigma*n_units+u
  *   unit_mask  optional device [n_streams][unit_mask_stride][grid_words] u32 out: OR of the unit's frame masks
  *              (the per-unit mask a token-unit KV ring is built from); NULL = not written
+ *   frame_type, unit_type  optional together: frame_type device [n_streams][mask_frame_stride] u8 (the frame type
+ *              ring), unit_type device [n_streams][unit_mask_stride] u8 out = CS_FRAME_P iff every frame of the
+ *              unit is a P-frame, else CS_FRAME_I (a unit holding an I-frame is an anchor of the KV refresh)
  * Order, offsets, capacity and status as codecsight_compact (rows of 3*tp*patch^2 bf16); temporal_patch = 1 is
  * codecsight_compact.  A clip whose length is not a multiple of tp repeats its last frame (pass the same pointer
  * and mask twice), as the Hugging Face processor does.  Limits: 1 <= temporal_patch <= 4; 8 tiles of
  * 3*tp*(group*patch)^2 bf16 fit 227 KB of shared memory (else CS_ERR_UNSUPPORTED).
- *   counters: BYTES_COMPACT (+ 4*tp*grid_words+4 per unit, + 4*grid_words per unit mask written), PACKED_ROWS
+ *   counters: BYTES_COMPACT (+ 4*tp*grid_words+4 per unit, + 4*grid_words per unit mask and tp+1 per unit type
+ *             written), PACKED_ROWS
  * --------------------------------------------------------------------------------------------------------- */
 int codecsight_compact_tp(const cs_grid* g, int32_t temporal_patch, int32_t n_streams, int32_t n_units,
                           const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* unit_index,
                           const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
                           int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, uint32_t* unit_mask,
-                          int64_t unit_mask_stride, unsigned long long* counters, int32_t* status,
-                          cudaStream_t stream);
+                          int64_t unit_mask_stride, const uint8_t* frame_type, uint8_t* unit_type,
+                          unsigned long long* counters, int32_t* status, cudaStream_t stream);
 
 /* ------------------------------------------------------------------------------------------------------------
  * codecsight_compact_nv12 — NEXT-2: the GPU preprocessing fused into the compaction ("Resizing, color-space

@@ -275,12 +275,14 @@ int codecsight_ref_compact_tp(const ref_grid* g, int32_t tp, int32_t n_streams, 
                               const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* unit_index,
                               const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
                               int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, uint32_t* unit_mask,
-                              int64_t unit_mask_stride, unsigned long long* counters, int32_t* status) {
+                              int64_t unit_mask_stride, const uint8_t* frame_type, uint8_t* unit_type,
+                              unsigned long long* counters, int32_t* status) {
   int rc = ref_grid_ok(g);
   if (rc) return rc;
   if (tp < 1 || tp > 4) return -3;
   if (n_streams < 0 || n_units < 1 || mask_frame_stride < (int64_t)n_units * tp || capacity < 0) return -1;
-  if (unit_mask && unit_mask_stride < n_units) return -1;
+  if ((unit_mask || unit_type) && unit_mask_stride < n_units) return -1;
+  if ((frame_type == 0) != (unit_type == 0)) return -1;
   if (frame_layout != REF_LAYOUT_PLANAR && frame_layout != REF_LAYOUT_GROUPED) return -1;
   const int64_t np = (int64_t)g->grid_w * g->grid_h, nw = ref_words(g), G = g->group, p = g->patch;
   const int64_t n_slots = (int64_t)n_streams * n_units;
@@ -303,6 +305,12 @@ int codecsight_ref_compact_tp(const ref_grid* g, int32_t tp, int32_t n_streams, 
           for (int64_t f = 0; f < tp; ++f) w |= keep_mask[(s * mask_frame_stride + u * tp + f) * nw + t];
           unit_mask[(s * unit_mask_stride + u) * nw + t] = w;
         }
+      if (unit_type) { /* a unit holding an I-frame (or an unknown type, read as I) is an I unit */
+        uint8_t ty = REF_FRAME_P;
+        for (int64_t f = 0; f < tp; ++f)
+          if (frame_type[s * mask_frame_stride + u * tp + f] != REF_FRAME_P) ty = REF_FRAME_I;
+        unit_type[s * unit_mask_stride + u] = ty;
+      }
       for (int64_t gr = 0; gr < g->grid_h / G; ++gr)
         for (int64_t gc = 0; gc < g->grid_w / G; ++gc) {
           int any = 0;
@@ -340,7 +348,8 @@ int codecsight_ref_compact_tp(const ref_grid* g, int32_t tp, int32_t n_streams, 
   frame_offsets[n_slots] = (int32_t)off;
   counters[REF_C_PACKED_ROWS] += (unsigned long long)written;
   counters[REF_C_BYTES_COMPACT] += (unsigned long long)(n_slots * (4 * nw * tp + 4) + written * (2 * row * 2 + 16) +
-                                                        (unit_mask ? n_slots * 4 * nw : 0));
+                                                        (unit_mask ? n_slots * 4 * nw : 0) +
+                                                        (unit_type ? n_slots * (tp + 1) : 0));
   return 0;
 }
 

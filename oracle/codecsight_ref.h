@@ -124,12 +124,14 @@ int codecsight_ref_compact_nv12(const ref_grid* g, const ref_pre* pp, int32_t n_
                                 unsigned long long* counters, int32_t* status);
 
 /* NEXT-3: temporal patches (Qwen2-VL temporal_patch_size): a token unit = tp consecutive frames, row [3][tp][p][p];
- * a group is emitted iff any of its patches is kept in any frame of the unit; unit masks (OR) optionally written. */
+ * a group is emitted iff any of its patches is kept in any frame of the unit; unit masks (OR) optionally written,
+ * and unit types (I iff any frame of the unit is not a P-frame) when frame_type and unit_type are given. */
 int codecsight_ref_compact_tp(const ref_grid* g, int32_t tp, int32_t n_streams, int32_t n_units,
                               const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* unit_index,
                               const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
                               int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, uint32_t* unit_mask,
-                              int64_t unit_mask_stride, unsigned long long* counters, int32_t* status);
+                              int64_t unit_mask_stride, const uint8_t* frame_type, uint8_t* unit_type,
+                              unsigned long long* counters, int32_t* status);
 
 /* NEXT-4: FFmpeg AVMotionVector records -> MB grid; similar-patch-ratio histogram. */
 typedef struct {

@@ -88,7 +88,7 @@ def lib():
                                              C.c_int32, C.c_int64, P, P, P, P, P, P]
         L.codecsight_ref_compact_tp.restype = C.c_int
         L.codecsight_ref_compact_tp.argtypes = [C.POINTER(RefGrid), C.c_int32, C.c_int32, C.c_int32, P, C.c_int64, P,
-                                                P, C.c_int32, C.c_int64, P, P, P, P, P, C.c_int64, P, P]
+                                                P, C.c_int32, C.c_int64, P, P, P, P, P, C.c_int64, P, P, P, P]
         L.codecsight_ref_kv_refresh.restype = C.c_int
         L.codecsight_ref_kv_refresh.argtypes = [C.POINTER(RefGrid), C.POINTER(RefKv), C.POINTER(RefWindow),
                                                 C.c_int32, P, P, P, P, P, C.c_int64, P, P, P, P, P]
@@ -201,8 +201,9 @@ def compact(g: dict, keep_mask: np.ndarray, frame_index: np.ndarray, frames: lis
 
 def compact_tp(g: dict, tp: int, keep_mask: np.ndarray, unit_index: np.ndarray, frames: list, capacity: int,
                n_streams: int, n_units: int, mask_frame_stride: int | None = None, frame_layout: int = 0,
-               want_unit_mask: bool = False, counters: np.ndarray | None = None):
-    """NEXT-3 temporal patches: keep_mask [S][mask_frame_stride][words] (per frame); frames: n_slots*tp arrays."""
+               want_unit_mask: bool = False, counters: np.ndarray | None = None, frame_type: np.ndarray | None = None):
+    """NEXT-3 temporal patches: keep_mask [S][mask_frame_stride][words] (per frame); frames: n_slots*tp arrays;
+    frame_type [S][mask_frame_stride] (optional) -> unit_type [S][n_units]."""
     nw = grid_words(g)
     mfs = n_units * tp if mask_frame_stride is None else mask_frame_stride
     keep_mask = np.ascontiguousarray(keep_mask, dtype=np.uint32).reshape(n_streams, mfs, nw)
@@ -217,13 +218,15 @@ def compact_tp(g: dict, tp: int, keep_mask: np.ndarray, unit_index: np.ndarray, 
     src = np.zeros(max(capacity, 0), np.int32)
     offs = np.zeros(n_slots + 1, np.int32)
     um = np.zeros((n_streams, n_units, nw), np.uint32) if want_unit_mask else None
+    ft = None if frame_type is None else np.ascontiguousarray(frame_type, dtype=np.uint8).reshape(n_streams, mfs)
+    ut = None if frame_type is None else np.zeros((n_streams, n_units), np.uint8)
     counters = np.zeros(NCOUNTERS, np.uint64) if counters is None else counters
     status = np.zeros(1, np.int32)
     rc = lib().codecsight_ref_compact_tp(C.byref(make_grid(g)), tp, n_streams, n_units, _p(keep_mask), mfs,
                                          _p(unit_index), C.cast(ptrs, C.c_void_p), frame_layout, capacity,
                                          _p(packed), _p(pos), _p(src), _p(offs), _p(um) if um is not None else None,
-                                         n_units, _p(counters), _p(status))
-    return dict(rc=rc, packed=packed, pos_ids=pos, src_index=src, frame_offsets=offs, unit_mask=um,
+                                         n_units, _p(ft), _p(ut), _p(counters), _p(status))
+    return dict(rc=rc, packed=packed, pos_ids=pos, src_index=src, frame_offsets=offs, unit_mask=um, unit_type=ut,
                 counters=counters, status=int(status[0]))
 
 

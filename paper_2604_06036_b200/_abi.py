@@ -88,7 +88,7 @@ def lib():
                                               I64, P, P, P, P, P, P, P]
         L.codecsight_compact_tp.restype = C.c_int
         L.codecsight_compact_tp.argtypes = [C.POINTER(CsGrid), I32, I32, I32, P, I64, P, P, I32, I64, P, P, P, P, P,
-                                            I64, P, P, P]
+                                            I64, P, P, P, P, P]
         L.codecsight_mv_rasterize.restype = C.c_int
         L.codecsight_mv_rasterize.argtypes = [C.POINTER(CsGrid), I32, P, P, P, P]
         L.codecsight_similar_hist.restype = C.c_int
@@ -195,11 +195,12 @@ def codecsight_compact_nv12(g: dict, pre: dict, n_streams: int, n_frames: int, k
 def codecsight_compact_tp(g: dict, temporal_patch: int, n_streams: int, n_units: int, keep_mask,
                           mask_frame_stride: int, unit_index, frames, capacity: int, packed, pos_ids, src_index,
                           frame_offsets, counters, status, frame_layout: int = CS_LAYOUT_PLANAR, unit_mask=None,
-                          unit_mask_stride: int = 0, stream=None) -> None:
+                          unit_mask_stride: int = 0, frame_type=None, unit_type=None, stream=None) -> None:
     rc = lib().codecsight_compact_tp(C.byref(make_grid(g)), temporal_patch, n_streams, n_units, _ptr(keep_mask),
                                      mask_frame_stride, _ptr(unit_index), _ptr(frames), frame_layout, capacity,
                                      _ptr(packed), _ptr(pos_ids), _ptr(src_index), _ptr(frame_offsets),
-                                     _ptr(unit_mask), unit_mask_stride, _ptr(counters), _ptr(status),
+                                     _ptr(unit_mask), unit_mask_stride, _ptr(frame_type), _ptr(unit_type),
+                                     _ptr(counters), _ptr(status),
                                      _stream(stream))
     _check(rc, "codecsight_compact_tp")
 

@@ -125,14 +125,15 @@ int codecsight_compact_tp(const cs_grid* g, int32_t temporal_patch, int32_t n_st
                           const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* unit_index,
                           const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
                           int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, uint32_t* unit_mask,
-                          int64_t unit_mask_stride, unsigned long long* counters, int32_t* status,
-                          cudaStream_t stream) {
+                          int64_t unit_mask_stride, const uint8_t* frame_type, uint8_t* unit_type,
+                          unsigned long long* counters, int32_t* status, cudaStream_t stream) {
   int rc = grid_ok(g);
   if (rc) return rc;
   if (temporal_patch < 1 || temporal_patch > 4) return CS_ERR_UNSUPPORTED;
   if (n_streams < 0 || n_units < 1 || capacity < 0) return CS_ERR_INVALID_ARGUMENT;
   if (mask_frame_stride < static_cast<long long>(n_units) * temporal_patch) return CS_ERR_INVALID_ARGUMENT;
-  if (unit_mask && unit_mask_stride < n_units) return CS_ERR_INVALID_ARGUMENT;
+  if ((unit_mask || unit_type) && unit_mask_stride < n_units) return CS_ERR_INVALID_ARGUMENT;
+  if ((frame_type == nullptr) != (unit_type == nullptr)) return CS_ERR_INVALID_ARGUMENT;
   if (frame_layout != CS_LAYOUT_PLANAR && frame_layout != CS_LAYOUT_GROUPED) return CS_ERR_INVALID_ARGUMENT;
   const long long n_slots = static_cast<long long>(n_streams) * n_units;
   if (n_slots * g->grid_w * g->grid_h >= 2147483648LL) return CS_ERR_UNSUPPORTED;
@@ -146,7 +147,7 @@ int codecsight_compact_tp(const cs_grid* g, int32_t temporal_patch, int32_t n_st
   if ((rc = device_ok())) return rc;
   return cs_launch_compact_tp(g, temporal_patch, n_streams, n_units, keep_mask, mask_frame_stride, unit_index, frames,
                               frame_layout, capacity, packed, pos_ids, src_index, frame_offsets, unit_mask,
-                              unit_mask_stride, counters, status, stream);
+                              unit_mask_stride, frame_type, unit_type, counters, status, stream);
 }
 
 int codecsight_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,

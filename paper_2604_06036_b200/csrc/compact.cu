@@ -34,6 +34,8 @@ struct CompactParams {
   long long mask_frame_stride;
   uint32_t* unit_mask;                // optional [n_streams][unit_mask_stride][nw] OR of the unit's masks
   long long unit_mask_stride;
+  const uint8_t* frame_type;          // optional [n_streams][mask_frame_stride] -> unit_type
+  uint8_t* unit_type;                 // optional [n_streams][unit_mask_stride]: I iff any frame is not P
   long long capacity;
   int FH, FW;  // model-input frame height / width in pixels
   int vec_out;
@@ -138,6 +140,14 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
     __syncthreads();
     const int slot = base + tid;
     const int cnt = s_cnt[tid];
+    if (P.unit_type && slot < P.n_slots) {
+      const int s = slot / P.n_frames, j = slot - s * P.n_frames;
+      const uint8_t* ft = P.frame_type + (long long)s * P.mask_frame_stride + (long long)j * P.tp;
+      uint8_t ty = CS_FRAME_P;
+      for (int f = 0; f < P.tp; ++f)
+        if (ft[f] != CS_FRAME_P) ty = CS_FRAME_I;
+      P.unit_type[(long long)s * P.unit_mask_stride + j] = ty;
+    }
     int inc = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -176,6 +186,7 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
     cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_COMPACT],
                        static_cast<unsigned long long>(P.n_slots) * (4ull * P.nw * P.tp + 4ull) +
                            (P.unit_mask ? static_cast<unsigned long long>(P.n_slots) * 4ull * P.nw : 0ull) +
+                           (P.unit_type ? static_cast<unsigned long long>(P.n_slots) * (P.tp + 1ull) : 0ull) +
                            static_cast<unsigned long long>(rows) * per_row);
   }
 }
@@ -498,7 +509,8 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
                           const int32_t* frame_index, const void* const* frames, const void* const* uv_planes,
                           int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
                           int32_t* frame_offsets, uint32_t* unit_mask, int64_t unit_mask_stride,
-                          unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+                          const uint8_t* frame_type, uint8_t* unit_type, unsigned long long* counters,
+                          int32_t* status, cudaStream_t stream) {
   CompactParams P{};
   P.grid_w = g->grid_w;
   P.grid_h = g->grid_h;
@@ -514,6 +526,8 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
   P.tp = tp;
   P.unit_mask = unit_mask;
   P.unit_mask_stride = unit_mask_stride;
+  P.frame_type = frame_type;
+  P.unit_type = unit_type;
   P.mask_frame_stride = mask_frame_stride;
   P.capacity = capacity;
   P.FH = g->grid_h * g->patch;
@@ -592,17 +606,18 @@ int cs_launch_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, con
                       int32_t* frame_offsets, unsigned long long* counters, int32_t* status, cudaStream_t stream) {
   return launch_compact(g, nullptr, 1, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, frames,
                         nullptr, frame_layout, capacity, packed, pos_ids, src_index, frame_offsets, nullptr, 0,
-                        counters, status, stream);
+                        nullptr, nullptr, counters, status, stream);
 }
 
 int cs_launch_compact_tp(const cs_grid* g, int32_t tp, int32_t n_streams, int32_t n_units, const uint32_t* keep_mask,
                          int64_t mask_frame_stride, const int32_t* unit_index, const void* const* frames,
                          int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
                          int32_t* frame_offsets, uint32_t* unit_mask, int64_t unit_mask_stride,
-                         unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+                         const uint8_t* frame_type, uint8_t* unit_type, unsigned long long* counters,
+                         int32_t* status, cudaStream_t stream) {
   return launch_compact(g, nullptr, tp, n_streams, n_units, keep_mask, mask_frame_stride, unit_index, frames,
                         nullptr, frame_layout, capacity, packed, pos_ids, src_index, frame_offsets, unit_mask,
-                        unit_mask_stride, counters, status, stream);
+                        unit_mask_stride, frame_type, unit_type, counters, status, stream);
 }
 
 int cs_launch_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n_streams, int32_t n_frames,
@@ -612,5 +627,5 @@ int cs_launch_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n_
                            unsigned long long* counters, int32_t* status, cudaStream_t stream) {
   return launch_compact(g, pp, 1, n_streams, n_frames, keep_mask, mask_frame_stride, frame_index, y_planes,
                         uv_planes, kLayoutNV12, capacity, packed, pos_ids, src_index, frame_offsets, nullptr, 0,
-                        counters, status, stream);
+                        nullptr, nullptr, counters, status, stream);
 }

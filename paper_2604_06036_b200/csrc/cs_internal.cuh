@@ -160,7 +160,8 @@ int cs_launch_compact_tp(const cs_grid* g, int32_t tp, int32_t n_streams, int32_
                          int64_t mask_frame_stride, const int32_t* unit_index, const void* const* frames,
                          int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
                          int32_t* frame_offsets, uint32_t* unit_mask, int64_t unit_mask_stride,
-                         unsigned long long* counters, int32_t* status, cudaStream_t stream);
+                         const uint8_t* frame_type, uint8_t* unit_type, unsigned long long* counters,
+                         int32_t* status, cudaStream_t stream);
 int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window* win, int32_t n_streams,
                          const uint32_t* keep_mask_ring, const uint8_t* frame_type_ring,
                          const void* const* old_cache, void* const* new_cache, const void* const* refreshed,

@@ -27,8 +27,17 @@ class Pipeline:
     def __init__(self, grid: dict, n_streams: int, window: int, stride: int, gop: int, kv: dict | None,
                  n_prompt: int = 0, device=None, want_score: bool = False, packed_capacity: int | None = None,
                  with_refreshed: bool = True, frame_layout: int = abi.CS_LAYOUT_PLANAR, kv_mode: str = "copy",
-                 compact_chunk: int | None = None, preprocess: dict | None = None, overlap: bool = False):
+                 compact_chunk: int | None = None, preprocess: dict | None = None, overlap: bool = False,
+                 temporal_patch: int = 1):
         self.g = dict(grid)
+        # temporal patches (NEXT-3, Qwen2-VL temporal_patch_size): a token unit = tp consecutive frames; scoring stays
+        # per frame, compaction emits [3][tp][p][p] rows per unit (codecsight_compact_tp) and writes the unit masks /
+        # types into a unit ring, and the KV refresh runs over units (window w/tp, stride s/tp)
+        self.tp = tp = temporal_patch
+        if tp > 1:
+            assert window % tp == 0 and stride % tp == 0, "window and stride must be multiples of temporal_patch"
+            assert preprocess is None and not overlap, "temporal patches: planar/grouped frames, no overlap mode"
+            assert compact_chunk is None or compact_chunk % tp == 0
         self.frame_layout = frame_layout
         self.kv_mode = kv_mode
         # preprocess set: frames are decoded NV12 (frame_ptrs = (y_ptrs, uv_ptrs)) and compaction runs the fused
@@ -60,20 +69,29 @@ class Pipeline:
         # packed ViT input: enough rows for the first window (every patch kept)
         p = grid["patch"]
         chunk = compact_chunk if compact_chunk is not None else window
-        self.capacity = packed_capacity if packed_capacity is not None else S * chunk * self.np
-        self._packed = [torch.empty(self.capacity, 3 * p * p, dtype=torch.bfloat16, device=d) for _ in range(nb)]
+        self.capacity = packed_capacity if packed_capacity is not None else S * (chunk // tp) * self.np
+        self._packed = [torch.empty(self.capacity, 3 * tp * p * p, dtype=torch.bfloat16, device=d)
+                        for _ in range(nb)]
         self._pos_ids = [torch.empty(self.capacity, 3, dtype=torch.int32, device=d) for _ in range(nb)]
         self._src_index = [torch.empty(self.capacity, dtype=torch.int32, device=d) for _ in range(nb)]
-        self._frame_offsets = [torch.zeros(S * window + 1, dtype=torch.int32, device=d) for _ in range(nb)]
+        self._frame_offsets = [torch.zeros(S * (window // tp) + 1, dtype=torch.int32, device=d) for _ in range(nb)]
         self.packed, self.pos_ids = self._packed[0], self._pos_ids[0]
         self.src_index, self.frame_offsets = self._src_index[0], self._frame_offsets[0]
         self.frame_index = torch.zeros(S * window, dtype=torch.int32, device=d)
+        # KV token units: frames (tp = 1) or frame tuples with their own mask / type ring
+        self.wu, self.su, self.uring = window // tp, stride // tp, ring // tp
+        if tp > 1:
+            self.unit_ring = torch.zeros(S, self.uring, nw, dtype=torch.int32, device=d)
+            self.unit_type_ring = torch.zeros(S, self.uring, dtype=torch.uint8, device=d)
+        else:
+            self.unit_ring, self.unit_type_ring = self.mask_ring, self.type_ring
         self.kv = None
         if kv is not None:
             self.n_prompt = n_prompt
-            cap = window * self.groups + n_prompt
-            anchors = 1 + math.ceil(max(0, window - stride) / max(1, gop))
-            rcap = (stride + anchors) * self.groups + n_prompt
+            wu, su = self.wu, self.su
+            cap = wu * self.groups + n_prompt
+            anchors = 1 + math.ceil(max(0, wu - su) / max(1, gop // tp))
+            rcap = (su + anchors) * self.groups + n_prompt
             self.kv = dict(kv, capacity=cap, refresh_capacity=rcap, n_prompt=n_prompt)
             dt = torch.bfloat16 if kv["dtype"] == abi.CS_BF16 else torch.float32
             shape = (kv["layers"], 2, cap, kv["kv_heads"], kv["head_dim"])
@@ -90,7 +108,7 @@ class Pipeline:
             self._p_old = [torch.zeros(S, cap, dtype=torch.int32, device=d) for _ in range(nb)]
             self._n_tokens = [torch.zeros(S, 4, dtype=torch.int32, device=d) for _ in range(nb)]
             self.disposition, self.p_old, self.n_tokens = self._disposition[0], self._p_old[0], self._n_tokens[0]
-            win1 = dict(window=window, stride=stride, step=1, ring_frames=ring)
+            win1 = dict(window=self.wu, stride=self.su, step=1, ring_frames=self.uring)
             nbytes = (abi.kv_paged_workspace_size(grid, self.kv, win1, S) if kv_mode == "paged"
                       else abi.kv_workspace_size(self.kv, win1, S))
             self.workspace = torch.empty((nbytes + 15) // 16 * 16, dtype=torch.uint8, device=d)
@@ -186,7 +204,8 @@ class Pipeline:
         """codecsight_compact of the step's n new frames, in chunks of compact_chunk frames when set (the packed
         buffer then holds one chunk at a time, as a streaming ViT would consume it)."""
         g = self.g
-        fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
+        # frame_index: [S * n] stream-local frame indices, or [S * n / tp] unit indices with temporal patches
+        fi = self.frame_index[: self.S * n // self.tp] if frame_index is None else frame_index
         c = n if self.compact_chunk is None else min(n, self.compact_chunk)
         for j0 in range(0, n, c):
             nj = min(c, n - j0)
@@ -195,8 +214,17 @@ class Pipeline:
                 fptrs, fidx = ptrs, fi
             else:  # frames / indices of the chunk: per stream the slots j0..j0+nj-1 of [S][n]
                 fptrs = tuple(p.view(self.S, n)[:, j0:j0 + nj].contiguous().view(-1) for p in ptrs)
-                fidx = fi.view(self.S, n)[:, j0:j0 + nj].contiguous().view(-1)
-            if self.preprocess is not None:
+                tp = self.tp
+                fidx = fi.view(self.S, n // tp)[:, j0 // tp:(j0 + nj) // tp].contiguous().view(-1)
+            if self.tp > 1:
+                tp, uoff = self.tp, (off + j0) // self.tp
+                abi.codecsight_compact_tp(g, tp, self.S, nj // tp, self.mask_ring[:, off + j0:], self.ring, fidx,
+                                          fptrs[0], self.capacity, self.packed, self.pos_ids, self.src_index,
+                                          self.frame_offsets[: self.S * (nj // tp) + 1], self.counters, self.status,
+                                          frame_layout=self.frame_layout, unit_mask=self.unit_ring[:, uoff:],
+                                          unit_mask_stride=self.uring, frame_type=self.type_ring[:, off + j0:],
+                                          unit_type=self.unit_type_ring[:, uoff:], stream=stream)
+            elif self.preprocess is not None:
                 abi.codecsight_compact_nv12(g, self.preprocess, self.S, nj, self.mask_ring[:, off + j0:], self.ring,
                                             fidx, fptrs[0], fptrs[1], self.capacity, self.packed, self.pos_ids,
                                             self.src_index, self.frame_offsets[: self.S * nj + 1], self.counters,
@@ -209,18 +237,18 @@ class Pipeline:
 
     def kv_refresh(self, k, use_refreshed=None, stream=None):
         g = self.g
-        win = dict(window=self.w, stride=self.s, step=k, ring_frames=self.ring)
+        win = dict(window=self.wu, stride=self.su, step=k, ring_frames=self.uring)
         use_r = (k >= 1) if use_refreshed is None else use_refreshed
         ref = self.refreshed_ptrs if use_r else None
         if self.kv_mode == "paged":
             so, sn = self.slots[self.cur], self.slots[1 - self.cur]
-            abi.codecsight_kv_refresh_paged(g, self.kv, win, self.S, self.mask_ring, self.type_ring,
+            abi.codecsight_kv_refresh_paged(g, self.kv, win, self.S, self.unit_ring, self.unit_type_ring,
                                             self.cache_ptrs[0], so if k >= 1 else None, sn, self.token_cap, ref,
                                             self.token_cap, self.disposition, self.p_old, self.n_tokens,
                                             self.workspace, self.counters, self.status, stream)
         else:
             old, new = self.cache_ptrs[self.cur], self.cache_ptrs[1 - self.cur]
-            abi.codecsight_kv_refresh(g, self.kv, win, self.S, self.mask_ring, self.type_ring, old, new, ref,
+            abi.codecsight_kv_refresh(g, self.kv, win, self.S, self.unit_ring, self.unit_type_ring, old, new, ref,
                                       self.token_cap, self.disposition, self.p_old, self.n_tokens, self.workspace,
                                       self.counters, self.status, stream)
         self.cur = 1 - self.cur

@@ -273,12 +273,15 @@ def run_compact_tp_both(abi, ref, g, tp, keep_mask, unit_index, frames, capacity
     src = torch.full((cap,), -7, dtype=torch.int32, device=DEV)
     offs = torch.zeros(S * nu + 1, dtype=torch.int32, device=DEV)
     um = torch.full((max(S, 1), nu, nw), -1, dtype=torch.int32, device=DEV) if want_unit_mask else None
+    ft = np.random.default_rng(S + nu).integers(0, 3, size=(S, mfs)).astype(np.uint8) if want_unit_mask else None
+    ft_d = torch.from_numpy(ft).to(DEV) if ft is not None else None
+    ut = torch.full((max(S, 1), nu), 9, dtype=torch.uint8, device=DEV) if want_unit_mask else None
     cnt_d = torch.zeros(16, dtype=torch.int64, device=DEV)
     st_d = torch.zeros(1, dtype=torch.int32, device=DEV)
     abi.codecsight_compact_tp(g, tp, S, nu, km_d, mfs, ui_d, fptr, capacity, packed, pos, src, offs, cnt_d, st_d,
-                              frame_layout=layout, unit_mask=um, unit_mask_stride=nu)
+                              frame_layout=layout, unit_mask=um, unit_mask_stride=nu, frame_type=ft_d, unit_type=ut)
     o = ref.compact_tp(g, tp, keep_mask, unit_index, frames, capacity, S, nu, mask_frame_stride=mfs,
-                       frame_layout=layout, want_unit_mask=want_unit_mask)
+                       frame_layout=layout, want_unit_mask=want_unit_mask, frame_type=ft)
     torch.cuda.synchronize()
     rows = min(int(o["frame_offsets"][-1]), capacity)
     assert int(st_d.item()) == o["status"]
@@ -289,6 +292,7 @@ def run_compact_tp_both(abi, ref, g, tp, keep_mask, unit_index, frames, capacity
     assert (cnt_d.cpu().numpy().view(np.uint64) == o["counters"]).all()
     if want_unit_mask and S > 0:
         assert (um.cpu().numpy().view(np.uint32) == o["unit_mask"]).all()
+        assert (ut.cpu().numpy() == o["unit_type"]).all()
     if rows < cap:
         assert (src.cpu().numpy()[rows:] == -7).all()
     return o
@@ -604,6 +608,83 @@ def test_pipeline_end_to_end_c4_shape(abi, ref, overlap):
             fa = (a[:, 0, :nt].astype(np.uint32) << 16).view(np.float32)
             fb = (b[:, 0, :nt].astype(np.uint32) << 16).view(np.float32)
             assert np.abs(fa - fb).max() <= 1e-2
+    assert int(pipe.status.item()) == 0
+
+
+@pytest.mark.parametrize("rope", ["1d", "mrope"])
+def test_pipeline_temporal_patch2(abi, ref, rope):
+    """Pipeline with Qwen2-VL temporal patches (tp = 2) on a C4-shaped shard, paged KV over token units: per-frame
+    scoring, [3][2][14][14] unit rows with unit masks / types written into the unit ring, KV refresh with window
+    w/2 and stride s/2 -- every output compared with the oracle driven the same way for 5 steps."""
+    from paper_2604_06036_b200.pipeline import Pipeline
+    cfg = synth.CONFIGS["C4"]
+    g = make_grid(1920, 1080)
+    S, w, s, gop, tp = 4, 16, 4, 16, 2
+    kvb = dict(synth.QWEN_KV if rope == "1d" else synth.QWEN_MROPE_KV, layers=2)
+    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=32, device=DEV, kv_mode="paged", temporal_patch=tp,
+                    frame_layout=abi.CS_LAYOUT_GROUPED)
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(5)
+    pipe.init_cache_fill(gen)
+    nw, ring, uring = 32, pipe.ring, pipe.uring
+    gens = [synth.StreamGen(1920, 1080, synth.scene_of(cfg, si), synth.stream_seed(cfg, si)) for si in range(S)]
+    gop_h = np.zeros((S, nw + 1), np.uint32)
+    mring_h = np.zeros((S, ring, nw), np.uint32)
+    tring_h = np.zeros((S, ring), np.uint8)
+    uring_h = np.zeros((S, uring, nw), np.uint32)
+    utring_h = np.zeros((S, uring), np.uint8)
+    rng = np.random.default_rng(2)
+    frames_h = synth.random_frames(S * w, 448, 448, rng)
+    frames_g = [to_grouped(f, g) for f in frames_h]
+    frames_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in frames_g]
+    slot_h = None
+    for k in range(5):
+        f0, n = pipe.new_frames(k)
+        nu = n // tp
+        mb = np.stack([np.stack([gens[si].next_frame() for _ in range(n)]) for si in range(S)])
+        types = np.stack([synth.frame_types(n, gop, f0) for _ in range(S)])
+        fptr = abi.ptr_array(frames_d[:S * n], DEV)
+        uidx = np.tile(np.arange(f0 // tp, f0 // tp + nu, dtype=np.int32), S)
+        pool_h = [_host_cache(c).copy() for c in pipe.caches[0]]
+        ref_h = [_host_cache(c) for c in pipe.refreshed]
+        pipe.step(k, d_mb(mb), fptr, torch.from_numpy(uidx).to(DEV), torch.from_numpy(types).to(DEV))
+        torch.cuda.synchronize()
+        off, uoff = f0 % ring, (f0 % ring) // tp
+        tring_h[:, off:off + n] = types
+        so = ref.score_patches(g, mb, np.ascontiguousarray(tring_h[:, off:]), gop_h, want_score=False,
+                               frame_stride=ring - off)
+        mring_h[:, off:off + n] = so["keep_mask"][:, :n]
+        assert (u32(pipe.mask_ring) == mring_h).all()
+        co = ref.compact_tp(g, tp, mring_h[:, off:].copy(), uidx, frames_g[:S * n], pipe.capacity, S, nu,
+                            mask_frame_stride=ring - off, frame_layout=1, want_unit_mask=True,
+                            frame_type=np.ascontiguousarray(tring_h[:, off:]))
+        uring_h[:, uoff:uoff + nu] = co["unit_mask"]
+        utring_h[:, uoff:uoff + nu] = co["unit_type"]
+        assert (u32(pipe.unit_ring) == uring_h).all()
+        assert (pipe.unit_type_ring.cpu().numpy() == utring_h).all()
+        tot = int(co["frame_offsets"][-1])
+        assert (pipe.frame_offsets[:S * nu + 1].cpu().numpy() == co["frame_offsets"]).all()
+        assert (pipe.pos_ids[:tot].cpu().numpy() == co["pos_ids"][:tot]).all()
+        assert (pipe.src_index[:tot].cpu().numpy() == co["src_index"][:tot]).all()
+        assert (pipe.packed[:tot].view(torch.int16).cpu().numpy().view(np.uint16) == co["packed"][:tot]).all()
+        win = dict(window=w // tp, stride=s // tp, step=k, ring_frames=uring)
+        ko = ref.kv_refresh_paged(g, pipe.kv, win, uring_h, utring_h, pool_h, slot_h, pipe.token_cap,
+                                  ref_h if k >= 1 else None, pipe.token_cap)
+        assert (pipe.n_tokens.cpu().numpy() == ko["n_tokens"]).all()
+        sn = pipe.slots[pipe.cur].cpu().numpy()
+        for si in range(S):
+            nt = int(ko["n_tokens"][si, 0]) + 32
+            assert (pipe.disposition.cpu().numpy()[si, :nt] == ko["disposition"][si, :nt]).all()
+            assert (pipe.p_old.cpu().numpy()[si, :nt] == ko["p_old"][si, :nt]).all()
+            assert (sn[si, :nt] == ko["slot_new"][si, :nt]).all()
+            a, b = _host_cache(pipe.caches[0][si]), pool_h[si]
+            assert (a[:, 1] == b[:, 1]).all()
+            fa = (a[:, 0].astype(np.uint32) << 16).view(np.float32)
+            fb = (b[:, 0].astype(np.uint32) << 16).view(np.float32)
+            assert np.abs(fa - fb).max() <= 1e-2
+        slot_h = ko["slot_new"]
+        if k >= 1:
+            assert any((ko["disposition"][si, :int(ko["n_tokens"][si, 0])] == 2).any() for si in range(S))
     assert int(pipe.status.item()) == 0
 
 

@@ -62,7 +62,8 @@ def test_tp2_pruned_rows_are_hf_rows_and_union_rule(ref):
     km[0, 0, 0] = 1 << 0            # unit 0, frame 0: patch (0,0) -> group (0,0)
     km[0, 1, 0] = 1 << (1 * 8 + 7)  # unit 0, frame 1: patch (1,7) -> group (0,3)
     km[0, 3, 1] = 1 << (40 - 32)    # unit 1, frame 1: patch (5,0) -> group (2,0)
-    o = ref.compact_tp(g, 2, km, np.array([7, 8], np.int32), fr, 100, 1, 2, want_unit_mask=True)
+    o = ref.compact_tp(g, 2, km, np.array([7, 8], np.int32), fr, 100, 1, 2, want_unit_mask=True,
+                       frame_type=np.array([[1, 1, 0, 1]], np.uint8))
     assert o["frame_offsets"].tolist() == [0, 8, 12]
     hw = [tuple(x) for x in o["pos_ids"][:12, 1:].tolist()]
     assert hw[:4] == [(0, 0), (0, 1), (1, 0), (1, 1)] and hw[4:8] == [(0, 6), (0, 7), (1, 6), (1, 7)]
@@ -76,6 +77,7 @@ def test_tp2_pruned_rows_are_hf_rows_and_union_rule(ref):
         assert (_f32(o["packed"][n]) == hf[r]).all()
         assert o["src_index"][n] == t * 48 + h * 8 + w
     assert o["unit_mask"][0, 0].tolist() == [1 | (1 << 15), 0] and o["unit_mask"][0, 1].tolist() == [0, 1 << 8]
+    assert o["unit_type"][0].tolist() == [1, 0]          # (P, P) -> P; (I, P) -> I
 
 
 def test_tp1_equals_plain_compaction(ref):
