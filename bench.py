@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--overlap", action="store_true",
                     help="run compact and kv_refresh on side streams concurrently with the next step's scoring "
                          "(measured: no gain -- kv_refresh already saturates HBM and holds every SM; default off)")
+    ap.add_argument("--temporal-patch", type=int, default=1, choices=[1, 2],
+                    help="frames per visual token (Qwen2-VL video: 2; NEXT-3); KV refresh over token units")
     ap.add_argument("--kv-mode", default="paged", choices=["paged", "copy"],
                     help="paged: codecsight_kv_refresh_paged (in place, NEXT-1); copy: out-of-place double buffer")
     ap.add_argument("--rope", default="1d", choices=["1d", "mrope"],
@@ -175,7 +177,7 @@ def ncu_traffic(kernel: str):
 # --------------------------------------------------------------------------------------------------------------
 # CPU oracle (baseline / reference arm)
 # --------------------------------------------------------------------------------------------------------------
-def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "paged"):
+def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "paged", tp: int = 1):
     """Run the oracle, as it stands, on a bounded sample of the workload: whole stream-steps (score + compact +
     kv_refresh) of alternating streams, until ~budget_s seconds of single-threaded CPU work are spent."""
     import oracle.ref as ref
@@ -186,8 +188,9 @@ def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "pag
     nw = (g["grid_w"] * g["grid_h"] + 31) // 32
     kvb = cfg["kv"]
     groups = (g["grid_w"] // 2) * (g["grid_h"] // 2)
-    cap = w * groups + cfg["n_prompt"]
-    rcap = (s + 1 + math.ceil(max(0, w - s) / gop)) * groups + cfg["n_prompt"]
+    wu, su, uring = w // tp, s // tp, ring // tp
+    cap = wu * groups + cfg["n_prompt"]
+    rcap = (su + 1 + math.ceil(max(0, wu - su) / max(1, gop // tp))) * groups + cfg["n_prompt"]
     kv = dict(kvb, capacity=cap, refresh_capacity=rcap, n_prompt=cfg["n_prompt"]) if kvb else None
     rng = np.random.default_rng(0)
     frames = synth.random_frames(w, g["grid_h"] * g["patch"], g["grid_w"] * g["patch"], rng)
@@ -202,6 +205,8 @@ def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "pag
         gop_h = np.zeros((1, nw + 1), np.uint32)
         mring = np.zeros((1, ring, nw), np.uint32)
         tring = np.zeros((1, ring), np.uint8)
+        umring = np.zeros((1, uring, nw), np.uint32) if tp > 1 else mring
+        utring = np.zeros((1, uring), np.uint8) if tp > 1 else tring
 
         def do_step(k, timed):
             f0, n = step_frames(cfg, k)
@@ -212,8 +217,16 @@ def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "pag
             so = ref.score_patches(g, mb, np.ascontiguousarray(tring[:, off:]), gop_h, frame_stride=ring - off,
                                    want_score=False)
             mring[0, off:off + n] = so["keep_mask"][0, :n]
-            ref.compact(g, mring[:, off:].copy(), np.arange(f0, f0 + n, dtype=np.int32), frames[:n],
-                        n * g["grid_w"] * g["grid_h"], 1, n, mask_frame_stride=ring - off)
+            if tp > 1:
+                co = ref.compact_tp(g, tp, mring[:, off:].copy(), np.arange(f0 // tp, (f0 + n) // tp, dtype=np.int32),
+                                    frames[:n], n // tp * g["grid_w"] * g["grid_h"], 1, n // tp,
+                                    mask_frame_stride=ring - off, want_unit_mask=True,
+                                    frame_type=np.ascontiguousarray(tring[:, off:]))
+                umring[0, off // tp:(off + n) // tp] = co["unit_mask"][0]
+                utring[0, off // tp:(off + n) // tp] = co["unit_type"][0]
+            else:
+                ref.compact(g, mring[:, off:].copy(), np.arange(f0, f0 + n, dtype=np.int32), frames[:n],
+                            n * g["grid_w"] * g["grid_h"], 1, n, mask_frame_stride=ring - off)
             t1 = time.perf_counter()
             return t1 - t0, mb
 
@@ -229,15 +242,15 @@ def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "pag
                 old[...] = rng.integers(0, 65536, size=(1,), dtype=np.uint16)  # content irrelevant to the timing
             new = np.zeros(shape, dtp)
             refr = np.zeros(rshape, dtp)
-            win = dict(window=w, stride=s, step=k_meas, ring_frames=ring)
+            win = dict(window=wu, stride=su, step=k_meas, ring_frames=uring)
             if kv_mode == "paged":
                 slot_old = np.arange(cap, dtype=np.int32)[None]     # any valid slot map of window k-1
                 t0 = time.perf_counter()
-                ref.kv_refresh_paged(g, kv, win, mring, tring, [old], slot_old, cap, [refr], cap)
+                ref.kv_refresh_paged(g, kv, win, umring, utring, [old], slot_old, cap, [refr], cap)
                 dt += time.perf_counter() - t0
             else:
                 t0 = time.perf_counter()
-                ref.kv_refresh(g, kv, win, mring, tring, [old], [new], [refr], cap)
+                ref.kv_refresh(g, kv, win, umring, utring, [old], [new], [refr], cap)
                 dt += time.perf_counter() - t0
         t_total += dt
         frames_done += s
@@ -251,10 +264,10 @@ def run_reference(args, cfg, rank, world):
         return
     per_step = max(1.0, args.cpu_seconds / max(1, args.steps))
     for _ in range(args.warmup):
-        oracle_sample(cfg, 0.0, max_steps=1, kv_mode=args.kv_mode)
+        oracle_sample(cfg, 0.0, max_steps=1, kv_mode=args.kv_mode, tp=args.temporal_patch)
     tot = dict(seconds=0.0, frames=0, stream_steps=0)
     for _ in range(args.steps):
-        r = oracle_sample(cfg, per_step, max_steps=4, kv_mode=args.kv_mode)
+        r = oracle_sample(cfg, per_step, max_steps=4, kv_mode=args.kv_mode, tp=args.temporal_patch)
         for kk in tot:
             tot[kk] += r[kk]
     fps = tot["frames"] / tot["seconds"]
@@ -263,7 +276,7 @@ def run_reference(args, cfg, rank, world):
            "ms_per_step": 1000.0 * tot["seconds"] / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
            "config": {"workload": cfg["name"], "streams_per_gpu": cfg["streams"], "window": cfg["window"],
-                      "stride": cfg["stride"], "gop": cfg["gop"]},
+                      "stride": cfg["stride"], "gop": cfg["gop"], "temporal_patch": args.temporal_patch},
            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": 1, "kind": "oracle",
                             "sample": f"{tot['stream_steps']} whole stream-steps (k=4) of alternating "
                                       f"static/high-motion streams, single-threaded C oracle"},
@@ -295,7 +308,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
     pre = dict(src_w=sw, src_h=sh, y_pitch=sw, uv_pitch=sw) if args.frames == "nv12" else None
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
-                    kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre, overlap=args.overlap)
+                    kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre, overlap=args.overlap,
+                    temporal_patch=args.temporal_patch)
+    tp = args.temporal_patch
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     pipe.init_cache_fill(gen)
@@ -326,7 +341,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         t = np.stack([synth.frame_types(n, gop, f0)] * S)
         types_host.append(torch.from_numpy(t).pin_memory())
         types_dev.append(types_host[-1].to(dev))
-        fidx_dev.append(torch.from_numpy(np.tile(np.arange(f0, f0 + n, dtype=np.int32), S)).to(dev))
+        fidx_dev.append(torch.from_numpy(np.tile(np.arange(f0 // tp, (f0 + n) // tp, dtype=np.int32), S)).to(dev))
     torch.cuda.synchronize()
     if not args.quiet:
         free, tot = torch.cuda.mem_get_info(dev)
@@ -424,6 +439,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         layouts["nv12_fused"] = time_compact(fused)
         layouts["nv12_preprocess_all_then_compact"] = time_compact(unfused)
         del model_frames
+    elif tp > 1:
+        for lname, lid in (("grouped", abi.CS_LAYOUT_GROUPED), ("planar", abi.CS_LAYOUT_PLANAR)):
+            layouts[lname] = time_compact(lambda lid=lid: abi.codecsight_compact_tp(
+                g, tp, S, s // tp, pipe.mask_ring[:, off_l:], pipe.ring, fidx_dev[k_last], ptr_s, pipe.capacity,
+                pipe.packed, pipe.pos_ids, pipe.src_index, pipe.frame_offsets[:S * s // tp + 1], pipe.counters,
+                pipe.status, frame_layout=lid))
     else:
         for lname, lid in (("grouped", abi.CS_LAYOUT_GROUPED), ("planar", abi.CS_LAYOUT_PLANAR)):
             layouts[lname] = time_compact(lambda lid=lid: abi.codecsight_compact(
@@ -445,7 +466,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             f0, n = step_frames(cfg, k)
             in_mb.append(mb_host[1 + (k - 1) % n_pool])
             in_ty.append(torch.from_numpy(np.stack([synth.frame_types(n, gop, f0)] * S)).pin_memory())
-            in_fi.append(torch.from_numpy(np.tile(np.arange(f0, f0 + n, dtype=np.int32), S)).pin_memory())
+            in_fi.append(torch.from_numpy(np.tile(np.arange(f0 // tp, (f0 + n) // tp, dtype=np.int32),
+                                                  S)).pin_memory())
         st_mb = [torch.empty_like(mb_dev[1]) for _ in range(2)]
         st_ty = [torch.empty_like(in_ty[0], device=dev) for _ in range(2)]
         st_fi = [torch.empty_like(in_fi[0], device=dev) for _ in range(2)]
@@ -485,7 +507,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 if pipe.kv is not None:                                    # D2H: the step's results
                     res[b][:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
                 res[b][S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
-                res[b][-1:].copy_(pipe.frame_offsets[S * n:S * n + 1], non_blocking=True)
+                res[b][-1:].copy_(pipe.frame_offsets[S * n // tp:S * n // tp + 1], non_blocking=True)
                 consumed[b].record(res_stream)
                 done[b].record(res_stream)
             if i >= 1:
@@ -532,7 +554,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": 0.25, "alpha": 0.0,
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
-                   "frames": args.frames, "overlap": args.overlap,
+                   "frames": args.frames, "overlap": args.overlap, "temporal_patch": tp,
                    "parallelism": f"stream-shard x{world}",
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
                          "see per-step bytes)"},
@@ -572,7 +594,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                       "pipelining": "H2D of step k+1 on a copy stream overlaps step k; host reads step k-1's result"}
     if not args.no_cpu_baseline:
         log("[rank 0] timing the CPU oracle on a bounded sample ...")
-        r = oracle_sample(cfg, args.cpu_seconds, kv_mode=args.kv_mode)
+        r = oracle_sample(cfg, args.cpu_seconds, kv_mode=args.kv_mode, tp=tp)
         out["cpu_baseline"] = {"value": r["frames"] / r["seconds"], "unit": "frames/s", "cores": 1, "kind": "oracle",
                                "sample": f"{r['stream_steps']} whole stream-steps (window k=4: {s} new frames + "
                                          f"KV refresh) of streams {r['scenes'][:4]}..., single-threaded C oracle, "

@@ -217,40 +217,62 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
   const long long FW = P.FW;
   const long long plane = (long long)P.FH * FW;
   if (LAYOUT == CS_LAYOUT_GROUPED && tp > 1) {
-    // the unit's frames hold the group as contiguous blocks [q][3][p][p]; interleave them per (q, c) into the
-    // tile in 8-B pieces (a p*p segment is 392 B = 49 x 8 B for 14-px patches; pp % 4 == 0 is checked by vec_in)
+    // direct, no staging: every 16-B store of the group's output rows [q][3][tp][p][p] is assembled from two 8-B loads of the
+    // unit's frames (a p*p segment is a multiple of 4 elements, so a 4-element half never straddles segments)
     const int gs2 = G * G;
-    const long long blk_el = (long long)gs2 * 3 * pp;
-    const long long goff = ((long long)gr * P.ngc + gc) * blk_el;
-    for (int f = 0; f < tp; ++f) {
-      const uint16_t* blk = (f == 0 ? frame : static_cast<const uint16_t*>(P.frames[(long long)slot * tp + f])) + goff;
-      if (vec_in) {
-        const int n8 = static_cast<int>(blk_el / 4);
-        constexpr int kU = 4;
-        for (int e0 = 0; e0 < n8; e0 += 32 * kU) {
-          uint2 v[kU];
+    long long nvalid = P.capacity - n0;
+    nvalid = nvalid < 0 ? 0 : (nvalid > gs2 ? gs2 : nvalid);
+    const int row_el = 3 * tp * pp;
+    const long long goff = ((long long)gr * P.ngc + gc) * ((long long)gs2 * 3 * pp);
+    const uint16_t* fb[4];
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int e = e0 + u * 32 + lane;
-            if (e < n8) v[u] = cs::ld_nc_v2(blk + 4 * e);
-          }
+    for (int f = 0; f < 4; ++f)
+      fb[f] = f < tp ? (f == 0 ? frame : static_cast<const uint16_t*>(P.frames[(long long)slot * tp + f])) + goff
+                     : frame;
+    auto src_of = [&](int el) -> const uint16_t* {
+      const int q = el / row_el, r = el - q * row_el;
+      const int c = r / (tp * pp), r2 = r - c * tp * pp;
+      const int f = r2 / pp, x = r2 - f * pp;
+      const uint16_t* b = f == 0 ? fb[0] : (f == 1 ? fb[1] : (f == 2 ? fb[2] : fb[3]));
+      return b + (q * 3 + c) * pp + x;
+    };
+    uint16_t* dst = P.packed + n0 * row_el;
+    const int nel = static_cast<int>(nvalid) * row_el;
+    const int n16 = nel / 8;
+    if (!(vec_in && P.vec_out)) {  // unaligned frames or rows: element copies
+      for (int e = lane; e < nel; e += 32) dst[e] = *src_of(e);
+    } else {
+    for (int e = n16 * 8 + lane; e < nel; e += 32) dst[e] = *src_of(e);  // tail of a truncated group
+    constexpr int kU = TP > 0 ? 4 : 1;  // the generic (runtime-shape) instance stays within 64 registers
+    for (int e0 = 0; e0 < n16; e0 += 32 * kU) {
+      uint2 lo[kU], hi[kU];
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int e = e0 + u * 32 + lane;
-            if (e < n8) {
-              const int el = 4 * e, seg = el / pp, r = el - seg * pp;
-              *reinterpret_cast<uint2*>(tile + (seg * tp + f) * pp + r) = v[u];
-            }
-          }
-        }
-      } else {
-        for (int el = lane; el < blk_el; el += 32) {
-          const int seg = el / pp, r = el - seg * pp;
-          tile[(seg * tp + f) * pp + r] = blk[el];
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * 32 + lane;
+        if (e < n16) {
+          lo[u] = cs::ld_nc_v2(src_of(8 * e));
+          hi[u] = cs::ld_nc_v2(src_of(8 * e + 4));
         }
       }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * 32 + lane;
+        if (e < n16) reinterpret_cast<uint4*>(dst)[e] = make_uint4(lo[u].x, lo[u].y, hi[u].x, hi[u].y);
+      }
     }
-  } else if (LAYOUT == CS_LAYOUT_GROUPED) {
+    }
+    if (lane < nvalid) {
+      const int dy = lane / G, dx = lane - dy * G;
+      const int h = gr * G + dy, w = gc * G + dx;
+      const long long n = n0 + lane;
+      P.pos_ids[3 * n + 0] = t_index;
+      P.pos_ids[3 * n + 1] = h;
+      P.pos_ids[3 * n + 2] = w;
+      P.src_index[n] = slot * P.np + h * P.grid_w + w;
+    }
+    return;
+  }
+  if (LAYOUT == CS_LAYOUT_GROUPED) {
     // the kept group is one contiguous block already in packed order: straight 16-B copy (no smem staging)
     const int gs2 = G * G;
     long long nvalid = P.capacity - n0;
@@ -293,9 +315,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     }
     return;
   }
-  if (LAYOUT == CS_LAYOUT_GROUPED) {
-    // tp > 1: the tile was filled above
-  } else if (LAYOUT == kLayoutNV12) {
+  if (LAYOUT == kLayoutNV12) {
     // preprocess only the kept group's 3 x gp x gp model pixels straight from the decoded NV12 frame
     const uint8_t* Yp = reinterpret_cast<const uint8_t*>(frame);
     const uint8_t* UVp = static_cast<const uint8_t*>(P.uv_planes[slot]);
@@ -434,7 +454,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
 }
 
 template <int TP, int TG, int LAYOUT, int TT>
-__global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED && TT == 1) ? 4 : 2)
+__global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED && TP > 0) ? 4 : 2)
     compact_gather(const __grid_constant__ CompactParams P) {
   extern __shared__ __align__(16) unsigned char g_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -447,7 +467,7 @@ __global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED &
   const long long q1 = total_groups * (wid + 1) / nwarps;
   if (q >= q1) return;
   const int tp = TT > 0 ? TT : P.tp;
-  const int tile_bytes = (LAYOUT == CS_LAYOUT_GROUPED && tp == 1) ? 0 : tile_bytes_of(TP > 0 ? TP : P.p, G, tp);
+  const int tile_bytes = LAYOUT == CS_LAYOUT_GROUPED ? 0 : tile_bytes_of(TP > 0 ? TP : P.p, G, tp);
   uint16_t* tile = reinterpret_cast<uint16_t*>(g_smem + (size_t)wib * tile_bytes);
   uint32_t* mask = reinterpret_cast<uint32_t*>(g_smem + (size_t)kWarpsPerCta * tile_bytes) + wib * P.nw;
 
@@ -567,9 +587,9 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
   const bool grouped = frame_layout == CS_LAYOUT_GROUPED;
   const bool nv12 = frame_layout == kLayoutNV12;
   const size_t smem =
-      (size_t)kWarpsPerCta * (((grouped && tp == 1) ? 0 : tile_bytes_of(g->patch, g->group, tp)) + 4 * P.nw);
+      (size_t)kWarpsPerCta * ((grouped ? 0 : tile_bytes_of(g->patch, g->group, tp)) + 4 * P.nw);
   const bool fast = g->patch == 14 && g->group == 2 && (tp == 1 || tp == 2);
-  const int grid = cs_num_sms() * ((grouped && tp == 1) ? 8 : 4);
+  const int grid = cs_num_sms() * (grouped ? 8 : 4);
   const void* fn;
   int slot;
 #define CS_PICK(TP, TG, LY, TT, SL) \
