@@ -189,6 +189,30 @@ int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, co
                        cudaStream_t stream);
 
 /* ------------------------------------------------------------------------------------------------------------
+ * codecsight_score_compact — NEXT-2: scoring and compaction fused into ONE kernel pass ("single batched operation",
+ * P:268, over the pruned patches).  Results are bit-identical to codecsight_score_patches followed by
+ * codecsight_compact(keep_mask, mask_frame_stride = frame_stride) on the same arguments -- every output of both
+ * calls (keep_mask, gop_state, score, kept_count, packed, pos_ids, src_index, frame_offsets), the counters of both
+ * and the status bits of both.  Each stream's cluster scores its frames, then finds its offset in the packed batch
+ * by a decoupled look-back over the streams (no separate scan pass, no mask round trip through a second launch) and
+ * copies its kept groups.
+ *   workspace       device, >= codecsight_score_compact_workspace_size(n_streams) bytes, 8-B aligned, ZERO-FILLED
+ *                   once by the caller before first use; every call leaves it zeroed again.  One call at a time
+ *                   per workspace (calls on different CUDA streams need different workspaces).
+ *   other arguments as codecsight_score_patches and codecsight_compact (frame_index / frames / frame_layout /
+ *   capacity / packed / pos_ids / src_index / frame_offsets over the n_streams x n_frames slots).
+ * n_streams == 0 enqueues nothing (frame_offsets untouched).
+ * --------------------------------------------------------------------------------------------------------- */
+size_t codecsight_score_compact_workspace_size(int32_t n_streams);
+int codecsight_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                             const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
+                             uint32_t* gop_state, float* score, int32_t* kept_count, const int32_t* frame_index,
+                             const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
+                             int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, void* workspace,
+                             size_t workspace_bytes, unsigned long long* counters, int32_t* status,
+                             cudaStream_t stream);
+
+/* ------------------------------------------------------------------------------------------------------------
  * codecsight_compact_tp — NEXT-3: temporal patches.  Qwen2-VL / Qwen3-VL embed video with
  * temporal_patch_size 2: one visual token covers `temporal_patch` consecutive frames and its patch row is
  * [3][temporal_patch][patch][patch] (channel, frame, y, x -- the Hugging Face processor's flatten order).

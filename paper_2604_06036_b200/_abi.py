@@ -86,6 +86,11 @@ def lib():
         L.codecsight_compact_nv12.restype = C.c_int
         L.codecsight_compact_nv12.argtypes = [C.POINTER(CsGrid), C.POINTER(CsPreprocess), I32, I32, P, I64, P, P, P,
                                               I64, P, P, P, P, P, P, P]
+        L.codecsight_score_compact_workspace_size.restype = C.c_size_t
+        L.codecsight_score_compact_workspace_size.argtypes = [I32]
+        L.codecsight_score_compact.restype = C.c_int
+        L.codecsight_score_compact.argtypes = [C.POINTER(CsGrid), I32, I32, P, P, P, I64, P, P, P, P, P, I32, I64, P,
+                                               P, P, P, P, C.c_size_t, P, P, P]
         L.codecsight_compact_tp.restype = C.c_int
         L.codecsight_compact_tp.argtypes = [C.POINTER(CsGrid), I32, I32, I32, P, I64, P, P, I32, I64, P, P, P, P, P,
                                             I64, P, P, P, P, P]
@@ -192,6 +197,23 @@ def codecsight_compact_nv12(g: dict, pre: dict, n_streams: int, n_frames: int, k
     _check(rc, "codecsight_compact_nv12")
 
 
+def score_compact_workspace_size(n_streams: int) -> int:
+    return int(lib().codecsight_score_compact_workspace_size(n_streams))
+
+
+def codecsight_score_compact(g: dict, n_streams: int, n_frames: int, mb, frame_type, keep_mask, frame_stride: int,
+                             gop_state, score, kept_count, frame_index, frames, capacity: int, packed, pos_ids,
+                             src_index, frame_offsets, workspace, counters, status,
+                             frame_layout: int = CS_LAYOUT_PLANAR, stream=None) -> None:
+    rc = lib().codecsight_score_compact(C.byref(make_grid(g)), n_streams, n_frames, _ptr(mb), _ptr(frame_type),
+                                        _ptr(keep_mask), frame_stride, _ptr(gop_state), _ptr(score),
+                                        _ptr(kept_count), _ptr(frame_index), _ptr(frames), frame_layout, capacity,
+                                        _ptr(packed), _ptr(pos_ids), _ptr(src_index), _ptr(frame_offsets),
+                                        _ptr(workspace), workspace.numel() * workspace.element_size(),
+                                        _ptr(counters), _ptr(status), _stream(stream))
+    _check(rc, "codecsight_score_compact")
+
+
 def codecsight_compact_tp(g: dict, temporal_patch: int, n_streams: int, n_units: int, keep_mask,
                           mask_frame_stride: int, unit_index, frames, capacity: int, packed, pos_ids, src_index,
                           frame_offsets, counters, status, frame_layout: int = CS_LAYOUT_PLANAR, unit_mask=None,
@@ -259,5 +281,6 @@ compact = codecsight_compact
 compact_nv12 = codecsight_compact_nv12
 mv_rasterize = codecsight_mv_rasterize
 compact_tp = codecsight_compact_tp
+score_compact = codecsight_score_compact
 similar_hist = codecsight_similar_hist
 kv_refresh = codecsight_kv_refresh

@@ -99,6 +99,37 @@ int codecsight_score_patches(const cs_grid* g, int32_t n_streams, int32_t n_fram
                          kept_count, counters, status, stream);
 }
 
+size_t codecsight_score_compact_workspace_size(int32_t n_streams) { return cs_score_compact_workspace_bytes(n_streams); }
+
+int codecsight_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                             const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
+                             uint32_t* gop_state, float* score, int32_t* kept_count, const int32_t* frame_index,
+                             const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
+                             int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, void* workspace,
+                             size_t workspace_bytes, unsigned long long* counters, int32_t* status,
+                             cudaStream_t stream) {
+  int rc = grid_ok(g);
+  if (rc) return rc;
+  if (n_streams < 0 || n_frames < 1 || n_frames > cs::kMaxFramesPerCall || frame_stride < n_frames || capacity < 0)
+    return CS_ERR_INVALID_ARGUMENT;
+  if (n_streams == 0) return CS_OK;
+  if (!mb || !frame_type || !keep_mask || !gop_state || !kept_count || !counters || !status) return CS_ERR_INVALID_ARGUMENT;
+  if (!frame_index || !frames || !frame_offsets || !workspace) return CS_ERR_INVALID_ARGUMENT;
+  if (capacity > 0 && (!packed || !pos_ids || !src_index)) return CS_ERR_INVALID_ARGUMENT;
+  if (frame_layout != CS_LAYOUT_PLANAR && frame_layout != CS_LAYOUT_GROUPED) return CS_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < cs_score_compact_workspace_bytes(n_streams)) return CS_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 7u) != 0) return CS_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(mb) & 7u) != 0) return CS_ERR_INVALID_ARGUMENT;
+  if (g->mb_cols > 4096) return CS_ERR_UNSUPPORTED;
+  const long long n_slots = static_cast<long long>(n_streams) * n_frames;
+  if (n_slots * g->grid_w * g->grid_h >= 2147483648LL) return CS_ERR_UNSUPPORTED;
+  if (g->group * g->patch > 32) return CS_ERR_UNSUPPORTED;
+  if ((rc = device_ok())) return rc;
+  return cs_launch_score_compact(g, n_streams, n_frames, mb, frame_type, keep_mask, frame_stride, gop_state, score,
+                                 kept_count, frame_index, frames, frame_layout, capacity, packed, pos_ids, src_index,
+                                 frame_offsets, workspace, counters, status, stream);
+}
+
 int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,
                        int64_t mask_frame_stride, const int32_t* frame_index, const void* const* frames,
                        int32_t frame_layout, int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,

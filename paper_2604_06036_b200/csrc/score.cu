@@ -48,8 +48,93 @@ struct ScoreParams {
   unsigned long long* counters;
   int32_t* status;
   unsigned off_vrow, off_srow, off_dyn, off_bar;
+  // ---- fused compaction (NEXT-2: codecsight_score_compact) ----
+  int fused;
+  int layout;            // CS_LAYOUT_PLANAR | CS_LAYOUT_GROUPED
+  int patch, FW, FH, ngc, vec_out;
+  long long capacity;
+  const int32_t* frame_index;
+  const void* const* frames;
+  uint16_t* packed;
+  int32_t* pos_ids;
+  int32_t* src_index;
+  int32_t* frame_offsets;
+  unsigned* ws_ctr;              // [0] ticket, [1] CTAs done
+  unsigned long long* ws_flags;  // [n_streams] look-back words: (state << 62) | rows, state 1 = aggregate, 2 = prefix
+  unsigned total_ctas;
 };
 
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kFlagVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// One kept group (gr, gc) of frame `fr` -> packed rows [n0, n0 + G^2) (rows >= capacity dropped); returns rows
+// written.  Same bytes and order as codecsight_compact (reading Q14/Q15).
+__device__ __forceinline__ int fused_copy_group(const ScoreParams& P, const uint16_t* __restrict__ fr, bool vec_in,
+                                                int gr, int gc, long long n0, long long slot, int t_index,
+                                                int lane) {
+  const int G = P.G, p = P.patch, pp = p * p, gs2 = G * G;
+  long long nvalid = P.capacity - n0;
+  nvalid = nvalid < 0 ? 0 : (nvalid > gs2 ? gs2 : nvalid);
+  if (nvalid == 0) return 0;
+  const long long row_el = 3ll * pp;
+  uint16_t* dst = P.packed + n0 * row_el;
+  const int nel = static_cast<int>(nvalid * row_el);
+  if (P.layout == CS_LAYOUT_GROUPED) {
+    const uint16_t* blk = fr + ((long long)gr * P.ngc + gc) * gs2 * row_el;
+    if (vec_in && P.vec_out) {
+      const int n16 = nel / 8;
+      for (int e = n16 * 8 + lane; e < nel; e += 32) dst[e] = blk[e];
+      const uint4* s4 = reinterpret_cast<const uint4*>(blk);
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      constexpr int kU = 5;
+      for (int e0 = 0; e0 < n16; e0 += 32 * kU) {
+        uint4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int e = e0 + u * 32 + lane;
+          if (e < n16) v[u] = cs::ld_nc_v4(s4 + e);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int e = e0 + u * 32 + lane;
+          if (e < n16) d4[e] = v[u];
+        }
+      }
+    } else {
+      for (int e = lane; e < nel; e += 32) dst[e] = blk[e];
+    }
+  } else {
+    // planar CHW: element (q, c, y, x) of the packed group reads pixel (c, (gr*G + dy)*p + y, (gc*G + dx)*p + x)
+    const long long plane = (long long)P.FH * P.FW;
+    for (int e = lane; e < nel; e += 32) {
+      const int q = e / (3 * pp), r = e - q * 3 * pp;
+      const int c = r / pp, r2 = r - c * pp;
+      const int y = r2 / p, x = r2 - y * p;
+      const int dy = q / G, dx = q - dy * G;
+      dst[e] = fr[c * plane + (long long)((gr * G + dy) * p + y) * P.FW + (gc * G + dx) * p + x];
+    }
+  }
+  if (lane < nvalid) {
+    const int dy = lane / G, dx = lane - dy * G;
+    const int h = gr * G + dy, w = gc * G + dx;
+    const long long n = n0 + lane;
+    P.pos_ids[3 * n + 0] = t_index;
+    P.pos_ids[3 * n + 1] = h;
+    P.pos_ids[3 * n + 2] = w;
+    P.src_index[n] = static_cast<int32_t>(slot * P.np + h * P.grid_w + w);
+  }
+  return static_cast<int>(nvalid);
+}
+
+template <bool FUSED>
 __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__ ScoreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint8_t s_types[cs::kMaxFramesPerCall];
@@ -60,9 +145,18 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   __shared__ int s_np, s_kept, s_badmb;
   __shared__ unsigned long long s_near;
 
+  __shared__ int s_sidx;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
-  const int sidx = blockIdx.x / P.cluster;
+  int sidx_ = blockIdx.x / P.cluster;
+  if (FUSED) {
+    // streams are taken in ticket order (cluster start order), so every stream a look-back waits for belongs to a
+    // cluster that is already running: the decoupled look-back below cannot deadlock
+    if (rank == 0 && threadIdx.x == 0) s_sidx = static_cast<int>(atomicAdd(&P.ws_ctr[0], 1u));
+    cluster.sync();
+    sidx_ = *cluster.map_shared_rank(&s_sidx, 0);
+  }
+  const int sidx = sidx_;
   const int tid = threadIdx.x, lane = tid & 31;
   const int nthr = blockDim.x;
 
@@ -329,16 +423,120 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_SCORE], bytes);
     cs::atomic_or_status(P.status, st_bits);
   }
+  if (FUSED) {
+    // ---- NEXT-2: compaction fused into the scoring pass -----------------------------------------------------
+    // (1) stream-local prefix of emitted patches over the stream's frames (kept counts are group-complete, so a
+    //     frame emits exactly kept_count rows); (2) the stream's offset in the batch by a decoupled look-back over
+    //     the streams (ticket order = stream order); (3) the cluster's warps split the stream's kept groups evenly
+    //     and copy them (frame -> packed rows), exactly as codecsight_compact would.
+    __shared__ int s_lp[cs::kMaxFramesPerCall + 1];
+    __shared__ long long s_prefix;
+    __shared__ int s_written;
+    cluster.sync();  // the stream's keep masks and kept counts are in global memory (cluster-scope acquire)
+    if (tid == 0) {
+      int acc = 0;
+      for (int f = 0; f < P.n_frames; ++f) {
+        s_lp[f] = acc;
+        acc += P.kept_count[(long long)sidx * P.n_frames + f];
+      }
+      s_lp[P.n_frames] = acc;
+      s_written = 0;
+      if (rank == 0) {
+        const unsigned long long tot = static_cast<unsigned long long>(acc);
+        unsigned long long excl = 0;
+        if (sidx == 0) {
+          st_release_u64(&P.ws_flags[0], kFlagPre | tot);
+        } else {
+          st_release_u64(&P.ws_flags[sidx], kFlagAgg | tot);
+          for (int j = sidx - 1; j >= 0;) {
+            const unsigned long long v = ld_acquire_u64(&P.ws_flags[j]);
+            if ((v & ~kFlagVal) == 0ull) continue;  // stream j not counted yet
+            excl += v & kFlagVal;
+            if ((v & ~kFlagVal) == kFlagPre) break;
+            --j;
+          }
+          st_release_u64(&P.ws_flags[sidx], kFlagPre | (excl + tot));
+        }
+        s_prefix = static_cast<long long>(excl);
+        if (static_cast<long long>(excl + tot) > P.capacity) cs::atomic_or_status(P.status, CS_STATUS_CAPACITY);
+        if (sidx == P.n_streams - 1) P.frame_offsets[(long long)P.n_streams * P.n_frames] = static_cast<int32_t>(excl + tot);
+      }
+    }
+    cluster.sync();
+    const long long pre = *cluster.map_shared_rank(&s_prefix, 0);
+    for (int f = f_begin + tid; f < f_end; f += nthr)
+      P.frame_offsets[(long long)sidx * P.n_frames + f] = static_cast<int32_t>(pre + s_lp[f]);
+    const int gs2 = P.G * P.G;
+    const long long groups = s_lp[P.n_frames] / gs2;
+    const long long nwarp_c = static_cast<long long>(P.cluster) * (nthr >> 5);
+    const long long wid = static_cast<long long>(rank) * (nthr >> 5) + (tid >> 5);
+    long long q = groups * wid / nwarp_c;
+    const long long q1 = groups * (wid + 1) / nwarp_c;
+    int written = 0;
+    if (q < q1) {
+      int f = 0;
+      while (f + 1 < P.n_frames && s_lp[f + 1] / gs2 <= q) ++f;
+      long long skip = q - s_lp[f] / gs2;
+      const int ngroups = (P.grid_h / P.G) * P.ngc;
+      for (; f < P.n_frames && q < q1; ++f, skip = 0) {
+        const long long slot = (long long)sidx * P.n_frames + f;
+        const uint32_t* m = P.keep_mask + ((long long)sidx * P.frame_stride + f) * nw;
+        const uint16_t* fr = static_cast<const uint16_t*>(P.frames[slot]);
+        const int t_index = P.frame_index[slot];
+        const bool vec_in = ((reinterpret_cast<uintptr_t>(fr) & 15u) == 0) && ((3 * gs2 * P.patch * P.patch * 2) % 16 == 0);
+        for (int base = 0; base < ngroups && q < q1; base += 32) {
+          const int qq = base + lane;
+          const bool kept = qq < ngroups && cs::group_kept(m, qq, P.ngc, P.G, P.grid_w);
+          uint32_t bal = __ballot_sync(0xffffffffu, kept);
+          const int nb = __popc(bal);
+          if (skip >= nb) {
+            skip -= nb;
+            continue;
+          }
+          while (skip > 0) {
+            bal &= bal - 1;
+            --skip;
+          }
+          while (bal && q < q1) {
+            const int b = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const int gi = base + b;
+            const int gr = gi / P.ngc, gc = gi - gr * P.ngc;
+            written += fused_copy_group(P, fr, vec_in, gr, gc, pre + q * gs2, slot, t_index, lane);
+            ++q;
+          }
+        }
+      }
+    }
+    if (lane == 0 && written) atomicAdd(&s_written, written);
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned long long rows = static_cast<unsigned long long>(s_written);
+      const unsigned long long row_bytes = 3ull * P.patch * P.patch * 2ull;
+      const unsigned long long nf = static_cast<unsigned long long>(f_end - f_begin);
+      cs::atomic_add_u64(&P.counters[CS_CNT_PACKED_ROWS], rows);
+      cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_COMPACT], nf * (4ull * nw + 4ull) + rows * (2ull * row_bytes + 16ull));
+      // the last CTA out returns the workspace to zero (every look-back has completed by then)
+      __threadfence();
+      if (atomicAdd(&P.ws_ctr[1], 1u) == P.total_ctas - 1) {
+        for (int j = 0; j < P.n_streams; ++j) P.ws_flags[j] = 0ull;
+        P.ws_ctr[0] = 0u;
+        P.ws_ctr[1] = 0u;
+        __threadfence();
+      }
+    }
+  }
   cluster.sync();  // keep this CTA's shared memory alive until every DSMEM reader is done
 }
 
 }  // namespace
 
-int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
-                    const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride, uint32_t* gop_state,
-                    float* score, int32_t* kept_count, unsigned long long* counters, int32_t* status,
-                    cudaStream_t stream) {
+static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                        const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride, uint32_t* gop_state,
+                        float* score, int32_t* kept_count, unsigned long long* counters, int32_t* status,
+                        const ScoreParams* fuse, cudaStream_t stream) {
   ScoreParams P{};
+  if (fuse) P = *fuse;
   P.src_w = g->src_w;
   P.src_h = g->src_h;
   P.mb = g->mb_size;
@@ -398,7 +596,10 @@ int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const
   const size_t smem = off;
 
   if (smem > 200 * 1024) return CS_ERR_UNSUPPORTED;
-  if (cs_set_smem_attr(reinterpret_cast<const void*>(score_kernel), 0, 200 * 1024) != 0) return CS_ERR_CUDA;
+  P.total_ctas = static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster);
+  const void* fn = P.fused ? reinterpret_cast<const void*>(score_kernel<true>)
+                          : reinterpret_cast<const void*>(score_kernel<false>);
+  if (cs_set_smem_attr(fn, P.fused ? 19 : 0, 200 * 1024) != 0) return CS_ERR_CUDA;
 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster), 1, 1);
@@ -412,6 +613,47 @@ int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, score_kernel, P) != cudaSuccess) return CS_ERR_CUDA;
+  void* args[] = {&P};
+  if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
+}
+
+int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                    const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride, uint32_t* gop_state,
+                    float* score, int32_t* kept_count, unsigned long long* counters, int32_t* status,
+                    cudaStream_t stream) {
+  return launch_score(g, n_streams, n_frames, mb, frame_type, keep_mask, frame_stride, gop_state, score, kept_count,
+                      counters, status, nullptr, stream);
+}
+
+size_t cs_score_compact_workspace_bytes(int32_t n_streams) {
+  return n_streams < 0 ? 0 : 8u + 8u * static_cast<size_t>(n_streams);
+}
+
+int cs_launch_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                            const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
+                            uint32_t* gop_state, float* score, int32_t* kept_count, const int32_t* frame_index,
+                            const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
+                            int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, void* workspace,
+                            unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+  ScoreParams F{};
+  F.fused = 1;
+  F.layout = frame_layout;
+  F.patch = g->patch;
+  F.FW = g->grid_w * g->patch;
+  F.FH = g->grid_h * g->patch;
+  F.ngc = g->grid_w / g->group;
+  const long long group_bytes = 3ll * g->patch * g->patch * 2ll * g->group * g->group;
+  F.vec_out = ((reinterpret_cast<uintptr_t>(packed) & 15u) == 0 && group_bytes % 16 == 0) ? 1 : 0;
+  F.capacity = capacity;
+  F.frame_index = frame_index;
+  F.frames = frames;
+  F.packed = static_cast<uint16_t*>(packed);
+  F.pos_ids = pos_ids;
+  F.src_index = src_index;
+  F.frame_offsets = frame_offsets;
+  F.ws_ctr = static_cast<unsigned*>(workspace);
+  F.ws_flags = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(workspace) + 8);
+  return launch_score(g, n_streams, n_frames, mb, frame_type, keep_mask, frame_stride, gop_state, score, kept_count,
+                      counters, status, &F, stream);
 }

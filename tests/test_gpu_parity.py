@@ -255,6 +255,114 @@ def test_compact_generic_geometries(abi, ref, geom, layout):
 
 
 # ------------------------------------------------------------------------------------------------------------
+# score_compact (NEXT-2: scoring + compaction fused, decoupled look-back)
+# ------------------------------------------------------------------------------------------------------------
+def run_score_compact_both(abi, ref, g, mb, types, frames, capacity, layout=0, gop_h=None, frame_stride=None,
+                           want_score=True, ws=None, check=True):
+    S, n = mb.shape[:2]
+    nw = abi.grid_words(g)
+    p = g["patch"]
+    fs = n if frame_stride is None else frame_stride
+    gop_h = np.zeros((S, nw + 1), np.uint32) if gop_h is None else gop_h
+    gs_d = torch.from_numpy(gop_h.view(np.int32).copy()).to(DEV)
+    km_d = torch.zeros(S, fs, nw, dtype=torch.int32, device=DEV)
+    sc_d = torch.zeros(S, n, g["grid_w"] * g["grid_h"], dtype=torch.float32, device=DEV) if want_score else None
+    kc_d = torch.zeros(S, n, dtype=torch.int32, device=DEV)
+    cnt_d = torch.zeros(16, dtype=torch.int64, device=DEV)
+    st_d = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ty_d = torch.from_numpy(np.ascontiguousarray(types, dtype=np.uint8)).to(DEV)
+    fr_h = [to_grouped(f, g) for f in frames] if layout == 1 else frames
+    fr_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in fr_h]
+    fptr = abi.ptr_array(fr_d, DEV)
+    fidx = np.tile(np.arange(7, 7 + n, dtype=np.int32), S)
+    fi_d = torch.from_numpy(fidx).to(DEV)
+    cap = max(capacity, 1)
+    packed = torch.full((cap, 3 * p * p), -1, dtype=torch.int16, device=DEV)
+    pos = torch.full((cap, 3), -7, dtype=torch.int32, device=DEV)
+    src = torch.full((cap,), -7, dtype=torch.int32, device=DEV)
+    offs = torch.full((S * n + 1,), -5, dtype=torch.int32, device=DEV)
+    if ws is None:
+        ws = torch.zeros(abi.score_compact_workspace_size(S), dtype=torch.uint8, device=DEV)
+    abi.codecsight_score_compact(g, S, n, d_mb(mb), ty_d, km_d, fs, gs_d, sc_d, kc_d, fi_d, fptr, capacity, packed,
+                                 pos, src, offs, ws, cnt_d, st_d, frame_layout=layout)
+    so = ref.score_patches(g, mb, types, gop_h, frame_stride=fs, want_score=want_score)
+    co = ref.compact(g, so["keep_mask"], fidx, fr_h, capacity, S, n, mask_frame_stride=fs, frame_layout=layout,
+                     counters=so["counters"].copy())
+    torch.cuda.synchronize()
+    gpu = dict(keep_mask=u32(km_d), kept_count=kc_d.cpu().numpy(), score=None if sc_d is None else sc_d.cpu().numpy(),
+               gop_state=u32(gs_d), counters=cnt_d.cpu().numpy().view(np.uint64), status=int(st_d.item()))
+    so["gop_state"] = gop_h
+    so["counters"] = co["counters"]
+    so["status"] = so["status"] | co["status"]
+    assert_score_equal(gpu, so, n, fs)
+    rows = min(int(co["frame_offsets"][-1]), capacity)
+    assert (offs.cpu().numpy() == co["frame_offsets"]).all()
+    assert (packed.cpu().numpy().view(np.uint16)[:rows] == co["packed"][:rows]).all()
+    assert (pos.cpu().numpy()[:rows] == co["pos_ids"][:rows]).all()
+    assert (src.cpu().numpy()[:rows] == co["src_index"][:rows]).all()
+    if rows < cap:
+        assert (src.cpu().numpy()[rows:] == -7).all()
+    assert (ws.cpu().numpy() == 0).all()            # the call leaves its workspace zeroed
+    return co
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("cfg_name,S,n", [("C1", 3, 8), ("C2", 32, 4), ("C4", 16, 4), ("C4", 3, 16), ("C1", 2, 20)])
+def test_score_compact_configs(abi, ref, cfg_name, S, n, layout):
+    cfg = synth.CONFIGS[cfg_name]
+    sw, sh = cfg["src"]
+    g = make_grid(sw, sh)
+    mb = np.stack([synth.stream_metadata(sw, sh, synth.scene_of(cfg, s), synth.stream_seed(cfg, s, 5), n)
+                   for s in range(S)])
+    types = np.stack([synth.frame_types(n, cfg["gop"], 3) for _ in range(S)])
+    rng = np.random.default_rng(21)
+    base = synth.random_frames(8, 448, 448, rng)
+    frames = [base[i % 8] for i in range(S * n)]
+    co = run_score_compact_both(abi, ref, g, mb, types, frames, S * n * 1024, layout)
+    total = int(co["frame_offsets"][-1])
+    # capacity truncation mid-group, want_score off, ring stride
+    run_score_compact_both(abi, ref, g, mb, types, frames, total // 2 + 1, layout, want_score=False)
+    ty_r = np.zeros((S, n + 3), np.uint8)
+    ty_r[:, :n] = types
+    run_score_compact_both(abi, ref, g, mb, ty_r, frames, total, layout, frame_stride=n + 3)
+
+
+@pytest.mark.parametrize("geom", [(64, 48, 16, 8, 6, 2, 4), (30, 30, 8, 6, 6, 3, 6), (100, 44, 16, 8, 8, 4, 8),
+                                  (72, 40, 8, 12, 10, 2, 3)])
+def test_score_compact_generic(abi, ref, geom):
+    sw, sh, m, gw, gh, G, p = geom
+    g = make_grid(sw, sh, mb_size=m, grid_w=gw, grid_h=gh, group=G, patch=p)
+    rng = np.random.default_rng(23)
+    S, n = 5, 3
+    mb = np.stack([np.stack([synth.random_mb(g["mb_rows"], g["mb_cols"], rng) for _ in range(n)])
+                   for _ in range(S)])
+    types = rng.integers(0, 2, size=(S, n)).astype(np.uint8)
+    frames = [rng.integers(0, 65536, size=(3, gh * p, gw * p), dtype=np.uint16) for _ in range(S * n)]
+    for layout in (0, 1):
+        run_score_compact_both(abi, ref, g, mb, types, frames, S * n * gw * gh, layout)
+
+
+def test_score_compact_many_streams_workspace_reuse(abi, ref):
+    """300 streams (several waves of clusters, long look-back chains), the same workspace over 3 calls with the
+    GOP state carried."""
+    cfg = synth.CONFIGS["C4"]
+    g = make_grid(1920, 1080)
+    S, n = 300, 2
+    nw = 32
+    ws = torch.zeros(abi.score_compact_workspace_size(S), dtype=torch.uint8, device=DEV)
+    gens = [synth.StreamGen(1920, 1080, synth.scene_of(cfg, i), synth.stream_seed(cfg, i)) for i in range(S)]
+    rng = np.random.default_rng(4)
+    base = synth.random_frames(4, 448, 448, rng)
+    frames = [base[i % 4] for i in range(S * n)]
+    gop_h = np.zeros((S, nw + 1), np.uint32)
+    for call in range(3):
+        mb = np.stack([np.stack([gn.next_frame() for _ in range(n)]) for gn in gens])
+        types = np.stack([synth.frame_types(n, 16, call * n)] * S)
+        # gop_h is uploaded, then advanced in place by the oracle: the state carries into the next call
+        run_score_compact_both(abi, ref, g, mb, types, frames, S * n * 1024, 1, gop_h=gop_h, want_score=False, ws=ws)
+
+
+# ------------------------------------------------------------------------------------------------------------
 # compact_tp (NEXT-3 temporal patches)
 # ------------------------------------------------------------------------------------------------------------
 def run_compact_tp_both(abi, ref, g, tp, keep_mask, unit_index, frames, capacity, S, nu, mfs, layout=0,
