@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--overlap", action="store_true",
                     help="run compact and kv_refresh on side streams concurrently with the next step's scoring "
                          "(measured: no gain -- kv_refresh already saturates HBM and holds every SM; default off)")
+    ap.add_argument("--fused", action="store_true",
+                    help="one codecsight_score_compact launch per step instead of score_patches + compact (NEXT-2)")
     ap.add_argument("--temporal-patch", type=int, default=1, choices=[1, 2],
                     help="frames per visual token (Qwen2-VL video: 2; NEXT-3); KV refresh over token units")
     ap.add_argument("--kv-mode", default="paged", choices=["paged", "copy"],
@@ -309,7 +311,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     pre = dict(src_w=sw, src_h=sh, y_pitch=sw, uv_pitch=sw) if args.frames == "nv12" else None
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
                     kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre, overlap=args.overlap,
-                    temporal_patch=args.temporal_patch)
+                    temporal_patch=args.temporal_patch, fused=args.fused)
     tp = args.temporal_patch
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
@@ -539,11 +541,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     kv_bytes_launch = float(dcnt[abi.CNT_BYTES_KV].item()) / K
     peak, peak_kind = measured_peak_hbm()
     achieved = kv_bytes_launch / (kv_ms / 1e3) / 1e9 if kvb else 0.0
-    cmp_ms = float(np.mean(per["compact"]))
-    cmp_bytes = float(dcnt[abi.CNT_BYTES_COMPACT].item()) / K
-    cmp_gbs = cmp_bytes / (cmp_ms / 1e3) / 1e9
     sc_ms = float(np.mean(per["score"]))
     sc_bytes = float(dcnt[abi.CNT_BYTES_SCORE].item()) / K
+    cmp_bytes = float(dcnt[abi.CNT_BYTES_COMPACT].item()) / K
+    if args.fused:   # one launch does both: its time and the bytes of both calls
+        cmp_ms = sc_ms
+        cmp_bytes += sc_bytes
+    else:
+        cmp_ms = float(np.mean(per["compact"]))
+    cmp_gbs = cmp_bytes / (cmp_ms / 1e3) / 1e9
     kept_frac = float(dcnt[abi.CNT_KEPT].item()) / max(1.0, float(dcnt[abi.CNT_PATCHES].item()))
     out = {
         "metric": "codec-pruned frames/sec (whole hot path: score+compact+kv_refresh), all GPUs",
@@ -554,14 +560,16 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": 0.25, "alpha": 0.0,
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
-                   "frames": args.frames, "overlap": args.overlap, "temporal_patch": tp,
+                   "frames": args.frames, "overlap": args.overlap, "temporal_patch": tp, "fused": args.fused,
                    "parallelism": f"stream-shard x{world}",
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
                          "see per-step bytes)"},
         "streams_per_sec": stream_steps,
         "kv_refresh_gbs": achieved,
-        "per_kernel_ms": {"score_patches": sc_ms, "compact": cmp_ms, "kv_refresh": kv_ms},
-        "per_kernel_gbs": {"score_patches": sc_bytes / (sc_ms / 1e3) / 1e9, "compact": cmp_gbs,
+        "per_kernel_ms": ({"score_compact": sc_ms, "kv_refresh": kv_ms} if args.fused else
+                          {"score_patches": sc_ms, "compact": cmp_ms, "kv_refresh": kv_ms}),
+        "per_kernel_gbs": {"score_patches" if not args.fused else "score_compact":
+                           (sc_bytes if not args.fused else cmp_bytes) / (sc_ms / 1e3) / 1e9, "compact": cmp_gbs,
                            "kv_refresh": achieved},
         "frame_layout": args.frame_layout,
         "compact_by_layout": layouts,
@@ -578,7 +586,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                       "frac": achieved / peak,
                       "traffic": ncu_traffic("kv_refresh_paged" if args.kv_mode == "paged" else "kv_refresh_copy"),
                       "algorithmic_bytes_per_launch": kv_bytes_launch} if kvb else
-                     {"bound": "hbm", "kernel": "codecsight_compact (compact_scan + compact_gather)",
+                     {"bound": "hbm", "kernel": ("codecsight_score_compact (score_kernel<fused>)" if args.fused else
+                                                 "codecsight_compact (compact_scan + compact_gather)"),
                       "achieved": cmp_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                       "frac": cmp_gbs / peak, "traffic": ncu_traffic("compact_gather"),
                       "algorithmic_bytes_per_launch": cmp_bytes}),

@@ -441,25 +441,39 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       }
       s_lp[P.n_frames] = acc;
       s_written = 0;
-      if (rank == 0) {
-        const unsigned long long tot = static_cast<unsigned long long>(acc);
-        unsigned long long excl = 0;
-        if (sidx == 0) {
-          st_release_u64(&P.ws_flags[0], kFlagPre | tot);
-        } else {
-          st_release_u64(&P.ws_flags[sidx], kFlagAgg | tot);
-          for (int j = sidx - 1; j >= 0;) {
-            const unsigned long long v = ld_acquire_u64(&P.ws_flags[j]);
-            if ((v & ~kFlagVal) == 0ull) continue;  // stream j not counted yet
-            excl += v & kFlagVal;
-            if ((v & ~kFlagVal) == kFlagPre) break;
-            --j;
-          }
-          st_release_u64(&P.ws_flags[sidx], kFlagPre | (excl + tot));
+    }
+    __syncthreads();
+    if (rank == 0 && tid < 32) {
+      // warp-parallel decoupled look-back: lane l inspects stream (j - l); the closest PREFIX flag ends the walk
+      const unsigned long long tot = static_cast<unsigned long long>(s_lp[P.n_frames]);
+      unsigned long long excl = 0;
+      if (sidx == 0) {
+        if (lane == 0) st_release_u64(&P.ws_flags[0], kFlagPre | tot);
+      } else {
+        if (lane == 0) st_release_u64(&P.ws_flags[sidx], kFlagAgg | tot);
+        int j = sidx - 1;
+        while (true) {
+          const int jj = j - lane;
+          unsigned long long v = jj >= 0 ? ld_acquire_u64(&P.ws_flags[jj]) : kFlagPre;  // before stream 0: prefix 0
+          const uint32_t pre_mask = __ballot_sync(0xffffffffu, (v & ~kFlagVal) == kFlagPre);
+          const uint32_t bad_mask = __ballot_sync(0xffffffffu, (v & ~kFlagVal) == 0ull);
+          const int stop = pre_mask ? __ffs(pre_mask) - 1 : 32;  // lanes [0, stop] are summed (stop: the prefix)
+          const uint32_t need = stop >= 31 ? 0xffffffffu : ((2u << stop) - 1u);
+          if (bad_mask & need) continue;  // a stream in the window has not published yet: re-read
+          unsigned long long add = (lane <= stop && jj >= 0) ? (v & kFlagVal) : 0ull;
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) add += __shfl_xor_sync(0xffffffffu, add, d);
+          excl += add;
+          if (pre_mask) break;
+          j -= 32;
         }
+        if (lane == 0) st_release_u64(&P.ws_flags[sidx], kFlagPre | (excl + tot));
+      }
+      if (lane == 0) {
         s_prefix = static_cast<long long>(excl);
         if (static_cast<long long>(excl + tot) > P.capacity) cs::atomic_or_status(P.status, CS_STATUS_CAPACITY);
-        if (sidx == P.n_streams - 1) P.frame_offsets[(long long)P.n_streams * P.n_frames] = static_cast<int32_t>(excl + tot);
+        if (sidx == P.n_streams - 1)
+          P.frame_offsets[(long long)P.n_streams * P.n_frames] = static_cast<int32_t>(excl + tot);
       }
     }
     cluster.sync();

@@ -28,8 +28,13 @@ class Pipeline:
                  n_prompt: int = 0, device=None, want_score: bool = False, packed_capacity: int | None = None,
                  with_refreshed: bool = True, frame_layout: int = abi.CS_LAYOUT_PLANAR, kv_mode: str = "copy",
                  compact_chunk: int | None = None, preprocess: dict | None = None, overlap: bool = False,
-                 temporal_patch: int = 1):
+                 temporal_patch: int = 1, fused: bool = False):
         self.g = dict(grid)
+        # fused: one codecsight_score_compact launch per step (NEXT-2) instead of score_patches + compact
+        self.fused = fused
+        if fused:
+            assert temporal_patch == 1 and preprocess is None and not overlap, \
+                "fused score+compact: model frames, temporal_patch 1, no overlap mode"
         # temporal patches (NEXT-3, Qwen2-VL temporal_patch_size): a token unit = tp consecutive frames; scoring stays
         # per frame, compaction emits [3][tp][p][p] rows per unit (codecsight_compact_tp) and writes the unit masks /
         # types into a unit ring, and the KV refresh runs over units (window w/tp, stride s/tp)
@@ -68,7 +73,7 @@ class Pipeline:
         self.status = torch.zeros(1, dtype=torch.int32, device=d)
         # packed ViT input: enough rows for the first window (every patch kept)
         p = grid["patch"]
-        chunk = compact_chunk if compact_chunk is not None else window
+        chunk = compact_chunk if (compact_chunk is not None and not fused) else window
         self.capacity = packed_capacity if packed_capacity is not None else S * (chunk // tp) * self.np
         self._packed = [torch.empty(self.capacity, 3 * tp * p * p, dtype=torch.bfloat16, device=d)
                         for _ in range(nb)]
@@ -113,6 +118,8 @@ class Pipeline:
                       else abi.kv_workspace_size(self.kv, win1, S))
             self.workspace = torch.empty((nbytes + 15) // 16 * 16, dtype=torch.uint8, device=d)
         self.cur = 0  # which cache set holds window k-1
+        if fused:
+            self.sc_workspace = torch.zeros(abi.score_compact_workspace_size(S), dtype=torch.uint8, device=d)
         self._side_done = {}  # step -> events closing its compact / kv_refresh work (overlap mode)
         if overlap:
             self.stream_compact = torch.cuda.Stream(d)
@@ -169,18 +176,30 @@ class Pipeline:
             if types is not None:
                 self.type_ring[:, off:off + n].copy_(types, non_blocking=True)
             s0 = ev(main)
-            abi.codecsight_score_patches(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:],
-                                         self.ring, self.gop_state, None if self.score is None else self.score[:, :n],
-                                         self.kept_count[:, :n], self.counters, self.status, main)
+            if self.fused:
+                fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
+                abi.codecsight_score_compact(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:],
+                                             self.ring, self.gop_state,
+                                             None if self.score is None else self.score[:, :n],
+                                             self.kept_count[:, :n], fi, frame_ptrs, self.capacity, self.packed,
+                                             self.pos_ids, self.src_index, self.frame_offsets[: self.S * n + 1],
+                                             self.sc_workspace, self.counters, self.status,
+                                             frame_layout=self.frame_layout, stream=main)
+            else:
+                abi.codecsight_score_patches(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:],
+                                             self.ring, self.gop_state,
+                                             None if self.score is None else self.score[:, :n],
+                                             self.kept_count[:, :n], self.counters, self.status, main)
             out["score"] = (s0, ev(main))
         cs_stream = self.stream_compact if self.overlap else main
         kv_stream = self.stream_kv if self.overlap else main
         if self.overlap:
             cs_stream.wait_event(out["score"][1])
-        with torch.cuda.stream(cs_stream):
-            c0 = ev(cs_stream)
-            self.compact(k, n, off, frame_ptrs, frame_index, cs_stream)
-            out["compact"] = (c0, ev(cs_stream))
+        if not self.fused:
+            with torch.cuda.stream(cs_stream):
+                c0 = ev(cs_stream)
+                self.compact(k, n, off, frame_ptrs, frame_index, cs_stream)
+                out["compact"] = (c0, ev(cs_stream))
         if self.kv is not None and do_kv:
             if self.overlap:
                 kv_stream.wait_event(out["score"][1])
@@ -257,7 +276,7 @@ class Pipeline:
         """Kernels of this library launched by one step (score 1, compact 2 per chunk, kv_refresh 3)."""
         _, nf = self.new_frames(k)
         c = nf if self.compact_chunk is None else min(nf, self.compact_chunk)
-        n = 1 + 2 * ((nf + c - 1) // c)
+        n = 1 if self.fused else 1 + 2 * ((nf + c - 1) // c)
         if self.kv is not None:
             n += 3
         return n
