@@ -47,8 +47,9 @@ def parse():
     ap.add_argument("--overlap", action="store_true",
                     help="run compact and kv_refresh on side streams concurrently with the next step's scoring "
                          "(measured: no gain -- kv_refresh already saturates HBM and holds every SM; default off)")
-    ap.add_argument("--fused", action="store_true",
-                    help="one codecsight_score_compact launch per step instead of score_patches + compact (NEXT-2)")
+    ap.add_argument("--fused", action=argparse.BooleanOptionalAction, default=True,
+                    help="one codecsight_score_compact launch per step (NEXT-2, default) instead of score_patches + "
+                         "compact (--no-fused)")
     ap.add_argument("--temporal-patch", type=int, default=1, choices=[1, 2],
                     help="frames per visual token (Qwen2-VL video: 2; NEXT-3); KV refresh over token units")
     ap.add_argument("--kv-mode", default="paged", choices=["paged", "copy"],
@@ -617,6 +618,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = workload(args.workload, args.streams, args.kv_mode)
+    # the fused score+compact kernel takes model frames, one frame per token, no overlap mode
+    args.fused = bool(args.fused and args.frames == "model" and args.temporal_patch == 1 and not args.overlap)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

@@ -27,8 +27,10 @@ def to_grouped(frame, g):
     return np.ascontiguousarray(x.transpose(1, 4, 2, 5, 0, 3, 6)).reshape(-1)
 
 
-@pytest.mark.parametrize("cfg_name,S,steps,sample", [("C4", 256, 3, [0, 1, 254, 255]), ("C5", 128, 2, [0, 127])])
-def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample):
+@pytest.mark.parametrize("cfg_name,S,steps,sample,fused", [("C4", 256, 3, [0, 1, 254, 255], False),
+                                                          ("C4", 256, 3, [0, 1, 254, 255], True),
+                                                          ("C5", 128, 2, [0, 127], False)])
+def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused):
     import gc
     gc.collect()
     torch.cuda.empty_cache()
@@ -41,7 +43,7 @@ def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample):
     ring = w + s
     kvb = cfg["kv"]
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=DEV,
-                    frame_layout=abi.CS_LAYOUT_GROUPED, kv_mode="paged", compact_chunk=s)
+                    frame_layout=abi.CS_LAYOUT_GROUPED, kv_mode="paged", compact_chunk=s, fused=fused)
     gen = torch.Generator(device=DEV)
     gen.manual_seed(11)
     pipe.init_cache_fill(gen)
@@ -103,7 +105,7 @@ def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample):
             assert np.abs(fa - fb).max() <= 1e-2                   # keys: rotated within the bf16 bound
             h["slot"] = ko["slot_new"]
         # compaction of the last chunk (the packed buffer holds the last s frames of the step)
-        last0 = n - min(n, s)
+        last0 = 0 if fused else n - min(n, s)   # fused: one compaction of all the step's frames
         nl = n - last0
         offs = pipe.frame_offsets[:S * nl + 1].cpu().numpy()
         src_d = pipe.src_index.cpu().numpy()
