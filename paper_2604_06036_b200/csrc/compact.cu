@@ -21,6 +21,7 @@ constexpr int kGatherThreads = 256;
 constexpr int kWarpsPerCta = kGatherThreads / 32;
 
 constexpr int kLayoutNV12 = 2;  // internal: frames are decoded NV12 planes, preprocessing fused (NEXT-2)
+constexpr float kInv255 = 1.0f / 255.0f;  // RN(1/255)
 
 // per-warp tile of one group in packed order: 3 x tp x (group*patch)^2 bf16, padded to 16 B
 __host__ __device__ __forceinline__ int tile_bytes_of(int p, int G, int tp = 1) {
@@ -321,7 +322,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     const uint8_t* UVp = static_cast<const uint8_t*>(P.uv_planes[slot]);
     // batches of 4 output pixels per lane: the 4 x (4 luma bytes + 4 chroma pairs) loads of a batch are all
     // issued before any is consumed (memory-level parallelism), then converted, interpolated and normalised
-    constexpr int kB = 4;
+    constexpr int kB = TP > 0 ? 1 : 4;
     const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
     for (int e0 = 0; e0 < gp * gp; e0 += 32 * kB) {
       uint32_t yv[kB][4], uvv[kB][4];
@@ -367,7 +368,10 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
           const float top = __fadd_rn(__fmul_rn(hx, rgb[0][c]), __fmul_rn(lx, rgb[1][c]));
           const float bot = __fadd_rn(__fmul_rn(hx, rgb[2][c]), __fmul_rn(lx, rgb[3][c]));
           const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
-          const float t = __fdiv_rn(v, 255.0f);
+          // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
+          // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
+          const float q255 = __fmul_rn(v, kInv255);
+          const float t = __fmaf_rn(__fmaf_rn(-q255, 255.0f, v), kInv255, q255);
           const float o = __fdiv_rn(__fsub_rn(t, P.mean[c]), P.stdv[c]);
           tile[((dy * G + dx) * 3 + c) * pp + y * p + x] = static_cast<uint16_t>(cs::f32_to_bf16_rne(o));
         }
@@ -454,7 +458,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
 }
 
 template <int TP, int TG, int LAYOUT, int TT>
-__global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED && TP > 0) ? 4 : 2)
+__global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED && TP > 0) ? 4 : (LAYOUT == kLayoutNV12 && TP > 0) ? 5 : 2)
     compact_gather(const __grid_constant__ CompactParams P) {
   extern __shared__ __align__(16) unsigned char g_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -589,7 +593,7 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
   const size_t smem =
       (size_t)kWarpsPerCta * ((grouped ? 0 : tile_bytes_of(g->patch, g->group, tp)) + 4 * P.nw);
   const bool fast = g->patch == 14 && g->group == 2 && (tp == 1 || tp == 2);
-  const int grid = cs_num_sms() * (grouped ? 8 : 4);
+  const int grid = cs_num_sms() * (grouped ? 8 : (nv12 && fast) ? 5 : 4);  // resident CTAs per SM
   const void* fn;
   int slot;
 #define CS_PICK(TP, TG, LY, TT, SL) \
