@@ -12,6 +12,8 @@
 //                   memory tile laid out in packed order, and writes the tile out with coalesced 16-byte stores
 //                   (a 2x2 group of 14-px patches = 4,704 B = 294 x 16 B, so every group starts 16-B aligned).
 // Pixels of pruned patches are never read.
+#include <cstdlib>
+
 #include "cs_internal.cuh"
 
 namespace {
@@ -526,6 +528,156 @@ __global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED &
   }
 }
 
+// ---- grouped frames, 2x2 groups of 14-px patches on a 32-wide grid: TMA bulk copies ------------------------
+// A kept group is one contiguous 4,704-B block of the frame and of the packed output (16-B aligned): each warp is
+// an independent TMA ring (lane 0 drives it, like kv_gather_tma): cp.async.bulk global -> smem completes on the
+// stage's mbarrier, cp.async.bulk smem -> global (bulk_group) writes the packed rows, and the stage is refilled once
+// wait_group.read says the store has read it.  Groups that cannot take the bulk path (a capacity-truncated group, a
+// misaligned frame) are copied by the warp with ordinary loads/stores in the same order.
+constexpr int kTmaWarps = kWarpsPerCta;
+constexpr int kTmaMaxStages = 8;
+constexpr unsigned kTmaGroupBytes = 4704u;  // 4 patches x 3 x 14 x 14 bf16
+constexpr unsigned kTmaStageAlloc = 4736u;  // rounded up to 128 B
+
+struct TmaGroup {
+  long long n0;     // first packed row
+  int slot;         // frame slot
+  int gi;           // group index gr * ngc + gc
+  int t_index;      // pos id t
+  int kind;         // 0 bulk, 1 direct (warp copy), -1 end of work
+  const uint16_t* src;
+};
+
+__global__ void __launch_bounds__(kGatherThreads, 1) compact_gather_tma(const __grid_constant__ CompactParams P,
+                                                                        int nst) {
+  extern __shared__ __align__(128) unsigned char t_smem[];
+  __shared__ TmaGroup s_desc[kTmaWarps][kTmaMaxStages];
+  __shared__ __align__(8) uint64_t s_full[kTmaWarps][kTmaMaxStages];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* stages = t_smem + (size_t)wib * nst * kTmaStageAlloc;
+  uint64_t* full = s_full[wib];
+  TmaGroup* desc = s_desc[wib];
+  const long long total_groups = static_cast<long long>(__ldg(P.frame_offsets + P.n_slots)) / 4;
+  const long long nwarps = static_cast<long long>(gridDim.x) * kTmaWarps;
+  const long long wid = static_cast<long long>(blockIdx.x) * kTmaWarps + wib;
+  long long q = total_groups * wid / nwarps;
+  const long long q1 = total_groups * (wid + 1) / nwarps;
+  if (q >= q1) return;  // the warp's range is empty (no block-wide synchronisation below)
+  constexpr int kNgr = 16;  // group rows of a 32 x 32 patch grid
+  const long long row_el = 3ll * 14 * 14;
+
+  // ---- generator state (lane 0): current slot, group row, remaining kept-group bits of that row -------------
+  int slot = 0, gr = 0, t_index = 0;
+  uint32_t ybits = 0u;
+  const uint16_t* frame = nullptr;
+  bool aligned = false;
+  auto load_row = [&]() {
+    const uint32_t* m = slot_mask(P, slot);
+    const uint32_t x = __ldg(m + 2 * gr) | __ldg(m + 2 * gr + 1);
+    ybits = (x | (x >> 1)) & 0x55555555u;  // bit 2*gc set iff group (gr, gc) is kept
+  };
+  auto load_slot = [&]() {
+    frame = static_cast<const uint16_t*>(P.frames[slot]);
+    t_index = __ldg(P.frame_index + slot);
+    aligned = (reinterpret_cast<uintptr_t>(frame) & 15u) == 0;
+  };
+  bool more = true;
+  if (lane == 0) {
+    int lo = 0, hi = P.n_slots;  // largest slot with frame_offsets[slot] <= q * 4
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (static_cast<long long>(__ldg(P.frame_offsets + mid)) <= q * 4) lo = mid; else hi = mid;
+    }
+    slot = lo;
+    long long skip = q - __ldg(P.frame_offsets + slot) / 4;
+    load_slot();
+    load_row();
+    while (skip >= __popc(ybits)) {
+      skip -= __popc(ybits);
+      ++gr;  // stays inside the slot: the slot holds more than `skip` kept groups
+      load_row();
+    }
+    for (; skip > 0; --skip) ybits &= ybits - 1u;
+    for (int st = 0; st < nst; ++st) cs::mbar_init(&full[st], 1);
+    cs::fence_mbar_init();
+  }
+  __syncwarp();
+
+  auto issue = [&](int st) {  // lane 0: next kept group of the range into stage st
+    TmaGroup d;
+    if (q >= q1) {
+      d.kind = -1;
+      desc[st] = d;
+      cs::mbar_arrive(&full[st]);
+      more = false;
+      return;
+    }
+    while (ybits == 0u) {
+      if (++gr == kNgr) {
+        gr = 0;
+        ++slot;
+        load_slot();
+      }
+      load_row();
+    }
+    const int b = __ffs(ybits) - 1;
+    ybits &= ybits - 1u;
+    d.n0 = q * 4;
+    d.slot = slot;
+    d.gi = gr * 16 + (b >> 1);
+    d.t_index = t_index;
+    d.src = frame + (long long)d.gi * 4 * row_el;
+    ++q;
+    if (d.n0 + 4 <= P.capacity && aligned) {
+      d.kind = 0;
+      desc[st] = d;
+      cs::mbar_arrive_expect_tx(&full[st], kTmaGroupBytes);
+      cs::bulk_g2s(stages + (size_t)st * kTmaStageAlloc, d.src, kTmaGroupBytes, &full[st]);
+    } else {
+      d.kind = d.n0 < P.capacity ? 1 : 2;  // 2: entirely beyond the capacity, nothing to write
+      desc[st] = d;
+      cs::mbar_arrive(&full[st]);
+    }
+  };
+  if (lane == 0)
+    for (int st = 0; st < nst && more; ++st) issue(st);
+
+  for (int it = 0;; ++it) {
+    const int st = it % nst;
+    cs::mbar_wait(&full[st], (it / nst) & 1);
+    const TmaGroup d = desc[st];
+    if (d.kind < 0) break;
+    long long nvalid = P.capacity - d.n0;
+    nvalid = nvalid < 0 ? 0 : (nvalid > 4 ? 4 : nvalid);
+    if (d.kind == 0) {
+      if (lane == 0) cs::bulk_s2g(P.packed + d.n0 * row_el, stages + (size_t)st * kTmaStageAlloc, kTmaGroupBytes);
+    } else if (d.kind == 1) {
+      uint16_t* dst = P.packed + d.n0 * row_el;
+      const int nel = static_cast<int>(nvalid * row_el);
+      for (int e = lane; e < nel; e += 32) dst[e] = d.src[e];
+    }
+    if (lane < nvalid) {
+      const int gr_ = d.gi >> 4, gc_ = d.gi & 15;
+      const int h = gr_ * 2 + (lane >> 1), w = gc_ * 2 + (lane & 1);
+      const long long n = d.n0 + lane;
+      P.pos_ids[3 * n + 0] = d.t_index;
+      P.pos_ids[3 * n + 1] = h;
+      P.pos_ids[3 * n + 2] = w;
+      P.src_index[n] = d.slot * P.np + h * 32 + w;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      cs::bulk_commit();  // one (possibly empty) bulk group per consumed stage keeps the group count aligned
+      if (it >= 1 && more) {
+        cs::bulk_wait_read<1>();  // the store of item it-1 has read its stage
+        issue((it - 1) % nst);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) cs::bulk_wait_all<0>();
+}
+
 }  // namespace
 
 static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp, int32_t n_streams,
@@ -617,6 +769,21 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
     }
   }
 #undef CS_PICK
+  if (grouped && tp == 1 && fast && g->grid_w == 32 && g->grid_h % 2 == 0 && g->grid_h == 32 && P.vec_out) {
+    static const int use_tma = [] {
+      const char* e = getenv("CS_COMPACT_TMA");
+      return e ? atoi(e) : 1;
+    }();
+    if (use_tma) {
+      const int nst = 5;
+      const size_t tsmem = (size_t)kTmaWarps * nst * kTmaStageAlloc;
+      const void* tf = reinterpret_cast<const void*>(compact_gather_tma);
+      if (cs_set_smem_attr(tf, 20, 200 * 1024)) return CS_ERR_CUDA;  // + 2.5 KB static <= 227 KB
+      compact_gather_tma<<<cs_num_sms(), kGatherThreads, tsmem, stream>>>(P, nst);
+      if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+      return CS_OK;
+    }
+  }
   if (cs_set_smem_attr(fn, slot, 227 * 1024)) return CS_ERR_CUDA;
   void* args[] = {&P};
   if (cudaLaunchKernel(fn, dim3(grid), dim3(kGatherThreads), args, smem, stream) != cudaSuccess) return CS_ERR_CUDA;
