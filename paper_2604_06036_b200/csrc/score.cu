@@ -62,8 +62,10 @@ struct ScoreParams {
   unsigned* ws_ctr;              // [0] ticket, [1] CTAs done
   unsigned long long* ws_flags;  // [n_streams] look-back words: (state << 62) | rows, state 1 = aggregate, 2 = prefix
   unsigned total_ctas;
+  int tma_stages;  // 4,736-B TMA stages that fit the score's staging memory (fused compaction ring)
 };
 
+constexpr int kFusedMaxStages = 16;
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kFlagVal = (1ull << 62) - 1;
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -482,22 +484,16 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       P.frame_offsets[(long long)sidx * P.n_frames + f] = static_cast<int32_t>(pre + s_lp[f]);
     const int gs2 = P.G * P.G;
     const long long groups = s_lp[P.n_frames] / gs2;
-    const long long nwarp_c = static_cast<long long>(P.cluster) * (nthr >> 5);
-    const long long wid = static_cast<long long>(rank) * (nthr >> 5) + (tid >> 5);
-    long long q = groups * wid / nwarp_c;
-    const long long q1 = groups * (wid + 1) / nwarp_c;
-    int written = 0;
-    if (q < q1) {
+    const int ngroups = (P.grid_h / P.G) * P.ngc;
+    // enumerate, for one warp, the stream's kept groups q in [q, q1) in packed order and call fn on each
+    auto for_each_group = [&](long long q, long long q1, auto&& fn) {
+      if (q >= q1) return;
       int f = 0;
       while (f + 1 < P.n_frames && s_lp[f + 1] / gs2 <= q) ++f;
       long long skip = q - s_lp[f] / gs2;
-      const int ngroups = (P.grid_h / P.G) * P.ngc;
       for (; f < P.n_frames && q < q1; ++f, skip = 0) {
         const long long slot = (long long)sidx * P.n_frames + f;
         const uint32_t* m = P.keep_mask + ((long long)sidx * P.frame_stride + f) * nw;
-        const uint16_t* fr = static_cast<const uint16_t*>(P.frames[slot]);
-        const int t_index = P.frame_index[slot];
-        const bool vec_in = ((reinterpret_cast<uintptr_t>(fr) & 15u) == 0) && ((3 * gs2 * P.patch * P.patch * 2) % 16 == 0);
         for (int base = 0; base < ngroups && q < q1; base += 32) {
           const int qq = base + lane;
           const bool kept = qq < ngroups && cs::group_kept(m, qq, P.ngc, P.G, P.grid_w);
@@ -515,14 +511,146 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
             const int b = __ffs(bal) - 1;
             bal &= bal - 1;
             const int gi = base + b;
-            const int gr = gi / P.ngc, gc = gi - gr * P.ngc;
-            written += fused_copy_group(P, fr, vec_in, gr, gc, pre + q * gs2, slot, t_index, lane);
+            fn(slot, gi / P.ngc, gi - (gi / P.ngc) * P.ngc, pre + q * gs2);
             ++q;
           }
         }
       }
+    };
+    int written = 0;
+    const bool tma = P.layout == CS_LAYOUT_GROUPED && P.vec_out && P.patch == 14 && P.G == 2 && P.grid_w == 32 &&
+                     P.grid_h == 32 && P.tma_stages >= 12;  // >= 3 stages per ring, else direct copies (measured)
+    if (tma) {
+      // the CTA's share of the stream's kept groups: thread 0 runs a TMA bulk ring over it (4,704-B groups,
+      // global -> smem on an mbarrier, smem -> global as a bulk group, the stage reused once the store has read
+      // it) in the score's staging memory, which is free now; warps 1.. write the position ids / source indices
+      const long long qa0 = groups * rank / P.cluster, qb0 = groups * (rank + 1) / P.cluster;
+      // R ring warps (lane 0 of each drives its own TMA ring over its own stages and share of the range)
+      const int R = min(4, P.tma_stages / 2);
+      const int wq = tid >> 5;
+      const long long qa = qa0 + (qb0 - qa0) * min(wq, R) / R, qb = qa0 + (qb0 - qa0) * min(wq + 1, R) / R;
+      __shared__ __align__(8) uint64_t s_tfull_all[kFusedMaxStages];
+      __shared__ long long s_tn0_all[kFusedMaxStages];
+      __shared__ const uint16_t* s_tsrc_all[kFusedMaxStages];
+      if (wq < R && lane == 0 && qa < qb) {
+        const int nst = P.tma_stages / R, sb = wq * nst;
+        uint64_t* s_tfull = s_tfull_all + sb;
+        long long* s_tn0 = s_tn0_all + sb;
+        const uint16_t** s_tsrc = s_tsrc_all + sb;
+        unsigned char* tbase = smem + (size_t)sb * 4736u;
+        const long long row_el = 3ll * 14 * 14;
+        for (int st = 0; st < nst; ++st) cs::mbar_init(&s_tfull[st], 1);
+        cs::fence_mbar_init();
+        cs::fence_proxy_async_smem();  // the staging memory was last used through the generic proxy
+        int f = 0;
+        while (f + 1 < P.n_frames && s_lp[f + 1] / 4 <= qa) ++f;
+        long long skip = qa - s_lp[f] / 4;
+        int gr = 0;
+        uint32_t ybits = 0u;
+        const uint16_t* fr = nullptr;
+        bool aligned = false;
+        auto load_row = [&]() {
+          const uint32_t* m = P.keep_mask + ((long long)sidx * P.frame_stride + f) * nw;
+          const uint32_t x = m[2 * gr] | m[2 * gr + 1];
+          ybits = (x | (x >> 1)) & 0x55555555u;
+        };
+        auto load_frame = [&]() {
+          fr = static_cast<const uint16_t*>(P.frames[(long long)sidx * P.n_frames + f]);
+          aligned = (reinterpret_cast<uintptr_t>(fr) & 15u) == 0;
+        };
+        load_frame();
+        load_row();
+        while (skip >= __popc(ybits)) {
+          skip -= __popc(ybits);
+          ++gr;
+          load_row();
+        }
+        for (; skip > 0; --skip) ybits &= ybits - 1u;
+        long long q = qa;
+        bool more = true;
+        auto issue = [&](int st) {
+          if (q >= qb) {
+            s_tn0[st] = -1;
+            cs::mbar_arrive(&s_tfull[st]);
+            more = false;
+            return;
+          }
+          while (ybits == 0u) {
+            if (++gr == 16) {
+              gr = 0;
+              ++f;
+              load_frame();
+            }
+            load_row();
+          }
+          const int b = __ffs(ybits) - 1;
+          ybits &= ybits - 1u;
+          const long long n0 = pre + q * 4;
+          const uint16_t* src = fr + (long long)(gr * 16 + (b >> 1)) * 4 * row_el;
+          ++q;
+          s_tn0[st] = n0;
+          s_tsrc[st] = src;
+          if (n0 + 4 <= P.capacity && aligned) {
+            cs::mbar_arrive_expect_tx(&s_tfull[st], 4704u);
+            cs::bulk_g2s(tbase + (size_t)st * 4736u, src, 4704u, &s_tfull[st]);
+          } else {
+            cs::mbar_arrive(&s_tfull[st]);  // copied directly below (truncated group / misaligned frame)
+          }
+        };
+        for (int st = 0; st < nst && more; ++st) issue(st);
+        for (int it = 0;; ++it) {
+          const int st = it % nst;
+          cs::mbar_wait(&s_tfull[st], (it / nst) & 1);
+          const long long n0 = s_tn0[st];
+          if (n0 < 0) break;
+          if (n0 + 4 <= P.capacity) {
+            if (s_tsrc[st] && (reinterpret_cast<uintptr_t>(s_tsrc[st]) & 15u) == 0) {
+              cs::bulk_s2g(P.packed + n0 * row_el, tbase + (size_t)st * 4736u, 4704u);
+            } else {
+              for (long long e = 0; e < 4 * row_el; ++e) P.packed[n0 * row_el + e] = s_tsrc[st][e];
+            }
+          } else if (n0 < P.capacity) {
+            for (long long e = 0; e < (P.capacity - n0) * row_el; ++e) P.packed[n0 * row_el + e] = s_tsrc[st][e];
+          }
+          cs::bulk_commit();  // one (possibly empty) bulk group per item
+          if (it >= 1 && more) {
+            cs::bulk_wait_read<1>();
+            issue((it - 1) % nst);
+          }
+        }
+        cs::bulk_wait_all<0>();
+      } else if (wq >= R && qa0 < qb0) {
+        const long long nw7 = (nthr >> 5) - R, w7 = wq - R;
+        for_each_group(qa0 + (qb0 - qa0) * w7 / nw7, qa0 + (qb0 - qa0) * (w7 + 1) / nw7,
+                       [&](long long slot, int gr, int gc, long long n0) {
+                         const int t_index = P.frame_index[slot];
+                         if (lane < 4 && n0 + lane < P.capacity) {
+                           const int h = gr * 2 + (lane >> 1), w = gc * 2 + (lane & 1);
+                           const long long n = n0 + lane;
+                           P.pos_ids[3 * n + 0] = t_index;
+                           P.pos_ids[3 * n + 1] = h;
+                           P.pos_ids[3 * n + 2] = w;
+                           P.src_index[n] = static_cast<int32_t>(slot * P.np + h * P.grid_w + w);
+                         }
+                       });
+      }
+      if (tid == 0) {
+        long long r = P.capacity - (pre + qa0 * 4);
+        r = r < 0 ? 0 : (r > (qb0 - qa0) * 4 ? (qb0 - qa0) * 4 : r);
+        written = static_cast<int>(r);
+      }
+    } else {
+      const long long nwarp_c = static_cast<long long>(P.cluster) * (nthr >> 5);
+      const long long wid = static_cast<long long>(rank) * (nthr >> 5) + (tid >> 5);
+      for_each_group(groups * wid / nwarp_c, groups * (wid + 1) / nwarp_c,
+                     [&](long long slot, int gr, int gc, long long n0) {
+                       const uint16_t* fr = static_cast<const uint16_t*>(P.frames[slot]);
+                       const bool vec_in = ((reinterpret_cast<uintptr_t>(fr) & 15u) == 0) &&
+                                           ((3 * gs2 * P.patch * P.patch * 2) % 16 == 0);
+                       written += fused_copy_group(P, fr, vec_in, gr, gc, n0, slot, P.frame_index[slot], lane);
+                     });
     }
-    if (lane == 0 && written) atomicAdd(&s_written, written);
+    if ((lane == 0 || tma) && written) atomicAdd(&s_written, written);
     __syncthreads();
     if (tid == 0) {
       const unsigned long long rows = static_cast<unsigned long long>(s_written);
@@ -611,6 +739,10 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
 
   if (smem > 200 * 1024) return CS_ERR_UNSUPPORTED;
   P.total_ctas = static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster);
+  {
+    const unsigned st = P.off_dyn / 4736u;
+    P.tma_stages = static_cast<int>(st > static_cast<unsigned>(kFusedMaxStages) ? kFusedMaxStages : st);
+  }
   const void* fn = P.fused ? reinterpret_cast<const void*>(score_kernel<true>)
                           : reinterpret_cast<const void*>(score_kernel<false>);
   if (cs_set_smem_attr(fn, P.fused ? 19 : 0, 200 * 1024) != 0) return CS_ERR_CUDA;
