@@ -508,6 +508,12 @@ int codecsight_ref_kv_refresh(const ref_grid* g, const ref_kv* kv, const ref_win
                 const int64_t e1 = h * D + i, e2 = h * D + i + D / 2;
                 const int64_t src = ((l * 2 + 0) * cap + po) * rowel, dst = ((l * 2 + 0) * cap + p_new) * rowel;
                 float x1, x2, o1, o2;
+                if (kv->rope_mode == REF_ROPE_MROPE && i >= kv->mrope_section[0]) {
+                  /* h / w sections: the token's (h, w) are unchanged -> the stored bits are kept (NEXT-3) */
+                  memcpy(nc + (dst + e1) * esz, oc + (src + e1) * esz, (size_t)esz);
+                  memcpy(nc + (dst + e2) * esz, oc + (src + e2) * esz, (size_t)esz);
+                  continue;
+                }
                 if (esz == 2) {
                   x1 = ref_bf16_to_f32(((const uint16_t*)oc)[src + e1]);
                   x2 = ref_bf16_to_f32(((const uint16_t*)oc)[src + e2]);
@@ -659,6 +665,10 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
     /* 4. outputs and row updates */
     const uint8_t* rf = refreshed ? (const uint8_t*)refreshed[sg] : NULL;
     uint8_t* pl = (uint8_t*)pool[sg];
+    /* In place, a reused key is rewritten only where Eq. 5 changes it: every pair for 1-D RoPE; for M-RoPE only
+     * the s_t pairs of the temporal section -- (h, w) of a reused token do not change, so the h / w sections keep
+     * their stored bits (R(0) = identity; reading NEXT-3). */
+    const int64_t rot_pairs = kv->rope_mode == REF_ROPE_MROPE ? kv->mrope_section[0] : D / 2;
     int64_t n_reuse = 0, n_anchor = 0, n_new = 0, rrow = 0, rot = 0, cop = 0, dp = 0;
     for (int64_t p = 0; p < nt; ++p) {
       const int d = tdisp[p];
@@ -681,7 +691,7 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
         const int64_t dpos[3] = {((tfrm[p] - ks) - (tfrm[p] - (k - 1) * s)) * kv->t_per_frame, 0, 0};
         for (int64_t l = 0; l < L; ++l)
           for (int64_t h = 0; h < H; ++h)
-            for (int64_t i = 0; i < D / 2; ++i) {
+            for (int64_t i = 0; i < rot_pairs; ++i) {
               const int64_t base = ((l * 2 + 0) * cap + sl) * rowel; /* the key row, rotated in place */
               const int64_t e1 = base + h * D + i, e2 = base + h * D + i + D / 2;
               float x1, x2, o1, o2;
@@ -721,8 +731,8 @@ int codecsight_ref_kv_refresh_paged(const ref_grid* g, const ref_kv* kv, const r
     counters[REF_C_TOK_REUSE] += (unsigned long long)n_reuse;
     counters[REF_C_TOK_ANCHOR] += (unsigned long long)n_anchor;
     counters[REF_C_TOK_NEW] += (unsigned long long)n_new;
-    /* keys only for REUSE (read + write), keys and values for refreshed rows (read + write) */
-    counters[REF_C_BYTES_KV] += (unsigned long long)((rot * L * 1 + cop * L * 2) * rowel * esz * 2);
+    /* REUSE: the rotated pairs of the key rows (read + write); refreshed rows: keys and values (read + write) */
+    counters[REF_C_BYTES_KV] += (unsigned long long)((rot * L * H * 2 * rot_pairs + cop * L * 2 * rowel) * esz * 2);
     counters[REF_C_STREAM_STEPS] += 1;
   }
   free(tdisp);

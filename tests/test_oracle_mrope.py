@@ -133,3 +133,43 @@ def test_mrope_paged_equals_out_of_place(ref, dtype):
         sn = pg["slot_new"][0, :nt]
         assert (pool[:, :, sn] == oop_new[:, :, :nt]).all()
         slot, oop_old = pg["slot_new"], oop_new
+
+
+@pytest.mark.parametrize("paged", [False, True])
+def test_mrope_hw_sections_keep_their_bits(ref, paged):
+    """-0.0, +inf and NaN stored in the h / w sections survive a reuse bit for bit (they are not rotated by 0,
+    which would turn -0 into +0 and inf into NaN); the temporal section is rotated."""
+    g, kept, masks, types, kv = _setup()
+    rng = np.random.default_rng(7)
+    old = rng.standard_normal((2, 2, 32, 2, 16)).astype(np.float32)
+    special = np.array([-0.0, np.inf, -np.inf, np.nan], np.float32)
+    old[:, 0, :, :, 2:6] = special                       # pairs 2..5 (h section), first halves
+    win = dict(window=12, stride=4, step=1, ring_frames=16)
+    if paged:
+        pool = old.copy()
+        slot_old = np.arange(32, dtype=np.int32)[None]
+        out = ref.kv_refresh_paged(g, kv, win, masks[None], types[None], [pool], slot_old, 32, None, 32)
+        got = lambda p: pool[:, 0, out["slot_new"][0, p]]
+    else:
+        new = np.zeros_like(old)
+        out = ref.kv_refresh(g, kv, win, masks[None], types[None], [old], [new], None, 32)
+        got = lambda p: new[:, 0, p]
+    reuse = [p for p in range(21) if out["disposition"][0, p] == 2]
+    assert reuse
+    for p in reuse:
+        po = out["p_old"][0, p]
+        a, b = got(p), old[:, 0, po]
+        assert (a[..., 2:8].view(np.uint32) == b[..., 2:8].view(np.uint32)).all()
+        assert (a[..., 10:16].view(np.uint32) == b[..., 10:16].view(np.uint32)).all()
+        assert not (a[..., 0:2] == b[..., 0:2]).all()     # temporal pairs rotated
+
+
+def test_mrope_paged_bytes_count_the_rotated_section(ref):
+    """In place, a reused key moves only its temporal section: L * H * 2 * s_t elements read + written."""
+    g, kept, masks, types, kv = _setup(dtype=1, H=2, D=16, sections=(2, 3, 3))
+    pool = np.zeros((2, 2, 32, 2, 16), np.float32)
+    out = ref.kv_refresh_paged(g, kv, dict(window=12, stride=4, step=1, ring_frames=16), masks[None], types[None],
+                               [pool], np.arange(32, dtype=np.int32)[None], 32, None, 32)
+    n_reuse = int(out["n_tokens"][0, 1])
+    assert n_reuse == 5
+    assert int(out["counters"][10]) == n_reuse * 2 * 2 * 2 * 2 * 4 * 2   # L * H * 2 s_t * 4 B * (r + w); no refreshed
