@@ -78,6 +78,10 @@ struct KvParams {
   int rope_mode;    // CS_ROPE_1D | CS_ROPE_MROPE
   int mrope_t;      // M-RoPE: pairs of the temporal section (rotated by dt); the h / w sections stay
   long long mrope_dt;  // M-RoPE: temporal position change of a reused token (-stride * t_per_frame)
+  int rot_pairs;       // pairs (i, i + D/2) of a reused key that Eq. 5 rewrites: D/2 (1-D), s_t (M-RoPE); the
+                       // others keep their stored bits (reading NEXT-3)
+  int partial_mode;    // paged with rot_pairs < D/2: a REUSE key chunk is rotated in place (its rotated pairs only)
+                       // straight in global memory by the ring's warp instead of a TMA round trip of whole rows
   long long mv_off;  // byte offset of the move list inside a stream's workspace slice
   double inv_freq[cs::kMaxHeadDim / 2];  // base^(-2i/D), computed on the host
 };
@@ -296,7 +300,8 @@ __device__ __forceinline__ void rot4_f32(uint4& a, uint4& b, const float* c, con
 // and second half of one head).  TH/TD > 0: compile-time head count / head dim (production shape).
 template <typename T, int TH, int TD>
 __device__ __forceinline__ void rotate_run(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
-                                           int nrows, int rH, int rD, const float* s_c, const float* s_s) {
+                                           int nrows, int rH, int rD, const float* s_c, const float* s_s,
+                                           int rot_pairs) {
   constexpr int VE = Vec<T>::N;
   const int H = TH > 0 ? TH : rH;
   const int D = TD > 0 ? TD : rD;
@@ -327,8 +332,10 @@ __device__ __forceinline__ void rotate_run(const unsigned char* __restrict__ src
       if (e < total) {
         const float* c = s_c + jv[u] * VE;
         const float* s = s_s + jv[u] * VE;
-        if constexpr (sizeof(T) == 2) rot8_bf16(a[u], b[u], c, s);
-        else rot4_f32(a[u], b[u], c, s);
+        if (jv[u] * VE < rot_pairs) {  // else: a pair of an unchanged M-RoPE section, copied bit for bit
+          if constexpr (sizeof(T) == 2) rot8_bf16(a[u], b[u], c, s);
+          else rot4_f32(a[u], b[u], c, s);
+        }
         cs::st_na_v4(dst + off1[u], a[u]);
         cs::st_na_v4(dst + off1[u] + half * static_cast<int>(sizeof(T)), b[u]);
       }
@@ -362,7 +369,7 @@ __device__ __forceinline__ void copy_run(const unsigned char* __restrict__ src, 
 template <typename T>
 __device__ __forceinline__ void rotate_run_scalar(const unsigned char* __restrict__ src,
                                                   unsigned char* __restrict__ dst, int nrows, int H, int D,
-                                                  const float* s_c, const float* s_s) {
+                                                  const float* s_c, const float* s_s, int rot_pairs) {
   const int half = D / 2;
   const int total = nrows * H * half;
   const T* sp = reinterpret_cast<const T*>(src);
@@ -371,6 +378,11 @@ __device__ __forceinline__ void rotate_run_scalar(const unsigned char* __restric
     const int row = e / (H * half), r = e - row * H * half;
     const int h = r / half, i = r - h * half;
     const long long o1 = (long long)row * H * D + h * D + i, o2 = o1 + half;
+    if (i >= rot_pairs) {  // unchanged M-RoPE section: bit copy
+      dp[o1] = sp[o1];
+      dp[o2] = sp[o2];
+      continue;
+    }
     float x1, x2;
     if constexpr (sizeof(T) == 2) {
       x1 = __uint_as_float(static_cast<uint32_t>(sp[o1]) << 16);
@@ -488,8 +500,8 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather_ldg(const __grid_con
       if (sg.kind == SEG_REUSE) {
         const unsigned char* src = oc + (plane_new + srow) * row_bytes;
         if (kv == 0) {  // Eq. 5
-          if (TH > 0 || P.vec_rot) rotate_run<T, TH, TD>(src, dst, n, P.H, P.D, s_c, s_s);
-          else rotate_run_scalar<T>(src, dst, n, P.H, P.D, s_c, s_s);
+          if (P.vec_rot) rotate_run<T, TH, TD>(src, dst, n, P.H, P.D, s_c, s_s, P.rot_pairs);
+          else rotate_run_scalar<T>(src, dst, n, P.H, P.D, s_c, s_s, P.rot_pairs);
         } else {  // value reuse
           if (TH > 0 || P.vec_copy) copy_run(src, dst, n * row_bytes);
           else copy_run_u32(src, dst, n * row_bytes);
@@ -515,6 +527,7 @@ constexpr int kTmaChunk = 8192;
 constexpr int kClaim = 4;  // items per dynamic work claim
 constexpr int kWarpsPerGather = kGatherThreads / 32;
 constexpr int kMaxStages = 6;
+constexpr int kPartialRows = 32;  // rows per in-place partial (M-RoPE temporal section) rotation item
 
 struct ChunkDesc {
   unsigned char* dst;
@@ -613,7 +626,10 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
         ++g.seg;
         continue;
       }
-      const int n = min(cr, x1 - x0);
+      // in place with M-RoPE only the temporal section of a reused key changes: no TMA round trip of the whole
+      // row, the warp rotates those pairs straight in global memory (rotate = 2), in larger row batches
+      const bool partial = P.partial_mode && sg.kind == SEG_REUSE && g.kv == 0;
+      const int n = min(partial ? kPartialRows : cr, x1 - x0);
       const long long plane = static_cast<long long>(g.l * 2 + g.kv);
       const long long srow = sg.src + (x0 - sg.p_new);
       const long long drow = sg.dst + (x0 - sg.p_new);
@@ -622,7 +638,7 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
       d.rows = n;
       if (sg.kind == SEG_REUSE) {
         src = g.oc + (plane * P.cap + srow) * row_bytes;
-        d.rotate = (g.kv == 0);
+        d.rotate = partial ? 2 : (g.kv == 0);
       } else {
         src = g.rf + (plane * P.rcap + srow) * row_bytes;
         d.rotate = 0;
@@ -699,12 +715,12 @@ __device__ __forceinline__ void rot8_bf16_pack(uint4& a, uint4& b, const float* 
 // rotate the K rows of one chunk in shared memory; executed by the 32 lanes of one warp
 template <typename T, int TH, int TD>
 __device__ __forceinline__ void rotate_smem_warp(unsigned char* buf, const float2* tab, int rows, int rH, int rD,
-                                                 int lane) {
+                                                 int rot_pairs, int lane) {
   constexpr int VE = Vec<T>::N;
   const int H = TH > 0 ? TH : rH;
   const int D = TD > 0 ? TD : rD;
   const int half = D / 2;
-  const int vph = half / VE;
+  const int vph = rot_pairs / VE;  // rotated vectors per half-head (the rest of the row is already in place)
   const int upr = H * vph;
   const int rowb = H * D * static_cast<int>(sizeof(T));
   const int total = rows * upr;
@@ -728,6 +744,56 @@ __device__ __forceinline__ void rotate_smem_warp(unsigned char* buf, const float
     else rot4_f32(a, b, c, s);
     *reinterpret_cast<uint4*>(p1) = a;
     *reinterpret_cast<uint4*>(p2) = b;
+  }
+}
+
+// In-place rotation of the first rot_pairs pairs (i, i + D/2) of every head of `rows` contiguous key rows, straight
+// in global memory (M-RoPE: the temporal section; the h / w sections are not touched).  All loads of a batch are
+// issued before any rotation (memory-level parallelism); executed by the 32 lanes of one warp.
+template <typename T, int TH, int TD>
+__device__ __forceinline__ void rotate_partial_global(unsigned char* base, const float2* tab, int rows, int rH, int rD,
+                                                      int rot_pairs, int lane) {
+  constexpr int VE = Vec<T>::N;
+  const int H = TH > 0 ? TH : rH;
+  const int D = TD > 0 ? TD : rD;
+  const int half = D / 2;
+  const int vph = rot_pairs / VE;
+  const int upr = H * vph;
+  const int rowb = H * D * static_cast<int>(sizeof(T));
+  const int total = rows * upr;
+  constexpr int kU = 8;
+  for (int e0 = lane; e0 < total; e0 += 32 * kU) {
+    uint4 a[kU], b[kU];
+    int off[kU], jv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * 32;
+      if (e < total) {
+        const int row = e / upr, un = e - row * upr;
+        const int h = un / vph, j = un - h * vph;
+        off[u] = row * rowb + (h * D + j * VE) * static_cast<int>(sizeof(T));
+        jv[u] = j;
+        a[u] = *reinterpret_cast<const uint4*>(base + off[u]);
+        b[u] = *reinterpret_cast<const uint4*>(base + off[u] + half * static_cast<int>(sizeof(T)));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * 32;
+      if (e < total) {
+        float c[VE], sn[VE];
+#pragma unroll
+        for (int v = 0; v < VE; ++v) {
+          const float2 t = tab[jv[u] * VE + v];
+          c[v] = t.x;
+          sn[v] = t.y;
+        }
+        if constexpr (sizeof(T) == 2) rot8_bf16_pack(a[u], b[u], c, sn);
+        else rot4_f32(a[u], b[u], c, sn);
+        cs::st_na_v4(base + off[u], a[u]);
+        cs::st_na_v4(base + off[u] + half * static_cast<int>(sizeof(T)), b[u]);
+      }
+    }
   }
 }
 
@@ -773,6 +839,11 @@ __global__ void __launch_bounds__(kGatherThreads, 1) kv_gather_tma(const __grid_
       return;
     }
     desc[st] = d;
+    if (d.rotate == 2) {  // partial in-place rotation: only the cos/sin table goes through the stage
+      cs::mbar_arrive_expect_tx(&full[st], tab_bytes);
+      cs::bulk_g2s(tabs + (size_t)st * tab_bytes, tab, tab_bytes, &full[st]);
+      return;
+    }
     cs::mbar_arrive_expect_tx(&full[st], d.bytes + (d.rotate ? tab_bytes : 0u));
     cs::bulk_g2s(stages + (size_t)st * stage_bytes, src, d.bytes, &full[st]);
     if (d.rotate) cs::bulk_g2s(tabs + (size_t)st * tab_bytes, tab, tab_bytes, &full[st]);
@@ -786,15 +857,18 @@ __global__ void __launch_bounds__(kGatherThreads, 1) kv_gather_tma(const __grid_
     const ChunkDesc d = desc[st];
     if (d.bytes == 0) break;
     unsigned char* buf = stages + (size_t)st * stage_bytes;
-    if (d.rotate) {
+    if (d.rotate == 2) {
+      rotate_partial_global<T, TH, TD>(d.dst, reinterpret_cast<const float2*>(tabs + (size_t)st * tab_bytes), d.rows,
+                                       P.H, P.D, P.rot_pairs, lane);
+    } else if (d.rotate) {
       rotate_smem_warp<T, TH, TD>(buf, reinterpret_cast<const float2*>(tabs + (size_t)st * tab_bytes), d.rows, P.H,
-                                  P.D, lane);
+                                  P.D, P.rot_pairs, lane);
       cs::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
     }
     __syncwarp();
     if (lane == 0) {
-      cs::bulk_s2g(d.dst, buf, d.bytes);
-      cs::bulk_commit();
+      if (d.rotate != 2) cs::bulk_s2g(d.dst, buf, d.bytes);
+      cs::bulk_commit();  // (an empty group for a partial item keeps the wait_group accounting per item)
       if (q >= 1 && more) {
         cs::bulk_wait_read<1>();  // the store of chunk q-1 has read its stage
         issue((q - 1) % nst);
@@ -1115,7 +1189,9 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   if (tid == 0) {
     cs::atomic_or_status(P.status, s_st);
     const unsigned long long rowb = (unsigned long long)(P.H * P.D * P.esz);
-    cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_KV], (s_rot * P.L + s_cop * P.L * 2ull) * rowb * 2ull);
+    // REUSE: the rotated pairs of the key rows (M-RoPE: the temporal section only); refreshed rows: K and V
+    const unsigned long long rotb = (unsigned long long)P.H * 2ull * P.rot_pairs * P.esz;
+    cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_KV], (s_rot * P.L * rotb + s_cop * P.L * 2ull * rowb) * 2ull);
   }
 }
 
@@ -1128,7 +1204,7 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather_paged(const __grid_c
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int H = TH > 0 ? TH : P.H;
   const int D = TD > 0 ? TD : P.D;
-  const int half = D / 2, vph = half / VE, upr = H * vph;
+  const int half = D / 2;
   const int rowb = H * D * static_cast<int>(sizeof(T));
   float2* tab = reinterpret_cast<float2*>(smem) + wib * (P.D / 2);  // this warp's (cos, sin) table
   const int* pref = ws_prefix(P);
@@ -1172,10 +1248,11 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather_paged(const __grid_c
       // Eq. 5 in place on the key rows (plane 2l) of every layer
       unsigned char* base = pl + (long long)me.slot * rowb;
       if (P.vec_rot && P.vec_copy) {
-        const int total = upr;  // units per row
+        const int vphr = P.rot_pairs / VE;  // rotated vectors per half-head (M-RoPE: the temporal section)
+        const int total = H * vphr;         // units per row
         for (int l0 = 0; l0 < P.L; l0 += 4) {
           for (int e = lane; e < total; e += 32) {
-            const int h = e / vph, j = e - h * vph;
+            const int h = e / vphr, j = e - h * vphr;
             const int off1 = (h * D + j * VE) * static_cast<int>(sizeof(T));
             const int off2 = off1 + half * static_cast<int>(sizeof(T));
             uint4 a[4], b[4];
@@ -1209,8 +1286,8 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather_paged(const __grid_c
       } else {
         for (int l = 0; l < P.L; ++l) {
           T* r = reinterpret_cast<T*>(base + (long long)(2 * l) * plane);
-          for (int e = lane; e < H * half; e += 32) {
-            const int h = e / half, i = e - h * half;
+          for (int e = lane; e < H * P.rot_pairs; e += 32) {
+            const int h = e / P.rot_pairs, i = e - h * P.rot_pairs;
             float x1, x2;
             if constexpr (sizeof(T) == 2) {
               x1 = __uint_as_float(static_cast<uint32_t>(r[h * D + i]) << 16);
@@ -1328,7 +1405,8 @@ static void fill_params(KvParams& P, const cs_grid* g, const cs_kv_desc* kv, con
   P.has_refreshed = refreshed != nullptr;
   {
     const int ve = 16 / P.esz;
-    P.vec_rot = ((P.D / 2) % ve) == 0;
+    P.rot_pairs = kv->rope_mode == CS_ROPE_MROPE ? kv->mrope_section[0] : kv->head_dim / 2;
+    P.vec_rot = ((P.D / 2) % ve) == 0 && (P.rot_pairs % ve) == 0;
     P.vec_copy = ((static_cast<long long>(P.H) * P.D * P.esz) % 16) == 0;
   }
   const size_t max_seg = static_cast<size_t>(P.max_seg);
@@ -1428,10 +1506,12 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   P.ws_stride = static_cast<long long>(paged_stride(g, kv, win, &P.mv_off, &P.max_tok));
   P.max_seg = P.max_tok + 1;  // run list capacity (also locates the cos/sin table)
   P.paged = 1;
+  P.partial_mode = 0;
   P.old_cache = pool;  // REUSE runs read and write the same pool rows
   P.new_cache = pool;
   const long long row_bytes = static_cast<long long>(P.H) * P.D * P.esz;
   const bool tma_ok = P.vec_rot && P.vec_copy && row_bytes <= kTmaChunk && (P.D % 4) == 0;
+  P.partial_mode = (tma_ok && P.rot_pairs < P.D / 2) ? 1 : 0;
   P.prefix_mode = tma_ok ? 0 : 1;
   const int lo = win->step >= 1 ? (win->step - 1) * win->stride : 0;
   const int nfr = win->step * win->stride + win->window - lo;

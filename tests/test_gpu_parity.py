@@ -474,6 +474,16 @@ def run_kv_both(abi, ref, g, kv, win, mring, tring, old_d, new_d, ref_d, token_c
     return gpu, o, new_h
 
 
+def _rot_cols(kv):
+    """(rotated, kept) column index arrays of a key row [H][D] under kv's RoPE: with M-RoPE only the temporal
+    pairs (i, i + D/2), i < s_t, are rotated; the h / w sections keep their bits (reading NEXT-3)."""
+    D = kv["head_dim"]
+    st = kv["mrope_section"][0] if kv.get("rope_mode", 0) == 1 else D // 2
+    rot = np.array([i for i in range(D) if (i % (D // 2)) < st])
+    keep = np.array([i for i in range(D) if (i % (D // 2)) >= st], dtype=np.int64)
+    return rot, keep
+
+
 def assert_kv_equal(gpu, o, new_d, new_h, kv, stats=None):
     assert gpu["status"] == o["status"]
     assert (gpu["n_tokens"] == o["n_tokens"]).all()
@@ -494,7 +504,9 @@ def assert_kv_equal(gpu, o, new_d, new_h, kv, stats=None):
         nonre = np.flatnonzero(disp != 2)
         assert (a[:, 0, nonre] == b[:, 0, nonre]).all()
         re = np.flatnonzero(disp == 2)
-        ka, kb = a[:, 0, re], b[:, 0, re]
+        rot, keep = _rot_cols(kv)
+        assert (a[:, 0, re][..., keep].view(np.uint8) == b[:, 0, re][..., keep].view(np.uint8)).all()  # M-RoPE h/w: bits
+        ka, kb = a[:, 0, re][..., rot], b[:, 0, re][..., rot]
         if kv["dtype"] == 0:
             fa = (ka.astype(np.uint32) << 16).view(np.float32)
             fb = (kb.astype(np.uint32) << 16).view(np.float32)
@@ -832,16 +844,19 @@ def run_paged_both(abi, ref, g, kv, win, mring, tring, pools_d, slot_old_h, slot
         a, b = _host_cache(pools_d[s]), pools_h[s]
         # values and every row that is not a rotated key: bit-identical
         assert (a[:, 1] == b[:, 1]).all()
+        rot, keep = _rot_cols(kv)
+        assert (a[:, 0][..., keep].view(np.uint8) == b[:, 0][..., keep].view(np.uint8)).all()
+        ka, kb = a[:, 0][..., rot], b[:, 0][..., rot]
         if kv["dtype"] == 0:
-            fa = (a[:, 0].astype(np.uint32) << 16).view(np.float32)
-            fb = (b[:, 0].astype(np.uint32) << 16).view(np.float32)
+            fa = (ka.astype(np.uint32) << 16).view(np.float32)
+            fb = (kb.astype(np.uint32) << 16).view(np.float32)
             tol = 1e-2
         else:
-            fa, fb, tol = a[:, 0], b[:, 0], 1e-5
+            fa, fb, tol = ka, kb, 1e-5
         d = float(np.abs(fa - fb).max())
         assert d <= tol, d
         stats["max_diff"] = max(stats["max_diff"], d)
-        stats["not_bit_exact"] += int((a[:, 0] != b[:, 0]).sum())
+        stats["not_bit_exact"] += int((ka != kb).sum())
     return sn, o, stats
 
 
@@ -944,11 +959,18 @@ def test_mrope_gpu_both_modes(abi, ref, dtype):
     dt = torch.bfloat16 if dtype == 0 else torch.float32
     shape = (kv["layers"], 2, cap, kv["kv_heads"], kv["head_dim"])
     pools = [torch.randn(shape, generator=gen, device=DEV).to(dt) for _ in range(S)]
+    _, keep = _rot_cols(kv)
+    special = torch.tensor([-0.0, float("inf"), float("-inf"), float("nan")], device=DEV).to(dt)
+    for t in pools:   # -0 / inf / NaN in the h / w sections must survive reuse bit for bit
+        t[:, 0, :, :, keep[:4]] = special
     slot = None
     stats = {}
     for k in range(6):
         mring, tring = stream_rings(ref, g, cfg, S, ring, k, w, s)
         old, new, refr = make_caches(kv, S, gen)
+        if k:
+            for t in old:
+                t[:, 0, :, :, keep[:4]] = special
         win = dict(window=w, stride=s, step=k, ring_frames=ring)
         gpu, o, new_h = run_kv_both(abi, ref, g, kv, win, mring, tring, old if k else None, new, refr, cap)
         assert_kv_equal(gpu, o, new, new_h, kv, stats)
