@@ -505,7 +505,8 @@ def assert_kv_equal(gpu, o, new_d, new_h, kv, stats=None):
         assert (a[:, 0, nonre] == b[:, 0, nonre]).all()
         re = np.flatnonzero(disp == 2)
         rot, keep = _rot_cols(kv)
-        assert (a[:, 0, re][..., keep].view(np.uint8) == b[:, 0, re][..., keep].view(np.uint8)).all()  # M-RoPE h/w: bits
+        assert (np.ascontiguousarray(a[:, 0, re][..., keep]).view(np.uint8) ==
+                np.ascontiguousarray(b[:, 0, re][..., keep]).view(np.uint8)).all()   # M-RoPE h/w sections: bits
         ka, kb = a[:, 0, re][..., rot], b[:, 0, re][..., rot]
         if kv["dtype"] == 0:
             fa = (ka.astype(np.uint32) << 16).view(np.float32)
@@ -845,7 +846,8 @@ def run_paged_both(abi, ref, g, kv, win, mring, tring, pools_d, slot_old_h, slot
         # values and every row that is not a rotated key: bit-identical
         assert (a[:, 1] == b[:, 1]).all()
         rot, keep = _rot_cols(kv)
-        assert (a[:, 0][..., keep].view(np.uint8) == b[:, 0][..., keep].view(np.uint8)).all()
+        assert (np.ascontiguousarray(a[:, 0][..., keep]).view(np.uint8) ==
+                np.ascontiguousarray(b[:, 0][..., keep]).view(np.uint8)).all()
         ka, kb = a[:, 0][..., rot], b[:, 0][..., rot]
         if kv["dtype"] == 0:
             fa = (ka.astype(np.uint32) << 16).view(np.float32)
