@@ -94,3 +94,64 @@ def test_compact_validation(abi):
     assert call(dict(g, patch=40)) == abi.CS_ERR_SHAPE
     assert call(dict(g, patch=20)) == abi.CS_ERR_UNSUPPORTED     # group * patch > 32
     assert call(g, n_streams=1 << 20, n_frames=4096, mfs=4096) == abi.CS_ERR_UNSUPPORTED   # int32 offsets
+
+
+def test_extension_validation(abi):
+    """Argument checks of the extension entry points happen on the host, before any device work."""
+    L = abi.lib()
+    g = make_grid(448, 448)
+    G = C.byref(abi.make_grid(g))
+    nocuda = not torch.cuda.is_available()
+    # fused score + compact (NEXT-2)
+    ws_need = abi.score_compact_workspace_size(4)
+    assert ws_need == 8 + 8 * 4
+
+    def sc(n_streams=4, n_frames=2, fs=2, layout=1, cap=16, ws=FAKE, ws_bytes=1 << 10, mb=FAKE):
+        return L.codecsight_score_compact(G, n_streams, n_frames, mb, FAKE, FAKE, fs, FAKE, None, FAKE, FAKE, FAKE,
+                                          layout, cap, FAKE, FAKE, FAKE, FAKE, ws, ws_bytes, FAKE, FAKE, None)
+    assert sc(ws_bytes=ws_need - 1) == abi.CS_ERR_INVALID_ARGUMENT        # workspace too small
+    assert sc(ws=None) == abi.CS_ERR_INVALID_ARGUMENT
+    assert sc(layout=3) == abi.CS_ERR_INVALID_ARGUMENT
+    assert sc(fs=1) == abi.CS_ERR_INVALID_ARGUMENT                        # frame stride < n_frames
+    assert sc(mb=FAKE + 2) == abi.CS_ERR_INVALID_ARGUMENT                  # 8-B aligned records
+    assert sc(n_streams=0) == abi.CS_OK
+    if nocuda:
+        assert sc() == abi.CS_ERR_CUDA                                     # no CPU fallback
+    # temporal patches (NEXT-3)
+
+    def tp(t=2, n_units=2, mfs=4, cap=16, um=None, ums=0, ft=None, ut=None):
+        return L.codecsight_compact_tp(G, t, 1, n_units, FAKE, mfs, FAKE, FAKE, 0, cap, FAKE, FAKE, FAKE, FAKE, um,
+                                       ums, ft, ut, FAKE, FAKE, None)
+    assert tp(t=0) == abi.CS_ERR_UNSUPPORTED and tp(t=5) == abi.CS_ERR_UNSUPPORTED
+    assert tp(mfs=3) == abi.CS_ERR_INVALID_ARGUMENT                        # n_units * tp frames needed
+    assert tp(um=FAKE, ums=1) == abi.CS_ERR_INVALID_ARGUMENT               # unit mask stride < n_units
+    assert tp(ft=FAKE) == abi.CS_ERR_INVALID_ARGUMENT                      # frame_type needs unit_type
+    if nocuda:
+        assert tp(um=FAKE, ums=2, ft=FAKE, ut=FAKE) == abi.CS_ERR_CUDA
+    # MV rasterisation / similar histogram (NEXT-4)
+    assert L.codecsight_mv_rasterize(G, -1, FAKE, FAKE, FAKE, None) == abi.CS_ERR_INVALID_ARGUMENT
+    assert L.codecsight_mv_rasterize(G, 0, None, None, None, None) == abi.CS_OK
+    assert L.codecsight_mv_rasterize(G, 2, FAKE, FAKE, FAKE + 4, None) == abi.CS_ERR_INVALID_ARGUMENT  # 8-B out
+    assert L.codecsight_similar_hist(FAKE, FAKE, 4, 1024, FAKE, 0, 10, FAKE, None) == abi.CS_ERR_INVALID_ARGUMENT
+    assert L.codecsight_similar_hist(FAKE, FAKE, 4, 1024, FAKE, 2, 0, FAKE, None) == abi.CS_ERR_INVALID_ARGUMENT
+    assert L.codecsight_similar_hist(None, None, 0, 1024, None, 2, 10, None, None) == abi.CS_OK
+    if nocuda:
+        assert L.codecsight_mv_rasterize(G, 2, FAKE, FAKE, FAKE, None) == abi.CS_ERR_CUDA
+        assert L.codecsight_similar_hist(FAKE, FAKE, 4, 1024, FAKE, 2, 10, FAKE, None) == abi.CS_ERR_CUDA
+
+
+def test_nv12_validation(abi):
+    L = abi.lib()
+    G = C.byref(abi.make_grid(make_grid(1920, 1080)))
+
+    def nv(**kw):
+        pre = dict(dict(src_w=1920, src_h=1080), **kw)
+        return L.codecsight_compact_nv12(G, C.byref(abi.make_preprocess(pre)), 1, 2, FAKE, 2, FAKE, FAKE, FAKE, 16,
+                                         FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, None)
+    assert nv(src_w=1921) == abi.CS_ERR_SHAPE                  # 4:2:0 needs even sizes
+    assert nv(y_pitch=1900) == abi.CS_ERR_SHAPE                # pitch < width
+    assert nv(color=1) == abi.CS_ERR_UNSUPPORTED
+    assert nv(std=(0.2, 0.0, 0.2)) == abi.CS_ERR_INVALID_ARGUMENT
+    assert nv(mean=(float("nan"), 0.4, 0.4)) == abi.CS_ERR_INVALID_ARGUMENT
+    if not torch.cuda.is_available():
+        assert nv() == abi.CS_ERR_CUDA
