@@ -605,7 +605,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                       "h2d_bytes_per_step": e2e["h2d"] * world, "d2h_bytes_per_step": e2e["d2h"] * world,
                       "wall_clock_value": frames_total / (e2e["wall_ms"] / 1e3),
                       "pipelining": "H2D of step k+1 on a copy stream overlaps step k; host reads step k-1's result"}
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the oracle baseline is timed at N = 1 only
         log("[rank 0] timing the CPU oracle on a bounded sample ...")
         r = oracle_sample(cfg, args.cpu_seconds, kv_mode=args.kv_mode, tp=tp)
         out["cpu_baseline"] = {"value": r["frames"] / r["seconds"], "unit": "frames/s", "cores": 1, "kind": "oracle",
