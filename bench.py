@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--fused", action=argparse.BooleanOptionalAction, default=True,
                     help="one codecsight_score_compact launch per step (NEXT-2, default) instead of score_patches + "
                          "compact (--no-fused)")
+    ap.add_argument("--graphs", action="store_true",
+                    help="replay steps k >= 1 as captured CUDA graphs (one per ring phase and slot parity)")
     ap.add_argument("--temporal-patch", type=int, default=1, choices=[1, 2],
                     help="frames per visual token (Qwen2-VL video: 2; NEXT-3); KV refresh over token units")
     ap.add_argument("--kv-mode", default="paged", choices=["paged", "copy"],
@@ -314,12 +316,16 @@ def run_ours(args, cfg, rank, world, local_rank):
                     kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre, overlap=args.overlap,
                     temporal_patch=args.temporal_patch, fused=args.fused)
     tp = args.temporal_patch
+    # --graphs: steps k >= 1 are CUDA graph replays, one graph per (ring phase, slot parity); the warm-up covers a
+    # whole cycle of keys so that no capture happens inside a timed region
+    period = pipe.uring // math.gcd(pipe.uring, pipe.su)
+    warm = max(args.warmup, 2 * period + 2) if args.graphs else args.warmup
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     pipe.init_cache_fill(gen)
     t_setup = time.time()
     # metadata pool: step 0 (w frames) + `pool` stride steps, cycled during the run
-    n_pool = max(1, min(args.pool if cfg["src"][0] < 3000 else min(args.pool, 3), args.warmup + args.steps))
+    n_pool = max(1, min(args.pool if cfg["src"][0] < 3000 else min(args.pool, 3), warm + args.steps))
     md = gen_metadata(cfg, global_ids, n_pool)
     mb_host = [torch.from_numpy(m.view(np.uint8).copy()).pin_memory() for m in md]
     mb_dev = [t.to(dev) for t in mb_host]
@@ -337,7 +343,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         frames = [torch.randn(3, H, W, generator=gen, device=dev).to(torch.bfloat16) for _ in range(S * s)]
         ptr_w = abi.ptr_array([frames[i % len(frames)] for i in range(S * w)], dev)
         ptr_s = abi.ptr_array(frames, dev)
-    total_steps = args.warmup + args.steps
+    calib = 2 * period if args.graphs else 0  # eager steps after the graph-timed loop: per-kernel event times
+    total_steps = warm + args.steps + calib
     types_dev, fidx_dev, types_host = [], [], []
     for k in range(total_steps + 1):
         f0, n = step_frames(cfg, k)
@@ -358,16 +365,33 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---- device-resident timed loop ------------------------------------------------------------------------
     ev = {name: [] for name in ("score", "compact", "kv")}
 
+    # fixed staging buffers (graph inputs; the e2e loop uploads into the same ones)
+    stage = [dict(mb=torch.empty_like(mb_dev[1 if len(mb_dev) > 1 else 0]), ty=torch.empty_like(types_dev[1]),
+                  fi=torch.empty_like(fidx_dev[1])) for _ in range(2)]
+
+    def run_step_eager(k):
+        evs = pipe.step(k, md_for(k), ptr_s, fidx_dev[k], types_dev[k], timing=True)
+        for name in ("score", "compact", "kv"):
+            if name in evs:
+                ev[name].append(evs[name])
+
     def run_step(k, timed):
         _, n = step_frames(cfg, k)
         ptrs = ptr_w if k == 0 else ptr_s
+        if args.graphs and k >= 1:
+            st = stage[k & 1]
+            st["mb"].copy_(md_for(k), non_blocking=True)    # stage this step's inputs (device copies)
+            st["ty"].copy_(types_dev[k], non_blocking=True)
+            st["fi"].copy_(fidx_dev[k], non_blocking=True)
+            pipe.graph_step(k, st["mb"], ptrs, st["fi"], st["ty"])
+            return
         evs = pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k], timing=timed)
         if timed:
             for name in ("score", "compact", "kv"):
                 if name in evs:
                     ev[name].append(evs[name])
 
-    for k in range(args.warmup):
+    for k in range(warm):
         run_step(k, False)
     pipe.join(stream)
     torch.cuda.synchronize()
@@ -384,7 +408,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    for k in range(args.warmup, args.warmup + args.steps):
+    for k in range(warm, warm + args.steps):
         run_step(k, True)
     pipe.join(stream)
     t_end.record(stream)
@@ -395,12 +419,18 @@ def run_ours(args, cfg, rank, world, local_rank):
     clk = clocks.stop()
     ms = t_start.elapsed_time(t_end)
     dcnt = (pipe.counters - cnt0)
+    if args.graphs:
+        # per-kernel times of the graph-timed steps: the same kernels timed eagerly with events right after
+        # (counters of these steps are excluded from dcnt above)
+        for k in range(warm + args.steps, warm + args.steps + calib):
+            run_step_eager(k)
+        torch.cuda.synchronize()
     per = {kname: [a.elapsed_time(b) for a, b in lst] for kname, lst in ev.items()}
     status = int(pipe.status.item())
 
     # ---- compact alone on the last step's masks, both frame layouts (context for the layout choice) ---------
     layouts = {}
-    k_last = args.warmup + args.steps - 1
+    k_last = warm + args.steps + calib - 1
     off_l = pipe.ring_slot(k_last)
 
     def time_compact(fn, reps=10):
@@ -464,7 +494,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # the host waits for step k-1's results while step k runs (a streaming server's pipeline).
     e2e = None
     if not args.no_e2e:
-        k0 = args.warmup + args.steps
+        k0 = warm + args.steps + calib
         nsteps = args.steps
         in_mb, in_ty, in_fi = [], [], []
         for k in range(k0, k0 + nsteps):
@@ -473,9 +503,10 @@ def run_ours(args, cfg, rank, world, local_rank):
             in_ty.append(torch.from_numpy(np.stack([synth.frame_types(n, gop, f0)] * S)).pin_memory())
             in_fi.append(torch.from_numpy(np.tile(np.arange(f0 // tp, (f0 + n) // tp, dtype=np.int32),
                                                   S)).pin_memory())
-        st_mb = [torch.empty_like(mb_dev[1]) for _ in range(2)]
-        st_ty = [torch.empty_like(in_ty[0], device=dev) for _ in range(2)]
-        st_fi = [torch.empty_like(in_fi[0], device=dev) for _ in range(2)]
+        # the timed loop's staging buffers (same addresses, so graph keys match): slot b = k & 1
+        st_mb = [stage[0]["mb"], stage[1]["mb"]]
+        st_ty = [stage[0]["ty"], stage[1]["ty"]]
+        st_fi = [stage[0]["fi"], stage[1]["fi"]]
         res = [torch.empty(S * 4 + S * s + 1, dtype=torch.int32).pin_memory() for _ in range(2)]
         copy_stream = torch.cuda.Stream(dev)
         loaded = [torch.cuda.Event() for _ in range(2)]
@@ -492,7 +523,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         res_stream = torch.cuda.Stream(dev)
         for i in range(nsteps):
             k = k0 + i
-            b = i & 1
+            b = k & 1
             _, n = step_frames(cfg, k)
             with torch.cuda.stream(copy_stream):
                 if i >= 2:
@@ -502,10 +533,22 @@ def run_ours(args, cfg, rank, world, local_rank):
                 st_fi[b].copy_(in_fi[i], non_blocking=True)
                 loaded[b].record(copy_stream)
             stream.wait_event(loaded[b])
-            # the step's output buffers (parity b) were last read back by step i-2's results copy
-            evs = pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b], wait_events=[done[b]] if i >= 2 else [])
+            if args.overlap:
+                # double-buffered outputs (parity b) were last read back by step i-2's results copy
+                evs = pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b], wait_events=[done[b]] if i >= 2 else [])
+            else:
+                # single output buffers: step i overwrites them only after step i-1's results were copied out
+                if i >= 1:
+                    stream.wait_event(done[1 - b])
+                if args.graphs:
+                    pipe.graph_step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b])
+                    e_step = torch.cuda.Event()
+                    e_step.record(stream)
+                    evs = {"step": (None, e_step)}
+                else:
+                    evs = pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b])
             # results stream: waits for the step's kernels, reads the results back (D2H), releases the staging slot
-            for name in ("score", "compact", "kv"):
+            for name in ("score", "compact", "kv", "step"):
                 if name in evs:
                     res_stream.wait_event(evs[name][1])
             with torch.cuda.stream(res_stream):
@@ -520,8 +563,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                 checksum += int(res[1 - b][-1])
         stream.wait_stream(res_stream)
         e_b.record(stream)
-        done[(nsteps - 1) & 1].synchronize()
-        checksum += int(res[(nsteps - 1) & 1][-1])
+        done[(k0 + nsteps - 1) & 1].synchronize()
+        checksum += int(res[(k0 + nsteps - 1) & 1][-1])
         torch.cuda.synchronize()
         wall_ms = (time.perf_counter() - t0) * 1e3
         e2e_ms = e_a.elapsed_time(e_b)
@@ -556,7 +599,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     kept_frac = float(dcnt[abi.CNT_KEPT].item()) / max(1.0, float(dcnt[abi.CNT_PATCHES].item()))
     out = {
         "metric": "codec-pruned frames/sec (whole hot path: score+compact+kv_refresh), all GPUs",
-        "value": value, "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "value": value, "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": warm,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfg["name"], "streams_per_gpu": S, "streams_total": S * world, "src": list(cfg["src"]),
@@ -564,6 +607,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
                    "frames": args.frames, "overlap": args.overlap, "temporal_patch": tp, "fused": args.fused,
+                   "graphs": args.graphs,
                    "parallelism": f"stream-shard x{world}",
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
                          "see per-step bytes)"},

@@ -121,6 +121,7 @@ class Pipeline:
         if fused:
             self.sc_workspace = torch.zeros(abi.score_compact_workspace_size(S), dtype=torch.uint8, device=d)
         self._side_done = {}  # step -> events closing its compact / kv_refresh work (overlap mode)
+        self._graphs = {}     # graph_step: key -> captured torch.cuda.CUDAGraph
         if overlap:
             self.stream_compact = torch.cuda.Stream(d)
             self.stream_kv = torch.cuda.Stream(d)
@@ -254,9 +255,45 @@ class Pipeline:
                                        self.frame_offsets[: self.S * nj + 1], self.counters, self.status, stream,
                                        frame_layout=self.frame_layout)
 
+    def kv_step(self, k: int) -> int:
+        """Window index handed to kv_refresh.  A plan depends on k only through k == 0 and the ring phase -- every
+        frame index it uses is relative to ks and read through slot f % ring -- so k >= 1 is folded into
+        [1, period] with period = ring / gcd(ring, s) (in token units).  Equivalent by construction (every parity
+        test runs through it); it is what lets one captured CUDA graph serve all steps of a phase."""
+        if k == 0:
+            return 0
+        period = self.uring // math.gcd(self.uring, self.su)
+        return (k - 1) % period + 1
+
+    def graph_key(self, k: int):
+        """Steps with equal keys run identical kernel sequences with identical arguments (given fixed inputs)."""
+        return (self.kv_step(k), self.ring_slot(k), self.cur)
+
+    def graph_step(self, k: int, mb, frame_ptrs, frame_index, types, use_refreshed=None):
+        """Step k >= 1 as one CUDA graph replay (captured on first use of its key).  The inputs must be the same
+        tensors (addresses) for every step that shares a key -- callers stage per-step data into fixed buffers."""
+        assert k >= 1 and not self.overlap and self.preprocess is None
+        use_r = (k >= 1) if use_refreshed is None else use_refreshed
+        key = self.graph_key(k) + (mb.data_ptr(), frame_index.data_ptr(), types.data_ptr(),
+                                   frame_ptrs.data_ptr(), use_r)
+        gr = self._graphs.get(key)
+        if gr is None:
+            cur0 = self.cur
+            gr = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(self.dev)
+            side.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.graph(gr, stream=side):
+                self.step(k, mb, frame_ptrs, frame_index, types, use_refreshed)
+            torch.cuda.current_stream(self.dev).wait_stream(side)
+            self.cur = cur0  # capture recorded the step without running it; the replay below runs it
+            self._graphs[key] = gr
+        gr.replay()
+        if self.kv is not None:
+            self.cur = 1 - self.cur
+
     def kv_refresh(self, k, use_refreshed=None, stream=None):
         g = self.g
-        win = dict(window=self.wu, stride=self.su, step=k, ring_frames=self.uring)
+        win = dict(window=self.wu, stride=self.su, step=self.kv_step(k), ring_frames=self.uring)
         use_r = (k >= 1) if use_refreshed is None else use_refreshed
         ref = self.refreshed_ptrs if use_r else None
         if self.kv_mode == "paged":

@@ -809,6 +809,83 @@ def test_pipeline_temporal_patch2(abi, ref, rope):
     assert int(pipe.status.item()) == 0
 
 
+def test_pipeline_cuda_graphs(abi, ref):
+    """Steps k >= 1 replayed as captured CUDA graphs (one per (ring phase, slot parity)), inputs staged into fixed
+    buffers: 12 steps (graphs reused across two ring periods), fused score+compact + paged KV, every output compared
+    with the oracle driven the same way."""
+    from paper_2604_06036_b200.pipeline import Pipeline
+    cfg = synth.CONFIGS["C4"]
+    g = make_grid(1920, 1080)
+    S, w, s, gop = 4, 16, 4, 16
+    kvb = dict(synth.QWEN_KV, layers=2)
+    pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=32, device=DEV, kv_mode="paged", fused=True,
+                    frame_layout=abi.CS_LAYOUT_GROUPED)
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(9)
+    pipe.init_cache_fill(gen)
+    nw, ring = 32, pipe.ring
+    gens = [synth.StreamGen(1920, 1080, synth.scene_of(cfg, si), synth.stream_seed(cfg, si)) for si in range(S)]
+    gop_h = np.zeros((S, nw + 1), np.uint32)
+    mring_h = np.zeros((S, ring, nw), np.uint32)
+    tring_h = np.zeros((S, ring), np.uint8)
+    rng = np.random.default_rng(3)
+    frames_h = [to_grouped(f, g) for f in synth.random_frames(S * s, 448, 448, rng)]
+    frames_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in frames_h]
+    ptr_w = abi.ptr_array([frames_d[i % len(frames_d)] for i in range(S * w)], DEV)
+    ptr_s = abi.ptr_array(frames_d, DEV)
+    stage = [dict(mb=torch.empty(S * s * 68 * 120 * 8, dtype=torch.uint8, device=DEV),
+                  ty=torch.empty(S, s, dtype=torch.uint8, device=DEV),
+                  fi=torch.empty(S * s, dtype=torch.int32, device=DEV)) for _ in range(2)]
+    slot_h = None
+    for k in range(12):
+        f0, n = pipe.new_frames(k)
+        mb = np.stack([np.stack([gn.next_frame() for _ in range(n)]) for gn in gens])
+        types = np.stack([synth.frame_types(n, gop, f0) for _ in range(S)])
+        fidx = np.tile(np.arange(f0, f0 + n, dtype=np.int32), S)
+        pool_h = [_host_cache(c).copy() for c in pipe.caches[0]]
+        ref_h = [_host_cache(c) for c in pipe.refreshed]
+        if k == 0:
+            pipe.step(k, d_mb(mb), ptr_w, torch.from_numpy(fidx).to(DEV), torch.from_numpy(types).to(DEV))
+        else:
+            st = stage[k & 1]
+            st["mb"].copy_(torch.from_numpy(mb.view(np.uint8).reshape(-1)))
+            st["ty"].copy_(torch.from_numpy(types))
+            st["fi"].copy_(torch.from_numpy(fidx))
+            pipe.graph_step(k, st["mb"], ptr_s, st["fi"], st["ty"])
+        torch.cuda.synchronize()
+        off = f0 % ring
+        tring_h[:, off:off + n] = types
+        so = ref.score_patches(g, mb, np.ascontiguousarray(tring_h[:, off:]), gop_h, want_score=False,
+                               frame_stride=ring - off)
+        mring_h[:, off:off + n] = so["keep_mask"][:, :n]
+        assert (u32(pipe.mask_ring) == mring_h).all()
+        fr = [frames_h[i % len(frames_h)] for i in range(S * n)]
+        co = ref.compact(g, mring_h[:, off:].copy(), fidx, fr, pipe.capacity, S, n, mask_frame_stride=ring - off,
+                         frame_layout=1)
+        tot = int(co["frame_offsets"][-1])
+        assert (pipe.frame_offsets[:S * n + 1].cpu().numpy() == co["frame_offsets"]).all()
+        assert (pipe.packed[:tot].view(torch.int16).cpu().numpy().view(np.uint16) == co["packed"][:tot]).all()
+        assert (pipe.pos_ids[:tot].cpu().numpy() == co["pos_ids"][:tot]).all()
+        win = dict(window=w, stride=s, step=k, ring_frames=ring)            # the true window index
+        ko = ref.kv_refresh_paged(g, pipe.kv, win, mring_h, tring_h, pool_h, slot_h, pipe.token_cap,
+                                  ref_h if k >= 1 else None, pipe.token_cap)
+        assert (pipe.n_tokens.cpu().numpy() == ko["n_tokens"]).all()
+        sn = pipe.slots[pipe.cur].cpu().numpy()
+        for si in range(S):
+            nt = int(ko["n_tokens"][si, 0]) + 32
+            assert (pipe.disposition.cpu().numpy()[si, :nt] == ko["disposition"][si, :nt]).all()
+            assert (pipe.p_old.cpu().numpy()[si, :nt] == ko["p_old"][si, :nt]).all()
+            assert (sn[si, :nt] == ko["slot_new"][si, :nt]).all()
+            a, b = _host_cache(pipe.caches[0][si]), pool_h[si]
+            assert (a[:, 1] == b[:, 1]).all()
+            fa = (a[:, 0].astype(np.uint32) << 16).view(np.float32)
+            fb = (b[:, 0].astype(np.uint32) << 16).view(np.float32)
+            assert np.abs(fa - fb).max() <= 1e-2
+        slot_h = ko["slot_new"]
+    assert int(pipe.status.item()) == 0
+    assert 1 <= len(pipe._graphs) <= 10          # reused across ring periods: at most period x 2 captures
+
+
 # ------------------------------------------------------------------------------------------------------------
 # kv_refresh_paged (NEXT-1: in place, slot maps)
 # ------------------------------------------------------------------------------------------------------------
