@@ -508,6 +508,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         st_ty = [stage[0]["ty"], stage[1]["ty"]]
         st_fi = [stage[0]["fi"], stage[1]["fi"]]
         res = [torch.empty(S * 4 + S * s + 1, dtype=torch.int32).pin_memory() for _ in range(2)]
+        snap = [torch.zeros(S * 4 + S * s + 1, dtype=torch.int32, device=dev) for _ in range(2)]
         copy_stream = torch.cuda.Stream(dev)
         loaded = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
@@ -537,25 +538,34 @@ def run_ours(args, cfg, rank, world, local_rank):
                 # double-buffered outputs (parity b) were last read back by step i-2's results copy
                 evs = pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b], wait_events=[done[b]] if i >= 2 else [])
             else:
-                # single output buffers: step i overwrites them only after step i-1's results were copied out
-                if i >= 1:
-                    stream.wait_event(done[1 - b])
                 if args.graphs:
                     pipe.graph_step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b])
-                    e_step = torch.cuda.Event()
-                    e_step.record(stream)
-                    evs = {"step": (None, e_step)}
                 else:
-                    evs = pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b])
-            # results stream: waits for the step's kernels, reads the results back (D2H), releases the staging slot
+                    pipe.step(k, st_mb[b], ptr_s, st_fi[b], st_ty[b])
+                # the outputs are single-buffered: snapshot the step's results on the compute stream (device
+                # copies, stream-ordered before step i+1 overwrites them) into slot b, free once step i-2's
+                # read-back of slot b is done; the D2H then runs off the compute stream's critical path
+                if i >= 2:
+                    stream.wait_event(done[b])
+                if pipe.kv is not None:
+                    snap[b][:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
+                snap[b][S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
+                snap[b][-1:].copy_(pipe.frame_offsets[S * n // tp:S * n // tp + 1], non_blocking=True)
+                e_step = torch.cuda.Event()
+                e_step.record(stream)
+                evs = {"step": (None, e_step)}
+            # results stream: waits for the step, reads the results back (D2H), releases the staging slot
             for name in ("score", "compact", "kv", "step"):
                 if name in evs:
                     res_stream.wait_event(evs[name][1])
             with torch.cuda.stream(res_stream):
-                if pipe.kv is not None:                                    # D2H: the step's results
-                    res[b][:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
-                res[b][S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
-                res[b][-1:].copy_(pipe.frame_offsets[S * n // tp:S * n // tp + 1], non_blocking=True)
+                if args.overlap:
+                    if pipe.kv is not None:                                # D2H: the step's results
+                        res[b][:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
+                    res[b][S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
+                    res[b][-1:].copy_(pipe.frame_offsets[S * n // tp:S * n // tp + 1], non_blocking=True)
+                else:
+                    res[b].copy_(snap[b], non_blocking=True)               # D2H: the step's results
                 consumed[b].record(res_stream)
                 done[b].record(res_stream)
             if i >= 1:
