@@ -78,72 +78,44 @@ __device__ __forceinline__ void put_unit_word(const CompactParams& P, int slot, 
   P.unit_mask[((long long)s * P.unit_mask_stride + j) * P.nw + t] = w;
 }
 
-__global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_constant__ CompactParams P) {
-  __shared__ int s_warp[kScanThreads / 32];
-  __shared__ int s_cnt[kScanThreads];
-  __shared__ int s_carry;
-  __shared__ uint32_t s_m[kScanThreads / 32][128];  // per-warp unit mask (grid_words <= 128)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Per-slot emitted-patch counts, one WARP per slot over the whole grid (lane l holds word l of the mask on 32-wide
+// grids); the count goes to frame_offsets[slot] and is turned into the exclusive offset by compact_scan.  Also
+// writes the unit masks / types of temporal patches.
+constexpr int kCountThreads = 256;
+__global__ void __launch_bounds__(kCountThreads) compact_count(const __grid_constant__ CompactParams P) {
+  __shared__ uint32_t s_m[kCountThreads / 32][128];  // per-warp unit mask (grid_words <= 128)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = blockIdx.x * (kCountThreads / 32) + warp;
+  if (slot >= P.n_slots) return;
   const int gs2 = P.G * P.G;
-  const bool fast = (P.G == 2 && P.grid_w == 32 && P.nw <= 32);  // one mask word per patch row, one per lane
-  if (tid == 0) s_carry = 0;
-  __syncthreads();
-  for (int base = 0; base < P.n_slots; base += kScanThreads) {
-    // counts of this tile of slots: warp w handles slots w, w + 32, ...; lane l holds word l of the slot's mask
-    if (fast) {
-      // all 32 masks of the warp are loaded before any is reduced (32 coalesced 128-B loads in flight)
-      uint32_t wv[kScanThreads / 32];
+  int c = 0;
+  if (P.G == 2 && P.grid_w == 32 && P.nw <= 32) {
+    // word r = patch row r; group row g = rows 2g, 2g+1; fold horizontal pairs onto even bits
+    const uint32_t wv = lane < P.nw ? (P.tp == 1 ? __ldg(slot_mask(P, slot) + lane) : unit_word(P, slot, lane)) : 0u;
+    if (P.unit_mask && lane < P.nw) put_unit_word(P, slot, lane, wv);
+    const uint32_t x = wv | __shfl_down_sync(0xffffffffu, wv, 1);
+    c = (lane & 1) == 0 ? __popc((x | (x >> 1)) & 0x55555555u) : 0;
 #pragma unroll
-      for (int i = 0; i < kScanThreads / 32; ++i) {
-        const int slot = base + warp + 32 * i;
-        wv[i] = (slot < P.n_slots && lane < P.nw) ? (P.tp == 1 ? __ldg(slot_mask(P, slot) + lane)
-                                                                  : unit_word(P, slot, lane))
-                                                  : 0u;
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
+  } else {
+    const uint32_t* m = slot_mask(P, slot);
+    if (P.tp > 1 || P.unit_mask) {
+      for (int t = lane; t < P.nw; t += 32) {
+        const uint32_t w = unit_word(P, slot, t);
+        s_m[warp][t] = w;
+        if (P.unit_mask) put_unit_word(P, slot, t, w);
       }
-      if (P.unit_mask) {
-#pragma unroll
-        for (int i = 0; i < kScanThreads / 32; ++i) {
-          const int slot = base + warp + 32 * i;
-          if (slot < P.n_slots && lane < P.nw) put_unit_word(P, slot, lane, wv[i]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < kScanThreads / 32; ++i) {
-        // word r = patch row r; group row g = rows 2g, 2g+1; fold horizontal pairs onto even bits
-        const uint32_t x = wv[i] | __shfl_down_sync(0xffffffffu, wv[i], 1);
-        int c = (lane & 1) == 0 ? __popc((x | (x >> 1)) & 0x55555555u) : 0;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
-        if (lane == 0) s_cnt[warp + 32 * i] = c * gs2;
-      }
-    } else {
-      for (int j = warp; j < kScanThreads; j += kScanThreads / 32) {
-        const int slot = base + j;
-        int c = 0;
-        if (slot < P.n_slots) {
-          const uint32_t* m = slot_mask(P, slot);
-          if (P.tp > 1 || P.unit_mask) {
-            for (int t = lane; t < P.nw; t += 32) {
-              const uint32_t w = unit_word(P, slot, t);
-              s_m[warp][t] = w;
-              if (P.unit_mask) put_unit_word(P, slot, t, w);
-            }
-            __syncwarp();
-            m = s_m[warp];
-          }
-          for (int q0 = 0; q0 < P.ngroups; q0 += 32) {
-            const int q = q0 + lane;
-            c += __popc(__ballot_sync(0xffffffffu, q < P.ngroups && cs::group_kept(m, q, P.ngc, P.G, P.grid_w)));
-          }
-        }
-        if (lane == 0) s_cnt[j] = c * gs2;
-        __syncwarp();
-      }
+      __syncwarp();
+      m = s_m[warp];
     }
-    __syncthreads();
-    const int slot = base + tid;
-    const int cnt = s_cnt[tid];
-    if (P.unit_type && slot < P.n_slots) {
+    for (int q0 = 0; q0 < P.ngroups; q0 += 32) {
+      const int q = q0 + lane;
+      c += __popc(__ballot_sync(0xffffffffu, q < P.ngroups && cs::group_kept(m, q, P.ngc, P.G, P.grid_w)));
+    }
+  }
+  if (lane == 0) {
+    P.frame_offsets[slot] = c * gs2;
+    if (P.unit_type) {
       const int s = slot / P.n_frames, j = slot - s * P.n_frames;
       const uint8_t* ft = P.frame_type + (long long)s * P.mask_frame_stride + (long long)j * P.tp;
       uint8_t ty = CS_FRAME_P;
@@ -151,6 +123,20 @@ __global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_consta
         if (ft[f] != CS_FRAME_P) ty = CS_FRAME_I;
       P.unit_type[(long long)s * P.unit_mask_stride + j] = ty;
     }
+  }
+}
+
+// One CTA: frame_offsets[slot] (counts) -> exclusive scan in place (block-wide, running carry) + the total, capacity
+// status and counters.
+__global__ void __launch_bounds__(kScanThreads) compact_scan(const __grid_constant__ CompactParams P) {
+  __shared__ int s_warp[kScanThreads / 32];
+  __shared__ int s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < P.n_slots; base += kScanThreads) {
+    const int slot = base + tid;
+    const int cnt = slot < P.n_slots ? P.frame_offsets[slot] : 0;
     int inc = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -737,6 +723,10 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
   P.counters = counters;
   P.status = status;
 
+  if (P.n_slots > 0) {
+    compact_count<<<(P.n_slots + kCountThreads / 32 - 1) / (kCountThreads / 32), kCountThreads, 0, stream>>>(P);
+    if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+  }
   compact_scan<<<1, kScanThreads, 0, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   if (P.n_slots == 0 || capacity == 0) return CS_OK;

@@ -310,10 +310,11 @@ class Pipeline:
         self.cur = 1 - self.cur
 
     def kernel_launches_per_step(self, k: int) -> int:
-        """Kernels of this library launched by one step (score 1, compact 2 per chunk, kv_refresh 3)."""
+        """Kernels of this library launched by one step (score 1 or fused score+compact 1, compact 3 per chunk:
+        count + scan + gather, kv_refresh 3: plan + prefix + gather)."""
         _, nf = self.new_frames(k)
         c = nf if self.compact_chunk is None else min(nf, self.compact_chunk)
-        n = 1 if self.fused else 1 + 2 * ((nf + c - 1) // c)
+        n = 1 if self.fused else 1 + 3 * ((nf + c - 1) // c)
         if self.kv is not None:
             n += 3
         return n
