@@ -519,14 +519,14 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     };
     int written = 0;
     const bool tma = P.layout == CS_LAYOUT_GROUPED && P.vec_out && P.patch == 14 && P.G == 2 && P.grid_w == 32 &&
-                     P.grid_h == 32 && P.tma_stages >= 12;  // >= 3 stages per ring, else direct copies (measured)
+                     P.grid_h == 32 && P.tma_stages >= 9;  // R = stages/3 rings of >= 3 stages each, else direct copies (measured)
     if (tma) {
       // the CTA's share of the stream's kept groups: thread 0 runs a TMA bulk ring over it (4,704-B groups,
       // global -> smem on an mbarrier, smem -> global as a bulk group, the stage reused once the store has read
       // it) in the score's staging memory, which is free now; warps 1.. write the position ids / source indices
       const long long qa0 = groups * rank / P.cluster, qb0 = groups * (rank + 1) / P.cluster;
       // R ring warps (lane 0 of each drives its own TMA ring over its own stages and share of the range)
-      const int R = min(4, P.tma_stages / 2);
+      const int R = min(4, P.tma_stages / 3);
       const int wq = tid >> 5;
       const long long qa = qa0 + (qb0 - qa0) * min(wq, R) / R, qb = qa0 + (qb0 - qa0) * min(wq + 1, R) / R;
       __shared__ __align__(8) uint64_t s_tfull_all[kFusedMaxStages];
