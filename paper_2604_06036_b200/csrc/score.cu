@@ -47,7 +47,7 @@ struct ScoreParams {
   int32_t* kept_count;
   unsigned long long* counters;
   int32_t* status;
-  unsigned off_vrow, off_srow, off_dyn, off_bar;
+  unsigned off_vrow, off_srow, off_dyn, off_bar, off_stage;
   // ---- fused compaction (NEXT-2: codecsight_score_compact) ----
   int fused;
   int layout;            // CS_LAYOUT_PLANAR | CS_LAYOUT_GROUPED
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   const int tid = threadIdx.x, lane = tid & 31;
   const int nthr = blockDim.x;
 
-  unsigned char* stage = smem;
+  unsigned char* stage = smem + P.off_stage;
   uint32_t* Vrow = reinterpret_cast<uint32_t*>(smem + P.off_vrow);  // max |mv|^2 per (MB row, patch col)
   uint32_t* Srow = reinterpret_cast<uint32_t*>(smem + P.off_srow);
   uint32_t* dyn = reinterpret_cast<uint32_t*>(smem + P.off_dyn);
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
         uint64_t* s_tfull = s_tfull_all + sb;
         long long* s_tn0 = s_tn0_all + sb;
         const uint16_t** s_tsrc = s_tsrc_all + sb;
-        unsigned char* tbase = smem + (size_t)sb * 4736u;
+        unsigned char* tbase = smem + P.off_stage + (size_t)sb * 4736u;
         const long long row_el = 3ll * 14 * 14;
         for (int st = 0; st < nst; ++st) cs::mbar_init(&s_tfull[st], 1);
         cs::fence_mbar_init();
@@ -722,26 +722,36 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
   P.kept_count = kept_count;
   P.counters = counters;
   P.status = status;
-  unsigned off = P.nstage * P.chunk_alloc;
-  P.off_vrow = off;
-  off += ((static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u);
-  P.off_srow = off;
-  off += ((static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u);
+  // layout: small regions first, then the MB staging ring + Vrow + Srow, which the fused compaction reuses as its
+  // TMA stages once scoring is done (and may extend past them, up to kFusedSmem bytes per CTA)
+  unsigned off = 0;
   P.off_dyn = off;
   off += ((static_cast<unsigned>(P.fpc * P.nw) * 4u + 127u) & ~127u);
   P.off_bar = off;
-  off += 64u;
+  off += 128u;
   P.off_col = off;
   off += ((static_cast<unsigned>(g->grid_w) * 8u + 127u) & ~127u);
   P.off_row = off;
   off += ((static_cast<unsigned>(g->grid_h) * 8u + 127u) & ~127u);
-  const size_t smem = off;
+  P.off_stage = off;
+  off += P.nstage * P.chunk_alloc;
+  P.off_vrow = off;
+  off += ((static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u);
+  P.off_srow = off;
+  off += ((static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u);
+  size_t smem = off;
 
   if (smem > 200 * 1024) return CS_ERR_UNSUPPORTED;
   P.total_ctas = static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster);
-  {
-    const unsigned st = P.off_dyn / 4736u;
-    P.tma_stages = static_cast<int>(st > static_cast<unsigned>(kFusedMaxStages) ? kFusedMaxStages : st);
+  if (P.fused) {
+    // grow the staging region to kFusedSmem per CTA when that still leaves 3 CTAs per SM
+    constexpr unsigned kFusedSmem = 68u * 1024u;
+    const size_t want = smem < kFusedSmem ? kFusedSmem : smem;
+    unsigned st = static_cast<unsigned>((want - P.off_stage) / 4736u);
+    if (st > static_cast<unsigned>(kFusedMaxStages)) st = kFusedMaxStages;
+    P.tma_stages = static_cast<int>(st);
+    const size_t need = P.off_stage + static_cast<size_t>(st) * 4736u;
+    if (need > smem) smem = need;
   }
   const void* fn = P.fused ? reinterpret_cast<const void*>(score_kernel<true>)
                           : reinterpret_cast<const void*>(score_kernel<false>);
