@@ -170,13 +170,14 @@ def measured_peak_hbm():
     return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, workload: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu launch list, if it was captured on this workload."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        d = json.load(f)
-    return d.get(kernel, {}).get("dram_bytes_per_launch")
+        d = json.load(f).get(kernel, {})
+    return d.get("dram_bytes_per_launch") if d.get("workload") == workload else None
 
 
 # --------------------------------------------------------------------------------------------------------------
@@ -641,16 +642,20 @@ def run_ours(args, cfg, rank, world, local_rank):
                       "codecsight_kv_refresh (kv_plan + kv_prefix + kv_gather_tma)",
                       "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                       "frac": achieved / peak,
-                      "traffic": ncu_traffic("kv_refresh_paged" if args.kv_mode == "paged" else "kv_refresh_copy"),
+                      "traffic": ncu_traffic("kv_refresh_paged" if args.kv_mode == "paged" else "kv_refresh_copy",
+                                             cfg["name"]),
                       "algorithmic_bytes_per_launch": kv_bytes_launch} if kvb else
                      {"bound": "hbm", "kernel": ("codecsight_score_compact (score_kernel<fused>)" if args.fused else
                                                  "codecsight_compact (compact_scan + compact_gather)"),
                       "achieved": cmp_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                      "frac": cmp_gbs / peak, "traffic": ncu_traffic("compact_gather"),
+                      "frac": cmp_gbs / peak,
+                      "traffic": ncu_traffic("score_compact" if args.fused else "compact_gather", cfg["name"]),
                       "algorithmic_bytes_per_launch": cmp_bytes}),
         "secondary_roofline": {"kernel": "codecsight_score_compact" if args.fused else "codecsight_compact",
                                "achieved": cmp_gbs, "peak": peak,
-                               "frac": cmp_gbs / peak, "unit": "GB/s", "algorithmic_bytes_per_launch": cmp_bytes},
+                               "frac": cmp_gbs / peak, "unit": "GB/s", "algorithmic_bytes_per_launch": cmp_bytes,
+                               "traffic": ncu_traffic("score_compact" if args.fused else "compact_gather",
+                                                      cfg["name"])},
         "gpu_launches": K * pipe.kernel_launches_per_step(1),
         "clocks": clk,
     }
