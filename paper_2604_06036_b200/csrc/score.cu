@@ -65,7 +65,22 @@ struct ScoreParams {
   int tma_stages;  // 4,736-B TMA stages that fit the score's staging memory (fused compaction ring)
 };
 
-constexpr int kFusedMaxStages = 16;
+#ifdef CS_PHASE_TIMING
+// experiment build only (scripts/phase_timing.py): per-CTA %globaltimer stamps at the phase boundaries
+__device__ unsigned long long g_cs_phase[16384][12];
+__device__ __forceinline__ void cs_phase(int k) {
+  if (threadIdx.x == 0 && blockIdx.x < 16384) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_cs_phase[blockIdx.x][k] = t;
+  }
+}
+#define CS_PHASE(k) cs_phase(k)
+#else
+#define CS_PHASE(k)
+#endif
+
+constexpr int kFusedMaxStages = 42;  // 200 KB of 4,736-B stages (one-wave grids, see launch_score)
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kFlagVal = (1ull << 62) - 1;
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -148,6 +163,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   __shared__ unsigned long long s_near;
 
   __shared__ int s_sidx;
+  CS_PHASE(0);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   int sidx_ = blockIdx.x / P.cluster;
@@ -159,6 +175,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     sidx_ = *cluster.map_shared_rank(&s_sidx, 0);
   }
   const int sidx = sidx_;
+  CS_PHASE(1);
   const int tid = threadIdx.x, lane = tid & 31;
   const int nthr = blockDim.x;
 
@@ -172,36 +189,12 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   const int f_end = min(P.n_frames, f_begin + P.fpc);
   const int nw = P.nw;
 
-  // ---- prologue: frame types of the whole stream (the scan needs the earlier frames), GOP state in ----
-  for (int f = tid; f < P.n_frames; f += nthr) s_types[f] = P.frame_type[(long long)sidx * P.frame_stride + f];
-  for (int t = tid; t <= nw; t += nthr) s_state[t] = P.gop_state[(long long)sidx * (nw + 1) + t];
-  if (tid == 0) {
-    s_badmb = 0;
-    s_near = 0ull;
-    if (P.use_bulk)
-      for (int s = 0; s < P.nstage; ++s) cs::mbar_init(&bars[s], 1);
-    cs::fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int n = 0;
-    for (int f = f_begin; f < f_end; ++f)
-      if (s_types[f] == CS_FRAME_P) s_plist[n++] = f;
-    s_np = n;
-  }
-  __syncthreads();
-
-  const int T = s_np * P.n_chunks;  // chunk sequence over this CTA's P-frames
+  // ---- prologue: warp 0 reads this CTA's frame types, lists its P-frames and starts the MB loads at once; the
+  // other warps meanwhile stage the frame types of the whole stream (the scan needs the earlier frames), the GOP
+  // state and the MB column / row ranges of the patch columns / rows ----
   const cs_mb* stream_mb = P.mb_ptr + (long long)sidx * P.n_frames * P.mb_rows * P.mb_cols;
   int2* s_col = reinterpret_cast<int2*>(smem + P.off_col);  // [grid_w] MB column range of each patch column
   int2* s_row = reinterpret_cast<int2*>(smem + P.off_row);  // [grid_h] MB row range of each patch row
-  {
-    const int cw = P.mb * P.grid_w, ch = P.mb * P.grid_h;  // MB width / height in scaled units
-    for (int c = tid; c < P.grid_w; c += nthr) s_col[c] = make_int2((c * P.src_w) / cw, ((c + 1) * P.src_w - 1) / cw);
-    for (int r = tid; r < P.grid_h; r += nthr) s_row[r] = make_int2((r * P.src_h) / ch, ((r + 1) * P.src_h - 1) / ch);
-  }
-  __syncthreads();
-
   // producer (thread 0) walks the chunk sequence with its own counters: frame list index, chunk in frame, stage
   int pf = 0, pc = 0, ps = 0;
   auto issue_next = [&]() {
@@ -215,9 +208,36 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     if (++pc == P.n_chunks) { pc = 0; ++pf; }
     if (++ps == P.nstage) ps = 0;
   };
-  if (P.use_bulk && tid == 0)
-    for (int q = 0; q < min(T, P.nstage); ++q) issue_next();
+  if (tid < 32) {
+    const int f = f_begin + lane;  // fpc <= kMaxFramesPerCall / 8 = 32
+    const bool isP = f < f_end && P.frame_type[(long long)sidx * P.frame_stride + f] == CS_FRAME_P;
+    uint32_t pm = __ballot_sync(0xffffffffu, isP);
+    if (lane == 0) {
+      int n = 0;
+      for (; pm; pm &= pm - 1u) s_plist[n++] = f_begin + __ffs(pm) - 1;
+      s_np = n;
+      s_badmb = 0;
+      s_near = 0ull;
+      if (P.use_bulk) {
+        for (int st = 0; st < P.nstage; ++st) cs::mbar_init(&bars[st], 1);
+        cs::fence_mbar_init();
+        for (int q = 0; q < min(n * P.n_chunks, P.nstage); ++q) issue_next();
+      }
+    }
+  } else {
+    const int t0 = tid - 32, nt = nthr - 32;
+    for (int f = t0; f < P.n_frames; f += nt) s_types[f] = P.frame_type[(long long)sidx * P.frame_stride + f];
+    for (int t = t0; t <= nw; t += nt) s_state[t] = P.gop_state[(long long)sidx * (nw + 1) + t];
+    const int cw = P.mb * P.grid_w, ch = P.mb * P.grid_h;  // MB width / height in scaled units
+    for (int c = t0; c < P.grid_w; c += nt) s_col[c] = make_int2((c * P.src_w) / cw, ((c + 1) * P.src_w - 1) / cw);
+    for (int r = t0; r < P.grid_h; r += nt) s_row[r] = make_int2((r * P.src_h) / ch, ((r + 1) * P.src_h - 1) / ch);
+  }
+  __syncthreads();
+  const int T = s_np * P.n_chunks;  // chunk sequence over this CTA's P-frames
+  // every chunk of every P-frame of this CTA is in flight at once: warps need not wait for each other per chunk
+  const bool resident = T <= P.nstage;
 
+  CS_PHASE(2);
   unsigned long long near_local = 0;
   const int lane_w = tid >> 5, nwarps = nthr >> 5;
   const int cw = P.mb * P.grid_w;
@@ -229,6 +249,8 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     const uint2* buf = reinterpret_cast<const uint2*>(stage + (size_t)cs_ * P.chunk_alloc);
     if (P.use_bulk) {
       cs::mbar_wait(&bars[cs_], cph);
+      if (q == 0) CS_PHASE(3);
+      if (q == T - 1) CS_PHASE(10);
     } else {
       const uint2* g = reinterpret_cast<const uint2*>(stream_mb + ((long long)f * P.mb_rows + r0) * P.mb_cols);
       uint2* d = reinterpret_cast<uint2*>(stage + (size_t)cs_ * P.chunk_alloc);
@@ -268,14 +290,18 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       }
     }
     if (badmb) s_badmb = 1;
-    __syncthreads();  // chunk fully consumed, Vrow/Srow rows complete
-    if (P.use_bulk && tid == 0 && q + P.nstage < T) issue_next();
+    if (!resident) {
+      __syncthreads();  // chunk fully consumed (its stage is refilled below), Vrow/Srow rows complete
+      if (P.use_bulk && tid == 0 && q + P.nstage < T) issue_next();
+    }
     if (++cs_ == P.nstage) { cs_ = 0; cph ^= 1; }
 
     if (++cc == P.n_chunks) {
       cc = 0;
       ++cf;
       // ---- pass 2: patch rows; Eq. 3 and Eq. 4; ballot into dynamic words ------------------------------
+      if (resident) __syncthreads();  // Vrow/Srow rows of the frame complete
+      CS_PHASE(9);
       const int lf = f - f_begin;
       const int ch = P.mb * P.grid_h;  // MB height in scaled y units
       for (int i = tid; i < nw * 32; i += nthr) {
@@ -326,6 +352,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       if (s_types[f] != CS_FRAME_P)
         for (int i = tid; i < P.np; i += nthr) P.score[((long long)sidx * P.n_frames + f) * P.np + i] = CUDART_INF_F;
 
+  CS_PHASE(4);
   cluster.sync();  // every CTA's dynamic words are published
 
   // ---- segmented OR-scan over time (GOP accumulation) + group-complete expansion ----------
@@ -409,6 +436,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   }
 
   // ---- counters / status -------------------------------------------------------------------------------
+  CS_PHASE(5);
   if (near_local) atomicAdd(&s_near, near_local);
   __syncthreads();
   if (tid == 0) {
@@ -435,14 +463,23 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     __shared__ long long s_prefix;
     __shared__ int s_written;
     cluster.sync();  // the stream's keep masks and kept counts are in global memory (cluster-scope acquire)
-    if (tid == 0) {
-      int acc = 0;
-      for (int f = 0; f < P.n_frames; ++f) {
-        s_lp[f] = acc;
-        acc += P.kept_count[(long long)sidx * P.n_frames + f];
+    if (tid < 32) {  // s_lp = exclusive prefix of the stream's kept counts (warp scan, 32 frames per round)
+      int carry = 0;
+      for (int f0 = 0; f0 < P.n_frames; f0 += 32) {
+        const int f = f0 + lane;
+        int v = f < P.n_frames ? P.kept_count[(long long)sidx * P.n_frames + f] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, v, d);
+          if (lane >= d) v += u;
+        }
+        if (f < P.n_frames) s_lp[f + 1] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
       }
-      s_lp[P.n_frames] = acc;
-      s_written = 0;
+      if (lane == 0) {
+        s_lp[0] = 0;
+        s_written = 0;
+      }
     }
     __syncthreads();
     if (rank == 0 && tid < 32) {
@@ -480,6 +517,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     }
     cluster.sync();
     const long long pre = *cluster.map_shared_rank(&s_prefix, 0);
+    CS_PHASE(6);
     for (int f = f_begin + tid; f < f_end; f += nthr)
       P.frame_offsets[(long long)sidx * P.n_frames + f] = static_cast<int32_t>(pre + s_lp[f]);
     const int gs2 = P.G * P.G;
@@ -652,6 +690,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     }
     if ((lane == 0 || tma) && written) atomicAdd(&s_written, written);
     __syncthreads();
+    CS_PHASE(7);
     if (tid == 0) {
       const unsigned long long rows = static_cast<unsigned long long>(s_written);
       const unsigned long long row_bytes = 3ull * P.patch * P.patch * 2ull;
@@ -668,10 +707,35 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       }
     }
   }
+  CS_PHASE(8);
   cluster.sync();  // keep this CTA's shared memory alive until every DSMEM reader is done
 }
 
 }  // namespace
+
+constexpr unsigned kWideSmem = 200u * 1024u;  // the kernels' dynamic shared memory limit (set once per device)
+
+// true when all n_streams clusters of `cfg` are co-resident with kWideSmem bytes of dynamic shared memory per CTA
+// (cudaOccupancyMaxActiveClusters; the answer for the last (device, cluster size) is cached)
+static bool fused_one_wave(const void* fn, const cudaLaunchConfig_t& cfg, int32_t n_streams) {
+  static thread_local int c_dev = -1, c_cluster = -1, c_max = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const int cl = static_cast<int>(cfg.attrs[0].val.clusterDim.x);
+  if (dev != c_dev || cl != c_cluster) {
+    cudaLaunchConfig_t q = cfg;
+    q.dynamicSmemBytes = kWideSmem;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &q) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    c_dev = dev;
+    c_cluster = cl;
+    c_max = n;
+  }
+  return n_streams <= c_max;
+}
 
 static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
                         const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride, uint32_t* gop_state,
@@ -707,8 +771,6 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
   if (P.chunk_rows > P.mb_rows) P.chunk_rows = P.mb_rows;
   P.n_chunks = (P.mb_rows + P.chunk_rows - 1) / P.chunk_rows;
   P.chunk_alloc = (static_cast<unsigned>(P.chunk_rows) * P.row_bytes + 127u) & ~127u;
-  P.nstage = P.chunk_alloc <= 8192u ? 4 : 2;
-  if (!P.use_bulk) P.nstage = 1;
   P.want_score = score != nullptr;
   P.use_r = g->alpha != 0.0f;
   P.gw_shift = -1;
@@ -722,8 +784,32 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
   P.kept_count = kept_count;
   P.counters = counters;
   P.status = status;
-  // layout: small regions first, then the MB staging ring + Vrow + Srow, which the fused compaction reuses as its
-  // TMA stages once scoring is done (and may extend past them, up to kFusedSmem bytes per CTA)
+  P.total_ctas = static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster);
+  const void* fn = P.fused ? reinterpret_cast<const void*>(score_kernel<true>)
+                          : reinterpret_cast<const void*>(score_kernel<false>);
+  if (cs_set_smem_attr(fn, P.fused ? 19 : 0, kWideSmem) != 0) return CS_ERR_CUDA;
+
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster), 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+
+  // dynamic shared memory budget per CTA: 50 KB for score_patches (4 CTAs/SM, register-limited anyway), 68 KB for
+  // the fused kernel (3 CTAs/SM; the compaction's TMA rings reuse the staging memory), and the SM's whole 200 KB
+  // when all the fused grid's clusters are co-resident even then (one wave at one CTA per SM, e.g. C2): deeper
+  // rings, more bytes in flight per SM (measured)
+  unsigned budget = P.fused ? 68u * 1024u : 50u * 1024u;
+  if (P.fused && fused_one_wave(fn, cfg, n_streams)) budget = kWideSmem;
+
+  // layout: small regions first, then the MB staging ring, Vrow, Srow (only with alpha != 0); the MB ring takes
+  // whatever the budget leaves (all of a frame's chunks in flight when they fit, at most 16 mbarriers, >= 2 stages)
   unsigned off = 0;
   P.off_dyn = off;
   off += ((static_cast<unsigned>(P.fpc * P.nw) * 4u + 127u) & ~127u);
@@ -734,41 +820,29 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
   P.off_row = off;
   off += ((static_cast<unsigned>(g->grid_h) * 8u + 127u) & ~127u);
   P.off_stage = off;
+  const unsigned vr_bytes = (static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u;
+  const unsigned fixed = off + vr_bytes + (P.use_r ? vr_bytes : 0u);
+  int nst = fixed + 2u * P.chunk_alloc <= budget ? static_cast<int>((budget - fixed) / P.chunk_alloc) : 2;
+  nst = nst > P.n_chunks ? P.n_chunks : nst;
+  nst = nst > 16 ? 16 : (nst < 2 ? 2 : nst);
+  P.nstage = P.use_bulk ? nst : 1;
   off += P.nstage * P.chunk_alloc;
   P.off_vrow = off;
-  off += ((static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u);
+  off += vr_bytes;
   P.off_srow = off;
-  off += ((static_cast<unsigned>(P.mb_rows * P.grid_w) * 4u + 127u) & ~127u);
+  off += P.use_r ? vr_bytes : 0u;
   size_t smem = off;
-
-  if (smem > 200 * 1024) return CS_ERR_UNSUPPORTED;
-  P.total_ctas = static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster);
+  if (smem > kWideSmem) return CS_ERR_UNSUPPORTED;
   if (P.fused) {
-    // grow the staging region to kFusedSmem per CTA when that still leaves 3 CTAs per SM
-    constexpr unsigned kFusedSmem = 68u * 1024u;
-    const size_t want = smem < kFusedSmem ? kFusedSmem : smem;
+    // the compaction's TMA rings: 4,736-B stages from off_stage up to the budget
+    const size_t want = smem < budget ? budget : smem;
     unsigned st = static_cast<unsigned>((want - P.off_stage) / 4736u);
     if (st > static_cast<unsigned>(kFusedMaxStages)) st = kFusedMaxStages;
     P.tma_stages = static_cast<int>(st);
     const size_t need = P.off_stage + static_cast<size_t>(st) * 4736u;
     if (need > smem) smem = need;
   }
-  const void* fn = P.fused ? reinterpret_cast<const void*>(score_kernel<true>)
-                          : reinterpret_cast<const void*>(score_kernel<false>);
-  if (cs_set_smem_attr(fn, P.fused ? 19 : 0, 200 * 1024) != 0) return CS_ERR_CUDA;
-
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster), 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
   void* args[] = {&P};
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
@@ -813,3 +887,10 @@ int cs_launch_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frame
   return launch_score(g, n_streams, n_frames, mb, frame_type, keep_mask, frame_stride, gop_state, score, kept_count,
                       counters, status, &F, stream);
 }
+
+#ifdef CS_PHASE_TIMING
+extern "C" int codecsight_debug_phase(unsigned long long* host, int n_ctas) {
+  if (n_ctas > 16384) n_ctas = 16384;
+  return cudaMemcpyFromSymbol(host, g_cs_phase, sizeof(unsigned long long) * 12 * n_ctas) == cudaSuccess ? 0 : -1;
+}
+#endif
