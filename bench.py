@@ -34,8 +34,8 @@ import synth  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)   # 10 warm-up steps, >= 50 timed
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--streams", type=int, default=None, help="streams per GPU (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
