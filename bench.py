@@ -686,6 +686,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     else:
         cmp_ms = float(np.mean(per["compact"]))
     cmp_gbs = cmp_bytes / (cmp_ms / 1e3) / 1e9
+    step_bytes = float(dcnt[abi.CNT_BYTES_SCORE].item() + dcnt[abi.CNT_BYTES_COMPACT].item() +
+                       dcnt[abi.CNT_BYTES_KV].item()) / K
     kept_frac = float(dcnt[abi.CNT_KEPT].item()) / max(1.0, float(dcnt[abi.CNT_PATCHES].item()))
     out = {
         "metric": "codec-pruned frames/sec (whole hot path: score+compact+kv_refresh), all GPUs",
@@ -736,6 +738,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                                "frac": cmp_gbs / peak, "unit": "GB/s", "algorithmic_bytes_per_launch": cmp_bytes,
                                "traffic": ncu_traffic("score_compact" if args.fused else "compact_gather",
                                                       cfg["name"])},
+        # the whole step against the same roofline: every call's algorithmic bytes per step / the step's time
+        "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms_max / K / 1e3) / 1e9,
+                          "peak": peak, "unit": "GB/s", "frac": step_bytes / (ms_max / K / 1e3) / 1e9 / peak},
         "gpu_launches": K * pipe.kernel_launches_per_step(1),
         # the paper's own numbers for this path (context, not the target): per-request overheads of its Python
         # implementation on vLLM/LMCache, InternVL3 on 2 x A100 40GB SXM4; a request there is
