@@ -1,9 +1,10 @@
-"""Full-size parity in the bench's own launch configuration (BASELINE configs C4 and C5 shapes).
+"""Full-size parity in the bench's own launch configuration (BASELINE configs C3, C4 and C5 shapes).
 
 The GPU runs the whole batch of streams exactly as bench.py does (Pipeline, paged KV, grouped frames); the oracle,
 which is per-stream independent, re-runs a deterministic sample of streams from the same inputs and every output of
 those streams is compared (masks, GOP state, compaction rows of their frames, dispositions, p_old, slot maps and the
-pool rows).  Sizes: C4 = 256 1080p streams (w=16, s=4, 28-layer Qwen2-VL-7B KV); C5 = 128 4K streams (w=64, s=8).
+pool rows).  Sizes: C4 = 256 1080p streams (w=16, s=4, 28-layer Qwen2-VL-7B KV); C3 = 64 1080p streams (w=32, s=4); C5 = 128 4K
+streams (w=64, s=8); fused = the bench's default one-launch score+compact.
 """
 import numpy as np
 import pytest
@@ -29,7 +30,9 @@ def to_grouped(frame, g):
 
 @pytest.mark.parametrize("cfg_name,S,steps,sample,fused", [("C4", 256, 3, [0, 1, 254, 255], False),
                                                           ("C4", 256, 3, [0, 1, 254, 255], True),
-                                                          ("C5", 128, 2, [0, 127], False)])
+                                                          ("C3", 64, 3, [0, 63], True),
+                                                          ("C5", 128, 2, [0, 127], False),
+                                                          ("C5", 128, 2, [0, 127], True)])
 def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused):
     import gc
     gc.collect()
