@@ -629,7 +629,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                     stream.wait_event(done[b])
                 if pipe.kv is not None:
                     snap[b][:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
-                snap[b][S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
+                snap[b][S * 4:S * 4 + S * n].copy_(pipe.kept_counts(n).reshape(-1), non_blocking=True)
                 snap[b][-1:].copy_(pipe.frame_offsets[S * n // tp:S * n // tp + 1], non_blocking=True)
                 e_step = torch.cuda.Event()
                 e_step.record(stream)
@@ -642,7 +642,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 if args.overlap:
                     if pipe.kv is not None:                                # D2H: the step's results
                         res[b][:S * 4].copy_(pipe.n_tokens.view(-1), non_blocking=True)
-                    res[b][S * 4:S * 4 + S * n].copy_(pipe.kept_count[:, :n].reshape(-1), non_blocking=True)
+                    res[b][S * 4:S * 4 + S * n].copy_(pipe.kept_counts(n).reshape(-1), non_blocking=True)
                     res[b][-1:].copy_(pipe.frame_offsets[S * n // tp:S * n // tp + 1], non_blocking=True)
                 else:
                     res[b].copy_(snap[b], non_blocking=True)               # D2H: the step's results

@@ -214,6 +214,30 @@ def codecsight_score_compact(g: dict, n_streams: int, n_frames: int, mb, frame_t
     _check(rc, "codecsight_score_compact")
 
 
+class BoundScoreCompact:
+    """codecsight_score_compact with every argument but the per-step inputs (mb, frame_index, frames, stream)
+    marshalled once: the Pipeline's per-step host cost is then one ctypes call (same C entry point, same checks)."""
+
+    def __init__(self, g: dict, n_streams: int, n_frames: int, frame_type, keep_mask, frame_stride: int, gop_state,
+                 score, kept_count, capacity: int, packed, pos_ids, src_index, frame_offsets, workspace, counters,
+                 status, frame_layout: int = CS_LAYOUT_PLANAR):
+        self._grid = make_grid(g)  # kept alive: passed by reference on every call
+        self._fn = lib().codecsight_score_compact
+        self._head = (C.byref(self._grid), n_streams, n_frames)
+        self._mid = (_ptr(frame_type), _ptr(keep_mask), frame_stride, _ptr(gop_state), _ptr(score),
+                     _ptr(kept_count))
+        self._tail = (frame_layout, capacity, _ptr(packed), _ptr(pos_ids), _ptr(src_index), _ptr(frame_offsets),
+                      _ptr(workspace), workspace.numel() * workspace.element_size(), _ptr(counters), _ptr(status))
+
+    def __call__(self, mb, frame_index, frames, stream: int) -> None:
+        if not (mb.is_cuda and frame_index.is_cuda and frames.is_cuda):
+            raise CodecSightError("expected CUDA tensors")
+        rc = self._fn(*self._head, mb.data_ptr(), *self._mid, frame_index.data_ptr(), frames.data_ptr(), *self._tail,
+                      stream)
+        if rc != CS_OK:
+            _check(rc, "codecsight_score_compact")
+
+
 def codecsight_compact_tp(g: dict, temporal_patch: int, n_streams: int, n_units: int, keep_mask,
                           mask_frame_stride: int, unit_index, frames, capacity: int, packed, pos_ids, src_index,
                           frame_offsets, counters, status, frame_layout: int = CS_LAYOUT_PLANAR, unit_mask=None,

@@ -122,6 +122,8 @@ class Pipeline:
             self.sc_workspace = torch.zeros(abi.score_compact_workspace_size(S), dtype=torch.uint8, device=d)
         self._side_done = {}  # step -> events closing its compact / kv_refresh work (overlap mode)
         self._graphs = {}     # graph_step: key -> captured torch.cuda.CUDAGraph
+        self._bound = {}      # (ring slot, frames) -> abi.BoundScoreCompact
+        self._type_views = {}
         if overlap:
             self.stream_compact = torch.cuda.Stream(d)
             self.stream_kv = torch.cuda.Stream(d)
@@ -144,6 +146,15 @@ class Pipeline:
         for lst in self.caches + ([self.refreshed] if self.refreshed is not None else []):
             for t in lst:
                 t.normal_(generator=gen)
+
+    def kept_counts(self, n: int) -> torch.Tensor:
+        """[S][n] kept-patch counts of a step's n new frames: the calls write a contiguous [n_streams][n_frames]
+        array, i.e. the first S*n elements of the buffer (not the strided [:, :n] slice of its [S][window] shape)."""
+        return self.kept_count.view(-1)[: self.S * n].view(self.S, n)
+
+    def scores(self, n: int):
+        """[S][n][patches] scores of a step's n new frames (contiguous prefix of the buffer), or None."""
+        return None if self.score is None else self.score.view(-1)[: self.S * n * self.np].view(self.S, n, self.np)
 
     def step(self, k: int, mb: torch.Tensor, frame_ptrs: torch.Tensor, frame_index: torch.Tensor | None = None,
              types: torch.Tensor | None = None, use_refreshed: bool | None = None, do_kv: bool = True,
@@ -175,22 +186,27 @@ class Pipeline:
                 main.wait_event(e)
         with torch.cuda.stream(main):
             if types is not None:
-                self.type_ring[:, off:off + n].copy_(types, non_blocking=True)
+                tv = self._type_views.get((off, n))
+                if tv is None:
+                    tv = self._type_views[(off, n)] = self.type_ring[:, off:off + n]
+                tv.copy_(types, non_blocking=True)
             s0 = ev(main)
             if self.fused:
                 fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
-                abi.codecsight_score_compact(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:],
-                                             self.ring, self.gop_state,
-                                             None if self.score is None else self.score[:, :n],
-                                             self.kept_count[:, :n], fi, frame_ptrs, self.capacity, self.packed,
-                                             self.pos_ids, self.src_index, self.frame_offsets[: self.S * n + 1],
-                                             self.sc_workspace, self.counters, self.status,
-                                             frame_layout=self.frame_layout, stream=main)
+                call = self._bound.get((off, n))
+                if call is None:  # arguments of this ring slot marshalled once (fused mode has no buffer parity)
+                    call = abi.BoundScoreCompact(
+                        g, self.S, n, self.type_ring[:, off:], self.mask_ring[:, off:], self.ring, self.gop_state,
+                        self.scores(n), self.kept_counts(n), self.capacity, self.packed, self.pos_ids,
+                        self.src_index, self.frame_offsets[: self.S * n + 1], self.sc_workspace, self.counters,
+                        self.status, frame_layout=self.frame_layout)
+                    self._bound[(off, n)] = call
+                call(mb, fi, frame_ptrs, main.cuda_stream)
             else:
                 abi.codecsight_score_patches(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:],
                                              self.ring, self.gop_state,
-                                             None if self.score is None else self.score[:, :n],
-                                             self.kept_count[:, :n], self.counters, self.status, main)
+                                             self.scores(n),
+                                             self.kept_counts(n), self.counters, self.status, main)
             out["score"] = (s0, ev(main))
         cs_stream = self.stream_compact if self.overlap else main
         kv_stream = self.stream_kv if self.overlap else main

@@ -69,16 +69,32 @@ def run():
             gs = torch.zeros(S, nw + 1, dtype=torch.int32, device=dev)
             gs[:, nw] = 1
             torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             abi.codecsight_score_compact(g, S, n, mb_d, types, km, n, gs, None, kc, fidx, fptr, cap, packed, pos, src,
                                          offs, ws, cnt, st, frame_layout=abi.CS_LAYOUT_GROUPED)
+            e1.record()
             torch.cuda.synchronize()
+            ev_ms = e0.elapsed_time(e1)
             h = np.zeros((nct, 12), np.uint64)
             assert L.codecsight_debug_phase(h.ctypes.data, nct) == 0
             if rep >= 2:
                 res.append(h.astype(np.int64) - int(h[:, 0].min()))
+        gs = torch.zeros(S, nw + 1, dtype=torch.int32, device=dev)
+        gs[:, nw] = 1
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            abi.codecsight_score_compact(g, S, n, mb_d, types, km, n, gs, None, kc, fidx, fptr, cap, packed, pos, src,
+                                         offs, ws, cnt, st, frame_layout=abi.CS_LAYOUT_GROUPED)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"   20 back-to-back calls: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us per call")
         kept = float(kc.sum().item()) / (S * n * 1024)
         print(f"== {name}: {S} streams x {n} frames, {nct} CTAs, kept {kept:.2f}")
         labels = ["start", "ticket", "prologue", "1st chunk", "scored", "masks", "offset", "compacted", "end"]
+        print(f"   CUDA-event time of the call: {ev_ms * 1e3:.1f} us (launch + CTA span + drain)")
         for r in res[-1:]:
             for k, lab in enumerate(labels):
                 v = r[:, k] / 1e3

@@ -705,6 +705,7 @@ def test_pipeline_end_to_end_c4_shape(abi, ref, overlap):
         mring_h[:, off:off + n] = so["keep_mask"][:, :n]
         assert (u32(pipe.mask_ring) == mring_h).all()
         assert (u32(pipe.gop_state) == gop_h).all()
+        assert (pipe.kept_counts(n).cpu().numpy() == so["kept_count"]).all()
         co = ref.compact(g, mring_h[:, off:].copy(), fidx, frames_h[:S * n], pipe.capacity, S, n,
                          mask_frame_stride=ring - off)
         tot = int(co["frame_offsets"][-1])
