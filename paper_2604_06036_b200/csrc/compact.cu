@@ -308,10 +308,71 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     // preprocess only the kept group's 3 x gp x gp model pixels straight from the decoded NV12 frame
     const uint8_t* Yp = reinterpret_cast<const uint8_t*>(frame);
     const uint8_t* UVp = static_cast<const uint8_t*>(P.uv_planes[slot]);
-    // batches of 4 output pixels per lane: the 4 x (4 luma bytes + 4 chroma pairs) loads of a batch are all
-    // issued before any is consumed (memory-level parallelism), then converted, interpolated and normalised
-    constexpr int kB = TP > 0 ? 1 : 4;
     const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
+    if (TP > 0 && TG == 2 && gp <= 32) {
+      // fast path (issue-bound: every instruction per pixel counts).  The source taps of output column xx / row yy
+      // are computed once per group by lane xx / yy and fetched with shuffles; the pixel's (yy, xx) advance by
+      // (32 / gp, 32 % gp) per round; the bf16 store is the hardware RNE conversion (the outputs are never NaN:
+      // std > 0 and mean is not NaN are checked on the host, so it equals the oracle's rounding bit for bit).
+      int ax0 = 0, ay0 = 0;
+      float alx = 0.0f, aly = 0.0f;
+      if (lane < gp) {
+        int i1;
+        nv12_axis(gc * gp + lane, P.src_w, P.scale_x, ax0, i1, alx);
+        nv12_axis(gr * gp + lane, P.src_h, P.scale_y, ay0, i1, aly);
+      }
+      int yy = lane / gp, xx = lane - (lane / gp) * gp;
+      for (int e0 = 0; e0 < gp * gp; e0 += 32) {  // warp-uniform trip count (the shuffles need every lane)
+        const int x0 = __shfl_sync(0xffffffffu, ax0, xx), y0 = __shfl_sync(0xffffffffu, ay0, yy);
+        const float lx = __shfl_sync(0xffffffffu, alx, xx), ly = __shfl_sync(0xffffffffu, aly, yy);
+        if (e0 + lane >= gp * gp) break;  // last round: the lanes past the group's end are done
+        const int x1 = x0 + (x0 < P.src_w - 1 ? 1 : 0), y1 = y0 + (y0 < P.src_h - 1 ? 1 : 0);
+        const uint8_t* r0 = Yp + (long long)y0 * P.y_pitch;
+        const uint8_t* r1 = Yp + (long long)y1 * P.y_pitch;
+        const uint8_t* c0 = UVp + (long long)(y0 >> 1) * P.uv_pitch;
+        const uint8_t* c1 = UVp + (long long)(y1 >> 1) * P.uv_pitch;
+        const uint32_t yv[4] = {__ldg(r0 + x0), __ldg(r0 + x1), __ldg(r1 + x0), __ldg(r1 + x1)};
+        const uint32_t uvv[4] = {__ldg(reinterpret_cast<const uint16_t*>(c0 + 2 * (x0 >> 1))),
+                                 __ldg(reinterpret_cast<const uint16_t*>(c0 + 2 * (x1 >> 1))),
+                                 __ldg(reinterpret_cast<const uint16_t*>(c1 + 2 * (x0 >> 1))),
+                                 __ldg(reinterpret_cast<const uint16_t*>(c1 + 2 * (x1 >> 1)))};
+        float rgb[4][3];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float c = static_cast<float>(static_cast<int>(yv[q]) - 16);
+          const float d = static_cast<float>(static_cast<int>(uvv[q] & 0xffu) - 128);
+          const float ee = static_cast<float>(static_cast<int>(uvv[q] >> 8) - 128);
+          rgb[q][0] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kRV, ee)), 0.0f), 255.0f);
+          rgb[q][1] = fminf(fmaxf(__fsub_rn(__fsub_rn(__fmul_rn(kY, c), __fmul_rn(kGU, d)), __fmul_rn(kGV, ee)), 0.0f),
+                            255.0f);
+          rgb[q][2] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kBU, d)), 0.0f), 255.0f);
+        }
+        const float hx = __fsub_rn(1.0f, lx), hy = __fsub_rn(1.0f, ly);
+        const int dy = yy >= p ? 1 : 0, y = yy - dy * p, dx = xx >= p ? 1 : 0, x = xx - dx * p;
+        uint16_t* tq = tile + (dy * G + dx) * 3 * pp + y * p + x;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float top = __fadd_rn(__fmul_rn(hx, rgb[0][c]), __fmul_rn(lx, rgb[1][c]));
+          const float bot = __fadd_rn(__fmul_rn(hx, rgb[2][c]), __fmul_rn(lx, rgb[3][c]));
+          const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
+          // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
+          // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
+          const float q255 = __fmul_rn(v, kInv255);
+          const float t = __fmaf_rn(__fmaf_rn(-q255, 255.0f, v), kInv255, q255);
+          const float o = __fdiv_rn(__fsub_rn(t, P.mean[c]), P.stdv[c]);
+          tq[c * pp] = cs::f32_to_bf16_cvt(o);
+        }
+        xx += 32 % gp;
+        yy += 32 / gp;
+        if (xx >= gp) {
+          xx -= gp;
+          ++yy;
+        }
+      }
+    } else {
+    // generic path: batches of 4 output pixels per lane: the 4 x (4 luma bytes + 4 chroma pairs) loads of a batch
+    // are all issued before any is consumed (memory-level parallelism), then converted, interpolated, normalised
+    constexpr int kB = 4;
     for (int e0 = 0; e0 < gp * gp; e0 += 32 * kB) {
       uint32_t yv[kB][4], uvv[kB][4];
       float lyv[kB], lxv[kB];
@@ -356,14 +417,13 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
           const float top = __fadd_rn(__fmul_rn(hx, rgb[0][c]), __fmul_rn(lx, rgb[1][c]));
           const float bot = __fadd_rn(__fmul_rn(hx, rgb[2][c]), __fmul_rn(lx, rgb[3][c]));
           const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
-          // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
-          // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
           const float q255 = __fmul_rn(v, kInv255);
           const float t = __fmaf_rn(__fmaf_rn(-q255, 255.0f, v), kInv255, q255);
           const float o = __fdiv_rn(__fsub_rn(t, P.mean[c]), P.stdv[c]);
           tile[((dy * G + dx) * 3 + c) * pp + y * p + x] = static_cast<uint16_t>(cs::f32_to_bf16_rne(o));
         }
       }
+    }
     }
   } else if (vec_in) {
     // 8-byte loads: each group row segment is gp pixels = gp/4 pieces of 4 bf16.  Pairs of pixels never

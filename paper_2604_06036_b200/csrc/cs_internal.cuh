@@ -110,6 +110,13 @@ CS_DEV uint32_t f32_to_bf16_rne(float f) {
   return u >> 16;
 }
 
+// fp32 -> bf16 bits, round to nearest even, one cvt.rn.bf16.f32 (equal to f32_to_bf16_rne for every non-NaN f)
+CS_DEV uint16_t f32_to_bf16_cvt(float f) {
+  uint16_t r;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(f));
+  return r;
+}
+
 // two fp32 -> packed bf16x2 (low half = lo), round to nearest even (cvt.rn.bf16x2.f32)
 CS_DEV uint32_t pack_bf16x2_rn(float lo, float hi) {
   uint32_t r;
