@@ -39,6 +39,11 @@ def parse():
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--streams", type=int, default=None, help="streams per GPU (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tau", type=float, default=0.25, help="Eq. 4 threshold in source px (P:459)")
+    ap.add_argument("--alpha", type=float, default=0.0, help="Eq. 3 residual weight (P:299)")
+    ap.add_argument("--window-frames", type=int, default=None, help="window w (default: the workload's)")
+    ap.add_argument("--stride-frames", type=int, default=None, help="stride s (default: the workload's)")
+    ap.add_argument("--gop", type=int, default=None, help="I-frame period (default: the workload's)")
     ap.add_argument("--pool", type=int, default=6, help="distinct metadata steps kept on the device")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -75,8 +80,17 @@ def log(*a):
 # --------------------------------------------------------------------------------------------------------------
 # workload
 # --------------------------------------------------------------------------------------------------------------
-def workload(name: str, streams: int | None, kv_mode: str = "paged"):
+def workload(name: str, streams: int | None, kv_mode: str = "paged", args=None):
     cfg = dict(synth.CONFIGS[name])
+    # method parameters (SPEC CLI names): defaults are the paper's (tau 0.25 px, alpha 0)
+    cfg["tau"] = getattr(args, "tau", 0.25)
+    cfg["alpha"] = getattr(args, "alpha", 0.0)
+    for key, opt in (("window", "window_frames"), ("stride", "stride_frames"), ("gop", "gop")):
+        v = getattr(args, opt, None)
+        if v is not None:
+            cfg[key] = v
+    if not 1 <= cfg["stride"] <= cfg["window"]:
+        raise SystemExit("need 1 <= stride <= window (S:129)")
     if cfg["kv"] is None and name != "C2":
         raise SystemExit(f"workload {name} has no KV shape")
     if name == "C5":
@@ -193,7 +207,7 @@ def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "pag
     spent."""
     import oracle.ref as ref
     sw, sh = cfg["src"]
-    g = synth.make_grid(sw, sh)
+    g = synth.make_grid(sw, sh, tau=cfg["tau"], alpha=cfg["alpha"])
     w, s, gop = cfg["window"], cfg["stride"], cfg["gop"]
     ring = w + s
     nw = (g["grid_w"] * g["grid_h"] + 31) // 32
@@ -358,7 +372,8 @@ def run_reference(args, cfg, rank, world):
            "ms_per_step": 1000.0 * tot["seconds"] / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
            "config": {"workload": cfg["name"], "streams_per_gpu": cfg["streams"], "window": cfg["window"],
-                      "stride": cfg["stride"], "gop": cfg["gop"], "temporal_patch": args.temporal_patch},
+                      "stride": cfg["stride"], "gop": cfg["gop"], "tau": cfg["tau"], "alpha": cfg["alpha"],
+                      "temporal_patch": args.temporal_patch},
            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
                             "sample": f"{tot['stream_steps']} whole stream-steps (k=4) of alternating "
                                       f"static/high-motion streams, {cores} concurrent single-threaded C oracle "
@@ -382,7 +397,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     abi.lib()
     sw, sh = cfg["src"]
-    g = synth.make_grid(sw, sh)
+    g = synth.make_grid(sw, sh, tau=cfg["tau"], alpha=cfg["alpha"])
     S, w, s, gop = cfg["streams"], cfg["window"], cfg["stride"], cfg["gop"]
     global_ids = shard.stream_ids(rank, world, S)
     kvb = cfg["kv"]
@@ -695,7 +710,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfg["name"], "streams_per_gpu": S, "streams_total": S * world, "src": list(cfg["src"]),
-                   "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": 0.25, "alpha": 0.0,
+                   "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": cfg["tau"], "alpha": cfg["alpha"],
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
                    "frames": args.frames, "overlap": args.overlap, "temporal_patch": tp, "fused": args.fused,
@@ -785,7 +800,7 @@ def main():
     shared = os.environ.get("CS_BENCH_SHARED_GPU") == "1"
     if shared:
         local_rank = 0
-    cfg = workload(args.workload, args.streams, args.kv_mode)
+    cfg = workload(args.workload, args.streams, args.kv_mode, args)
     # the fused score+compact kernel takes model frames, one frame per token, no overlap mode
     args.fused = bool(args.fused and args.frames == "model" and args.temporal_patch == 1 and not args.overlap)
     if args.impl == "reference":
