@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tau", type=float, default=0.25, help="Eq. 4 threshold in source px (P:459)")
     ap.add_argument("--alpha", type=float, default=0.0, help="Eq. 3 residual weight (P:299)")
+    ap.add_argument("--group-size", type=int, default=2,
+                    help="patches per token edge (2x2 groups -> one LLM token, P:304; SPEC --group-size)")
     ap.add_argument("--window-frames", type=int, default=None, help="window w (default: the workload's)")
     ap.add_argument("--stride-frames", type=int, default=None, help="stride s (default: the workload's)")
     ap.add_argument("--gop", type=int, default=None, help="I-frame period (default: the workload's)")
@@ -85,6 +87,9 @@ def workload(name: str, streams: int | None, kv_mode: str = "paged", args=None):
     # method parameters (SPEC CLI names): defaults are the paper's (tau 0.25 px, alpha 0)
     cfg["tau"] = getattr(args, "tau", 0.25)
     cfg["alpha"] = getattr(args, "alpha", 0.0)
+    cfg["group"] = getattr(args, "group_size", 2)
+    if cfg["group"] < 1 or 32 % cfg["group"]:
+        raise SystemExit("--group-size must divide the 32x32 patch grid")
     for key, opt in (("window", "window_frames"), ("stride", "stride_frames"), ("gop", "gop")):
         v = getattr(args, opt, None)
         if v is not None:
@@ -207,7 +212,7 @@ def oracle_sample(cfg, budget_s: float, max_steps: int = 64, kv_mode: str = "pag
     spent."""
     import oracle.ref as ref
     sw, sh = cfg["src"]
-    g = synth.make_grid(sw, sh, tau=cfg["tau"], alpha=cfg["alpha"])
+    g = synth.make_grid(sw, sh, tau=cfg["tau"], alpha=cfg["alpha"], group=cfg["group"])
     w, s, gop = cfg["window"], cfg["stride"], cfg["gop"]
     ring = w + s
     nw = (g["grid_w"] * g["grid_h"] + 31) // 32
@@ -303,7 +308,7 @@ class OraclePool:
         kvb = cfg["kv"]
         per_proc = 0.7e9
         if kvb is not None:   # old + new cache + recompute buffer of one stream, bf16
-            rows = (cfg["window"] // tp) * 256 + cfg["n_prompt"]
+            rows = (cfg["window"] // tp) * (32 // cfg.get("group", 2)) ** 2 + cfg["n_prompt"]
             per_proc += 3.0 * rows * kvb["layers"] * 2 * kvb["kv_heads"] * kvb["head_dim"] * 2
         try:
             with open("/proc/meminfo") as f:
@@ -372,7 +377,7 @@ def run_reference(args, cfg, rank, world):
            "ms_per_step": 1000.0 * tot["seconds"] / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
            "config": {"workload": cfg["name"], "streams_per_gpu": cfg["streams"], "window": cfg["window"],
-                      "stride": cfg["stride"], "gop": cfg["gop"], "tau": cfg["tau"], "alpha": cfg["alpha"],
+                      "stride": cfg["stride"], "gop": cfg["gop"], "tau": cfg["tau"], "alpha": cfg["alpha"], "group": cfg["group"],
                       "temporal_patch": args.temporal_patch},
            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
                             "sample": f"{tot['stream_steps']} whole stream-steps (k=4) of alternating "
@@ -397,7 +402,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     abi.lib()
     sw, sh = cfg["src"]
-    g = synth.make_grid(sw, sh, tau=cfg["tau"], alpha=cfg["alpha"])
+    g = synth.make_grid(sw, sh, tau=cfg["tau"], alpha=cfg["alpha"], group=cfg["group"])
     S, w, s, gop = cfg["streams"], cfg["window"], cfg["stride"], cfg["gop"]
     global_ids = shard.stream_ids(rank, world, S)
     kvb = cfg["kv"]
@@ -710,7 +715,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfg["name"], "streams_per_gpu": S, "streams_total": S * world, "src": list(cfg["src"]),
-                   "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": cfg["tau"], "alpha": cfg["alpha"],
+                   "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": cfg["tau"], "alpha": cfg["alpha"], "group": cfg["group"],
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
                    "frames": args.frames, "overlap": args.overlap, "temporal_patch": tp, "fused": args.fused,
