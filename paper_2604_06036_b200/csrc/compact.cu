@@ -23,6 +23,14 @@ constexpr int kGatherThreads = 256;
 constexpr int kWarpsPerCta = kGatherThreads / 32;
 
 constexpr int kLayoutNV12 = 2;  // internal: frames are decoded NV12 planes, preprocessing fused (NEXT-2)
+#ifndef CS_NV12_BATCH
+#define CS_NV12_BATCH 2
+#endif
+#ifndef CS_NV12_CTAS
+#define CS_NV12_CTAS 4
+#endif
+constexpr int kNvBatch = CS_NV12_BATCH;  // output pixels per lane in flight (fused NV12 fast path)
+constexpr int kNvCtas = CS_NV12_CTAS;    // resident CTAs per SM of the fused NV12 kernel (register budget)
 constexpr float kInv255 = 1.0f / 255.0f;  // RN(1/255)
 
 // per-warp tile of one group in packed order: 3 x tp x (group*patch)^2 bf16, padded to 16 B
@@ -47,6 +55,8 @@ struct CompactParams {
   int src_w, src_h, y_pitch, uv_pitch;
   float scale_y, scale_x;  // src / model, fp32 (computed once on the host, IEEE division)
   float mean[3], stdv[3];
+  float rstd[3];  // RN(1 / std[c]) (host IEEE division)
+  int fast_div;   // every std in [2^-20, 2^20]: bf16((t - mean) / std) through the guarded reciprocal (norm_bf16)
   const void* const* uv_planes;
   const uint32_t* keep_mask;
   const int32_t* frame_index;
@@ -191,6 +201,23 @@ __device__ __forceinline__ void nv12_axis(int o, int src, float scale, int& i0, 
   l = __fsub_rn(f, static_cast<float>(i0));
 }
 
+// bf16 bits of RN_bf16(RN_f32(a / std)) -- the oracle's fp32 division then round-to-nearest-even to bf16 --
+// without the IEEE division in the common case.  q = RN(a * RN(1/std)) is within 2.5 ulp of a / std (relative
+// error < 2^-23 + 2^-48; |q - RN(a/std)| <= 5 fp32 steps even across a binade edge), so q and RN(a/std) round to
+// the same bf16 unless a bf16 rounding midpoint (low 16 bits 0x8000) lies within 8 steps of q; only then is the
+// exact division taken.  Valid for std in [2^-20, 2^20] and |mean| <= 2^60 (fast_div: q stays normal, no overflow); the
+// outputs are never NaN.  Pinned in scripts/check_norm_bf16.c / tests/test_div255.py.
+__device__ __forceinline__ uint16_t norm_bf16(float a, float stdv, float rstd, bool fast) {
+  float q;
+  if (fast) {
+    q = __fmul_rn(a, rstd);
+    if ((__float_as_uint(q) & 0xffffu) - 0x7ff8u <= 16u) q = __fdiv_rn(a, stdv);
+  } else {
+    q = __fdiv_rn(a, stdv);
+  }
+  return cs::f32_to_bf16_cvt(q);
+}
+
 // Gather one kept group (gr, gc) of `frame` into the warp tile and write it to packed rows [n0, n0 + G^2).
 // TT = frames per token unit (temporal patch, NEXT-3); 0 = runtime P.tp.  With TT > 1 the packed row is
 // [3][TT][p][p] and tile element (patch q, c, f, y, x) sits at ((q*3 + c)*TT + f)*p*p + y*p + x.
@@ -322,51 +349,90 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
         nv12_axis(gr * gp + lane, P.src_h, P.scale_y, ay0, i1, aly);
       }
       int yy = lane / gp, xx = lane - (lane / gp) * gp;
-      for (int e0 = 0; e0 < gp * gp; e0 += 32) {  // warp-uniform trip count (the shuffles need every lane)
-        const int x0 = __shfl_sync(0xffffffffu, ax0, xx), y0 = __shfl_sync(0xffffffffu, ay0, yy);
-        const float lx = __shfl_sync(0xffffffffu, alx, xx), ly = __shfl_sync(0xffffffffu, aly, yy);
-        if (e0 + lane >= gp * gp) break;  // last round: the lanes past the group's end are done
-        const int x1 = x0 + (x0 < P.src_w - 1 ? 1 : 0), y1 = y0 + (y0 < P.src_h - 1 ? 1 : 0);
-        const uint8_t* r0 = Yp + (long long)y0 * P.y_pitch;
-        const uint8_t* r1 = Yp + (long long)y1 * P.y_pitch;
-        const uint8_t* c0 = UVp + (long long)(y0 >> 1) * P.uv_pitch;
-        const uint8_t* c1 = UVp + (long long)(y1 >> 1) * P.uv_pitch;
-        const uint32_t yv[4] = {__ldg(r0 + x0), __ldg(r0 + x1), __ldg(r1 + x0), __ldg(r1 + x1)};
-        const uint32_t uvv[4] = {__ldg(reinterpret_cast<const uint16_t*>(c0 + 2 * (x0 >> 1))),
-                                 __ldg(reinterpret_cast<const uint16_t*>(c0 + 2 * (x1 >> 1))),
-                                 __ldg(reinterpret_cast<const uint16_t*>(c1 + 2 * (x0 >> 1))),
-                                 __ldg(reinterpret_cast<const uint16_t*>(c1 + 2 * (x1 >> 1)))};
-        float rgb[4][3];
+      // two output pixels per lane per iteration (rounds e0 and e0 + 32): their 16 loads are all in flight
+      // before either is converted (the kernel is latency-bound on these scattered byte loads)
+      const int npx = gp * gp;
+      for (int e0 = 0; e0 < npx; e0 += 32 * kNvBatch) {  // warp-uniform trip count (the shuffles need every lane)
+        uint32_t yv[kNvBatch][4], uvv[kNvBatch][4];
+        float lxv[kNvBatch], lyv[kNvBatch];
+        int pxx[kNvBatch], pyy[kNvBatch];
+        bool valid[kNvBatch];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float c = static_cast<float>(static_cast<int>(yv[q]) - 16);
-          const float d = static_cast<float>(static_cast<int>(uvv[q] & 0xffu) - 128);
-          const float ee = static_cast<float>(static_cast<int>(uvv[q] >> 8) - 128);
-          rgb[q][0] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kRV, ee)), 0.0f), 255.0f);
-          rgb[q][1] = fminf(fmaxf(__fsub_rn(__fsub_rn(__fmul_rn(kY, c), __fmul_rn(kGU, d)), __fmul_rn(kGV, ee)), 0.0f),
-                            255.0f);
-          rgb[q][2] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kBU, d)), 0.0f), 255.0f);
+        for (int b = 0; b < kNvBatch; ++b) {
+          // lanes past the group's end fetch an in-group pixel (valid addresses) and do not emit it
+          valid[b] = e0 + 32 * b + lane < npx;
+          pxx[b] = valid[b] ? xx : 0;
+          pyy[b] = valid[b] ? yy : 0;
+          const int x0 = __shfl_sync(0xffffffffu, ax0, pxx[b]), y0 = __shfl_sync(0xffffffffu, ay0, pyy[b]);
+          lxv[b] = __shfl_sync(0xffffffffu, alx, pxx[b]);
+          lyv[b] = __shfl_sync(0xffffffffu, aly, pyy[b]);
+          const int x1 = x0 + (x0 < P.src_w - 1 ? 1 : 0), y1 = y0 + (y0 < P.src_h - 1 ? 1 : 0);
+          const uint8_t* r0 = Yp + (long long)y0 * P.y_pitch;
+          const uint8_t* r1 = Yp + (long long)y1 * P.y_pitch;
+          const uint8_t* c0 = UVp + (long long)(y0 >> 1) * P.uv_pitch;
+          const uint8_t* c1 = UVp + (long long)(y1 >> 1) * P.uv_pitch;
+          yv[b][0] = __ldg(r0 + x0);
+          yv[b][1] = __ldg(r0 + x1);
+          yv[b][2] = __ldg(r1 + x0);
+          yv[b][3] = __ldg(r1 + x1);
+          uvv[b][0] = __ldg(reinterpret_cast<const uint16_t*>(c0 + 2 * (x0 >> 1)));
+          uvv[b][1] = __ldg(reinterpret_cast<const uint16_t*>(c0 + 2 * (x1 >> 1)));
+          uvv[b][2] = __ldg(reinterpret_cast<const uint16_t*>(c1 + 2 * (x0 >> 1)));
+          uvv[b][3] = __ldg(reinterpret_cast<const uint16_t*>(c1 + 2 * (x1 >> 1)));
+          // (yy, xx) of this lane's next pixel (32 further in row-major order)
+          xx += 32 % gp;
+          yy += 32 / gp;
+          if (xx >= gp) {
+            xx -= gp;
+            ++yy;
+          }
         }
-        const float hx = __fsub_rn(1.0f, lx), hy = __fsub_rn(1.0f, ly);
-        const int dy = yy >= p ? 1 : 0, y = yy - dy * p, dx = xx >= p ? 1 : 0, x = xx - dx * p;
-        uint16_t* tq = tile + (dy * G + dx) * 3 * pp + y * p + x;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const float top = __fadd_rn(__fmul_rn(hx, rgb[0][c]), __fmul_rn(lx, rgb[1][c]));
-          const float bot = __fadd_rn(__fmul_rn(hx, rgb[2][c]), __fmul_rn(lx, rgb[3][c]));
-          const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
-          // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
-          // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
-          const float q255 = __fmul_rn(v, kInv255);
-          const float t = __fmaf_rn(__fmaf_rn(-q255, 255.0f, v), kInv255, q255);
-          const float o = __fdiv_rn(__fsub_rn(t, P.mean[c]), P.stdv[c]);
-          tq[c * pp] = cs::f32_to_bf16_cvt(o);
-        }
-        xx += 32 % gp;
-        yy += 32 / gp;
-        if (xx >= gp) {
-          xx -= gp;
-          ++yy;
+        for (int b = 0; b < kNvBatch; ++b) {
+          if (!valid[b]) continue;
+          float rgb[4][3];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float c = static_cast<float>(static_cast<int>(yv[b][q]) - 16);
+            const float d = static_cast<float>(static_cast<int>(uvv[b][q] & 0xffu) - 128);
+            const float ee = static_cast<float>(static_cast<int>(uvv[b][q] >> 8) - 128);
+            rgb[q][0] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kRV, ee)), 0.0f), 255.0f);
+            rgb[q][1] = fminf(fmaxf(__fsub_rn(__fsub_rn(__fmul_rn(kY, c), __fmul_rn(kGU, d)), __fmul_rn(kGV, ee)),
+                                    0.0f), 255.0f);
+            rgb[q][2] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kBU, d)), 0.0f), 255.0f);
+          }
+          const float lx = lxv[b], ly = lyv[b];
+          const float hx = __fsub_rn(1.0f, lx), hy = __fsub_rn(1.0f, ly);
+          const int dy = pyy[b] >= p ? 1 : 0, y = pyy[b] - dy * p, dx = pxx[b] >= p ? 1 : 0, x = pxx[b] - dx * p;
+          uint16_t* tq = tile + (dy * G + dx) * 3 * pp + y * p + x;
+          float an[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const float top = __fadd_rn(__fmul_rn(hx, rgb[0][c]), __fmul_rn(lx, rgb[1][c]));
+            const float bot = __fadd_rn(__fmul_rn(hx, rgb[2][c]), __fmul_rn(lx, rgb[3][c]));
+            const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
+            // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
+            // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
+            const float q255 = __fmul_rn(v, kInv255);
+            const float t = __fmaf_rn(__fmaf_rn(-q255, 255.0f, v), kInv255, q255);
+            an[c] = __fsub_rn(t, P.mean[c]);
+          }
+          // (t - mean) / std -> bf16 (norm_bf16), the three channels' midpoint guards folded into one branch
+          float on[3];
+          uint32_t near_mid = 0u;
+          if (P.fast_div) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              on[c] = __fmul_rn(an[c], P.rstd[c]);
+              near_mid |= static_cast<uint32_t>((__float_as_uint(on[c]) & 0xffffu) - 0x7ff8u <= 16u);
+            }
+          }
+          if (!P.fast_div || near_mid) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) on[c] = __fdiv_rn(an[c], P.stdv[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < 3; ++c) tq[c * pp] = cs::f32_to_bf16_cvt(on[c]);
         }
       }
     } else {
@@ -419,8 +485,8 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
           const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
           const float q255 = __fmul_rn(v, kInv255);
           const float t = __fmaf_rn(__fmaf_rn(-q255, 255.0f, v), kInv255, q255);
-          const float o = __fdiv_rn(__fsub_rn(t, P.mean[c]), P.stdv[c]);
-          tile[((dy * G + dx) * 3 + c) * pp + y * p + x] = static_cast<uint16_t>(cs::f32_to_bf16_rne(o));
+          tile[((dy * G + dx) * 3 + c) * pp + y * p + x] =
+              norm_bf16(__fsub_rn(t, P.mean[c]), P.stdv[c], P.rstd[c], P.fast_div != 0);
         }
       }
     }
@@ -506,7 +572,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
 }
 
 template <int TP, int TG, int LAYOUT, int TT>
-__global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED && TP > 0) ? 4 : (LAYOUT == kLayoutNV12 && TP > 0) ? 5 : 2)
+__global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED && TP > 0) ? 4 : (LAYOUT == kLayoutNV12 && TP > 0) ? kNvCtas : 2)
     compact_gather(const __grid_constant__ CompactParams P) {
   extern __shared__ __align__(16) unsigned char g_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -767,9 +833,12 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
     P.uv_pitch = pre->uv_pitch;
     P.scale_y = static_cast<float>(pre->src_h) / static_cast<float>(P.FH);
     P.scale_x = static_cast<float>(pre->src_w) / static_cast<float>(P.FW);
+    P.fast_div = 1;
     for (int c = 0; c < 3; ++c) {
       P.mean[c] = pre->mean[c];
       P.stdv[c] = pre->std[c];
+      P.rstd[c] = 1.0f / pre->std[c];
+      if (!(pre->std[c] >= 0x1p-20f && pre->std[c] <= 0x1p20f && fabsf(pre->mean[c]) <= 0x1p60f)) P.fast_div = 0;
     }
     P.uv_planes = uv_planes;
   }
@@ -795,7 +864,7 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
   const size_t smem =
       (size_t)kWarpsPerCta * ((grouped ? 0 : tile_bytes_of(g->patch, g->group, tp)) + 4 * P.nw);
   const bool fast = g->patch == 14 && g->group == 2 && (tp == 1 || tp == 2);
-  const int grid = cs_num_sms() * (grouped ? 8 : (nv12 && fast) ? 5 : 4);  // resident CTAs per SM
+  const int grid = cs_num_sms() * (grouped ? 8 : (nv12 && fast) ? kNvCtas : 4);  // resident CTAs per SM
   const void* fn;
   int slot;
 #define CS_PICK(TP, TG, LY, TT, SL) \

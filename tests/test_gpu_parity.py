@@ -1064,8 +1064,15 @@ def test_mrope_gpu_both_modes(abi, ref, dtype):
 # ------------------------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("geom", [(448, 448, 14, 2, 32, 32), (1920, 1080, 14, 2, 32, 32),
                                   (3840, 2160, 14, 2, 32, 32), (120, 90, 6, 2, 8, 6), (64, 48, 8, 2, 4, 4)])
-def test_compact_nv12(abi, ref, geom):
+@pytest.mark.parametrize("norm", ["clip", "odd", "exact"])
+def test_compact_nv12(abi, ref, geom, norm):
+    """norm: the CLIP mean/std; unusual stds on the guarded-reciprocal path (norm_bf16); a std outside
+    [2^-20, 2^20], which takes the IEEE division for every pixel."""
     sw, sh, p, G, gw, gh = geom
+    if norm != "clip" and geom[0] in (3840, 1920):
+        pytest.skip("normalisation variants on the small geometries")
+    mean, std = {"clip": (None, None), "odd": ((0.5, -0.25, 0.0), (0.0173, 3.7, 1.0)),
+                 "exact": ((0.4815, 0.4578, 0.4082), (2.0 ** -21, 0.2613, 0.2758))}[norm]
     g = make_grid(sw, sh, patch=p, group=G, grid_w=gw, grid_h=gh)
     rng = np.random.default_rng(sw + sh)
     S, n = 2, 3
@@ -1075,8 +1082,10 @@ def test_compact_nv12(abi, ref, geom):
     pitch = sw + 64                                  # padded planes, as NVDEC allocates them
     ys = [rng.integers(16, 236, size=(sh, pitch), dtype=np.uint8) for _ in range(S * n)]
     uvs = [rng.integers(16, 241, size=(sh // 2, pitch), dtype=np.uint8) for _ in range(S * n)]
-    pre_h = ref.make_pre(sw, sh, pitch, pitch)
+    pre_h = ref.make_pre(sw, sh, pitch, pitch) if mean is None else ref.make_pre(sw, sh, pitch, pitch, mean, std)
     pre = dict(src_w=sw, src_h=sh, y_pitch=pitch, uv_pitch=pitch)
+    if mean is not None:
+        pre.update(mean=mean, std=std)
     fidx = np.arange(S * n, dtype=np.int32) + 7
     for cap in (S * n * gw * gh, S * n * gw * gh // 3 + 1):
         y_d = [torch.from_numpy(a).to(DEV) for a in ys]
