@@ -700,6 +700,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     sc_ms = float(np.mean(per["score"]))
     sc_bytes = float(dcnt[abi.CNT_BYTES_SCORE].item()) / K
     cmp_bytes = float(dcnt[abi.CNT_BYTES_COMPACT].item()) / K
+    # ncu_summary.json keys of this run's kernels (traffic of a variant is only reported when it was captured)
+    kv_key = ("kv_refresh_paged" if args.kv_mode == "paged" else "kv_refresh_copy") + \
+        ("+mrope" if args.rope == "mrope" else "") + ("+tp2" if tp == 2 else "")
+    cmp_key = ("compact_nv12" if args.frames == "nv12" else "compact_tp" if tp == 2 else
+               "score_compact" if args.fused else "compact_gather") + ("+planar" if args.frame_layout == "planar" else "")
     if args.fused:   # one launch does both: its time and the bytes of both calls
         cmp_ms = sc_ms
         cmp_bytes += sc_bytes
@@ -744,20 +749,20 @@ def run_ours(args, cfg, rank, world, local_rank):
                       "codecsight_kv_refresh (kv_plan + kv_prefix + kv_gather_tma)",
                       "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                       "frac": achieved / peak,
-                      "traffic": ncu_traffic("kv_refresh_paged" if args.kv_mode == "paged" else "kv_refresh_copy",
-                                             cfg["name"]),
+                      "traffic": ncu_traffic(kv_key, cfg["name"]),
                       "algorithmic_bytes_per_launch": kv_bytes_launch} if kvb else
                      {"bound": "hbm", "kernel": ("codecsight_score_compact (score_kernel<fused>)" if args.fused else
                                                  "codecsight_compact (compact_scan + compact_gather)"),
                       "achieved": cmp_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                       "frac": cmp_gbs / peak,
-                      "traffic": ncu_traffic("score_compact" if args.fused else "compact_gather", cfg["name"]),
+                      "traffic": ncu_traffic(cmp_key, cfg["name"]),
                       "algorithmic_bytes_per_launch": cmp_bytes}),
-        "secondary_roofline": {"kernel": "codecsight_score_compact" if args.fused else "codecsight_compact",
+        "secondary_roofline": {"kernel": {"compact_nv12": "codecsight_compact_nv12", "compact_tp": "codecsight_compact_tp",
+                                          "score_compact": "codecsight_score_compact"}.get(cmp_key.split("+")[0],
+                                                                                            "codecsight_compact"),
                                "achieved": cmp_gbs, "peak": peak,
                                "frac": cmp_gbs / peak, "unit": "GB/s", "algorithmic_bytes_per_launch": cmp_bytes,
-                               "traffic": ncu_traffic("score_compact" if args.fused else "compact_gather",
-                                                      cfg["name"])},
+                               "traffic": ncu_traffic(cmp_key, cfg["name"])},
         # the whole step against the same roofline: every call's algorithmic bytes per step / the step's time
         "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms_max / K / 1e3) / 1e9,
                           "peak": peak, "unit": "GB/s", "frac": step_bytes / (ms_max / K / 1e3) / 1e9 / peak},
