@@ -28,12 +28,13 @@ def to_grouped(frame, g):
     return np.ascontiguousarray(x.transpose(1, 4, 2, 5, 0, 3, 6)).reshape(-1)
 
 
-@pytest.mark.parametrize("cfg_name,S,steps,sample,fused", [("C4", 256, 3, [0, 1, 254, 255], False),
-                                                          ("C4", 256, 3, [0, 1, 254, 255], True),
-                                                          ("C3", 64, 3, [0, 63], True),
-                                                          ("C5", 128, 2, [0, 127], False),
-                                                          ("C5", 128, 2, [0, 127], True)])
-def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused):
+@pytest.mark.parametrize("cfg_name,S,steps,sample,fused,rope", [("C4", 256, 3, [0, 1, 254, 255], False, "1d"),
+                                                               ("C4", 256, 3, [0, 1, 254, 255], True, "1d"),
+                                                               ("C4", 256, 3, [0, 255], True, "mrope"),
+                                                               ("C3", 64, 3, [0, 63], True, "1d"),
+                                                               ("C5", 128, 2, [0, 127], False, "1d"),
+                                                               ("C5", 128, 2, [0, 127], True, "1d")])
+def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused, rope):
     import gc
     gc.collect()
     torch.cuda.empty_cache()
@@ -44,7 +45,7 @@ def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused):
     g = make_grid(sw, sh)
     w, s, gop = cfg["window"], cfg["stride"], cfg["gop"]
     ring = w + s
-    kvb = cfg["kv"]
+    kvb = cfg["kv"] if rope == "1d" else synth.QWEN_MROPE_KV   # M-RoPE: the bench's --rope mrope cache (NEXT-3)
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=DEV,
                     frame_layout=abi.CS_LAYOUT_GROUPED, kv_mode="paged", compact_chunk=s, fused=fused)
     gen = torch.Generator(device=DEV)
