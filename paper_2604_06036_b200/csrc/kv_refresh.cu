@@ -22,7 +22,10 @@
 
 namespace {
 
-constexpr int kPlanThreads = 256;
+#ifndef CS_PLAN_THREADS
+#define CS_PLAN_THREADS 512
+#endif
+constexpr int kPlanThreads = CS_PLAN_THREADS;  // one CTA per stream; 512: C4 plan 58 -> 56 us, C5 127 -> 116 us (ncu)
 constexpr int kGatherThreads = 256;
 constexpr int kRowBlock = 128;
 constexpr int kMaxSeg = 1025;  // w + 1 with w + s <= 1024
@@ -1065,16 +1068,28 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   for (int i = warp; i < nseg; i += nwarp) {
     const PlanSeg sg = s_seg[i];
     const int d = s_disp[i], pold = s_pold[i];
-    for (int t = lane; t < sg.len; t += 32) {
+    // the previous window's slots of 4 x 32 tokens are loaded before any is used (one latency per batch)
+    constexpr int kU = 4;
+    for (int t0 = lane; t0 < sg.len; t0 += 32 * kU) {
+     int slv[kU];
+#pragma unroll
+     for (int u = 0; u < kU; ++u) {
+      const int t = t0 + 32 * u;
+      const long long q = (long long)pold + t;
+      slv[u] = (d != CS_DISP_NEW && t < sg.len && q < P.slot_cap && q < n_old)
+                   ? __ldg(P.slot_old + (long long)sidx * P.slot_cap + q) : -1;
+     }
+#pragma unroll
+     for (int u = 0; u < kU; ++u) {
+      const int t = t0 + 32 * u;
+      if (t >= sg.len) break;
       const long long p = (long long)sg.p_new + t;
       if (p < P.token_cap) {
         dsp[p] = static_cast<uint8_t>(d);
         po_out[p] = d == CS_DISP_NEW ? -1 : pold + t;
       }
       if (d == CS_DISP_NEW) continue;
-      const long long q = (long long)pold + t;
-      int sl = -1;
-      if (q < P.slot_cap && q < n_old) sl = __ldg(P.slot_old + (long long)sidx * P.slot_cap + q);
+      int sl = slv[u];
       if (sl < 0 || sl >= P.cap) {
         sl = -1;
         st_local |= CS_STATUS_ORIGIN;
@@ -1095,6 +1110,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
         cop += ok;
       }
       if (p < P.max_tok) mv[p] = me;
+     }
     }
   }
   __syncthreads();
@@ -1142,9 +1158,18 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     const int per = (nmv + blockDim.x - 1) / blockDim.x;
     const int b = tid * per, e = min(nmv, b + per);
     auto cls = [](const MoveEntry& m) { return (m.slot < 0 || m.src == -2) ? 0 : (m.src == -1 ? 1 : 2); };
-    auto starts = [&](int p) {
+    // the thread's entries are read in batches of kB (+ the one before), all loads in flight at once: a run
+    // start depends on the entry and its predecessor only
+    constexpr int kB = 8;
+    auto batch = [&](int p0, MoveEntry (&m)[kB + 1]) {
+#pragma unroll
+      for (int u = 0; u <= kB; ++u) {
+        const int p = p0 - 1 + u;
+        m[u] = (p >= 0 && p < e) ? mv[p] : MoveEntry{-1, -2};
+      }
+    };
+    auto is_start = [&](const MoveEntry& a, const MoveEntry& c, int p) {
       if (p == 0) return true;
-      const MoveEntry a = mv[p - 1], c = mv[p];
       const int ca = cls(a), cc = cls(c);
       if (ca != cc) return true;
       if (cc == 0) return false;
@@ -1152,23 +1177,34 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
       return cc == 2 && c.src != a.src + 1;
     };
     int cnt = 0;
-    for (int p = b; p < e; ++p) cnt += starts(p) ? 1 : 0;
+    for (int p0 = b; p0 < e; p0 += kB) {
+      MoveEntry m[kB + 1];
+      batch(p0, m);
+#pragma unroll
+      for (int u = 1; u <= kB; ++u)
+        if (p0 - 1 + u < e) cnt += is_start(m[u - 1], m[u], p0 - 1 + u) ? 1 : 0;
+    }
     s_cnt[tid] = cnt;
     __syncthreads();
     const int nruns = block_exclusive_scan(s_cnt, blockDim.x);
     KvSeg* runs = reinterpret_cast<KvSeg*>(stream_ws(P, sidx) + sizeof(KvHdr));
     int idx = s_cnt[tid];
-    for (int p = b; p < e; ++p) {
-      if (!starts(p)) continue;
-      const MoveEntry m = mv[p];
-      const int c = cls(m);
-      KvSeg r;
-      r.p_new = p;
-      r.len = 0;
-      r.kind = c == 0 ? SEG_SKIP : (c == 1 ? SEG_REUSE : SEG_COPY);
-      r.src = c == 2 ? m.src : m.slot;
-      r.dst = m.slot;
-      runs[idx++] = r;
+    for (int p0 = b; p0 < e; p0 += kB) {
+      MoveEntry m[kB + 1];
+      batch(p0, m);
+#pragma unroll
+      for (int u = 1; u <= kB; ++u) {
+        const int p = p0 - 1 + u;
+        if (p >= e || !is_start(m[u - 1], m[u], p)) continue;
+        const int c = cls(m[u]);
+        KvSeg r;
+        r.p_new = p;
+        r.len = 0;
+        r.kind = c == 0 ? SEG_SKIP : (c == 1 ? SEG_REUSE : SEG_COPY);
+        r.src = c == 2 ? m[u].src : m[u].slot;
+        r.dst = m[u].slot;
+        runs[idx++] = r;
+      }
     }
     __syncthreads();
     for (int i = tid; i < nruns; i += blockDim.x) runs[i].len = (i + 1 < nruns ? runs[i + 1].p_new : nmv) - runs[i].p_new;
