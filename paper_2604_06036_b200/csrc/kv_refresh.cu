@@ -25,8 +25,25 @@ namespace {
 #ifndef CS_PLAN_THREADS
 #define CS_PLAN_THREADS 512
 #endif
-constexpr int kPlanThreads = CS_PLAN_THREADS;  // one CTA per stream; 512: C4 plan 58 -> 56 us, C5 127 -> 116 us (ncu)
+constexpr int kPlanThreads = CS_PLAN_THREADS;  // one CTA per stream (512: measured faster than 256 / 1024)
 constexpr int kGatherThreads = 256;
+constexpr size_t kPlanSmem = 188 * 1024;  // kv_plan_paged dynamic shared memory limit (+ 33 KB static <= 227 KB)
+
+#ifdef CS_PLAN_TIMING
+// experiment build only (scripts/experiments/plan_phase.py): per-CTA %globaltimer stamps of kv_plan_paged
+__device__ unsigned long long g_cs_plan_phase[4096][10];
+#define CS_PLAN_PHASE(k)                                                              \
+  do {                                                                                \
+    __syncthreads();                                                                  \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {                                      \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_cs_plan_phase[blockIdx.x][k] = t_;                                            \
+    }                                                                                 \
+  } while (0)
+#else
+#define CS_PLAN_PHASE(k)
+#endif
 constexpr int kRowBlock = 128;
 constexpr int kMaxSeg = 1025;  // w + 1 with w + s <= 1024
 
@@ -76,6 +93,7 @@ struct KvParams {
   int32_t* slot_new;
   long long slot_cap;
   int max_tok;      // w * groups + n_prompt: entries of the per-stream move list
+  int mv_smem;      // kv_plan_paged: the move list is also staged in shared memory (runs pass reads it there)
   int prefix_mode;  // kv_prefix items: 0 = (stream, 128-row block, layer, K|V), 1 = tokens
   int paged;        // 1: REUSE runs rotate keys in place and leave values alone
   int rope_mode;    // CS_ROPE_1D | CS_ROPE_MROPE
@@ -942,7 +960,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   __shared__ PlanSeg s_seg[kMaxSeg];
   __shared__ int s_pold[kMaxSeg];
   __shared__ int s_disp[kMaxSeg];
-  __shared__ int s_nseg, s_dp, s_ntotal, s_p0, s_n_old, s_r0, s_st;
+  __shared__ int s_nseg, s_ntotal, s_p0, s_n_old, s_r0, s_st;
   __shared__ unsigned long long s_rot, s_cop;
 
   const int sidx = blockIdx.x;
@@ -953,13 +971,27 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   const int nfr = hi - lo;
   const int nw = P.nw;
   const int cw = static_cast<int>((P.cap + 31) / 32);  // words of the slot bitmap
+  CS_PLAN_PHASE(0);
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(smem);                 // [nfr][nw]
   uint32_t* s_used = s_mask + nfr * nw;                                 // [cw]
   int* s_free = reinterpret_cast<int*>(s_used + cw);                    // [cw + 1] free-slot prefix
+  MoveEntry* s_mv = reinterpret_cast<MoveEntry*>(  // [max_tok] if P.mv_smem, 8-B aligned after s_free
+      smem + ((static_cast<size_t>(nfr * nw + 2 * cw + 1) * 4 + 7) & ~static_cast<size_t>(7)));
 
-  for (int e = tid; e < nfr * nw; e += blockDim.x) {
-    const int fi = e / nw, t = e - fi * nw;
-    s_mask[e] = __ldg(P.mring + ((long long)sidx * P.ring + ((lo + fi) % P.ring)) * nw + t);
+  {  // the window's masks: up to 8 words per thread in flight at once
+    constexpr int kM = 8;
+    for (int e0 = tid; e0 < nfr * nw; e0 += kM * blockDim.x) {
+      uint32_t v[kM];
+#pragma unroll
+      for (int u = 0; u < kM; ++u) {
+        const int e = e0 + u * blockDim.x;
+        const int fi = e / nw, t = e - fi * nw;
+        v[u] = e < nfr * nw ? __ldg(P.mring + ((long long)sidx * P.ring + ((lo + fi) % P.ring)) * nw + t) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kM; ++u)
+        if (e0 + u * blockDim.x < nfr * nw) s_mask[e0 + u * blockDim.x] = v[u];
+    }
   }
   for (int fi = tid; fi < nfr; fi += blockDim.x) s_t[fi] = __ldg(P.tring + (long long)sidx * P.ring + ((lo + fi) % P.ring));
   for (int i = tid; i < cw; i += blockDim.x) s_used[i] = 0u;
@@ -969,16 +1001,48 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     s_st = 0;
   }
   __syncthreads();
-  for (int fi = warp; fi < nfr; fi += nwarp) {
-    int n = 0;
-    for (int base = 0; base < P.ngroups; base += 32) {
-      const int q = base + lane;
-      const bool kept = q < P.ngroups && cs::group_kept(s_mask + fi * nw, q, P.ngc, P.G, P.grid_w);
-      n += __popc(__ballot_sync(0xffffffffu, kept));
+  if (P.G == 2 && P.grid_w == 32 && (P.grid_h & 1) == 0 && P.grid_h <= 64) {
+    // 2x2 groups of a 32-wide grid: word r = patch row r; a group row's kept groups = popc of the OR of its two
+    // words folded onto even bits.  One lane per group row, one warp per frame.
+    const int ngr = P.grid_h / 2;
+    for (int fi = warp; fi < nfr; fi += nwarp) {
+      int n = 0;
+      for (int gr = lane; gr < ngr; gr += 32) {
+        const uint32_t x = s_mask[fi * nw + 2 * gr] | s_mask[fi * nw + 2 * gr + 1];
+        n += __popc((x | (x >> 1)) & 0x55555555u);
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) n += __shfl_xor_sync(0xffffffffu, n, d);
+      if (lane == 0) s_n[fi] = n;
     }
-    if (lane == 0) s_n[fi] = n;
+  } else {
+    for (int fi = warp; fi < nfr; fi += nwarp) {
+      int n = 0;
+      for (int base = 0; base < P.ngroups; base += 32) {
+        const int q = base + lane;
+        const bool kept = q < P.ngroups && cs::group_kept(s_mask + fi * nw, q, P.ngc, P.G, P.grid_w);
+        n += __popc(__ballot_sync(0xffffffffu, kept));
+      }
+      if (lane == 0) s_n[fi] = n;
+    }
   }
   __syncthreads();
+  // (cos, sin) of R(dp), dp = -(tokens of the s dropped frames): warps 1.. compute it while thread 0 builds the
+  // segment table below (64 double-precision sincos calls were the longest phase of this kernel, measured)
+  float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
+  if (warp >= 1) {
+    long long drop = 0;
+    if (k >= 1)
+      for (int f = lo; f < ks; ++f) drop += s_n[f - lo];
+    for (int i = tid - 32; i < P.D / 2; i += blockDim.x - 32) {
+      // position change of pair i: the sequence-index change (1-D RoPE) or its section's component (M-RoPE)
+      const long long delta = P.rope_mode == CS_ROPE_MROPE ? (i < P.mrope_t ? P.mrope_dt : 0ll) : -drop;
+      double sn, cs;
+      sincos(static_cast<double>(delta) * P.inv_freq[i], &sn, &cs);
+      cs_tab[i] = make_float2(__double2float_rn(cs), __double2float_rn(sn));
+    }
+  }
+  CS_PLAN_PHASE(1);
 
   if (tid == 0) {
     long long drop = 0, n_old = 0;
@@ -1032,7 +1096,6 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     n_new += P.n_prompt;
     const long long n_total = n_visual + P.n_prompt;
     s_nseg = nseg;
-    s_dp = static_cast<int>(-drop);
     s_ntotal = static_cast<int>(n_total);
     s_p0 = static_cast<int>(p0);
     s_r0 = static_cast<int>(r0);
@@ -1057,6 +1120,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   }
   __syncthreads();
 
+  CS_PLAN_PHASE(2);
   const int nseg = s_nseg, n_total = s_ntotal, p0 = s_p0, n_old = s_n_old;
   MoveEntry* mv = stream_moves(P, sidx);
   int32_t* slot_new = P.slot_new + (long long)sidx * P.slot_cap;
@@ -1109,11 +1173,15 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
         me.src = ok ? static_cast<int>(r) : -2;
         cop += ok;
       }
-      if (p < P.max_tok) mv[p] = me;
+      if (p < P.max_tok) {
+        mv[p] = me;
+        if (P.mv_smem) s_mv[p] = me;
+      }
      }
     }
   }
   __syncthreads();
+  CS_PLAN_PHASE(3);
   // ---- free slots (not held by a survivor), ascending -> NEW tokens in p_new order -------------------------
   for (int i = tid; i < cw; i += blockDim.x) {
     uint32_t valid = 0xffffffffu;
@@ -1124,6 +1192,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   const int total_free = block_exclusive_scan(s_free, cw);
   if (tid == 0) s_free[cw] = total_free;
   __syncthreads();
+  CS_PLAN_PHASE(4);
   for (int p = p0 + tid; p < n_total; p += blockDim.x) {
     const int i = p - p0;  // index among the NEW tokens
     int sl = -1;
@@ -1147,11 +1216,15 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     me.slot = sl;
     me.src = ok ? static_cast<int>(r) : -2;
     cop += ok;
-    if (p < P.max_tok) mv[p] = me;
+    if (p < P.max_tok) {
+        mv[p] = me;
+        if (P.mv_smem) s_mv[p] = me;
+      }
   }
   // ---- runs for the bulk-copy gather: maximal token ranges with one action and consecutive slots (and
   //      consecutive refreshed rows for copies); skipped tokens form SKIP runs so runs tile [0, n_total) -------
   __syncthreads();  // move entries of every token written
+  CS_PLAN_PHASE(5);
   {
     __shared__ int s_cnt[kPlanThreads];
     const int nmv = min(n_total, P.max_tok);
@@ -1165,7 +1238,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
 #pragma unroll
       for (int u = 0; u <= kB; ++u) {
         const int p = p0 - 1 + u;
-        m[u] = (p >= 0 && p < e) ? mv[p] : MoveEntry{-1, -2};
+        m[u] = (p >= 0 && p < e) ? (P.mv_smem ? s_mv[p] : mv[p]) : MoveEntry{-1, -2};
       }
     };
     auto is_start = [&](const MoveEntry& a, const MoveEntry& c, int p) {
@@ -1187,6 +1260,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     s_cnt[tid] = cnt;
     __syncthreads();
     const int nruns = block_exclusive_scan(s_cnt, blockDim.x);
+    CS_PLAN_PHASE(6);
     KvSeg* runs = reinterpret_cast<KvSeg*>(stream_ws(P, sidx) + sizeof(KvHdr));
     int idx = s_cnt[tid];
     for (int p0 = b; p0 < e; p0 += kB) {
@@ -1210,17 +1284,19 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     for (int i = tid; i < nruns; i += blockDim.x) runs[i].len = (i + 1 < nruns ? runs[i + 1].p_new : nmv) - runs[i].p_new;
     if (tid == 0) reinterpret_cast<KvHdr*>(stream_ws(P, sidx))->n_seg = nruns;
   }
-  // ---- (cos, sin) of R(dp) ----------------------------------------------------------------------------------
-  float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
-  for (int i = tid; i < P.D / 2; i += blockDim.x) {
-    // position change of pair i: the sequence-index change (1-D RoPE) or its section's component (M-RoPE)
-    const long long delta = P.rope_mode == CS_ROPE_MROPE ? (i < P.mrope_t ? P.mrope_dt : 0ll) : (long long)s_dp;
-    const double ang = static_cast<double>(delta) * P.inv_freq[i];
-    cs_tab[i] = make_float2(__double2float_rn(cos(ang)), __double2float_rn(sin(ang)));
+  CS_PLAN_PHASE(7);
+  // per-warp reductions first: one shared atomic per warp instead of one per thread
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    st_local |= __shfl_xor_sync(0xffffffffu, st_local, d);
+    rot += __shfl_xor_sync(0xffffffffu, rot, d);
+    cop += __shfl_xor_sync(0xffffffffu, cop, d);
   }
-  if (st_local) atomicOr(&s_st, st_local);
-  if (rot) atomicAdd(&s_rot, rot);
-  if (cop) atomicAdd(&s_cop, cop);
+  if (lane == 0) {
+    if (st_local) atomicOr(&s_st, st_local);
+    if (rot) atomicAdd(&s_rot, rot);
+    if (cop) atomicAdd(&s_cop, cop);
+  }
   __syncthreads();
   if (tid == 0) {
     cs::atomic_or_status(P.status, s_st);
@@ -1229,6 +1305,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     const unsigned long long rotb = (unsigned long long)P.H * 2ull * P.rot_pairs * P.esz;
     cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_KV], (s_rot * P.L * rotb + s_cop * P.L * 2ull * rowb) * 2ull);
   }
+  CS_PLAN_PHASE(8);
 }
 
 // One token per warp iteration: REUSE -> rotate the key rows of all layers in place; copy -> K and V rows of all
@@ -1552,10 +1629,15 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   const int lo = win->step >= 1 ? (win->step - 1) * win->stride : 0;
   const int nfr = win->step * win->stride + win->window - lo;
   const long long cw = (kv->capacity + 31) / 32;
-  const size_t plan_smem = static_cast<size_t>(nfr) * P.nw * 4 + static_cast<size_t>(cw) * 4 +
-                           static_cast<size_t>(cw + 1) * 4;
-  if (plan_smem > 160 * 1024) return CS_ERR_UNSUPPORTED;
-  if (cs_set_smem_attr(reinterpret_cast<const void*>(kv_plan_paged), 10, 160 * 1024)) return CS_ERR_CUDA;
+  size_t plan_smem = static_cast<size_t>(nfr) * P.nw * 4 + static_cast<size_t>(cw) * 4 +
+                     static_cast<size_t>(cw + 1) * 4;
+  plan_smem = (plan_smem + 7) & ~static_cast<size_t>(7);
+  if (plan_smem > kPlanSmem) return CS_ERR_UNSUPPORTED;
+  // the move list staged in shared memory too when it fits (the runs pass then reads it there, not from L2)
+  const size_t mv_bytes = static_cast<size_t>(P.max_tok) * sizeof(MoveEntry);
+  P.mv_smem = plan_smem + mv_bytes <= kPlanSmem ? 1 : 0;
+  if (P.mv_smem) plan_smem += mv_bytes;
+  if (cs_set_smem_attr(reinterpret_cast<const void*>(kv_plan_paged), 10, kPlanSmem)) return CS_ERR_CUDA;
   kv_plan_paged<<<n_streams, kPlanThreads, plan_smem, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   kv_prefix<<<1, 1024, 0, stream>>>(P);
@@ -1572,3 +1654,10 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
 }
+
+#ifdef CS_PLAN_TIMING
+extern "C" int codecsight_debug_plan_phase(unsigned long long* host, int n_ctas) {
+  if (n_ctas > 4096) n_ctas = 4096;
+  return cudaMemcpyFromSymbol(host, g_cs_plan_phase, sizeof(unsigned long long) * 10 * n_ctas) == cudaSuccess ? 0 : -1;
+}
+#endif
