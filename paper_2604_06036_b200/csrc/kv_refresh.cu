@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
   __shared__ PlanSeg s_seg[kMaxSeg];                  // index segments (unclamped), one per frame + prompt
   __shared__ int s_pold[kMaxSeg];                     // p_old of the first token of the segment (-1: NEW)
   __shared__ int s_disp[kMaxSeg];
-  __shared__ int s_nseg, s_dp;
+  __shared__ int s_nseg;
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(smem);  // [nfr][nw]
 
   const int sidx = blockIdx.x;
@@ -146,6 +146,20 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
     if (lane == 0) s_n[fi] = n;
   }
   __syncthreads();
+  // ---- (cos, sin) of R(dp), fp64 angle rounded to fp32 (reading Q20): warps 1.. while thread 0 builds the
+  //      segment table (one sincos per pair) --------------------------------------------------------------------
+  if (warp >= 1) {
+    long long drop = 0;
+    for (int f = lo; f < ks; ++f) drop += s_n[f - lo];
+    float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
+    for (int i = tid - 32; i < P.D / 2; i += blockDim.x - 32) {
+      // position change of pair i: the sequence-index change (1-D RoPE) or its section's component (M-RoPE)
+      const long long delta = P.rope_mode == CS_ROPE_MROPE ? (i < P.mrope_t ? P.mrope_dt : 0ll) : -drop;
+      double sn, cs;
+      sincos(static_cast<double>(delta) * P.inv_freq[i], &sn, &cs);
+      cs_tab[i] = make_float2(__double2float_rn(cs), __double2float_rn(sn));
+    }
+  }
 
   if (tid == 0) {
     // ---- serial segment construction over <= w + 1 entries -------------------------------------------
@@ -189,7 +203,6 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
     n_new += P.n_prompt;
     const long long n_total = n_visual + P.n_prompt;
     s_nseg = nseg;
-    s_dp = static_cast<int>(-drop);
 
     int* nt = P.n_tokens + (long long)sidx * 4;
     nt[0] = static_cast<int>(n_visual);
@@ -265,14 +278,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
       }
     }
   }
-  // ---- (cos, sin) of R(dp), fp64 angle rounded to fp32 (reading Q20) -------------------------------------
-  float2* cs_tab = reinterpret_cast<float2*>(stream_ws(P, sidx) + sizeof(KvHdr) + sizeof(KvSeg) * P.max_seg);
-  for (int i = tid; i < P.D / 2; i += blockDim.x) {
-    // position change of pair i: the sequence-index change (1-D RoPE) or its section's component (M-RoPE)
-    const long long delta = P.rope_mode == CS_ROPE_MROPE ? (i < P.mrope_t ? P.mrope_dt : 0ll) : (long long)s_dp;
-    const double ang = static_cast<double>(delta) * P.inv_freq[i];
-    cs_tab[i] = make_float2(__double2float_rn(cos(ang)), __double2float_rn(sin(ang)));
-  }
+
 }
 
 // ------------------------------------------------------------------------------------------------------------
