@@ -1019,6 +1019,37 @@ def test_paged_edge_cases(abi, ref):
         run_paged_both(abi, ref, g, kv, win, mring, tring, pools, slot_old, slot_cap, refr if with_ref else None, tc)
 
 
+def _random_group_rings(g, S, ring, gop, rng, p_keep=0.5):
+    """Group-complete masks (each 2x2 group kept with p_keep) and I/P types for a ring of frames."""
+    ngr, ngc = g["grid_h"] // 2, g["grid_w"] // 2
+    keep = rng.random((S, ring, ngr, ngc)) < p_keep
+    bits = np.repeat(np.repeat(keep, 2, axis=2), 2, axis=3)            # [S][ring][32][32] patch bits
+    words = (bits.astype(np.uint64) << np.arange(g["grid_w"], dtype=np.uint64)).sum(axis=-1).astype(np.uint32)
+    types = np.where(np.arange(ring) % gop == 0, 0, 1).astype(np.uint8)
+    return words, np.broadcast_to(types, (S, ring)).copy()
+
+
+def test_paged_long_window_move_list_in_global(abi, ref):
+    """w = 96: the plan's per-stream move list (96 x 256 + 32 entries, 197 KB) no longer fits the plan kernel's
+    shared memory and is read back from the workspace instead (kv_plan_paged, P.mv_smem = 0)."""
+    g = make_grid(448, 448)
+    w, s = 96, 4
+    ring = w + s
+    S = 2
+    rng = np.random.default_rng(21)
+    mring, tring = _random_group_rings(g, S, ring, 16, rng)
+    win = dict(window=w, stride=s, step=3, ring_frames=ring)
+    cap = w * 256 + 32
+    kv = dict(synth.TOY_KV, capacity=cap + 10, refresh_capacity=cap, n_prompt=32)
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(4)
+    shape = (kv["layers"], 2, cap + 10, kv["kv_heads"], kv["head_dim"])
+    pools = [torch.randn(shape, generator=gen, device=DEV) for _ in range(S)]
+    slot_old = np.stack([rng.permutation(cap + 10)[:cap] for _ in range(S)]).astype(np.int32)
+    _, _, refr = make_caches(kv, S, gen)
+    run_paged_both(abi, ref, g, kv, win, mring, tring, pools, slot_old, cap, refr, cap)
+
+
 # ------------------------------------------------------------------------------------------------------------
 # M-RoPE position correction (NEXT-3), both KV modes
 # ------------------------------------------------------------------------------------------------------------
