@@ -1141,49 +1141,49 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     // the previous window's slots of 4 x 32 tokens are loaded before any is used (one latency per batch)
     constexpr int kU = 4;
     for (int t0 = lane; t0 < sg.len; t0 += 32 * kU) {
-     int slv[kU];
+      int slv[kU];
 #pragma unroll
-     for (int u = 0; u < kU; ++u) {
-      const int t = t0 + 32 * u;
-      const long long q = (long long)pold + t;
-      slv[u] = (d != CS_DISP_NEW && t < sg.len && q < P.slot_cap && q < n_old)
-                   ? __ldg(P.slot_old + (long long)sidx * P.slot_cap + q) : -1;
-     }
+      for (int u = 0; u < kU; ++u) {
+        const int t = t0 + 32 * u;
+        const long long q = (long long)pold + t;
+        slv[u] = (d != CS_DISP_NEW && t < sg.len && q < P.slot_cap && q < n_old)
+                     ? __ldg(P.slot_old + (long long)sidx * P.slot_cap + q) : -1;
+      }
 #pragma unroll
-     for (int u = 0; u < kU; ++u) {
-      const int t = t0 + 32 * u;
-      if (t >= sg.len) break;
-      const long long p = (long long)sg.p_new + t;
-      if (p < P.token_cap) {
-        dsp[p] = static_cast<uint8_t>(d);
-        po_out[p] = d == CS_DISP_NEW ? -1 : pold + t;
+      for (int u = 0; u < kU; ++u) {
+        const int t = t0 + 32 * u;
+        if (t >= sg.len) break;
+        const long long p = (long long)sg.p_new + t;
+        if (p < P.token_cap) {
+          dsp[p] = static_cast<uint8_t>(d);
+          po_out[p] = d == CS_DISP_NEW ? -1 : pold + t;
+        }
+        if (d == CS_DISP_NEW) continue;
+        int sl = slv[u];
+        if (sl < 0 || sl >= P.cap) {
+          sl = -1;
+          st_local |= CS_STATUS_ORIGIN;
+        } else {
+          atomicOr(&s_used[sl >> 5], 1u << (sl & 31));
+        }
+        if (p < P.slot_cap) slot_new[p] = sl;
+        MoveEntry me;
+        me.slot = sl;
+        if (d == CS_DISP_REUSE) {
+          me.src = sl >= 0 ? -1 : -2;
+          rot += sl >= 0;
+        } else {
+          const long long r = (long long)sg.src + t;
+          const bool ok = P.has_refreshed && sl >= 0 && r < P.rcap;
+          if (P.has_refreshed && sl >= 0 && r >= P.rcap) st_local |= CS_STATUS_CAPACITY;
+          me.src = ok ? static_cast<int>(r) : -2;
+          cop += ok;
+        }
+        if (p < P.max_tok) {
+          mv[p] = me;
+          if (P.mv_smem) s_mv[p] = me;
+        }
       }
-      if (d == CS_DISP_NEW) continue;
-      int sl = slv[u];
-      if (sl < 0 || sl >= P.cap) {
-        sl = -1;
-        st_local |= CS_STATUS_ORIGIN;
-      } else {
-        atomicOr(&s_used[sl >> 5], 1u << (sl & 31));
-      }
-      if (p < P.slot_cap) slot_new[p] = sl;
-      MoveEntry me;
-      me.slot = sl;
-      if (d == CS_DISP_REUSE) {
-        me.src = sl >= 0 ? -1 : -2;
-        rot += sl >= 0;
-      } else {
-        const long long r = (long long)sg.src + t;
-        const bool ok = P.has_refreshed && sl >= 0 && r < P.rcap;
-        if (P.has_refreshed && sl >= 0 && r >= P.rcap) st_local |= CS_STATUS_CAPACITY;
-        me.src = ok ? static_cast<int>(r) : -2;
-        cop += ok;
-      }
-      if (p < P.max_tok) {
-        mv[p] = me;
-        if (P.mv_smem) s_mv[p] = me;
-      }
-     }
     }
   }
   __syncthreads();
