@@ -88,8 +88,10 @@ def workload(name: str, streams: int | None, kv_mode: str = "paged", args=None):
     cfg["tau"] = getattr(args, "tau", 0.25)
     cfg["alpha"] = getattr(args, "alpha", 0.0)
     cfg["group"] = getattr(args, "group_size", 2)
-    if cfg["group"] < 1 or 32 % cfg["group"]:
-        raise SystemExit("--group-size must divide the 32x32 patch grid")
+    if cfg["group"] < 1 or 32 % cfg["group"] or cfg["group"] * 14 > 32:
+        raise SystemExit("--group-size: 1 or 2 (it must divide the 32x32 patch grid, and group * patch <= 32 px is "
+                         "the compaction's warp tile, include/codecsight.h); group 1 has 4x the tokens of group 2, so "
+                         "the KV caches of a workload need 4x the memory (use --streams)")
     for key, opt in (("window", "window_frames"), ("stride", "stride_frames"), ("gop", "gop")):
         v = getattr(args, opt, None)
         if v is not None:

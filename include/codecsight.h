@@ -100,7 +100,8 @@ typedef struct {
 /* Frame / macroblock / patch geometry and the pruning policy parameters.
  * Limits: 1 <= src_w, src_h <= 16384; 1 <= mb_size <= 64; mb_cols == ceil(src_w/mb_size) and
  * mb_rows == ceil(src_h/mb_size) (coded grid, reading Q3); 1 <= grid_w, grid_h; grid_w*grid_h <= 4096;
- * group >= 1 divides grid_w and grid_h; mb_rows*grid_w <= 8192; 1 <= patch <= 32 (compact only);
+ * group >= 1 divides grid_w and grid_h; mb_rows*grid_w <= 8192; 1 <= patch and group*patch <= 32 (the
+ * compaction calls: a group's pixel rows fit one warp; else CS_ERR_UNSUPPORTED);
  * tau >= 0 (may be +inf), alpha >= 0 finite.                                                                 */
 typedef struct {
   int32_t src_w, src_h;     /* displayed source size in px (448x448, 1920x1080, 3840x2160)                   */
