@@ -685,9 +685,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         e2e = dict(ms=e2e_ms, wall_ms=wall_ms, steps=nsteps, h2d=h2d, d2h=d2h, checksum=checksum)
 
     # ---- reduce over ranks --------------------------------------------------------------------------------
-    tens = shard.reduce_max(torch.tensor([ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device=dev))
+    tens = shard.reduce_max(torch.tensor([ms, e2e["ms"] if e2e else 0.0, e2e["wall_ms"] if e2e else 0.0],
+                                         dtype=torch.float64, device=dev))
     cnt_all = shard.reduce_counters(dcnt)
     ms_max, e2e_ms_max = float(tens[0]), float(tens[1])
+    if e2e:
+        e2e["wall_ms"] = float(tens[2])  # the slowest rank's host wall clock (all ranks' frames are counted)
     if rank != 0:
         return
     c = cnt_all.cpu().numpy().astype(np.int64)
