@@ -23,6 +23,9 @@ namespace cg = cooperative_groups;
 
 namespace {
 
+#ifndef CS_FUSED_SMEM_KB
+#define CS_FUSED_SMEM_KB 68u  // fused kernel dynamic shared memory per CTA (3 CTAs per SM; registers allow no 4th)
+#endif
 constexpr int kThreads = 256;
 constexpr uint32_t kIntraSq = 0xffffffffu;  // > any |mv|^2 (<= 2^31)
 
@@ -805,7 +808,7 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
   // the fused kernel (3 CTAs/SM; the compaction's TMA rings reuse the staging memory), and the SM's whole 200 KB
   // when all the fused grid's clusters are co-resident even then (one wave at one CTA per SM, e.g. C2): deeper
   // rings, more bytes in flight per SM (measured)
-  unsigned budget = P.fused ? 68u * 1024u : 50u * 1024u;
+  unsigned budget = P.fused ? CS_FUSED_SMEM_KB * 1024u : 50u * 1024u;
   if (P.fused && fused_one_wave(fn, cfg, n_streams)) budget = kWideSmem;
 
   // layout: small regions first, then the MB staging ring, Vrow, Srow (only with alpha != 0); the MB ring takes
