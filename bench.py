@@ -816,8 +816,8 @@ def main():
     if shared:
         local_rank = 0
     cfg = workload(args.workload, args.streams, args.kv_mode, args)
-    # the fused score+compact kernel takes model frames, one frame per token, no overlap mode
-    args.fused = bool(args.fused and args.frames == "model" and args.temporal_patch == 1 and not args.overlap)
+    # the fused score+compact kernel takes model frames, one frame per token
+    args.fused = bool(args.fused and args.frames == "model" and args.temporal_patch == 1)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

@@ -33,8 +33,7 @@ class Pipeline:
         # fused: one codecsight_score_compact launch per step (NEXT-2) instead of score_patches + compact
         self.fused = fused
         if fused:
-            assert temporal_patch == 1 and preprocess is None and not overlap, \
-                "fused score+compact: model frames, temporal_patch 1, no overlap mode"
+            assert temporal_patch == 1 and preprocess is None, "fused score+compact: model frames, temporal_patch 1"
         # temporal patches (NEXT-3, Qwen2-VL temporal_patch_size): a token unit = tp consecutive frames; scoring stays
         # per frame, compaction emits [3][tp][p][p] rows per unit (codecsight_compact_tp) and writes the unit masks /
         # types into a unit ring, and the KV refresh runs over units (window w/tp, stride s/tp)
@@ -52,7 +51,7 @@ class Pipeline:
         self.compact_chunk = compact_chunk
         self.S, self.w, self.s, self.gop = n_streams, window, stride, gop
         # overlap: compact and kv_refresh of step k run on their own streams concurrently with the scoring of step
-        # k+1; the ring then holds w + 2s frames so that step k+1's new masks never land on slots kv_refresh(k)
+        # k+1 (fused: kv_refresh of step k concurrently with the score+compact of step k+1); the ring then holds w + 2s frames so that step k+1's new masks never land on slots kv_refresh(k)
         # still reads (frames [(k-1)s, ks+w) and the next s frames are w + 2s distinct slots)
         self.overlap = overlap
         self.ring = window + (2 * stride if overlap else stride)
@@ -122,7 +121,7 @@ class Pipeline:
             self.sc_workspace = torch.zeros(abi.score_compact_workspace_size(S), dtype=torch.uint8, device=d)
         self._side_done = {}  # step -> events closing its compact / kv_refresh work (overlap mode)
         self._graphs = {}     # graph_step: key -> captured torch.cuda.CUDAGraph
-        self._bound = {}      # (ring slot, frames) -> abi.BoundScoreCompact
+        self._bound = {}      # (ring slot, frames, buffer parity) -> abi.BoundScoreCompact
         self._type_views = {}
         if overlap:
             self.stream_compact = torch.cuda.Stream(d)
@@ -193,14 +192,15 @@ class Pipeline:
             s0 = ev(main)
             if self.fused:
                 fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
-                call = self._bound.get((off, n))
-                if call is None:  # arguments of this ring slot marshalled once (fused mode has no buffer parity)
+                key = (off, n, k & 1 if self.overlap else 0)
+                call = self._bound.get(key)
+                if call is None:  # arguments of this ring slot (and output buffer set) marshalled once
                     call = abi.BoundScoreCompact(
                         g, self.S, n, self.type_ring[:, off:], self.mask_ring[:, off:], self.ring, self.gop_state,
                         self.scores(n), self.kept_counts(n), self.capacity, self.packed, self.pos_ids,
                         self.src_index, self.frame_offsets[: self.S * n + 1], self.sc_workspace, self.counters,
                         self.status, frame_layout=self.frame_layout)
-                    self._bound[(off, n)] = call
+                    self._bound[key] = call
                 call(mb, fi, frame_ptrs, main.cuda_stream)
             else:
                 abi.codecsight_score_patches(g, self.S, n, mb, self.type_ring[:, off:], self.mask_ring[:, off:],

@@ -733,6 +733,81 @@ def test_pipeline_end_to_end_c4_shape(abi, ref, overlap):
     assert int(pipe.status.item()) == 0
 
 
+@pytest.mark.parametrize("kv_mode", ["paged", "copy"])
+def test_pipeline_fused_overlap_matches_sequential(abi, ref, kv_mode):
+    """Fused score+compact with overlap (kv_refresh of step k on its own stream, concurrent with score+compact of
+    step k+1), every step enqueued without a host synchronisation, against the same steps run sequentially (itself
+    parity-tested against the oracle): final GOP state, each frame's mask, the K/V cache state, slot maps and the
+    last two steps' outputs (one per buffer set) must be bit-identical."""
+    from paper_2604_06036_b200.pipeline import Pipeline
+    cfg = synth.CONFIGS["C4"]
+    g = make_grid(1920, 1080)
+    S, w, s, gop = 6, 16, 4, 16
+    kvb = dict(synth.QWEN_KV, layers=2)
+    K = 9
+    rng = np.random.default_rng(5)
+    frames_h = synth.random_frames(S * w, 448, 448, rng)
+    frames_d = [torch.from_numpy(to_grouped(f, g).view(np.int16)).to(DEV) for f in frames_h]
+    gens = [synth.StreamGen(1920, 1080, synth.scene_of(cfg, si), synth.stream_seed(cfg, si)) for si in range(S)]
+    inputs = []
+    for k in range(K):
+        f0, n = (0, w) if k == 0 else ((k - 1) * s + w, s)
+        mb = np.stack([np.stack([gens[si].next_frame() for _ in range(n)]) for si in range(S)])
+        types = np.stack([synth.frame_types(n, gop, f0) for _ in range(S)])
+        fidx = np.tile(np.arange(f0, f0 + n, dtype=np.int32), S)
+        inputs.append((d_mb(mb), abi.ptr_array(frames_d[:S * n], DEV), torch.from_numpy(fidx).to(DEV),
+                       torch.from_numpy(types).to(DEV)))
+    runs = {}
+    for overlap in (False, True):
+        pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=32, device=DEV, frame_layout=abi.CS_LAYOUT_GROUPED,
+                        kv_mode=kv_mode, compact_chunk=s, fused=True, overlap=overlap)
+        gen = torch.Generator(device=DEV)
+        gen.manual_seed(9)
+        pipe.init_cache_fill(gen)
+        outs = {}
+        for k in range(K):
+            pipe.step(k, *inputs[k])
+            if not overlap:
+                torch.cuda.synchronize()
+            if k >= K - 2:   # the last two steps' outputs live in different buffer sets with overlap
+                bufs = (pipe.packed, pipe.pos_ids, pipe.src_index, pipe.frame_offsets, pipe.kept_count,
+                        pipe.disposition, pipe.p_old, pipe.n_tokens)
+                outs[k] = bufs if overlap else tuple(t.clone() for t in bufs)   # sequential: one buffer set
+        pipe.join()
+        torch.cuda.synchronize()
+        f_last = (K - 1) * s + w   # frames 0 .. f_last-1 exist; masks of the last w + s frames by frame index
+        masks = {f: pipe.mask_ring[:, f % pipe.ring].cpu().numpy() for f in range(f_last - w - s, f_last)}
+        state = dict(gop=pipe.gop_state.cpu().numpy(), masks=masks, status=int(pipe.status.item()),
+                     counters=pipe.counters.cpu().numpy(),
+                     caches=[_host_cache(c).copy() for c in pipe.caches[pipe.cur if kv_mode == "copy" else 0]],
+                     slots=pipe.slots[pipe.cur].cpu().numpy() if kv_mode == "paged" else None,
+                     outs={k: [(t.view(torch.int16) if t.dtype == torch.bfloat16 else t).cpu().numpy().copy()
+                               for t in v] for k, v in outs.items()})
+        runs[overlap] = state
+        del pipe
+    a, b = runs[False], runs[True]
+    assert a["status"] == b["status"] == 0
+    assert (a["gop"] == b["gop"]).all()
+    for f in a["masks"]:
+        assert (a["masks"][f] == b["masks"][f]).all(), f
+    assert (a["counters"] == b["counters"]).all()
+    for x, y in zip(a["caches"], b["caches"]):
+        assert (x.view(np.uint16) == y.view(np.uint16)).all()
+    if kv_mode == "paged":
+        assert (a["slots"] == b["slots"]).all()
+    for k in a["outs"]:   # the valid part of each output (stale rows of earlier steps differ by buffer set)
+        (pa, qa, sa, fa, ka, da, oa, na), (pb, qb, sb, fb, kb, db, ob, nb_) = a["outs"][k], b["outs"][k]
+        assert (fa[:S * s + 1] == fb[:S * s + 1]).all(), k
+        tot = int(fa[S * s])
+        assert (pa[:tot].view(np.uint16) == pb[:tot].view(np.uint16)).all(), k
+        assert (qa[:tot] == qb[:tot]).all() and (sa[:tot] == sb[:tot]).all(), k
+        assert (ka.reshape(-1)[:S * s] == kb.reshape(-1)[:S * s]).all(), k
+        assert (na == nb_).all(), k
+        for si in range(S):
+            nt = int(na[si, 0]) + 32
+            assert (da[si, :nt] == db[si, :nt]).all() and (oa[si, :nt] == ob[si, :nt]).all(), (k, si)
+
+
 @pytest.mark.parametrize("rope", ["1d", "mrope"])
 def test_pipeline_temporal_patch2(abi, ref, rope):
     """Pipeline with Qwen2-VL temporal patches (tp = 2) on a C4-shaped shard, paged KV over token units: per-frame
