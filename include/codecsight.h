@@ -58,7 +58,9 @@ enum {
   CS_STATUS_ORIGIN = 4,         /* an ANCHOR/REUSE token's p_old lies outside the old cache's capacity (the
                                    previous window was truncated; SPEC "origin mismatch"); row skipped    */
   CS_STATUS_BAD_FRAME_TYPE = 8, /* frame type not in {I, P} (B-frames are out of scope, S:8); treated as I       */
-  CS_STATUS_BAD_MB_TYPE = 16    /* macroblock type not in {INTER, SKIP, INTRA}; treated as INTRA (dynamic)        */
+  CS_STATUS_BAD_MB_TYPE = 16,   /* macroblock type not in {INTER, SKIP, INTRA}; treated as INTRA (dynamic)        */
+  CS_STATUS_MISALIGNED = 32     /* kv_refresh: a stream's cache / pool / refreshed buffer violates the alignment
+                                   rule below; no K/V row of that stream is moved (its index outputs are written)  */
 };
 
 enum { CS_FRAME_I = 0, CS_FRAME_P = 1 };
@@ -326,6 +328,10 @@ typedef struct {
  *
  *   keep_mask_ring    device [n_streams][ring_frames][grid_words] u32 (masks from score_patches)
  *   frame_type_ring   device [n_streams][ring_frames] u8
+ *   Alignment: when a row (H * D * element size bytes) is a multiple of 16 B, rows move by 16-B vectors and TMA
+ *   bulk copies, so every old_cache / new_cache / refreshed pointer must be 16-B aligned; otherwise element
+ *   aligned.  The pointers live in device arrays, so this is checked on the device: a stream that violates it
+ *   raises CS_STATUS_MISALIGNED and none of its rows move (never a misaligned-access fault).
  *   old_cache         device array [n_streams] of device pointers to window k-1 caches (not read when k == 0)
  *   new_cache         device array [n_streams] of device pointers to window k caches; must not alias old_cache
  *   refreshed         device array [n_streams] of device pointers to [layers][2][refresh_capacity][H][D]
@@ -360,7 +366,8 @@ int codecsight_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_windo
  *            in ascending slot order, in p_new order; rows copied from refreshed row r (if refreshed != NULL).
  * Only keys of reused tokens move: 57,344 B per reused token instead of 114,688 B (Qwen2-VL-7B bf16).
  *
- *   pool        device array [n_streams] of device pointers to the row pools (in/out, 16-B aligned)
+ *   pool        device array [n_streams] of device pointers to the row pools (in/out; pool and refreshed
+ *               pointers follow codecsight_kv_refresh's alignment rule, else CS_STATUS_MISALIGNED)
  *   slot_old    device [n_streams][slot_cap] i32: slots of window k-1 (read when k >= 1; entries outside
  *               [0, capacity) raise CS_STATUS_ORIGIN and the token gets no row)
  *   slot_new    device [n_streams][slot_cap] i32 out: slots of window k (-1 = no row); must not alias slot_old

@@ -20,6 +20,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "codecsight.h")
 CS_OK, CS_ERR_INVALID_ARGUMENT, CS_ERR_SHAPE, CS_ERR_UNSUPPORTED, CS_ERR_CUDA = 0, -1, -2, -3, -4
 CS_STATUS_CAPACITY, CS_STATUS_NO_IFRAME, CS_STATUS_ORIGIN, CS_STATUS_BAD_FRAME_TYPE, CS_STATUS_BAD_MB_TYPE = \
     1, 2, 4, 8, 16
+CS_STATUS_MISALIGNED = 32
 CS_FRAME_I, CS_FRAME_P = 0, 1
 CS_MB_INTER, CS_MB_SKIP, CS_MB_INTRA = 0, 1, 2
 CS_DISP_NEW, CS_DISP_ANCHOR, CS_DISP_REUSE = 0, 1, 2

@@ -889,11 +889,7 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
   }
 #undef CS_PICK
   if (grouped && tp == 1 && fast && g->grid_w == 32 && g->grid_h % 2 == 0 && g->grid_h == 32 && P.vec_out) {
-    static const int use_tma = [] {
-      const char* e = getenv("CS_COMPACT_TMA");
-      return e ? atoi(e) : 1;
-    }();
-    if (use_tma) {
+    {
       const int nst = 5;
       const size_t tsmem = (size_t)kTmaWarps * nst * kTmaStageAlloc;
       const void* tf = reinterpret_cast<const void*>(compact_gather_tma);

@@ -109,6 +109,18 @@ struct KvParams {
 
 __device__ __forceinline__ unsigned char* stream_ws(const KvParams& P, int s) { return P.ws + 16 + (long long)s * P.ws_stride; }
 
+// Rows are moved with 16-B vectors / TMA bulk copies whenever a row is a multiple of 16 B: every cache, pool and
+// recompute buffer of a stream must then be 16-B aligned (element-aligned otherwise).  Device pointer arrays cannot
+// be checked on the host, so each plan CTA checks its stream's buffers and, if one is misaligned, raises
+// CS_STATUS_MISALIGNED and moves no row of that stream (a misaligned vector access would be a sticky fault).
+__device__ __forceinline__ bool kv_misaligned(const KvParams& P, int sidx) {
+  const uintptr_t a = P.vec_copy ? 15u : static_cast<uintptr_t>(P.esz - 1);
+  uintptr_t m = reinterpret_cast<uintptr_t>(P.new_cache[sidx]);
+  if (P.k >= 1) m |= reinterpret_cast<uintptr_t>(P.old_cache[sidx]);
+  if (P.has_refreshed) m |= reinterpret_cast<uintptr_t>(P.refreshed[sidx]);
+  return (m & a) != 0;
+}
+
 // ------------------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ KvParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -213,6 +225,8 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
     // ---- clamp the data moves (same rules as the oracle, per row) ---------------------------------------
     int st = 0;
     if (n_total > P.token_cap) st |= CS_STATUS_CAPACITY;
+    const bool mis = kv_misaligned(P, sidx);
+    if (mis) st |= CS_STATUS_MISALIGNED;
     unsigned char* ws = stream_ws(P, sidx);
     KvSeg* wseg = reinterpret_cast<KvSeg*>(ws + sizeof(KvHdr));
     int nout = 0;
@@ -238,7 +252,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan(const __grid_constant__ 
         if (valid < len) st |= CS_STATUS_CAPACITY;
         kind = SEG_COPY;
       }
-      if (valid > 0) {
+      if (valid > 0 && !mis) {
         wseg[nout].p_new = static_cast<int>(pn);
         wseg[nout].len = static_cast<int>(valid);
         wseg[nout].kind = kind;
@@ -966,7 +980,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
   __shared__ PlanSeg s_seg[kMaxSeg];
   __shared__ int s_pold[kMaxSeg];
   __shared__ int s_disp[kMaxSeg];
-  __shared__ int s_nseg, s_ntotal, s_p0, s_n_old, s_r0, s_st;
+  __shared__ int s_nseg, s_ntotal, s_p0, s_n_old, s_r0, s_st, s_mis;
   __shared__ unsigned long long s_rot, s_cop;
 
   const int sidx = blockIdx.x;
@@ -1113,6 +1127,8 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     nt[3] = static_cast<int>(n_new);
     int st = 0;
     if (n_total > P.token_cap || n_total > P.slot_cap) st |= CS_STATUS_CAPACITY;
+    s_mis = kv_misaligned(P, sidx) ? 1 : 0;
+    if (s_mis) st |= CS_STATUS_MISALIGNED;
     s_st = st;
     KvHdr* hdr = reinterpret_cast<KvHdr*>(stream_ws(P, sidx));
     hdr->n_rows = static_cast<int>(n_total < P.max_tok ? n_total : P.max_tok);
@@ -1288,7 +1304,7 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     }
     __syncthreads();
     for (int i = tid; i < nruns; i += blockDim.x) runs[i].len = (i + 1 < nruns ? runs[i + 1].p_new : nmv) - runs[i].p_new;
-    if (tid == 0) reinterpret_cast<KvHdr*>(stream_ws(P, sidx))->n_seg = nruns;
+    if (tid == 0) reinterpret_cast<KvHdr*>(stream_ws(P, sidx))->n_seg = s_mis ? 0 : nruns;
   }
   CS_PLAN_PHASE(7);
   // per-warp reductions first: one shared atomic per warp instead of one per thread
@@ -1304,6 +1320,12 @@ __global__ void __launch_bounds__(kPlanThreads) kv_plan_paged(const __grid_const
     if (cop) atomicAdd(&s_cop, cop);
   }
   __syncthreads();
+  if (tid == 0 && s_mis) {  // misaligned buffers: no row of this stream moves (kv_prefix then counts no item)
+    KvHdr* hdr = reinterpret_cast<KvHdr*>(stream_ws(P, sidx));
+    hdr->n_rows = 0;
+    hdr->n_seg = 0;
+    s_rot = s_cop = 0;
+  }
   if (tid == 0) {
     cs::atomic_or_status(P.status, s_st);
     const unsigned long long rowb = (unsigned long long)(P.H * P.D * P.esz);
@@ -1457,18 +1479,36 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather_paged(const __grid_c
 }
 
 
-// Launch the TMA ring gather.  Geometry: warps per CTA x stages x stage bytes (one CTA per SM); default 8 warps x
-// 8 KB stages, as many stages (<= 6) as fit.  CS_KV_TMA="warps,stage_kb,stages" overrides (tuning experiments).
-static int launch_gather_tma(const KvParams& P, const cs_kv_desc* kv, cudaStream_t stream) {
-  int warps = 8, stage_kb = 8, nst = 0;
-  if (const char* e = getenv("CS_KV_TMA")) sscanf(e, "%d,%d,%d", &warps, &stage_kb, &nst);
-  if (warps < 1 || warps > kWarpsPerGather) warps = kWarpsPerGather;
-  const unsigned stage_bytes = static_cast<unsigned>(stage_kb) * 1024u;
-  const unsigned tab_bytes = static_cast<unsigned>(((8 * (P.D / 2)) + 127) & ~127);
-  const int fit = static_cast<int>((216u * 1024u) / (warps * (stage_bytes + tab_bytes)));
-  if (nst <= 0 || nst > fit) nst = fit;
-  if (nst > kMaxStages) nst = kMaxStages;
-  if (nst < 3) return CS_ERR_UNSUPPORTED;
+// Geometry of the TMA ring gather: warps per CTA x stages x 8 KB stages (one CTA per SM).  8 warps with as many
+// stages (<= 6) as fit; a row set whose per-stage cos/sin table leaves fewer than 3 stages per warp (head_dim > 256)
+// halves the warps until 3 fit.  Computed before ANY kernel of the call is enqueued: a configuration no geometry
+// serves takes the register-path gather instead (never a failure after the plan kernel ran, codecsight.h:24).
+struct TmaGeom {
+  int warps, nst;
+  unsigned stage_bytes, tab_bytes;
+};
+
+static bool tma_geometry(const KvParams& P, TmaGeom* t) {
+  const long long row_bytes = static_cast<long long>(P.H) * P.D * P.esz;
+  if (!(P.vec_rot && P.vec_copy && row_bytes <= kTmaChunk && (P.D % 4) == 0)) return false;
+  t->stage_bytes = static_cast<unsigned>(kTmaChunk);  // >= one row, so every chunk carries >= 1 row
+  t->tab_bytes = static_cast<unsigned>(((8 * (P.D / 2)) + 127) & ~127);
+  for (int warps = kWarpsPerGather; warps >= 2; warps /= 2) {
+    int nst = static_cast<int>((216u * 1024u) / (warps * (t->stage_bytes + t->tab_bytes)));
+    if (nst > kMaxStages) nst = kMaxStages;
+    if (nst >= 3) {
+      t->warps = warps;
+      t->nst = nst;
+      return true;
+    }
+  }
+  return false;
+}
+
+// Launch the TMA ring gather with a geometry from tma_geometry().
+static int launch_gather_tma(const KvParams& P, const cs_kv_desc* kv, const TmaGeom& t, cudaStream_t stream) {
+  const int warps = t.warps, nst = t.nst;
+  const unsigned stage_bytes = t.stage_bytes, tab_bytes = t.tab_bytes;
   const size_t smem = static_cast<size_t>(warps) * nst * (stage_bytes + tab_bytes);
   const int grid = cs_num_sms();
   const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
@@ -1564,17 +1604,17 @@ int cs_launch_kv_refresh(const cs_grid* g, const cs_kv_desc* kv, const cs_window
   const int lo = win->step >= 1 ? (win->step - 1) * win->stride : 0;
   const int nfr = win->step * win->stride + win->window - lo;
   const size_t plan_smem = static_cast<size_t>(nfr) * P.nw * 4;
+  TmaGeom geom{};
+  const bool tma_ok = tma_geometry(P, &geom);
   if (cs_set_smem_attr(reinterpret_cast<const void*>(kv_plan), 3, 128 * 1024)) return CS_ERR_CUDA;
   kv_plan<<<n_streams, kPlanThreads, plan_smem, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
 
-  const long long row_bytes = static_cast<long long>(P.H) * P.D * P.esz;
-  const bool tma_ok = P.vec_rot && P.vec_copy && row_bytes <= kTmaChunk && (P.D % 4) == 0;
   const int sms = cs_num_sms();
   kv_prefix<<<1, 1024, 0, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   if (tma_ok) {
-    const int rc = launch_gather_tma(P, kv, stream);
+    const int rc = launch_gather_tma(P, kv, geom, stream);
     if (rc) return rc;
   } else {
     const size_t gsmem = 8 * static_cast<size_t>((n_streams + 2) & ~1) + sizeof(KvSeg) * max_seg +
@@ -1628,8 +1668,8 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   P.partial_mode = 0;
   P.old_cache = pool;  // REUSE runs read and write the same pool rows
   P.new_cache = pool;
-  const long long row_bytes = static_cast<long long>(P.H) * P.D * P.esz;
-  const bool tma_ok = P.vec_rot && P.vec_copy && row_bytes <= kTmaChunk && (P.D % 4) == 0;
+  TmaGeom geom{};
+  const bool tma_ok = tma_geometry(P, &geom);
   P.partial_mode = (tma_ok && P.rot_pairs < P.D / 2) ? 1 : 0;
   P.prefix_mode = tma_ok ? 0 : 1;
   const int lo = win->step >= 1 ? (win->step - 1) * win->stride : 0;
@@ -1649,7 +1689,7 @@ int cs_launch_kv_refresh_paged(const cs_grid* g, const cs_kv_desc* kv, const cs_
   kv_prefix<<<1, 1024, 0, stream>>>(P);
   if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   if (tma_ok) {
-    const int rc = launch_gather_tma(P, kv, stream);
+    const int rc = launch_gather_tma(P, kv, geom, stream);
     if (rc) return rc;
   } else {
     const int grid = cs_num_sms() * 4;

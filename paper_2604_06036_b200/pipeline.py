@@ -30,6 +30,15 @@ class Pipeline:
                  compact_chunk: int | None = None, preprocess: dict | None = None, overlap: bool = False,
                  temporal_patch: int = 1, fused: bool = False):
         self.g = dict(grid)
+        # Ring slots: frame f lives in slot f % ring and a step's n new frames are handed to the kernels as ONE
+        # contiguous run of slots [off, off + n) (the calls take a pointer and a frame stride, not a modular index).
+        # The run of step k >= 1 starts at ((k-1)s + w) % ring; with s dividing w (and hence the ring, w + s or
+        # w + 2s) it always ends inside the ring.  Otherwise some step would write past the ring's last slot (into
+        # the next stream's ring row), so such windows are rejected here rather than corrupted (SPEC allows any
+        # 1 <= s <= w; every BASELINE config has s | w).
+        if not (1 <= stride <= window) or window % stride != 0:
+            raise ValueError(f"Pipeline needs 1 <= stride <= window and stride | window (got w={window}, s={stride}): "
+                             "a step's new frames must be one contiguous run of ring slots")
         # fused: one codecsight_score_compact launch per step (NEXT-2) instead of score_patches + compact
         self.fused = fused
         if fused:

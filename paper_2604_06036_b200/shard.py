@@ -1,8 +1,13 @@
 """Stream sharding across GPUs: independent camera streams, no data-path collective.
 
 Stream sigma runs on rank sigma mod N (round-robin interleaves scene kinds so static and high-motion streams are
-spread over ranks); after the timed loop the u64 counters are summed and the device time is max-reduced with one
-collective each (NCCL on the GPU box, gloo in the CPU tests).
+spread over ranks).  Two ways to size a run (BASELINE.json configs):
+  strong  a fixed set of streams split over the ranks (C4: "256 streams ... sharded over 2/4/8 B200"): rank r owns
+          {sigma < n_total : sigma mod N = r}, i.e. n_total / N streams (the first n_total mod N ranks one more);
+  weak    a fixed number of streams per rank (C5: 1,024 streams on 8 GPUs = 128 per GPU): rank r owns
+          r, r + N, ..., r + N (per_rank - 1).
+After the timed loop the u64 counters are summed, the device time is max-reduced and the per-rank times are
+gathered (load imbalance) -- one small collective each (NCCL on the GPU box, gloo in the CPU tests).
 """
 from __future__ import annotations
 
@@ -15,14 +20,32 @@ def stream_ids(rank: int, world: int, per_rank: int) -> list[int]:
     return [rank + world * i for i in range(per_rank)]
 
 
+def partition(rank: int, world: int, n_total: int) -> list[int]:
+    """Global stream ids owned by `rank` under strong scaling (`n_total` streams split over `world` ranks)."""
+    return list(range(rank, n_total, world))
+
+
+def shard_ids(rank: int, world: int, streams: int, scaling: str) -> list[int]:
+    """`streams` = the total under "strong", the per-rank count under "weak"."""
+    if scaling == "strong":
+        return partition(rank, world, streams)
+    if scaling == "weak":
+        return stream_ids(rank, world, streams)
+    raise ValueError(f"scaling must be 'strong' or 'weak', got {scaling!r}")
+
+
 def owner(stream_id: int, world: int) -> int:
     return stream_id % world
+
+
+def _multi() -> bool:
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
 
 
 def reduce_counters(counters: torch.Tensor) -> torch.Tensor:
     """SUM of the per-rank counter vectors (int64); identity without a process group."""
     out = counters.clone()
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if _multi():
         dist.all_reduce(out, op=dist.ReduceOp.SUM)
     return out
 
@@ -30,6 +53,15 @@ def reduce_counters(counters: torch.Tensor) -> torch.Tensor:
 def reduce_max(values: torch.Tensor) -> torch.Tensor:
     """MAX over ranks (device times: the job is as slow as its slowest rank)."""
     out = values.clone()
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if _multi():
         dist.all_reduce(out, op=dist.ReduceOp.MAX)
     return out
+
+
+def gather_per_rank(values: torch.Tensor) -> list[list[float]]:
+    """Every rank's copy of a small vector (per-rank device times and shard sizes), in rank order."""
+    if not _multi():
+        return [values.double().cpu().tolist()]
+    parts = [torch.empty_like(values) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, values.contiguous())
+    return [p.double().cpu().tolist() for p in parts]

@@ -13,6 +13,8 @@ import torch
 import synth
 from synth import make_grid
 
+import kvcheck
+
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
@@ -62,6 +64,7 @@ def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused, rope):
     st_h = {si: dict(gop=np.zeros((1, nw + 1), np.uint32), mring=np.zeros((1, ring, nw), np.uint32),
                      tring=np.zeros((1, ring), np.uint8), slot=None) for si in sample}
     L = kvb["layers"]
+    stats = {}
     for k in range(steps):
         f0, n = pipe.new_frames(k)
         mb = np.stack([np.stack([gn.next_frame() for _ in range(n)]) for gn in gens])
@@ -95,6 +98,7 @@ def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused, rope):
             kv = pipe.kv
             win = dict(window=w, stride=s, step=k, ring_frames=ring)
             pool = pool_before[si]
+            pre = pool.copy()
             ko = ref.kv_refresh_paged(g, kv, win, h["mring"], h["tring"], [pool], h["slot"], pipe.token_cap,
                                       [refr[si]] if k >= 1 else None, pipe.token_cap)
             ntok = int(ko["n_tokens"][0, 0]) + cfg["n_prompt"]
@@ -102,11 +106,10 @@ def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused, rope):
             assert (disp_d[si, :ntok] == ko["disposition"][0, :ntok]).all()
             assert (pold_d[si, :ntok] == ko["p_old"][0, :ntok]).all()
             assert (slot_d[si, :ntok] == ko["slot_new"][0, :ntok]).all()
-            got = _host(pipe.caches[0][si])
-            assert (got[:, 1] == pool[:, 1]).all()                 # values: bit copies / untouched
-            fa = (got[:, 0].astype(np.uint32) << 16).view(np.float32)
-            fb = (pool[:, 0].astype(np.uint32) << 16).view(np.float32)
-            assert np.abs(fa - fb).max() <= 1e-2                   # keys: rotated within the bf16 bound
+            # the whole pool: refreshed rows and untouched rows bit-identical, rotated keys within the bf16 bound
+            kvcheck.check_pool_step(_host(pipe.caches[0][si]), pre, pool, ko["disposition"][0], ko["slot_new"][0],
+                                    ntok, kv, refr=refr[si] if k >= 1 else None, stats=stats,
+                                    tag=f"{cfg_name} step {k} stream {si}")
             h["slot"] = ko["slot_new"]
         # compaction of the last chunk (the packed buffer holds the last s frames of the step)
         last0 = 0 if fused else n - min(n, s)   # fused: one compaction of all the step's frames
@@ -126,3 +129,4 @@ def test_fullsize_sampled_streams(ref, cfg_name, S, steps, sample, fused, rope):
             assert (packed_d[a:b] == co["packed"][:cnt]).all()
             assert (pos_d[a:b] == co["pos_ids"][:cnt]).all()
             assert (src_d[a:b] - si * nl * 1024 == co["src_index"][:cnt]).all()
+    kvcheck.assert_rotation_bits(stats)

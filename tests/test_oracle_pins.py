@@ -600,16 +600,38 @@ def test_kv_bf16_rotation_vs_textbook(ref):
 
 
 def test_bf16_rne_store(ref):
-    # rotation by 0 of a bf16 row must reproduce the bits exactly (RNE of an exactly representable value)
+    """The bf16 store of a rotated key rounds to nearest, ties to EVEN (reading Q20).  Keys are chosen
+    (tests/rne_ties.py) so that the fp32 result of Eq. 5 is exactly a bf16 tie, with both parities of the upper
+    half; the expected bits come from PyTorch's own fp32 -> bf16 conversion, not from the oracle."""
+    import rne_ties
     g = make_grid(128, 128, mb_size=32, grid_w=4, grid_h=4, patch=4, group=2)
-    masks = _masks_from_groups(g, [[0], [1], [0], [1], [], [], [2], [3]])
+    masks = _masks_from_groups(g, [[0], [1], [0, 1], [2], [0], [0, 1, 2, 3], [1], [2]])
     types = np.ones(8, np.uint8)
     types[0] = 0
-    kv = dict(layers=1, kv_heads=1, head_dim=8, dtype=0, capacity=16, refresh_capacity=16, rope_base=1e4, n_prompt=0)
+    D, base = 128, 1e4
+    kv = dict(layers=1, kv_heads=1, head_dim=D, dtype=0, capacity=16, refresh_capacity=16, rope_base=base,
+              n_prompt=0)
+    # window k=2 ([4,8) after [2,6)): dropped frames 2, 3 carry 3 tokens -> dp = -3; f4 ANCHOR (first overlap
+    # frame), f5's 4 tokens REUSE from p_old 4..7 to p_new 1..4
+    rows, ties = rne_ties.tie_rows(4, D, base, -3)
     rng = np.random.default_rng(1)
-    old = rng.integers(0, 65536, size=(1, 2, 16, 1, 8), dtype=np.uint16) & np.uint16(0xBFFF)
+    old = rng.integers(0, 65536, size=(1, 2, 16, 1, D), dtype=np.uint16) & np.uint16(0xBFFF)
+    old[0, 0, 4:8, 0] = rows
     new = np.zeros_like(old)
-    # window k=2, s=2, w=4 -> [4,8); dropped frames [2,4) have 2 tokens -> dp = -2
     out = ref.kv_refresh(g, kv, dict(window=4, stride=2, step=2, ring_frames=8), masks[None], types[None],
                          [old], [new], None, 16)
-    assert out["rc"] == 0
+    assert out["rc"] == 0 and out["status"] == 0
+    assert list(out["disposition"][0, :6]) == [1, 2, 2, 2, 2, 0]
+    assert list(out["p_old"][0, 1:5]) == [4, 5, 6, 7]
+    n_even = n_odd = 0
+    for j in range(4):
+        idx = np.array([e for e, _ in ties[j]])
+        o = np.array([v for _, v in ties[j]], np.float32)
+        exp = rne_ties.rne_bf16(o)
+        up = (o.view(np.uint32) >> 16).astype(np.uint16)
+        assert ((exp == up) | (exp == up + 1)).all()               # a tie rounds to one of its neighbours
+        assert (new[0, 0, 1 + j, 0, idx] == exp).all(), j          # ... the even one
+        assert (new[0, 1, 1 + j] == old[0, 1, 4 + j]).all()        # V reused bit for bit (P:361)
+        n_even += int((up % 2 == 0).sum())
+        n_odd += int((up % 2 == 1).sum())
+    assert n_even >= 20 and n_odd >= 20, (n_even, n_odd)        # both directions of the tie rule exercised
