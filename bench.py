@@ -37,7 +37,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)   # 10 warm-up steps, >= 50 timed
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="C4")
-    ap.add_argument("--streams", type=int, default=None, help="streams per GPU (default: the config's)")
+    ap.add_argument("--streams", type=int, default=None,
+                    help="streams: the total under --scaling strong, per GPU under weak (default: the config's)")
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="strong: the workload's streams split over the GPUs (C4: 256 streams 'sharded over 2/4/8 "
+                         "B200'); weak: that many streams on every GPU (C5: 128 per GPU, 1,024 on 8).  Default: "
+                         "strong for C4, weak otherwise")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tau", type=float, default=0.25, help="Eq. 4 threshold in source px (P:459)")
     ap.add_argument("--alpha", type=float, default=0.0, help="Eq. 3 residual weight (P:299)")
@@ -76,6 +81,9 @@ def parse():
     return ap.parse_args()
 
 
+SCENE_KINDS = list(synth.SCENES)
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -109,7 +117,22 @@ def workload(name: str, streams: int | None, kv_mode: str = "paged", args=None):
             raise SystemExit("C5 needs --kv-mode paged (out-of-place caches do not fit one GPU)")
     if streams is not None:
         cfg["streams"] = streams
+    # BASELINE configs[3] (C4): a fixed set of 256 streams sharded over 1/2/4/8 GPUs -> strong scaling; C5 is quoted
+    # per GPU (1,024 streams on 8 = 128 each) -> weak; C2 / C3 are single-GPU configs (N > 1 replicates them)
+    cfg["scaling"] = getattr(args, "scaling", None) or ("strong" if name == "C4" else "weak")
     return cfg
+
+
+def host_cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def step_frames(cfg, k):
@@ -377,12 +400,15 @@ def run_reference(args, cfg, rank, world):
     fps = tot["frames"] / tot["seconds"]
     out = {"impl": "reference", "metric": "codec-pruned frames/sec (whole hot path: score+compact+kv_refresh), all GPUs",
            "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": 1000.0 * tot["seconds"] / args.steps, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-           "config": {"workload": cfg["name"], "streams_per_gpu": cfg["streams"], "window": cfg["window"],
+           "ms_per_step": 1000.0 * tot["seconds"] / args.steps, "higher_is_better": True,
+           "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+           "config": {"workload": cfg["name"], "streams_total": cfg["streams"] * (1 if cfg["scaling"] == "strong"
+                                                                                   else world),
+                      "window": cfg["window"],
                       "stride": cfg["stride"], "gop": cfg["gop"], "tau": cfg["tau"], "alpha": cfg["alpha"], "group": cfg["group"],
                       "temporal_patch": args.temporal_patch},
            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                            "cpu_model": host_cpu_model(),
                             "sample": f"{tot['stream_steps']} whole stream-steps (k=4) of alternating "
                                       f"static/high-motion streams, {cores} concurrent single-threaded C oracle "
                                       f"process(es)"},
@@ -406,8 +432,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     abi.lib()
     sw, sh = cfg["src"]
     g = synth.make_grid(sw, sh, tau=cfg["tau"], alpha=cfg["alpha"], group=cfg["group"])
-    S, w, s, gop = cfg["streams"], cfg["window"], cfg["stride"], cfg["gop"]
-    global_ids = shard.stream_ids(rank, world, S)
+    w, s, gop = cfg["window"], cfg["stride"], cfg["gop"]
+    scaling = cfg["scaling"]
+    global_ids = shard.shard_ids(rank, world, cfg["streams"], scaling)
+    S = len(global_ids)                     # this rank's streams
+    S_total = cfg["streams"] if scaling == "strong" else cfg["streams"] * world
+    if S == 0:
+        raise SystemExit(f"rank {rank}: no streams ({cfg['streams']} streams over {world} ranks)")
     kvb = cfg["kv"]
     if kvb is not None and args.rope == "mrope":
         kvb = dict(kvb, rope_mode=1, mrope_section=(16, 24, 24), t_per_frame=1)
@@ -596,6 +627,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # compute stream, and the step's results (token counts per stream, kept counts, packed rows) come back D2H;
     # the host waits for step k-1's results while step k runs (a streaming server's pipeline).
     e2e = None
+    scene_acc = [0.0] * (2 * len(SCENE_KINDS))
     if not args.no_e2e:
         k0 = warm + args.steps + calib
         nsteps = args.steps
@@ -622,6 +654,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         e_a = torch.cuda.Event(enable_timing=True)
         e_b = torch.cuda.Event(enable_timing=True)
         checksum = 0
+        kept_acc = np.zeros(S, np.int64)   # per-stream kept patches of the e2e steps (results the host reads)
         t0 = time.perf_counter()
         e_a.record(copy_stream)
         res_stream = torch.cuda.Stream(dev)
@@ -674,20 +707,31 @@ def run_ours(args, cfg, rank, world, local_rank):
             if i >= 1:
                 done[1 - b].synchronize()                                  # the host consumes step k-1's result
                 checksum += int(res[1 - b][-1])
+                kept_acc += res[1 - b][S * 4:S * 4 + S * s].numpy().reshape(S, s).sum(axis=1)
         stream.wait_stream(res_stream)
         e_b.record(stream)
         done[(k0 + nsteps - 1) & 1].synchronize()
         checksum += int(res[(k0 + nsteps - 1) & 1][-1])
+        kept_acc += res[(k0 + nsteps - 1) & 1][S * 4:S * 4 + S * s].numpy().reshape(S, s).sum(axis=1)
         torch.cuda.synchronize()
         wall_ms = (time.perf_counter() - t0) * 1e3
         e2e_ms = e_a.elapsed_time(e_b)
         h2d = in_mb[0].numel() + in_ty[0].numel() + in_fi[0].numel() * 4
         d2h = (S * 4 + S * s + 1) * 4
         e2e = dict(ms=e2e_ms, wall_ms=wall_ms, steps=nsteps, h2d=h2d, d2h=d2h, checksum=checksum)
+        # per scene kind: kept patches / patches over the e2e steps (calibration check against P:563)
+        for i, gid in enumerate(global_ids):
+            j = SCENE_KINDS.index(synth.scene_of(cfg, gid))
+            scene_acc[2 * j] += float(kept_acc[i])
+            scene_acc[2 * j + 1] += float(nsteps * s * pipe.np)
 
     # ---- reduce over ranks --------------------------------------------------------------------------------
+    scene_tot = shard.reduce_counters(torch.tensor(scene_acc, dtype=torch.float64, device=dev)).cpu().numpy()
     tens = shard.reduce_max(torch.tensor([ms, e2e["ms"] if e2e else 0.0, e2e["wall_ms"] if e2e else 0.0],
                                          dtype=torch.float64, device=dev))
+    # per-rank device times and shard sizes (load imbalance across ranks)
+    per_rank = shard.gather_per_rank(torch.tensor([ms, float(S), e2e["ms"] if e2e else 0.0], dtype=torch.float64,
+                                                  device=dev))
     cnt_all = shard.reduce_counters(dcnt)
     ms_max, e2e_ms_max = float(tens[0]), float(tens[1])
     if e2e:
@@ -696,9 +740,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         return
     c = cnt_all.cpu().numpy().astype(np.int64)
     K = args.steps
-    frames_total = S * world * s * K
+    frames_total = S_total * s * K
     value = frames_total / (ms_max / 1e3)
-    stream_steps = S * world * K / (ms_max / 1e3)
+    stream_steps = S_total * K / (ms_max / 1e3)
     kv_ms = float(np.mean(per["kv"])) if per["kv"] else 0.0
     kv_bytes_launch = float(dcnt[abi.CNT_BYTES_KV].item()) / K
     peak, peak_kind = measured_peak_hbm()
@@ -723,9 +767,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     out = {
         "metric": "codec-pruned frames/sec (whole hot path: score+compact+kv_refresh), all GPUs",
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": warm,
-        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": cfg["name"], "streams_per_gpu": S, "streams_total": S * world, "src": list(cfg["src"]),
+        "config": {"workload": cfg["name"], "streams_per_gpu": S if scaling == "weak" else
+                   [int(r[1]) for r in per_rank], "streams_total": S_total, "src": list(cfg["src"]),
                    "model_input": [448, 448], "window": w, "stride": s, "gop": gop, "tau": cfg["tau"], "alpha": cfg["alpha"], "group": cfg["group"],
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
@@ -735,6 +780,11 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "
                          "see per-step bytes)"},
         "streams_per_sec": stream_steps,
+        "per_gpu": {"frames_per_sec": value / world, "streams_per_sec": stream_steps / world},
+        "per_rank": [{"rank": i, "streams": int(r[1]), "ms_per_step": r[0] / K,
+                      "frames_per_sec": r[1] * s * K / (r[0] / 1e3), "e2e_ms_per_step": r[2] / K if e2e else None}
+                     for i, r in enumerate(per_rank)],
+        "host_cpu": host_cpu_model(),
         "host_enqueue_ms_per_step": host_ms / K,
         "kv_refresh_gbs": achieved,
         "per_kernel_ms": ({"score_compact": sc_ms, "kv_refresh": kv_ms} if args.fused else
@@ -745,13 +795,17 @@ def run_ours(args, cfg, rank, world, local_rank):
         "frame_layout": args.frame_layout,
         "compact_by_layout": layouts,
         "kept_fraction": kept_frac,
+        # per scene kind over the e2e steps; calibration targets kept 0.50 / 0.73 / 0.87 for low / medium / high
+        # motion (50 / 27 / 13 % of visual tokens pruned), traffic "medium-high" ~0.80, static = I-frames only
+        "kept_fraction_by_scene": {kind: scene_tot[2 * j] / scene_tot[2 * j + 1]
+                                   for j, kind in enumerate(SCENE_KINDS) if scene_tot[2 * j + 1] > 0},
         "tokens_per_step": {"reuse": int(c[abi.CNT_TOK_REUSE]) // K, "anchor": int(c[abi.CNT_TOK_ANCHOR]) // K,
                             "new": int(c[abi.CNT_TOK_NEW]) // K},
         "near_tau_patches": int(c[abi.CNT_NEAR_TAU]),
         "status": status,
         "kv_mode": args.kv_mode,
         "roofline": ({"bound": "hbm", "kernel": ("codecsight_kv_refresh_paged (kv_plan_paged + kv_prefix + "
-                                                 "kv_gather_paged)") if args.kv_mode == "paged" else
+                                                 "kv_gather_tma)") if args.kv_mode == "paged" else
                       "codecsight_kv_refresh (kv_plan + kv_prefix + kv_gather_tma)",
                       "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                       "frac": achieved / peak,
@@ -783,13 +837,14 @@ def run_ours(args, cfg, rank, world, local_rank):
     }
     if e2e:
         out["e2e"] = {"value": frames_total / (e2e_ms_max / 1e3), "unit": "frames/s",
-                      "h2d_bytes_per_step": e2e["h2d"] * world, "d2h_bytes_per_step": e2e["d2h"] * world,
+                      "h2d_bytes_per_step": e2e["h2d"] * S_total // S, "d2h_bytes_per_step": e2e["d2h"] * S_total // S,
                       "wall_clock_value": frames_total / (e2e["wall_ms"] / 1e3),
                       "pipelining": "H2D of step k+1 on a copy stream overlaps step k; host reads step k-1's result"}
     if not args.no_cpu_baseline and world == 1:  # the oracle baseline is timed at N = 1 only
         log("[rank 0] timing the CPU oracle on a bounded sample ...")
         r = oracle_sample(cfg, args.cpu_seconds, kv_mode=args.kv_mode, tp=tp)
         out["cpu_baseline"] = {"value": r["frames"] / r["seconds"], "unit": "frames/s", "cores": 1, "kind": "oracle",
+                               "cpu_model": host_cpu_model(),
                                "sample": f"{r['stream_steps']} whole stream-steps (window k=4: {s} new frames + "
                                          f"KV refresh) of streams {r['scenes'][:4]}..., single-threaded C oracle, "
                                          f"{r['seconds']:.1f} s"}
@@ -799,7 +854,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             if ra is not None:
                 out["cpu_baseline_all_cores"] = {
                     "value": ra["value"], "unit": "frames/s", "cores": ra["processes"], "kind": "oracle",
-                    "host_cpus": ra["host_cpus"],
+                    "host_cpus": ra["host_cpus"], "cpu_model": host_cpu_model(),
                     "sample": f"{ra['processes']} concurrent single-threaded oracle processes (one per core, capped "
                               f"by host memory and 32), {ra['stream_steps']} whole stream-steps (k=4) of disjoint "
                               f"streams, ~{ra['seconds']:.1f} s each"}

@@ -65,14 +65,24 @@ def frame_types(n_frames: int, gop: int, first: int = 0) -> np.ndarray:
     return np.where(f % gop == 0, FRAME_I, FRAME_P).astype(np.uint8)
 
 
-# Scene kinds (SURVEY §8(d) generator table; SPEC S:516 kinds for parity).
+# Scene kinds (SURVEY §8(d) generator table; SPEC S:516 kinds for parity).  Calibrated with the oracle
+# (scripts/calibrate_synth.py, tests/test_synth_calibration.py) to the paper's per-motion-level pruning, P:563:
+# 50 / 27 / 13 % of visual tokens pruned for low / medium / high motion (kept 0.50 / 0.73 / 0.87 of the patches of
+# a 16-frame window, its I-frame included); traffic is "medium-high" (kept ~0.80).
+#   k / v / size : moving objects (count, speed in px/frame, width as a fraction of the frame width)
+#   tex / blobs  : fraction of the frame covered by textured background regions (foliage, water, screens) in
+#                  `blobs` rectangles fixed per stream; each of their MBs flickers with a +-1 qpel vector (= tau, so
+#                  dynamic) with probability p_tex per frame.  Sensor noise on real encoders is spatially persistent
+#                  like this, not i.i.d. per frame (an i.i.d. 1-qpel MB anywhere would, under the GOP union of
+#                  P:318, end up touching almost every patch within a GOP)
+#   p_noise      : i.i.d. +-1 qpel MBs anywhere (only the SPEC "noise" kind and, sparsely, scene_cut)
 SCENES = {
-    #                 objects      speed px/frame  noise MB prob  object size (fraction of width)
     "static": dict(k=(0, 0), v=(0.0, 0.0), p_noise=0.0, size=(0.05, 0.1)),
-    "low": dict(k=(1, 2), v=(0.25, 1.0), p_noise=0.004, size=(0.12, 0.30)),
-    "medium": dict(k=(3, 5), v=(0.5, 3.0), p_noise=0.01, size=(0.12, 0.28)),
-    "high": dict(k=(6, 10), v=(1.0, 6.0), p_noise=0.05, size=(0.10, 0.25)),
-    "traffic": dict(k=(0, 0), v=(2.0, 8.0), p_noise=0.01, size=(0.03, 0.06), lanes=(3, 4), cars=(8, 20)),
+    "low": dict(k=(2, 4), v=(0.25, 1.0), p_noise=0.0, size=(0.15, 0.30), tex=0.15, blobs=(1, 3), p_tex=0.3),
+    "medium": dict(k=(6, 8), v=(0.5, 3.5), p_noise=0.0, size=(0.16, 0.30), tex=0.25, blobs=(2, 3), p_tex=0.3),
+    "high": dict(k=(11, 14), v=(1.5, 6.0), p_noise=0.0, size=(0.17, 0.32), tex=0.35, blobs=(2, 4), p_tex=0.3),
+    "traffic": dict(k=(0, 0), v=(2.0, 8.0), p_noise=0.0, size=(0.042, 0.082), lanes=(4, 5), cars=(8, 20),
+                    tex=0.05, blobs=(1, 2), p_tex=0.3),
     "translating_object": dict(k=(1, 1), v=(1.0, 2.0), p_noise=0.0, size=(0.15, 0.3)),
     "multi_object": dict(k=(3, 5), v=(0.25, 3.0), p_noise=0.0, size=(0.08, 0.2)),
     "noise": dict(k=(0, 0), v=(0.0, 0.0), p_noise=0.3, size=(0.05, 0.1)),
@@ -86,8 +96,9 @@ class StreamGen:
     Objects are axis-aligned boxes moving with a constant velocity (bouncing at the borders).  Macroblocks whose
     centre lies in a moving object get MV = round(4 v) qpel with +-1 qpel jitter (p = 0.2), type INTER,
     SAD ~ 256 U(8, 40); with p = 0.02 an object MB is INTRA (entering content).  Background MBs are SKIP with a
-    zero MV and SAD 0, except a fraction p_noise of INTER MBs with a +-1 qpel MV and SAD ~ 256 U(0, 3)
-    (sensor noise).  "scene_cut" P-frames (probability p_cut) turn >= 80% of MBs INTRA."""
+    zero MV and SAD 0, except flickering MBs of the stream's textured regions (p_tex per frame) and a fraction
+    p_noise of i.i.d. MBs, both INTER with a +-1 qpel MV and SAD ~ 256 U(0, 3) (sensor noise).  "scene_cut"
+    P-frames (probability p_cut) turn >= 80% of MBs INTRA."""
 
     def __init__(self, src_w: int, src_h: int, scene: str, seed: int, mb_size: int = 16):
         self.src_w, self.src_h, self.mb = src_w, src_h, mb_size
@@ -118,6 +129,18 @@ class StreamGen:
                 objs.append([r.uniform(0, src_w), r.uniform(0, src_h), w, h, speed * math.cos(ang),
                              speed * math.sin(ang)])
         self.objs = np.array(objs, dtype=np.float64).reshape(-1, 6)
+        # textured background regions: `blobs` rectangles whose areas sum to ~tex of the frame, fixed per stream
+        self.tex = np.zeros((self.rows, self.cols), bool)
+        if sc.get("tex", 0.0) > 0:
+            nb = int(r.integers(sc["blobs"][0], sc["blobs"][1] + 1))
+            for _ in range(nb):
+                area = sc["tex"] / nb * self.rows * self.cols
+                aspect = r.uniform(0.5, 2.0)
+                bh = max(1, int(round(math.sqrt(area / aspect))))
+                bw = max(1, int(round(area / bh)))
+                j0 = int(r.integers(0, max(1, self.rows - bh + 1)))
+                i0 = int(r.integers(0, max(1, self.cols - bw + 1)))
+                self.tex[j0:j0 + bh, i0:i0 + bw] = True
         self.cx = (np.arange(self.cols) * mb_size + mb_size / 2.0)[None, :]
         self.cy = (np.arange(self.rows) * mb_size + mb_size / 2.0)[:, None]
 
@@ -143,8 +166,13 @@ class StreamGen:
         sc = self.scene
         rec = np.zeros((self.rows, self.cols), MB_DTYPE)
         rec["type"] = MB_SKIP
+        noise = None
         if sc["p_noise"] > 0:
             noise = r.random((self.rows, self.cols)) < sc["p_noise"]
+        if sc.get("tex", 0.0) > 0:
+            flick = self.tex & (r.random((self.rows, self.cols)) < sc["p_tex"])
+            noise = flick if noise is None else (noise | flick)
+        if noise is not None:
             if noise.any():
                 k = int(noise.sum())
                 mv = r.integers(-1, 2, size=(k, 2))
