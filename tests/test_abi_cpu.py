@@ -32,6 +32,24 @@ def test_sm100a_cubin_only(abi):
     assert "sm_100a" in out
 
 
+def test_sass_keeps_the_bulk_copy_pipelines(abi):
+    """The hot kernels move data with Blackwell bulk copies behind mbarriers: the KV gather's per-warp
+    TMA rings, the fused score+compact's MB ring and group ring, the grouped compaction's ring.  A change that
+    silently falls back to register copies fails here (evidence: profiles/r02_sass.txt)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    import sass_summary
+    ks = sass_summary.parse(abi.LIB_PATH)
+    need = {"void kv_gather_tma<unsigned short, 4, 128>": (1, 1), "void kv_gather_tma<float, 0, 0>": (1, 1),
+            "void score_kernel<true>": (1, 1), "void score_kernel<false>": (1, 0), "compact_gather_tma": (1, 1)}
+    for name, (g2s, s2g) in need.items():
+        v = ks[name]
+        assert v["UBLKCP.S.G"] >= g2s and v["UBLKCP.G.S"] >= s2g and v["SYNCS"] >= 1, (name, v)
+        if name != "void score_kernel<false>":     # (the unfused score kernel is off the default path)
+            assert v["stack"] == 0, (name, v)      # no local-memory spills in the hot kernels
+
+
 FAKE = 0x1000  # never dereferenced: validation fails (or the device check does) before any launch
 
 
