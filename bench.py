@@ -4,12 +4,14 @@ streams/s at 1/2/4/8 GPUs, KV-refresh GB/s vs HBM).
 
 A step = one pass of the whole hot path for every stream of the rank:
   codecsight_score_patches (s new frames/stream) -> codecsight_compact -> codecsight_kv_refresh (window k).
-Workload (default C4, BASELINE configs[3]): 256 1080p streams per GPU, even ids static / odd ids high-motion,
-w = 16, s = 4, GOP 16, Qwen2-VL-7B KV (28 x 4 x 128 bf16), 32 prompt rows.  Weak scaling: every rank owns 256
-streams (global ids rank + N*i), no collective on the data path; one NCCL all_reduce of counters and a MAX of the
-device time after the timed loop.
+Workload (default C4, BASELINE configs[3]): 256 1080p streams in total, even ids static / odd ids high-motion,
+w = 16, s = 4, GOP 16, Qwen2-VL-7B KV (28 x 4 x 128 bf16), 32 prompt rows, sharded over the N GPUs (strong scaling,
+snake-order stream assignment, paper_2604_06036_b200/shard.py); C5 runs 128 4K streams per GPU (weak scaling).
+No collective on the data path; one NCCL all_reduce of counters, a MAX of the device time and a gather of the
+per-rank times after the timed loop.  --workload cdf: the NEXT-4 similar-patch analysis (bench_cdf.py).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4|C3|C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4|C5|C3|C2|cdf] [--scaling strong|weak]
+                    [--impl ours|reference]
 """
 from __future__ import annotations
 
@@ -92,6 +94,7 @@ def log(*a):
 # workload
 # --------------------------------------------------------------------------------------------------------------
 def workload(name: str, streams: int | None, kv_mode: str = "paged", args=None):
+    name = name.upper()
     cfg = dict(synth.CONFIGS[name])
     # method parameters (SPEC CLI names): defaults are the paper's (tau 0.25 px, alpha 0)
     cfg["tau"] = getattr(args, "tau", 0.25)
@@ -107,7 +110,7 @@ def workload(name: str, streams: int | None, kv_mode: str = "paged", args=None):
             cfg[key] = v
     if not 1 <= cfg["stride"] <= cfg["window"]:
         raise SystemExit("need 1 <= stride <= window (S:129)")
-    if cfg["kv"] is None and name != "C2":
+    if cfg["kv"] is None and name not in ("C2", "CDF"):
         raise SystemExit(f"workload {name} has no KV shape")
     if name == "C5":
         # BASELINE: 1,024 streams on 8 B200 -> 128 streams per GPU (weak scaling unit).  Out of place, 128 x 2 x
@@ -874,6 +877,22 @@ def main():
     cfg = workload(args.workload, args.streams, args.kv_mode, args)
     # the fused score+compact kernel takes model frames, one frame per token
     args.fused = bool(args.fused and args.frames == "model" and args.temporal_patch == 1)
+    if cfg["name"].startswith("NEXT4"):
+        import bench_cdf
+        if args.impl == "reference":
+            bench_cdf.run_reference(args, cfg, rank, world)
+            return
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo" if shared else "nccl")
+        bench_cdf.run_ours(args, cfg, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

@@ -1,11 +1,15 @@
 """Stream sharding across GPUs: independent camera streams, no data-path collective.
 
-Stream sigma runs on rank sigma mod N (round-robin interleaves scene kinds so static and high-motion streams are
-spread over ranks).  Two ways to size a run (BASELINE.json configs):
+Streams are dealt to ranks in snake order: block b = sigma // N of N consecutive stream ids goes to ranks
+0, 1, ..., N-1 when b is even and N-1, ..., 0 when b is odd.  Neighbouring ids therefore land on different ranks and
+every rank gets the same mix of any periodic scene pattern (C4 alternates static / high-motion streams: plain
+round-robin sigma mod N would put every static stream on the even ranks -- measured 1.75 vs 6.82 ms per step at
+N = 2, profiles/r02_multirank_roundrobin.json -- while snake order gives each rank one of each per pair of blocks).
+Two ways to size a run (BASELINE.json configs):
   strong  a fixed set of streams split over the ranks (C4: "256 streams ... sharded over 2/4/8 B200"): rank r owns
-          {sigma < n_total : sigma mod N = r}, i.e. n_total / N streams (the first n_total mod N ranks one more);
-  weak    a fixed number of streams per rank (C5: 1,024 streams on 8 GPUs = 128 per GPU): rank r owns
-          r, r + N, ..., r + N (per_rank - 1).
+          {sigma < n_total : owner(sigma) = r}, n_total / N streams each when N divides n_total;
+  weak    a fixed number of streams per rank (C5: 1,024 streams on 8 GPUs = 128 per GPU): the same rule over
+          per_rank * N streams.
 After the timed loop the u64 counters are summed, the device time is max-reduced and the per-rank times are
 gathered (load imbalance) -- one small collective each (NCCL on the GPU box, gloo in the CPU tests).
 """
@@ -15,14 +19,20 @@ import torch
 import torch.distributed as dist
 
 
-def stream_ids(rank: int, world: int, per_rank: int) -> list[int]:
-    """Global stream ids owned by `rank` under weak scaling (`per_rank` streams on every rank)."""
-    return [rank + world * i for i in range(per_rank)]
+def owner(stream_id: int, world: int) -> int:
+    """Rank of a global stream id (snake order over blocks of `world` consecutive ids)."""
+    b, pos = divmod(stream_id, world)
+    return pos if b % 2 == 0 else world - 1 - pos
 
 
 def partition(rank: int, world: int, n_total: int) -> list[int]:
     """Global stream ids owned by `rank` under strong scaling (`n_total` streams split over `world` ranks)."""
-    return list(range(rank, n_total, world))
+    return [sid for sid in range(n_total) if owner(sid, world) == rank]
+
+
+def stream_ids(rank: int, world: int, per_rank: int) -> list[int]:
+    """Global stream ids owned by `rank` under weak scaling (`per_rank` streams on every rank)."""
+    return partition(rank, world, per_rank * world)
 
 
 def shard_ids(rank: int, world: int, streams: int, scaling: str) -> list[int]:
@@ -32,10 +42,6 @@ def shard_ids(rank: int, world: int, streams: int, scaling: str) -> list[int]:
     if scaling == "weak":
         return stream_ids(rank, world, streams)
     raise ValueError(f"scaling must be 'strong' or 'weak', got {scaling!r}")
-
-
-def owner(stream_id: int, world: int) -> int:
-    return stream_id % world
 
 
 def _multi() -> bool:

@@ -45,6 +45,12 @@ CONFIGS = {
                frames=None, scenes="mixed", kv=QWEN_KV, n_prompt=32, config_id=4),
     "C5": dict(name="C5-full-4k-traffic", src=(3840, 2160), streams=1024, window=64, stride=8, gop=16,
                frames=None, scenes=["traffic"], kv=QWEN_KV, n_prompt=32, config_id=5),
+    # NEXT-4: the similar-patch analysis of fig:mv_residual_analysis_cdf as a
+    # second workload -- H.264-shaped AVMotionVector exports -> MB grid -> scores -> per-frame similar-patch
+    # histograms over tau in {0.25, 0.5, 1, 2, 5} px; a step = one GOP (16 frames) of every stream
+    "CDF": dict(name="NEXT4-cdf-1080p", src=(1920, 1080), streams=64, window=16, stride=16, gop=16, frames=None,
+                scenes=["static", "low", "medium", "high"], kv=None, n_prompt=0, config_id=6,
+                taus=(0.25, 0.5, 1.0, 2.0, 5.0), n_bins=20),
 }
 
 
@@ -240,3 +246,66 @@ def random_bf16(shape, rng: np.random.Generator) -> np.ndarray:
 def random_frames(n: int, H: int, W: int, rng: np.random.Generator) -> list:
     """n model-input frames [3][H][W] (bf16 bits)."""
     return [random_bf16((3, H, W), rng) for _ in range(n)]
+
+
+# FFmpeg's public AVMotionVector layout (libavutil/motion_vector.h), 40 B: the decoder's motion-vector export that
+# codecsight_mv_rasterize ingests (NEXT-4).
+AV_MV_DTYPE = np.dtype([("source", "<i4"), ("w", "u1"), ("h", "u1"), ("src_x", "<i2"), ("src_y", "<i2"),
+                        ("dst_x", "<i2"), ("dst_y", "<i2"), ("pad0", "<u2"), ("flags", "<u8"), ("motion_x", "<i4"),
+                        ("motion_y", "<i4"), ("motion_scale", "<u2"), ("pad1", "u1", (6,))])
+assert AV_MV_DTYPE.itemsize == 40
+
+# H.264 inter partition modes of a 16x16 MB (partition w, h) and their frequencies in the generated streams:
+# 16x16 (skip and most inter MBs), 16x8, 8x16, 8x8 -- an 8x8 further split into 4x4 sub-partitions with p = 0.25
+_PART_MODES = ((16, 16), (16, 8), (8, 16), (8, 8))
+_PART_P = (0.55, 0.15, 0.15, 0.15)
+
+
+def avmv_records(mb: np.ndarray, rng: np.random.Generator, mb_size: int = 16) -> np.ndarray:
+    """AVMotionVector records of one P-frame, shaped like libavcodec's H.264 export, drawn from the frame's MB
+    records `mb` [rows][cols] (the scene truth): an INTRA MB exports nothing; a SKIP MB one 16x16 record with its
+    (predicted) vector; an INTER MB 1, 2, 4 or up to 16 partitions (16x16 / 16x8 / 8x16 / 8x8, 8x8 -> 4x4) whose
+    vectors are the MB's vector with +-1 qpel jitter on some partitions (p = 0.3).  motion_scale 4 (quarter pel),
+    source -1 (past reference), dst = the partition centre in px.  Records are in raster order of MBs."""
+    rows, cols = mb.shape
+    jj, ii = np.nonzero(mb["type"] != MB_INTRA)
+    mode = rng.choice(len(_PART_MODES), size=jj.size, p=_PART_P)
+    mode[mb["type"][jj, ii] == MB_SKIP] = 0
+    recs = []
+    for m, (pw, ph) in enumerate(_PART_MODES):
+        sel = mode == m
+        if not sel.any():
+            continue
+        j, i = jj[sel], ii[sel]
+        for oy in range(0, mb_size, ph):
+            for ox in range(0, mb_size, pw):
+                if (pw, ph) == (8, 8):   # 8x8: split into four 4x4 sub-partitions with p = 0.25
+                    split = rng.random(j.size) < 0.25
+                    parts = [(~split, ox, oy, 8, 8)] + [(split, ox + sx, oy + sy, 4, 4) for sy in (0, 4)
+                                                         for sx in (0, 4)]
+                else:
+                    parts = [(np.ones(j.size, bool), ox, oy, pw, ph)]
+                for msk, px, py, w, h in parts:
+                    if not msk.any():
+                        continue
+                    jm, im = j[msk], i[msk]
+                    a = np.zeros(jm.size, AV_MV_DTYPE)
+                    a["source"] = -1
+                    a["w"], a["h"] = w, h
+                    a["dst_x"] = im * mb_size + px + w // 2
+                    a["dst_y"] = jm * mb_size + py + h // 2
+                    a["src_x"], a["src_y"] = a["dst_x"], a["dst_y"]
+                    jit = (rng.random((jm.size, 2)) < 0.3) * rng.integers(-1, 2, size=(jm.size, 2))
+                    skip = mb["type"][jm, im] == MB_SKIP
+                    jit[skip] = 0
+                    a["motion_x"] = mb["mvx"][jm, im].astype(np.int32) + jit[:, 0]
+                    a["motion_y"] = mb["mvy"][jm, im].astype(np.int32) + jit[:, 1]
+                    a["motion_scale"] = 4
+                    a["src_x"] = (a["dst_x"] + a["motion_x"] // 4).astype(np.int16)
+                    a["src_y"] = (a["dst_y"] + a["motion_y"] // 4).astype(np.int16)
+                    recs.append((jm * cols + im, a))
+    if not recs:
+        return np.zeros(0, AV_MV_DTYPE)
+    key = np.concatenate([k for k, _ in recs])
+    out = np.concatenate([a for _, a in recs])
+    return out[np.argsort(key, kind="stable")]

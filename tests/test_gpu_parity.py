@@ -1401,3 +1401,45 @@ def test_similar_hist_gpu(abi, ref):
     exp = ref.similar_hist(sc.reshape(S * n, -1), types.reshape(-1), taus, 50)
     torch.cuda.synchronize()
     assert (hist_d.cpu().numpy().view(np.uint64) == exp).all()
+
+
+def test_cdf_workload_pipeline(abi, ref):
+    """NEXT-4 workload as bench.py --workload cdf runs it: H.264-shaped AVMotionVector exports (synth.avmv_records)
+    of whole GOPs -> mv_rasterize -> score_patches (scores out) -> similar_hist over 5 taus, against the oracle
+    driven the same way: MB grids, scores, masks and the histogram bit-exact."""
+    import bench_cdf
+    cfg = dict(synth.CONFIGS["CDF"], tau=0.25, alpha=0.0, group=2)
+    g = make_grid(*cfg["src"])
+    S, F = 3, cfg["window"]
+    gens = [synth.StreamGen(*cfg["src"], synth.scene_of(cfg, i), synth.stream_seed(cfg, i)) for i in range(S)]
+    recs, offs, types = bench_cdf.gen_step(cfg, gens, np.random.default_rng(1))
+    n = S * F
+    nmb = g["mb_rows"] * g["mb_cols"]
+    grid_d = torch.zeros(n * nmb, dtype=torch.int64, device=DEV)
+    abi.codecsight_mv_rasterize(g, n, torch.from_numpy(recs.view(np.uint8)).to(DEV), torch.from_numpy(offs).to(DEV),
+                                grid_d)
+    gop = torch.zeros(S, 33, dtype=torch.int32, device=DEV)
+    keep = torch.zeros(S, F, 32, dtype=torch.int32, device=DEV)
+    score = torch.zeros(n, 1024, dtype=torch.float32, device=DEV)
+    kept = torch.zeros(S, F, dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(16, dtype=torch.int64, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ty_d = torch.from_numpy(types).to(DEV)
+    abi.codecsight_score_patches(g, S, F, grid_d, ty_d, keep, F, gop, score, kept, cnt, st)
+    taus = np.array(cfg["taus"], np.float32)
+    hist = torch.zeros(len(taus), cfg["n_bins"], dtype=torch.int64, device=DEV)
+    abi.codecsight_similar_hist(score, ty_d, n, 1024, torch.from_numpy(taus).to(DEV), len(taus), cfg["n_bins"], hist)
+    grid_o = ref.mv_rasterize(g, recs, offs, n)
+    so = ref.score_patches(g, grid_o.reshape(S, F, g["mb_rows"], g["mb_cols"]), types, np.zeros((S, 33), np.uint32),
+                           want_score=True)
+    ho = ref.similar_hist(so["score"].reshape(n, -1), types.reshape(-1), taus, cfg["n_bins"])
+    torch.cuda.synchronize()
+    got = grid_d.cpu().numpy().view(MB_DTYPE).reshape(grid_o.shape)
+    p = types.reshape(-1) == synth.FRAME_P
+    for f in ("mvx", "mvy", "sad", "type"):
+        assert (got[p][f] == grid_o[p][f]).all(), f
+    assert (score.cpu().numpy().view(np.uint32)[p] == so["score"].reshape(n, -1).view(np.uint32)[p]).all()
+    assert (u32(keep).reshape(S, F, -1) == so["keep_mask"]).all()
+    assert (hist.cpu().numpy().astype(np.uint64) == ho).all()
+    assert int(st.item()) == so["status"] == 0
+    assert ho.sum() == len(taus) * p.sum()

@@ -68,7 +68,7 @@ def test_sharded_counters_equal_single_process(world, scaling):
     # per-rank vectors gathered in rank order (the bench's per-rank times / shard sizes)
     assert [r[0] for r in per] == [10.0 * r for r in range(world)]
     if scaling == "strong":
-        assert [int(r[1]) for r in per] == [len(range(r, N_STREAMS, world)) for r in range(world)]
+        assert [int(r[1]) for r in per] == [len(shard.partition(r, world, N_STREAMS)) for r in range(world)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -82,7 +82,8 @@ def test_sharded_counters_equal_single_process(world, scaling):
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 def test_bench_shards_partition_the_configs(world, n_total, per_rank):
     """C4 (strong: the same 256 streams at every N) and C5 (weak: 128 per GPU, 1,024 at N = 8): every global stream
-    id owned by exactly one rank, round-robin (sigma -> sigma mod N), equal shard sizes."""
+    id owned by exactly one rank, equal shard sizes, and C4's alternating static / high-motion streams split evenly
+    (each rank holds as many of one as of the other)."""
     if n_total is not None:
         shards = [shard.shard_ids(r, world, n_total, "strong") for r in range(world)]
         expect = n_total
@@ -96,6 +97,11 @@ def test_bench_shards_partition_the_configs(world, n_total, per_rank):
         assert all(shard.owner(i, world) == r for i in x)
     if n_total is None and world == 8:
         assert expect == 1024
+    if n_total is not None and world > 1:
+        cfg = synth.CONFIGS["C4"]
+        for x in shards:
+            kinds = [synth.scene_of(cfg, i) for i in x]
+            assert kinds.count("static") == kinds.count("high") == len(x) // 2
     with pytest.raises(ValueError):
         shard.shard_ids(0, world, 8, "bogus")
 
