@@ -821,6 +821,50 @@ void codecsight_ref_preprocess_frame(const ref_grid* g, const ref_pre* pp, const
         out[(c * MH + y) * MW + x] = ref_f32_to_bf16(codecsight_ref_model_pixel(g, pp, Y, UV, c, y, x));
 }
 
+/* Distinct 32-B source sectors (Y plane: row y, byte x; UV plane: row y/2, bytes 2(x/2), 2(x/2)+1 -- the same
+ * sector) touched by the four taps of every model pixel of every kept group, summed over the frames, x 32 B. */
+static unsigned long long ref_nv12_source_bytes(const ref_grid* g, const ref_pre* pp, const uint32_t* keep_mask,
+                                                int64_t mask_frame_stride, int32_t n_streams, int32_t n_frames) {
+  const int64_t MH = (int64_t)g->grid_h * g->patch, MW = (int64_t)g->grid_w * g->patch, G = g->group;
+  const int64_t gp = G * g->patch, nw = ref_words(g), sc = (pp->src_w + 31) / 32;
+  const int64_t yrows = pp->src_h, uvrows = (pp->src_h + 1) / 2;
+  uint8_t* ys = (uint8_t*)malloc((size_t)(yrows * sc));
+  uint8_t* uvs = (uint8_t*)malloc((size_t)(uvrows * sc));
+  unsigned long long total = 0;
+  if (!ys || !uvs) { free(ys); free(uvs); return 0; }
+  for (int64_t s = 0; s < n_streams; ++s)
+    for (int64_t j = 0; j < n_frames; ++j) {
+      const uint32_t* m = keep_mask + (s * mask_frame_stride + j) * nw;
+      memset(ys, 0, (size_t)(yrows * sc));
+      memset(uvs, 0, (size_t)(uvrows * sc));
+      for (int64_t gr = 0; gr < g->grid_h / G; ++gr)
+        for (int64_t gc = 0; gc < g->grid_w / G; ++gc) {
+          int any = 0;
+          for (int64_t dy = 0; dy < G; ++dy)
+            for (int64_t dx = 0; dx < G; ++dx) any |= ref_bit(m, (gr * G + dy) * g->grid_w + gc * G + dx);
+          if (!any) continue;
+          for (int64_t yo = gr * gp; yo < (gr + 1) * gp; ++yo)
+            for (int64_t xo = gc * gp; xo < (gc + 1) * gp; ++xo) {
+              int64_t y0, y1, x0, x1;
+              float ly, lx;
+              ref_axis(yo, pp->src_h, MH, &y0, &y1, &ly);
+              ref_axis(xo, pp->src_w, MW, &x0, &x1, &lx);
+              const int64_t yy[2] = {y0, y1}, xx[2] = {x0, x1};
+              for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 2; ++b) {
+                  ys[yy[a] * sc + xx[b] / 32] = 1;
+                  uvs[(yy[a] / 2) * sc + (2 * (xx[b] / 2)) / 32] = 1;
+                }
+            }
+        }
+      for (int64_t i = 0; i < yrows * sc; ++i) total += ys[i];
+      for (int64_t i = 0; i < uvrows * sc; ++i) total += uvs[i];
+    }
+  free(ys);
+  free(uvs);
+  return total * 32ull;
+}
+
 int codecsight_ref_compact_nv12(const ref_grid* g, const ref_pre* pp, int32_t n_streams, int32_t n_frames,
                                 const uint32_t* keep_mask, int64_t mask_frame_stride, const int32_t* frame_index,
                                 const void* const* y_planes, const void* const* uv_planes, int64_t capacity,
@@ -871,9 +915,13 @@ int codecsight_ref_compact_nv12(const ref_grid* g, const ref_pre* pp, int32_t n_
     }
   frame_offsets[n_slots] = (int32_t)off;
   counters[REF_C_PACKED_ROWS] += (unsigned long long)written;
-  /* algorithmic bytes: masks + offsets, and per written row its output (+16 B of ids); the source pixels a row
-     needs are counted by the caller (they depend on the scale) */
+  /* algorithmic bytes: masks + offsets, per written row its output (+16 B of ids), and the source the kept groups
+     read: per frame, every distinct 32-B sector of the Y and UV planes (offsets from the plane start) holding a
+     bilinear tap of a kept group's model pixel (reading NEXT-2 bytes; counted when both pitches are multiples of
+     32, so that a sector is (row, byte column / 32)) */
   counters[REF_C_BYTES_COMPACT] += (unsigned long long)(n_slots * (4 * nw + 4) + written * (row * 2 + 16));
+  if (pp->y_pitch % 32 == 0 && pp->uv_pitch % 32 == 0)
+    counters[REF_C_BYTES_COMPACT] += ref_nv12_source_bytes(g, pp, keep_mask, mask_frame_stride, n_streams, n_frames);
   return 0;
 }
 

@@ -230,6 +230,7 @@ int codecsight_compact_nv12(const cs_grid* g, const cs_preprocess* pp, int32_t n
   const long long n_slots = static_cast<long long>(n_streams) * n_frames;
   if (n_slots * g->grid_w * g->grid_h >= 2147483648LL) return CS_ERR_UNSUPPORTED;
   if (g->group * g->patch > 32) return CS_ERR_UNSUPPORTED;
+  if (g->grid_w / g->group > 64 || g->grid_h / g->group > 64) return CS_ERR_UNSUPPORTED;  // source-byte count masks
   if (!frame_offsets || !counters || !status) return CS_ERR_INVALID_ARGUMENT;
   if (n_slots > 0 && (!keep_mask || !frame_index || !y_planes || !uv_planes)) return CS_ERR_INVALID_ARGUMENT;
   if (capacity > 0 && (!packed || !pos_ids || !src_index)) return CS_ERR_INVALID_ARGUMENT;

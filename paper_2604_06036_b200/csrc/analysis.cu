@@ -66,6 +66,58 @@ __global__ void __launch_bounds__(kThreads) mv_rasterize(int mb, int cols, int r
   }
 }
 
+// The same arbitration with the frame's keys in shared memory (grids up to kSmemMbs MBs: 1080p's 8,160 MBs are 65 KB):
+// shared-memory atomics instead of L2 atomics, and the output written once, coalesced.
+constexpr int kSmemMbs = 12288;
+__global__ void __launch_bounds__(kThreads) mv_rasterize_smem(int mb, int cols, int rows,
+                                                               const cs_av_mv* __restrict__ mvs,
+                                                               const long long* __restrict__ offs, cs_mb* out) {
+  extern __shared__ unsigned long long s_key[];
+  const int f = blockIdx.x;
+  const int n_mb = rows * cols;
+  for (int e = threadIdx.x; e < n_mb; e += blockDim.x) s_key[e] = 0ull;
+  __syncthreads();
+  const long long r0 = offs[f], r1 = offs[f + 1];
+  for (long long r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const cs_av_mv m = mvs[r];
+    if (m.source >= 0) continue;
+    const int x0 = static_cast<int>(m.dst_x) - m.w / 2, y0 = static_cast<int>(m.dst_y) - m.h / 2;
+    const int x1 = x0 + m.w, y1 = y0 + m.h;  // [x0, x1) x [y0, y1)
+    if (x1 <= 0 || y1 <= 0) continue;
+    const int qx = qpel(m.motion_x, m.motion_scale), qy = qpel(m.motion_y, m.motion_scale);
+    const unsigned long long sq = static_cast<unsigned long long>(static_cast<long long>(qx) * qx +
+                                                                  static_cast<long long>(qy) * qy);
+    const unsigned long long k = ((sq + 1ull) << 32) | (0xffffffffull - static_cast<unsigned long long>(r - r0));
+    const int i_lo = max(0, (x0 >= 0 ? x0 : x0 - mb + 1) / mb), i_hi = min(cols - 1, (x1 - 1) / mb);
+    const int j_lo = max(0, (y0 >= 0 ? y0 : y0 - mb + 1) / mb), j_hi = min(rows - 1, (y1 - 1) / mb);
+    for (int j = j_lo; j <= j_hi; ++j)
+      for (int i = i_lo; i <= i_hi; ++i) {
+        const int ox = min(x1, mb * (i + 1)) - max(x0, mb * i);
+        const int oy = min(y1, mb * (j + 1)) - max(y0, mb * j);
+        if (ox > 0 && oy > 0) atomicMax(&s_key[j * cols + i], k);
+      }
+  }
+  __syncthreads();
+  cs_mb* o = out + static_cast<long long>(f) * n_mb;
+  for (int e = threadIdx.x; e < n_mb; e += blockDim.x) {
+    const unsigned long long k = s_key[e];
+    cs_mb v;
+    v.sad = 0;
+    v.reserved = 0;
+    if (k == 0ull) {
+      v.mvx_qpel = 0;
+      v.mvy_qpel = 0;
+      v.mb_type = CS_MB_INTRA;
+    } else {
+      const long long r = r0 + static_cast<long long>(0xffffffffull - (k & 0xffffffffull));
+      v.mvx_qpel = static_cast<int16_t>(qpel(mvs[r].motion_x, mvs[r].motion_scale));
+      v.mvy_qpel = static_cast<int16_t>(qpel(mvs[r].motion_y, mvs[r].motion_scale));
+      v.mb_type = CS_MB_INTER;
+    }
+    o[e] = v;
+  }
+}
+
 // One warp per (frame, threshold): ballot-count patches with score < tau, bin = count * n_bins / n_patches.
 __global__ void __launch_bounds__(kThreads) similar_hist(const float* __restrict__ score,
                                                           const uint8_t* __restrict__ frame_type, long long n_frames,
@@ -96,6 +148,14 @@ __global__ void __launch_bounds__(kThreads) similar_hist(const float* __restrict
 int cs_launch_mv_rasterize(const cs_grid* g, int32_t n_frames, const cs_av_mv* mvs, const int64_t* mv_offsets,
                            cs_mb* out, cudaStream_t stream) {
   if (n_frames == 0) return CS_OK;
+  const long long n_mb = static_cast<long long>(g->mb_rows) * g->mb_cols;
+  if (n_mb <= kSmemMbs) {
+    const size_t smem = static_cast<size_t>(n_mb) * 8;
+    if (cs_set_smem_attr(reinterpret_cast<const void*>(mv_rasterize_smem), 21, 8 * kSmemMbs)) return CS_ERR_CUDA;
+    mv_rasterize_smem<<<n_frames, kThreads, smem, stream>>>(g->mb_size, g->mb_cols, g->mb_rows, mvs,
+                                                            reinterpret_cast<const long long*>(mv_offsets), out);
+    return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+  }
   mv_rasterize<<<n_frames, kThreads, 0, stream>>>(g->mb_size, g->mb_cols, g->mb_rows, mvs,
                                                   reinterpret_cast<const long long*>(mv_offsets), out);
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;

@@ -16,6 +16,9 @@
 
 #include "cs_internal.cuh"
 
+#include <memory>
+#include <vector>
+
 namespace {
 
 constexpr int kScanThreads = 1024;
@@ -29,7 +32,7 @@ constexpr int kLayoutNV12 = 2;  // internal: frames are decoded NV12 planes, pre
 #ifndef CS_NV12_CTAS
 #define CS_NV12_CTAS 4
 #endif
-constexpr int kNvBatch = CS_NV12_BATCH;  // output pixels per lane in flight (fused NV12 fast path)
+constexpr int kNvRows = CS_NV12_BATCH;   // output rows per warp iteration, loads all in flight (fused NV12 fast path)
 constexpr int kNvCtas = CS_NV12_CTAS;    // resident CTAs per SM of the fused NV12 kernel (register budget)
 constexpr float kInv255 = 1.0f / 255.0f;  // RN(1/255)
 
@@ -69,6 +72,25 @@ struct CompactParams {
   int32_t* status;
 };
 
+// Source bytes of the fused NV12 preprocessing (algorithmic bytes, reading NEXT-2 bytes): per frame, the distinct
+// 32-B sectors of the Y and UV planes holding a bilinear tap of a kept group's model pixel.  With pitches that are
+// multiples of 32 a sector is (row, x / 32) in both planes (a chroma pair 2(x/2), 2(x/2)+1 shares luma x's sector).
+// The taps of model row o depend only on o, so every source row r is touched by a contiguous range of group rows
+// (its mask over gr), and every sector column by a range of group columns.  Rows with the same mask form a class
+// (at most 2 per group row); the frame's sector count is sum over (row class, column class) of rows x columns x
+// [some kept group lies in mask_r x mask_c].  The classes are geometry only (host, once per call).
+struct NvClass {
+  unsigned long long mask;  // group rows (row classes) / group columns (column classes)
+  int n;                    // source rows / sector columns in the class
+  int plane;                // row classes: 0 = Y, 1 = UV
+};
+constexpr int kNvMaxRowClasses = 256, kNvMaxColClasses = 128;
+struct NvSrcClasses {
+  int enabled, n_rows, n_cols;
+  NvClass rows[kNvMaxRowClasses];
+  NvClass cols[kNvMaxColClasses];
+};
+
 // mask of frame f of token unit `slot` (frame j*tp + f of its stream)
 __device__ __forceinline__ const uint32_t* slot_mask(const CompactParams& P, int slot, int f = 0) {
   const int s = slot / P.n_frames, j = slot - s * P.n_frames;
@@ -92,11 +114,37 @@ __device__ __forceinline__ void put_unit_word(const CompactParams& P, int slot, 
 // grids); the count goes to frame_offsets[slot] and is turned into the exclusive offset by compact_scan.  Also
 // writes the unit masks / types of temporal patches.
 constexpr int kCountThreads = 256;
-__global__ void __launch_bounds__(kCountThreads) compact_count(const __grid_constant__ CompactParams P) {
+__global__ void __launch_bounds__(kCountThreads) compact_count(const __grid_constant__ CompactParams P,
+                                                                const __grid_constant__ NvSrcClasses C) {
   __shared__ uint32_t s_m[kCountThreads / 32][128];  // per-warp unit mask (grid_words <= 128)
+  __shared__ unsigned long long s_k[kCountThreads / 32][64];  // NV12 source count: kept group columns per group row
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = blockIdx.x * (kCountThreads / 32) + warp;
   if (slot >= P.n_slots) return;
+  if (C.enabled) {
+    const uint32_t* m = slot_mask(P, slot);
+    const int ngr = P.grid_h / P.G;
+    for (int gr = lane; gr < ngr; gr += 32) {
+      unsigned long long k = 0ull;
+      for (int gc = 0; gc < P.ngc; ++gc)
+        if (cs::group_kept(m, gr * P.ngc + gc, P.ngc, P.G, P.grid_w)) k |= 1ull << gc;
+      s_k[warp][gr] = k;
+    }
+    __syncwarp();
+    unsigned long long sectors = 0ull;
+    for (int i = lane; i < C.n_rows; i += 32) {
+      const NvClass rc = C.rows[i];
+      unsigned long long K = 0ull;
+      for (unsigned long long b = rc.mask; b; b &= b - 1) K |= s_k[warp][__ffsll(static_cast<long long>(b)) - 1];
+      unsigned long long cols = 0ull;
+      for (int j = 0; j < C.n_cols; ++j)
+        if (K & C.cols[j].mask) cols += static_cast<unsigned long long>(C.cols[j].n);
+      sectors += cols * static_cast<unsigned long long>(rc.n);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sectors += __shfl_xor_sync(0xffffffffu, sectors, d);
+    if (lane == 0 && sectors) cs::atomic_add_u64(&P.counters[CS_CNT_BYTES_COMPACT], sectors * 32ull);
+  }
   const int gs2 = P.G * P.G;
   int c = 0;
   if (P.G == 2 && P.grid_w == 32 && P.nw <= 32) {
@@ -336,103 +384,122 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
     const uint8_t* Yp = reinterpret_cast<const uint8_t*>(frame);
     const uint8_t* UVp = static_cast<const uint8_t*>(P.uv_planes[slot]);
     const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
-    if (TP > 0 && TG == 2 && gp <= 32) {
-      // fast path (issue-bound: every instruction per pixel counts).  The source taps of output column xx / row yy
-      // are computed once per group by lane xx / yy and fetched with shuffles; the pixel's (yy, xx) advance by
-      // (32 / gp, 32 % gp) per round; the bf16 store is the hardware RNE conversion (the outputs are never NaN:
-      // std > 0 and mean is not NaN are checked on the host, so it equals the oracle's rounding bit for bit).
-      int ax0 = 0, ay0 = 0;
-      float alx = 0.0f, aly = 0.0f;
-      if (lane < gp) {
-        int i1;
-        nv12_axis(gc * gp + lane, P.src_w, P.scale_x, ax0, i1, alx);
-        nv12_axis(gr * gp + lane, P.src_h, P.scale_y, ay0, i1, aly);
-      }
-      int yy = lane / gp, xx = lane - (lane / gp) * gp;
-      // two output pixels per lane per iteration (rounds e0 and e0 + 32): their 16 loads are all in flight
-      // before either is converted (the kernel is latency-bound on these scattered byte loads)
-      const int npx = gp * gp;
-      for (int e0 = 0; e0 < npx; e0 += 32 * kNvBatch) {  // warp-uniform trip count (the shuffles need every lane)
-        uint32_t yv[kNvBatch][4], uvv[kNvBatch][4];
-        float lxv[kNvBatch], lyv[kNvBatch];
-        int pxx[kNvBatch], pyy[kNvBatch];
-        bool valid[kNvBatch];
+    if (TP > 0 && TG == 2 && gp <= 32 && gp % kNvRows == 0) {
+      // fast path (issue-bound: every instruction per pixel counts).  Lanes run along the group's output columns
+      // (lane xx < gp = 28; lanes 28..31 duplicate the last column and store nothing) and every iteration handles
+      // kNvRows output rows: a column's source taps, weights and chroma offsets are per-lane constants, a row's
+      // are warp-uniform (computed once per row by the whole warp), so a pixel costs no index arithmetic beyond
+      // its eight loads.  Bytes become floats exactly with the 2^23 trick: float(2^23 + b) - (2^23 + 16) = b - 16
+      // (one PRMT + one FADD instead of integer subtract + I2F); when both tap rows of an output row fall in the
+      // same chroma row (uniform), the two lower taps reuse the upper taps' chroma terms.  Same fp32 operations
+      // in the same order as the oracle; the bf16 store is the hardware RNE conversion (outputs are never NaN:
+      // std > 0 and mean not NaN are checked on the host).
+      const int xx = lane < gp ? lane : gp - 1;
+      int x0, x1;
+      float lx;
+      nv12_axis(gc * gp + xx, P.src_w, P.scale_x, x0, x1, lx);
+      const float hx = __fsub_rn(1.0f, lx);
+      const uint8_t* yc0 = Yp + x0;
+      const uint8_t* yc1 = Yp + x1;
+      const uint8_t* cc0 = UVp + 2 * (x0 >> 1);
+      const uint8_t* cc1 = UVp + 2 * (x1 >> 1);
+      const int dxp = xx >= p ? 1 : 0;
+      uint16_t* tcol = tile + dxp * 3 * pp + (xx - dxp * p);
+      const bool store = lane < gp;
+      constexpr float kBiasY = 8388624.0f, kBiasC = 8388736.0f;  // 2^23 + 16, 2^23 + 128
+      auto u8f = [](uint32_t v, uint32_t sel, float bias) {
+        return __fsub_rn(__uint_as_float(__byte_perm(v, 0x4B000000u, sel)), bias);
+      };
+      // per pair of output rows: its 16 loads are all issued before any is consumed (software-pipelining the next
+      // pair's loads, or prefetching a group's source band into L2, measured slower: DESIGN §6)
+      for (int yy0 = 0; yy0 < gp; yy0 += kNvRows) {
+        uint32_t yv[kNvRows][4], uvv[kNvRows][4];
+        float lyv[kNvRows];
+        bool cshare[kNvRows];
 #pragma unroll
-        for (int b = 0; b < kNvBatch; ++b) {
-          // lanes past the group's end fetch an in-group pixel (valid addresses) and do not emit it
-          valid[b] = e0 + 32 * b + lane < npx;
-          pxx[b] = valid[b] ? xx : 0;
-          pyy[b] = valid[b] ? yy : 0;
-          const int x0 = __shfl_sync(0xffffffffu, ax0, pxx[b]), y0 = __shfl_sync(0xffffffffu, ay0, pyy[b]);
-          lxv[b] = __shfl_sync(0xffffffffu, alx, pxx[b]);
-          lyv[b] = __shfl_sync(0xffffffffu, aly, pyy[b]);
-          const int x1 = x0 + (x0 < P.src_w - 1 ? 1 : 0), y1 = y0 + (y0 < P.src_h - 1 ? 1 : 0);
-          const uint8_t* r0 = Yp + (long long)y0 * P.y_pitch;
-          const uint8_t* r1 = Yp + (long long)y1 * P.y_pitch;
-          const uint8_t* c0 = UVp + (long long)(y0 >> 1) * P.uv_pitch;
-          const uint8_t* c1 = UVp + (long long)(y1 >> 1) * P.uv_pitch;
-          yv[b][0] = __ldg(r0 + x0);
-          yv[b][1] = __ldg(r0 + x1);
-          yv[b][2] = __ldg(r1 + x0);
-          yv[b][3] = __ldg(r1 + x1);
-          uvv[b][0] = __ldg(reinterpret_cast<const uint16_t*>(c0 + 2 * (x0 >> 1)));
-          uvv[b][1] = __ldg(reinterpret_cast<const uint16_t*>(c0 + 2 * (x1 >> 1)));
-          uvv[b][2] = __ldg(reinterpret_cast<const uint16_t*>(c1 + 2 * (x0 >> 1)));
-          uvv[b][3] = __ldg(reinterpret_cast<const uint16_t*>(c1 + 2 * (x1 >> 1)));
-          // (yy, xx) of this lane's next pixel (32 further in row-major order)
-          xx += 32 % gp;
-          yy += 32 / gp;
-          if (xx >= gp) {
-            xx -= gp;
-            ++yy;
+        for (int r = 0; r < kNvRows; ++r) {
+          int y0, y1;
+          nv12_axis(gr * gp + yy0 + r, P.src_h, P.scale_y, y0, y1, lyv[r]);
+          const long long o0 = (long long)y0 * P.y_pitch, o1 = (long long)y1 * P.y_pitch;
+          const long long c0 = (long long)(y0 >> 1) * P.uv_pitch, c1 = (long long)(y1 >> 1) * P.uv_pitch;
+          cshare[r] = (y0 >> 1) == (y1 >> 1);
+          yv[r][0] = __ldg(yc0 + o0);
+          yv[r][1] = __ldg(yc1 + o0);
+          yv[r][2] = __ldg(yc0 + o1);
+          yv[r][3] = __ldg(yc1 + o1);
+          uvv[r][0] = __ldg(reinterpret_cast<const uint16_t*>(cc0 + c0));
+          uvv[r][1] = __ldg(reinterpret_cast<const uint16_t*>(cc1 + c0));
+          if (!cshare[r]) {
+            uvv[r][2] = __ldg(reinterpret_cast<const uint16_t*>(cc0 + c1));
+            uvv[r][3] = __ldg(reinterpret_cast<const uint16_t*>(cc1 + c1));
+          } else {
+            uvv[r][2] = uvv[r][0];
+            uvv[r][3] = uvv[r][1];
           }
         }
+        // the two output rows of the iteration as the two halves of packed fp32 pairs (FADD2 / FMUL2 / FFMA2: one
+        // issue per pair, each half the same IEEE operation as the scalar oracle's); sums of products stay scalar
+        // per half (ptxas would fuse them into FFMA2, cs_internal.cuh)
+        static_assert(kNvRows == 2, "the packed fp32 path pairs two output rows");
+        const float2 kY2 = make_float2(kY, kY), kRV2 = make_float2(kRV, kRV), kGU2 = make_float2(kGU, kGU);
+        const float2 kGV2 = make_float2(kGV, kGV), kBU2 = make_float2(kBU, kBU);
+        const float2 bY = make_float2(kBiasY, kBiasY), bC = make_float2(kBiasC, kBiasC);
+        auto bytes2 = [](uint32_t v0, uint32_t v1, uint32_t sel) {
+          return make_float2(__uint_as_float(__byte_perm(v0, 0x4B000000u, sel)),
+                             __uint_as_float(__byte_perm(v1, 0x4B000000u, sel)));
+        };
+        float2 rgb[4][3];
 #pragma unroll
-        for (int b = 0; b < kNvBatch; ++b) {
-          if (!valid[b]) continue;
-          float rgb[4][3];
+        for (int q = 0; q < 4; ++q) {
+          const float2 d = cs::sub2(bytes2(uvv[0][q], uvv[1][q], 0x7540u), bC);
+          const float2 e = cs::sub2(bytes2(uvv[0][q], uvv[1][q], 0x7541u), bC);
+          const float2 yk = cs::mul2(kY2, cs::sub2(bytes2(yv[0][q], yv[1][q], 0x7540u), bY));
+          // sums of products: per-half scalar adds (cs::addp, never contracted), see cs_internal.cuh
+          rgb[q][0] = cs::clamp255_2(cs::addp(yk, cs::mul2(kRV2, e)));
+          rgb[q][1] = cs::clamp255_2(cs::subp(cs::subp(yk, cs::mul2(kGU2, d)), cs::mul2(kGV2, e)));
+          rgb[q][2] = cs::clamp255_2(cs::addp(yk, cs::mul2(kBU2, d)));
+        }
+        const float2 lx2 = make_float2(lx, lx), hx2 = make_float2(hx, hx);
+        const float2 ly2 = make_float2(lyv[0], lyv[1]);
+        const float2 hy2 = cs::sub2(make_float2(1.0f, 1.0f), ly2);
+        const float2 inv255 = make_float2(kInv255, kInv255), n255 = make_float2(255.0f, 255.0f);
+        float2 an[3];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float c = static_cast<float>(static_cast<int>(yv[b][q]) - 16);
-            const float d = static_cast<float>(static_cast<int>(uvv[b][q] & 0xffu) - 128);
-            const float ee = static_cast<float>(static_cast<int>(uvv[b][q] >> 8) - 128);
-            rgb[q][0] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kRV, ee)), 0.0f), 255.0f);
-            rgb[q][1] = fminf(fmaxf(__fsub_rn(__fsub_rn(__fmul_rn(kY, c), __fmul_rn(kGU, d)), __fmul_rn(kGV, ee)),
-                                    0.0f), 255.0f);
-            rgb[q][2] = fminf(fmaxf(__fadd_rn(__fmul_rn(kY, c), __fmul_rn(kBU, d)), 0.0f), 255.0f);
-          }
-          const float lx = lxv[b], ly = lyv[b];
-          const float hx = __fsub_rn(1.0f, lx), hy = __fsub_rn(1.0f, ly);
-          const int dy = pyy[b] >= p ? 1 : 0, y = pyy[b] - dy * p, dx = pxx[b] >= p ? 1 : 0, x = pxx[b] - dx * p;
-          uint16_t* tq = tile + (dy * G + dx) * 3 * pp + y * p + x;
-          float an[3];
+        for (int c = 0; c < 3; ++c) {
+          const float2 top = cs::addp(cs::mul2(hx2, rgb[0][c]), cs::mul2(lx2, rgb[1][c]));
+          const float2 bot = cs::addp(cs::mul2(hx2, rgb[2][c]), cs::mul2(lx2, rgb[3][c]));
+          const float2 v = cs::addp(cs::mul2(hy2, top), cs::mul2(ly2, bot));
+          // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
+          // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
+          const float2 q255 = cs::mul2(v, inv255);
+          const float2 res = cs::fma2(make_float2(-q255.x, -q255.y), n255, v);
+          const float2 t = cs::fma2(res, inv255, q255);
+          an[c] = cs::sub2(t, make_float2(P.mean[c], P.mean[c]));
+        }
+        // (t - mean) / std -> bf16 (norm_bf16), the six values' midpoint guards folded into one branch
+        float2 on[3];
+        uint32_t near_mid = 0u;
+        if (P.fast_div) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const float top = __fadd_rn(__fmul_rn(hx, rgb[0][c]), __fmul_rn(lx, rgb[1][c]));
-            const float bot = __fadd_rn(__fmul_rn(hx, rgb[2][c]), __fmul_rn(lx, rgb[3][c]));
-            const float v = __fadd_rn(__fmul_rn(hy, top), __fmul_rn(ly, bot));
-            // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
-            // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
-            const float q255 = __fmul_rn(v, kInv255);
-            const float t = __fmaf_rn(__fmaf_rn(-q255, 255.0f, v), kInv255, q255);
-            an[c] = __fsub_rn(t, P.mean[c]);
+            on[c] = cs::mul2(an[c], make_float2(P.rstd[c], P.rstd[c]));
+            near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].x) & 0xffffu) - 0x7ff8u <= 16u);
+            near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].y) & 0xffffu) - 0x7ff8u <= 16u);
           }
-          // (t - mean) / std -> bf16 (norm_bf16), the three channels' midpoint guards folded into one branch
-          float on[3];
-          uint32_t near_mid = 0u;
-          if (P.fast_div) {
+        }
+        if (!P.fast_div || near_mid) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              on[c] = __fmul_rn(an[c], P.rstd[c]);
-              near_mid |= static_cast<uint32_t>((__float_as_uint(on[c]) & 0xffffu) - 0x7ff8u <= 16u);
-            }
+          for (int c = 0; c < 3; ++c)
+            on[c] = make_float2(__fdiv_rn(an[c].x, P.stdv[c]), __fdiv_rn(an[c].y, P.stdv[c]));
+        }
+        if (store) {
+#pragma unroll
+          for (int r = 0; r < kNvRows; ++r) {
+            const int yy = yy0 + r, dyp = yy >= p ? 1 : 0;
+            uint16_t* tq = tcol + dyp * G * 3 * pp + (yy - dyp * p) * p;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) tq[c * pp] = cs::f32_to_bf16_cvt(r == 0 ? on[c].x : on[c].y);
           }
-          if (!P.fast_div || near_mid) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) on[c] = __fdiv_rn(an[c], P.stdv[c]);
-          }
-#pragma unroll
-          for (int c = 0; c < 3; ++c) tq[c * pp] = cs::f32_to_bf16_cvt(on[c]);
         }
       }
     } else {
@@ -792,6 +859,66 @@ __global__ void __launch_bounds__(kGatherThreads, 1) compact_gather_tma(const __
 
 }  // namespace
 
+// model coordinate o -> its two source taps along an axis (the device's nv12_axis, in the same fp32 operations)
+static void host_axis(int o, int src, float scale, int* i0, int* i1) {
+  volatile float t = static_cast<float>(o) + 0.5f;  // separate roundings, never contracted
+  t = t * scale;
+  t = t - 0.5f;
+  float f = t;
+  f = f < 0.0f ? 0.0f : f;
+  *i0 = static_cast<int>(f);
+  *i1 = *i0 + (*i0 < src - 1 ? 1 : 0);
+}
+
+// Row / column classes of the NV12 source-byte count (see NvSrcClasses); false = count only the outputs (pitches
+// that are not multiples of 32)
+static bool nv12_classes(const CompactParams& P, NvSrcClasses* C) {
+  if (P.y_pitch % 32 != 0 || P.uv_pitch % 32 != 0) return false;
+  const int gp = P.G * P.p, ncol = (P.src_w + 31) / 32;
+  std::vector<unsigned long long> ry(P.src_h, 0ull), ruv((P.src_h + 1) / 2, 0ull), cm(ncol, 0ull);
+  for (int o = 0; o < P.FH; ++o) {
+    int a, b;
+    host_axis(o, P.src_h, P.scale_y, &a, &b);
+    const unsigned long long bit = 1ull << (o / gp);
+    ry[a] |= bit;
+    ry[b] |= bit;
+    ruv[a / 2] |= bit;
+    ruv[b / 2] |= bit;
+  }
+  for (int o = 0; o < P.FW; ++o) {
+    int a, b;
+    host_axis(o, P.src_w, P.scale_x, &a, &b);
+    const unsigned long long bit = 1ull << (o / gp);
+    cm[a / 32] |= bit;
+    cm[b / 32] |= bit;
+  }
+  // classes: runs of equal masks (a row's group range is monotone in the row, so equal masks are contiguous;
+  // merging runs of the same mask anyway keeps the tables small)
+  auto add = [](NvClass* t, int* n, int cap, unsigned long long mask, int plane) -> bool {
+    if (!mask) return true;
+    for (int i = 0; i < *n; ++i)
+      if (t[i].mask == mask && t[i].plane == plane) {
+        ++t[i].n;
+        return true;
+      }
+    if (*n >= cap) return false;
+    t[*n].mask = mask;
+    t[*n].n = 1;
+    t[*n].plane = plane;
+    ++*n;
+    return true;
+  };
+  C->n_rows = C->n_cols = 0;
+  for (unsigned long long m : ry)
+    if (!add(C->rows, &C->n_rows, kNvMaxRowClasses, m, 0)) return false;
+  for (unsigned long long m : ruv)
+    if (!add(C->rows, &C->n_rows, kNvMaxRowClasses, m, 1)) return false;
+  for (unsigned long long m : cm)
+    if (!add(C->cols, &C->n_cols, kNvMaxColClasses, m, 0)) return false;
+  C->enabled = 1;
+  return true;
+}
+
 static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp, int32_t n_streams,
                           int32_t n_frames, const uint32_t* keep_mask, int64_t mask_frame_stride,
                           const int32_t* frame_index, const void* const* frames, const void* const* uv_planes,
@@ -852,8 +979,16 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
   P.counters = counters;
   P.status = status;
 
+  static NvSrcClasses none{};  // (zero: no source-byte count)
+  NvSrcClasses* cls = &none;
+  std::unique_ptr<NvSrcClasses> nvc;
+  if (pre) {
+    nvc.reset(new NvSrcClasses{});
+    if (nv12_classes(P, nvc.get())) cls = nvc.get();
+  }
   if (P.n_slots > 0) {
-    compact_count<<<(P.n_slots + kCountThreads / 32 - 1) / (kCountThreads / 32), kCountThreads, 0, stream>>>(P);
+    compact_count<<<(P.n_slots + kCountThreads / 32 - 1) / (kCountThreads / 32), kCountThreads, 0, stream>>>(P,
+                                                                                                          *cls);
     if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
   }
   compact_scan<<<1, kScanThreads, 0, stream>>>(P);

@@ -110,6 +110,47 @@ CS_DEV uint32_t f32_to_bf16_rne(float f) {
   return u >> 16;
 }
 
+// Blackwell packed fp32 pairs (FADD2 / FMUL2 / FFMA2: two IEEE round-to-nearest fp32 operations, one per half, in
+// one instruction issue -- each half is bit-identical to __fadd_rn / __fmul_rn / __fmaf_rn on it).
+// CAUTION (measured, ptxas 12.9): ptxas contracts mul.rn.f32x2 feeding add/sub.rn.f32x2 into FFMA2 -- even with
+// -fmad=false, and even through fma(x, 1, y) -- which changes the rounding.  So a sum or difference whose operand is
+// a packed product must use the scalar per-half forms addp / subp (scalar FADD is never fused with FMUL2).
+CS_DEV unsigned long long f2pk(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+CS_DEV float2 f2upk(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+CS_DEV float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+  return f2upk(r);
+}
+CS_DEV float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+  return f2upk(r);
+}
+CS_DEV float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+  return f2upk(r);
+}
+CS_DEV float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)), "l"(f2pk(c)));
+  return f2upk(r);
+}
+CS_DEV float2 addp(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+CS_DEV float2 subp(float2 a, float2 b) { return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y)); }
+CS_DEV float2 clamp255_2(float2 a) {
+  return make_float2(fminf(fmaxf(a.x, 0.0f), 255.0f), fminf(fmaxf(a.y, 0.0f), 255.0f));
+}
+
 // fp32 -> bf16 bits, round to nearest even, one cvt.rn.bf16.f32 (equal to f32_to_bf16_rne for every non-NaN f)
 CS_DEV uint16_t f32_to_bf16_cvt(float f) {
   uint16_t r;

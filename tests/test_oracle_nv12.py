@@ -84,3 +84,57 @@ def test_compact_nv12_equals_compact_of_preprocessed(ref):
     for key in ("packed", "pos_ids", "src_index", "frame_offsets"):
         assert (a[key] == b[key]).all(), key
     assert b["counters"][ref.C_PACKED_ROWS] == a["counters"][ref.C_PACKED_ROWS]
+
+
+def _group_mask(g, groups):
+    """Keep mask (one frame) with the given (gr, gc) groups set."""
+    bits = np.zeros(g["grid_w"] * g["grid_h"], np.uint8)
+    G = g["group"]
+    for gr, gc in groups:
+        for dy in range(G):
+            for dx in range(G):
+                bits[(gr * G + dy) * g["grid_w"] + gc * G + dx] = 1
+    return np.packbits(bits, bitorder="little").view(np.uint32)
+
+
+@pytest.mark.parametrize("src", [(64, 64), (128, 96)])
+def test_nv12_source_sector_bytes(ref, src):
+    """Algorithmic source bytes of the fused preprocessing (reading NEXT-2 bytes): the distinct 32-B sectors of the
+    Y and UV planes that the kept groups' bilinear taps touch.  Closed forms at a 64 x 64 model input (grid 8 x 8,
+    patch 8, 2 x 2 groups of 16 px):
+      identity scale (src 64 x 64): taps of model px o are o and o + 1 (clamped), so group (0, 0) reads luma rows
+        and columns 0..16 -> 17 rows x 1 sector + 9 UV rows x 1 sector = 26 sectors; every group -> all 64 rows x
+        2 sectors + 32 UV rows x 2 = 192 sectors;
+      src 128 x 96 (scale 2 x 1.5): group (0, 0) taps columns 2o, 2o + 1 for o < 16 -> 0..31 (sector 0) and rows
+        floor(1.5 o + 0.25), +1 -> rows 0..23: 24 rows + 12 UV rows = 36 sectors.
+    Pitches that are not multiples of 32 leave the source bytes uncounted."""
+    g = make_grid(*src, grid_w=8, grid_h=8, patch=8, group=2)
+    rng = np.random.default_rng(0)
+    Y, UV = _nv12(src[1], src[0], rng)
+    pre = ref.make_pre(*src)
+    out_only = 4 * 2 + 4
+    row = 3 * 8 * 8 * 2 + 16
+
+    def bytes_for(groups, pre_=pre):
+        km = _group_mask(g, groups)[None, None]
+        o = ref.compact_nv12(g, pre_, km, np.zeros(1, np.int32), [Y], [UV], 64, 1, 1)
+        return int(o["counters"][ref.C_BYTES_COMPACT]) - out_only - 4 * len(groups) * row
+
+    one = 26 if src == (64, 64) else 36
+    assert bytes_for([(0, 0)]) == one * 32
+    if src == (64, 64):
+        assert bytes_for([(r, c) for r in range(4) for c in range(4)]) == 192 * 32
+    # vertically adjacent groups share their boundary rows: the union, not the sum
+    if src == (64, 64):
+        assert bytes_for([(0, 0), (1, 0)]) == (33 + 17) * 32     # luma rows 0..32, UV rows 0..16, one sector each
+    else:                                                        # scale 1.5: group row 1 starts at luma row 24
+        assert bytes_for([(0, 0), (1, 0)]) == 2 * one * 32
+    # a pitch that is not a multiple of 32: outputs only
+    Yp = np.zeros((src[1], src[0] + 8), np.uint8)
+    Yp[:, :src[0]] = Y
+    UVp = np.zeros((src[1] // 2, src[0] + 8), np.uint8)
+    UVp[:, :src[0]] = UV
+    pre2 = ref.make_pre(*src, y_pitch=src[0] + 8, uv_pitch=src[0] + 8)
+    km = _group_mask(g, [(0, 0)])[None, None]
+    o = ref.compact_nv12(g, pre2, km, np.zeros(1, np.int32), [Yp], [UVp], 64, 1, 1)
+    assert int(o["counters"][ref.C_BYTES_COMPACT]) == out_only + 4 * row
