@@ -67,6 +67,12 @@ def parse():
     ap.add_argument("--fused", action=argparse.BooleanOptionalAction, default=True,
                     help="one codecsight_score_compact launch per step (NEXT-2, default) instead of score_patches + "
                          "compact (--no-fused)")
+    ap.add_argument("--pdl", action="store_true",
+                    help="prune-only workloads (C2): launch each step's fused score+compact as a programmatic dependent "
+                         "of the previous step's (CS_LAUNCH_PDL), so its scoring overlaps the previous compaction; the "
+                         "kernel time is then the timed region / K (no per-kernel events between the launches)")
+    ap.add_argument("--chain-depth", type=int, default=4,
+                    help="--pdl: output buffer sets the chained calls rotate (call g reuses call g - depth's)")
     ap.add_argument("--graphs", action="store_true",
                     help="replay steps k >= 1 as captured CUDA graphs (one per ring phase and slot parity)")
     ap.add_argument("--temporal-patch", type=int, default=1, choices=[1, 2],
@@ -447,9 +453,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         kvb = dict(kvb, rope_mode=1, mrope_section=(16, 24, 24), t_per_frame=1)
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
     pre = dict(src_w=sw, src_h=sh, y_pitch=sw, uv_pitch=sw) if args.frames == "nv12" else None
+    if args.pdl and (kvb is not None or not args.fused or args.overlap or args.graphs):
+        raise SystemExit("--pdl: prune-only workload (C2), fused score+compact, no --overlap / --graphs")
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
                     kv_mode=args.kv_mode, compact_chunk=s, preprocess=pre, overlap=args.overlap,
-                    temporal_patch=args.temporal_patch, fused=args.fused)
+                    temporal_patch=args.temporal_patch, fused=args.fused, pdl=args.pdl, chain_depth=args.chain_depth)
     tp = args.temporal_patch
     # --graphs: steps k >= 1 are CUDA graph replays, one graph per (ring phase, slot parity); the warm-up covers a
     # whole cycle of keys so that no capture happens inside a timed region
@@ -520,8 +528,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             st["fi"].copy_(fidx_dev[k], non_blocking=True)
             pipe.graph_step(k, st["mb"], ptrs, st["fi"], st["ty"])
             return
-        evs = pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k], timing=timed)
-        if timed:
+        evs = pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k], timing=timed and not args.pdl)
+        if timed and not args.pdl:
             for name in ("score", "compact", "kv"):
                 if name in evs:
                     ev[name].append(evs[name])
@@ -563,6 +571,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             run_step_eager(k)
         torch.cuda.synchronize()
     per = {kname: [a.elapsed_time(b) for a, b in lst] for kname, lst in ev.items()}
+    if args.pdl:  # back-to-back overlapping launches: the average launch duration is the timed region / K
+        per["score"] = [ms / args.steps] * args.steps
     status = int(pipe.status.item())
 
     # ---- compact alone on the last step's masks, both frame layouts (context for the layout choice) ---------
@@ -778,6 +788,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "kv": "Qwen2-VL-7B 28x4x128 bf16" if kvb else None, "n_prompt": cfg["n_prompt"],
                    "frame_layout": args.frame_layout, "kv_mode": args.kv_mode, "rope": args.rope,
                    "frames": args.frames, "overlap": args.overlap, "temporal_patch": tp, "fused": args.fused,
+                   "pdl": args.pdl, "chain_depth": args.chain_depth if args.pdl else None,
                    "graphs": args.graphs,
                    "parallelism": f"stream-shard x{world}",
                    "l2": "inputs larger than L2 (KV caches, frames and metadata of one step exceed the 126 MB L2; "

@@ -206,6 +206,40 @@ int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, co
  *   capacity / packed / pos_ids / src_index / frame_offsets over the n_streams x n_frames slots).
  * n_streams == 0 enqueues nothing (frame_offsets untouched).
  * --------------------------------------------------------------------------------------------------------- */
+/* codecsight_score_compact_ex — the same call with two launch options:
+ *   type_stride   row stride (frames) of frame_type, which may then be the step's own [n_streams][type_stride]
+ *                 input array instead of the mask ring's type slots (codecsight_score_compact: = frame_stride)
+ *   flags         CS_LAUNCH_PDL: a CHAINED call g (chain->generation = g = 0, 1, 2, ... on one chain of depth
+ *                 d = chain->depth, 2 <= d <= 8), launched as a programmatic dependent of the preceding kernel on
+ *                 `stream` (the preceding chained call g-1): its stream ticket, MB loads and scoring passes run
+ *                 while earlier calls are still compacting; it then waits until chain->gop_ready[s] == g (call g-1
+ *                 published stream s's final GOP state) and until chain->done[g mod d] >= g-d+1 (call g-d, whose
+ *                 output buffers it reuses, has completed), computes, and publishes gop_ready[s] = g+1 and, when
+ *                 its last CTA finishes, done[g mod d] = g+1 (release stores; the waits are acquire spins on calls
+ *                 that are already resident, so they cannot deadlock).  Successive chained calls therefore overlap
+ *                 each other's scoring and compaction.  Requirements: gop_ready [n_streams] and done [d] device
+ *                 u32, zero before call 0, the same n_streams on every call of a chain; call g's workspace differs
+ *                 from calls g-1 .. g-d's (rotate d + 1); call g writes the outputs kept_count, packed, pos_ids,
+ *                 src_index and frame_offsets that call g-d wrote (rotate d sets); mb, frame_type and frames are
+ *                 not written by the preceding kernels; score must be NULL (else CS_ERR_UNSUPPORTED).  Results are
+ *                 identical to plain calls.  (Other flag bits, or CS_LAUNCH_PDL without a valid chain:
+ *                 CS_ERR_INVALID_ARGUMENT.)
+ */
+enum { CS_LAUNCH_PDL = 1 };
+typedef struct {
+  uint32_t* gop_ready;  /* device [n_streams]  */
+  uint32_t* done;       /* device [depth]      */
+  uint32_t generation;  /* this call's index g */
+  uint32_t depth;       /* output buffer sets  */
+} cs_chain;
+int codecsight_score_compact_ex(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                                const uint8_t* frame_type, int64_t type_stride, uint32_t* keep_mask,
+                                int64_t frame_stride, uint32_t* gop_state, float* score, int32_t* kept_count,
+                                const int32_t* frame_index, const void* const* frames, int32_t frame_layout,
+                                int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                                int32_t* frame_offsets, void* workspace, size_t workspace_bytes,
+                                unsigned long long* counters, int32_t* status, uint32_t flags,
+                                const cs_chain* chain, cudaStream_t stream);
 size_t codecsight_score_compact_workspace_size(int32_t n_streams);
 int codecsight_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
                              const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,

@@ -21,6 +21,7 @@ CS_OK, CS_ERR_INVALID_ARGUMENT, CS_ERR_SHAPE, CS_ERR_UNSUPPORTED, CS_ERR_CUDA = 
 CS_STATUS_CAPACITY, CS_STATUS_NO_IFRAME, CS_STATUS_ORIGIN, CS_STATUS_BAD_FRAME_TYPE, CS_STATUS_BAD_MB_TYPE = \
     1, 2, 4, 8, 16
 CS_STATUS_MISALIGNED = 32
+CS_LAUNCH_PDL = 1
 CS_FRAME_I, CS_FRAME_P = 0, 1
 CS_MB_INTER, CS_MB_SKIP, CS_MB_INTRA = 0, 1, 2
 CS_DISP_NEW, CS_DISP_ANCHOR, CS_DISP_REUSE = 0, 1, 2
@@ -92,6 +93,10 @@ def lib():
         L.codecsight_score_compact.restype = C.c_int
         L.codecsight_score_compact.argtypes = [C.POINTER(CsGrid), I32, I32, P, P, P, I64, P, P, P, P, P, I32, I64, P,
                                                P, P, P, P, C.c_size_t, P, P, P]
+        L.codecsight_score_compact_ex.restype = C.c_int
+        L.codecsight_score_compact_ex.argtypes = [C.POINTER(CsGrid), I32, I32, P, P, I64, P, I64, P, P, P, P, P, I32,
+                                                  I64, P, P, P, P, P, C.c_size_t, P, P, C.c_uint32,
+                                                  C.POINTER(CsChain), P]
         L.codecsight_compact_tp.restype = C.c_int
         L.codecsight_compact_tp.argtypes = [C.POINTER(CsGrid), I32, I32, I32, P, I64, P, P, I32, I64, P, P, P, P, P,
                                             I64, P, P, P, P, P]
@@ -122,6 +127,10 @@ def declared_symbols() -> list[str]:
     with open(HEADER) as f:
         txt = f.read()
     return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(codecsight_\w+)\s*\(", txt, re.M)))
+
+
+class CsChain(C.Structure):
+    _fields_ = [("gop_ready", C.c_void_p), ("done", C.c_void_p), ("generation", C.c_uint32), ("depth", C.c_uint32)]
 
 
 def make_grid(g: dict) -> CsGrid:
@@ -215,28 +224,55 @@ def codecsight_score_compact(g: dict, n_streams: int, n_frames: int, mb, frame_t
     _check(rc, "codecsight_score_compact")
 
 
+def codecsight_score_compact_ex(g: dict, n_streams: int, n_frames: int, mb, frame_type, type_stride: int, keep_mask,
+                                frame_stride: int, gop_state, score, kept_count, frame_index, frames, capacity: int,
+                                packed, pos_ids, src_index, frame_offsets, workspace, counters, status,
+                                flags: int = 0, chain=None, frame_layout: int = CS_LAYOUT_PLANAR, stream=None) -> None:
+    """chain = (gop_ready tensor [S] int32, done tensor [depth] int32, generation) with flags = CS_LAUNCH_PDL."""
+    ch = None if chain is None else C.byref(CsChain(_ptr(chain[0]), _ptr(chain[1]), chain[2], chain[1].numel()))
+    rc = lib().codecsight_score_compact_ex(C.byref(make_grid(g)), n_streams, n_frames, _ptr(mb), _ptr(frame_type),
+                                           type_stride, _ptr(keep_mask), frame_stride, _ptr(gop_state), _ptr(score),
+                                           _ptr(kept_count), _ptr(frame_index), _ptr(frames), frame_layout, capacity,
+                                           _ptr(packed), _ptr(pos_ids), _ptr(src_index), _ptr(frame_offsets),
+                                           _ptr(workspace), workspace.numel() * workspace.element_size(),
+                                           _ptr(counters), _ptr(status), flags, ch, _stream(stream))
+    _check(rc, "codecsight_score_compact_ex")
+
+
 class BoundScoreCompact:
-    """codecsight_score_compact with every argument but the per-step inputs (mb, frame_index, frames, stream)
-    marshalled once: the Pipeline's per-step host cost is then one ctypes call (same C entry point, same checks)."""
+    """codecsight_score_compact_ex with every argument but the per-step inputs (mb, frame_index, frames, stream and,
+    with types_per_call, frame_type) marshalled once: the Pipeline's per-step host cost is then one ctypes call (same
+    C entry point, same checks).  flags = CS_LAUNCH_PDL: programmatic dependent launch."""
 
     def __init__(self, g: dict, n_streams: int, n_frames: int, frame_type, keep_mask, frame_stride: int, gop_state,
                  score, kept_count, capacity: int, packed, pos_ids, src_index, frame_offsets, workspace, counters,
-                 status, frame_layout: int = CS_LAYOUT_PLANAR):
+                 status, frame_layout: int = CS_LAYOUT_PLANAR, flags: int = 0, type_stride: int | None = None,
+                 chain=None):
         self._grid = make_grid(g)  # kept alive: passed by reference on every call
-        self._fn = lib().codecsight_score_compact
+        self._fn = lib().codecsight_score_compact_ex
         self._head = (C.byref(self._grid), n_streams, n_frames)
-        self._mid = (_ptr(frame_type), _ptr(keep_mask), frame_stride, _ptr(gop_state), _ptr(score),
-                     _ptr(kept_count))
+        self._types_per_call = frame_type is None
+        self._ty = None if frame_type is None else _ptr(frame_type)
+        self._ts = frame_stride if type_stride is None else type_stride
+        self._mid = (_ptr(keep_mask), frame_stride, _ptr(gop_state), _ptr(score), _ptr(kept_count))
         self._tail = (frame_layout, capacity, _ptr(packed), _ptr(pos_ids), _ptr(src_index), _ptr(frame_offsets),
-                      _ptr(workspace), workspace.numel() * workspace.element_size(), _ptr(counters), _ptr(status))
+                      _ptr(workspace), workspace.numel() * workspace.element_size(), _ptr(counters), _ptr(status),
+                      flags)
+        # chained calls (CS_LAUNCH_PDL): (gop_ready, done) tensors; the generation is given per call
+        self._chain = None if chain is None else CsChain(_ptr(chain[0]), _ptr(chain[1]), 0, chain[1].numel())
 
-    def __call__(self, mb, frame_index, frames, stream: int) -> None:
+    def __call__(self, mb, frame_index, frames, stream: int, frame_type=None, generation: int = 0) -> None:
         if not (mb.is_cuda and frame_index.is_cuda and frames.is_cuda):
             raise CodecSightError("expected CUDA tensors")
-        rc = self._fn(*self._head, mb.data_ptr(), *self._mid, frame_index.data_ptr(), frames.data_ptr(), *self._tail,
-                      stream)
+        ty = frame_type.data_ptr() if self._types_per_call else self._ty
+        ch = None
+        if self._chain is not None:
+            self._chain.generation = generation & 0xFFFFFFFF
+            ch = C.byref(self._chain)
+        rc = self._fn(*self._head, mb.data_ptr(), ty, self._ts, *self._mid, frame_index.data_ptr(), frames.data_ptr(),
+                      *self._tail, ch, stream)
         if rc != CS_OK:
-            _check(rc, "codecsight_score_compact")
+            _check(rc, "codecsight_score_compact_ex")
 
 
 def codecsight_compact_tp(g: dict, temporal_patch: int, n_streams: int, n_units: int, keep_mask,

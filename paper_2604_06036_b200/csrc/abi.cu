@@ -101,17 +101,24 @@ int codecsight_score_patches(const cs_grid* g, int32_t n_streams, int32_t n_fram
 
 size_t codecsight_score_compact_workspace_size(int32_t n_streams) { return cs_score_compact_workspace_bytes(n_streams); }
 
-int codecsight_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
-                             const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
-                             uint32_t* gop_state, float* score, int32_t* kept_count, const int32_t* frame_index,
-                             const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
-                             int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, void* workspace,
-                             size_t workspace_bytes, unsigned long long* counters, int32_t* status,
-                             cudaStream_t stream) {
+int codecsight_score_compact_ex(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                                const uint8_t* frame_type, int64_t type_stride, uint32_t* keep_mask,
+                                int64_t frame_stride, uint32_t* gop_state, float* score, int32_t* kept_count,
+                                const int32_t* frame_index, const void* const* frames, int32_t frame_layout,
+                                int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                                int32_t* frame_offsets, void* workspace, size_t workspace_bytes,
+                                unsigned long long* counters, int32_t* status, uint32_t flags, const cs_chain* chain,
+                                cudaStream_t stream) {
   int rc = grid_ok(g);
   if (rc) return rc;
-  if (n_streams < 0 || n_frames < 1 || n_frames > cs::kMaxFramesPerCall || frame_stride < n_frames || capacity < 0)
+  if (n_streams < 0 || n_frames < 1 || n_frames > cs::kMaxFramesPerCall || frame_stride < n_frames ||
+      type_stride < n_frames || capacity < 0)
     return CS_ERR_INVALID_ARGUMENT;
+  if ((flags & ~static_cast<uint32_t>(CS_LAUNCH_PDL)) != 0) return CS_ERR_INVALID_ARGUMENT;
+  const bool pdl = (flags & CS_LAUNCH_PDL) != 0;
+  if (pdl && (!chain || !chain->gop_ready || !chain->done || chain->depth < 2 || chain->depth > 8))
+    return CS_ERR_INVALID_ARGUMENT;
+  if (pdl && score) return CS_ERR_UNSUPPORTED;  // chained calls: no score output (it would race call g-2's)
   if (n_streams == 0) return CS_OK;
   if (!mb || !frame_type || !keep_mask || !gop_state || !kept_count || !counters || !status) return CS_ERR_INVALID_ARGUMENT;
   if (!frame_index || !frames || !frame_offsets || !workspace) return CS_ERR_INVALID_ARGUMENT;
@@ -125,9 +132,23 @@ int codecsight_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_fram
   if (n_slots * g->grid_w * g->grid_h >= 2147483648LL) return CS_ERR_UNSUPPORTED;
   if (g->group * g->patch > 32) return CS_ERR_UNSUPPORTED;
   if ((rc = device_ok())) return rc;
-  return cs_launch_score_compact(g, n_streams, n_frames, mb, frame_type, keep_mask, frame_stride, gop_state, score,
-                                 kept_count, frame_index, frames, frame_layout, capacity, packed, pos_ids, src_index,
-                                 frame_offsets, workspace, counters, status, stream);
+  return cs_launch_score_compact(g, n_streams, n_frames, mb, frame_type, type_stride, keep_mask, frame_stride,
+                                 gop_state, score, kept_count, frame_index, frames, frame_layout, capacity, packed,
+                                 pos_ids, src_index, frame_offsets, workspace, counters, status,
+                                 pdl ? chain : nullptr, stream);
+}
+
+int codecsight_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
+                             const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
+                             uint32_t* gop_state, float* score, int32_t* kept_count, const int32_t* frame_index,
+                             const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
+                             int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, void* workspace,
+                             size_t workspace_bytes, unsigned long long* counters, int32_t* status,
+                             cudaStream_t stream) {
+  return codecsight_score_compact_ex(g, n_streams, n_frames, mb, frame_type, frame_stride, keep_mask, frame_stride,
+                                     gop_state, score, kept_count, frame_index, frames, frame_layout, capacity,
+                                     packed, pos_ids, src_index, frame_offsets, workspace, workspace_bytes, counters,
+                                     status, 0u, nullptr, stream);
 }
 
 int codecsight_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const uint32_t* keep_mask,

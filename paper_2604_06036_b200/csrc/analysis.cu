@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(kThreads) mv_rasterize(int mb, int cols, int r
 // The same arbitration with the frame's keys in shared memory (grids up to kSmemMbs MBs: 1080p's 8,160 MBs are 65 KB):
 // shared-memory atomics instead of L2 atomics, and the output written once, coalesced.
 constexpr int kSmemMbs = 12288;
-__global__ void __launch_bounds__(kThreads) mv_rasterize_smem(int mb, int cols, int rows,
+constexpr int kRastThreads = 1024;  // the per-thread record loop and the winner decode are latency chains: wide CTAs
+__global__ void __launch_bounds__(kRastThreads) mv_rasterize_smem(int mb, int cols, int rows,
                                                                const cs_av_mv* __restrict__ mvs,
                                                                const long long* __restrict__ offs, cs_mb* out) {
   extern __shared__ unsigned long long s_key[];
@@ -152,7 +153,7 @@ int cs_launch_mv_rasterize(const cs_grid* g, int32_t n_frames, const cs_av_mv* m
   if (n_mb <= kSmemMbs) {
     const size_t smem = static_cast<size_t>(n_mb) * 8;
     if (cs_set_smem_attr(reinterpret_cast<const void*>(mv_rasterize_smem), 21, 8 * kSmemMbs)) return CS_ERR_CUDA;
-    mv_rasterize_smem<<<n_frames, kThreads, smem, stream>>>(g->mb_size, g->mb_cols, g->mb_rows, mvs,
+    mv_rasterize_smem<<<n_frames, kRastThreads, smem, stream>>>(g->mb_size, g->mb_cols, g->mb_rows, mvs,
                                                             reinterpret_cast<const long long*>(mv_offsets), out);
     return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
   }

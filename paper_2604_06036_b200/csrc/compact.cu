@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "cs_internal.cuh"
+#include "group_ring.cuh"
 
 #include <memory>
 #include <vector>
@@ -715,146 +716,31 @@ __global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED &
 // misaligned frame) are copied by the warp with ordinary loads/stores in the same order.
 constexpr int kTmaWarps = kWarpsPerCta;
 constexpr int kTmaMaxStages = 8;
-constexpr unsigned kTmaGroupBytes = 4704u;  // 4 patches x 3 x 14 x 14 bf16
-constexpr unsigned kTmaStageAlloc = 4736u;  // rounded up to 128 B
-
-struct TmaGroup {
-  long long n0;     // first packed row
-  int slot;         // frame slot
-  int gi;           // group index gr * ngc + gc
-  int t_index;      // pos id t
-  int kind;         // 0 bulk, 1 direct (warp copy), -1 end of work
-  const uint16_t* src;
-};
+constexpr unsigned kTmaStageAlloc = cs::kRingStageAlloc;
 
 __global__ void __launch_bounds__(kGatherThreads, 1) compact_gather_tma(const __grid_constant__ CompactParams P,
                                                                         int nst) {
   extern __shared__ __align__(128) unsigned char t_smem[];
-  __shared__ TmaGroup s_desc[kTmaWarps][kTmaMaxStages];
+  __shared__ cs::RingGroup s_desc[kTmaWarps][kTmaMaxStages];
   __shared__ __align__(8) uint64_t s_full[kTmaWarps][kTmaMaxStages];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  unsigned char* stages = t_smem + (size_t)wib * nst * kTmaStageAlloc;
-  uint64_t* full = s_full[wib];
-  TmaGroup* desc = s_desc[wib];
   const long long total_groups = static_cast<long long>(__ldg(P.frame_offsets + P.n_slots)) / 4;
   const long long nwarps = static_cast<long long>(gridDim.x) * kTmaWarps;
   const long long wid = static_cast<long long>(blockIdx.x) * kTmaWarps + wib;
-  long long q = total_groups * wid / nwarps;
-  const long long q1 = total_groups * (wid + 1) / nwarps;
-  if (q >= q1) return;  // the warp's range is empty (no block-wide synchronisation below)
-  constexpr int kNgr = 16;  // group rows of a 32 x 32 patch grid
-  const long long row_el = 3ll * 14 * 14;
-
-  // ---- generator state (lane 0): current slot, group row, remaining kept-group bits of that row -------------
-  int slot = 0, gr = 0, t_index = 0;
-  uint32_t ybits = 0u;
-  const uint16_t* frame = nullptr;
-  bool aligned = false;
-  auto load_row = [&]() {
-    const uint32_t* m = slot_mask(P, slot);
-    const uint32_t x = __ldg(m + 2 * gr) | __ldg(m + 2 * gr + 1);
-    ybits = (x | (x >> 1)) & 0x55555555u;  // bit 2*gc set iff group (gr, gc) is kept
-  };
-  auto load_slot = [&]() {
-    frame = static_cast<const uint16_t*>(P.frames[slot]);
-    t_index = __ldg(P.frame_index + slot);
-    aligned = (reinterpret_cast<uintptr_t>(frame) & 15u) == 0;
-  };
-  bool more = true;
-  if (lane == 0) {
-    int lo = 0, hi = P.n_slots;  // largest slot with frame_offsets[slot] <= q * 4
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (static_cast<long long>(__ldg(P.frame_offsets + mid)) <= q * 4) lo = mid; else hi = mid;
-    }
-    slot = lo;
-    long long skip = q - __ldg(P.frame_offsets + slot) / 4;
-    load_slot();
-    load_row();
-    while (skip >= __popc(ybits)) {
-      skip -= __popc(ybits);
-      ++gr;  // stays inside the slot: the slot holds more than `skip` kept groups
-      load_row();
-    }
-    for (; skip > 0; --skip) ybits &= ybits - 1u;
-    for (int st = 0; st < nst; ++st) cs::mbar_init(&full[st], 1);
-    cs::fence_mbar_init();
-  }
-  __syncwarp();
-
-  auto issue = [&](int st) {  // lane 0: next kept group of the range into stage st
-    TmaGroup d;
-    if (q >= q1) {
-      d.kind = -1;
-      desc[st] = d;
-      cs::mbar_arrive(&full[st]);
-      more = false;
-      return;
-    }
-    while (ybits == 0u) {
-      if (++gr == kNgr) {
-        gr = 0;
-        ++slot;
-        load_slot();
-      }
-      load_row();
-    }
-    const int b = __ffs(ybits) - 1;
-    ybits &= ybits - 1u;
-    d.n0 = q * 4;
-    d.slot = slot;
-    d.gi = gr * 16 + (b >> 1);
-    d.t_index = t_index;
-    d.src = frame + (long long)d.gi * 4 * row_el;
-    ++q;
-    if (d.n0 + 4 <= P.capacity && aligned) {
-      d.kind = 0;
-      desc[st] = d;
-      cs::mbar_arrive_expect_tx(&full[st], kTmaGroupBytes);
-      cs::bulk_g2s(stages + (size_t)st * kTmaStageAlloc, d.src, kTmaGroupBytes, &full[st]);
-    } else {
-      d.kind = d.n0 < P.capacity ? 1 : 2;  // 2: entirely beyond the capacity, nothing to write
-      desc[st] = d;
-      cs::mbar_arrive(&full[st]);
-    }
-  };
-  if (lane == 0)
-    for (int st = 0; st < nst && more; ++st) issue(st);
-
-  for (int it = 0;; ++it) {
-    const int st = it % nst;
-    cs::mbar_wait(&full[st], (it / nst) & 1);
-    const TmaGroup d = desc[st];
-    if (d.kind < 0) break;
-    long long nvalid = P.capacity - d.n0;
-    nvalid = nvalid < 0 ? 0 : (nvalid > 4 ? 4 : nvalid);
-    if (d.kind == 0) {
-      if (lane == 0) cs::bulk_s2g(P.packed + d.n0 * row_el, stages + (size_t)st * kTmaStageAlloc, kTmaGroupBytes);
-    } else if (d.kind == 1) {
-      uint16_t* dst = P.packed + d.n0 * row_el;
-      const int nel = static_cast<int>(nvalid * row_el);
-      for (int e = lane; e < nel; e += 32) dst[e] = d.src[e];
-    }
-    if (lane < nvalid) {
-      const int gr_ = d.gi >> 4, gc_ = d.gi & 15;
-      const int h = gr_ * 2 + (lane >> 1), w = gc_ * 2 + (lane & 1);
-      const long long n = d.n0 + lane;
-      P.pos_ids[3 * n + 0] = d.t_index;
-      P.pos_ids[3 * n + 1] = h;
-      P.pos_ids[3 * n + 2] = w;
-      P.src_index[n] = d.slot * P.np + h * 32 + w;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      cs::bulk_commit();  // one (possibly empty) bulk group per consumed stage keeps the group count aligned
-      if (it >= 1 && more) {
-        cs::bulk_wait_read<1>();  // the store of item it-1 has read its stage
-        issue((it - 1) % nst);
-      }
-    }
-    __syncwarp();
-  }
-  if (lane == 0) cs::bulk_wait_all<0>();
+  cs::RingBatch B;
+  B.frame_offsets = P.frame_offsets;
+  B.n_slots = P.n_slots;
+  B.n_frames = P.n_frames;
+  B.keep_mask = P.keep_mask;
+  B.mask_frame_stride = P.mask_frame_stride;
+  B.frames = P.frames;
+  B.frame_index = P.frame_index;
+  B.capacity = P.capacity;
+  B.packed = P.packed;
+  B.pos_ids = P.pos_ids;
+  B.src_index = P.src_index;
+  cs::group_ring(B, total_groups * wid / nwarps, total_groups * (wid + 1) / nwarps,
+                 t_smem + (size_t)wib * nst * kTmaStageAlloc, nst, s_full[wib], s_desc[wib], lane);
 }
 
 }  // namespace

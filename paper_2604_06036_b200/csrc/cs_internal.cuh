@@ -232,11 +232,12 @@ int cs_launch_similar_hist(const float* score, const uint8_t* frame_type, int64_
                            cudaStream_t stream);
 size_t cs_score_compact_workspace_bytes(int32_t n_streams);
 int cs_launch_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
-                            const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
-                            uint32_t* gop_state, float* score, int32_t* kept_count, const int32_t* frame_index,
-                            const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
-                            int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, void* workspace,
-                            unsigned long long* counters, int32_t* status, cudaStream_t stream);
+                            const uint8_t* frame_type, int64_t type_stride, uint32_t* keep_mask,
+                            int64_t frame_stride, uint32_t* gop_state, float* score, int32_t* kept_count,
+                            const int32_t* frame_index, const void* const* frames, int32_t frame_layout,
+                            int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                            int32_t* frame_offsets, void* workspace, unsigned long long* counters, int32_t* status,
+                            const cs_chain* chain, cudaStream_t stream);
 int cs_num_sms();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel slot, device); 0 on success
 int cs_set_smem_attr(const void* func, int slot, int bytes);

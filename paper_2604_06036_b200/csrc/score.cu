@@ -18,6 +18,7 @@
 #include <math_constants.h>
 
 #include "cs_internal.cuh"
+#include "group_ring.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -36,6 +37,13 @@ struct ScoreParams {
   double denom;  // mb^2 * 255 * src_w * src_h (exact)
   int n_streams, n_frames, fpc, cluster;
   long long frame_stride;
+  long long type_stride;  // row stride of frame_type (frame_stride unless the types come from their own array)
+  int pdl;                // chained call launched as a programmatic dependent of the preceding one (see below)
+  unsigned* gop_ready;    // chain: [n_streams] generation of each stream's GOP state
+  unsigned* chain_done;   // chain: [depth] per g mod depth, generation + 1 of the last completed call of that class
+  unsigned chain_depth;   // chain: output buffer sets the calls rotate (call g writes what call g - depth wrote)
+  unsigned generation;    // chain: this call's index g
+  int phase_slot;         // CS_PHASE_TIMING builds only
   int use_bulk, chunk_rows, n_chunks, nstage;
   unsigned row_bytes, chunk_alloc;
   int want_score;
@@ -62,7 +70,8 @@ struct ScoreParams {
   int32_t* pos_ids;
   int32_t* src_index;
   int32_t* frame_offsets;
-  unsigned* ws_ctr;              // [0] ticket, [1] CTAs done
+  unsigned* ws_ctr;              // [0] ticket, [1] CTAs done, [2] CTAs whose frame offsets are published
+  int global_compact;            // every cluster co-resident: compaction balanced over the whole grid (see below)
   unsigned long long* ws_flags;  // [n_streams] look-back words: (state << 62) | rows, state 1 = aggregate, 2 = prefix
   unsigned total_ctas;
   int tma_stages;  // 4,736-B TMA stages that fit the score's staging memory (fused compaction ring)
@@ -70,15 +79,17 @@ struct ScoreParams {
 
 #ifdef CS_PHASE_TIMING
 // experiment build only (scripts/phase_timing.py): per-CTA %globaltimer stamps at the phase boundaries
-__device__ unsigned long long g_cs_phase[16384][12];
-__device__ __forceinline__ void cs_phase(int k) {
+// (two slots, alternating per launch, so that back-to-back launches -- PDL overlap -- can be compared)
+__device__ unsigned long long g_cs_phase[2][16384][12];
+static int g_cs_phase_launch = 0;
+__device__ __forceinline__ void cs_phase(int slot, int k) {
   if (threadIdx.x == 0 && blockIdx.x < 16384) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_cs_phase[blockIdx.x][k] = t;
+    g_cs_phase[slot][blockIdx.x][k] = t;
   }
 }
-#define CS_PHASE(k) cs_phase(k)
+#define CS_PHASE(k) cs_phase(P.phase_slot, k)
 #else
 #define CS_PHASE(k)
 #endif
@@ -86,9 +97,20 @@ __device__ __forceinline__ void cs_phase(int k) {
 constexpr int kFusedMaxStages = 42;  // 200 KB of 4,736-B stages (one-wave grids, see launch_score)
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kFlagVal = (1ull << 62) - 1;
 
+// programmatic dependent launch (sm_90+): allow the next grid on the stream to launch now
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
@@ -213,7 +235,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   };
   if (tid < 32) {
     const int f = f_begin + lane;  // fpc <= kMaxFramesPerCall / 8 = 32
-    const bool isP = f < f_end && P.frame_type[(long long)sidx * P.frame_stride + f] == CS_FRAME_P;
+    const bool isP = f < f_end && P.frame_type[(long long)sidx * P.type_stride + f] == CS_FRAME_P;
     uint32_t pm = __ballot_sync(0xffffffffu, isP);
     if (lane == 0) {
       int n = 0;
@@ -229,8 +251,9 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
     }
   } else {
     const int t0 = tid - 32, nt = nthr - 32;
-    for (int f = t0; f < P.n_frames; f += nt) s_types[f] = P.frame_type[(long long)sidx * P.frame_stride + f];
-    for (int t = t0; t <= nw; t += nt) s_state[t] = P.gop_state[(long long)sidx * (nw + 1) + t];
+    for (int f = t0; f < P.n_frames; f += nt) s_types[f] = P.frame_type[(long long)sidx * P.type_stride + f];
+    if (!(FUSED && P.pdl))  // (chained: the GOP state -- the preceding call's output -- is read once it is ready)
+      for (int t = t0; t <= nw; t += nt) s_state[t] = P.gop_state[(long long)sidx * (nw + 1) + t];
     const int cw = P.mb * P.grid_w, ch = P.mb * P.grid_h;  // MB width / height in scaled units
     for (int c = t0; c < P.grid_w; c += nt) s_col[c] = make_int2((c * P.src_w) / cw, ((c + 1) * P.src_w - 1) / cw);
     for (int r = t0; r < P.grid_h; r += nt) s_row[r] = make_int2((r * P.src_h) / ch, ((r + 1) * P.src_h - 1) / ch);
@@ -355,6 +378,27 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       if (s_types[f] != CS_FRAME_P)
         for (int i = tid; i < P.np; i += nthr) P.score[((long long)sidx * P.n_frames + f) * P.np + i] = CUDART_INF_F;
 
+  CS_PHASE(11);
+  if (FUSED && P.pdl) {
+    // Chained call (CS_LAUNCH_PDL): everything above (stream ticket in this call's own workspace, MB loads, passes
+    // 1 and 2 into shared memory) read only inputs staged before the preceding call started, so it overlapped that
+    // call.  The GOP state is the preceding call's output: wait until its generation says it is final, and (the
+    // outputs below go to buffers call g-d used, d = chain depth) until call g-d has completed (done[g mod d]: calls
+    // of one class complete in order).  Both are published with release stores; the calls we wait for are resident
+    // (this grid launched after all of g-1's CTAs passed this point, g-1 after all of g-2's, ...), so the spins
+    // cannot deadlock.  (The stream ticket above used this call's workspace before any wait: calls g-1 .. g-d may
+    // still run, so chained calls rotate d + 1 workspaces.)
+    if (tid == 0) {
+      while (ld_acquire_u32(&P.gop_ready[sidx]) != P.generation) __nanosleep(32);
+      const unsigned cls = P.generation % P.chain_depth;
+      while (static_cast<int>(ld_acquire_u32(&P.chain_done[cls]) - (P.generation - P.chain_depth + 1u)) < 0)
+        __nanosleep(32);
+    }
+    __syncthreads();
+    for (int t = tid; t <= nw; t += nthr) s_state[t] = P.gop_state[(long long)sidx * (nw + 1) + t];
+    __syncthreads();
+    pdl_launch_dependents();  // the next call may launch once every CTA of this one is here
+  }
   CS_PHASE(4);
   cluster.sync();  // every CTA's dynamic words are published
 
@@ -399,10 +443,13 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       if (f == P.n_frames - 1) {  // final GOP state of the stream
         P.gop_state[(long long)sidx * (nw + 1) + t] = acc;
         if (t == 0) P.gop_state[(long long)sidx * (nw + 1) + nw] = s_state[nw] | 1u;
+        if (FUSED && P.pdl) __threadfence();  // (chained: ordered before the generation published below)
       }
     }
     if (tid == 0) s_kept = 0;
     __syncthreads();
+    if (FUSED && P.pdl && f == P.n_frames - 1 && tid == 0)  // chained: the stream's final state, to call g+1
+      st_release_u32(&P.gop_ready[sidx], P.generation + 1u);
     if (P.G == 2 && P.grid_w == 32) {
       // word r = patch row r: a group row is rows 2g, 2g+1; fold horizontal pairs, spread back to both columns
       for (int gr = tid; gr < P.grid_h / 2; gr += nthr) {
@@ -559,7 +606,47 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       }
     };
     int written = 0;
-    const bool tma = P.layout == CS_LAYOUT_GROUPED && P.vec_out && P.patch == 14 && P.G == 2 && P.grid_w == 32 &&
+    bool tma = false;  // per-stream TMA ring: only thread 0 holds the CTA's count
+    if (P.global_compact) {
+      // Grid-balanced compaction (every cluster is co-resident, checked on the host): each stream's cluster would
+      // otherwise copy only its own stream's kept groups, and streams with more motion keep more (measured at C2:
+      // CTAs end 36-55 us apart).  Publish this CTA's frame offsets, wait until every CTA of the grid has, then
+      // every ring warp of the grid takes an equal share of ALL the batch's kept groups (the layout
+      // codecsight_compact's TMA gather uses, cs::group_ring).
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        atomicAdd(&P.ws_ctr[2], 1u);
+        while (ld_acquire_u32(&P.ws_ctr[2]) < P.total_ctas) __nanosleep(64);
+      }
+      __syncthreads();
+      __shared__ __align__(8) uint64_t s_gfull[kFusedMaxStages];
+      __shared__ cs::RingGroup s_gdesc[kFusedMaxStages];
+      const int R = min(nthr >> 5, P.tma_stages / 3);  // ring warps of >= 3 stages each
+      const int wq = tid >> 5;
+      if (wq < R) {
+        const int nst = P.tma_stages / R;
+        cs::RingBatch B;
+        B.frame_offsets = P.frame_offsets;
+        B.n_slots = P.n_streams * P.n_frames;
+        B.n_frames = P.n_frames;
+        B.keep_mask = P.keep_mask;
+        B.mask_frame_stride = P.frame_stride;
+        B.frames = P.frames;
+        B.frame_index = P.frame_index;
+        B.capacity = P.capacity;
+        B.packed = P.packed;
+        B.pos_ids = P.pos_ids;
+        B.src_index = P.src_index;
+        const long long T = static_cast<long long>(P.frame_offsets[B.n_slots]) / 4;
+        const long long NW = static_cast<long long>(gridDim.x) * R, gw = static_cast<long long>(blockIdx.x) * R + wq;
+        const long long rows = cs::group_ring(B, T * gw / NW, T * (gw + 1) / NW,
+                                              smem + P.off_stage + (size_t)wq * nst * cs::kRingStageAlloc, nst,
+                                              s_gfull + wq * nst, s_gdesc + wq * nst, lane);
+        if (lane == 0) written = static_cast<int>(rows);
+      }
+    } else {
+    tma = P.layout == CS_LAYOUT_GROUPED && P.vec_out && P.patch == 14 && P.G == 2 && P.grid_w == 32 &&
                      P.grid_h == 32 && P.tma_stages >= 9;  // R = stages/3 rings of >= 3 stages each, else direct copies (measured)
     if (tma) {
       // the CTA's share of the stream's kept groups: thread 0 runs a TMA bulk ring over it (4,704-B groups,
@@ -691,7 +778,9 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
                        written += fused_copy_group(P, fr, vec_in, gr, gc, n0, slot, P.frame_index[slot], lane);
                      });
     }
+    }  // (per-stream compaction)
     if ((lane == 0 || tma) && written) atomicAdd(&s_written, written);
+    if (P.pdl) __threadfence();  // (chained: every output write ordered before the completion published below)
     __syncthreads();
     CS_PHASE(7);
     if (tid == 0) {
@@ -706,7 +795,9 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
         for (int j = 0; j < P.n_streams; ++j) P.ws_flags[j] = 0ull;
         P.ws_ctr[0] = 0u;
         P.ws_ctr[1] = 0u;
+        P.ws_ctr[2] = 0u;
         __threadfence();
+        if (P.pdl) st_release_u32(&P.chain_done[P.generation % P.chain_depth], P.generation + 1u);  // call complete
       }
     }
   }
@@ -720,6 +811,30 @@ constexpr unsigned kWideSmem = 200u * 1024u;  // the kernels' dynamic shared mem
 
 // true when all n_streams clusters of `cfg` are co-resident with kWideSmem bytes of dynamic shared memory per CTA
 // (cudaOccupancyMaxActiveClusters; the answer for the last (device, cluster size) is cached)
+// clusters of this launch configuration that can be resident at once with `smem` dynamic bytes per CTA (cached)
+static int max_active_clusters(const void* fn, const cudaLaunchConfig_t& cfg, size_t smem) {
+  static thread_local int c_dev = -1, c_cluster = -1, c_max = 0;
+  static thread_local size_t c_smem = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  const int cl = static_cast<int>(cfg.attrs[0].val.clusterDim.x);
+  if (dev != c_dev || cl != c_cluster || smem != c_smem) {
+    cudaLaunchConfig_t q = cfg;
+    q.dynamicSmemBytes = smem;
+    q.numAttrs = 1;  // (the cluster dimension only)
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &q) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    c_dev = dev;
+    c_cluster = cl;
+    c_smem = smem;
+    c_max = n;
+  }
+  return c_max;
+}
+
 static bool fused_one_wave(const void* fn, const cudaLaunchConfig_t& cfg, int32_t n_streams) {
   static thread_local int c_dev = -1, c_cluster = -1, c_max = 0;
   int dev = 0;
@@ -767,6 +882,11 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
   cluster = (n_frames + P.fpc - 1) / P.fpc;
   P.cluster = cluster;
   P.frame_stride = frame_stride;
+  if (!fuse || P.type_stride <= 0) P.type_stride = frame_stride;
+#ifdef CS_PHASE_TIMING
+  P.phase_slot = g_cs_phase_launch & 1;
+  ++g_cs_phase_launch;
+#endif
   P.row_bytes = static_cast<unsigned>(g->mb_cols) * 8u;
   P.use_bulk = ((reinterpret_cast<uintptr_t>(mb) & 15u) == 0 && (P.row_bytes % 16u) == 0) ? 1 : 0;
   const unsigned target = 8192u;
@@ -796,20 +916,26 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
   cfg.gridDim = dim3(static_cast<unsigned>(n_streams) * static_cast<unsigned>(cluster), 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (P.fused && P.pdl) {  // may start while the preceding call on `stream` runs (chained by generations, above)
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
 
   // dynamic shared memory budget per CTA: 50 KB for score_patches (4 CTAs/SM, register-limited anyway), 68 KB for
   // the fused kernel (3 CTAs/SM; the compaction's TMA rings reuse the staging memory), and the SM's whole 200 KB
   // when all the fused grid's clusters are co-resident even then (one wave at one CTA per SM, e.g. C2): deeper
   // rings, more bytes in flight per SM (measured)
   unsigned budget = P.fused ? CS_FUSED_SMEM_KB * 1024u : 50u * 1024u;
-  if (P.fused && fused_one_wave(fn, cfg, n_streams)) budget = kWideSmem;
+  // (PDL: two calls' CTAs must fit an SM together, so no whole-SM budget)
+  if (P.fused && !P.pdl && fused_one_wave(fn, cfg, n_streams)) budget = kWideSmem;
 
   // layout: small regions first, then the MB staging ring, Vrow, Srow (only with alpha != 0); the MB ring takes
   // whatever the budget leaves (all of a frame's chunks in flight when they fit, at most 16 mbarriers, >= 2 stages)
@@ -846,6 +972,10 @@ static int launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, c
     if (need > smem) smem = need;
   }
   cfg.dynamicSmemBytes = smem;
+  // grid-balanced compaction when every cluster of the grid is resident at once (its CTAs wait for each other)
+  P.global_compact = (P.fused && P.layout == CS_LAYOUT_GROUPED && P.vec_out && P.patch == 14 && P.G == 2 &&
+                      P.grid_w == 32 && P.grid_h == 32 && P.tma_stages >= 3 &&
+                      n_streams <= max_active_clusters(fn, cfg, smem)) ? 1 : 0;
   void* args[] = {&P};
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return CS_ERR_CUDA;
   return CS_OK;
@@ -860,17 +990,26 @@ int cs_launch_score(const cs_grid* g, int32_t n_streams, int32_t n_frames, const
 }
 
 size_t cs_score_compact_workspace_bytes(int32_t n_streams) {
-  return n_streams < 0 ? 0 : 8u + 8u * static_cast<size_t>(n_streams);
+  return n_streams < 0 ? 0 : 16u + 8u * static_cast<size_t>(n_streams);
 }
 
 int cs_launch_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frames, const cs_mb* mb,
-                            const uint8_t* frame_type, uint32_t* keep_mask, int64_t frame_stride,
-                            uint32_t* gop_state, float* score, int32_t* kept_count, const int32_t* frame_index,
-                            const void* const* frames, int32_t frame_layout, int64_t capacity, void* packed,
-                            int32_t* pos_ids, int32_t* src_index, int32_t* frame_offsets, void* workspace,
-                            unsigned long long* counters, int32_t* status, cudaStream_t stream) {
+                            const uint8_t* frame_type, int64_t type_stride, uint32_t* keep_mask,
+                            int64_t frame_stride, uint32_t* gop_state, float* score, int32_t* kept_count,
+                            const int32_t* frame_index, const void* const* frames, int32_t frame_layout,
+                            int64_t capacity, void* packed, int32_t* pos_ids, int32_t* src_index,
+                            int32_t* frame_offsets, void* workspace, unsigned long long* counters, int32_t* status,
+                            const cs_chain* chain, cudaStream_t stream) {
   ScoreParams F{};
   F.fused = 1;
+  F.type_stride = type_stride;
+  F.pdl = chain ? 1 : 0;
+  if (chain) {
+    F.gop_ready = chain->gop_ready;
+    F.chain_done = chain->done;
+    F.generation = chain->generation;
+    F.chain_depth = chain->depth;
+  }
   F.layout = frame_layout;
   F.patch = g->patch;
   F.FW = g->grid_w * g->patch;
@@ -886,14 +1025,20 @@ int cs_launch_score_compact(const cs_grid* g, int32_t n_streams, int32_t n_frame
   F.src_index = src_index;
   F.frame_offsets = frame_offsets;
   F.ws_ctr = static_cast<unsigned*>(workspace);
-  F.ws_flags = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(workspace) + 8);
+  F.ws_flags = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(workspace) + 16);
   return launch_score(g, n_streams, n_frames, mb, frame_type, keep_mask, frame_stride, gop_state, score, kept_count,
                       counters, status, &F, stream);
 }
 
 #ifdef CS_PHASE_TIMING
-extern "C" int codecsight_debug_phase(unsigned long long* host, int n_ctas) {
+extern "C" int codecsight_debug_phase(unsigned long long* host, int n_ctas) {  // slot of the last launch
   if (n_ctas > 16384) n_ctas = 16384;
-  return cudaMemcpyFromSymbol(host, g_cs_phase, sizeof(unsigned long long) * 12 * n_ctas) == cudaSuccess ? 0 : -1;
+  const size_t off = sizeof(unsigned long long) * 12 * 16384 * ((g_cs_phase_launch + 1) & 1);
+  return cudaMemcpyFromSymbol(host, g_cs_phase, sizeof(unsigned long long) * 12 * n_ctas, off) == cudaSuccess ? 0 : -1;
+}
+extern "C" int codecsight_debug_phase_slot(unsigned long long* host, int n_ctas, int slot) {
+  if (n_ctas > 16384) n_ctas = 16384;
+  const size_t off = sizeof(unsigned long long) * 12 * 16384 * (slot & 1);
+  return cudaMemcpyFromSymbol(host, g_cs_phase, sizeof(unsigned long long) * 12 * n_ctas, off) == cudaSuccess ? 0 : -1;
 }
 #endif

@@ -28,7 +28,7 @@ class Pipeline:
                  n_prompt: int = 0, device=None, want_score: bool = False, packed_capacity: int | None = None,
                  with_refreshed: bool = True, frame_layout: int = abi.CS_LAYOUT_PLANAR, kv_mode: str = "copy",
                  compact_chunk: int | None = None, preprocess: dict | None = None, overlap: bool = False,
-                 temporal_patch: int = 1, fused: bool = False):
+                 temporal_patch: int = 1, fused: bool = False, pdl: bool = False, chain_depth: int = 4):
         self.g = dict(grid)
         # Ring slots: frame f lives in slot f % ring and a step's n new frames are handed to the kernels as ONE
         # contiguous run of slots [off, off + n) (the calls take a pointer and a frame stride, not a modular index).
@@ -41,6 +41,13 @@ class Pipeline:
                              "a step's new frames must be one contiguous run of ring slots")
         # fused: one codecsight_score_compact launch per step (NEXT-2) instead of score_patches + compact
         self.fused = fused
+        # pdl: step k's fused launch is chained call k (CS_LAUNCH_PDL, cs_chain): a programmatic dependent of step
+        # k-1's that overlaps it (scoring during k-1's compaction, then compaction alongside k-1's tail).  Prune-only
+        # pipelines (no KV refresh between the launches); the step's frame types are read straight from the caller's
+        # [S][n] tensor (no ring copy between the launches); workspaces and output buffer sets alternate by parity.
+        self.pdl = pdl
+        if pdl:
+            assert fused and kv is None and not overlap, "pdl: fused score+compact, no KV refresh, no overlap mode"
         if fused:
             assert temporal_patch == 1 and preprocess is None, "fused score+compact: model frames, temporal_patch 1"
         # temporal patches (NEXT-3, Qwen2-VL temporal_patch_size): a token unit = tp consecutive frames; scoring stays
@@ -73,7 +80,9 @@ class Pipeline:
         self.gop_state = torch.zeros(S, nw + 1, dtype=torch.int32, device=d)
         self.mask_ring = torch.zeros(S, ring, nw, dtype=torch.int32, device=d)
         self.type_ring = torch.zeros(S, ring, dtype=torch.uint8, device=d)
-        nb = 2 if overlap else 1  # per-step outputs alternate between nb buffer sets (step parity)
+        # per-step outputs alternate between nb buffer sets (step parity; chained PDL calls: step mod chain depth)
+        self.chain_depth = chain_depth
+        nb = self.chain_depth if pdl else (2 if overlap else 1)
         self._kept_count = [torch.zeros(S, window, dtype=torch.int32, device=d) for _ in range(nb)]
         self.kept_count = self._kept_count[0]
         self.score = torch.zeros(S, window, self.np, dtype=torch.float32, device=d) if want_score else None
@@ -128,6 +137,13 @@ class Pipeline:
         self.cur = 0  # which cache set holds window k-1
         if fused:
             self.sc_workspace = torch.zeros(abi.score_compact_workspace_size(S), dtype=torch.uint8, device=d)
+            # chained calls rotate three workspaces (a call takes its stream tickets while the two before it may
+            # still run); chain state: per-stream GOP-state generations + per-parity completed-call generations
+            nws = self.chain_depth + 1 if pdl else 1
+            self._sc_ws = [self.sc_workspace] + [torch.zeros_like(self.sc_workspace) for _ in range(nws - 1)]
+            if pdl:
+                self._chain = (torch.zeros(S, dtype=torch.int32, device=d),
+                               torch.zeros(self.chain_depth, dtype=torch.int32, device=d))
         self._side_done = {}  # step -> events closing its compact / kv_refresh work (overlap mode)
         self._graphs = {}     # graph_step: key -> captured torch.cuda.CUDAGraph
         self._bound = {}      # (ring slot, frames, buffer parity) -> abi.BoundScoreCompact
@@ -192,6 +208,26 @@ class Pipeline:
                 self.disposition, self.p_old, self.n_tokens = self._disposition[b], self._p_old[b], self._n_tokens[b]
             for e in self._side_done.pop(k - 2, []) + list(wait_events):
                 main.wait_event(e)
+        if self.pdl:
+            # no stream operation between two fused launches (an event or a copy would cancel the overlap)
+            assert types is not None, "pdl: pass the step's frame types"
+            b, nws = k % self.chain_depth, len(self._sc_ws)
+            self.kept_count, self.packed, self.pos_ids = self._kept_count[b], self._packed[b], self._pos_ids[b]
+            self.src_index, self.frame_offsets = self._src_index[b], self._frame_offsets[b]
+            key = (off, n, b, k % nws)
+            call = self._bound.get(key)
+            if call is None:
+                call = abi.BoundScoreCompact(
+                    g, self.S, n, None, self.mask_ring[:, off:], self.ring, self.gop_state, None,
+                    self.kept_counts(n), self.capacity, self.packed, self.pos_ids, self.src_index,
+                    self.frame_offsets[: self.S * n + 1], self._sc_ws[k % nws], self.counters, self.status,
+                    frame_layout=self.frame_layout, flags=abi.CS_LAUNCH_PDL, type_stride=n, chain=self._chain)
+                self._bound[key] = call
+            fi = self.frame_index[: self.S * n] if frame_index is None else frame_index
+            if timing:
+                s0 = ev(main)
+            call(mb, fi, frame_ptrs, main.cuda_stream, frame_type=types, generation=k)
+            return {"score": (s0, ev(main))} if timing else {}
         with torch.cuda.stream(main):
             if types is not None:
                 tv = self._type_views.get((off, n))

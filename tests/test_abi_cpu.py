@@ -122,7 +122,7 @@ def test_extension_validation(abi):
     nocuda = not torch.cuda.is_available()
     # fused score + compact (NEXT-2)
     ws_need = abi.score_compact_workspace_size(4)
-    assert ws_need == 8 + 8 * 4
+    assert ws_need == 16 + 8 * 4
 
     def sc(n_streams=4, n_frames=2, fs=2, layout=1, cap=16, ws=FAKE, ws_bytes=1 << 10, mb=FAKE):
         return L.codecsight_score_compact(G, n_streams, n_frames, mb, FAKE, FAKE, fs, FAKE, None, FAKE, FAKE, FAKE,
@@ -135,6 +135,21 @@ def test_extension_validation(abi):
     assert sc(n_streams=0) == abi.CS_OK
     if nocuda:
         assert sc() == abi.CS_ERR_CUDA                                     # no CPU fallback
+
+    # the extended call: type stride, chained launches (CS_LAUNCH_PDL needs a valid chain, no score output)
+    def sce(flags=0, chain=None, ts=2, score=None):
+        return L.codecsight_score_compact_ex(G, 4, 2, FAKE, FAKE, ts, FAKE, 2, FAKE, score, FAKE, FAKE, FAKE, 1, 16,
+                                             FAKE, FAKE, FAKE, FAKE, FAKE, 1 << 10, FAKE, FAKE, flags, chain, None)
+    good = abi.CsChain(FAKE, FAKE, 0, 4)
+    assert sce(ts=1) == abi.CS_ERR_INVALID_ARGUMENT                        # type stride < n_frames
+    assert sce(flags=2) == abi.CS_ERR_INVALID_ARGUMENT                     # unknown flag
+    assert sce(flags=abi.CS_LAUNCH_PDL) == abi.CS_ERR_INVALID_ARGUMENT     # PDL without a chain
+    for bad in (abi.CsChain(None, FAKE, 0, 4), abi.CsChain(FAKE, None, 0, 4), abi.CsChain(FAKE, FAKE, 0, 1),
+                abi.CsChain(FAKE, FAKE, 0, 9)):
+        assert sce(flags=abi.CS_LAUNCH_PDL, chain=C.byref(bad)) == abi.CS_ERR_INVALID_ARGUMENT
+    assert sce(flags=abi.CS_LAUNCH_PDL, chain=C.byref(good), score=FAKE) == abi.CS_ERR_UNSUPPORTED
+    if nocuda:
+        assert sce(flags=abi.CS_LAUNCH_PDL, chain=C.byref(good)) == abi.CS_ERR_CUDA
     # temporal patches (NEXT-3)
 
     def tp(t=2, n_units=2, mfs=4, cap=16, um=None, ums=0, ft=None, ut=None):

@@ -1444,3 +1444,67 @@ def test_cdf_workload_pipeline(abi, ref):
     assert (hist.cpu().numpy().astype(np.uint64) == ho).all()
     assert int(st.item()) == so["status"] == 0
     assert ho.sum() == len(taus) * p.sum()
+
+
+def test_pipeline_pdl_matches_plain(abi, ref):
+    """Prune-only (C2-shaped) pipeline with programmatic dependent launches (CS_LAUNCH_PDL): 10 steps enqueued back
+    to back with no host synchronisation and no stream operation between the fused launches, so each step's stream
+    ticket, MB loads and scoring passes really overlap the previous step's compaction.  Final GOP state, every mask
+    of the ring, counters, status and the last step's outputs must equal the plain fused pipeline's (itself
+    parity-tested against the oracle), and the last step's outputs the oracle's."""
+    from paper_2604_06036_b200.pipeline import Pipeline
+    cfg = synth.CONFIGS["C2"]
+    g = make_grid(1920, 1080)
+    S, w, s, gop, K = 12, 16, 4, 16, 10
+    rng = np.random.default_rng(8)
+    frames_h = [to_grouped(f, g) for f in synth.random_frames(S * s, 448, 448, rng)]
+    frames_d = [torch.from_numpy(f.view(np.int16)).to(DEV) for f in frames_h]
+    gens = [synth.StreamGen(1920, 1080, synth.scene_of(cfg, si), synth.stream_seed(cfg, si)) for si in range(S)]
+    inputs, host = [], []
+    for k in range(K):
+        f0, n = (0, w) if k == 0 else ((k - 1) * s + w, s)
+        mb = np.stack([np.stack([gens[si].next_frame() for _ in range(n)]) for si in range(S)])
+        types = np.stack([synth.frame_types(n, gop, f0) for _ in range(S)])
+        fidx = np.tile(np.arange(f0, f0 + n, dtype=np.int32), S)
+        ptrs = abi.ptr_array([frames_d[i % len(frames_d)] for i in range(S * n)], DEV)
+        inputs.append((d_mb(mb), ptrs, torch.from_numpy(fidx).to(DEV), torch.from_numpy(types).to(DEV)))
+        host.append((mb, types, fidx))
+    runs = {}
+    for pdl in (False, True):
+        pipe = Pipeline(g, S, w, s, gop, None, device=DEV, frame_layout=abi.CS_LAYOUT_GROUPED, fused=True, pdl=pdl)
+        torch.cuda.synchronize()
+        for k in range(K):
+            pipe.step(k, *inputs[k])
+        torch.cuda.synchronize()
+        n = s
+        tot = int(pipe.frame_offsets[S * n].item())
+        runs[pdl] = dict(gop=u32(pipe.gop_state), ring=u32(pipe.mask_ring), counters=pipe.counters.cpu().numpy(),
+                         status=int(pipe.status.item()), kept=pipe.kept_counts(n).cpu().numpy(),
+                         offs=pipe.frame_offsets[:S * n + 1].cpu().numpy(),
+                         packed=pipe.packed[:tot].view(torch.int16).cpu().numpy().view(np.uint16),
+                         pos=pipe.pos_ids[:tot].cpu().numpy(), src=pipe.src_index[:tot].cpu().numpy())
+        del pipe
+    a, b = runs[False], runs[True]
+    assert a["status"] == b["status"] == 0
+    for key in ("gop", "ring", "counters", "kept", "offs", "packed", "pos", "src"):
+        assert (a[key] == b[key]).all(), key
+    # the last step against the oracle (the GOP state carried through all K steps)
+    ring = w + s
+    gop_h = np.zeros((S, 33), np.uint32)
+    mring_h = np.zeros((S, ring, 32), np.uint32)
+    tring_h = np.zeros((S, ring), np.uint8)
+    for k in range(K):
+        mb, types, fidx = host[k]
+        f0, n = (0, w) if k == 0 else ((k - 1) * s + w, s)
+        off = f0 % ring
+        tring_h[:, off:off + n] = types
+        so = ref.score_patches(g, mb, np.ascontiguousarray(tring_h[:, off:]), gop_h, want_score=False,
+                               frame_stride=ring - off)
+        mring_h[:, off:off + n] = so["keep_mask"][:, :n]
+    assert (b["gop"] == gop_h).all() and (b["ring"] == mring_h).all()
+    fr = [frames_h[i % len(frames_h)] for i in range(S * s)]
+    co = ref.compact(g, mring_h[:, off:].copy(), fidx, fr, S * s * 1024, S, s, mask_frame_stride=ring - off,
+                     frame_layout=1)
+    assert (b["offs"] == co["frame_offsets"]).all()
+    tot = int(co["frame_offsets"][-1])
+    assert (b["packed"] == co["packed"][:tot]).all() and (b["pos"] == co["pos_ids"][:tot]).all()
