@@ -116,7 +116,7 @@ def run_reference(args, cfg, rank, world):
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
 
-    from bench import ClockSampler, host_cpu_model, log, measured_peak_hbm
+    from bench import ClockSampler, host_cpu_model, log, measured_peak_hbm, ncu_traffic
     from paper_2604_06036_b200 import _abi as abi
     from paper_2604_06036_b200 import shard
 
@@ -253,8 +253,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     for name, byt, t in (("codecsight_mv_rasterize", b_rast, kms[0]), ("codecsight_score_patches", b_score, kms[1]),
                          ("codecsight_similar_hist", b_hist, kms[2])):
         a = byt / (t / 1e3) / 1e9
+        key = {"codecsight_mv_rasterize": "rasterize", "codecsight_score_patches": "score_patches",
+               "codecsight_similar_hist": "similar_hist"}[name]
         rl[name] = {"bound": "hbm", "kernel": name, "achieved": a, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                    "frac": a / peak, "ms": float(t), "algorithmic_bytes_per_launch": byt, "traffic": None}
+                    "frac": a / peak, "ms": float(t), "algorithmic_bytes_per_launch": byt,
+                    "traffic": ncu_traffic(key, cfg["name"])}
     dom = max(rl, key=lambda x: rl[x]["ms"])
     out = {
         "metric": "frames/sec (NEXT-4: H.264 MV ingest + score + similar-patch histogram), all GPUs",

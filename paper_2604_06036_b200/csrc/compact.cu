@@ -708,6 +708,215 @@ __global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED &
   }
 }
 
+// ---- planar CHW frames, 2x2 groups of 14-px patches on a 32 x 32 grid: band-staged TMA gather --------------
+// A kept group of a planar frame is 84 row segments of 56 B (3 channels x 28 rows) at 8-B alignment.  Fetched one
+// group at a time, every segment drags in the rest of its 128-B lines, which are only useful if the neighbouring
+// group is kept AND still cached when its turn comes (measured round 1: DRAM reads 3.2x the algorithmic bytes,
+// 0.41 of the roofline).  Here a warp takes RUNS of up to kBandRun consecutive kept groups of one group row (the
+// packed order puts them in consecutive rows) and stages the run's band -- for each of the 84 source rows the one
+// contiguous span covering all of the run's groups, widened to 16-B alignment -- with 84 cp.async.bulk copies
+// into a stage of its TMA ring (mbarrier complete_tx), so each source line is requested once, by one copy, while
+// the next runs' copies are in flight.  The warp then writes each group's 4,704 output bytes with 16-B stores,
+// every 16-B chunk assembled from four 4-B pixel pairs of the staged rows (a pair never straddles a 14-px patch
+// row) through a per-CTA table of staged-row offsets.
+#ifndef CS_BAND_RUN
+#define CS_BAND_RUN 3
+#define CS_BAND_WARPS 7
+#define CS_BAND_STAGES 2
+#endif
+constexpr int kBandRun = CS_BAND_RUN;                                 // groups per run
+constexpr int kBandRowBytes = ((8 + 56 * kBandRun) + 15) & ~15;      // staged row pitch (3 groups: 176 B)
+constexpr int kBandStage = 84 * kBandRowBytes;                        // 3 channels x 28 rows
+constexpr int kBandWarps = CS_BAND_WARPS;                             // 7 x 2 stages x 14.8 KB: one CTA per SM
+constexpr int kBandMaxStages = CS_BAND_STAGES;
+static_assert(kBandWarps * kBandMaxStages * kBandStage <= 220 * 1024, "band stages exceed shared memory");
+
+struct BandRun {
+  long long n0;          // first packed row of the run
+  const uint16_t* row0;  // frame element of (c = 0, y = 28 gr, x = 28 gc_a), i.e. the run's first source pixel
+  int slot, gr, gc, k;   // frame slot, group row, first group column, groups in the run (0: end of work)
+  int t_index, lead;     // pos id t; bytes between the 16-B aligned copy start and the run's first pixel
+};
+
+__global__ void __launch_bounds__(kBandWarps * 32, 1) compact_gather_band(const __grid_constant__ CompactParams P,
+                                                                          int nst) {
+  extern __shared__ __align__(128) unsigned char b_smem[];
+  __shared__ BandRun s_run[kBandWarps][kBandMaxStages];
+  __shared__ __align__(8) uint64_t s_full[kBandWarps][kBandMaxStages];
+  __shared__ uint4 s_tab[294];  // per 16-B output chunk of a group: 4 pixel pairs -> (staged row, byte) as u16 pairs
+  __shared__ __align__(16) uint32_t s_mask[kBandWarps][32];  // the current slot's keep mask (lane 0's generator)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  constexpr int p = 14, pp = 196, row_el = 588;
+  constexpr long long FW = 448, plane = 448ll * 448;
+  // table: element i = 8 e + 2 t of a group -> patch q, channel c, (py, px) -> staged row c*28 + dy*14 + py and the
+  // byte offset 2 (dx*14 + px) within the group's 56 bytes (the run offset j*56 + lead is added per group)
+  for (int e = threadIdx.x; e < 294; e += blockDim.x) {
+    uint32_t w[4];
+    for (int t = 0; t < 4; ++t) {
+      const int i = 8 * e + 2 * t, q = i / row_el, r = i - q * row_el, c = r / pp, r2 = r - c * pp;
+      const int py = r2 / p, px = r2 - py * p, dy = q >> 1, dx = q & 1;
+      w[t] = static_cast<uint32_t>((c * 28 + dy * 14 + py) * kBandRowBytes) | (static_cast<uint32_t>(2 * (dx * 14 + px)) << 16);
+    }
+    s_tab[e] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __syncthreads();
+  const long long total_groups = static_cast<long long>(__ldg(P.frame_offsets + P.n_slots)) / 4;
+  const long long nwarps = static_cast<long long>(gridDim.x) * kBandWarps;
+  const long long wid = static_cast<long long>(blockIdx.x) * kBandWarps + wib;
+  long long q = total_groups * wid / nwarps;
+  const long long q1 = total_groups * (wid + 1) / nwarps;
+  if (q >= q1) return;
+  unsigned char* stages = b_smem + (size_t)wib * nst * kBandStage;
+  uint64_t* full = s_full[wib];
+  BandRun* runs = s_run[wib];
+
+  // ---- generator (lane 0): slot, group row, remaining kept-group bits of the row -------------------------------
+  int slot = 0, gr = 0, t_index = 0;
+  uint32_t ybits = 0u;
+  const uint16_t* frame = nullptr;
+  // the slot's 32 mask words are copied to shared memory once per slot (8 x 16-B loads), so walking its group rows
+  // costs no global-memory latency on the ring's critical path
+  uint32_t* smask = s_mask[wib];
+  auto load_row = [&]() {
+    const uint32_t x = smask[2 * gr] | smask[2 * gr + 1];
+    ybits = (x | (x >> 1)) & 0x55555555u;  // bit 2*gc set iff group (gr, gc) is kept
+  };
+  auto load_slot = [&]() {
+    frame = static_cast<const uint16_t*>(P.frames[slot]);
+    t_index = __ldg(P.frame_index + slot);
+    const uint4* m4 = reinterpret_cast<const uint4*>(slot_mask(P, slot));
+    uint4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldg(m4 + i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) reinterpret_cast<uint4*>(smask)[i] = v[i];
+  };
+  if (lane == 0) {
+    int lo = 0, hi = P.n_slots;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (static_cast<long long>(__ldg(P.frame_offsets + mid)) <= q * 4) lo = mid; else hi = mid;
+    }
+    slot = lo;
+    long long skip = q - __ldg(P.frame_offsets + slot) / 4;
+    load_slot();
+    load_row();
+    while (skip >= __popc(ybits)) {
+      skip -= __popc(ybits);
+      ++gr;
+      load_row();
+    }
+    for (; skip > 0; --skip) ybits &= ybits - 1u;
+    for (int st = 0; st < nst; ++st) cs::mbar_init(&full[st], 1);
+    cs::fence_mbar_init();
+  }
+  __syncwarp();
+  bool more = true;  // (lane 0)
+  // next run into stage st: lane 0 forms it and arms the barrier, then the lanes issue the 84 row copies
+  auto issue = [&](int st) {
+    BandRun r;
+    uint32_t bytes = 0;
+    if (lane == 0) {
+      if (q >= q1) {
+        r.k = 0;
+        more = false;
+      } else {
+        while (ybits == 0u) {
+          if (++gr == 16) {
+            gr = 0;
+            ++slot;
+            load_slot();
+          }
+          load_row();
+        }
+        const int gc = (__ffs(ybits) - 1) >> 1;
+        int k = 0;  // consecutive kept groups gc, gc+1, ... of this row, within the warp's range and the run cap
+        while (k < kBandRun && q + k < q1 && gc + k < 16 && ((ybits >> (2 * (gc + k))) & 1u)) ++k;
+        ybits &= ~((1u << (2 * (gc + k))) - 1u);
+        r.n0 = q * 4;
+        r.slot = slot;
+        r.gr = gr;
+        r.gc = gc;
+        r.k = k;
+        r.t_index = t_index;
+        r.row0 = frame + (long long)(gr * 28) * FW + gc * 28;
+        const uintptr_t a = reinterpret_cast<uintptr_t>(r.row0);
+        r.lead = static_cast<int>(a & 15u);
+        bytes = static_cast<uint32_t>(((r.lead + k * 56) + 15) & ~15);  // per row, 16-B multiple
+        q += k;
+        runs[st] = r;
+        cs::mbar_arrive_expect_tx(&full[st], 84u * bytes);
+      }
+      if (r.k == 0) {
+        runs[st].k = 0;
+        cs::mbar_arrive(&full[st]);
+      }
+    }
+    __syncwarp();
+    bytes = __shfl_sync(0xffffffffu, bytes, 0);
+    if (bytes) {
+      const BandRun rr = runs[st];
+      const unsigned char* base = reinterpret_cast<const unsigned char*>(rr.row0) - rr.lead;
+      for (int row = lane; row < 84; row += 32) {
+        const int c = row / 28, y = row - c * 28;
+        cs::bulk_g2s(stages + (size_t)st * kBandStage + row * kBandRowBytes,
+                     base + (c * plane + (long long)y * FW) * 2, bytes, &full[st]);
+      }
+    }
+  };
+  for (int st = 0; st < nst; ++st) {
+    const bool m = __shfl_sync(0xffffffffu, more ? 1 : 0, 0);
+    if (!m) break;
+    issue(st);
+  }
+  for (int it = 0;; ++it) {
+    const int st = it % nst;
+    cs::mbar_wait(&full[st], (it / nst) & 1);
+    const BandRun r = runs[st];
+    if (r.k == 0) break;
+    const unsigned char* stg = stages + (size_t)st * kBandStage;
+    for (int j = 0; j < r.k; ++j) {
+      const long long n0 = r.n0 + 4 * j;
+      long long nvalid = P.capacity - n0;
+      nvalid = nvalid < 0 ? 0 : (nvalid > 4 ? 4 : nvalid);
+      if (nvalid > 0) {
+        const unsigned char* g0 = stg + r.lead + j * 56;
+        uint16_t* dst = P.packed + n0 * row_el;
+        if (nvalid == 4) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+          for (int e = lane; e < 294; e += 32) {
+            const uint4 t = s_tab[e];
+            uint4 v;
+            v.x = *reinterpret_cast<const uint32_t*>(g0 + (t.x & 0xffffu) + (t.x >> 16));
+            v.y = *reinterpret_cast<const uint32_t*>(g0 + (t.y & 0xffffu) + (t.y >> 16));
+            v.z = *reinterpret_cast<const uint32_t*>(g0 + (t.z & 0xffffu) + (t.z >> 16));
+            v.w = *reinterpret_cast<const uint32_t*>(g0 + (t.w & 0xffffu) + (t.w >> 16));
+            d4[e] = v;
+          }
+        } else {  // capacity-truncated group: element stores of its first nvalid rows
+          for (int i = lane; i < nvalid * row_el; i += 32) {
+            const int qq = i / row_el, rr = i - qq * row_el, c = rr / pp, r2 = rr - c * pp;
+            const int py = r2 / p, px = r2 - py * p;
+            dst[i] = *reinterpret_cast<const uint16_t*>(g0 + (c * 28 + (qq >> 1) * 14 + py) * kBandRowBytes +
+                                                        2 * ((qq & 1) * 14 + px));
+          }
+        }
+        if (lane < nvalid) {
+          const int h = r.gr * 2 + (lane >> 1), w = (r.gc + j) * 2 + (lane & 1);
+          const long long n = n0 + lane;
+          P.pos_ids[3 * n + 0] = r.t_index;
+          P.pos_ids[3 * n + 1] = h;
+          P.pos_ids[3 * n + 2] = w;
+          P.src_index[n] = r.slot * 1024 + h * 32 + w;
+        }
+      }
+    }
+    __syncwarp();  // the stage is consumed (generic-proxy reads) before it is refilled by the async proxy
+    const bool m = __shfl_sync(0xffffffffu, more ? 1 : 0, 0);
+    if (m) issue(st);
+  }
+}
+
 // ---- grouped frames, 2x2 groups of 14-px patches on a 32-wide grid: TMA bulk copies ------------------------
 // A kept group is one contiguous 4,704-B block of the frame and of the packed output (16-B aligned): each warp is
 // an independent TMA ring (lane 0 drives it, like kv_gather_tma): cp.async.bulk global -> smem completes on the
@@ -739,8 +948,9 @@ __global__ void __launch_bounds__(kGatherThreads, 1) compact_gather_tma(const __
   B.packed = P.packed;
   B.pos_ids = P.pos_ids;
   B.src_index = P.src_index;
+  __shared__ __align__(16) uint32_t s_mask[kTmaWarps][32];
   cs::group_ring(B, total_groups * wid / nwarps, total_groups * (wid + 1) / nwarps,
-                 t_smem + (size_t)wib * nst * kTmaStageAlloc, nst, s_full[wib], s_desc[wib], lane);
+                 t_smem + (size_t)wib * nst * kTmaStageAlloc, nst, s_full[wib], s_desc[wib], s_mask[wib], lane);
 }
 
 }  // namespace
@@ -909,6 +1119,17 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
     }
   }
 #undef CS_PICK
+  if (!grouped && !nv12 && tp == 1 && fast && g->grid_w == 32 && g->grid_h == 32 && P.vec_out &&
+      (reinterpret_cast<uintptr_t>(keep_mask) & 15u) == 0) {
+    // planar frames: band-staged TMA gather (runs of consecutive kept groups, 84 row copies per run)
+    const int nst = kBandMaxStages;
+    const size_t bsmem = (size_t)kBandWarps * nst * kBandStage;
+    const void* bf = reinterpret_cast<const void*>(compact_gather_band);
+    if (cs_set_smem_attr(bf, 22, static_cast<int>(bsmem))) return CS_ERR_CUDA;
+    compact_gather_band<<<cs_num_sms(), kBandWarps * 32, bsmem, stream>>>(P, nst);
+    if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+    return CS_OK;
+  }
   if (grouped && tp == 1 && fast && g->grid_w == 32 && g->grid_h % 2 == 0 && g->grid_h == 32 && P.vec_out) {
     {
       const int nst = 5;

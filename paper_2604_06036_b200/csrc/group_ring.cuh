@@ -41,8 +41,10 @@ struct RingBatch {
 };
 
 // Returns the packed rows this warp wrote (lane 0's count; capacity-clamped).
+// smask: a 16-B aligned per-warp shared buffer of 32 words (the current slot's keep mask, copied once per slot so
+// that walking its group rows costs no global-memory latency on the ring's critical path).
 CS_DEV long long group_ring(const RingBatch& B, long long q, long long q1, unsigned char* stages, int nst,
-                            uint64_t* full, RingGroup* desc, int lane) {
+                            uint64_t* full, RingGroup* desc, uint32_t* smask, int lane) {
   if (q >= q1) return 0;
   constexpr int kNgr = 16;
   const long long row_el = 3ll * 14 * 14;
@@ -56,14 +58,23 @@ CS_DEV long long group_ring(const RingBatch& B, long long q, long long q1, unsig
     return B.keep_mask + ((long long)s * B.mask_frame_stride + f) * 32;
   };
   auto load_row = [&]() {
-    const uint32_t* m = mask_of(slot);
-    const uint32_t x = m[2 * gr] | m[2 * gr + 1];
+    const uint32_t x = smask[2 * gr] | smask[2 * gr + 1];
     ybits = (x | (x >> 1)) & 0x55555555u;  // bit 2*gc set iff group (gr, gc) is kept
   };
   auto load_slot = [&]() {
     frame = static_cast<const uint16_t*>(B.frames[slot]);
     t_index = B.frame_index[slot];
     aligned = (reinterpret_cast<uintptr_t>(frame) & 15u) == 0;
+    const uint32_t* m = mask_of(slot);
+    if ((reinterpret_cast<uintptr_t>(m) & 15u) == 0) {
+      uint4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = reinterpret_cast<const uint4*>(m)[i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) reinterpret_cast<uint4*>(smask)[i] = v[i];
+    } else {
+      for (int i = 0; i < 32; ++i) smask[i] = m[i];
+    }
   };
   bool more = true;
   if (lane == 0) {

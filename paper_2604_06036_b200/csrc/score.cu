@@ -622,6 +622,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
       __syncthreads();
       __shared__ __align__(8) uint64_t s_gfull[kFusedMaxStages];
       __shared__ cs::RingGroup s_gdesc[kFusedMaxStages];
+      __shared__ __align__(16) uint32_t s_gmask[kThreads / 32][32];
       const int R = min(nthr >> 5, P.tma_stages / 3);  // ring warps of >= 3 stages each
       const int wq = tid >> 5;
       if (wq < R) {
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
         const long long NW = static_cast<long long>(gridDim.x) * R, gw = static_cast<long long>(blockIdx.x) * R + wq;
         const long long rows = cs::group_ring(B, T * gw / NW, T * (gw + 1) / NW,
                                               smem + P.off_stage + (size_t)wq * nst * cs::kRingStageAlloc, nst,
-                                              s_gfull + wq * nst, s_gdesc + wq * nst, lane);
+                                              s_gfull + wq * nst, s_gdesc + wq * nst, s_gmask[wq], lane);
         if (lane == 0) written = static_cast<int>(rows);
       }
     } else {

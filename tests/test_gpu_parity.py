@@ -1364,7 +1364,9 @@ def _random_avmv(ref, g, n_frames, rng):
         a["dst_y"] = rng.integers(-8, g["src_h"] + 8, size=n)
         a["motion_x"] = rng.integers(-40, 41, size=n)
         a["motion_y"] = rng.integers(-40, 41, size=n)
-        a["motion_scale"] = rng.choice([1, 2, 4], size=n)
+        a["motion_scale"] = rng.choice([1, 2, 4, 4, 4, 3, 8, 0], size=n)      # 4/2/1: shift path, else division
+        big = rng.random(n) < 0.01
+        a["motion_x"][big] = rng.integers(-40000, 40000, size=int(big.sum()))   # int16 clamp
         recs.append(a)
         offs.append(offs[-1] + n)
     return np.concatenate(recs), np.array(offs, np.int64)
