@@ -17,6 +17,7 @@
 #include "cs_internal.cuh"
 #include "group_ring.cuh"
 
+#include <algorithm>
 #include <memory>
 #include <vector>
 
@@ -267,6 +268,80 @@ __device__ __forceinline__ uint16_t norm_bf16(float a, float stdv, float rstd, b
   return cs::f32_to_bf16_cvt(q);
 }
 
+// One pair of output rows (yy0, yy0 + 1) of a kept group, fused NV12 preprocessing, lanes on output columns: the
+// 4 luma taps yv and 4 chroma pairs uvv of both rows (loaded by the caller from global or shared memory) -> the
+// model pixels of the lane's column, written into the warp's group tile (tcol = the column's tile base).  The two
+// output rows are the two halves of packed fp32 pairs (FADD2 / FMUL2 / FFMA2: one issue per pair, each half the same
+// IEEE operation as the oracle's); sums of products stay scalar per half (ptxas would fuse them into FFMA2,
+// cs_internal.cuh).  Bytes become floats exactly: float(2^23 + b) - (2^23 + 16) = b - 16 (PRMT + FADD).
+__device__ __forceinline__ void nv12_pair(const CompactParams& P, const uint32_t (&yv)[2][4], const uint32_t (&uvv)[2][4],
+                                          const float (&lyv)[2], float lx, float hx, uint16_t* tcol, int yy0,
+                                          bool store) {
+  constexpr int p = 14, pp = 196, G = 2, kNvRows = 2;
+  const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
+  constexpr float kBiasY = 8388624.0f, kBiasC = 8388736.0f;  // 2^23 + 16, 2^23 + 128
+  const float2 kY2 = make_float2(kY, kY), kRV2 = make_float2(kRV, kRV), kGU2 = make_float2(kGU, kGU);
+  const float2 kGV2 = make_float2(kGV, kGV), kBU2 = make_float2(kBU, kBU);
+  const float2 bY = make_float2(kBiasY, kBiasY), bC = make_float2(kBiasC, kBiasC);
+  auto bytes2 = [](uint32_t v0, uint32_t v1, uint32_t sel) {
+    return make_float2(__uint_as_float(__byte_perm(v0, 0x4B000000u, sel)),
+                       __uint_as_float(__byte_perm(v1, 0x4B000000u, sel)));
+  };
+  float2 rgb[4][3];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 d = cs::sub2(bytes2(uvv[0][q], uvv[1][q], 0x7540u), bC);
+    const float2 e = cs::sub2(bytes2(uvv[0][q], uvv[1][q], 0x7541u), bC);
+    const float2 yk = cs::mul2(kY2, cs::sub2(bytes2(yv[0][q], yv[1][q], 0x7540u), bY));
+    // sums of products: per-half scalar adds (cs::addp, never contracted), see cs_internal.cuh
+    rgb[q][0] = cs::clamp255_2(cs::addp(yk, cs::mul2(kRV2, e)));
+    rgb[q][1] = cs::clamp255_2(cs::subp(cs::subp(yk, cs::mul2(kGU2, d)), cs::mul2(kGV2, e)));
+    rgb[q][2] = cs::clamp255_2(cs::addp(yk, cs::mul2(kBU2, d)));
+  }
+  const float2 lx2 = make_float2(lx, lx), hx2 = make_float2(hx, hx);
+  const float2 ly2 = make_float2(lyv[0], lyv[1]);
+  const float2 hy2 = cs::sub2(make_float2(1.0f, 1.0f), ly2);
+  const float2 inv255 = make_float2(kInv255, kInv255), n255 = make_float2(255.0f, 255.0f);
+  float2 an[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float2 top = cs::addp(cs::mul2(hx2, rgb[0][c]), cs::mul2(lx2, rgb[1][c]));
+    const float2 bot = cs::addp(cs::mul2(hx2, rgb[2][c]), cs::mul2(lx2, rgb[3][c]));
+    const float2 v = cs::addp(cs::mul2(hy2, top), cs::mul2(ly2, bot));
+    // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
+    // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
+    const float2 q255 = cs::mul2(v, inv255);
+    const float2 res = cs::fma2(make_float2(-q255.x, -q255.y), n255, v);
+    const float2 t = cs::fma2(res, inv255, q255);
+    an[c] = cs::sub2(t, make_float2(P.mean[c], P.mean[c]));
+  }
+  // (t - mean) / std -> bf16 (norm_bf16), the six values' midpoint guards folded into one branch
+  float2 on[3];
+  uint32_t near_mid = 0u;
+  if (P.fast_div) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      on[c] = cs::mul2(an[c], make_float2(P.rstd[c], P.rstd[c]));
+      near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].x) & 0xffffu) - 0x7ff8u <= 16u);
+      near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].y) & 0xffffu) - 0x7ff8u <= 16u);
+    }
+  }
+  if (!P.fast_div || near_mid) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      on[c] = make_float2(__fdiv_rn(an[c].x, P.stdv[c]), __fdiv_rn(an[c].y, P.stdv[c]));
+  }
+  if (store) {
+#pragma unroll
+    for (int r = 0; r < kNvRows; ++r) {
+      const int yy = yy0 + r, dyp = yy >= p ? 1 : 0;
+      uint16_t* tq = tcol + dyp * G * 3 * pp + (yy - dyp * p) * p;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) tq[c * pp] = cs::f32_to_bf16_cvt(r == 0 ? on[c].x : on[c].y);
+    }
+  }
+}
+
 // Gather one kept group (gr, gc) of `frame` into the warp tile and write it to packed rows [n0, n0 + G^2).
 // TT = frames per token unit (temporal patch, NEXT-3); 0 = runtime P.tp.  With TT > 1 the packed row is
 // [3][TT][p][p] and tile element (patch q, c, f, y, x) sits at ((q*3 + c)*TT + f)*p*p + y*p + x.
@@ -407,10 +482,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
       const int dxp = xx >= p ? 1 : 0;
       uint16_t* tcol = tile + dxp * 3 * pp + (xx - dxp * p);
       const bool store = lane < gp;
-      constexpr float kBiasY = 8388624.0f, kBiasC = 8388736.0f;  // 2^23 + 16, 2^23 + 128
-      auto u8f = [](uint32_t v, uint32_t sel, float bias) {
-        return __fsub_rn(__uint_as_float(__byte_perm(v, 0x4B000000u, sel)), bias);
-      };
+      static_assert(kNvRows == 2, "nv12_pair: pairs of output rows");
       // per pair of output rows: its 16 loads are all issued before any is consumed (software-pipelining the next
       // pair's loads, or prefetching a group's source band into L2, measured slower: DESIGN §6)
       for (int yy0 = 0; yy0 < gp; yy0 += kNvRows) {
@@ -438,70 +510,7 @@ __device__ __forceinline__ void gather_group(const CompactParams& P, const uint1
             uvv[r][3] = uvv[r][1];
           }
         }
-        // the two output rows of the iteration as the two halves of packed fp32 pairs (FADD2 / FMUL2 / FFMA2: one
-        // issue per pair, each half the same IEEE operation as the scalar oracle's); sums of products stay scalar
-        // per half (ptxas would fuse them into FFMA2, cs_internal.cuh)
-        static_assert(kNvRows == 2, "the packed fp32 path pairs two output rows");
-        const float2 kY2 = make_float2(kY, kY), kRV2 = make_float2(kRV, kRV), kGU2 = make_float2(kGU, kGU);
-        const float2 kGV2 = make_float2(kGV, kGV), kBU2 = make_float2(kBU, kBU);
-        const float2 bY = make_float2(kBiasY, kBiasY), bC = make_float2(kBiasC, kBiasC);
-        auto bytes2 = [](uint32_t v0, uint32_t v1, uint32_t sel) {
-          return make_float2(__uint_as_float(__byte_perm(v0, 0x4B000000u, sel)),
-                             __uint_as_float(__byte_perm(v1, 0x4B000000u, sel)));
-        };
-        float2 rgb[4][3];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 d = cs::sub2(bytes2(uvv[0][q], uvv[1][q], 0x7540u), bC);
-          const float2 e = cs::sub2(bytes2(uvv[0][q], uvv[1][q], 0x7541u), bC);
-          const float2 yk = cs::mul2(kY2, cs::sub2(bytes2(yv[0][q], yv[1][q], 0x7540u), bY));
-          // sums of products: per-half scalar adds (cs::addp, never contracted), see cs_internal.cuh
-          rgb[q][0] = cs::clamp255_2(cs::addp(yk, cs::mul2(kRV2, e)));
-          rgb[q][1] = cs::clamp255_2(cs::subp(cs::subp(yk, cs::mul2(kGU2, d)), cs::mul2(kGV2, e)));
-          rgb[q][2] = cs::clamp255_2(cs::addp(yk, cs::mul2(kBU2, d)));
-        }
-        const float2 lx2 = make_float2(lx, lx), hx2 = make_float2(hx, hx);
-        const float2 ly2 = make_float2(lyv[0], lyv[1]);
-        const float2 hy2 = cs::sub2(make_float2(1.0f, 1.0f), ly2);
-        const float2 inv255 = make_float2(kInv255, kInv255), n255 = make_float2(255.0f, 255.0f);
-        float2 an[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const float2 top = cs::addp(cs::mul2(hx2, rgb[0][c]), cs::mul2(lx2, rgb[1][c]));
-          const float2 bot = cs::addp(cs::mul2(hx2, rgb[2][c]), cs::mul2(lx2, rgb[3][c]));
-          const float2 v = cs::addp(cs::mul2(hy2, top), cs::mul2(ly2, bot));
-          // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
-          // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
-          const float2 q255 = cs::mul2(v, inv255);
-          const float2 res = cs::fma2(make_float2(-q255.x, -q255.y), n255, v);
-          const float2 t = cs::fma2(res, inv255, q255);
-          an[c] = cs::sub2(t, make_float2(P.mean[c], P.mean[c]));
-        }
-        // (t - mean) / std -> bf16 (norm_bf16), the six values' midpoint guards folded into one branch
-        float2 on[3];
-        uint32_t near_mid = 0u;
-        if (P.fast_div) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            on[c] = cs::mul2(an[c], make_float2(P.rstd[c], P.rstd[c]));
-            near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].x) & 0xffffu) - 0x7ff8u <= 16u);
-            near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].y) & 0xffffu) - 0x7ff8u <= 16u);
-          }
-        }
-        if (!P.fast_div || near_mid) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            on[c] = make_float2(__fdiv_rn(an[c].x, P.stdv[c]), __fdiv_rn(an[c].y, P.stdv[c]));
-        }
-        if (store) {
-#pragma unroll
-          for (int r = 0; r < kNvRows; ++r) {
-            const int yy = yy0 + r, dyp = yy >= p ? 1 : 0;
-            uint16_t* tq = tcol + dyp * G * 3 * pp + (yy - dyp * p) * p;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) tq[c * pp] = cs::f32_to_bf16_cvt(r == 0 ? on[c].x : on[c].y);
-          }
-        }
+        nv12_pair(P, yv, uvv, lyv, lx, hx, tcol, yy0, store);
       }
     } else {
     // generic path: batches of 4 output pixels per lane: the 4 x (4 luma bytes + 4 chroma pairs) loads of a batch
@@ -708,15 +717,16 @@ __global__ void __launch_bounds__(kGatherThreads, (LAYOUT == CS_LAYOUT_GROUPED &
   }
 }
 
-// ---- planar CHW frames, 2x2 groups of 14-px patches on a 32 x 32 grid: band-staged TMA gather --------------
+// ---- planar CHW frames, 2x2 groups of 14-px patches on a 32 x 32 grid: band-staged gather --------------------
 // A kept group of a planar frame is 84 row segments of 56 B (3 channels x 28 rows) at 8-B alignment.  Fetched one
 // group at a time, every segment drags in the rest of its 128-B lines, which are only useful if the neighbouring
 // group is kept AND still cached when its turn comes (measured round 1: DRAM reads 3.2x the algorithmic bytes,
 // 0.41 of the roofline).  Here a warp takes RUNS of up to kBandRun consecutive kept groups of one group row (the
 // packed order puts them in consecutive rows) and stages the run's band -- for each of the 84 source rows the one
-// contiguous span covering all of the run's groups, widened to 16-B alignment -- with 84 cp.async.bulk copies
-// into a stage of its TMA ring (mbarrier complete_tx), so each source line is requested once, by one copy, while
-// the next runs' copies are in flight.  The warp then writes each group's 4,704 output bytes with 16-B stores,
+// contiguous span covering all of the run's groups, widened to 16-B alignment -- into a stage of its ring with 16-B
+// asynchronous copies (cp.async, commit / wait groups), so each source line is requested once, by one warp, while
+// the next run's copies are in flight.  (1-D bulk copies, one per row span, were measured 2-4 % slower: 84
+// requests per run keep the TMA unit busy.)  The warp then writes each group's 4,704 output bytes with 16-B stores,
 // every 16-B chunk assembled from four 4-B pixel pairs of the staged rows (a pair never straddles a 14-px patch
 // row) through a per-CTA table of staged-row offsets.
 #ifndef CS_BAND_RUN
@@ -742,7 +752,6 @@ __global__ void __launch_bounds__(kBandWarps * 32, 1) compact_gather_band(const 
                                                                           int nst) {
   extern __shared__ __align__(128) unsigned char b_smem[];
   __shared__ BandRun s_run[kBandWarps][kBandMaxStages];
-  __shared__ __align__(8) uint64_t s_full[kBandWarps][kBandMaxStages];
   __shared__ uint4 s_tab[294];  // per 16-B output chunk of a group: 4 pixel pairs -> (staged row, byte) as u16 pairs
   __shared__ __align__(16) uint32_t s_mask[kBandWarps][32];  // the current slot's keep mask (lane 0's generator)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -767,7 +776,6 @@ __global__ void __launch_bounds__(kBandWarps * 32, 1) compact_gather_band(const 
   const long long q1 = total_groups * (wid + 1) / nwarps;
   if (q >= q1) return;
   unsigned char* stages = b_smem + (size_t)wib * nst * kBandStage;
-  uint64_t* full = s_full[wib];
   BandRun* runs = s_run[wib];
 
   // ---- generator (lane 0): slot, group row, remaining kept-group bits of the row -------------------------------
@@ -807,8 +815,6 @@ __global__ void __launch_bounds__(kBandWarps * 32, 1) compact_gather_band(const 
       load_row();
     }
     for (; skip > 0; --skip) ybits &= ybits - 1u;
-    for (int st = 0; st < nst; ++st) cs::mbar_init(&full[st], 1);
-    cs::fence_mbar_init();
   }
   __syncwarp();
   bool more = true;  // (lane 0)
@@ -845,24 +851,23 @@ __global__ void __launch_bounds__(kBandWarps * 32, 1) compact_gather_band(const 
         bytes = static_cast<uint32_t>(((r.lead + k * 56) + 15) & ~15);  // per row, 16-B multiple
         q += k;
         runs[st] = r;
-        cs::mbar_arrive_expect_tx(&full[st], 84u * bytes);
       }
-      if (r.k == 0) {
-        runs[st].k = 0;
-        cs::mbar_arrive(&full[st]);
-      }
+      if (r.k == 0) runs[st].k = 0;
     }
     __syncwarp();
     bytes = __shfl_sync(0xffffffffu, bytes, 0);
-    if (bytes) {
+    if (bytes) {  // the 84 row spans as 16-B asynchronous copies spread over the lanes
       const BandRun rr = runs[st];
       const unsigned char* base = reinterpret_cast<const unsigned char*>(rr.row0) - rr.lead;
-      for (int row = lane; row < 84; row += 32) {
+      const int nch = static_cast<int>(bytes >> 4);
+      unsigned char* sb = stages + (size_t)st * kBandStage;
+      for (int e = lane; e < 84 * nch; e += 32) {
+        const int row = e / nch, ch = e - row * nch;
         const int c = row / 28, y = row - c * 28;
-        cs::bulk_g2s(stages + (size_t)st * kBandStage + row * kBandRowBytes,
-                     base + (c * plane + (long long)y * FW) * 2, bytes, &full[st]);
+        cs::cp_async16(sb + row * kBandRowBytes + ch * 16, base + (c * plane + (long long)y * FW) * 2 + ch * 16);
       }
     }
+    cs::cp_async_commit();  // one (possibly empty) group per issued item keeps the wait count uniform
   };
   for (int st = 0; st < nst; ++st) {
     const bool m = __shfl_sync(0xffffffffu, more ? 1 : 0, 0);
@@ -871,7 +876,8 @@ __global__ void __launch_bounds__(kBandWarps * 32, 1) compact_gather_band(const 
   }
   for (int it = 0;; ++it) {
     const int st = it % nst;
-    cs::mbar_wait(&full[st], (it / nst) & 1);
+    cs::cp_async_wait<kBandMaxStages - 1>();  // this lane's copies of item `it` have landed (nst == kBandMaxStages)
+    __syncwarp();                             // ... and every lane's
     const BandRun r = runs[st];
     if (r.k == 0) break;
     const unsigned char* stg = stages + (size_t)st * kBandStage;
@@ -1121,8 +1127,8 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
 #undef CS_PICK
   if (!grouped && !nv12 && tp == 1 && fast && g->grid_w == 32 && g->grid_h == 32 && P.vec_out &&
       (reinterpret_cast<uintptr_t>(keep_mask) & 15u) == 0) {
-    // planar frames: band-staged TMA gather (runs of consecutive kept groups, 84 row copies per run)
-    const int nst = kBandMaxStages;
+    // planar frames: band-staged gather (runs of consecutive kept groups, their 84 row spans staged with cp.async)
+    const int nst = kBandMaxStages;  // (the cp.async wait count assumes exactly kBandMaxStages stages)
     const size_t bsmem = (size_t)kBandWarps * nst * kBandStage;
     const void* bf = reinterpret_cast<const void*>(compact_gather_band);
     if (cs_set_smem_attr(bf, 22, static_cast<int>(bsmem))) return CS_ERR_CUDA;

@@ -74,6 +74,18 @@ template <int N>
 CS_DEV void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+// Ampere-style asynchronous 16-B copy global -> shared (LDGSTS; src and dst 16-B aligned), tracked per thread by
+// commit / wait groups.  Many small row segments: one instruction moves 512 B per warp, where a 1-D bulk copy per
+// segment pays the TMA unit's per-request cost (measured).
+CS_DEV void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+CS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+CS_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 CS_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -1,7 +1,7 @@
 # planar band gather geometry sweep (compile-time macros): C4 planar compaction time
 O=gpurun_out/band; mkdir -p $O
 SRCS=$(ls paper_2604_06036_b200/csrc/*.cu)
-for v in "3 7 2" "3 6 2" "2 10 2"; do
+for v in "3 7 2" "5 5 2" "7 4 2" "3 6 3"; do
   set -- $v
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -I include \
     -DCS_BAND_RUN=$1 -DCS_BAND_WARPS=$2 -DCS_BAND_STAGES=$3 -o paper_2604_06036_b200/libcodecsight.so $SRCS > $O/build_$1_$2_$3.log 2>&1 || { echo "build $v failed"; continue; }
