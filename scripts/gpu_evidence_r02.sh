@@ -1,6 +1,6 @@
 # Round-2 evidence for the current code: smoke, all GPU tests, every bench line, ncu launch lists and full captures
 # of the hot kernels, the multi-rank (shared GPU, gloo) strong-scaling path.  Outputs in gpurun_out/ev2/.
-O=gpurun_out/ev2; mkdir -p $O
+O=${EV_OUT:-gpurun_out/ev3}; mkdir -p $O
 nproc > $O/host.txt; grep -m1 "model name" /proc/cpuinfo >> $O/host.txt
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,driver_version --format=csv > $O/gpu_info.txt
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo build rc=$?
@@ -19,6 +19,7 @@ run c4_tp2 --temporal-patch 2 --no-cpu-baseline
 run c4_mrope --rope mrope --no-cpu-baseline
 run c4_copy --kv-mode copy --no-cpu-baseline
 run c4_planar --frame-layout planar --no-fused --no-cpu-baseline
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"compact_" --csv --log-file $O/ncu_launches_C4planar.csv python bench.py --frame-layout planar --no-fused --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --quiet > /dev/null 2>$O/l_planar.err; echo l planar rc=$?
 run c4_graphs --graphs --no-cpu-baseline
 run cdf --workload cdf --steps 20
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 --cpu-seconds 6 > $O/bench_ref.json 2> $O/bench_ref.err; echo ref rc=$?
