@@ -61,6 +61,7 @@ struct CompactParams {
   float scale_y, scale_x;  // src / model, fp32 (computed once on the host, IEEE division)
   float mean[3], stdv[3];
   float rstd[3];  // RN(1 / std[c]) (host IEEE division)
+  float one, negone;  // 1.0f / -1.0f: the uncontractable packed add / subtract (cs::add1 / cs::sub1)
   int fast_div;   // every std in [2^-20, 2^20]: bf16((t - mean) / std) through the guarded reciprocal (norm_bf16)
   const void* const* uv_planes;
   const uint32_t* keep_mask;
@@ -270,14 +271,14 @@ __device__ __forceinline__ uint16_t norm_bf16(float a, float stdv, float rstd, b
 
 // One pair of output rows (yy0, yy0 + 1) of a kept group, fused NV12 preprocessing, lanes on output columns: the
 // 4 luma taps yv and 4 chroma pairs uvv of both rows (loaded by the caller from global or shared memory) -> the
-// model pixels of the lane's column, written into the warp's group tile (tcol = the column's tile base).  The two
-// output rows are the two halves of packed fp32 pairs (FADD2 / FMUL2 / FFMA2: one issue per pair, each half the same
-// IEEE operation as the oracle's); sums of products stay scalar per half (ptxas would fuse them into FFMA2,
-// cs_internal.cuh).  Bytes become floats exactly: float(2^23 + b) - (2^23 + 16) = b - 16 (PRMT + FADD).
-__device__ __forceinline__ void nv12_pair(const CompactParams& P, const uint32_t (&yv)[2][4], const uint32_t (&uvv)[2][4],
-                                          const float (&lyv)[2], float lx, float hx, uint16_t* tcol, int yy0,
-                                          bool store) {
-  constexpr int p = 14, pp = 196, G = 2, kNvRows = 2;
+// normalised fp32 model pixels of the lane's column (on[c] = (row yy0, row yy0 + 1) of channel c, before the bf16
+// rounding).  The two output rows are the two halves of packed fp32 pairs (FADD2 / FMUL2 / FFMA2: one issue per
+// pair, each half the same IEEE operation as the oracle's); a sum of products is an FFMA2 with a runtime 1.0
+// (cs::add1: ptxas would contract a plain packed add into the product, cs_internal.cuh).  Bytes become floats
+// exactly: float(2^23 + b) - (2^23 + 16) = b - 16 (PRMT + FADD).
+__device__ __forceinline__ void nv12_pair_px(const CompactParams& P, const uint32_t (&yv)[2][4],
+                                             const uint32_t (&uvv)[2][4], const float (&lyv)[2], float lx, float hx,
+                                             float2 (&on)[3]) {
   const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
   constexpr float kBiasY = 8388624.0f, kBiasC = 8388736.0f;  // 2^23 + 16, 2^23 + 128
   const float2 kY2 = make_float2(kY, kY), kRV2 = make_float2(kRV, kRV), kGU2 = make_float2(kGU, kGU);
@@ -287,16 +288,18 @@ __device__ __forceinline__ void nv12_pair(const CompactParams& P, const uint32_t
     return make_float2(__uint_as_float(__byte_perm(v0, 0x4B000000u, sel)),
                        __uint_as_float(__byte_perm(v1, 0x4B000000u, sel)));
   };
+  // sums / differences of products: FFMA2 with the runtime 1.0 (cs::add1 / cs::sub1, never contracted)
+  const float2 one = make_float2(P.one, P.one), neg = make_float2(P.negone, P.negone);
   float2 rgb[4][3];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const float2 d = cs::sub2(bytes2(uvv[0][q], uvv[1][q], 0x7540u), bC);
     const float2 e = cs::sub2(bytes2(uvv[0][q], uvv[1][q], 0x7541u), bC);
     const float2 yk = cs::mul2(kY2, cs::sub2(bytes2(yv[0][q], yv[1][q], 0x7540u), bY));
-    // sums of products: per-half scalar adds (cs::addp, never contracted), see cs_internal.cuh
-    rgb[q][0] = cs::clamp255_2(cs::addp(yk, cs::mul2(kRV2, e)));
-    rgb[q][1] = cs::clamp255_2(cs::subp(cs::subp(yk, cs::mul2(kGU2, d)), cs::mul2(kGV2, e)));
-    rgb[q][2] = cs::clamp255_2(cs::addp(yk, cs::mul2(kBU2, d)));
+    // the sums are never NaN or -0.0 (integer-valued c, d, e; x + (-x) = +0 in RN): the one-instruction clamp
+    rgb[q][0] = cs::clamp255_relu2(cs::add1(yk, cs::mul2(kRV2, e), one));
+    rgb[q][1] = cs::clamp255_relu2(cs::sub1(cs::sub1(yk, cs::mul2(kGU2, d), neg), cs::mul2(kGV2, e), neg));
+    rgb[q][2] = cs::clamp255_relu2(cs::add1(yk, cs::mul2(kBU2, d), one));
   }
   const float2 lx2 = make_float2(lx, lx), hx2 = make_float2(hx, hx);
   const float2 ly2 = make_float2(lyv[0], lyv[1]);
@@ -305,9 +308,9 @@ __device__ __forceinline__ void nv12_pair(const CompactParams& P, const uint32_t
   float2 an[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    const float2 top = cs::addp(cs::mul2(hx2, rgb[0][c]), cs::mul2(lx2, rgb[1][c]));
-    const float2 bot = cs::addp(cs::mul2(hx2, rgb[2][c]), cs::mul2(lx2, rgb[3][c]));
-    const float2 v = cs::addp(cs::mul2(hy2, top), cs::mul2(ly2, bot));
+    const float2 top = cs::add1(cs::mul2(hx2, rgb[0][c]), cs::mul2(lx2, rgb[1][c]), one);
+    const float2 bot = cs::add1(cs::mul2(hx2, rgb[2][c]), cs::mul2(lx2, rgb[3][c]), one);
+    const float2 v = cs::add1(cs::mul2(hy2, top), cs::mul2(ly2, bot), one);
     // v / 255 correctly rounded without a division: q = v * RN(1/255), one fma residual correction.
     // Exhaustively verified equal to IEEE v / 255 for every fp32 v in [0, 512] (scripts/check_div255.c)
     const float2 q255 = cs::mul2(v, inv255);
@@ -316,7 +319,6 @@ __device__ __forceinline__ void nv12_pair(const CompactParams& P, const uint32_t
     an[c] = cs::sub2(t, make_float2(P.mean[c], P.mean[c]));
   }
   // (t - mean) / std -> bf16 (norm_bf16), the six values' midpoint guards folded into one branch
-  float2 on[3];
   uint32_t near_mid = 0u;
   if (P.fast_div) {
 #pragma unroll
@@ -331,6 +333,15 @@ __device__ __forceinline__ void nv12_pair(const CompactParams& P, const uint32_t
     for (int c = 0; c < 3; ++c)
       on[c] = make_float2(__fdiv_rn(an[c].x, P.stdv[c]), __fdiv_rn(an[c].y, P.stdv[c]));
   }
+}
+
+// nv12_pair_px, then the bf16 pixels into the warp's group tile (tcol = the lane column's tile base)
+__device__ __forceinline__ void nv12_pair(const CompactParams& P, const uint32_t (&yv)[2][4], const uint32_t (&uvv)[2][4],
+                                          const float (&lyv)[2], float lx, float hx, uint16_t* tcol, int yy0,
+                                          bool store) {
+  constexpr int p = 14, pp = 196, G = 2, kNvRows = 2;
+  float2 on[3];
+  nv12_pair_px(P, yv, uvv, lyv, lx, hx, on);
   if (store) {
 #pragma unroll
     for (int r = 0; r < kNvRows; ++r) {
@@ -959,6 +970,249 @@ __global__ void __launch_bounds__(kGatherThreads, 1) compact_gather_tma(const __
                  t_smem + (size_t)wib * nst * kTmaStageAlloc, nst, s_full[wib], s_desc[wib], s_mask[wib], lane);
 }
 
+// ---- fused NV12 preprocessing, source rows staged in shared memory (NEXT-2; 2x2 groups of 14-px patches) -------
+// The work is a flat sequence of ITEMS per warp: item = one pair of output rows (2i, 2i + 1) of one kept group,
+// 14 items per group, the warp's kept groups in packed order.  An item reads 8 source rows: the luma tap rows
+// y0(r), y1(r) of its two output rows r and the chroma rows y0(r)/2, y1(r)/2, each over the group's column span
+// [xs, xs + 16 nch) (xs = the group's first luma tap rounded down to 16 B; nch 16-B chunks cover the span of the
+// last column's taps, luma and chroma alike).  Lane l copies row l/4, chunks (l%4) + 4m, with 16-B cp.async into a
+// stage of the warp's ring; the copies of item t + kNvsAhead are issued before item t is computed, across group
+// boundaries (the next group comes from the warp's kept-group enumeration when the producer reaches it).  The
+// compute is the LDG path's (lanes on the group's 28 output columns, nv12_pair_px) with every tap one shared-memory
+// load at a per-lane constant offset and no 64-bit index arithmetic; the bf16 pixels go straight to the packed rows
+// (a patch row of 14 px = 28 B per channel and row; the two rows of an item are adjacent, so sectors fill in L2).
+// Row taps / weights come from a per-CTA table (one nv12_axis per model row, computed once per launch).
+// Requires pitches that are multiples of 16; a slot whose planes are not 16-B aligned is staged with byte copies.
+constexpr int kNvsWarps = 8;
+constexpr int kNvsAhead = 2;                  // items in flight ahead of the one being computed
+constexpr int kNvsStages = kNvsAhead + 1;     // ring stages per warp
+constexpr int kNvsItems = 14;                 // items (output row pairs) per 28-row group
+
+struct NvsGroup {  // a kept group of the warp's range (warp-uniform)
+  long long n0;    // first packed row
+  const uint8_t* Y;
+  const uint8_t* UV;
+  int slot, gr, gc;
+};
+
+template <int RB>  // staged row pitch in bytes (16 * max chunks: 144 covers scale_x <= 4.6, 256 up to 8.6)
+__global__ void __launch_bounds__(kNvsWarps * 32, 3) compact_nv12_staged(const __grid_constant__ CompactParams P,
+                                                                         int nch) {
+  constexpr int p = 14, gp = 28, row_el = 588, kStage = 8 * RB;
+  extern __shared__ __align__(128) unsigned char n_smem[];
+  __shared__ NvsGroup s_grp[kNvsWarps][2];
+  __shared__ __align__(16) uint32_t s_mask[kNvsWarps][64];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* stages = n_smem + (size_t)wib * kNvsStages * kStage;
+  uint32_t* s_y01 = reinterpret_cast<uint32_t*>(n_smem + (size_t)kNvsWarps * kNvsStages * kStage);
+  float* s_ly = reinterpret_cast<float*>(s_y01 + P.FH);
+  for (int o = threadIdx.x; o < P.FH; o += blockDim.x) {
+    int y0, y1;
+    float ly;
+    nv12_axis(o, P.src_h, P.scale_y, y0, y1, ly);
+    s_y01[o] = static_cast<uint32_t>(y0) | (static_cast<uint32_t>(y1) << 16);
+    s_ly[o] = ly;
+  }
+  __syncthreads();
+
+  const long long total_groups = static_cast<long long>(__ldg(P.frame_offsets + P.n_slots)) / 4;
+  const long long nwarps = static_cast<long long>(gridDim.x) * kNvsWarps;
+  const long long wid = static_cast<long long>(blockIdx.x) * kNvsWarps + wib;
+  long long q = total_groups * wid / nwarps;
+  const long long q1 = total_groups * (wid + 1) / nwarps;
+  if (q >= q1) return;
+  uint32_t* mask = s_mask[wib];
+
+  // ---- the warp's kept-group enumeration (producer side): slot, 32-group chunk `base`, its remaining ballot bits
+  int g_slot, g_base = 0;
+  uint32_t g_bal = 0u;
+  auto load_mask = [&](int slot) {
+    __syncwarp();
+    for (int t = lane; t < P.nw; t += 32) mask[t] = __ldg(slot_mask(P, slot) + t);
+    __syncwarp();
+  };
+  auto ballot_chunk = [&]() {
+    const int qq = g_base + lane;
+    const bool kept = qq < P.ngroups && cs::group_kept(mask, qq, P.ngc, 2, P.grid_w);
+    g_bal = __ballot_sync(0xffffffffu, kept);
+  };
+  {
+    int lo = 0, hi = P.n_slots;  // largest slot with frame_offsets[slot] <= q * 4
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (static_cast<long long>(__ldg(P.frame_offsets + mid)) <= q * 4) lo = mid; else hi = mid;
+    }
+    g_slot = lo;
+    long long skip = q - __ldg(P.frame_offsets + g_slot) / 4;  // kept groups of the slot before q
+    load_mask(g_slot);
+    ballot_chunk();
+    while (skip >= __popc(g_bal)) {  // the slot holds more than `skip` kept groups
+      skip -= __popc(g_bal);
+      g_base += 32;
+      ballot_chunk();
+    }
+    for (; skip > 0; --skip) g_bal &= g_bal - 1u;
+  }
+  auto next_group = [&]() -> NvsGroup {
+    while (g_bal == 0u) {
+      g_base += 32;
+      if (g_base >= P.ngroups) {
+        g_base = 0;
+        ++g_slot;
+        load_mask(g_slot);
+      }
+      ballot_chunk();
+    }
+    const int gi = g_base + __ffs(g_bal) - 1;
+    g_bal &= g_bal - 1u;
+    NvsGroup d;
+    d.n0 = q * 4;
+    ++q;
+    d.slot = g_slot;
+    d.gr = gi / P.ngc;
+    d.gc = gi - d.gr * P.ngc;
+    d.Y = static_cast<const uint8_t*>(P.frames[g_slot]);
+    d.UV = static_cast<const uint8_t*>(P.uv_planes[g_slot]);
+    return d;
+  };
+  // the group's column span start (16-B aligned), identical on the producer and consumer sides
+  auto span_start = [&](int gc) {
+    int x0, x1;
+    float lx;
+    nv12_axis(gc * gp, P.src_w, P.scale_x, x0, x1, lx);
+    return x0 & ~15;
+  };
+
+  // ---- producer state (lane: staged row k = lane / 4, chunks cl + 4m)
+  const int k = lane >> 2, cl = lane & 3;
+  const long long pitch_k = k < 4 ? P.y_pitch : P.uv_pitch;
+  const uint8_t* p_src = nullptr;  // this lane's first chunk in source row 0 of the plane
+  uint32_t p_valid = 0u;           // chunks m this lane copies
+  bool p_aligned = true;
+  int p_gr = 0;
+  auto produce_group = [&](const NvsGroup& d) {
+    const int xs = span_start(d.gc);
+    p_src = (k < 4 ? d.Y : d.UV) + xs + 16 * cl;
+    p_valid = 0u;
+#pragma unroll
+    for (int m = 0; m < RB / 64 + 1; ++m) {
+      const int c = cl + 4 * m;
+      if (c < nch && xs + 16 * c < pitch_k) p_valid |= 1u << m;
+    }
+    p_aligned = ((reinterpret_cast<uintptr_t>(d.Y) | reinterpret_cast<uintptr_t>(d.UV)) & 15u) == 0;
+    p_gr = d.gr;
+  };
+  auto produce_item = [&](int i, unsigned char* sb) {
+    const int r = p_gr * gp + 2 * i + ((k >> 1) & 1);
+    const uint32_t yy = s_y01[r];
+    const int y = static_cast<int>((k & 1) ? (yy >> 16) : (yy & 0xffffu)) >> (k >> 2);
+    const uint8_t* src = p_src + (long long)y * pitch_k;
+    unsigned char* dst = sb + k * RB + 16 * cl;
+    if (p_aligned) {
+#pragma unroll
+      for (int m = 0; m < RB / 64 + 1; ++m)
+        if ((p_valid >> m) & 1u) cs::cp_async16(dst + 64 * m, src + 64 * m);
+    } else {
+#pragma unroll 1
+      for (int m = 0; m < RB / 64 + 1; ++m)
+        if ((p_valid >> m) & 1u)
+          for (int b = 0; b < 16; ++b) dst[64 * m + b] = __ldg(src + 64 * m + b);
+    }
+  };
+
+  // ---- consumer state (lane: output column xx of the group)
+  const int xx = lane < gp ? lane : gp - 1;
+  const int dx = xx >= p ? 1 : 0, xin = xx - dx * p;
+  int c_ox0 = 0, c_ox1 = 0, c_cx0 = 0, c_cx1 = 0;  // tap offsets in a staged luma / chroma row
+  float c_lx = 0.0f, c_hx = 0.0f;
+  uint16_t* c_out = nullptr;  // this lane's column in the group's packed row (patch dx), channel 0, row 0
+  NvsGroup cur{};
+
+  // flat item counters (32-bit, warp-uniform): producer item / stage, consumer item / stage / group parity
+  int pi = 0, ps = 0, pg = 0;
+  auto produce = [&]() {
+    if (pi == 0) {
+      const NvsGroup d = next_group();
+      if (lane == 0) s_grp[wib][pg & 1] = d;
+      ++pg;
+      produce_group(d);
+    }
+    produce_item(pi, stages + ps * kStage);
+    pi = pi == kNvsItems - 1 ? 0 : pi + 1;
+    ps = ps == kNvsStages - 1 ? 0 : ps + 1;
+  };
+  const int T = static_cast<int>(q1 - q) * kNvsItems;
+  for (int u = 0; u < kNvsAhead; ++u) {  // exactly kNvsAhead groups, empty past the end (wait count)
+    if (u < T) produce();
+    cs::cp_async_commit();
+  }
+  int i = 0, st = 0, cgp = 0;
+  const unsigned char* wst = stages;  // this warp's ring
+  for (int t = 0; t < T; ++t) {
+    __syncwarp();  // every lane is done with the stage item t + kNvsAhead reuses (item t - 1's)
+    if (t + kNvsAhead < T) produce();
+    cs::cp_async_commit();  // one (possibly empty) group per item keeps the wait count uniform
+    cs::cp_async_wait<kNvsAhead>();
+    __syncwarp();  // item t's rows (copied by all lanes) and its group descriptor are visible
+    if (i == 0) {
+      cur = s_grp[wib][cgp];
+      cgp ^= 1;
+      int x0, x1;
+      nv12_axis(cur.gc * gp + xx, P.src_w, P.scale_x, x0, x1, c_lx);
+      c_hx = __fsub_rn(1.0f, c_lx);
+      const int xs = span_start(cur.gc);
+      c_ox0 = x0 - xs;
+      c_ox1 = x1 - xs;
+      c_cx0 = 2 * (x0 >> 1) - xs;
+      c_cx1 = 2 * (x1 >> 1) - xs;
+      c_out = P.packed + (cur.n0 + dx) * row_el + xin;
+    }
+    const unsigned char* sb = wst + st * kStage;
+    uint32_t yv[2][4], uvv[2][4];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const unsigned char* ry0 = sb + (2 * r) * RB;
+      const unsigned char* ry1 = sb + (2 * r + 1) * RB;
+      const unsigned char* rc0 = sb + (4 + 2 * r) * RB;
+      const unsigned char* rc1 = sb + (5 + 2 * r) * RB;
+      yv[r][0] = ry0[c_ox0];
+      yv[r][1] = ry0[c_ox1];
+      yv[r][2] = ry1[c_ox0];
+      yv[r][3] = ry1[c_ox1];
+      uvv[r][0] = *reinterpret_cast<const uint16_t*>(rc0 + c_cx0);
+      uvv[r][1] = *reinterpret_cast<const uint16_t*>(rc0 + c_cx1);
+      uvv[r][2] = *reinterpret_cast<const uint16_t*>(rc1 + c_cx0);
+      uvv[r][3] = *reinterpret_cast<const uint16_t*>(rc1 + c_cx1);
+    }
+    const int r0 = cur.gr * gp + 2 * i;
+    const float lyv[2] = {s_ly[r0], s_ly[r0 + 1]};
+    float2 on[3];
+    nv12_pair_px(P, yv, uvv, lyv, c_lx, c_hx, on);
+    const int dy = 2 * i >= p ? 1 : 0, y = 2 * i - dy * p;
+    if (lane < gp && cur.n0 + 2 * dy + dx < P.capacity) {
+      uint16_t* o = c_out + dy * 2 * row_el + y * p;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        o[c * p * p] = cs::f32_to_bf16_cvt(on[c].x);
+        o[c * p * p + p] = cs::f32_to_bf16_cvt(on[c].y);
+      }
+    }
+    if (i == kNvsItems - 1 && lane < 4) {
+      const long long n = cur.n0 + lane;
+      if (n < P.capacity) {
+        const int h = cur.gr * 2 + (lane >> 1), w = cur.gc * 2 + (lane & 1);
+        P.pos_ids[3 * n + 0] = __ldg(P.frame_index + cur.slot);
+        P.pos_ids[3 * n + 1] = h;
+        P.pos_ids[3 * n + 2] = w;
+        P.src_index[n] = cur.slot * P.np + h * P.grid_w + w;
+      }
+    }
+    i = i == kNvsItems - 1 ? 0 : i + 1;
+    st = st == kNvsStages - 1 ? 0 : st + 1;
+  }
+  cs::cp_async_wait<0>();
+}
+
 }  // namespace
 
 // model coordinate o -> its two source taps along an axis (the device's nv12_axis, in the same fp32 operations)
@@ -1063,6 +1317,8 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
     P.scale_y = static_cast<float>(pre->src_h) / static_cast<float>(P.FH);
     P.scale_x = static_cast<float>(pre->src_w) / static_cast<float>(P.FW);
     P.fast_div = 1;
+    P.one = 1.0f;
+    P.negone = -1.0f;
     for (int c = 0; c < 3; ++c) {
       P.mean[c] = pre->mean[c];
       P.stdv[c] = pre->std[c];
@@ -1143,6 +1399,34 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
       const void* tf = reinterpret_cast<const void*>(compact_gather_tma);
       if (cs_set_smem_attr(tf, 20, 200 * 1024)) return CS_ERR_CUDA;  // + 2.5 KB static <= 227 KB
       compact_gather_tma<<<cs_num_sms(), kGatherThreads, tsmem, stream>>>(P, nst);
+      if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
+      return CS_OK;
+    }
+  }
+  if (nv12 && tp == 1 && fast && P.y_pitch % 16 == 0 && P.uv_pitch % 16 == 0 && P.nw <= 64) {
+    // staged fused preprocessing: the widest column span of a group (16-B chunks, luma and chroma) picks the
+    // staged row pitch
+    int nch = 0;
+    for (int gc = 0; gc < P.ngc; ++gc) {
+      int a, b, c, d;
+      host_axis(gc * 28, P.src_w, P.scale_x, &a, &b);
+      host_axis(gc * 28 + 27, P.src_w, P.scale_x, &c, &d);
+      const int xs = a & ~15;
+      nch = std::max(nch, ((2 * (d >> 1) + 1 - xs) >> 4) + 1);
+    }
+    if (nch <= 16) {
+      const int rb = nch <= 9 ? 144 : 256;
+      const size_t nsmem = (size_t)kNvsWarps * kNvsStages * 8 * rb + (size_t)P.FH * 8;
+      const void* sf = rb == 144 ? reinterpret_cast<const void*>(compact_nv12_staged<144>)
+                                 : reinterpret_cast<const void*>(compact_nv12_staged<256>);
+      if (cs_set_smem_attr(sf, rb == 144 ? 23 : 24, static_cast<int>(nsmem))) return CS_ERR_CUDA;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sf, kNvsWarps * 32, nsmem) != cudaSuccess ||
+          per_sm < 1)
+        per_sm = 1;
+      const int ngrid = cs_num_sms() * per_sm;
+      if (rb == 144) compact_nv12_staged<144><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P, nch);
+      else compact_nv12_staged<256><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P, nch);
       if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
       return CS_OK;
     }

@@ -159,8 +159,23 @@ CS_DEV float2 fma2(float2 a, float2 b, float2 c) {
 }
 CS_DEV float2 addp(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
 CS_DEV float2 subp(float2 a, float2 b) { return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y)); }
+// Packed sum / difference in ONE issue that ptxas cannot contract: FFMA2 with a multiplier of exactly 1.0 that
+// ptxas cannot see (`one` = a kernel parameter set to 1.0f / -1.0f on the host).  a * 1 and b * -1 are exact, so
+// the single rounding of the fma is the IEEE sum / difference; and a product feeding it stays a separately rounded
+// FMUL2 (the FFMA2 already spends its multiply on `one`).  Same bits as addp / subp, half the fma-pipe issues.
+CS_DEV float2 add1(float2 a, float2 b, float2 one) { return fma2(a, one, b); }
+CS_DEV float2 sub1(float2 a, float2 b, float2 negone) { return fma2(b, negone, a); }
 CS_DEV float2 clamp255_2(float2 a) {
   return make_float2(fminf(fmaxf(a.x, 0.0f), 255.0f), fminf(fmaxf(a.y, 0.0f), 255.0f));
+}
+// clamp to [0, 255] in one ALU instruction per half (VIMNMX.RELU on the bit patterns): for non-negative floats the
+// signed-int order of the bits is the float order, a negative float is a negative int (relu -> +0.0f).  Equal to
+// clamp255_2 for every non-NaN input except -0.0f (-> +0.0f instead of -0.0f); callers guarantee no NaN / -0.0f.
+CS_DEV float2 clamp255_relu2(float2 a) {
+  int x, y;
+  asm("min.relu.s32 %0, %1, %2;" : "=r"(x) : "r"(__float_as_int(a.x)), "r"(0x437F0000));
+  asm("min.relu.s32 %0, %1, %2;" : "=r"(y) : "r"(__float_as_int(a.y)), "r"(0x437F0000));
+  return make_float2(__int_as_float(x), __int_as_float(y));
 }
 
 // fp32 -> bf16 bits, round to nearest even, one cvt.rn.bf16.f32 (equal to f32_to_bf16_rne for every non-NaN f)

@@ -1348,6 +1348,62 @@ def test_compact_nv12(abi, ref, geom, norm):
         assert (cnt.cpu().numpy().view(np.uint64) == o["counters"]).all()
 
 
+@pytest.mark.parametrize("case", ["pitch8", "misaligned", "wide_span", "one_group", "ragged_cap"])
+def test_compact_nv12_paths(abi, ref, case):
+    """The launcher's NV12 paths beyond test_compact_nv12's: pitches that are not multiples of 16 (direct-load
+    path), planes off 16-B alignment (staged path, byte-copied stages), a column span wider than 16 chunks (scale
+    17: direct-load path), a batch with a single kept group (the staged ring's prologue / tail), and a capacity
+    that ends inside a group."""
+    sw, sh, gw, gh = 1920, 1080, 32, 32
+    pitch = sw + 64
+    if case == "pitch8":
+        pitch = sw + 8
+    if case == "wide_span":
+        gw = gh = 8
+    g = make_grid(sw, sh, patch=14, group=2, grid_w=gw, grid_h=gh)
+    rng = np.random.default_rng(77)
+    S, n = 2, 2
+    nw = abi.grid_words(g)
+    km = rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
+    km &= rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
+    if case == "one_group":
+        km[:] = 0
+        km[1, 1, 5] = 1 << 9
+    off = 1 if case == "misaligned" else 0
+    ys = [rng.integers(16, 236, size=(sh, pitch), dtype=np.uint8) for _ in range(S * n)]
+    uvs = [rng.integers(16, 241, size=(sh // 2, pitch), dtype=np.uint8) for _ in range(S * n)]
+    pre_h = ref.make_pre(sw, sh, pitch, pitch)
+    pre = dict(src_w=sw, src_h=sh, y_pitch=pitch, uv_pitch=pitch)
+    fidx = np.arange(S * n, dtype=np.int32) + 3
+    cap = S * n * gw * gh if case != "ragged_cap" else 4 * 37 + 3
+    # misaligned: each plane is a view 1 byte into its allocation
+    y_d = [torch.from_numpy(np.concatenate([np.zeros(off, np.uint8), a.ravel()])).to(DEV)[off:] for a in ys]
+    uv_d = [torch.from_numpy(np.concatenate([np.zeros(off, np.uint8), a.ravel()])).to(DEV)[off:] for a in uvs]
+    if off:
+        assert all(t.data_ptr() % 16 for t in y_d)
+    km_d = torch.from_numpy(km.view(np.int32)).to(DEV)
+    packed = torch.full((cap, 3 * 14 * 14), -1, dtype=torch.int16, device=DEV)
+    pos = torch.zeros(cap, 3, dtype=torch.int32, device=DEV)
+    src = torch.zeros(cap, dtype=torch.int32, device=DEV)
+    offs = torch.zeros(S * n + 1, dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(16, dtype=torch.int64, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    abi.codecsight_compact_nv12(g, pre, S, n, km_d, n, torch.from_numpy(fidx).to(DEV), abi.ptr_array(y_d, DEV),
+                                abi.ptr_array(uv_d, DEV), cap, packed, pos, src, offs, cnt, st)
+    o = ref.compact_nv12(g, pre_h, km, fidx, ys, uvs, cap, S, n)
+    torch.cuda.synchronize()
+    rows = min(int(o["frame_offsets"][-1]), cap)
+    assert rows > 0
+    assert int(st.item()) == o["status"]
+    assert (offs.cpu().numpy() == o["frame_offsets"]).all()
+    assert (pos.cpu().numpy()[:rows] == o["pos_ids"][:rows]).all()
+    assert (src.cpu().numpy()[:rows] == o["src_index"][:rows]).all()
+    got = packed.cpu().numpy().view(np.uint16)
+    assert (got[:rows] == o["packed"][:rows]).all(), int((got[:rows] != o["packed"][:rows]).sum())
+    assert (got[rows:] == 0xFFFF).all()   # nothing written past the packed rows / the capacity
+    assert (cnt.cpu().numpy().view(np.uint64) == o["counters"]).all()
+
+
 # ------------------------------------------------------------------------------------------------------------
 # NEXT-4: AVMotionVector rasterisation and the similar-patch histogram
 # ------------------------------------------------------------------------------------------------------------
