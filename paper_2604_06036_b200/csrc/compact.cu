@@ -18,6 +18,7 @@
 #include "group_ring.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <memory>
 #include <vector>
 
@@ -121,8 +122,13 @@ __global__ void __launch_bounds__(kCountThreads) compact_count(const __grid_cons
                                                                 const __grid_constant__ NvSrcClasses C) {
   __shared__ uint32_t s_m[kCountThreads / 32][128];  // per-warp unit mask (grid_words <= 128)
   __shared__ unsigned long long s_k[kCountThreads / 32][64];  // NV12 source count: kept group columns per group row
+  __shared__ NvClass s_rc[kNvMaxRowClasses];  // the row classes (lane-indexed: constant-bank reads would serialise)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = blockIdx.x * (kCountThreads / 32) + warp;
+  if (C.enabled) {
+    for (int i = threadIdx.x; i < C.n_rows; i += kCountThreads) s_rc[i] = C.rows[i];
+    __syncthreads();
+  }
   if (slot >= P.n_slots) return;
   if (C.enabled) {
     const uint32_t* m = slot_mask(P, slot);
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(kCountThreads) compact_count(const __grid_cons
     __syncwarp();
     unsigned long long sectors = 0ull;
     for (int i = lane; i < C.n_rows; i += 32) {
-      const NvClass rc = C.rows[i];
+      const NvClass rc = s_rc[i];
       unsigned long long K = 0ull;
       for (unsigned long long b = rc.mask; b; b &= b - 1) K |= s_k[warp][__ffsll(static_cast<long long>(b)) - 1];
       unsigned long long cols = 0ull;
@@ -276,9 +282,9 @@ __device__ __forceinline__ uint16_t norm_bf16(float a, float stdv, float rstd, b
 // pair, each half the same IEEE operation as the oracle's); a sum of products is an FFMA2 with a runtime 1.0
 // (cs::add1: ptxas would contract a plain packed add into the product, cs_internal.cuh).  Bytes become floats
 // exactly: float(2^23 + b) - (2^23 + 16) = b - 16 (PRMT + FADD).
-__device__ __forceinline__ void nv12_pair_px(const CompactParams& P, const uint32_t (&yv)[2][4],
+__device__ __forceinline__ void nv12_pair_an(const CompactParams& P, const uint32_t (&yv)[2][4],
                                              const uint32_t (&uvv)[2][4], const float (&lyv)[2], float lx, float hx,
-                                             float2 (&on)[3]) {
+                                             float2 (&an)[3]) {
   const float kY = 1.164383f, kRV = 1.596027f, kGU = 0.391762f, kGV = 0.812968f, kBU = 2.017232f;
   constexpr float kBiasY = 8388624.0f, kBiasC = 8388736.0f;  // 2^23 + 16, 2^23 + 128
   const float2 kY2 = make_float2(kY, kY), kRV2 = make_float2(kRV, kRV), kGU2 = make_float2(kGU, kGU);
@@ -305,7 +311,6 @@ __device__ __forceinline__ void nv12_pair_px(const CompactParams& P, const uint3
   const float2 ly2 = make_float2(lyv[0], lyv[1]);
   const float2 hy2 = cs::sub2(make_float2(1.0f, 1.0f), ly2);
   const float2 inv255 = make_float2(kInv255, kInv255), n255 = make_float2(255.0f, 255.0f);
-  float2 an[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const float2 top = cs::add1(cs::mul2(hx2, rgb[0][c]), cs::mul2(lx2, rgb[1][c]), one);
@@ -318,21 +323,31 @@ __device__ __forceinline__ void nv12_pair_px(const CompactParams& P, const uint3
     const float2 t = cs::fma2(res, inv255, q255);
     an[c] = cs::sub2(t, make_float2(P.mean[c], P.mean[c]));
   }
-  // (t - mean) / std -> bf16 (norm_bf16), the six values' midpoint guards folded into one branch
-  uint32_t near_mid = 0u;
-  if (P.fast_div) {
+}
+
+// (t - mean) / std -> bf16 (norm_bf16) for a pair's six values through the guarded reciprocal: on = an * RN(1/std);
+// returns nonzero when any product lies within 8 fp32 steps of a bf16 rounding midpoint (or fast_div is off), in
+// which case the caller takes nv12_norm_exact for it (one branch for any number of pairs).
+__device__ __forceinline__ uint32_t nv12_norm_fast(const CompactParams& P, const float2 (&an)[3], float2 (&on)[3]) {
+  uint32_t near_mid = P.fast_div ? 0u : 1u;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      on[c] = cs::mul2(an[c], make_float2(P.rstd[c], P.rstd[c]));
-      near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].x) & 0xffffu) - 0x7ff8u <= 16u);
-      near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].y) & 0xffffu) - 0x7ff8u <= 16u);
-    }
+  for (int c = 0; c < 3; ++c) {
+    on[c] = cs::mul2(an[c], make_float2(P.rstd[c], P.rstd[c]));
+    near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].x) & 0xffffu) - 0x7ff8u <= 16u);
+    near_mid |= static_cast<uint32_t>((__float_as_uint(on[c].y) & 0xffffu) - 0x7ff8u <= 16u);
   }
-  if (!P.fast_div || near_mid) {
+  return near_mid;
+}
+__device__ __forceinline__ void nv12_norm_exact(const CompactParams& P, const float2 (&an)[3], float2 (&on)[3]) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      on[c] = make_float2(__fdiv_rn(an[c].x, P.stdv[c]), __fdiv_rn(an[c].y, P.stdv[c]));
-  }
+  for (int c = 0; c < 3; ++c) on[c] = make_float2(__fdiv_rn(an[c].x, P.stdv[c]), __fdiv_rn(an[c].y, P.stdv[c]));
+}
+__device__ __forceinline__ void nv12_pair_px(const CompactParams& P, const uint32_t (&yv)[2][4],
+                                             const uint32_t (&uvv)[2][4], const float (&lyv)[2], float lx, float hx,
+                                             float2 (&on)[3]) {
+  float2 an[3];
+  nv12_pair_an(P, yv, uvv, lyv, lx, hx, an);
+  if (nv12_norm_fast(P, an, on)) nv12_norm_exact(P, an, on);
 }
 
 // nv12_pair_px, then the bf16 pixels into the warp's group tile (tcol = the lane column's tile base)
@@ -983,10 +998,23 @@ __global__ void __launch_bounds__(kGatherThreads, 1) compact_gather_tma(const __
 // (a patch row of 14 px = 28 B per channel and row; the two rows of an item are adjacent, so sectors fill in L2).
 // Row taps / weights come from a per-CTA table (one nv12_axis per model row, computed once per launch).
 // Requires pitches that are multiples of 16; a slot whose planes are not 16-B aligned is staged with byte copies.
-constexpr int kNvsWarps = 8;
-constexpr int kNvsAhead = 2;                  // items in flight ahead of the one being computed
-constexpr int kNvsStages = kNvsAhead + 1;     // ring stages per warp
-constexpr int kNvsItems = 14;                 // items (output row pairs) per 28-row group
+#ifndef CS_NVS_MINB
+#define CS_NVS_MINB 1  // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef CS_NVS_UNROLL
+#define CS_NVS_UNROLL 1  // unroll of the 7-pair loop
+#endif
+#define CS_PRAGMA_(x) _Pragma(#x)
+#define CS_PRAGMA(x) CS_PRAGMA_(x)
+#ifndef CS_NVS_WARPS
+#define CS_NVS_WARPS 16
+#endif
+#ifndef CS_NVS_STAGES
+#define CS_NVS_STAGES 3
+#endif
+constexpr int kNvsWarps = CS_NVS_WARPS;
+constexpr int kNvsStages = CS_NVS_STAGES;  // ring stages per warp (kNvsStages - 1 pairs in flight)
+constexpr int kNvsPairs = 7;  // item pairs (4 output rows) per 28-row group; a ring stage holds one pair
 
 struct NvsGroup {  // a kept group of the warp's range (warp-uniform)
   long long n0;    // first packed row
@@ -996,21 +1024,23 @@ struct NvsGroup {  // a kept group of the warp's range (warp-uniform)
 };
 
 template <int RB>  // staged row pitch in bytes (16 * max chunks: 144 covers scale_x <= 4.6, 256 up to 8.6)
-__global__ void __launch_bounds__(kNvsWarps * 32, 3) compact_nv12_staged(const __grid_constant__ CompactParams P,
-                                                                         int nch) {
-  constexpr int p = 14, gp = 28, row_el = 588, kStage = 8 * RB;
+__global__ void __launch_bounds__(kNvsWarps * 32, CS_NVS_MINB) compact_nv12_staged(const __grid_constant__ CompactParams P) {
+  constexpr int p = 14, gp = 28, row_el = 588, kItem = 8 * RB, kStage = 2 * kItem;
   extern __shared__ __align__(128) unsigned char n_smem[];
-  __shared__ NvsGroup s_grp[kNvsWarps][2];
   __shared__ __align__(16) uint32_t s_mask[kNvsWarps][64];
+  __shared__ NvsGroup s_grp[kNvsWarps][2];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned char* stages = n_smem + (size_t)wib * kNvsStages * kStage;
+  // per model row o: luma tap rows y0 | y1 << 16, chroma rows (y0 / 2) | (y1 / 2) << 16, the weight ly
   uint32_t* s_y01 = reinterpret_cast<uint32_t*>(n_smem + (size_t)kNvsWarps * kNvsStages * kStage);
-  float* s_ly = reinterpret_cast<float*>(s_y01 + P.FH);
+  uint32_t* s_c01 = s_y01 + P.FH;
+  float* s_ly = reinterpret_cast<float*>(s_c01 + P.FH);
   for (int o = threadIdx.x; o < P.FH; o += blockDim.x) {
     int y0, y1;
     float ly;
     nv12_axis(o, P.src_h, P.scale_y, y0, y1, ly);
     s_y01[o] = static_cast<uint32_t>(y0) | (static_cast<uint32_t>(y1) << 16);
+    s_c01[o] = static_cast<uint32_t>(y0 >> 1) | (static_cast<uint32_t>(y1 >> 1) << 16);
     s_ly[o] = ly;
   }
   __syncthreads();
@@ -1083,132 +1113,149 @@ __global__ void __launch_bounds__(kNvsWarps * 32, 3) compact_nv12_staged(const _
     return x0 & ~15;
   };
 
-  // ---- producer state (lane: staged row k = lane / 4, chunks cl + 4m)
+  // ---- producer (lane: staged row k = lane / 4 of each item, chunks cl + 4m; rows 0-3 luma, 4-7 chroma)
   const int k = lane >> 2, cl = lane & 3;
-  const long long pitch_k = k < 4 ? P.y_pitch : P.uv_pitch;
-  const uint8_t* p_src = nullptr;  // this lane's first chunk in source row 0 of the plane
-  uint32_t p_valid = 0u;           // chunks m this lane copies
+  const uint32_t p_pitch = static_cast<uint32_t>(k < 4 ? P.y_pitch : P.uv_pitch);
+  const uint32_t p_sel = (k & 1) ? 0x4432u : 0x4410u;  // PRMT: the y1 / y0 half of a row-table entry
+  const uint32_t p_dst = cs::smem_u32(stages) + k * RB + 16 * cl;
+  const uint8_t* p_src = nullptr;  // this lane's first chunk in source row 0 of its plane
+  const uint32_t* p_tab = nullptr; // the lane's row-table entry of item 0 of the producer's group
+  int p_nch = 0;                   // 16-B chunks of the group's span
   bool p_aligned = true;
-  int p_gr = 0;
   auto produce_group = [&](const NvsGroup& d) {
-    const int xs = span_start(d.gc);
+    int x0, x1, xa, xb;
+    float l;
+    nv12_axis(d.gc * gp, P.src_w, P.scale_x, x0, x1, l);
+    nv12_axis(d.gc * gp + gp - 1, P.src_w, P.scale_x, xa, xb, l);
+    const int xs = x0 & ~15;
+    p_nch = ((2 * (xb >> 1) + 1 - xs) >> 4) + 1;  // the host sized RB for the widest group (<= RB / 16)
     p_src = (k < 4 ? d.Y : d.UV) + xs + 16 * cl;
-    p_valid = 0u;
-#pragma unroll
-    for (int m = 0; m < RB / 64 + 1; ++m) {
-      const int c = cl + 4 * m;
-      if (c < nch && xs + 16 * c < pitch_k) p_valid |= 1u << m;
-    }
+    p_tab = (k < 4 ? s_y01 : s_c01) + d.gr * gp + ((k >> 1) & 1);
     p_aligned = ((reinterpret_cast<uintptr_t>(d.Y) | reinterpret_cast<uintptr_t>(d.UV)) & 15u) == 0;
-    p_gr = d.gr;
   };
-  auto produce_item = [&](int i, unsigned char* sb) {
-    const int r = p_gr * gp + 2 * i + ((k >> 1) & 1);
-    const uint32_t yy = s_y01[r];
-    const int y = static_cast<int>((k & 1) ? (yy >> 16) : (yy & 0xffffu)) >> (k >> 2);
-    const uint8_t* src = p_src + (long long)y * pitch_k;
-    unsigned char* dst = sb + k * RB + 16 * cl;
+  // items j and j + 7 (patch rows dy = 0 and 1) of the producer's group into the stage at byte offset soff of the
+  // warp's ring
+  auto produce_pair = [&](int j, uint32_t soff) {
+    uint32_t y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) y[h] = __byte_perm(p_tab[2 * j + 14 * h], 0u, p_sel);
     if (p_aligned) {
 #pragma unroll
-      for (int m = 0; m < RB / 64 + 1; ++m)
-        if ((p_valid >> m) & 1u) cs::cp_async16(dst + 64 * m, src + 64 * m);
+      for (int h = 0; h < 2; ++h) {
+        const uint8_t* src = p_src + y[h] * p_pitch;
+        const uint32_t dst = p_dst + soff + h * kItem;
+#pragma unroll
+        for (int m = 0; m < RB / 64 + 1; ++m) cs::cp_async16_if(dst + 64 * m, src + 64 * m, cl + 4 * m < p_nch);
+      }
     } else {
-#pragma unroll 1
-      for (int m = 0; m < RB / 64 + 1; ++m)
-        if ((p_valid >> m) & 1u)
-          for (int b = 0; b < 16; ++b) dst[64 * m + b] = __ldg(src + 64 * m + b);
+      for (int h = 0; h < 2; ++h) {
+        const uint8_t* src = p_src + y[h] * p_pitch;
+        unsigned char* d8 = stages + (p_dst - cs::smem_u32(stages)) + soff + h * kItem;
+        for (int m = 0; m < RB / 64 + 1; ++m)
+          if (cl + 4 * m < p_nch)
+            for (int b = 0; b < 16; ++b) d8[64 * m + b] = __ldg(src + 64 * m + b);
+      }
     }
   };
 
-  // ---- consumer state (lane: output column xx of the group)
-  const int xx = lane < gp ? lane : gp - 1;
-  const int dx = xx >= p ? 1 : 0, xin = xx - dx * p;
-  int c_ox0 = 0, c_ox1 = 0, c_cx0 = 0, c_cx1 = 0;  // tap offsets in a staged luma / chroma row
-  float c_lx = 0.0f, c_hx = 0.0f;
-  uint16_t* c_out = nullptr;  // this lane's column in the group's packed row (patch dx), channel 0, row 0
-  NvsGroup cur{};
-
-  // flat item counters (32-bit, warp-uniform): producer item / stage, consumer item / stage / group parity
-  int pi = 0, ps = 0, pg = 0;
-  auto produce = [&]() {
-    if (pi == 0) {
+  // ---- producer sequence: pair pj of the producer's current group into ring stage ps; a new group is fetched
+  // (and its descriptor published in s_grp[wib][pg & 1]) when pj wraps.  The producer runs kNvsStages - 1 pairs
+  // ahead of the consumer, i.e. at most one group ahead.
+  long long p_left = q1 - q;  // groups the producer has yet to fetch
+  int pj = 0, ps = 0, pg = 0;
+  auto produce_next = [&]() {
+    if (pj == 0) {
+      if (p_left == 0) return;
+      --p_left;
       const NvsGroup d = next_group();
       if (lane == 0) s_grp[wib][pg & 1] = d;
       ++pg;
       produce_group(d);
     }
-    produce_item(pi, stages + ps * kStage);
-    pi = pi == kNvsItems - 1 ? 0 : pi + 1;
+    produce_pair(pj, static_cast<uint32_t>(ps * kStage));
+    pj = pj == kNvsPairs - 1 ? 0 : pj + 1;
     ps = ps == kNvsStages - 1 ? 0 : ps + 1;
   };
-  const int T = static_cast<int>(q1 - q) * kNvsItems;
-  for (int u = 0; u < kNvsAhead; ++u) {  // exactly kNvsAhead groups, empty past the end (wait count)
-    if (u < T) produce();
-    cs::cp_async_commit();
+
+  // ---- consumer (lane: output column xx of the group)
+  const int xx = lane < gp ? lane : gp - 1;
+  const int dx = xx >= p ? 1 : 0, xin = xx - dx * p;
+  const long long n_groups = q1 - q;
+  for (int u = 0; u < kNvsStages - 1; ++u) {
+    produce_next();
+    cs::cp_async_commit();  // one (possibly empty) group per pair keeps the wait count uniform
   }
-  int i = 0, st = 0, cgp = 0;
-  const unsigned char* wst = stages;  // this warp's ring
-  for (int t = 0; t < T; ++t) {
-    __syncwarp();  // every lane is done with the stage item t + kNvsAhead reuses (item t - 1's)
-    if (t + kNvsAhead < T) produce();
-    cs::cp_async_commit();  // one (possibly empty) group per item keeps the wait count uniform
-    cs::cp_async_wait<kNvsAhead>();
-    __syncwarp();  // item t's rows (copied by all lanes) and its group descriptor are visible
-    if (i == 0) {
-      cur = s_grp[wib][cgp];
-      cgp ^= 1;
-      int x0, x1;
-      nv12_axis(cur.gc * gp + xx, P.src_w, P.scale_x, x0, x1, c_lx);
-      c_hx = __fsub_rn(1.0f, c_lx);
-      const int xs = span_start(cur.gc);
-      c_ox0 = x0 - xs;
-      c_ox1 = x1 - xs;
-      c_cx0 = 2 * (x0 >> 1) - xs;
-      c_cx1 = 2 * (x1 >> 1) - xs;
-      c_out = P.packed + (cur.n0 + dx) * row_el + xin;
-    }
-    const unsigned char* sb = wst + st * kStage;
-    uint32_t yv[2][4], uvv[2][4];
+  int cs_ = 0;  // ring stage of the pair being computed
+  for (long long g = 0; g < n_groups; ++g) {
+    __syncwarp();  // the group's descriptor (published at least one pair ago) is visible
+    const NvsGroup& dg = s_grp[wib][g & 1];
+    const long long n0 = dg.n0;
+    const int slot = dg.slot, gr = dg.gr, gc = dg.gc;
+    int x0, x1;
+    float lx;
+    nv12_axis(gc * gp + xx, P.src_w, P.scale_x, x0, x1, lx);
+    const float hx = __fsub_rn(1.0f, lx);
+    const int xs = span_start(gc);
+    const int ox0 = x0 - xs, ox1 = x1 - xs, cx0 = 2 * (x0 >> 1) - xs, cx1 = 2 * (x1 >> 1) - xs;
+    uint16_t* out = P.packed + (n0 + dx) * row_el + xin;  // this lane's column, patch row dy = 0
+    const bool st[2] = {lane < gp && n0 + dx < P.capacity, lane < gp && n0 + 2 + dx < P.capacity};
+    const float* lyp = s_ly + gr * gp;
+    CS_PRAGMA(unroll CS_NVS_UNROLL)
+    for (int j = 0; j < kNvsPairs; ++j) {
+      cs::cp_async_wait<kNvsStages - 2>();  // this lane's copies of pair j have landed
+      __syncwarp();  // ... and every lane's; every lane is done with the stage the next copies go to (pair j - 1's)
+      produce_next();
+      cs::cp_async_commit();
+      const uint32_t J = static_cast<uint32_t>(cs_ * kStage);
+      cs_ = cs_ == kNvsStages - 1 ? 0 : cs_ + 1;
+      const unsigned char* sb = stages + J;
+      float2 an[2][3], on[2][3];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const unsigned char* ry0 = sb + (2 * r) * RB;
-      const unsigned char* ry1 = sb + (2 * r + 1) * RB;
-      const unsigned char* rc0 = sb + (4 + 2 * r) * RB;
-      const unsigned char* rc1 = sb + (5 + 2 * r) * RB;
-      yv[r][0] = ry0[c_ox0];
-      yv[r][1] = ry0[c_ox1];
-      yv[r][2] = ry1[c_ox0];
-      yv[r][3] = ry1[c_ox1];
-      uvv[r][0] = *reinterpret_cast<const uint16_t*>(rc0 + c_cx0);
-      uvv[r][1] = *reinterpret_cast<const uint16_t*>(rc0 + c_cx1);
-      uvv[r][2] = *reinterpret_cast<const uint16_t*>(rc1 + c_cx0);
-      uvv[r][3] = *reinterpret_cast<const uint16_t*>(rc1 + c_cx1);
-    }
-    const int r0 = cur.gr * gp + 2 * i;
-    const float lyv[2] = {s_ly[r0], s_ly[r0 + 1]};
-    float2 on[3];
-    nv12_pair_px(P, yv, uvv, lyv, c_lx, c_hx, on);
-    const int dy = 2 * i >= p ? 1 : 0, y = 2 * i - dy * p;
-    if (lane < gp && cur.n0 + 2 * dy + dx < P.capacity) {
-      uint16_t* o = c_out + dy * 2 * row_el + y * p;
+      for (int h = 0; h < 2; ++h) {  // item j + 7h: output rows 2j, 2j + 1 of patch row dy = h
+        const unsigned char* ib = sb + h * kItem;
+        uint32_t yv[2][4], uvv[2][4];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        o[c * p * p] = cs::f32_to_bf16_cvt(on[c].x);
-        o[c * p * p + p] = cs::f32_to_bf16_cvt(on[c].y);
+        for (int r = 0; r < 2; ++r) {
+          const unsigned char* ry0 = ib + (2 * r) * RB;
+          const unsigned char* ry1 = ib + (2 * r + 1) * RB;
+          const unsigned char* rc0 = ib + (4 + 2 * r) * RB;
+          const unsigned char* rc1 = ib + (5 + 2 * r) * RB;
+          yv[r][0] = ry0[ox0];
+          yv[r][1] = ry0[ox1];
+          yv[r][2] = ry1[ox0];
+          yv[r][3] = ry1[ox1];
+          uvv[r][0] = *reinterpret_cast<const uint16_t*>(rc0 + cx0);
+          uvv[r][1] = *reinterpret_cast<const uint16_t*>(rc0 + cx1);
+          uvv[r][2] = *reinterpret_cast<const uint16_t*>(rc1 + cx0);
+          uvv[r][3] = *reinterpret_cast<const uint16_t*>(rc1 + cx1);
+        }
+        const float2 ly = *reinterpret_cast<const float2*>(lyp + 2 * j + 14 * h);
+        const float lyv[2] = {ly.x, ly.y};
+        nv12_pair_an(P, yv, uvv, lyv, lx, hx, an[h]);
       }
+      if (nv12_norm_fast(P, an[0], on[0]) | nv12_norm_fast(P, an[1], on[1])) {
+        nv12_norm_exact(P, an[0], on[0]);
+        nv12_norm_exact(P, an[1], on[1]);
+      }
+      uint16_t* o = out + 28 * j;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          cs::st_b16_if(o + h * 2 * row_el + c * p * p, cs::f32_to_bf16_cvt(on[h][c].x), st[h]);
+          cs::st_b16_if(o + h * 2 * row_el + c * p * p + p, cs::f32_to_bf16_cvt(on[h][c].y), st[h]);
+        }
     }
-    if (i == kNvsItems - 1 && lane < 4) {
-      const long long n = cur.n0 + lane;
+    if (lane < 4) {
+      const long long n = n0 + lane;
       if (n < P.capacity) {
-        const int h = cur.gr * 2 + (lane >> 1), w = cur.gc * 2 + (lane & 1);
-        P.pos_ids[3 * n + 0] = __ldg(P.frame_index + cur.slot);
+        const int h = gr * 2 + (lane >> 1), w = gc * 2 + (lane & 1);
+        P.pos_ids[3 * n + 0] = __ldg(P.frame_index + slot);
         P.pos_ids[3 * n + 1] = h;
         P.pos_ids[3 * n + 2] = w;
-        P.src_index[n] = cur.slot * P.np + h * P.grid_w + w;
+        P.src_index[n] = slot * P.np + h * P.grid_w + w;
       }
     }
-    i = i == kNvsItems - 1 ? 0 : i + 1;
-    st = st == kNvsStages - 1 ? 0 : st + 1;
   }
   cs::cp_async_wait<0>();
 }
@@ -1403,7 +1450,8 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
       return CS_OK;
     }
   }
-  if (nv12 && tp == 1 && fast && P.y_pitch % 16 == 0 && P.uv_pitch % 16 == 0 && P.nw <= 64) {
+  if (nv12 && tp == 1 && fast && P.y_pitch % 16 == 0 && P.uv_pitch % 16 == 0 && P.nw <= 64 &&
+      static_cast<long long>(std::max(P.y_pitch, P.uv_pitch)) * P.src_h < (1ll << 31)) {
     // staged fused preprocessing: the widest column span of a group (16-B chunks, luma and chroma) picks the
     // staged row pitch
     int nch = 0;
@@ -1416,21 +1464,31 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
     }
     if (nch <= 16) {
       const int rb = nch <= 9 ? 144 : 256;
-      const size_t nsmem = (size_t)kNvsWarps * kNvsStages * 8 * rb + (size_t)P.FH * 8;
+      const size_t nsmem = (size_t)kNvsWarps * kNvsStages * 16 * rb + (size_t)P.FH * 12;
+      if (nsmem > 200 * 1024) goto nv12_direct;  // (a tall model input with the widest span: direct loads)
       const void* sf = rb == 144 ? reinterpret_cast<const void*>(compact_nv12_staged<144>)
                                  : reinterpret_cast<const void*>(compact_nv12_staged<256>);
-      if (cs_set_smem_attr(sf, rb == 144 ? 23 : 24, static_cast<int>(nsmem))) return CS_ERR_CUDA;
+      if (cs_set_smem_attr(sf, rb == 144 ? 23 : 24, 220 * 1024)) return CS_ERR_CUDA;
+      static std::atomic<int> carveout_done[2];
+      if (!carveout_done[rb == 144 ? 0 : 1].load(std::memory_order_acquire)) {
+        // 4 CTAs x ~44 KB: ask for the largest shared-memory carveout (the kernel reads nothing through L1 twice)
+        if (cudaFuncSetAttribute(sf, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+          return CS_ERR_CUDA;
+        carveout_done[rb == 144 ? 0 : 1].store(1, std::memory_order_release);
+      }
       int per_sm = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sf, kNvsWarps * 32, nsmem) != cudaSuccess ||
           per_sm < 1)
         per_sm = 1;
       const int ngrid = cs_num_sms() * per_sm;
-      if (rb == 144) compact_nv12_staged<144><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P, nch);
-      else compact_nv12_staged<256><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P, nch);
+      if (rb == 144) compact_nv12_staged<144><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P);
+      else compact_nv12_staged<256><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P);
       if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;
       return CS_OK;
     }
   }
+nv12_direct:
   if (cs_set_smem_attr(fn, slot, 227 * 1024)) return CS_ERR_CUDA;
   void* args[] = {&P};
   if (cudaLaunchKernel(fn, dim3(grid), dim3(kGatherThreads), args, smem, stream) != cudaSuccess) return CS_ERR_CUDA;

@@ -80,6 +80,19 @@ CS_DEV void bulk_wait_all() {
 CS_DEV void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// predicated form (no branch around the copy): dst is a shared-space address (smem_u32)
+CS_DEV void cp_async16_if(uint32_t dst, const void* src, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(dst),
+      "l"(src), "r"(static_cast<int>(pred))
+      : "memory");
+}
+// predicated 2-B global store (no branch around it)
+CS_DEV void st_b16_if(void* p, uint16_t v, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.b16 [%0], %1;\n}" ::"l"(p), "h"(v),
+               "r"(static_cast<int>(pred))
+               : "memory");
+}
 CS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 CS_DEV void cp_async_wait() {

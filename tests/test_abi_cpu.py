@@ -49,6 +49,9 @@ def test_sass_keeps_the_bulk_copy_pipelines(abi):
         if name != "void score_kernel<false>":     # (the unfused score kernel is off the default path)
             assert v["stack"] == 0, (name, v)      # no local-memory spills in the hot kernels
     assert ks["compact_gather_band"]["LDGSTS"] >= 1 and ks["compact_gather_band"]["stack"] == 0  # planar: cp.async
+    for rb in (144, 256):  # fused NV12 preprocessing: source rows staged with cp.async, no spills
+        v = ks["void compact_nv12_staged<%d>" % rb]
+        assert v["LDGSTS"] >= 2 and v["stack"] == 0 and v["local"] == 0, (rb, v)
 
 
 FAKE = 0x1000  # never dereferenced: validation fails (or the device check does) before any launch
