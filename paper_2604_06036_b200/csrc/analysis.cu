@@ -74,36 +74,68 @@ __global__ void __launch_bounds__(kThreads) mv_rasterize(int mb, int cols, int r
 }
 
 // The same arbitration with the frame's keys in shared memory (grids up to kSmemMbs MBs: 1080p's 8,160 MBs are 65 KB):
-// shared-memory atomics instead of L2 atomics, and the output written once, coalesced.
+// shared-memory atomics instead of L2 atomics, and the output written once, coalesced.  Each record's quarter-pel
+// vector is also kept in shared memory (the frame's first kQCap records), so decoding a winner reads no global
+// memory; MB_SHIFT > 0: the MB size is 1 << MB_SHIFT (H.264: 16) and the partition -> MB range is two shifts.
 constexpr int kSmemMbs = 12288;
 constexpr int kRastThreads = 1024;  // the per-thread record loop and the winner decode are latency chains: wide CTAs
-__global__ void __launch_bounds__(kRastThreads) mv_rasterize_smem(int mb, int cols, int rows,
-                                                               const cs_av_mv* __restrict__ mvs,
-                                                               const long long* __restrict__ offs, cs_mb* out) {
+template <int MB_SHIFT>
+__global__ void __launch_bounds__(kRastThreads, 1) mv_rasterize_smem(int mb, int cols, int rows,
+                                                                  const cs_av_mv* __restrict__ mvs,
+                                                                  const long long* __restrict__ offs, cs_mb* out,
+                                                                  int qcap) {
   extern __shared__ unsigned long long s_key[];
+  uint32_t* s_q = reinterpret_cast<uint32_t*>(s_key + rows * cols);  // (qx & 0xffff) | qy << 16 per record
   const int f = blockIdx.x;
   const int n_mb = rows * cols;
   for (int e = threadIdx.x; e < n_mb; e += blockDim.x) s_key[e] = 0ull;
   __syncthreads();
   const long long r0 = offs[f], r1 = offs[f + 1];
-  for (long long r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    const cs_av_mv m = mvs[r];
-    if (m.source >= 0) continue;
-    const int x0 = static_cast<int>(m.dst_x) - m.w / 2, y0 = static_cast<int>(m.dst_y) - m.h / 2;
-    const int x1 = x0 + m.w, y1 = y0 + m.h;  // [x0, x1) x [y0, y1)
+  // a record's fields as four 8-B loads (bytes 0-15: source, w, h, src, dst; 24-31: motion; 32-39: scale; the
+  // flags word is never read), the next record's loads in flight while this one is arbitrated
+  struct Rec {
+    uint2 a, b, c, d;
+  };
+  auto load = [&](long long r) {
+    const uint2* p = reinterpret_cast<const uint2*>(mvs + r);
+    return Rec{__ldg(p), __ldg(p + 1), __ldg(p + 3), __ldg(p + 4)};
+  };
+  long long r = r0 + threadIdx.x;
+  Rec cur{};
+  if (r < r1) cur = load(r);
+  for (; r < r1; r += blockDim.x) {
+    Rec nxt{};
+    if (r + blockDim.x < r1) nxt = load(r + blockDim.x);
+    const Rec m = cur;
+    cur = nxt;
+    if (static_cast<int>(m.a.x) >= 0) continue;  // source: past references only
+    const int w = m.a.y & 0xffu, h = (m.a.y >> 8) & 0xffu;
+    const int x0 = static_cast<int>(static_cast<int16_t>(m.b.x >> 16)) - w / 2;
+    const int y0 = static_cast<int>(static_cast<int16_t>(m.b.y & 0xffffu)) - h / 2;
+    const int x1 = x0 + w, y1 = y0 + h;  // [x0, x1) x [y0, y1)
     if (x1 <= 0 || y1 <= 0) continue;
-    const int qx = qpel(m.motion_x, m.motion_scale), qy = qpel(m.motion_y, m.motion_scale);
+    const int scale = static_cast<int>(m.d.x & 0xffffu);
+    const int qx = qpel(static_cast<int>(m.c.x), scale), qy = qpel(static_cast<int>(m.c.y), scale);
+    if (r - r0 < qcap) s_q[r - r0] = (static_cast<uint32_t>(qx) & 0xffffu) | (static_cast<uint32_t>(qy) << 16);
     const unsigned long long sq = static_cast<unsigned long long>(static_cast<long long>(qx) * qx +
                                                                   static_cast<long long>(qy) * qy);
     const unsigned long long k = ((sq + 1ull) << 32) | (0xffffffffull - static_cast<unsigned long long>(r - r0));
-    const int i_lo = max(0, (x0 >= 0 ? x0 : x0 - mb + 1) / mb), i_hi = min(cols - 1, (x1 - 1) / mb);
-    const int j_lo = max(0, (y0 >= 0 ? y0 : y0 - mb + 1) / mb), j_hi = min(rows - 1, (y1 - 1) / mb);
+    // MBs i with [mb i, mb (i + 1)) meeting [x0, x1) in positive length: floor(x0 / mb) .. floor((x1 - 1) / mb),
+    // clamped to the grid (x1 > 0 and y1 > 0 here; a partition right of / below the grid gives an empty range)
+    int i_lo, i_hi, j_lo, j_hi;
+    if (MB_SHIFT > 0) {
+      i_lo = max(0, x0 >> MB_SHIFT);  // arithmetic shift = floor division
+      i_hi = min(cols - 1, (x1 - 1) >> MB_SHIFT);
+      j_lo = max(0, y0 >> MB_SHIFT);
+      j_hi = min(rows - 1, (y1 - 1) >> MB_SHIFT);
+    } else {
+      i_lo = max(0, (x0 >= 0 ? x0 : x0 - mb + 1) / mb);
+      i_hi = min(cols - 1, (x1 - 1) / mb);
+      j_lo = max(0, (y0 >= 0 ? y0 : y0 - mb + 1) / mb);
+      j_hi = min(rows - 1, (y1 - 1) / mb);
+    }
     for (int j = j_lo; j <= j_hi; ++j)
-      for (int i = i_lo; i <= i_hi; ++i) {
-        const int ox = min(x1, mb * (i + 1)) - max(x0, mb * i);
-        const int oy = min(y1, mb * (j + 1)) - max(y0, mb * j);
-        if (ox > 0 && oy > 0) atomicMax(&s_key[j * cols + i], k);
-      }
+      for (int i = i_lo; i <= i_hi; ++i) atomicMax(&s_key[j * cols + i], k);
   }
   __syncthreads();
   cs_mb* o = out + static_cast<long long>(f) * n_mb;
@@ -117,9 +149,15 @@ __global__ void __launch_bounds__(kRastThreads) mv_rasterize_smem(int mb, int co
       v.mvy_qpel = 0;
       v.mb_type = CS_MB_INTRA;
     } else {
-      const long long r = r0 + static_cast<long long>(0xffffffffull - (k & 0xffffffffull));
-      v.mvx_qpel = static_cast<int16_t>(qpel(mvs[r].motion_x, mvs[r].motion_scale));
-      v.mvy_qpel = static_cast<int16_t>(qpel(mvs[r].motion_y, mvs[r].motion_scale));
+      const long long i = static_cast<long long>(0xffffffffull - (k & 0xffffffffull));
+      if (i < qcap) {
+        const uint32_t qq = s_q[i];
+        v.mvx_qpel = static_cast<int16_t>(qq & 0xffffu);
+        v.mvy_qpel = static_cast<int16_t>(qq >> 16);
+      } else {
+        v.mvx_qpel = static_cast<int16_t>(qpel(mvs[r0 + i].motion_x, mvs[r0 + i].motion_scale));
+        v.mvy_qpel = static_cast<int16_t>(qpel(mvs[r0 + i].motion_y, mvs[r0 + i].motion_scale));
+      }
       v.mb_type = CS_MB_INTER;
     }
     o[e] = v;
@@ -158,10 +196,17 @@ int cs_launch_mv_rasterize(const cs_grid* g, int32_t n_frames, const cs_av_mv* m
   if (n_frames == 0) return CS_OK;
   const long long n_mb = static_cast<long long>(g->mb_rows) * g->mb_cols;
   if (n_mb <= kSmemMbs) {
-    const size_t smem = static_cast<size_t>(n_mb) * 8;
-    if (cs_set_smem_attr(reinterpret_cast<const void*>(mv_rasterize_smem), 21, 8 * kSmemMbs)) return CS_ERR_CUDA;
-    mv_rasterize_smem<<<n_frames, kRastThreads, smem, stream>>>(g->mb_size, g->mb_cols, g->mb_rows, mvs,
-                                                            reinterpret_cast<const long long*>(mv_offsets), out);
+    // keys of the whole grid + the frame's first qcap quarter-pel vectors; one CTA per SM leaves ~80 KB of L1
+    const int qcap = static_cast<int>((144 * 1024 - n_mb * 8) / 4);
+    const size_t smem = static_cast<size_t>(n_mb) * 8 + static_cast<size_t>(qcap) * 4;
+    const bool h264 = g->mb_size == 16;
+    const void* fn = h264 ? reinterpret_cast<const void*>(mv_rasterize_smem<4>)
+                          : reinterpret_cast<const void*>(mv_rasterize_smem<0>);
+    if (cs_set_smem_attr(fn, h264 ? 21 : 25, 144 * 1024)) return CS_ERR_CUDA;
+    const long long* offs = reinterpret_cast<const long long*>(mv_offsets);
+    if (h264) mv_rasterize_smem<4><<<n_frames, kRastThreads, smem, stream>>>(16, g->mb_cols, g->mb_rows, mvs, offs, out, qcap);
+    else mv_rasterize_smem<0><<<n_frames, kRastThreads, smem, stream>>>(g->mb_size, g->mb_cols, g->mb_rows, mvs, offs, out,
+                                                                  qcap);
     return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
   }
   mv_rasterize<<<n_frames, kThreads, 0, stream>>>(g->mb_size, g->mb_cols, g->mb_rows, mvs,

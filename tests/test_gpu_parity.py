@@ -1428,10 +1428,11 @@ def _random_avmv(ref, g, n_frames, rng):
     return np.concatenate(recs), np.array(offs, np.int64)
 
 
-@pytest.mark.parametrize("src", [(448, 448), (1920, 1080), (100, 60), (3840, 2160)])
+@pytest.mark.parametrize("src", [(448, 448), (1920, 1080), (100, 60), (3840, 2160), (640, 360, 8), (500, 300, 12)])
 def test_mv_rasterize_gpu(abi, ref, src):
-    """Keys in shared memory (grids up to 12,288 MBs) and in global memory (4K: 32,400 MBs)."""
-    g = make_grid(*src)
+    """Keys in shared memory (grids up to 12,288 MBs; 16-px MBs by shifts, other sizes by division; records past
+    the first 12,288 of a frame decoded from global memory) and in global memory (4K: 32,400 MBs)."""
+    g = make_grid(src[0], src[1], mb_size=src[2] if len(src) > 2 else 16)
     rng = np.random.default_rng(src[0])
     n = 1 if src[0] > 2000 else 5          # (the oracle's rasterisation is O(MBs x records) per frame)
     mvs, offs = _random_avmv(ref, g, n, rng)
