@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) mv_rasterize(int mb, int cols, int r
 
 // The same arbitration with the frame's keys in shared memory (grids up to kSmemMbs MBs: 1080p's 8,160 MBs are 65 KB):
 // shared-memory atomics instead of L2 atomics, and the output written once, coalesced.  Each record's quarter-pel
-// vector is also kept in shared memory (the frame's first kQCap records), so decoding a winner reads no global
+// vector is also kept in shared memory (the frame's first qcap records), so decoding a winner reads no global
 // memory; MB_SHIFT > 0: the MB size is 1 << MB_SHIFT (H.264: 16) and the partition -> MB range is two shifts.
 constexpr int kSmemMbs = 12288;
 constexpr int kRastThreads = 1024;  // the per-thread record loop and the winner decode are latency chains: wide CTAs

@@ -140,14 +140,25 @@ __global__ void __launch_bounds__(kCountThreads) compact_count(const __grid_cons
       s_k[warp][gr] = k;
     }
     __syncwarp();
+    // lanes own column classes (j = lane + 32 t, at most kNvMaxColClasses / 32 each); the row classes are walked
+    // warp-uniformly: K = the kept group columns of the class's group rows, one AND per owned column class
+    constexpr int kOwn = kNvMaxColClasses / 32;
+    unsigned long long cm[kOwn];
+    unsigned long long cn[kOwn];
+#pragma unroll
+    for (int t = 0; t < kOwn; ++t) {
+      const int j = lane + 32 * t;
+      cm[t] = j < C.n_cols ? C.cols[j].mask : 0ull;
+      cn[t] = j < C.n_cols ? static_cast<unsigned long long>(C.cols[j].n) : 0ull;
+    }
     unsigned long long sectors = 0ull;
-    for (int i = lane; i < C.n_rows; i += 32) {
+    for (int i = 0; i < C.n_rows; ++i) {
       const NvClass rc = s_rc[i];
       unsigned long long K = 0ull;
       for (unsigned long long b = rc.mask; b; b &= b - 1) K |= s_k[warp][__ffsll(static_cast<long long>(b)) - 1];
       unsigned long long cols = 0ull;
-      for (int j = 0; j < C.n_cols; ++j)
-        if (K & C.cols[j].mask) cols += static_cast<unsigned long long>(C.cols[j].n);
+#pragma unroll
+      for (int t = 0; t < kOwn; ++t) cols += (K & cm[t]) ? cn[t] : 0ull;
       sectors += cols * static_cast<unsigned long long>(rc.n);
     }
 #pragma unroll
@@ -1481,7 +1492,10 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sf, kNvsWarps * 32, nsmem) != cudaSuccess ||
           per_sm < 1)
         per_sm = 1;
-      const int ngrid = cs_num_sms() * per_sm;
+      int ngrid = cs_num_sms() * per_sm;
+#ifdef CS_NV12_SMS
+      ngrid = std::min(ngrid, CS_NV12_SMS * per_sm);  // experiment: leave SMs to a concurrent kv_refresh
+#endif
       if (rb == 144) compact_nv12_staged<144><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P);
       else compact_nv12_staged<256><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P);
       if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;

@@ -139,7 +139,8 @@ CS_DEV uint32_t f32_to_bf16_rne(float f) {
 // one instruction issue -- each half is bit-identical to __fadd_rn / __fmul_rn / __fmaf_rn on it).
 // CAUTION (measured, ptxas 12.9): ptxas contracts mul.rn.f32x2 feeding add/sub.rn.f32x2 into FFMA2 -- even with
 // -fmad=false, and even through fma(x, 1, y) -- which changes the rounding.  So a sum or difference whose operand is
-// a packed product must use the scalar per-half forms addp / subp (scalar FADD is never fused with FMUL2).
+// a packed product must use add1 / sub1 below (FFMA2 with a runtime 1.0) or the scalar per-half forms addp / subp
+// (scalar FADD is never fused with FMUL2).
 CS_DEV unsigned long long f2pk(float2 a) {
   unsigned long long r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));

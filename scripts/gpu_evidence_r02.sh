@@ -1,6 +1,6 @@
 # Round-2 evidence for the current code: smoke, all GPU tests, every bench line, ncu launch lists and full captures
 # of the hot kernels, the multi-rank (shared GPU, gloo) strong-scaling path.  Outputs in gpurun_out/ev2/.
-O=${EV_OUT:-gpurun_out/ev3}; mkdir -p $O
+O=${EV_OUT:-gpurun_out/ev4}; mkdir -p $O
 nproc > $O/host.txt; grep -m1 "model name" /proc/cpuinfo >> $O/host.txt
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,driver_version --format=csv > $O/gpu_info.txt
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo build rc=$?
@@ -35,7 +35,7 @@ timeout 900 ncu --metrics $M --clock-control none -k regex:'mv_rasterize|score_k
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'kv_gather_tma' -s 3 -c 1 -o $O/prof_kv_c4 $B > /dev/null 2>$O/f1.err; echo kv4 rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'score_kernel' -s 3 -c 1 -o $O/prof_fused_c4 $B > /dev/null 2>$O/f2.err; echo fused4 rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'score_kernel' -s 3 -c 1 -o $O/prof_fused_c2 $B --workload C2 > /dev/null 2>$O/f3.err; echo fused2 rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'compact_gather' -s 3 -c 1 -o $O/prof_nv12 $B --frames nv12 > /dev/null 2>$O/f4.err; echo nv12 rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'compact_nv12_staged' -s 3 -c 1 -o $O/prof_nv12 $B --frames nv12 > /dev/null 2>$O/f4.err; echo nv12 rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'mv_rasterize' -s 3 -c 1 -o $O/prof_rast $B --workload cdf > /dev/null 2>$O/f5.err; echo rast rc=$?
 timeout 300 python scripts/pdl_timing.py > $O/pdl_timing.txt 2>&1; echo pdl_timing rc=$?
 python scripts/sass_summary.py > $O/sass.txt 2>&1

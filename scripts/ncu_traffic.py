@@ -21,19 +21,22 @@ CALLS = {  # call -> kernel-name prefixes
     "kv": ("kv_plan", "kv_prefix", "kv_gather"),
     "fused": ("score_kernel<1>",),
     "score": ("score_kernel<0>",),
-    "compact": ("compact_count", "compact_scan", "compact_gather"),
+    "compact": ("compact_count", "compact_scan", "compact_gather", "compact_nv12"),
     "rasterize": ("mv_rasterize",),
     "similar_hist": ("similar_hist",),
 }
 
 
 def steps(path):
-    """[(kernel, read, write, time_ns)] grouped into bench steps (a new step at each score kernel)."""
+    """[(kernel, read, write, time_ns)] grouped into bench steps (a new step at each score kernel; in a list
+    captured with compaction kernels only, at each compact_count: one group per compact call)."""
     data = launches(path)
+    compact_only = not any(n.startswith(("score_kernel", "mv_rasterize")) for (_, n) in data)
     out, cur = [], None
     for (_, name), d in data.items():
-        if name.startswith("score_kernel") or name.startswith("mv_rasterize") or cur is None:
-            if name.startswith("compact_") and cur is not None:
+        if (name.startswith("score_kernel") or name.startswith("mv_rasterize") or cur is None or
+                (compact_only and name.startswith("compact_count"))):
+            if name.startswith("compact_") and cur is not None and not compact_only:
                 pass
             else:
                 cur = []
@@ -48,11 +51,11 @@ def steps(path):
     return trimmed
 
 
-def per_launch(groups, call, n_last=2, stop_after_kv=False):
-    """Mean DRAM bytes of `call` over the last n_last step groups that contain it."""
+def per_launch(groups, call, n_last=2, stop_after_kv=False, sel=None):
+    """Mean DRAM bytes of `call` over the last n_last step groups that contain it (or the groups `sel` picks)."""
     pref = CALLS[call]
     vals = []
-    for g in groups:
+    for g in (groups[sel] if sel is not None else groups):
         seen = False
         rd = wr = t = 0.0
         for name, r, w, tt in g:
@@ -85,6 +88,9 @@ def main():
             ("C3", "ncu_launches_C3.csv", [("kv_refresh_paged", "kv"), ("score_compact", "fused")]),
             ("C2", "ncu_launches_C2.csv", [("score_compact", "fused")]),
             ("C4", "ncu_launches_C4nv12.csv", [("compact_nv12", "compact")]),
+            # compaction kernels only (one group per call): the bench's timed steps are calls 3, 4 (--warmup 3
+            # --steps 2); later calls are its per-layout compaction timings
+            ("C4", "ncu_launches_C4planar.csv", [("compact_gather+planar", "compact", slice(3, 5))]),
             ("cdf", "ncu_launches_cdf.csv", [("rasterize", "rasterize"), ("score_patches", "score"),
                                             ("similar_hist", "similar_hist")])]
     for w, f, keys in jobs:
@@ -92,8 +98,8 @@ def main():
         if not os.path.exists(p):
             continue
         g = steps(p)
-        for key, call in keys:
-            r = per_launch(g, call)
+        for key, call, *sel in keys:
+            r = per_launch(g, call, sel=sel[0] if sel else None)
             if r is None:
                 continue
             r["workload"] = W[w]

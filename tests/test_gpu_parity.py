@@ -1407,11 +1407,11 @@ def test_compact_nv12_paths(abi, ref, case):
 # ------------------------------------------------------------------------------------------------------------
 # NEXT-4: AVMotionVector rasterisation and the similar-patch histogram
 # ------------------------------------------------------------------------------------------------------------
-def _random_avmv(ref, g, n_frames, rng):
+def _random_avmv(ref, g, n_frames, rng, n_first=None):
     recs = []
     offs = [0]
     for f in range(n_frames):
-        n = int(rng.integers(0, 3 * g["mb_rows"] * g["mb_cols"]))
+        n = int(rng.integers(0, 3 * g["mb_rows"] * g["mb_cols"])) if (f or n_first is None) else n_first
         a = np.zeros(n, ref.AV_MV_DTYPE)
         a["source"] = rng.choice([-1, -1, -1, 1], size=n)
         a["w"] = rng.choice([4, 8, 16], size=n)
@@ -1431,11 +1431,12 @@ def _random_avmv(ref, g, n_frames, rng):
 @pytest.mark.parametrize("src", [(448, 448), (1920, 1080), (100, 60), (3840, 2160), (640, 360, 8), (500, 300, 12)])
 def test_mv_rasterize_gpu(abi, ref, src):
     """Keys in shared memory (grids up to 12,288 MBs; 16-px MBs by shifts, other sizes by division; records past
-    the first 12,288 of a frame decoded from global memory) and in global memory (4K: 32,400 MBs)."""
+    the ~20k whose vectors stay in shared memory decoded from global memory: 1080p's first frame has 24,479) and in
+    global memory (4K: 32,400 MBs)."""
     g = make_grid(src[0], src[1], mb_size=src[2] if len(src) > 2 else 16)
     rng = np.random.default_rng(src[0])
     n = 1 if src[0] > 2000 else 5          # (the oracle's rasterisation is O(MBs x records) per frame)
-    mvs, offs = _random_avmv(ref, g, n, rng)
+    mvs, offs = _random_avmv(ref, g, n, rng, n_first=24479 if src == (1920, 1080) else None)
     out_d = torch.zeros(n * g["mb_rows"] * g["mb_cols"], dtype=torch.int64, device=DEV)
     abi.codecsight_mv_rasterize(g, n, torch.from_numpy(mvs.view(np.uint8)).to(DEV), torch.from_numpy(offs).to(DEV),
                                 out_d)
