@@ -1492,10 +1492,7 @@ static int launch_compact(const cs_grid* g, const cs_preprocess* pre, int32_t tp
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sf, kNvsWarps * 32, nsmem) != cudaSuccess ||
           per_sm < 1)
         per_sm = 1;
-      int ngrid = cs_num_sms() * per_sm;
-#ifdef CS_NV12_SMS
-      ngrid = std::min(ngrid, CS_NV12_SMS * per_sm);  // experiment: leave SMs to a concurrent kv_refresh
-#endif
+      const int ngrid = cs_num_sms() * per_sm;
       if (rb == 144) compact_nv12_staged<144><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P);
       else compact_nv12_staged<256><<<ngrid, kNvsWarps * 32, nsmem, stream>>>(P);
       if (cudaGetLastError() != cudaSuccess) return CS_ERR_CUDA;

@@ -1510,11 +1510,7 @@ static int launch_gather_tma(const KvParams& P, const cs_kv_desc* kv, const TmaG
   const int warps = t.warps, nst = t.nst;
   const unsigned stage_bytes = t.stage_bytes, tab_bytes = t.tab_bytes;
   const size_t smem = static_cast<size_t>(warps) * nst * (stage_bytes + tab_bytes);
-#ifdef CS_KV_SMS
-  const int grid = CS_KV_SMS;  // experiment: leave SMs to a concurrent compaction
-#else
   const int grid = cs_num_sms();
-#endif
   const bool qwen = kv->dtype == CS_BF16 && kv->kv_heads == 4 && kv->head_dim == 128;
   const void* fn = qwen ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 4, 128>)
                         : (kv->dtype == CS_BF16 ? reinterpret_cast<const void*>(kv_gather_tma<uint16_t, 0, 0>)
