@@ -60,10 +60,11 @@ def parse():
     ap.add_argument("--cpu-all-cores", action=argparse.BooleanOptionalAction, default=True,
                     help="also time the oracle as one process per host core (SURVEY §8(d)(ii))")
     ap.add_argument("--quiet", action="store_true")
-    ap.add_argument("--overlap", action="store_true",
-                    help="run kv_refresh of step k on a side stream while step k+1's score(+compact) runs "
-                         "(measured, same box: C4 +1.1 %%, C3 +0.7 %% -- the step is already at the HBM roofline; "
-                         "default off, profiles/r01_ovl_*.json)")
+    ap.add_argument("--overlap", action=argparse.BooleanOptionalAction, default=None,
+                    help="run step k's compaction / kv_refresh on side streams while step k+1's scoring runs (default: "
+                         "on for workloads with a KV refresh, unless --pdl / --graphs / --temporal-patch 2; measured, "
+                         "same box: C4 6.43 -> 6.38 ms, 32 streams per GPU (C4 strong-scaled to 8 GPUs) 0.941 -> 0.917 "
+                         "ms, NV12 C4 6.85 -> 6.72 ms; --no-overlap for the sequential step)")
     ap.add_argument("--fused", action=argparse.BooleanOptionalAction, default=True,
                     help="one codecsight_score_compact launch per step (NEXT-2, default) instead of score_patches + "
                          "compact (--no-fused)")
@@ -453,6 +454,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         kvb = dict(kvb, rope_mode=1, mrope_section=(16, 24, 24), t_per_frame=1)
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
     pre = dict(src_w=sw, src_h=sh, y_pitch=sw, uv_pitch=sw) if args.frames == "nv12" else None
+    if args.overlap is None:  # default: pipelined steps wherever the Pipeline supports them
+        args.overlap = kvb is not None and not args.pdl and not args.graphs and args.temporal_patch == 1
     if args.pdl and (kvb is not None or not args.fused or args.overlap or args.graphs):
         raise SystemExit("--pdl: prune-only workload (C2), fused score+compact, no --overlap / --graphs")
     pipe = Pipeline(g, S, w, s, gop, kvb, n_prompt=cfg["n_prompt"], device=dev, frame_layout=layout,
