@@ -68,10 +68,11 @@ def parse():
     ap.add_argument("--fused", action=argparse.BooleanOptionalAction, default=True,
                     help="one codecsight_score_compact launch per step (NEXT-2, default) instead of score_patches + "
                          "compact (--no-fused)")
-    ap.add_argument("--pdl", action="store_true",
+    ap.add_argument("--pdl", action=argparse.BooleanOptionalAction, default=None,
                     help="prune-only workloads (C2): launch each step's fused score+compact as a programmatic dependent "
                          "of the previous step's (CS_LAUNCH_PDL), so its scoring overlaps the previous compaction; the "
-                         "kernel time is then the timed region / K (no per-kernel events between the launches)")
+                         "kernel time is then the timed region / K (no per-kernel events between the launches); "
+                         "default: on for prune-only workloads with the fused call and no --graphs")
     ap.add_argument("--chain-depth", type=int, default=4,
                     help="--pdl: output buffer sets the chained calls rotate (call g reuses call g - depth's)")
     ap.add_argument("--graphs", action="store_true",
@@ -454,6 +455,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         kvb = dict(kvb, rope_mode=1, mrope_section=(16, 24, 24), t_per_frame=1)
     layout = abi.CS_LAYOUT_GROUPED if args.frame_layout == "grouped" else abi.CS_LAYOUT_PLANAR
     pre = dict(src_w=sw, src_h=sh, y_pitch=sw, uv_pitch=sw) if args.frames == "nv12" else None
+    if args.pdl is None:  # default: chained steps for prune-only workloads
+        args.pdl = kvb is None and args.fused and not args.graphs and not args.overlap and args.temporal_patch == 1 \
+            and args.frames == "model"
     if args.overlap is None:  # default: pipelined steps wherever the Pipeline supports them
         args.overlap = kvb is not None and not args.pdl and not args.graphs and args.temporal_patch == 1
     if args.pdl and (kvb is not None or not args.fused or args.overlap or args.graphs):

@@ -8,7 +8,7 @@
 //              writes the index outputs (disposition, p_old by p_new, n_tokens), clamps the data moves to the
 //              capacities (status bits), and leaves in the workspace: a header, the segment list and the fp32
 //              (cos, sin) table of R(dp) computed once per stream-step from fp64 angles (reading Q20).
-//   kv_gather  persistent grid (SM-count multiple).  The work items are (stream, 128-row block, layer, K|V);
+//   kv_gather  persistent grid (SM-count multiple).  The work items are (stream, 64-row block, layer, K|V);
 //              every CTA derives the same item prefix from the per-stream row counts and takes one contiguous,
 //              equal-sized range of items.  Each item walks the segments that overlap its row block: REUSE K runs
 //              are rotated (rotate_half pairs (i, i + D/2) loaded as two 16-B vectors, fp32 fma, RNE store),
@@ -44,7 +44,9 @@ __device__ unsigned long long g_cs_plan_phase[4096][10];
 #else
 #define CS_PLAN_PHASE(k)
 #endif
-constexpr int kRowBlock = 128;
+// rows per gather work item (stream, row block, layer, K|V): 64 balances the grid's tail with guided claims at 32
+// streams per GPU (0.896 -> 0.861 ms per step vs 128) and costs nothing at 256 / C5 (measured, round 2)
+constexpr int kRowBlock = 64;
 constexpr int kMaxSeg = 1025;  // w + 1 with w + s <= 1024
 
 enum { SEG_SKIP = 0, SEG_COPY = 1, SEG_REUSE = 2 };
@@ -94,7 +96,7 @@ struct KvParams {
   long long slot_cap;
   int max_tok;      // w * groups + n_prompt: entries of the per-stream move list
   int mv_smem;      // kv_plan_paged: the move list is also staged in shared memory (runs pass reads it there)
-  int prefix_mode;  // kv_prefix items: 0 = (stream, 128-row block, layer, K|V), 1 = tokens
+  int prefix_mode;  // kv_prefix items: 0 = (stream, kRowBlock-row block, layer, K|V), 1 = tokens
   int paged;        // 1: REUSE runs rotate keys in place and leave values alone
   int rope_mode;    // CS_ROPE_1D | CS_ROPE_MROPE
   int mrope_t;      // M-RoPE: pairs of the temporal section (rotated by dt); the h / w sections stay
@@ -565,7 +567,12 @@ __global__ void __launch_bounds__(kGatherThreads) kv_gather_ldg(const __grid_con
 // the issue overhead off the critical path and ~8 x NST x 8 KB in flight per SM without register staging.
 // ------------------------------------------------------------------------------------------------------------
 constexpr int kTmaChunk = 8192;
-constexpr int kClaim = 4;  // items per dynamic work claim
+// Dynamic work claims are GUIDED: a warp claims max(1, min(kClaimMax, remaining / (kClaimDiv * warps))) items,
+// sizing from the counter value it last saw, so claims shrink to single items at the end of the kernel (the tail
+// imbalance is then about one item, not one 4-item claim = up to 512 KB = ~90 us of a warp's ring at 32 streams per
+// GPU), while large batches (C5: 3.7 M items) keep few atomics on the shared counter.
+constexpr int kClaimMax = 16;
+constexpr int kClaimDiv = 8;
 constexpr int kWarpsPerGather = kGatherThreads / 32;
 constexpr int kMaxStages = 6;
 constexpr int kPartialRows = 32;  // rows per in-place partial (M-RoPE temporal section) rotation item
@@ -585,6 +592,8 @@ struct ChunkGen {  // generator state, owned by lane 0 of a warp
   int c_sidx, c_blk, c_seg;  // cache: stream whose pointers are loaded; (stream, block) of the last run search
   long long V;               // total items
   long long next_claim;      // start of the next claimed range (claimed one range ahead), >= V when exhausted
+  int next_size;             // items in that range
+  int claim_div;             // kClaimDiv x the grid's warps
   unsigned long long* ctr;   // work counter in the workspace header (zeroed by kv_prefix)
   const KvSeg* segs;
   unsigned char* nc;
@@ -592,6 +601,14 @@ struct ChunkGen {  // generator state, owned by lane 0 of a warp
   const unsigned char* rf;
   const void* tab;
 };
+
+// claim the next range (lane 0 of the warp); `seen` = the largest counter value this warp has observed
+__device__ __forceinline__ void claim(ChunkGen& g, long long seen) {
+  const long long rem = g.V - seen;
+  const int sz = static_cast<int>(rem <= 0 ? 1 : min(static_cast<long long>(kClaimMax), max(1ll, rem / g.claim_div)));
+  g.next_size = sz;
+  g.next_claim = static_cast<long long>(atomicAdd(g.ctr, static_cast<unsigned long long>(sz)));
+}
 
 __device__ __forceinline__ const int* ws_prefix(const KvParams& P) {
   return reinterpret_cast<const int*>(P.ws + 16 + (long long)P.n_streams * P.ws_stride);
@@ -606,8 +623,8 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
       // dynamic balancing: take the range claimed earlier, claim the next one now (latency hidden by the ring)
       if (g.next_claim >= g.V) return false;
       g.it = g.next_claim;
-      g.it1 = min(g.V, g.it + kClaim);
-      g.next_claim = static_cast<long long>(atomicAdd(g.ctr, static_cast<unsigned long long>(kClaim)));
+      g.it1 = min(g.V, g.it + g.next_size);
+      claim(g, g.it1);
       if (__ldg(pref + g.sidx) > g.it) g.sidx = 0;  // (claims only increase; defensive)
       g.active = 0;
     }
@@ -694,7 +711,7 @@ __device__ __forceinline__ bool gen_next(const KvParams& P, const int* pref, Chu
   }
 }
 
-// 1 CTA: item prefix over streams into the workspace (item = stream x 128-row block x layer x K|V)
+// 1 CTA: item prefix over streams into the workspace (item = stream x kRowBlock-row block x layer x K|V)
 __global__ void __launch_bounds__(1024) kv_prefix(const __grid_constant__ KvParams P) {
   __shared__ int s_wsum[32];
   __shared__ int s_carry;
@@ -860,8 +877,9 @@ __global__ void __launch_bounds__(kGatherThreads, 1) kv_gather_tma(const __grid_
   gen.c_sidx = -1;
   gen.c_blk = -1;
   gen.sidx = 0;
+  gen.claim_div = kClaimDiv * static_cast<int>(gridDim.x) * static_cast<int>(blockDim.x / 32);
   if (lane == 0) {
-    gen.next_claim = static_cast<long long>(atomicAdd(gen.ctr, static_cast<unsigned long long>(kClaim)));
+    claim(gen, 0);
     gen.it = gen.it1 = 0;  // empty: the first gen_next takes the claimed range
     for (int s = 0; s < nst; ++s) cs::mbar_init(&full[s], 1);
     cs::fence_mbar_init();
