@@ -997,35 +997,24 @@ __global__ void __launch_bounds__(kGatherThreads, 1) compact_gather_tma(const __
 }
 
 // ---- fused NV12 preprocessing, source rows staged in shared memory (NEXT-2; 2x2 groups of 14-px patches) -------
-// The work is a flat sequence of ITEMS per warp: item = one pair of output rows (2i, 2i + 1) of one kept group,
-// 14 items per group, the warp's kept groups in packed order.  An item reads 8 source rows: the luma tap rows
-// y0(r), y1(r) of its two output rows r and the chroma rows y0(r)/2, y1(r)/2, each over the group's column span
-// [xs, xs + 16 nch) (xs = the group's first luma tap rounded down to 16 B; nch 16-B chunks cover the span of the
-// last column's taps, luma and chroma alike).  Lane l copies row l/4, chunks (l%4) + 4m, with 16-B cp.async into a
-// stage of the warp's ring; the copies of item t + kNvsAhead are issued before item t is computed, across group
-// boundaries (the next group comes from the warp's kept-group enumeration when the producer reaches it).  The
-// compute is the LDG path's (lanes on the group's 28 output columns, nv12_pair_px) with every tap one shared-memory
-// load at a per-lane constant offset and no 64-bit index arithmetic; the bf16 pixels go straight to the packed rows
-// (a patch row of 14 px = 28 B per channel and row; the two rows of an item are adjacent, so sectors fill in L2).
-// Row taps / weights come from a per-CTA table (one nv12_axis per model row, computed once per launch).
-// Requires pitches that are multiples of 16; a slot whose planes are not 16-B aligned is staged with byte copies.
-#ifndef CS_NVS_MINB
-#define CS_NVS_MINB 1  // resident CTAs per SM the register budget is sized for
-#endif
-#ifndef CS_NVS_UNROLL
-#define CS_NVS_UNROLL 1  // unroll of the 7-pair loop
-#endif
-#define CS_PRAGMA_(x) _Pragma(#x)
-#define CS_PRAGMA(x) CS_PRAGMA_(x)
-#ifndef CS_NVS_WARPS
-#define CS_NVS_WARPS 16
-#endif
-#ifndef CS_NVS_STAGES
-#define CS_NVS_STAGES 3
-#endif
-constexpr int kNvsWarps = CS_NVS_WARPS;
-constexpr int kNvsStages = CS_NVS_STAGES;  // ring stages per warp (kNvsStages - 1 pairs in flight)
-constexpr int kNvsPairs = 7;  // item pairs (4 output rows) per 28-row group; a ring stage holds one pair
+// The work of a warp is a flat sequence of ITEMS -- one pair of output rows of one kept group, 14 per group, the
+// warp's kept groups in packed order -- taken two at a time: pair j of a group = items j and j + 7, i.e. rows
+// (2j, 2j + 1) of patch rows dy = 0 and 1, so the pair's 12 bf16 stores are immediates off one per-lane base.  An
+// item reads 8 source rows: the luma tap rows y0(r), y1(r) of its two output rows r and their chroma rows, each over
+// the group's column span [xs, xs + 16 nch) (xs = the group's first luma tap rounded down to 16 B; nch chunks cover
+// the last column's luma and chroma taps).  PRODUCER: lane l copies staged row l/4 of each item, chunks (l%4) + 4m,
+// with predicated 16-B cp.async into a stage of the warp's ring, kNvsStages - 1 pairs ahead of the compute, across
+// group boundaries (the next group comes from the warp's kept-group enumeration when the producer reaches it; its
+// descriptor is published in shared memory).  CONSUMER: lanes on the group's 28 output columns (nv12_pair_an, as
+// the direct-load path), every tap one shared-memory load at a per-lane constant offset, no 64-bit index arithmetic;
+// one midpoint-guard branch per pair; predicated 2-B stores straight to the packed rows (a pair covers 56 contiguous
+// bytes per channel and patch row, so sectors fill in L2).  Row taps / weights come from per-CTA tables (one
+// nv12_axis per model row per launch).  16 warps x 96 registers, one CTA per SM (measured against 8-24 warps and a
+// 64-register budget, which rematerialised the lane constants every pair).  Requires pitches that are
+// multiples of 16; a slot whose planes are not 16-B aligned is staged with byte copies.
+constexpr int kNvsWarps = 16;
+constexpr int kNvsStages = 3;  // ring stages per warp (kNvsStages - 1 pairs in flight)
+constexpr int kNvsPairs = 7;   // item pairs (4 output rows) per 28-row group; a ring stage holds one pair
 
 struct NvsGroup {  // a kept group of the warp's range (warp-uniform)
   long long n0;    // first packed row
@@ -1035,7 +1024,7 @@ struct NvsGroup {  // a kept group of the warp's range (warp-uniform)
 };
 
 template <int RB>  // staged row pitch in bytes (16 * max chunks: 144 covers scale_x <= 4.6, 256 up to 8.6)
-__global__ void __launch_bounds__(kNvsWarps * 32, CS_NVS_MINB) compact_nv12_staged(const __grid_constant__ CompactParams P) {
+__global__ void __launch_bounds__(kNvsWarps * 32, 1) compact_nv12_staged(const __grid_constant__ CompactParams P) {
   constexpr int p = 14, gp = 28, row_el = 588, kItem = 8 * RB, kStage = 2 * kItem;
   extern __shared__ __align__(128) unsigned char n_smem[];
   __shared__ __align__(16) uint32_t s_mask[kNvsWarps][64];
@@ -1211,7 +1200,7 @@ __global__ void __launch_bounds__(kNvsWarps * 32, CS_NVS_MINB) compact_nv12_stag
     uint16_t* out = P.packed + (n0 + dx) * row_el + xin;  // this lane's column, patch row dy = 0
     const bool st[2] = {lane < gp && n0 + dx < P.capacity, lane < gp && n0 + 2 + dx < P.capacity};
     const float* lyp = s_ly + gr * gp;
-    CS_PRAGMA(unroll CS_NVS_UNROLL)
+#pragma unroll 1
     for (int j = 0; j < kNvsPairs; ++j) {
       cs::cp_async_wait<kNvsStages - 2>();  // this lane's copies of pair j have landed
       __syncwarp();  // ... and every lane's; every lane is done with the stage the next copies go to (pair j - 1's)
