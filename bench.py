@@ -493,7 +493,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         frames = [torch.randn(3, H, W, generator=gen, device=dev).to(torch.bfloat16) for _ in range(S * s)]
         ptr_w = abi.ptr_array([frames[i % len(frames)] for i in range(S * w)], dev)
         ptr_s = abi.ptr_array(frames, dev)
-    calib = 2 * period if args.graphs else 0  # eager steps after the graph-timed loop: per-kernel event times
+    # eager sequential steps after the timed loop whose per-kernel events give the per-call times and rooflines: with
+    # --graphs (no events inside graphs) and in overlap mode (a side-stream call's events also cover the time it
+    # waits for SMs held by the other stream's kernel)
+    calib = 2 * period if args.graphs else (min(max(args.steps, 4), 10) if args.overlap else 0)
     total_steps = warm + args.steps + calib
     types_dev, fidx_dev, types_host = [], [], []
     for k in range(total_steps + 1):
@@ -535,8 +538,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             st["fi"].copy_(fidx_dev[k], non_blocking=True)
             pipe.graph_step(k, st["mb"], ptrs, st["fi"], st["ty"])
             return
-        evs = pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k], timing=timed and not args.pdl)
-        if timed and not args.pdl:
+        evs = pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k],
+                        timing=timed and not args.pdl and not args.overlap)
+        if timed and not args.pdl and not args.overlap:
             for name in ("score", "compact", "kv"):
                 if name in evs:
                     ev[name].append(evs[name])
@@ -571,12 +575,14 @@ def run_ours(args, cfg, rank, world, local_rank):
     clk = clocks.stop()
     ms = t_start.elapsed_time(t_end)
     dcnt = (pipe.counters - cnt0)
-    if args.graphs:
-        # per-kernel times of the graph-timed steps: the same kernels timed eagerly with events right after
-        # (counters of these steps are excluded from dcnt above)
+    if calib:
+        # per-kernel times of the timed steps: the same kernels timed eagerly and sequentially with events right
+        # after (counters of these steps are excluded from dcnt above)
+        pipe.overlap = False  # (the ring and buffers stay as they are; steps run on one stream)
         for k in range(warm + args.steps, warm + args.steps + calib):
             run_step_eager(k)
         torch.cuda.synchronize()
+        pipe.overlap = args.overlap
     per = {kname: [a.elapsed_time(b) for a, b in lst] for kname, lst in ev.items()}
     if args.pdl:  # back-to-back overlapping launches: the average launch duration is the timed region / K
         per["score"] = [ms / args.steps] * args.steps
