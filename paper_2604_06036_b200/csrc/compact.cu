@@ -122,43 +122,60 @@ __global__ void __launch_bounds__(kCountThreads) compact_count(const __grid_cons
                                                                 const __grid_constant__ NvSrcClasses C) {
   __shared__ uint32_t s_m[kCountThreads / 32][128];  // per-warp unit mask (grid_words <= 128)
   __shared__ unsigned long long s_k[kCountThreads / 32][64];  // NV12 source count: kept group columns per group row
-  __shared__ NvClass s_rc[kNvMaxRowClasses];  // the row classes (lane-indexed: constant-bank reads would serialise)
+  __shared__ NvClass s_rc[kNvMaxRowClasses];  // the row / column classes, staged once per CTA: a lane-indexed
+  __shared__ NvClass s_cc[kNvMaxColClasses];  // read of the parameter bank serialises its cache misses
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = blockIdx.x * (kCountThreads / 32) + warp;
   if (C.enabled) {
-    for (int i = threadIdx.x; i < C.n_rows; i += kCountThreads) s_rc[i] = C.rows[i];
+    // warp-uniform parameter reads (one address per warp instruction, the warps' misses in flight together)
+    for (int i = warp; i < C.n_rows; i += kCountThreads / 32) {
+      const NvClass v = C.rows[i];
+      if (lane == 0) s_rc[i] = v;
+    }
+    for (int j = warp; j < C.n_cols; j += kCountThreads / 32) {
+      const NvClass v = C.cols[j];
+      if (lane == 0) s_cc[j] = v;
+    }
     __syncthreads();
   }
   if (slot >= P.n_slots) return;
   if (C.enabled) {
-    const uint32_t* m = slot_mask(P, slot);
+    // the slot's keep mask in shared memory first (the group tests below would otherwise be dependent global loads)
+    const uint32_t* mg = slot_mask(P, slot);
+    for (int t = lane; t < P.nw; t += 32) s_m[warp][t] = __ldg(mg + t);
+    __syncwarp();
+    const uint32_t* m = s_m[warp];
     const int ngr = P.grid_h / P.G;
-    for (int gr = lane; gr < ngr; gr += 32) {
-      unsigned long long k = 0ull;
-      for (int gc = 0; gc < P.ngc; ++gc)
-        if (cs::group_kept(m, gr * P.ngc + gc, P.ngc, P.G, P.grid_w)) k |= 1ull << gc;
-      s_k[warp][gr] = k;
+    if (P.G == 2 && P.grid_w == 32) {
+      // kept group columns of group row gr: OR of patch rows 2gr, 2gr+1 (one word each), pairs folded onto even
+      // bits, even bits compressed to 16
+      for (int gr = lane; gr < ngr; gr += 32) {
+        const uint32_t x = m[2 * gr] | m[2 * gr + 1];
+        uint32_t y = (x | (x >> 1)) & 0x55555555u;
+        y = (y | (y >> 1)) & 0x33333333u;
+        y = (y | (y >> 2)) & 0x0F0F0F0Fu;
+        y = (y | (y >> 4)) & 0x00FF00FFu;
+        y = (y | (y >> 8)) & 0x0000FFFFu;
+        s_k[warp][gr] = y;
+      }
+    } else {
+      for (int gr = lane; gr < ngr; gr += 32) {
+        unsigned long long k = 0ull;
+        for (int gc = 0; gc < P.ngc; ++gc)
+          if (cs::group_kept(m, gr * P.ngc + gc, P.ngc, P.G, P.grid_w)) k |= 1ull << gc;
+        s_k[warp][gr] = k;
+      }
     }
     __syncwarp();
-    // lanes own column classes (j = lane + 32 t, at most kNvMaxColClasses / 32 each); the row classes are walked
-    // warp-uniformly: K = the kept group columns of the class's group rows, one AND per owned column class
-    constexpr int kOwn = kNvMaxColClasses / 32;
-    unsigned long long cm[kOwn];
-    unsigned long long cn[kOwn];
-#pragma unroll
-    for (int t = 0; t < kOwn; ++t) {
-      const int j = lane + 32 * t;
-      cm[t] = j < C.n_cols ? C.cols[j].mask : 0ull;
-      cn[t] = j < C.n_cols ? static_cast<unsigned long long>(C.cols[j].n) : 0ull;
-    }
+    // lanes take row classes (i = lane + 32 t): K = the kept group columns of the class's group rows, then one
+    // AND per column class (shared-memory broadcast reads); short per-lane chains, all lanes busy
     unsigned long long sectors = 0ull;
-    for (int i = 0; i < C.n_rows; ++i) {
+    for (int i = lane; i < C.n_rows; i += 32) {
       const NvClass rc = s_rc[i];
       unsigned long long K = 0ull;
-      for (unsigned long long b = rc.mask; b; b &= b - 1) K |= s_k[warp][__ffsll(static_cast<long long>(b)) - 1];
+      for (unsigned long long bm = rc.mask; bm; bm &= bm - 1) K |= s_k[warp][__ffsll(static_cast<long long>(bm)) - 1];
       unsigned long long cols = 0ull;
-#pragma unroll
-      for (int t = 0; t < kOwn; ++t) cols += (K & cm[t]) ? cn[t] : 0ull;
+      for (int j = 0; j < C.n_cols; ++j) cols += (K & s_cc[j].mask) ? static_cast<unsigned long long>(s_cc[j].n) : 0ull;
       sectors += cols * static_cast<unsigned long long>(rc.n);
     }
 #pragma unroll
