@@ -1568,3 +1568,52 @@ def test_pipeline_pdl_matches_plain(abi, ref):
     assert (b["offs"] == co["frame_offsets"]).all()
     tot = int(co["frame_offsets"][-1])
     assert (b["packed"] == co["packed"][:tot]).all() and (b["pos"] == co["pos_ids"][:tot]).all()
+
+
+@pytest.mark.parametrize("seed", list(range(24)))
+def test_compact_nv12_random_geometries(abi, ref, seed):
+    """The staged NV12 kernel over random geometries: source sizes from upscaling to ~8x downscaling (staged row
+    pitch 144 or 256 B, spans that end at the plane's right edge), random grids of 2x2 groups of 14-px patches,
+    pitches with and without 16-B multiples (staged vs direct path), random keep masks and capacities."""
+    rng = np.random.default_rng(1000 + seed)
+    gw, gh = int(rng.integers(2, 17)) * 2, int(rng.integers(2, 17)) * 2
+    sw = int(rng.integers(16, 1921)) * 2
+    sh = int(rng.integers(16, 1081)) * 2
+    if sw > 8.4 * gw * 14:          # keep within the staged path's widest span (or it takes the direct path)
+        sw = int(8.4 * gw * 14) // 2 * 2
+    pitch = sw + int(rng.choice([0, 16, 48, 8, 2]))
+    pitch += pitch % 2
+    g = make_grid(sw, sh, patch=14, group=2, grid_w=gw, grid_h=gh)
+    S, n = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+    nw = abi.grid_words(g)
+    km = rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
+    km &= rng.integers(0, 2**32, size=(S, n, nw), dtype=np.uint64).astype(np.uint32)
+    ys = [rng.integers(0, 256, size=(sh, pitch), dtype=np.uint8) for _ in range(S * n)]
+    uvs = [rng.integers(0, 256, size=(sh // 2, pitch), dtype=np.uint8) for _ in range(S * n)]
+    pre_h = ref.make_pre(sw, sh, pitch, pitch)
+    pre = dict(src_w=sw, src_h=sh, y_pitch=pitch, uv_pitch=pitch)
+    fidx = np.arange(S * n, dtype=np.int32)
+    total = S * n * gw * gh
+    cap = int(rng.choice([total, max(1, total // 2 + 1), 3]))
+    y_d = [torch.from_numpy(a).to(DEV) for a in ys]
+    uv_d = [torch.from_numpy(a).to(DEV) for a in uvs]
+    km_d = torch.from_numpy(km.view(np.int32)).to(DEV)
+    packed = torch.full((cap, 3 * 14 * 14), -1, dtype=torch.int16, device=DEV)
+    pos = torch.zeros(cap, 3, dtype=torch.int32, device=DEV)
+    src = torch.zeros(cap, dtype=torch.int32, device=DEV)
+    offs = torch.zeros(S * n + 1, dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(16, dtype=torch.int64, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    abi.codecsight_compact_nv12(g, pre, S, n, km_d, n, torch.from_numpy(fidx).to(DEV), abi.ptr_array(y_d, DEV),
+                                abi.ptr_array(uv_d, DEV), cap, packed, pos, src, offs, cnt, st)
+    o = ref.compact_nv12(g, pre_h, km, fidx, ys, uvs, cap, S, n)
+    torch.cuda.synchronize()
+    rows = min(int(o["frame_offsets"][-1]), cap)
+    assert int(st.item()) == o["status"]
+    assert (offs.cpu().numpy() == o["frame_offsets"]).all()
+    assert (pos.cpu().numpy()[:rows] == o["pos_ids"][:rows]).all()
+    assert (src.cpu().numpy()[:rows] == o["src_index"][:rows]).all()
+    got = packed.cpu().numpy().view(np.uint16)
+    assert (got[:rows] == o["packed"][:rows]).all(), (sw, sh, gw, gh, pitch, int((got[:rows] != o["packed"][:rows]).sum()))
+    assert (got[rows:] == 0xFFFF).all()
+    assert (cnt.cpu().numpy().view(np.uint64) == o["counters"]).all()
