@@ -862,6 +862,21 @@ def run_ours(args, cfg, rank, world, local_rank):
                           "ours_ms_per_stream_step": ms_max / K / S},
         "clocks": clk,
     }
+    if args.frames == "nv12":
+        # the fused NV12 preprocessing is bound by its exact fp32 arithmetic, not by bytes: its FP32-pipe
+        # roofline from the guide's unit counts -- 148 SMs x 128 FP32 lanes x the max SM clock -- and the kernel's
+        # static count of 91 packed FP32 instructions (FMUL2 / FFMA2 / FADD2, 2 lane-ops each) per item (a pair of
+        # output rows of a kept group: 14 per group) over the warp's 32 lanes
+        groups = float(dcnt[abi.CNT_PACKED_ROWS].item()) / K / 4.0
+        lane_ops = groups * 14 * 32 * 91 * 2
+        sm_mhz = (json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0)
+                  if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0)
+        fp32_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * sm_mhz * 1e6
+        nv_ms = cmp_ms  # the codecsight_compact_nv12 call in the step (count + scan included), as the secondary roofline
+        out["compute_roofline"] = {"bound": "fp32_pipe", "kernel": "codecsight_compact_nv12 (compact_nv12_staged)",
+                                   "achieved": lane_ops / (nv_ms / 1e3) / 1e12, "peak": fp32_peak / 1e12,
+                                   "unit": "T fp32 lane-ops/s", "frac": lane_ops / (nv_ms / 1e3) / fp32_peak,
+                                   "lane_ops_per_launch": lane_ops, "peak_kind": "guide unit counts x sm_max_mhz"}
     if e2e:
         out["e2e"] = {"value": frames_total / (e2e_ms_max / 1e3), "unit": "frames/s",
                       "h2d_bytes_per_step": e2e["h2d"] * S_total // S, "d2h_bytes_per_step": e2e["d2h"] * S_total // S,
