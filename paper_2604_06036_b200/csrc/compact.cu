@@ -1026,7 +1026,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) compact_gather_tma(const __
 // the direct-load path), every tap one shared-memory load at a per-lane constant offset, no 64-bit index arithmetic;
 // one midpoint-guard branch per pair; predicated 2-B stores straight to the packed rows (a pair covers 56 contiguous
 // bytes per channel and patch row, so sectors fill in L2).  Row taps / weights come from per-CTA tables (one
-// nv12_axis per model row per launch).  16 warps x 96 registers, one CTA per SM (measured against 8-24 warps and a
+// nv12_axis per model row per launch).  16 warps x ~107 registers, one CTA per SM (measured against 8-24 warps and a
 // 64-register budget, which rematerialised the lane constants every pair).  Requires pitches that are
 // multiples of 16; a slot whose planes are not 16-B aligned is staged with byte copies.
 constexpr int kNvsWarps = 16;
