@@ -8,9 +8,11 @@
 //              writes the index outputs (disposition, p_old by p_new, n_tokens), clamps the data moves to the
 //              capacities (status bits), and leaves in the workspace: a header, the segment list and the fp32
 //              (cos, sin) table of R(dp) computed once per stream-step from fp64 angles (reading Q20).
-//   kv_gather  persistent grid (SM-count multiple).  The work items are (stream, 64-row block, layer, K|V);
-//              every CTA derives the same item prefix from the per-stream row counts and takes one contiguous,
-//              equal-sized range of items.  Each item walks the segments that overlap its row block: REUSE K runs
+//   kv_prefix  one CTA: the item prefix over the streams (items per stream from the plans' row counts) and the
+//              gather's work counter zeroed.
+//   kv_gather  persistent grid (one CTA per SM; production path kv_gather_tma: a TMA bulk ring per warp).  The
+//              work items are (stream, 64-row block, layer, K|V), claimed dynamically by the warps from the work
+//              counter (guided claim sizes, see kClaimMax).  Each item walks the segments that overlap its row block: REUSE K runs
 //              are rotated (rotate_half pairs (i, i + D/2) loaded as two 16-B vectors, fp32 fma, RNE store),
 //              REUSE V runs and refreshed rows are contiguous 16-B vector copies.  No tensor cores: nothing here
 //              is a contraction; the kernel is HBM-bound.
