@@ -2,7 +2,8 @@
 vectors, so that FFmpeg's real H.264 decoder can export them (the image has no H.264 encoder).
 
 Stream: SPS + PPS; frame 0 an IDR picture of I_PCM macroblocks (raw samples); frames 1.. P pictures in which every
-macroblock is P_L0_16x16, P_L0_L0_16x8 or P_L0_L0_8x16 with the requested quarter-pel motion vectors,
+macroblock is P_L0_16x16, P_L0_L0_16x8, P_L0_L0_8x16 or P_8x8 (sub-partitions 8x8 / 8x4 / 4x8 / 4x4) with the
+requested quarter-pel motion vectors,
 coded_block_pattern 0 (no residual), one reference frame, deblocking off.  Each motion vector difference is coded
 against the standard's prediction (ITU-T H.264 §8.4.1.3: neighbours A = left, B = above, C = above-right or D =
 above-left of the partition; the directional rules of 16x8 / 8x16 partitions; else the median)."""
@@ -173,6 +174,17 @@ def predict_partition(f, x, y, pw, ph, part_idx):
 
 
 PARTS = {0: [(0, 0, 16, 16)], 1: [(0, 0, 16, 8), (0, 8, 16, 8)], 2: [(0, 0, 8, 16), (8, 0, 8, 16)]}
+# P_8x8 (mb_type 3): the four 8x8 blocks in order, each split by its sub_mb_type into these sub-partitions
+SUB_PARTS = {0: [(0, 0, 8, 8)], 1: [(0, 0, 8, 4), (0, 4, 8, 4)], 2: [(0, 0, 4, 8), (4, 0, 4, 8)],
+             3: [(0, 0, 4, 4), (4, 0, 4, 4), (0, 4, 4, 4), (4, 4, 4, 4)]}
+B8 = [(0, 0), (8, 0), (0, 8), (8, 8)]
+
+
+def partitions(mb_type, sub_types=None):
+    """Luma rectangles (x, y, w, h) inside the MB, in decoding (and export) order."""
+    if mb_type != 3:
+        return PARTS[mb_type]
+    return [(bx + x, by + y, w, h) for (bx, by), st in zip(B8, sub_types) for (x, y, w, h) in SUB_PARTS[st]]
 
 
 def _p_slice(frame_num, mbw, mbh, mbs):
@@ -190,12 +202,16 @@ def _p_slice(frame_num, mbw, mbh, mbs):
     f = MvField(mbw, mbh)
     for my in range(mbh):
         for mx in range(mbw):
-            mb_type, mvs = mbs[my][mx]
+            mb_type, mvs = mbs[my][mx][:2]
+            sub = mbs[my][mx][2] if mb_type == 3 else None
             w.ue(0)         # mb_skip_run
-            w.ue(mb_type)   # P_L0_16x16 / P_L0_L0_16x8 / P_L0_L0_8x16 (one reference: no ref_idx)
-            for pi, (px, py, pw, ph) in enumerate(PARTS[mb_type]):
+            w.ue(mb_type)   # P_L0_16x16 / P_L0_L0_16x8 / P_L0_L0_8x16 / P_8x8 (one reference: no ref_idx)
+            if mb_type == 3:
+                for st in sub:
+                    w.ue(st)  # sub_mb_type: 8x8 / 8x4 / 4x8 / 4x4
+            for pi, (px, py, pw, ph) in enumerate(partitions(mb_type, sub)):
                 x, y = 16 * mx + px, 16 * my + py
-                pred = predict_partition(f, x, y, pw, ph, pi)
+                pred = predict_partition(f, x, y, pw, ph, pi if mb_type in (1, 2) else 0)
                 w.se(mvs[pi][0] - pred[0])   # mvd_l0 x (quarter pel)
                 w.se(mvs[pi][1] - pred[1])   # mvd_l0 y
                 f.put(x, y, pw, ph, mvs[pi])
@@ -205,9 +221,9 @@ def _p_slice(frame_num, mbw, mbh, mbs):
 
 
 def write_stream(path, mbw, mbh, mv_frames, seed=0):
-    """mv_frames: list over P-frames of [mbh][mbw] entries, each (mvx, mvy) (a 16x16 partition) or
-    (mb_type, [mv, mv]) (1: two 16x8, 2: two 8x16 partitions), quarter pel; writes SPS, PPS, an I_PCM IDR picture
-    and one P picture per entry."""
+    """mv_frames: list over P-frames of [mbh][mbw] entries, each (mvx, mvy) (a 16x16 partition),
+    (mb_type, [mv, mv]) (1: two 16x8, 2: two 8x16 partitions) or (3, [mv per sub-partition], [4 sub_mb_types])
+    (P_8x8), quarter pel; writes SPS, PPS, an I_PCM IDR picture and one P picture per entry."""
     rng = np.random.default_rng(seed)
     luma = rng.integers(16, 236, size=(16 * mbh, 16 * mbw), dtype=np.uint8)
     cb = rng.integers(16, 240, size=(8 * mbh, 8 * mbw), dtype=np.uint8)
