@@ -4,7 +4,8 @@ The paper's motivation analysis (fig:mv_residual_analysis_cdf, P:185-194, P:210-
 that are 77%~94% similar when evaluated under motion and residual thresholds") as a GPU pipeline over decoder
 exports.  A step = one GOP (16 frames: an I-frame and 15 P-frames) of every stream of the rank:
 
-  codecsight_mv_rasterize   H.264-shaped AVMotionVector records (synth.avmv_records: 16x16 ... 4x4 partitions,
+  codecsight_mv_rasterize   H.264-shaped AVMotionVector records (synth.avmv_records: 16x16 ... 8x8 partitions, as
+                            libavcodec exports them (sub-8x8 at 8x8 granularity, tests/test_real_h264.py),
                             skip MBs with their vector, intra MBs without a record) -> the MB grid
   codecsight_score_patches  the grid -> per-patch scores M(i) (Eq. 1-3) + keep masks (GOP state carried)
   codecsight_similar_hist   per P-frame similar-patch counts #{M(i) < tau} for tau in {0.25, 0.5, 1, 2, 5} px,

@@ -256,7 +256,9 @@ AV_MV_DTYPE = np.dtype([("source", "<i4"), ("w", "u1"), ("h", "u1"), ("src_x", "
 assert AV_MV_DTYPE.itemsize == 40
 
 # H.264 inter partition modes of a 16x16 MB (partition w, h) and their frequencies in the generated streams:
-# 16x16 (skip and most inter MBs), 16x8, 8x16, 8x8 -- an 8x8 further split into 4x4 sub-partitions with p = 0.25
+# 16x16 (skip and most inter MBs), 16x8, 8x16, 8x8 (P_8x8: libavcodec exports each 8x8 block as one 8x8 record with
+# its first sub-partition's vector whatever its sub-partitioning -- checked against the real decoder,
+# tests/test_real_h264.py -- so no sub-8x8 records are generated)
 _PART_MODES = ((16, 16), (16, 8), (8, 16), (8, 8))
 _PART_P = (0.55, 0.15, 0.15, 0.15)
 
@@ -264,8 +266,8 @@ _PART_P = (0.55, 0.15, 0.15, 0.15)
 def avmv_records(mb: np.ndarray, rng: np.random.Generator, mb_size: int = 16) -> np.ndarray:
     """AVMotionVector records of one P-frame, shaped like libavcodec's H.264 export, drawn from the frame's MB
     records `mb` [rows][cols] (the scene truth): an INTRA MB exports nothing; a SKIP MB one 16x16 record with its
-    (predicted) vector; an INTER MB 1, 2, 4 or up to 16 partitions (16x16 / 16x8 / 8x16 / 8x8, 8x8 -> 4x4) whose
-    vectors are the MB's vector with +-1 qpel jitter on some partitions (p = 0.3).  motion_scale 4 (quarter pel),
+    (predicted) vector; an INTER MB 1, 2 or 4 partitions (16x16 / 16x8 / 8x16 / 8x8) whose vectors are the MB's
+    vector with +-1 qpel jitter on some partitions (p = 0.3).  motion_scale 4 (quarter pel),
     source -1 (past reference), dst = the partition centre in px.  Records are in raster order of MBs."""
     rows, cols = mb.shape
     jj, ii = np.nonzero(mb["type"] != MB_INTRA)
@@ -279,12 +281,7 @@ def avmv_records(mb: np.ndarray, rng: np.random.Generator, mb_size: int = 16) ->
         j, i = jj[sel], ii[sel]
         for oy in range(0, mb_size, ph):
             for ox in range(0, mb_size, pw):
-                if (pw, ph) == (8, 8):   # 8x8: split into four 4x4 sub-partitions with p = 0.25
-                    split = rng.random(j.size) < 0.25
-                    parts = [(~split, ox, oy, 8, 8)] + [(split, ox + sx, oy + sy, 4, 4) for sy in (0, 4)
-                                                         for sx in (0, 4)]
-                else:
-                    parts = [(np.ones(j.size, bool), ox, oy, pw, ph)]
+                parts = [(np.ones(j.size, bool), ox, oy, pw, ph)]
                 for msk, px, py, w, h in parts:
                     if not msk.any():
                         continue
