@@ -82,11 +82,17 @@ struct ScoreParams {
 // (two slots, alternating per launch, so that back-to-back launches -- PDL overlap -- can be compared)
 __device__ unsigned long long g_cs_phase[2][16384][12];
 static int g_cs_phase_launch = 0;
+__device__ unsigned g_cs_smid[16384];
 __device__ __forceinline__ void cs_phase(int slot, int k) {
   if (threadIdx.x == 0 && blockIdx.x < 16384) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_cs_phase[slot][blockIdx.x][k] = t;
+    if (k == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_cs_smid[blockIdx.x] = sm;
+    }
   }
 }
 #define CS_PHASE(k) cs_phase(P.phase_slot, k)
@@ -1036,6 +1042,10 @@ extern "C" int codecsight_debug_phase(unsigned long long* host, int n_ctas) {  /
   if (n_ctas > 16384) n_ctas = 16384;
   const size_t off = sizeof(unsigned long long) * 12 * 16384 * ((g_cs_phase_launch + 1) & 1);
   return cudaMemcpyFromSymbol(host, g_cs_phase, sizeof(unsigned long long) * 12 * n_ctas, off) == cudaSuccess ? 0 : -1;
+}
+extern "C" int codecsight_debug_smid(unsigned* host, int n_ctas) {  // SM of each CTA of the last launch
+  if (n_ctas > 16384) n_ctas = 16384;
+  return cudaMemcpyFromSymbol(host, g_cs_smid, sizeof(unsigned) * n_ctas) == cudaSuccess ? 0 : -1;
 }
 extern "C" int codecsight_debug_phase_slot(unsigned long long* host, int n_ctas, int slot) {
   if (n_ctas > 16384) n_ctas = 16384;

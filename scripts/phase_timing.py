@@ -35,6 +35,8 @@ def run():
     L = abi.lib()
     L.codecsight_debug_phase.restype = C.c_int
     L.codecsight_debug_phase.argtypes = [C.c_void_p, C.c_int]
+    L.codecsight_debug_smid.restype = C.c_int
+    L.codecsight_debug_smid.argtypes = [C.c_void_p, C.c_int]
     dev = torch.device("cuda:0")
     for name, S in (("C2", 32), ("C3", 64), ("C4", 256)):
         cfg = synth.CONFIGS[name]
@@ -78,6 +80,8 @@ def run():
             ev_ms = e0.elapsed_time(e1)
             h = np.zeros((nct, 12), np.uint64)
             assert L.codecsight_debug_phase(h.ctypes.data, nct) == 0
+            smid = np.zeros(nct, np.uint32)
+            assert L.codecsight_debug_smid(smid.ctypes.data, nct) == 0
             if rep >= 2:
                 res.append(h.astype(np.int64) - int(h[:, 0].min()))
         gs = torch.zeros(S, nw + 1, dtype=torch.int32, device=dev)
@@ -95,6 +99,14 @@ def run():
         print(f"== {name}: {S} streams x {n} frames, {nct} CTAs, kept {kept:.2f}")
         labels = ["start", "ticket", "prologue", "1st chunk", "scored", "masks", "offset", "compacted", "end"]
         print(f"   CUDA-event time of the call: {ev_ms * 1e3:.1f} us (launch + CTA span + drain)")
+        # compaction end by the number of this grid's CTAs sharing the CTA's SM (balanced shares are equal per warp)
+        r = res[-1]
+        per_sm = np.bincount(smid, minlength=int(smid.max()) + 1)
+        share = per_sm[smid]
+        for c in sorted(set(share.tolist())):
+            v = r[share == c, 7] / 1e3
+            print(f"   CTAs on SMs holding {c} of the grid's CTAs: {v.size:4d}, compacted med {np.median(v):7.1f} us"
+                  f"  max {v.max():7.1f}")
         for r in res[-1:]:
             for k, lab in enumerate(labels):
                 v = r[:, k] / 1e3
