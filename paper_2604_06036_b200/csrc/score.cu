@@ -198,9 +198,12 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   int sidx_ = blockIdx.x / P.cluster;
-  if (FUSED) {
+  if (FUSED && !(P.global_compact && !P.pdl)) {
     // streams are taken in ticket order (cluster start order), so every stream a look-back waits for belongs to a
-    // cluster that is already running: the decoupled look-back below cannot deadlock
+    // cluster that is already running: the decoupled look-back below cannot deadlock.  (A grid-balanced call has
+    // every cluster resident -- its grid barrier relies on that already -- so it takes its stream from blockIdx and
+    // starts its MB loads one atomic round trip earlier; chained calls keep the ticket, their predecessor's CTAs
+    // may still hold SMs.)
     if (rank == 0 && threadIdx.x == 0) s_sidx = static_cast<int>(atomicAdd(&P.ws_ctr[0], 1u));
     cluster.sync();
     sidx_ = *cluster.map_shared_rank(&s_sidx, 0);
