@@ -744,7 +744,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         e2e_ms = e_a.elapsed_time(e_b)
         h2d = in_mb[0].numel() + in_ty[0].numel() + in_fi[0].numel() * 4
         d2h = (S * 4 + S * s + 1) * 4
-        e2e = dict(ms=e2e_ms, wall_ms=wall_ms, steps=nsteps, h2d=h2d, d2h=d2h, checksum=checksum)
+        # the link's own rate for this upload: back-to-back pinned copies of one step's metadata buffer, nothing else
+        # on the GPU (the e2e rate above is bounded by it whenever a step's upload outlasts its kernels)
+        with torch.cuda.stream(copy_stream):
+            st_mb[0].copy_(in_mb[0], non_blocking=True)
+            c_a, c_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c_a.record(copy_stream)
+            for i in range(8):
+                st_mb[i & 1].copy_(in_mb[i % len(in_mb)], non_blocking=True)
+            c_b.record(copy_stream)
+        torch.cuda.synchronize()
+        link_gbs = 8 * in_mb[0].numel() / (c_a.elapsed_time(c_b) / 1e3) / 1e9
+        e2e = dict(ms=e2e_ms, wall_ms=wall_ms, steps=nsteps, h2d=h2d, d2h=d2h, checksum=checksum, link_gbs=link_gbs)
         # per scene kind: kept patches / patches over the e2e steps (calibration check against P:563)
         for i, gid in enumerate(global_ids):
             j = SCENE_KINDS.index(synth.scene_of(cfg, gid))
@@ -881,7 +892,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         out["e2e"] = {"value": frames_total / (e2e_ms_max / 1e3), "unit": "frames/s",
                       "h2d_bytes_per_step": e2e["h2d"] * S_total // S, "d2h_bytes_per_step": e2e["d2h"] * S_total // S,
                       "wall_clock_value": frames_total / (e2e["wall_ms"] / 1e3),
-                      "pipelining": "H2D of step k+1 on a copy stream overlaps step k; host reads step k-1's result"}
+                      "pipelining": "H2D of step k+1 on a copy stream overlaps step k; host reads step k-1's result",
+                      # upload rate the e2e steps achieved vs the pinned H2D rate of the same buffer measured alone
+                      "h2d_gbs": e2e["h2d"] * e2e["steps"] / (e2e["ms"] / 1e3) / 1e9,
+                      "h2d_link_gbs": e2e["link_gbs"]}
     if not args.no_cpu_baseline and world == 1:  # the oracle baseline is timed at N = 1 only
         log("[rank 0] timing the CPU oracle on a bounded sample ...")
         r = oracle_sample(cfg, args.cpu_seconds, kv_mode=args.kv_mode, tp=tp)

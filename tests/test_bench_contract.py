@@ -27,7 +27,10 @@ def test_reference_arm_json_line():
 
 
 BENCH_LINES = ["r01_final_bench.json", "r01_bench_c4.json", "r01_bench_c5.json", "r01_bench_c3.json",
-               "r01_bench_c2.json"]
+               "r01_bench_c2.json", "r02_final_bench.json", "r02_bench_c4.json", "r02_bench_c5.json", "r02_bench_c3.json",
+               "r02_bench_c2.json", "r02_bench_c4_nv12.json"]
+WITH_CPU_LEG = ("r01_final_bench.json", "r01_bench_c4.json", "r01_bench_c5.json", "r02_final_bench.json",
+                "r02_bench_c4.json", "r02_bench_c5.json")
 
 
 def _last_json(path):
@@ -43,7 +46,7 @@ def test_committed_gpu_bench_lines_carry_the_contract():
         for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                   "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
             assert k in d, (name, k)
-        if name in ("r01_final_bench.json", "r01_bench_c4.json", "r01_bench_c5.json"):   # runs with the CPU leg
+        if name in WITH_CPU_LEG:   # runs with the CPU leg
             cb = d["cpu_baseline"]
             assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"], name
         assert d["n_gpus"] == 1 and d["warmup"] >= 3 and d["value"] > 0 and d["gpu_launches"] > 0, name
@@ -54,6 +57,8 @@ def test_committed_gpu_bench_lines_carry_the_contract():
         assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9, name
         e = d["e2e"]
         assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0, name
+        if "h2d_link_gbs" in e:   # the upload rate e2e achieved cannot beat the link measured alone (10 % noise)
+            assert 0 < e["h2d_gbs"] <= 1.1 * e["h2d_link_gbs"], name
         assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}, name
         # frames/s = frames per step / step time: the whole-job value follows from ms_per_step
         assert d["value"] * d["ms_per_step"] / 1e3 > 0
