@@ -493,10 +493,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         frames = [torch.randn(3, H, W, generator=gen, device=dev).to(torch.bfloat16) for _ in range(S * s)]
         ptr_w = abi.ptr_array([frames[i % len(frames)] for i in range(S * w)], dev)
         ptr_s = abi.ptr_array(frames, dev)
-    # eager sequential steps after the timed loop whose per-kernel events give the per-call times and rooflines: with
-    # --graphs (no events inside graphs) and in overlap mode (a side-stream call's events also cover the time it
-    # waits for SMs held by the other stream's kernel)
-    calib = 2 * period if args.graphs else (min(max(args.steps, 4), 10) if args.overlap else 0)
+    # eager sequential steps after the timed loop whose per-kernel events give the per-call times and rooflines (the
+    # timed steps record no events: an event between two calls costs a few us of a small step; inside graphs there
+    # are none; in overlap mode a side-stream call's events would also cover the time it waits for SMs held by the
+    # other stream's kernel).  Chained (--pdl) calls overlap each other: their time is the timed region / K.
+    calib = 2 * period if args.graphs else (0 if args.pdl else min(max(args.steps, 4), 10))
     total_steps = warm + args.steps + calib
     types_dev, fidx_dev, types_host = [], [], []
     for k in range(total_steps + 1):
@@ -538,12 +539,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             st["fi"].copy_(fidx_dev[k], non_blocking=True)
             pipe.graph_step(k, st["mb"], ptrs, st["fi"], st["ty"])
             return
-        evs = pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k],
-                        timing=timed and not args.pdl and not args.overlap)
-        if timed and not args.pdl and not args.overlap:
-            for name in ("score", "compact", "kv"):
-                if name in evs:
-                    ev[name].append(evs[name])
+        pipe.step(k, md_for(k), ptrs, fidx_dev[k], types_dev[k])
 
     for k in range(warm):
         run_step(k, False)
